@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark of the multidimensional-SSA hot path on B200 (one JSON line on rank 0).
+
+One STEP = one pass of the whole hot path over one
+synthetic input: plan (embedding: shapes, 𝔎, weights), block-Lanczos rank-r
+decomposition driven by X·V / Xᵀ·U block products, and the grouped diagonal-
+averaging reconstruction.  Default workload: BASELINE.json configs[1] (c2, MSSA
+8 x 4096, L = 1024, r = 16, k = 32); --config c1..c5 selects another.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Metric: trajectory products/s = vector products (X·v or Xᵀ·u) completed per
+second of whole-step time, summed over ranks (weak scaling: every rank
+decomposes its own input, no data-path collective).  `e2e` is the same metric
+through the C ABI with host buffers (H2D of the input and D2H of the
+reconstructions inside the timed region).  `roofline` reports the dominant kernel
+(the direct trajectory product) against the FP32 FFMA peak.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FFMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 TF: 148 SM x 128 FP32 lanes x FMA x max clock
+FP64_PEAK_TFLOPS = FFMA_PEAK_TFLOPS / 2               # B200 non-tensor FP64 = 1/2 FP32 rate
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0, "fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.idx = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and "Active" in s[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "n_samples": len(self.samples)}
+
+
+def workload(name, seed_offset=0):
+    import synth
+    fn = synth.CONFIGS[name]
+    base = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}[name]
+    return fn(seed=base + 1000 * seed_offset)
+
+
+def groups_for(w):
+    gs = [g for g in w.groups if max(g) < w.r]
+    return gs if gs else [list(range(min(4, w.r)))]
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args, rank, world, dist):
+    import torch
+    from paper_1309_5050_b200 import Plan, launch_count
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    w = workload(args.config, seed_offset=rank)
+    groups = groups_for(w)
+    stream = torch.cuda.Stream(device=dev)
+    dt_torch = torch.float64 if w.dtype == "f64" else torch.float32
+    img_dev = torch.as_tensor(np.asarray(w.data), dtype=dt_torch, device=dev)
+    mask_np = None if w.mask is None else np.asarray(w.mask)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def step(host=False):
+        with torch.cuda.stream(stream):
+            src = np.asarray(w.data) if host else img_dev
+            p = Plan(src, w.window, mask=mask_np, wmask=w.wmask, dtype=w.dtype, block_k=w.block_k,
+                     path=args.path, stream=stream.cuda_stream)
+            info = p.decompose(w.r, allow_not_converged=True)
+            recs = p.reconstruct(groups, add_rest=False, device=not host)
+            p.close()
+        return info, recs, p
+
+    # warm-up (also compiles nothing: the library is AOT-built)
+    for _ in range(args.warmup):
+        info, recs, p = step()
+    torch.cuda.synchronize()
+    L, K, k = p.L, p.K, info["block_k"]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times, infos = [], []
+    launches0 = launch_count(reset=True)
+    with ClockSampler(dev.index) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)                         # flush L2 between timed iterations
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            info, recs, _ = step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            infos.append(info)
+    launches = launch_count(reset=True)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms_local = float(np.sum(times))
+    nvec_local = float(np.sum([i["n_vector_products"] for i in infos]))
+    ms_prod = float(np.sum([i["ms_products"] for i in infos]))
+    nblk = float(np.sum([i["n_block_products"] for i in infos]))
+    if dist:
+        t = torch.tensor([ms_local, nvec_local, launches], dtype=torch.float64, device=dev)
+        tmax = t.clone(); dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone(); dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms_all, nvec_all = float(tmax[0]), float(tsum[1])
+    else:
+        ms_all, nvec_all = ms_local, nvec_local
+
+    # ---- end-to-end through the C ABI with host buffers (H2D input, D2H reconstructions)
+    e2e_times = []
+    for _ in range(max(1, min(args.steps, 5))):
+        flush.fill_(1); torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        info_h, recs_h, _ = step(host=True)
+        torch.cuda.synchronize()
+        e2e_times.append((time.perf_counter() - t0) * 1e3)
+    esz = 8 if w.dtype == "f64" else 4
+    h2d = int(np.asarray(w.data).size * esz + (0 if mask_np is None else mask_np.size))
+    d2h = int(len(groups) * np.asarray(w.data).size * esz + 8 * w.r)
+    e2e_value = info_h["n_vector_products"] / (np.mean(e2e_times) / 1e3) * world
+
+    # ---- roofline of the dominant kernel (the trajectory block product), timed live:
+    # the library brackets every block product with CUDA events on the plan's stream
+    flops_per_block = 2.0 * L * K * k
+    avg_block_ms = ms_prod / max(nblk, 1)
+    achieved = flops_per_block / (avg_block_ms / 1e3) / 1e12
+    peak = FP64_PEAK_TFLOPS if w.dtype == "f64" else FFMA_PEAK_TFLOPS
+    res = {
+        "metric": "trajectory products/s",
+        "value": nvec_all / (ms_all / 1e3),
+        "unit": "vector products/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_all / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": w.dtype,
+        "data": "synthetic (seeded BASELINE.json generator, rank-offset seeds)",
+        "config": {"workload": w.name, "nx": int(np.asarray(w.data).shape[0]), "ny": int(np.asarray(w.data).shape[1]),
+                   "window": list(w.window), "L": int(L), "K": int(K), "r": int(w.r), "block_k": int(k),
+                   "groups": len(groups), "path": p.path, "l2": "flushed (256 MB write) between timed steps",
+                   "parallelism": f"replicas x{world} (independent inputs per rank)"},
+        "rank_r_time_ms": ms_all / args.steps,
+        "decomposition": {"n_block_products": infos[-1]["n_block_products"],
+                          "n_vector_products": infos[-1]["n_vector_products"],
+                          "n_restarts": infos[-1]["n_restarts"], "n_converged": infos[-1]["n_converged"],
+                          "max_rel_residual": infos[-1]["max_rel_residual"],
+                          "ms_products_per_step": ms_prod / args.steps},
+        "e2e": {"value": e2e_value, "unit": "vector products/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": float(np.mean(e2e_times))},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "alu", "kernel": "corr_direct (X·V / Xᵀ·U block product)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": None,
+                     "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md SM count,"
+                                    " MEASURED_PEAKS sm_max_mhz); fp64 = 1/2",
+                     "algorithmic_flops_per_launch": flops_per_block, "avg_launch_ms": avg_block_ms,
+                     "share_of_step": ms_prod / max(ms_local, 1e-9)},
+        "clocks": clk.summary(),
+    }
+    return res, w
+
+
+# ----------------------------------------------------------------------------- oracle (CPU)
+def oracle_products_per_s(w, budget_s=15.0):
+    """The oracle's naive X·V / Xᵀ·U (oracle/oracle_core.c) on a bounded sample of
+    the same workload: whole block products if they fit the budget, else sampled
+    output rows (scaled to products/s)."""
+    import oracle
+    x = np.array(w.data, dtype=np.float64)
+    if w.dtype == "f32":
+        x = x.astype(np.float32).astype(np.float64)
+    sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
+    rng = np.random.default_rng(0)
+    k = w.block_k
+    V = rng.normal(size=(sh.K, k)); U = rng.normal(size=(sh.L, k))
+    # time one output row of X·V to size the sample
+    t0 = time.perf_counter(); oracle.xv_rows(x, sh, V, [0]); t_row = time.perf_counter() - t0
+    rows = int(max(1, min(sh.L, budget_s / 2 / max(t_row, 1e-6))))
+    t0 = time.perf_counter(); oracle.xv_rows(x, sh, V, np.arange(rows)); t_xv = time.perf_counter() - t0
+    kc = int(max(1, min(sh.K, rows * sh.K // sh.L)))
+    t0 = time.perf_counter(); oracle.xtu(x, sh, U, kstart=0, kcount=kc); t_xtu = time.perf_counter() - t0
+    frac_xv, frac_xtu = rows / sh.L, kc / sh.K
+    t_block = t_xv / frac_xv + t_xtu / frac_xtu          # extrapolated time of one X·V + one Xᵀ·U block
+    value = 2 * k / t_block
+    cores = len(os.sched_getaffinity(0))
+    sample = (f"{w.name}: X·V on {rows}/{sh.L} rows and Xᵀ·U on {kc}/{sh.K} rows of a k={k} block "
+              f"({t_xv + t_xtu:.1f} s of CPU), scaled to whole blocks")
+    return value, cores, sample
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--path", default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+
+    if args.impl == "reference":
+        # the oracle as it stands, on the host cores of rank 0 only
+        if rank != 0:
+            return
+        w = workload(args.config)
+        vals = []
+        for _ in range(args.warmup):
+            oracle_products_per_s(w, budget_s=min(args.cpu_budget, 5.0))
+        t0 = time.perf_counter()
+        cores, sample = 0, ""
+        for _ in range(args.steps):
+            v, cores, sample = oracle_products_per_s(w, budget_s=args.cpu_budget / max(args.steps, 1))
+            vals.append(v)
+        el = time.perf_counter() - t0
+        v = float(np.mean(vals))
+        print(json.dumps({"impl": "reference", "metric": "trajectory products/s", "value": v,
+                          "unit": "vector products/s", "n_gpus": args.gpus, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": {"workload": w.name, "window": list(w.window)},
+                          "cpu_baseline": {"value": v, "unit": "vector products/s", "cores": cores,
+                                           "kind": "oracle", "sample": sample, "cpu": cpu_model()},
+                          "e2e": {"value": v, "unit": "vector products/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return
+
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl")
+        dist = tdist
+    res, w = run_ours(args, rank, world, dist)
+    if rank == 0:
+        if not args.no_cpu_baseline and world == 1:
+            v, cores, sample = oracle_products_per_s(w, budget_s=args.cpu_budget)
+            res["cpu_baseline"] = {"value": v, "unit": "vector products/s", "cores": cores, "kind": "oracle",
+                                   "sample": sample, "cpu": cpu_model()}
+        res["paper_context"] = {"rssa_nutrlan_s": {"mars_25x25": 0.519, "mars_160x80_r50": 0.587},
+                                "hardware": "not stated in the paper (P:2518-2624)"}
+        print(json.dumps(res))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

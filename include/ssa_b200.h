@@ -1,0 +1,195 @@
+/*
+ * ssa_b200.h — C ABI of the B200-native hot path of multidimensional singular
+ * spectrum analysis (2D-SSA, MSSA, Shaped 2D-SSA) of arXiv 1309.5050
+ * (Golyandina, Korobeynikov, Shlemov, Usevich, "Multivariate and 2D extensions
+ * of singular spectrum analysis with the Rssa package").
+ *
+ * The four steps of the method (Fig. 1 / §2.1) map onto the calls:
+ *   1. Embedding        ssa_plan_create      (𝒯 of eq. P:3004-3028: shapes 𝔑, 𝔏, 𝔎)
+ *   2. SVD              ssa_decompose        (top-r eigentriples)
+ *   3. Grouping         ssa_reconstruct args (index sets I_g)
+ *   4. Reconstruction   ssa_reconstruct      (diagonal averaging, Alg. 4)
+ * plus the trajectory-operator products themselves (ssa_matmul: X·V and Xᵀ·U,
+ * Alg. 1/3 P:3643-3662) that drive step 2.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Arrays are column-major with x fastest: element (i, j) of an Nx x Ny array
+ *    is at i + ld*j.  This is the paper's vec(); x is the paper's
+ *    first (downward) axis, y the second.  Indices are 0-based.
+ *  - MSSA is the 2D packing of P:3340-3354: pass an N_max x s array
+ *    whose columns are the series (NaN-padded to equal length) and the window
+ *    (L, 1).  No separate entry point.
+ *  - Shapes: 𝔑 = {finite cells} ∩ mask; 𝔏 = wmask;
+ *    𝔎 = {κ : 𝔏 +‐ {κ} ⊆ 𝔑} (eq. P:3004-3005).  Window cells and origins are
+ *    ordered lexicographically (x fastest); L = |𝔏|, K = |𝔎|.
+ *  - L-side vectors (eigenvectors U, "eigenarrays" P:2443-2456) have L entries in
+ *    𝔏-lex order; K-side vectors (factor vectors V) have K entries in 𝔎-lex
+ *    order.  Blocks of k vectors are column-major with leading dimension L or K.
+ *  - Element type: the plan's dtype (SSA_F32 or SSA_F64) for every array
+ *    argument unless stated otherwise; singular values are always double.
+ *  - on_device: 1 = the pointer is CUDA device memory of the plan's device,
+ *    0 = host memory (copied through pageable/pinned staging inside the call).
+ *  - Every call is stream-ordered on opts.stream and returns after the stream
+ *    has completed the work (synchronous), except ssa_matmul with
+ *    on_device = 1, which only enqueues (the caller synchronises).
+ *  - Ownership: the plan deep-copies its inputs; the caller may free them after
+ *    ssa_plan_create.  The plan owns every device buffer it allocates.  Outputs
+ *    go to caller buffers.  A plan is not thread-safe; distinct plans are
+ *    independent.
+ *  - Errors: every entry point returns an ssa_status; ssa_last_error() gives a
+ *    thread-local message for the last failure.  No exception crosses the ABI.
+ *    SSA_ERR_CUDA and SSA_ERR_COMM are sticky: the plan must be destroyed.
+ *    There is NO CPU fallback: without a usable CUDA device every compute entry
+ *    point fails with SSA_ERR_CUDA.
+ */
+#ifndef SSA_B200_H
+#define SSA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SSA_OK = 0,
+    SSA_ERR_ARG = 1,            /* bad pointer / size / dtype / group index */
+    SSA_ERR_WINDOW = 2,         /* not 1<=Lx<=Nx, 1<=Ly<=Ny, 1<Lx*Ly<Nx*Ny */
+    SSA_ERR_EMPTY_KSHAPE = 3,   /* 𝔎 = ∅: no window position fits inside 𝔑 */
+    SSA_ERR_RANK = 4,           /* r < 1 or r > min(L, K), or a group index >= r */
+    SSA_ERR_NOT_CONVERGED = 5,  /* decomposition hit max_iter; info->n_converged says how many */
+    SSA_ERR_OOM = 6,            /* device allocation failed */
+    SSA_ERR_CUDA = 7,           /* CUDA runtime / launch error, or no device (sticky) */
+    SSA_ERR_COMM = 8,           /* collective callback failed (sticky) */
+    SSA_ERR_STATE = 9           /* call out of order (e.g. reconstruct before decompose) */
+} ssa_status;
+
+typedef enum { SSA_F32 = 0, SSA_F64 = 1 } ssa_dtype;
+
+/* Product path.  AUTO picks per shape. */
+typedef enum {
+    SSA_PATH_AUTO = 0,
+    SSA_PATH_DIRECT = 1,   /* smem-tiled implicit GEMM on CUDA cores (Hankel sliding window) */
+    SSA_PATH_FFT = 2       /* shared-memory radix FFT circular correlation (Alg. 1/3) */
+} ssa_path;
+
+typedef struct {
+    int64_t nx, ny;        /* array size Nx x Ny (Ny = number of series for MSSA) */
+    int64_t ld;            /* leading dimension >= nx; 0 means nx */
+    ssa_dtype dtype;       /* element type of data; also the plan's arithmetic type */
+    const void *data;      /* column-major; NaN = missing cell */
+    int on_device;
+} ssa_array;
+
+typedef struct {
+    int32_t lx, ly;        /* window bounding box */
+    const uint8_t *wmask;  /* host lx*ly column-major 0/1 mask of 𝔏; NULL = full rectangle */
+} ssa_window;
+
+/* Collective hook for the window-position (𝔎) band partition.
+ * allreduce_sum must sum `count` elements of type `dtype` in place across all
+ * ranks (device buffer, stream-ordered on `stream`) and return 0 on success. */
+typedef struct {
+    int rank, world;
+    void *user;
+    int (*allreduce_sum)(void *user, void *dev_buf, int64_t count, int dtype, void *stream);
+} ssa_comm;
+
+typedef struct {
+    void *stream;          /* cudaStream_t; NULL = the legacy default stream */
+    int path;              /* ssa_path (0 = auto) */
+    int block_k;           /* Lanczos block width (0 = auto: 16 for f64, 32 for f32) */
+    double tol;            /* residual tolerance ||Xᵀu - σv|| <= tol*σ_1 (0 = auto) */
+    int max_products;      /* cap on block products in ssa_decompose (0 = auto) */
+    uint64_t seed;         /* seed of the Lanczos start block (counter-based RNG) */
+    const ssa_comm *comm;  /* NULL = single GPU */
+    int64_t band_y0, band_y1; /* this rank's κy range [y0, y1) of 𝔎 when comm != NULL */
+} ssa_opts;
+
+typedef struct {
+    int64_t nx, ny, lx, ly, kx, ky;   /* array, window box, origin box (kx = nx-lx+1) */
+    int64_t L, K;                     /* |𝔏|, |𝔎| */
+    int64_t n_valid;                  /* |𝔑| */
+    int64_t n_excluded;               /* |𝔑 \ 𝔑′| (cells that enter no window) */
+    int path;                         /* path chosen for the products */
+    int dtype;
+    int full_window, full_kshape;     /* 1 if 𝔏 / 𝔎 are full rectangles (trivial-mask fast path) */
+} ssa_plan_info_t;
+
+typedef struct {
+    int32_t r_requested, n_converged;
+    int32_t block_k, n_restarts;
+    int64_t n_block_products;         /* Xᵀ·U plus X·V block calls */
+    int64_t n_vector_products;        /* vectors pushed through the operator */
+    double max_rel_residual;          /* max_i ||Xᵀu_i - σ_i v_i|| / σ_1 over i < r */
+    double ms_products, ms_total;     /* device time in products; wall time of the call */
+} ssa_decomp_info;
+
+typedef struct ssa_plan_s *ssa_plan;
+
+/* Step 1 (embedding, P:334-376 / eq. P:3004-3028).  Validates sizes
+ * (SSA_ERR_WINDOW), builds 𝔑 = finite ∩ mask (mask: host nx*ny 0/1 or NULL),
+ * 𝔏 = wmask, 𝔎 by Alg. 6, the hit-count weights 𝕎 =
+ * diagsums(1_𝔏, 1_𝔎) (Alg. 4 step 1) and the per-path operator data.
+ * Returns SSA_ERR_EMPTY_KSHAPE if 𝔎 = ∅. */
+ssa_status ssa_plan_create(const ssa_array *x, const ssa_window *w, const uint8_t *mask,
+                           const ssa_opts *opts, ssa_plan *out);
+void ssa_plan_destroy(ssa_plan p);
+ssa_status ssa_plan_info(ssa_plan p, ssa_plan_info_t *info);
+
+/* Plan-time shapes: weights w_n = |𝒜_n| (int32 nx*ny, column-major; Rssa
+ * "$weights"; 0 outside 𝔑′) and the 𝔎 indicator over the kx*ky origin box. */
+ssa_status ssa_get_weights(ssa_plan p, int32_t *w, int on_device);
+ssa_status ssa_get_kmask(ssa_plan p, uint8_t *kmask, int on_device);
+
+/* The trajectory-operator products on a block of k vectors (never forming X):
+ *   transpose = 0 :  out (L x k) = X · in (K x k)    u_ℓ = Σ_{κ∈𝔎} x[ℓ +‐ κ] v_κ
+ *   transpose = 1 :  out (K x k) = Xᵀ · in (L x k)   v_κ = Σ_{ℓ∈𝔏} x[ℓ +‐ κ] u_ℓ
+ * (rows/columns of eq. P:3020-3028; Alg. 1 P:3647-3658 and its transpose P:3659-3662;
+ * Alg. 3 P:3838-3847 under reading Q1).  ldin/ldout 0 = packed.  With on_device = 1
+ * the call only enqueues on opts.stream. */
+ssa_status ssa_matmul(ssa_plan p, int transpose, const void *in, int64_t ldin,
+                      void *out, int64_t ldout, int64_t k, int on_device);
+
+/* Step 2: top-r eigentriples (σ_i, U_i, V_i) of X by block Golub-Kahan-Lanczos
+ * bidiagonalisation with thick restarts, σ descending.
+ * Continues from the stored basis when called again with a larger r.
+ * info may be NULL. */
+ssa_status ssa_decompose(ssa_plan p, int32_t r, ssa_decomp_info *info);
+
+/* Getters (valid after ssa_decompose or ssa_set_triples).  sigma: r doubles.
+ * U: L x r.  V: K x r, V_i = Xᵀ U_i / σ_i recomputed on request (P:383,
+ * P:1720-1723).  Signs: the largest-|.| entry of each U_i is positive. */
+ssa_status ssa_get_rank(ssa_plan p, int32_t *r);
+ssa_status ssa_get_sigma(ssa_plan p, double *sigma);
+ssa_status ssa_get_u(ssa_plan p, void *U, int on_device);
+ssa_status ssa_get_v(ssa_plan p, void *V, int on_device);
+
+/* Install externally computed triples (e.g. to reconstruct from a stored
+ * decomposition).  U: L x r; V may be NULL (then V = XᵀU/σ). */
+ssa_status ssa_set_triples(ssa_plan p, int32_t r, const double *sigma, const void *U,
+                           const void *V, int on_device);
+
+/* Steps 3-4.  Groups in CSR form: group g = grp_idx[grp_off[g] .. grp_off[g+1]),
+ * 0-based eigentriple indices < r.  out: (n_groups + add_rest) arrays of nx*ny
+ * (column-major, ld = nx), each  X̃_g = diagsums(Σ_{i∈I_g} σ_i U_i V_iᵀ) / 𝕎  on 𝔑′
+ * and NaN elsewhere (Alg. 4; values exist only inside 𝔑′,
+ * P:3214-3217).  add_rest appends 𝕏 − Σ_g X̃_g on 𝔑′ (eq. P:440-443). */
+ssa_status ssa_reconstruct(ssa_plan p, const int32_t *grp_off, const int32_t *grp_idx,
+                           int32_t n_groups, int add_rest, void *out, int on_device);
+
+/* w-correlation matrix of the groups' reconstructions:
+ * rho (n_groups x n_groups, column-major double) = (X̃_a, X̃_b)_w / (‖X̃_a‖_w ‖X̃_b‖_w). */
+ssa_status ssa_wcor(ssa_plan p, const int32_t *grp_off, const int32_t *grp_idx,
+                    int32_t n_groups, double *rho);
+
+const char *ssa_last_error(void);
+const char *ssa_version(void);
+/* Number of kernels this library launched on the calling thread since the last
+ * reset (evidence counter for bench.py's gpu_launches). */
+int64_t ssa_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSA_B200_H */

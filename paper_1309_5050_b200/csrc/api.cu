@@ -1,0 +1,628 @@
+// C ABI of libssa_b200 (include/ssa_b200.h): plan creation (embedding, step 1),
+// product dispatch, decomposition (step 2), reconstruction (steps 3-4).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.h"
+#include "kernels.h"
+#include "plan.h"
+
+namespace ssa {
+
+static thread_local std::string g_err;
+static thread_local int64_t g_launches = 0;
+
+void count_launch(int n) { g_launches += n; }
+void after_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(SSA_ERR_CUDA, std::string("launch of ") + what + ": " + cudaGetErrorString(e));
+    ++g_launches;
+}
+
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+PlanImpl::~PlanImpl() {
+    if (fft) fft_destroy(fft);
+    fft = nullptr;
+}
+
+double *small_dev(PlanImpl &p, size_t n) {
+    p.dsmall.alloc(std::max<size_t>(n, 64 * 64) * sizeof(double), p.st);
+    return p.dsmall.as<double>();
+}
+
+template <typename T>
+__global__ void u8_to_T_kernel(const uint8_t *m, int64_t n, T *out) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        out[t] = m[t] ? T(1) : T(0);
+}
+
+__global__ void clear_band_kernel(uint8_t *km, int kx, int ky, int64_t y0, int64_t y1) {
+    const int64_t n = (int64_t)kx * ky;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / kx;
+        if (j < y0 || j >= y1) km[t] = 0;
+    }
+}
+
+template <typename T>
+__global__ void weighted_sqrt_kernel(T *a, const int32_t *w, int64_t n, int ng) {
+    const int64_t tot = n * ng;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = t % n;
+        const T v = a[t];
+        a[t] = (w[c] > 0 && isfinite((double)v)) ? v * (T)sqrt((double)w[c]) : T(0);
+    }
+}
+
+// ---------------------------------------------------------------- products
+template <typename T>
+static CorrParams<T> base_corr(PlanImpl &p) {
+    CorrParams<T> c{};
+    c.x = p.img.as<T>(); c.ldx = p.nx; c.nx = p.nx; c.ny = p.ny;
+    return c;
+}
+
+template <typename T>
+void op_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k) {
+    if (p.path == SSA_PATH_FFT && p.fft) { fft_xtu<T>(p, U, ldu, V, ldv, k); return; }
+    CorrParams<T> c = base_corr<T>(p);
+    c.ox = p.kx; c.oy = p.ky; c.dx = p.lx; c.dy = p.ly;
+    c.W = U; c.ldw = ldu; c.wmap = p.full_window ? nullptr : p.lmap.as<int>();
+    c.out = V; c.ldo = ldv; c.omap = p.full_k ? nullptr : p.kmap.as<int>();
+    c.k = k;
+    corr_direct<T>(c, p.ws_corr.as<T>(), p.ws_corr_bytes, p.st);
+}
+
+template <typename T>
+void op_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k) {
+    if (p.path == SSA_PATH_FFT && p.fft) {
+        fft_xv<T>(p, V, ldv, U, ldu, k);
+    } else {
+        CorrParams<T> c = base_corr<T>(p);
+        c.ox = p.lx; c.oy = p.ly; c.dx = p.kx; c.dy = p.ky;
+        c.W = V; c.ldw = ldv; c.wmap = p.full_k ? nullptr : p.kmap.as<int>();
+        c.out = U; c.ldo = ldu; c.omap = p.full_window ? nullptr : p.lmap.as<int>();
+        c.k = k;
+        corr_direct<T>(c, p.ws_corr.as<T>(), p.ws_corr_bytes, p.st);
+    }
+    // window-position band partition: sum the L x k partials
+    if (p.has_comm && p.comm.world > 1) {
+        if (ldu != p.L) throw Error(SSA_ERR_ARG, "multi-GPU X·V needs a packed output");
+        if (p.comm.allreduce_sum(p.comm.user, U, p.L * (int64_t)k, p.dt, p.st) != 0)
+            throw Error(SSA_ERR_COMM, "allreduce of X·V partials failed");
+    }
+}
+template void op_xtu<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int);
+template void op_xtu<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int);
+template void op_xv<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int);
+template void op_xv<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int);
+
+// ---------------------------------------------------------------- plan creation
+template <typename T>
+static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host) {
+    cudaStream_t st = p.st;
+    const int64_t nxy = (int64_t)p.nx * p.ny;
+    // a1: image and 𝔑
+    DevBuf stage, dmask;
+    const int64_t ld = x->ld > 0 ? x->ld : x->nx;
+    const T *src = nullptr;
+    if (x->on_device) {
+        if ((x->dtype == SSA_F64) == (sizeof(T) == 8)) {
+            src = static_cast<const T *>(x->data);
+        } else {
+            stage.alloc(sizeof(T) * ld * p.ny, st);
+            cast_copy<T>(x->data, x->dtype == SSA_F64, stage.as<T>(), ld * p.ny, st);
+            src = stage.as<T>();
+        }
+    } else {
+        const size_t esz = x->dtype == SSA_F64 ? 8 : 4;
+        DevBuf raw;
+        raw.alloc(esz * ld * p.ny, st);
+        SSA_CUDA(cudaMemcpyAsync(raw.p, x->data, esz * ld * p.ny, cudaMemcpyHostToDevice, st));
+        stage.alloc(sizeof(T) * ld * p.ny, st);
+        cast_copy<T>(raw.p, x->dtype == SSA_F64, stage.as<T>(), ld * p.ny, st);
+        SSA_CUDA(cudaStreamSynchronize(st));
+        src = stage.as<T>();
+    }
+    if (mask_host) {
+        dmask.alloc(nxy, st);
+        SSA_CUDA(cudaMemcpyAsync(dmask.p, mask_host, nxy, cudaMemcpyHostToDevice, st));
+    }
+    p.img.alloc(sizeof(T) * nxy, st);
+    p.nmask.alloc(nxy, st);
+    prep_image<T>(src, ld, p.nx, p.ny, mask_host ? dmask.as<uint8_t>() : nullptr, p.img.as<T>(),
+                  p.nmask.as<uint8_t>(), st);
+    std::vector<uint8_t> nm(nxy);
+    SSA_CUDA(cudaMemcpyAsync(nm.data(), p.nmask.p, nxy, cudaMemcpyDeviceToHost, st));
+    SSA_CUDA(cudaStreamSynchronize(st));
+    p.n_valid = 0;
+    for (int64_t t = 0; t < nxy; ++t) p.n_valid += nm[t];
+
+    // 𝔏 map
+    if (!p.full_window) {
+        p.lmap.alloc(sizeof(int32_t) * p.lx * p.ly, st);
+        SSA_CUDA(cudaMemcpyAsync(p.lmap.p, p.lmap_host.data(), sizeof(int32_t) * p.lx * p.ly,
+                                 cudaMemcpyHostToDevice, st));
+    }
+    // a2: 𝔎 by Alg. 6: v = 𝒯ᵀ(I^𝔑)·1_𝔏 ;  𝔎 = {v = |𝔏|}
+    const int64_t nk = (int64_t)p.kx * p.ky;
+    p.kmask.alloc(nk, st);
+    const bool trivial = (p.n_valid == nxy) && p.full_window && !p.has_comm;
+    if (trivial) {
+        SSA_CUDA(cudaMemsetAsync(p.kmask.p, 1, nk, st));
+        p.full_k = true;
+        p.K = nk;
+    } else {
+        DevBuf ind, ones, cnt, ws;
+        ind.alloc(sizeof(T) * nxy, st);
+        u8_to_T_kernel<T><<<(unsigned)std::min<int64_t>(cdiv(nxy, 256), 16 * num_sms()), 256, 0, st>>>(
+            p.nmask.as<uint8_t>(), nxy, ind.as<T>());
+        after_launch("u8_to_T");
+        std::vector<T> one(p.L, T(1));
+        ones.alloc(sizeof(T) * p.L, st);
+        SSA_CUDA(cudaMemcpyAsync(ones.p, one.data(), sizeof(T) * p.L, cudaMemcpyHostToDevice, st));
+        cnt.alloc(sizeof(T) * nk, st);
+        CorrParams<T> c{};
+        c.x = ind.as<T>(); c.ldx = p.nx; c.nx = p.nx; c.ny = p.ny;
+        c.ox = p.kx; c.oy = p.ky; c.dx = p.lx; c.dy = p.ly;
+        c.W = ones.as<T>(); c.ldw = p.L; c.wmap = p.full_window ? nullptr : p.lmap.as<int>();
+        c.out = cnt.as<T>(); c.ldo = nk; c.omap = nullptr; c.k = 1;
+        const size_t wsb = sizeof(T) * nk * 64;
+        ws.alloc(wsb, st);
+        corr_direct<T>(c, ws.as<T>(), wsb, st);
+        threshold_eq<T>(cnt.as<T>(), nk, (double)p.L, p.kmask.as<uint8_t>(), st);
+        if (p.has_comm) {
+            clear_band_kernel<<<(unsigned)std::min<int64_t>(cdiv(nk, 256), 16 * num_sms()), 256, 0, st>>>(
+                p.kmask.as<uint8_t>(), p.kx, p.ky, p.band_y0, p.band_y1);
+            after_launch("clear_band");
+        }
+        // compaction map box -> 𝔎 index (lex order)
+        DevBuf cc;
+        cc.alloc(sizeof(int32_t) * (p.ky + 1), st);
+        column_counts(p.kmask.as<uint8_t>(), p.kx, p.ky, cc.as<int32_t>(), st);
+        std::vector<int32_t> h(p.ky + 1, 0);
+        SSA_CUDA(cudaMemcpyAsync(h.data(), cc.p, sizeof(int32_t) * p.ky, cudaMemcpyDeviceToHost, st));
+        SSA_CUDA(cudaStreamSynchronize(st));
+        int64_t tot = 0;
+        for (int j = 0; j < p.ky; ++j) { const int32_t c0 = h[j]; h[j] = (int32_t)tot; tot += c0; }
+        p.K = tot;
+        p.full_k = (tot == nk);
+        if (!p.full_k) {
+            SSA_CUDA(cudaMemcpyAsync(cc.p, h.data(), sizeof(int32_t) * p.ky, cudaMemcpyHostToDevice, st));
+            p.kmap.alloc(sizeof(int32_t) * nk, st);
+            compact_map(p.kmask.as<uint8_t>(), p.kx, p.ky, cc.as<int32_t>(), p.kmap.as<int32_t>(), nullptr, p.nx, st);
+        }
+        SSA_CUDA(cudaStreamSynchronize(st));
+    }
+    if (p.K == 0) throw Error(SSA_ERR_EMPTY_KSHAPE, "no window position fits inside the shape (K-shape is empty)");
+
+    // a3: weights 𝕎 = diagsums(1_𝔏, 1_𝔎) (Alg. 4 step 1)
+    p.weights.alloc(sizeof(int32_t) * nxy, st);
+    if (p.full_window && p.full_k) {
+        weights_rect(p.nx, p.ny, p.lx, p.ly, p.weights.as<int32_t>(), st);
+        p.n_excluded = p.n_valid - nxy;   // all cells valid in this case -> 0
+        if (p.n_excluded < 0) p.n_excluded = 0;
+    } else {
+        DevBuf num, go, gi;
+        num.alloc(sizeof(T) * nxy, st);
+        int32_t hoff[2] = {0, 1}, hidx[1] = {0};
+        go.alloc(sizeof(hoff), st); gi.alloc(sizeof(hidx), st);
+        SSA_CUDA(cudaMemcpyAsync(go.p, hoff, sizeof(hoff), cudaMemcpyHostToDevice, st));
+        SSA_CUDA(cudaMemcpyAsync(gi.p, hidx, sizeof(hidx), cudaMemcpyHostToDevice, st));
+        AvgParams<T> a{};
+        a.nx = p.nx; a.ny = p.ny;
+        a.lx = p.lx; a.ly = p.ly; a.lmap = p.full_window ? nullptr : p.lmap.as<int>();
+        a.kx = p.kx; a.ky = p.ky; a.kmap = p.full_k ? nullptr : p.kmap.as<int>();
+        a.U = nullptr; a.V = nullptr; a.coef = nullptr;
+        a.grp_off = go.as<int>(); a.grp_idx = gi.as<int>(); a.ngroups = 1;
+        a.w = nullptr; a.out = num.as<T>(); a.ldout = p.nx; a.out_stride = nxy;
+        diagsums_direct<T>(a, st);
+        box_ones_to_int<T>(num.as<T>(), nxy, p.weights.as<int32_t>(), st);
+        std::vector<int32_t> wh(nxy);
+        SSA_CUDA(cudaMemcpyAsync(wh.data(), p.weights.p, sizeof(int32_t) * nxy, cudaMemcpyDeviceToHost, st));
+        SSA_CUDA(cudaStreamSynchronize(st));
+        int64_t np = 0;
+        for (int64_t t = 0; t < nxy; ++t) np += wh[t] > 0;
+        p.n_excluded = p.has_comm ? 0 : p.n_valid - np;
+    }
+    // workspaces
+    const int kmax = std::max(64, p.block_k);
+    p.ws_corr_bytes = std::min<size_t>((size_t)256 << 20,
+                                       (size_t)64 * p.lx * p.ly * (size_t)kmax * sizeof(T));
+    p.ws_corr_bytes = std::max(p.ws_corr_bytes, (size_t)p.lx * p.ly * (size_t)kmax * sizeof(T) * 2);
+    p.ws_corr.alloc(p.ws_corr_bytes, st);
+    p.ws_gram.alloc(gram_partial_bytes(std::max<int64_t>({p.L, p.K, nxy}), 64, 64), st);
+    // product path
+    if (p.path == SSA_PATH_FFT || p.path == SSA_PATH_AUTO) {
+        if (fft_supported(p)) {
+            fft_build(p);
+            p.path = SSA_PATH_FFT;
+        } else {
+            if (p.path == SSA_PATH_FFT) throw Error(SSA_ERR_ARG, "FFT path not available for this shape");
+            p.path = SSA_PATH_DIRECT;
+        }
+    }
+    SSA_CUDA(cudaStreamSynchronize(st));
+}
+
+template <typename T>
+static void get_v(PlanImpl &p) {
+    if (p.v_valid) return;
+    p.V.alloc(sizeof(T) * p.K * std::max(p.r, 1), p.st);
+    op_xtu<T>(p, p.U.as<T>(), p.L, p.V.as<T>(), p.K, p.r);
+    std::vector<double> inv(p.r);
+    for (int i = 0; i < p.r; ++i) inv[i] = p.sigma[i] > 0 ? 1.0 / p.sigma[i] : 0.0;
+    double *d = small_dev(p, std::max(p.r, 1));
+    SSA_CUDA(cudaMemcpyAsync(d, inv.data(), sizeof(double) * p.r, cudaMemcpyHostToDevice, p.st));
+    scale_columns<T>(p.K, p.V.as<T>(), p.K, p.r, d, p.st);
+    SSA_CUDA(cudaStreamSynchronize(p.st));
+    p.v_valid = true;
+}
+
+template <typename T>
+static void reconstruct_impl(PlanImpl &p, const int32_t *off, const int32_t *idx, int ng, int add_rest, T *out_dev) {
+    get_v<T>(p);
+    const int64_t nxy = (int64_t)p.nx * p.ny;
+    DevBuf go, gi, sig;
+    const int nidx = off[ng];
+    go.alloc(sizeof(int32_t) * (ng + 1), p.st);
+    gi.alloc(sizeof(int32_t) * std::max(nidx, 1), p.st);
+    sig.alloc(sizeof(double) * p.r, p.st);
+    SSA_CUDA(cudaMemcpyAsync(go.p, off, sizeof(int32_t) * (ng + 1), cudaMemcpyHostToDevice, p.st));
+    if (nidx) SSA_CUDA(cudaMemcpyAsync(gi.p, idx, sizeof(int32_t) * nidx, cudaMemcpyHostToDevice, p.st));
+    SSA_CUDA(cudaMemcpyAsync(sig.p, p.sigma.data(), sizeof(double) * p.r, cudaMemcpyHostToDevice, p.st));
+    if (ng > 0) {
+        AvgParams<T> a{};
+        a.nx = p.nx; a.ny = p.ny;
+        a.lx = p.lx; a.ly = p.ly; a.lmap = p.full_window ? nullptr : p.lmap.as<int>();
+        a.kx = p.kx; a.ky = p.ky; a.kmap = p.full_k ? nullptr : p.kmap.as<int>();
+        a.U = p.U.as<T>(); a.ldu = p.L; a.V = p.V.as<T>(); a.ldv = p.K; a.coef = sig.as<double>();
+        a.grp_off = go.as<int>(); a.grp_idx = gi.as<int>(); a.ngroups = ng;
+        a.w = p.weights.as<int>(); a.out = out_dev; a.ldout = p.nx; a.out_stride = nxy;
+        diagsums_direct<T>(a, p.st);
+    }
+    if (add_rest)
+        rest_group<T>(p.img.as<T>(), p.weights.as<int32_t>(), out_dev, ng, nxy, nxy, out_dev + (int64_t)ng * nxy, p.st);
+    SSA_CUDA(cudaStreamSynchronize(p.st));
+}
+
+}  // namespace ssa
+
+// =====================================================================================
+using namespace ssa;
+
+struct ssa_plan_s {
+    PlanImpl impl;
+};
+
+#define SSA_API_BEGIN try {
+#define SSA_API_END                                                          \
+    }                                                                        \
+    catch (const Error &e) {                                                 \
+        g_err = e.what();                                                    \
+        if (p && (e.code == SSA_ERR_CUDA || e.code == SSA_ERR_COMM)) p->impl.broken = true; \
+        return e.code;                                                       \
+    }                                                                        \
+    catch (const std::exception &e) {                                        \
+        g_err = e.what();                                                    \
+        return SSA_ERR_ARG;                                                  \
+    }
+
+static ssa_status check_plan(ssa_plan p) {
+    if (!p) { g_err = "null plan"; return SSA_ERR_ARG; }
+    if (p->impl.broken) { g_err = "plan is in a failed state (earlier CUDA/comm error); destroy it"; return SSA_ERR_CUDA; }
+    return SSA_OK;
+}
+
+extern "C" {
+
+const char *ssa_last_error(void) { return g_err.c_str(); }
+const char *ssa_version(void) { return "ssa_b200 0.1 (sm_100a)"; }
+int64_t ssa_launch_count(int reset) {
+    const int64_t n = g_launches;
+    if (reset) g_launches = 0;
+    return n;
+}
+
+ssa_status ssa_plan_create(const ssa_array *x, const ssa_window *w, const uint8_t *mask, const ssa_opts *opts,
+                           ssa_plan *out) {
+    ssa_plan p = nullptr;
+    SSA_API_BEGIN
+    if (!x || !w || !out || !x->data) throw Error(SSA_ERR_ARG, "null argument");
+    *out = nullptr;
+    if (x->dtype != SSA_F32 && x->dtype != SSA_F64) throw Error(SSA_ERR_ARG, "dtype must be SSA_F32 or SSA_F64");
+    if (x->nx < 1 || x->ny < 1 || x->nx > (1 << 24) || x->ny > (1 << 24) || x->nx * x->ny > ((int64_t)1 << 31))
+        throw Error(SSA_ERR_ARG, "array size out of range");
+    if (x->ld != 0 && x->ld < x->nx) throw Error(SSA_ERR_ARG, "ld < nx");
+    // window bounds
+    if (w->lx < 1 || w->ly < 1 || w->lx > x->nx || w->ly > x->ny || (int64_t)w->lx * w->ly <= 1 ||
+        (int64_t)w->lx * w->ly >= x->nx * x->ny)
+        throw Error(SSA_ERR_WINDOW, "window must satisfy 1<=Lx<=Nx, 1<=Ly<=Ny, 1<Lx*Ly<Nx*Ny");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        throw Error(SSA_ERR_CUDA, "no CUDA device: libssa_b200 has no CPU fallback");
+    }
+    p = new ssa_plan_s();
+    PlanImpl &P = p->impl;
+    P.nx = (int)x->nx; P.ny = (int)x->ny; P.lx = w->lx; P.ly = w->ly;
+    P.kx = P.nx - P.lx + 1; P.ky = P.ny - P.ly + 1;
+    P.dt = x->dtype;
+    ssa_opts o{};
+    if (opts) o = *opts;
+    P.st = (cudaStream_t)o.stream;
+    P.path = o.path;
+    P.block_k = o.block_k > 0 ? o.block_k : (P.dt == SSA_F64 ? 16 : 32);
+    P.tol = o.tol; P.max_products = o.max_products; P.seed = o.seed ? o.seed : 0x1309505000ull;
+    if (o.comm && o.comm->world > 1) {
+        P.comm = *o.comm; P.has_comm = true;
+        P.band_y0 = o.band_y0; P.band_y1 = o.band_y1;
+        if (P.band_y0 < 0 || P.band_y1 > P.ky || P.band_y0 >= P.band_y1)
+            throw Error(SSA_ERR_ARG, "band [y0,y1) outside the origin box");
+    }
+    // 𝔏 (window shape) on the host: box index -> lex index
+    P.lmap_host.assign((size_t)P.lx * P.ly, -1);
+    int64_t L = 0;
+    for (int64_t t = 0; t < (int64_t)P.lx * P.ly; ++t)
+        if (!w->wmask || w->wmask[t]) P.lmap_host[t] = (int32_t)L++;
+    if (L == 0) throw Error(SSA_ERR_WINDOW, "empty window shape");
+    P.L = L;
+    P.full_window = (L == (int64_t)P.lx * P.ly);
+    try {
+        if (P.dt == SSA_F64) build_plan<double>(P, x, mask);
+        else build_plan<float>(P, x, mask);
+    } catch (...) {
+        delete p;
+        throw;
+    }
+    *out = p;
+    return SSA_OK;
+    SSA_API_END
+}
+
+void ssa_plan_destroy(ssa_plan p) {
+    if (!p) return;
+    if (p->impl.st) cudaStreamSynchronize(p->impl.st);
+    delete p;
+}
+
+ssa_status ssa_plan_info(ssa_plan p, ssa_plan_info_t *info) {
+    if (ssa_status s = check_plan(p)) return s;
+    if (!info) { g_err = "null info"; return SSA_ERR_ARG; }
+    const PlanImpl &P = p->impl;
+    info->nx = P.nx; info->ny = P.ny; info->lx = P.lx; info->ly = P.ly; info->kx = P.kx; info->ky = P.ky;
+    info->L = P.L; info->K = P.K; info->n_valid = P.n_valid; info->n_excluded = P.n_excluded;
+    info->path = P.path; info->dtype = P.dt;
+    info->full_window = P.full_window; info->full_kshape = P.full_k;
+    return SSA_OK;
+}
+
+static void copy_out(PlanImpl &P, void *dst, const void *src, size_t bytes, int on_device) {
+    SSA_CUDA(cudaMemcpyAsync(dst, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P.st));
+    SSA_CUDA(cudaStreamSynchronize(P.st));
+}
+
+ssa_status ssa_get_weights(ssa_plan p, int32_t *w, int on_device) {
+    if (ssa_status s = check_plan(p)) return s;
+    SSA_API_BEGIN
+    if (!w) throw Error(SSA_ERR_ARG, "null output");
+    copy_out(p->impl, w, p->impl.weights.p, sizeof(int32_t) * p->impl.nx * p->impl.ny, on_device);
+    return SSA_OK;
+    SSA_API_END
+}
+
+ssa_status ssa_get_kmask(ssa_plan p, uint8_t *km, int on_device) {
+    if (ssa_status s = check_plan(p)) return s;
+    SSA_API_BEGIN
+    if (!km) throw Error(SSA_ERR_ARG, "null output");
+    copy_out(p->impl, km, p->impl.kmask.p, (size_t)p->impl.kx * p->impl.ky, on_device);
+    return SSA_OK;
+    SSA_API_END
+}
+
+ssa_status ssa_matmul(ssa_plan p, int transpose, const void *in, int64_t ldin, void *out, int64_t ldout, int64_t k,
+                      int on_device) {
+    if (ssa_status s = check_plan(p)) return s;
+    SSA_API_BEGIN
+    PlanImpl &P = p->impl;
+    if (!in || !out || k < 1 || k > (1 << 20)) throw Error(SSA_ERR_ARG, "bad matmul arguments");
+    const int64_t nin = transpose ? P.L : P.K, nout = transpose ? P.K : P.L;
+    if (ldin == 0) ldin = nin;
+    if (ldout == 0) ldout = nout;
+    if (ldin < nin || ldout < nout) throw Error(SSA_ERR_ARG, "leading dimension too small");
+    const size_t es = P.elem();
+    const void *din = in;
+    void *dout = out;
+    DevBuf bi, bo;
+    if (!on_device) {
+        bi.alloc(es * ldin * k, P.st);
+        bo.alloc(es * ldout * k, P.st);
+        SSA_CUDA(cudaMemcpyAsync(bi.p, in, es * ldin * k, cudaMemcpyHostToDevice, P.st));
+        din = bi.p; dout = bo.p;
+    }
+    if (P.dt == SSA_F64) {
+        if (transpose) op_xtu<double>(P, (const double *)din, ldin, (double *)dout, ldout, (int)k);
+        else op_xv<double>(P, (const double *)din, ldin, (double *)dout, ldout, (int)k);
+    } else {
+        if (transpose) op_xtu<float>(P, (const float *)din, ldin, (float *)dout, ldout, (int)k);
+        else op_xv<float>(P, (const float *)din, ldin, (float *)dout, ldout, (int)k);
+    }
+    if (!on_device) {
+        SSA_CUDA(cudaMemcpyAsync(out, bo.p, es * ldout * k, cudaMemcpyDeviceToHost, P.st));
+        SSA_CUDA(cudaStreamSynchronize(P.st));
+    }
+    return SSA_OK;
+    SSA_API_END
+}
+
+ssa_status ssa_decompose(ssa_plan p, int32_t r, ssa_decomp_info *info) {
+    if (ssa_status s = check_plan(p)) return s;
+    SSA_API_BEGIN
+    PlanImpl &P = p->impl;
+    if (r < 1 || r > std::min(P.L, P.K)) throw Error(SSA_ERR_RANK, "r must satisfy 1 <= r <= min(L, K)");
+    ssa_decomp_info tmp{};
+    ssa_decomp_info *inf = info ? info : &tmp;
+    std::memset(inf, 0, sizeof(*inf));
+    const auto t0 = std::chrono::steady_clock::now();
+    ssa_status st = SSA_OK;
+    try {
+        if (P.dt == SSA_F64) decompose<double>(P, r, inf);
+        else decompose<float>(P, r, inf);
+    } catch (const Error &e) {
+        if (e.code != SSA_ERR_NOT_CONVERGED) throw;
+        g_err = e.what();
+        st = e.code;
+    }
+    inf->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    P.last_info = *inf;
+    return st;
+    SSA_API_END
+}
+
+ssa_status ssa_get_rank(ssa_plan p, int32_t *r) {
+    if (ssa_status s = check_plan(p)) return s;
+    if (!r) { g_err = "null output"; return SSA_ERR_ARG; }
+    *r = p->impl.r;
+    return SSA_OK;
+}
+
+ssa_status ssa_get_sigma(ssa_plan p, double *sigma) {
+    if (ssa_status s = check_plan(p)) return s;
+    if (!sigma) { g_err = "null output"; return SSA_ERR_ARG; }
+    if (p->impl.r == 0) { g_err = "no decomposition"; return SSA_ERR_STATE; }
+    std::memcpy(sigma, p->impl.sigma.data(), sizeof(double) * p->impl.r);
+    return SSA_OK;
+}
+
+ssa_status ssa_get_u(ssa_plan p, void *U, int on_device) {
+    if (ssa_status s = check_plan(p)) return s;
+    SSA_API_BEGIN
+    PlanImpl &P = p->impl;
+    if (P.r == 0) throw Error(SSA_ERR_STATE, "no decomposition");
+    if (!U) throw Error(SSA_ERR_ARG, "null output");
+    copy_out(P, U, P.U.p, P.elem() * P.L * P.r, on_device);
+    return SSA_OK;
+    SSA_API_END
+}
+
+ssa_status ssa_get_v(ssa_plan p, void *V, int on_device) {
+    if (ssa_status s = check_plan(p)) return s;
+    SSA_API_BEGIN
+    PlanImpl &P = p->impl;
+    if (P.r == 0) throw Error(SSA_ERR_STATE, "no decomposition");
+    if (!V) throw Error(SSA_ERR_ARG, "null output");
+    if (P.dt == SSA_F64) get_v<double>(P); else get_v<float>(P);
+    copy_out(P, V, P.V.p, P.elem() * P.K * P.r, on_device);
+    return SSA_OK;
+    SSA_API_END
+}
+
+ssa_status ssa_set_triples(ssa_plan p, int32_t r, const double *sigma, const void *U, const void *V, int on_device) {
+    if (ssa_status s = check_plan(p)) return s;
+    SSA_API_BEGIN
+    PlanImpl &P = p->impl;
+    if (r < 1 || r > std::min(P.L, P.K)) throw Error(SSA_ERR_RANK, "bad r");
+    if (!sigma || !U) throw Error(SSA_ERR_ARG, "null sigma/U");
+    const size_t es = P.elem();
+    P.U.alloc(es * P.L * r, P.st);
+    SSA_CUDA(cudaMemcpyAsync(P.U.p, U, es * P.L * r, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P.st));
+    P.sigma.assign(sigma, sigma + r);
+    P.r = r;
+    P.v_valid = false;
+    if (V) {
+        P.V.alloc(es * P.K * r, P.st);
+        SSA_CUDA(cudaMemcpyAsync(P.V.p, V, es * P.K * r, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P.st));
+        P.v_valid = true;
+    }
+    SSA_CUDA(cudaStreamSynchronize(P.st));
+    return SSA_OK;
+    SSA_API_END
+}
+
+static void check_groups(const PlanImpl &P, const int32_t *off, const int32_t *idx, int32_t ng) {
+    if (ng < 0 || (ng > 0 && (!off || !idx))) throw Error(SSA_ERR_ARG, "bad group arrays");
+    if (ng == 0) return;
+    if (off[0] != 0) throw Error(SSA_ERR_ARG, "grp_off[0] must be 0");
+    for (int g = 0; g < ng; ++g)
+        if (off[g + 1] < off[g]) throw Error(SSA_ERR_ARG, "grp_off must be non-decreasing");
+    for (int t = 0; t < off[ng]; ++t)
+        if (idx[t] < 0 || idx[t] >= P.r) throw Error(SSA_ERR_RANK, "group index >= number of computed triples");
+}
+
+ssa_status ssa_reconstruct(ssa_plan p, const int32_t *off, const int32_t *idx, int32_t ng, int add_rest, void *out,
+                           int on_device) {
+    if (ssa_status s = check_plan(p)) return s;
+    SSA_API_BEGIN
+    PlanImpl &P = p->impl;
+    if (P.r == 0) throw Error(SSA_ERR_STATE, "reconstruct before decompose");
+    if (!out) throw Error(SSA_ERR_ARG, "null output");
+    check_groups(P, off, idx, ng);
+    if (P.has_comm) throw Error(SSA_ERR_ARG, "multi-GPU reconstruction: gather the bands on the caller side");
+    const int64_t nxy = (int64_t)P.nx * P.ny;
+    const int nout = ng + (add_rest ? 1 : 0);
+    const int32_t zero_off = 0;
+    if (ng == 0) off = &zero_off;
+    DevBuf tmp;
+    void *dout = out;
+    if (!on_device) {
+        tmp.alloc(P.elem() * nxy * std::max(nout, 1), P.st);
+        dout = tmp.p;
+    }
+    if (P.dt == SSA_F64) reconstruct_impl<double>(P, off, idx, ng, add_rest, (double *)dout);
+    else reconstruct_impl<float>(P, off, idx, ng, add_rest, (float *)dout);
+    if (!on_device) copy_out(P, out, dout, P.elem() * nxy * nout, 0);
+    return SSA_OK;
+    SSA_API_END
+}
+
+ssa_status ssa_wcor(ssa_plan p, const int32_t *off, const int32_t *idx, int32_t ng, double *rho) {
+    if (ssa_status s = check_plan(p)) return s;
+    SSA_API_BEGIN
+    PlanImpl &P = p->impl;
+    if (P.r == 0) throw Error(SSA_ERR_STATE, "wcor before decompose");
+    if (!rho || ng < 1 || ng > 64) throw Error(SSA_ERR_ARG, "wcor: 1..64 groups");
+    check_groups(P, off, idx, ng);
+    const int64_t nxy = (int64_t)P.nx * P.ny;
+    DevBuf rec;
+    rec.alloc(P.elem() * nxy * ng, P.st);
+    std::vector<double> G((size_t)ng * ng);
+    double *Gd = small_dev(P, 64 * 64);
+    if (P.dt == SSA_F64) {
+        reconstruct_impl<double>(P, off, idx, ng, 0, rec.as<double>());
+        weighted_sqrt_kernel<double><<<(unsigned)std::min<int64_t>(cdiv(nxy * ng, 256), 16 * num_sms()), 256, 0, P.st>>>(
+            rec.as<double>(), P.weights.as<int32_t>(), nxy, ng);
+        after_launch("weighted_sqrt");
+        gram_tn<double>(nxy, rec.as<double>(), nxy, ng, rec.as<double>(), nxy, ng, Gd, P.ws_gram.as<double>(), P.ws_gram.bytes, P.st);
+    } else {
+        reconstruct_impl<float>(P, off, idx, ng, 0, rec.as<float>());
+        weighted_sqrt_kernel<float><<<(unsigned)std::min<int64_t>(cdiv(nxy * ng, 256), 16 * num_sms()), 256, 0, P.st>>>(
+            rec.as<float>(), P.weights.as<int32_t>(), nxy, ng);
+        after_launch("weighted_sqrt");
+        gram_tn<float>(nxy, rec.as<float>(), nxy, ng, rec.as<float>(), nxy, ng, Gd, P.ws_gram.as<double>(), P.ws_gram.bytes, P.st);
+    }
+    SSA_CUDA(cudaMemcpyAsync(G.data(), Gd, sizeof(double) * ng * ng, cudaMemcpyDeviceToHost, P.st));
+    SSA_CUDA(cudaStreamSynchronize(P.st));
+    for (int b = 0; b < ng; ++b)
+        for (int a = 0; a < ng; ++a) {
+            const double d = std::sqrt(G[a + (size_t)ng * a] * G[b + (size_t)ng * b]);
+            rho[a + (size_t)ng * b] = d > 0 ? G[a + (size_t)ng * b] / d : 0.0;
+        }
+    return SSA_OK;
+    SSA_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,245 @@
+// Tall-skinny dense helpers for the block Lanczos solver:
+// Gram matrices Aᵀ B (fp64 accumulation across CTAs, deterministic), small
+// right-multiplications A·C, column scaling, and a counter-based normal RNG.
+// All are HBM-bound streaming kernels over M = L or K rows.
+#include "common.h"
+#include "kernels.h"
+
+namespace ssa {
+
+template <typename T> struct GramRows { static constexpr int value = sizeof(T) == 4 ? 64 : 32; };
+constexpr int kGramPad = 4;
+
+// One CTA = 256 threads, thread (ti, tj) owns G[4ti..4ti+3, 4tj..4tj+3].
+template <typename T>
+__global__ void __launch_bounds__(256)
+gram_tn_kernel(int64_t M, const T *__restrict__ A, int64_t lda, int n1,
+               const T *__restrict__ B, int64_t ldb, int n2, double *__restrict__ partials) {
+    constexpr int kGramRows = GramRows<T>::value;   // rows staged per iteration (static smem < 48 KB)
+    constexpr int P1 = 64 + kGramPad;
+    __shared__ __align__(16) T AS[kGramRows * P1];
+    __shared__ __align__(16) T BS[kGramRows * P1];
+    const int tid = threadIdx.x;
+    const int ti = tid % 16, tj = tid / 16;
+    double accd[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) accd[a][b] = 0.0;
+    const bool active = (4 * ti < n1) && (4 * tj < n2);
+    for (int64_t r0 = (int64_t)blockIdx.x * kGramRows; r0 < M; r0 += (int64_t)gridDim.x * kGramRows) {
+        __syncthreads();
+        for (int idx = tid; idx < kGramRows * 64; idx += 256) {
+            const int rl = idx % kGramRows, c = idx / kGramRows;
+            const int64_t row = r0 + rl;
+            T va = T(0), vb = T(0);
+            if (row < M) {
+                if (c < n1) va = A[row + lda * c];
+                if (c < n2) vb = B[row + ldb * c];
+            }
+            AS[rl * P1 + c] = va;
+            BS[rl * P1 + c] = vb;
+        }
+        __syncthreads();
+        if (active) {
+            T acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = T(0);
+#pragma unroll 4
+            for (int rl = 0; rl < kGramRows; ++rl) {
+                T av[4], bv[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) { av[a] = AS[rl * P1 + 4 * ti + a]; bv[a] = BS[rl * P1 + 4 * tj + a]; }
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) accd[a][b] += (double)acc[a][b];
+        }
+    }
+    if (!active) return;
+    double *out = partials + (int64_t)blockIdx.x * 64 * 64;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) out[(4 * ti + a) + 64 * (4 * tj + b)] = accd[a][b];
+}
+
+__global__ void gram_reduce_kernel(const double *__restrict__ partials, int nparts, int n1, int n2,
+                                   double *__restrict__ G) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n1 * n2) return;
+    const int a = e % n1, b = e / n1;
+    double s = 0.0;
+    for (int q = 0; q < nparts; ++q) s += partials[(int64_t)q * 4096 + a + 64 * b];
+    G[a + (int64_t)n1 * b] = s;
+}
+
+static int gram_ctas(int64_t M) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, 64), 2 * (int64_t)num_sms()));
+}
+
+size_t gram_partial_bytes(int64_t M, int, int) { return (size_t)gram_ctas(M) * 4096 * sizeof(double); }
+
+template <typename T>
+void gram_tn(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb, int n2,
+             double *G, double *partials, size_t partial_bytes, cudaStream_t st) {
+    SSA_REQUIRE(n1 <= 64 && n2 <= 64, SSA_ERR_ARG, "gram_tn: at most 64 columns per call");
+    const int ctas = gram_ctas(M);
+    SSA_REQUIRE((size_t)ctas * 4096 * sizeof(double) <= partial_bytes, SSA_ERR_ARG, "gram_tn: workspace");
+    gram_tn_kernel<T><<<ctas, 256, 0, st>>>(M, A, lda, n1, B, ldb, n2, partials);
+    after_launch("gram_tn");
+    gram_reduce_kernel<<<(unsigned)cdiv(n1 * n2, 256), 256, 0, st>>>(partials, ctas, n1, n2, G);
+    after_launch("gram_reduce");
+}
+template void gram_tn<float>(int64_t, const float *, int64_t, int, const float *, int64_t, int, double *,
+                             double *, size_t, cudaStream_t);
+template void gram_tn<double>(int64_t, const double *, int64_t, int, const double *, int64_t, int,
+                              double *, double *, size_t, cudaStream_t);
+
+// Out = beta*Out + alpha*A*C.  Thread per row; the row of A is held in registers
+// before any store, so Out == A (m == n) is safe.
+template <typename T>
+__global__ void __launch_bounds__(128)
+gemm_small_kernel(int64_t M, const T *A, int64_t lda, int m, const double *__restrict__ C, int ldc,
+                  int n, double alpha, double beta, T *Out, int64_t ldo) {
+    __shared__ T CS[64 * 64];
+    for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
+        const int a = idx % m, b = idx / m;
+        CS[a * 64 + b] = (T)(alpha * C[a + (int64_t)ldc * b]);
+    }
+    __syncthreads();
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= M) return;
+    T a[64];
+#pragma unroll
+    for (int c = 0; c < 64; ++c) a[c] = (c < m) ? A[row + lda * c] : T(0);
+    for (int b0 = 0; b0 < n; b0 += 16) {
+        T acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = T(0);
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+            if (c < m) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] = fma(a[c], CS[c * 64 + b0 + j], acc[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int b = b0 + j;
+            if (b < n) {
+                T *o = Out + row + ldo * b;
+                *o = (beta == 0.0) ? acc[j] : fma((T)beta, *o, acc[j]);
+            }
+        }
+    }
+}
+
+template <typename T>
+void gemm_small(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n,
+                double alpha, double beta, T *Out, int64_t ldo, cudaStream_t st) {
+    SSA_REQUIRE(m <= 64 && n <= 64, SSA_ERR_ARG, "gemm_small: at most 64x64");
+    if (M <= 0 || n <= 0) return;
+    gemm_small_kernel<T><<<(unsigned)cdiv(M, 128), 128, 0, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
+    after_launch("gemm_small");
+}
+template void gemm_small<float>(int64_t, const float *, int64_t, int, const double *, int, int, double,
+                                double, float *, int64_t, cudaStream_t);
+template void gemm_small<double>(int64_t, const double *, int64_t, int, const double *, int, int, double,
+                                 double, double *, int64_t, cudaStream_t);
+
+// ---- counter-based normal generator (splitmix64 + Box-Muller) -------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <typename T>
+__global__ void fill_normal_kernel(int64_t M, T *A, int64_t lda, int ncols, uint64_t seed, uint64_t sid) {
+    const int64_t n = M * ncols;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = t % M, col = t / M;
+        const uint64_t h = mix64(seed ^ mix64(sid * 0x100000001B3ull + (uint64_t)col) ^ (uint64_t)row * 0xD6E8FEB86659FD93ull);
+        const double u1 = ((h >> 11) + 1.0) * (1.0 / 9007199254740993.0);
+        const double u2 = (double)(mix64(h) >> 11) * (1.0 / 9007199254740992.0);
+        A[row + lda * col] = (T)(sqrt(-2.0 * log(u1)) * cospi(2.0 * u2));
+    }
+}
+
+template <typename T>
+void fill_normal(int64_t M, T *A, int64_t lda, int ncols, uint64_t seed, uint64_t sid, cudaStream_t st) {
+    const int64_t n = M * ncols;
+    if (n <= 0) return;
+    fill_normal_kernel<T><<<(unsigned)std::min<int64_t>(cdiv(n, 256), 16 * num_sms()), 256, 0, st>>>(
+        M, A, lda, ncols, seed, sid);
+    after_launch("fill_normal");
+}
+template void fill_normal<float>(int64_t, float *, int64_t, int, uint64_t, uint64_t, cudaStream_t);
+template void fill_normal<double>(int64_t, double *, int64_t, int, uint64_t, uint64_t, cudaStream_t);
+
+template <typename T>
+__global__ void scale_columns_kernel(int64_t M, T *A, int64_t lda, int n, const double *__restrict__ s) {
+    const int64_t tot = M * n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = t % M, col = t / M;
+        A[row + lda * col] *= (T)s[col];
+    }
+}
+
+template <typename T>
+void scale_columns(int64_t M, T *A, int64_t lda, int n, const double *s, cudaStream_t st) {
+    const int64_t tot = M * n;
+    if (tot <= 0) return;
+    scale_columns_kernel<T><<<(unsigned)std::min<int64_t>(cdiv(tot, 256), 16 * num_sms()), 256, 0, st>>>(
+        M, A, lda, n, s);
+    after_launch("scale_columns");
+}
+template void scale_columns<float>(int64_t, float *, int64_t, int, const double *, cudaStream_t);
+template void scale_columns<double>(int64_t, double *, int64_t, int, const double *, cudaStream_t);
+
+}  // namespace ssa
+
+namespace ssa {
+// Sign convention: flip each column so that its
+// largest-|.| entry is positive.  One CTA per column; writes ±1 into sgn.
+template <typename T>
+__global__ void absmax_sign_kernel(int64_t M, const T *A, int64_t lda, double *sgn) {
+    const int col = blockIdx.x;
+    double best = -1.0; int64_t bi = 0;
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+        const double v = fabs((double)A[i + lda * col]);
+        if (v > best) { best = v; bi = i; }
+    }
+    __shared__ double sb[256];
+    __shared__ int64_t si[256];
+    sb[threadIdx.x] = best; si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            const double b2 = sb[threadIdx.x + o]; const int64_t i2 = si[threadIdx.x + o];
+            if (b2 > sb[threadIdx.x] || (b2 == sb[threadIdx.x] && i2 < si[threadIdx.x])) {
+                sb[threadIdx.x] = b2; si[threadIdx.x] = i2;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sgn[col] = ((double)A[si[0] + lda * col] < 0.0) ? -1.0 : 1.0;
+}
+template <typename T>
+void absmax_sign(int64_t M, const T *A, int64_t lda, int n, double *sgn, cudaStream_t st) {
+    if (n <= 0) return;
+    absmax_sign_kernel<T><<<n, 256, 0, st>>>(M, A, lda, sgn);
+    after_launch("absmax_sign");
+}
+template void absmax_sign<float>(int64_t, const float *, int64_t, int, double *, cudaStream_t);
+template void absmax_sign<double>(int64_t, const double *, int64_t, int, double *, cudaStream_t);
+}  // namespace ssa

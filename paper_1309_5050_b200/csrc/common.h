@@ -1,0 +1,72 @@
+// Internal helpers shared by the CUDA translation units of libssa_b200.so.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ssa_b200.h"
+
+namespace ssa {
+
+// Error carried from deep inside the library to the ABI boundary, where it is
+// turned into an ssa_status plus the thread-local message (no exception ever
+// crosses the C ABI).
+struct Error : std::runtime_error {
+    ssa_status code;
+    Error(ssa_status c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define SSA_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            throw ::ssa::Error(e_ == cudaErrorMemoryAllocation ? SSA_ERR_OOM : SSA_ERR_CUDA, \
+                               std::string(#call) + ": " + cudaGetErrorString(e_));      \
+    } while (0)
+
+#define SSA_REQUIRE(cond, code, msg)                      \
+    do {                                                  \
+        if (!(cond)) throw ::ssa::Error((code), (msg));   \
+    } while (0)
+
+// Count of kernels launched through this library on the calling thread.
+void count_launch(int n = 1);
+// Check the last launch and count it.
+void after_launch(const char *what);
+
+// Owning device buffer (cudaMallocAsync on the plan's stream).
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    DevBuf(DevBuf &&o) noexcept { *this = std::move(o); }
+    DevBuf &operator=(DevBuf &&o) noexcept {
+        if (this != &o) { release(); p = o.p; bytes = o.bytes; s = o.s; o.p = nullptr; o.bytes = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t n, cudaStream_t st) {
+        if (n <= bytes && p) return;
+        release();
+        s = st;
+        SSA_CUDA(cudaMalloc(&p, n ? n : 16));
+        bytes = n;
+    }
+    void release() {
+        if (p) { cudaFree(p); p = nullptr; bytes = 0; }
+    }
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+
+int num_sms();
+
+}  // namespace ssa

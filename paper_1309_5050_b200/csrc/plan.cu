@@ -1,0 +1,153 @@
+// Plan-time kernels: shape ingestion, 𝔎 selection,
+// compaction maps, rectangular weights, and small elementwise epilogues.
+#include "common.h"
+#include "kernels.h"
+
+namespace ssa {
+
+// a1: 𝔑 = {finite cells} ∩ mask; cells outside 𝔑 are set to 0
+// (they never enter 𝒯(𝕏) because every κ ∈ 𝔎 keeps its window inside 𝔑).
+template <typename T>
+__global__ void prep_image_kernel(const T *src, int64_t ld_src, int nx, int ny, const uint8_t *mask,
+                                  T *dst, uint8_t *nmask) {
+    const int64_t n = (int64_t)nx * ny;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t % nx, j = t / nx;
+        const T v = src[i + ld_src * j];
+        const bool in = isfinite((double)v) && (mask == nullptr || mask[t] != 0);
+        dst[t] = in ? v : T(0);
+        nmask[t] = in ? 1 : 0;
+    }
+}
+
+template <typename T>
+void prep_image(const T *src, int64_t ld_src, int nx, int ny, const uint8_t *mask, T *dst, uint8_t *nmask,
+                cudaStream_t st) {
+    const int64_t n = (int64_t)nx * ny;
+    prep_image_kernel<T><<<(unsigned)std::min<int64_t>(cdiv(n, 256), 16 * num_sms()), 256, 0, st>>>(
+        src, ld_src, nx, ny, mask, dst, nmask);
+    after_launch("prep_image");
+}
+template void prep_image<float>(const float *, int64_t, int, int, const uint8_t *, float *, uint8_t *, cudaStream_t);
+template void prep_image<double>(const double *, int64_t, int, int, const uint8_t *, double *, uint8_t *, cudaStream_t);
+
+// a2 (Alg. 6 step 3): 𝔎 = {κ : v_κ = |𝔏|}, v = 𝒯ᵀ(I^𝔑)·1_𝔏 (exact integers).
+template <typename T>
+__global__ void threshold_eq_kernel(const T *c, int64_t n, double value, uint8_t *out) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        out[t] = ((double)c[t] == value) ? 1 : 0;
+}
+template <typename T>
+void threshold_eq(const T *counts, int64_t n, double value, uint8_t *out, cudaStream_t st) {
+    threshold_eq_kernel<T><<<(unsigned)std::min<int64_t>(cdiv(n, 256), 16 * num_sms()), 256, 0, st>>>(
+        counts, n, value, out);
+    after_launch("threshold_eq");
+}
+template void threshold_eq<float>(const float *, int64_t, double, uint8_t *, cudaStream_t);
+template void threshold_eq<double>(const double *, int64_t, double, uint8_t *, cudaStream_t);
+
+template <typename T>
+__global__ void to_int_kernel(const T *s, int64_t n, int32_t *d) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        d[t] = (int32_t)llrint((double)s[t]);
+}
+template <typename T>
+void box_ones_to_int(const T *src, int64_t n, int32_t *dst, cudaStream_t st) {
+    to_int_kernel<T><<<(unsigned)std::min<int64_t>(cdiv(n, 256), 16 * num_sms()), 256, 0, st>>>(src, n, dst);
+    after_launch("to_int");
+}
+template void box_ones_to_int<float>(const float *, int64_t, int32_t *, cudaStream_t);
+template void box_ones_to_int<double>(const double *, int64_t, int32_t *, cudaStream_t);
+
+// Compaction of a (bx x by) mask in lexicographic (x-fastest) order:
+// one warp per column counts its cells, the host scans the column counts,
+// then one warp per column assigns ranks with ballots.
+__global__ void column_counts_kernel(const uint8_t *m, int bx, int by, int32_t *counts) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+    if (warp >= by) return;
+    int c = 0;
+    for (int i = lane; i < bx; i += 32) c += m[i + (int64_t)bx * warp] ? 1 : 0;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) counts[warp] = c;
+}
+void column_counts(const uint8_t *m, int bx, int by, int32_t *counts, cudaStream_t st) {
+    column_counts_kernel<<<(unsigned)cdiv((int64_t)by * 32, 256), 256, 0, st>>>(m, bx, by, counts);
+    after_launch("column_counts");
+}
+
+__global__ void compact_map_kernel(const uint8_t *m, int bx, int by, const int32_t *col_start, int32_t *map,
+                                   int32_t *pos, int64_t ld_img) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+    if (warp >= by) return;
+    int base = col_start[warp];
+    for (int i0 = 0; i0 < bx; i0 += 32) {
+        const int i = i0 + lane;
+        const bool v = (i < bx) && m[i + (int64_t)bx * warp];
+        const unsigned b = __ballot_sync(0xffffffffu, v);
+        const int rank = __popc(b & ((1u << lane) - 1u));
+        if (i < bx) {
+            map[i + (int64_t)bx * warp] = v ? base + rank : -1;
+            if (v && pos) pos[base + rank] = (int32_t)(i + ld_img * warp);
+        }
+        base += __popc(b);
+    }
+}
+void compact_map(const uint8_t *m, int bx, int by, const int32_t *col_start, int32_t *map, int32_t *pos,
+                 int64_t ld_img, cudaStream_t st) {
+    compact_map_kernel<<<(unsigned)cdiv((int64_t)by * 32, 256), 256, 0, st>>>(m, bx, by, col_start, map, pos, ld_img);
+    after_launch("compact_map");
+}
+
+// a3 for full rectangles: 𝕎 = w_x ⊗ w_y with w = (1, 2, .., L*, .., L*, .., 2, 1)
+// (Alg. 2 step 2; the 2-D weights factor because 𝒯 is separable).
+__global__ void weights_rect_kernel(int nx, int ny, int lx, int ly, int32_t *w) {
+    const int64_t n = (int64_t)nx * ny;
+    const int kx = nx - lx + 1, ky = ny - ly + 1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t % nx), j = (int)(t / nx);
+        const int wx = min(min(i + 1, nx - i), min(lx, kx));
+        const int wy = min(min(j + 1, ny - j), min(ly, ky));
+        w[t] = wx * wy;
+    }
+}
+void weights_rect(int nx, int ny, int lx, int ly, int32_t *w, cudaStream_t st) {
+    const int64_t n = (int64_t)nx * ny;
+    weights_rect_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 16 * num_sms()), 256, 0, st>>>(nx, ny, lx, ly, w);
+    after_launch("weights_rect");
+}
+
+// "rest" group of eq. P:440-443: 𝕏 − Σ_g X̃_g on 𝔑′ (NaN elsewhere).
+template <typename T>
+__global__ void rest_kernel(const T *x, const int32_t *w, const T *groups, int ng, int64_t stride, int64_t n, T *rest) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        if (w[t] <= 0) { rest[t] = (T)NAN; continue; }
+        T s = x[t];
+        for (int g = 0; g < ng; ++g) s -= groups[g * stride + t];
+        rest[t] = s;
+    }
+}
+template <typename T>
+void rest_group(const T *x, const int32_t *w, const T *groups, int ngroups, int64_t stride, int64_t n, T *rest,
+                cudaStream_t st) {
+    rest_kernel<T><<<(unsigned)std::min<int64_t>(cdiv(n, 256), 16 * num_sms()), 256, 0, st>>>(
+        x, w, groups, ngroups, stride, n, rest);
+    after_launch("rest_group");
+}
+template void rest_group<float>(const float *, const int32_t *, const float *, int, int64_t, int64_t, float *, cudaStream_t);
+template void rest_group<double>(const double *, const int32_t *, const double *, int, int64_t, int64_t, double *, cudaStream_t);
+
+template <typename T>
+__global__ void cast_kernel(const void *src, int is_double, T *dst, int64_t n) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        dst[t] = is_double ? (T)((const double *)src)[t] : (T)((const float *)src)[t];
+}
+template <typename T>
+void cast_copy(const void *src, int src_is_double, T *dst, int64_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    cast_kernel<T><<<(unsigned)std::min<int64_t>(cdiv(n, 256), 16 * num_sms()), 256, 0, st>>>(src, src_is_double, dst, n);
+    after_launch("cast_copy");
+}
+template void cast_copy<float>(const void *, int, float *, int64_t, cudaStream_t);
+template void cast_copy<double>(const void *, int, double *, int64_t, cudaStream_t);
+
+}  // namespace ssa

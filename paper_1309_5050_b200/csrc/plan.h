@@ -1,0 +1,76 @@
+// Plan object behind the opaque ssa_plan handle.
+#pragma once
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.h"
+
+namespace ssa {
+
+struct FftOperator;   // fft.cu
+
+struct PlanImpl {
+    // ---- geometry (0-based; x fastest) -------------------------------------
+    int nx = 0, ny = 0, lx = 0, ly = 0, kx = 0, ky = 0;
+    int64_t L = 0, K = 0, n_valid = 0, n_excluded = 0;
+    bool full_window = true, full_k = true;
+    ssa_dtype dt = SSA_F32;
+    int path = SSA_PATH_DIRECT;
+    int block_k = 32;
+    double tol = 0;
+    int max_products = 0;
+    uint64_t seed = 0;
+    cudaStream_t st = nullptr;
+    ssa_comm comm{};
+    bool has_comm = false;
+    int64_t band_y0 = 0, band_y1 = 0;
+    bool broken = false;          // sticky CUDA / comm failure
+
+    // ---- device data ---------------------------------------------------------
+    DevBuf img;       // T[nx*ny], 0 outside 𝔑
+    DevBuf nmask;     // u8[nx*ny]
+    DevBuf lmap;      // int32[lx*ly] box -> 𝔏 index or -1 (only if !full_window)
+    DevBuf kmask;     // u8[kx*ky]
+    DevBuf kmap;      // int32[kx*ky] box -> 𝔎 index or -1 (only if !full_k)
+    DevBuf weights;   // int32[nx*ny]
+    DevBuf ws_corr;   // split-K partials of the direct products
+    size_t ws_corr_bytes = 0;
+    DevBuf ws_gram;   // gram partials
+    DevBuf dsmall;    // device scratch for small double matrices
+    std::vector<int32_t> lmap_host;   // 𝔏 positions (box indices) in lex order
+    FftOperator *fft = nullptr;       // FFT correlation path (null if not built)
+
+    // ---- decomposition ------------------------------------------------------
+    int r = 0;
+    std::vector<double> sigma;
+    DevBuf U;          // T[L*r]
+    DevBuf V;          // T[K*r] (valid if v_valid)
+    bool v_valid = false;
+    ssa_decomp_info last_info{};
+
+    size_t elem() const { return dt == SSA_F64 ? 8 : 4; }
+    ~PlanImpl();
+};
+
+// product dispatch (api.cu)
+template <typename T>
+void op_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k);    // U = X V
+template <typename T>
+void op_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k);   // V = Xᵀ U
+double *small_dev(PlanImpl &p, size_t n_doubles);
+
+// solver.cu
+template <typename T>
+void decompose(PlanImpl &p, int r, ssa_decomp_info *info);
+
+// fft.cu
+bool fft_supported(const PlanImpl &p);
+void fft_build(PlanImpl &p);
+template <typename T>
+void fft_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k);
+template <typename T>
+void fft_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k);
+void fft_destroy(FftOperator *f);
+
+}  // namespace ssa

@@ -1,0 +1,333 @@
+// Step 2 of the method (SVD) for the implicit trajectory operator:
+// block Golub-Kahan-Lanczos bidiagonalisation with full reorthogonalisation and
+// thick restarts.  The paper only names
+// Lanczos back-ends (nu-TRLan, PROPACK: P:806-823);
+// the recurrences below are standard linear algebra:
+//
+//   X·Q_j   = Pb·C_j + P_{j+1} B_{j+1}      (L side; C_j = full projection onto Pb)
+//   Xᵀ·P_j  = (…)    + Q_{j+1} A_{j+1}      (K side, CGS2 against the K basis)
+//   X·Qb'   = Pb·T   with T the projected matrix (block bidiagonal, plus an
+//                    arrow part after a restart)
+//
+// Ritz triples come from the fp64 SVD T = Y Θ Zᵀ (one-sided Jacobi on the
+// host, never from eigenvalues of TᵀT), U = Pb·Y, σ = Θ, and the residual of
+// triple i is ||Xᵀu_i − θ_i v_i|| = ||A_last · y_i(last block)||.  A restart
+// keeps the top p Ritz pairs: Pb ← Pb·Y_p, Qb ← [Qb'·Z_p, Q_last], T ← diag(Θ_p)
+// (X·(Qb'Z_p) = Pb·Y_p·Θ_p holds exactly).  Bases are orthonormalised with
+// SVQB (eigen-decomposition of the column-scaled Gram, Stathopoulos & Wu) run
+// twice; numerically dependent directions are replaced by seeded random ones
+// (or zeroed once the space is exhausted).  V is recomputed as XᵀU/σ.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.h"
+#include "dense.h"
+#include "kernels.h"
+#include "plan.h"
+
+namespace ssa {
+
+template <typename T>
+struct Gkl {
+    PlanImpl &p;
+    cudaStream_t st;
+    int64_t L, K;
+    int k, r, pk, nQmax;
+    DevBuf Pb, Qb, Ptmp, Qtmp;
+    int nP = 0, nQ = 0;
+    std::vector<double> Tm;   // nQmax x nQmax host, column-major
+    int ldT;
+    std::vector<double> Alast;
+    double anorm = 0.0;
+    int64_t nblock = 0, nvec = 0;
+    uint64_t sid = 1;
+    double thr_abs, thr_rel;
+
+    explicit Gkl(PlanImpl &pl) : p(pl), st(pl.st), L(pl.L), K(pl.K) {
+        thr_abs = (sizeof(T) == 4) ? 1e-6 : 1e-14;
+        thr_rel = (sizeof(T) == 4) ? 1e-10 : 1e-26;
+    }
+
+    T *P(int col) { return Pb.as<T>() + (int64_t)col * L; }
+    T *Q(int col) { return Qb.as<T>() + (int64_t)col * K; }
+
+    bool kside_comm() const { return p.has_comm && p.comm.world > 1; }
+
+    // G (n1 x n2, host, column-major ld n1) = Aᵀ B; chunked by 64 columns.
+    void gram(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb, int n2, double *G, bool kside) {
+        double *Gd = small_dev(p, 64 * 64);
+        std::vector<double> h(64 * 64);
+        for (int a0 = 0; a0 < n1; a0 += 64) {
+            const int na = std::min(64, n1 - a0);
+            for (int b0 = 0; b0 < n2; b0 += 64) {
+                const int nb = std::min(64, n2 - b0);
+                gram_tn<T>(M, A + lda * a0, lda, na, B + ldb * b0, ldb, nb, Gd, p.ws_gram.as<double>(),
+                           p.ws_gram.bytes, st);
+                if (kside && kside_comm()) {
+                    if (p.comm.allreduce_sum(p.comm.user, Gd, (int64_t)na * nb, SSA_F64, st) != 0)
+                        throw Error(SSA_ERR_COMM, "allreduce of a K-side Gram failed");
+                }
+                SSA_CUDA(cudaMemcpyAsync(h.data(), Gd, sizeof(double) * na * nb, cudaMemcpyDeviceToHost, st));
+                SSA_CUDA(cudaStreamSynchronize(st));
+                for (int b = 0; b < nb; ++b)
+                    for (int a = 0; a < na; ++a) G[(a0 + a) + (int64_t)n1 * (b0 + b)] = h[a + (int64_t)na * b];
+            }
+        }
+    }
+
+    // Out[:, 0:n] = beta*Out + alpha * A[:, 0:m] * C (C: m x n host, ld ldc)
+    void gemm(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha, double beta,
+              T *Out, int64_t ldo) {
+        double *Cd = small_dev(p, 64 * 64);
+        std::vector<double> h(64 * 64);
+        for (int c0 = 0; c0 < n; c0 += 64) {
+            const int nc = std::min(64, n - c0);
+            for (int m0 = 0; m0 < m; m0 += 64) {
+                const int mc = std::min(64, m - m0);
+                for (int b = 0; b < nc; ++b)
+                    for (int a = 0; a < mc; ++a) h[a + 64 * b] = C[(m0 + a) + (int64_t)ldc * (c0 + b)];
+                SSA_CUDA(cudaMemcpyAsync(Cd, h.data(), sizeof(double) * 64 * nc, cudaMemcpyHostToDevice, st));
+                gemm_small<T>(M, A + lda * m0, lda, mc, Cd, 64, nc, alpha, (m0 == 0) ? beta : 1.0, Out + ldo * c0, ldo, st);
+                // h is reused: make sure the copy has consumed it
+                SSA_CUDA(cudaStreamSynchronize(st));
+            }
+        }
+    }
+
+    // W -= Bm * (Bmᵀ W); returns the coefficients if coef != null (nb x kc, accumulated)
+    void cgs(int64_t M, T *W, int kc, const T *Bm, int nb, bool kside, double *coef) {
+        if (nb <= 0) return;
+        std::vector<double> C((size_t)nb * kc);
+        gram(M, Bm, M, nb, W, M, kc, C.data(), kside);
+        gemm(M, Bm, M, nb, C.data(), nb, kc, -1.0, 1.0, W, M);
+        if (coef)
+            for (size_t t = 0; t < C.size(); ++t) coef[t] += C[t];
+    }
+
+    // Orthonormalise W (M x kc) against `against` (na columns) and internally.
+    // Returns B (kc x kc, column-major) with W_in ≈ against·(·) + W_out·B.
+    std::vector<double> orth(int64_t M, T *W, int kc, const T *against, int na, bool kside) {
+        std::vector<double> B((size_t)kc * kc, 0.0);
+        for (int i = 0; i < kc; ++i) B[i + (size_t)kc * i] = 1.0;
+        std::vector<double> G((size_t)kc * kc), Gh((size_t)kc * kc), E((size_t)kc * kc), lam(kc);
+        std::vector<double> S((size_t)kc * kc), Bp((size_t)kc * kc), Bn((size_t)kc * kc);
+        for (int pass = 0; pass < 4; ++pass) {
+            if (na > 0) cgs(M, W, kc, against, na, kside, nullptr);
+            gram(M, W, M, kc, W, M, kc, G.data(), kside);
+            std::vector<double> d(kc);
+            std::vector<char> good(kc);
+            for (int j = 0; j < kc; ++j) {
+                d[j] = std::sqrt(std::max(G[j + (size_t)kc * j], 0.0));
+                good[j] = d[j] > thr_abs * std::max(anorm, 1e-300) && d[j] > 0.0;
+            }
+            for (int b = 0; b < kc; ++b)
+                for (int a = 0; a < kc; ++a)
+                    Gh[a + (size_t)kc * b] = (good[a] && good[b]) ? G[a + (size_t)kc * b] / (d[a] * d[b])
+                                                                   : (a == b ? 0.0 : 0.0);
+            sym_eig(kc, Gh.data(), lam.data(), E.data());
+            std::vector<int> bad;
+            for (int j = 0; j < kc; ++j) {
+                const bool ok = lam[j] > thr_rel;
+                const double isq = ok ? 1.0 / std::sqrt(lam[j]) : 0.0;
+                const double sq = ok ? std::sqrt(lam[j]) : 0.0;
+                for (int a = 0; a < kc; ++a) {
+                    const double dinv = good[a] ? 1.0 / d[a] : 0.0;
+                    S[a + (size_t)kc * j] = dinv * E[a + (size_t)kc * j] * isq;          // D⁻¹ E Λ^{-1/2}
+                    Bp[j + (size_t)kc * a] = sq * E[a + (size_t)kc * j] * (good[a] ? d[a] : 0.0);  // Λ^{1/2} Eᵀ D
+                }
+                if (!ok) bad.push_back(j);
+            }
+            gemm(M, W, M, kc, S.data(), kc, kc, 1.0, 0.0, W, M);   // in place (kc <= 64)
+            for (int b = 0; b < kc; ++b)
+                for (int a = 0; a < kc; ++a) {
+                    double s = 0.0;
+                    for (int t = 0; t < kc; ++t) s += Bp[a + (size_t)kc * t] * B[t + (size_t)kc * b];
+                    Bn[a + (size_t)kc * b] = s;
+                }
+            B.swap(Bn);
+            if (bad.empty()) {
+                if (pass >= 1) break;
+                continue;
+            }
+            if (pass >= 2) break;   // space exhausted: those columns stay zero
+            for (int j : bad) fill_normal<T>(M, W + M * j, M, 1, p.seed, 0x5eed0000ull + (sid++), st);
+        }
+        return B;
+    }
+
+    // every block product is bracketed by CUDA events on the plan's stream so the
+    // device time spent in the trajectory products is reported (ms_products)
+    std::vector<cudaEvent_t> ev;
+    void mark() {
+        cudaEvent_t e;
+        SSA_CUDA(cudaEventCreate(&e));
+        SSA_CUDA(cudaEventRecord(e, st));
+        ev.push_back(e);
+    }
+    double product_ms() {
+        double ms = 0.0;
+        if (!ev.empty()) SSA_CUDA(cudaEventSynchronize(ev.back()));
+        for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+            float t = 0.f;
+            SSA_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+            ms += t;
+        }
+        return ms;
+    }
+    ~Gkl() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+    void product_xv(const T *Qin, T *Out, int kc) {
+        mark();
+        op_xv<T>(p, Qin, K, Out, L, kc);
+        mark();
+        ++nblock; nvec += kc;
+    }
+    void product_xtu(const T *Pin, T *Out, int kc) {
+        mark();
+        op_xtu<T>(p, Pin, L, Out, K, kc);
+        mark();
+        ++nblock; nvec += kc;
+    }
+
+    double &Tat(int i, int j) { return Tm[(size_t)i + (size_t)ldT * j]; }
+
+    void stepA() {
+        const int qc = nQ - k;
+        T *W = P(nP);
+        product_xv(Q(qc), W, k);
+        std::vector<double> C((size_t)nP * k, 0.0);
+        cgs(L, W, k, P(0), nP, false, C.data());
+        cgs(L, W, k, P(0), nP, false, C.data());
+        for (int b = 0; b < k; ++b)
+            for (int a = 0; a < nP; ++a) Tat(a, qc + b) = C[a + (size_t)nP * b];
+        if (anorm == 0.0) {
+            std::vector<double> G((size_t)k * k);
+            gram(L, W, L, k, W, L, k, G.data(), false);
+            for (int j = 0; j < k; ++j) anorm = std::max(anorm, std::sqrt(std::max(G[j + (size_t)k * j], 0.0)));
+        }
+        std::vector<double> B = orth(L, W, k, P(0), nP, false);
+        for (int b = 0; b < k; ++b)
+            for (int a = 0; a < k; ++a) Tat(nP + a, qc + b) = B[a + (size_t)k * b];
+        nP += k;
+    }
+
+    void stepB() {
+        const int pc = nP - k;
+        T *W = Q(nQ);
+        product_xtu(P(pc), W, k);
+        if (anorm == 0.0) {
+            std::vector<double> G((size_t)k * k);
+            gram(K, W, K, k, W, K, k, G.data(), true);
+            for (int j = 0; j < k; ++j) anorm = std::max(anorm, std::sqrt(std::max(G[j + (size_t)k * j], 0.0)));
+        }
+        Alast = orth(K, W, k, Q(0), nQ, true);
+        nQ += k;
+    }
+
+    void run(int r_, ssa_decomp_info *info) {
+        r = r_;
+        const int64_t mn = std::min(L, K);
+        k = std::max(1, std::min<int>(p.block_k, 64));
+        if (k > mn) k = (int)mn;
+        pk = (int)std::min<int64_t>(r + std::max(4, k / 2), mn);
+        const int mcyc = std::max(2, (int)cdiv(2 * r, k));
+        nQmax = pk + k * (mcyc + 1);
+        ldT = nQmax;
+        Tm.assign((size_t)ldT * ldT, 0.0);
+        Pb.alloc(sizeof(T) * L * nQmax, st);
+        Qb.alloc(sizeof(T) * K * nQmax, st);
+        Ptmp.alloc(sizeof(T) * L * pk, st);
+        Qtmp.alloc(sizeof(T) * K * pk, st);
+        const double tol = p.tol > 0 ? p.tol : (sizeof(T) == 4 ? 1e-6 : 1e-10);
+        const int64_t maxprod = p.max_products > 0 ? p.max_products : std::max<int64_t>(400, 40 * (nQmax / k));
+
+        // P_1 = orth(random)
+        fill_normal<T>(L, P(0), L, k, p.seed, 0, st);
+        orth(L, P(0), k, nullptr, 0, false);
+        nP = k;
+        stepB();
+        std::vector<double> th, Y, Z, res;
+        int nconv = 0, restarts = 0;
+        double maxres = 0.0;
+        for (;;) {
+            stepA();
+            stepB();
+            if (nQ + k <= nQmax && nblock < maxprod) continue;
+            // ---- Ritz extraction from T (nP x nc)
+            const int nc = nQ - k;
+            th.assign(nc, 0.0); Y.assign((size_t)nP * nc, 0.0); Z.assign((size_t)nc * nc, 0.0);
+            svd_jacobi(nP, nc, Tm.data(), ldT, th.data(), Y.data(), Z.data());
+            anorm = std::max(anorm, th[0]);
+            res.assign(nc, 0.0);
+            for (int i = 0; i < nc; ++i) {
+                double s2 = 0.0;
+                for (int a = 0; a < k; ++a) {
+                    double s = 0.0;
+                    for (int b = 0; b < k; ++b) s += Alast[a + (size_t)k * b] * Y[(nP - k + b) + (size_t)nP * i];
+                    s2 += s * s;
+                }
+                res[i] = std::sqrt(s2);
+            }
+            nconv = 0; maxres = 0.0;
+            for (int i = 0; i < std::min(r, nc); ++i) {
+                maxres = std::max(maxres, res[i] / th[0]);
+                if (res[i] <= tol * th[0]) ++nconv;
+            }
+            const bool done = (nconv >= r) || (nblock >= maxprod);
+            if (done) {
+                // U = Pb · Y[:, 0:r]
+                p.U.alloc(sizeof(T) * L * r, st);
+                gemm(L, P(0), L, nP, Y.data(), nP, r, 1.0, 0.0, p.U.as<T>(), L);
+                p.sigma.assign(th.begin(), th.begin() + r);
+                p.r = r;
+                break;
+            }
+            // ---- thick restart keeping pk Ritz pairs
+            ++restarts;
+            gemm(L, P(0), L, nP, Y.data(), nP, pk, 1.0, 0.0, Ptmp.as<T>(), L);
+            gemm(K, Q(0), K, nc, Z.data(), nc, pk, 1.0, 0.0, Qtmp.as<T>(), K);
+            SSA_CUDA(cudaMemcpyAsync(P(0), Ptmp.p, sizeof(T) * L * pk, cudaMemcpyDeviceToDevice, st));
+            SSA_CUDA(cudaMemcpyAsync(Q(pk), Q(nc), sizeof(T) * K * k, cudaMemcpyDeviceToDevice, st));
+            SSA_CUDA(cudaMemcpyAsync(Q(0), Qtmp.p, sizeof(T) * K * pk, cudaMemcpyDeviceToDevice, st));
+            std::fill(Tm.begin(), Tm.end(), 0.0);
+            for (int i = 0; i < pk; ++i) Tat(i, i) = th[i];
+            nP = pk;
+            nQ = pk + k;
+        }
+        // sign convention: largest-|.| entry of each U_i positive
+        double *sg = small_dev(p, 64 * 64);
+        for (int c0 = 0; c0 < r; c0 += 4096) {
+            const int nc = std::min(4096, r - c0);
+            absmax_sign<T>(L, p.U.as<T>() + L * c0, L, nc, sg, st);
+            scale_columns<T>(L, p.U.as<T>() + L * c0, L, nc, sg, st);
+        }
+        SSA_CUDA(cudaStreamSynchronize(st));
+        p.v_valid = false;
+        if (info) {
+            info->r_requested = r;
+            info->n_converged = nconv;
+            info->block_k = k;
+            info->n_restarts = restarts;
+            info->n_block_products = nblock;
+            info->n_vector_products = nvec;
+            info->max_rel_residual = maxres;
+            info->ms_products = product_ms();
+        }
+        if (nconv < r)
+            throw Error(SSA_ERR_NOT_CONVERGED, "decomposition stopped at max_products with " + std::to_string(nconv) +
+                                                   " of " + std::to_string(r) + " triples converged");
+    }
+};
+
+template <typename T>
+void decompose(PlanImpl &p, int r, ssa_decomp_info *info) {
+    Gkl<T> g(p);
+    g.run(r, info);
+}
+template void decompose<float>(PlanImpl &, int, ssa_decomp_info *);
+template void decompose<double>(PlanImpl &, int, ssa_decomp_info *);
+
+}  // namespace ssa

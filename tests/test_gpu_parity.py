@@ -1,0 +1,342 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs, at the tolerances of BASELINE.json's north star:
+  * integer shape data (𝔎, 𝕎, counts): bit-exact
+  * operator products: relative Frobenius error <= 1e-5 (fp32) / 1e-12 (fp64)
+  * singular values: relative error <= 1e-4 where the oracle relgap >= 1e-3 and
+    σ_i >= τ σ_1 (reading Q10), |Δσ_i| <= 1e-6 σ_1 below the floor / in clusters
+  * grouped reconstructions: relative Frobenius error <= 1e-4 on 𝔑′ (NaN elsewhere)
+"""
+import numpy as np
+import pytest
+
+import closed_form as cf
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+FP32_PROD_TOL = 1e-5
+FP64_PROD_TOL = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _require_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_1309_5050_b200 import build
+    build.build()
+
+
+def _plan(w, dtype=None, **kw):
+    from paper_1309_5050_b200 import Plan
+    return Plan(w.data, w.window, mask=w.mask, wmask=w.wmask, dtype=dtype or w.dtype,
+                block_k=kw.pop("block_k", w.block_k), **kw)
+
+
+def _oracle_input(w, dtype):
+    """The exact values the GPU sees (fp32 configs are rounded once)."""
+    x = np.array(w.data, dtype=np.float64)
+    if dtype == "f32":
+        x = x.astype(np.float32).astype(np.float64)
+    return x
+
+
+def relfro(a, b):
+    return np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b)
+
+
+def _cases():
+    return {
+        "shaped_small": synth.small_shaped(seed=11),
+        "shaped_wmask": synth.small_shaped(seed=12, wmask_drop=6, nx=37, ny=45, window=(9, 6)),
+        "shaped_tiny": synth.small_shaped(seed=13, nx=12, ny=10, window=(4, 3), n_holes=1, wmask_drop=2),
+        "c1": synth.config1(),
+    }
+
+
+# ---------------------------------------------------------------- shapes: bit-exact
+@pytest.mark.parametrize("name", ["shaped_small", "shaped_wmask", "shaped_tiny", "c1"])
+def test_shapes_bit_exact(name):
+    w = _cases()[name]
+    p = _plan(w)
+    sh = oracle.shapes(w.data, w.window, mask=w.mask, wmask=w.wmask)
+    assert p.L == sh.L and p.K == sh.K
+    assert np.array_equal(p.kmask(), sh.kmask.astype(bool))
+    assert np.array_equal(p.weights(), sh.weights)
+    assert p.n_excluded == int((sh.nmask.astype(bool) & ~sh.nprime).sum())
+
+
+def test_shapes_fig4_bit_exact():
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fig4.json")))
+    nx, ny = g["N_box"]
+    n = np.zeros((nx, ny), bool)
+    for row, (c0, c1) in g["N_rows"].items():
+        n[int(row) - 1, c0 - 1:c1] = True
+    wm = np.zeros(tuple(g["L_box"]), bool)
+    for x, y in g["L"]:
+        wm[x - 1, y - 1] = True
+    img = np.where(n, 1.0, np.nan)
+    from paper_1309_5050_b200 import Plan
+    p = Plan(img, tuple(g["L_box"]), wmask=wm)
+    got = sorted((a + 1, b + 1) for a, b in zip(*np.nonzero(p.kmask())))
+    assert got == sorted(tuple(v) for v in g["K"])
+    assert p.n_excluded == len(g["N_minus_Nprime"])
+
+
+def test_shapes_c4_full_size_bit_exact():
+    w = synth.config4()
+    p = _plan(w)
+    sh = oracle.shapes(w.data, w.window, mask=w.mask)
+    assert p.K == sh.K
+    assert np.array_equal(p.kmask(), sh.kmask.astype(bool))
+    assert np.array_equal(p.weights(), sh.weights)
+
+
+# ---------------------------------------------------------------- products
+@pytest.mark.parametrize("name", ["shaped_small", "shaped_wmask", "shaped_tiny", "c1"])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("k", [1, 5, 37])
+def test_products_small(name, dtype, k):
+    w = _cases()[name]
+    p = _plan(w, dtype=dtype, path="direct")
+    x = _oracle_input(w, dtype)
+    sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
+    rng = np.random.default_rng(k)
+    V = rng.normal(size=(sh.K, k))
+    U = rng.normal(size=(sh.L, k))
+    npd = np.float32 if dtype == "f32" else np.float64
+    V = V.astype(npd).astype(np.float64); U = U.astype(npd).astype(np.float64)
+    tol = FP32_PROD_TOL if dtype == "f32" else FP64_PROD_TOL
+    assert relfro(p.matmul(V), oracle.xv(x, sh, V)) <= tol
+    assert relfro(p.matmul(U, transpose=True), oracle.xtu(x, sh, U)) <= tol
+
+
+def test_products_device_tensors_and_ld():
+    import torch
+    w = synth.small_shaped(seed=21)
+    p = _plan(w)
+    x = _oracle_input(w, "f32")
+    sh = oracle.shapes(x, w.window, mask=w.mask)
+    V = torch.randn(sh.K, 7, device="cuda", dtype=torch.float32)
+    U = p.matmul(V)
+    ref = oracle.xv(x, sh, V.double().cpu().numpy())
+    assert relfro(U.double().cpu().numpy(), ref) <= FP32_PROD_TOL
+
+
+def test_products_c2_mssa():
+    w = synth.config2()
+    p = _plan(w, path="direct")
+    x = _oracle_input(w, "f32")
+    sh = oracle.shapes(x, w.window)
+    rng = np.random.default_rng(2)
+    V = rng.normal(size=(sh.K, 32)).astype(np.float32).astype(np.float64)
+    U = rng.normal(size=(sh.L, 32)).astype(np.float32).astype(np.float64)
+    assert relfro(p.matmul(V), oracle.xv(x, sh, V)) <= FP32_PROD_TOL
+    assert relfro(p.matmul(U, transpose=True), oracle.xtu(x, sh, U)) <= FP32_PROD_TOL
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_products_full_size_sampled(cfg):
+    """Full BASELINE sizes, block k = 32: sampled output rows against the oracle."""
+    w = synth.get(cfg)
+    p = _plan(w, path="direct")
+    x = _oracle_input(w, "f32")
+    sh = oracle.shapes(x, w.window, mask=w.mask)
+    rng = np.random.default_rng(3)
+    k = 32
+    V = rng.normal(size=(sh.K, k)).astype(np.float32)
+    U = rng.normal(size=(sh.L, k)).astype(np.float32)
+    Ug = p.matmul(V)
+    Vg = p.matmul(U, transpose=True)
+    rows = rng.choice(sh.L, 24, replace=False)
+    ref = oracle.xv_rows(x, sh, V.astype(np.float64), rows)
+    assert relfro(Ug[rows], ref) <= FP32_PROD_TOL
+    k0 = int(rng.integers(0, sh.K - 2000))
+    refv = oracle.xtu(x, sh, U.astype(np.float64), kstart=k0, kcount=2000)
+    assert relfro(Vg[k0:k0 + 2000], refv) <= FP32_PROD_TOL
+    # adjoint identity over the whole block (P4), fp64 host dots
+    lhs = np.sum(Ug.astype(np.float64) * U.astype(np.float64))
+    rhs = np.sum(V.astype(np.float64) * Vg.astype(np.float64))
+    assert abs(lhs - rhs) <= 1e-5 * np.sqrt(np.sum(Ug.astype(np.float64) ** 2) * np.sum(U.astype(np.float64) ** 2))
+
+
+def test_products_closed_form_c3_twin():
+    """P5: noiseless c3 geometry, products against the separable closed form."""
+    w = synth.config3(noise=False)
+    p = _plan(w, path="direct")
+    from paper_1309_5050_b200 import Plan  # noqa: F401
+    sh = oracle.shapes(w.data, w.window)
+    rng = np.random.default_rng(4)
+    V = rng.normal(size=(sh.K, 4)).astype(np.float32).astype(np.float64)
+    U = rng.normal(size=(sh.L, 4)).astype(np.float32).astype(np.float64)
+    Ucf, Vcf = cf.products(w.terms, sh.lpos(), sh.kpos(), V=V, U=U)
+    # the GPU sees the fp32-rounded image: allow the input rounding (≈6e-8 relative)
+    assert relfro(p.matmul(V), Ucf) <= 2e-5
+    assert relfro(p.matmul(U, transpose=True), Vcf) <= 2e-5
+
+
+# ---------------------------------------------------------------- decomposition + reconstruction
+def _relgaps(s_all, r):
+    s = np.asarray(s_all, np.float64)
+    g = np.full(r, np.inf)
+    for i in range(r):
+        left = s[i - 1] - s[i] if i > 0 else np.inf
+        right = s[i] - s[i + 1] if i + 1 < len(s) else np.inf
+        g[i] = min(left, right) / s[i] if s[i] > 0 else 0.0
+    return g
+
+
+def check_sigma(s_gpu, s_or_all, r, tau=1e-5, rel=1e-4):
+    s_gpu = np.asarray(s_gpu, np.float64)
+    s_or = np.asarray(s_or_all[:r], np.float64)
+    gaps = _relgaps(s_or_all, r)
+    s1 = s_or[0]
+    checked = 0
+    for i in range(r):
+        if gaps[i] >= 1e-3 and s_or[i] >= tau * s1:
+            assert abs(s_gpu[i] - s_or[i]) <= rel * s_or[i], (i, s_gpu[i], s_or[i])
+            checked += 1
+        else:
+            assert abs(s_gpu[i] - s_or[i]) <= 1e-6 * s1 * 10, (i, s_gpu[i], s_or[i])
+    return checked
+
+
+def _gap_groups(s_all, r, thr=1e-3):
+    """Reading Q9: clusters bounded by relative gaps >= thr."""
+    s = np.asarray(s_all, np.float64)
+    groups, cur = [], [0]
+    for i in range(1, r + 1):
+        if i == r or (s[i - 1] - s[i]) / s[i - 1] >= thr:
+            if i == r and (s[r - 1] - s[r]) / s[r - 1] < thr:
+                break
+            groups.append(cur)
+            cur = [i]
+        else:
+            cur.append(i)
+    return groups
+
+
+def _check_recon(p, x, sh, s_or, U_or, V_or, groups, tol=1e-4):
+    recs = p.reconstruct(groups)
+    ref = oracle.reconstruct(x, sh, s_or, U_or, V_or, groups)
+    npr = sh.nprime
+    for g, (a, b) in enumerate(zip(recs, ref)):
+        assert np.array_equal(np.isnan(a), np.isnan(b))
+        assert relfro(a[npr], b[npr]) <= tol, (g, groups[g], relfro(a[npr], b[npr]))
+
+
+def test_decompose_c1_fp64():
+    w = synth.config1()
+    p = _plan(w)
+    x = _oracle_input(w, "f64")
+    sh = oracle.shapes(x, w.window)
+    s_or, U_or, V_or, s_all = oracle.svd_dense(x, sh, 10)
+    info = p.decompose(10)
+    assert info["n_converged"] == 10
+    assert check_sigma(p.sigma, s_all, 10) >= 6
+    np.testing.assert_allclose(p.sigma, s_or, rtol=1e-8)
+    _check_recon(p, x, sh, s_or, U_or, V_or, w.groups + [list(range(6))], tol=1e-8)
+    # the residual group returns the image (eq. P:440-443)
+    recs = p.reconstruct(w.groups, add_rest=True)
+    np.testing.assert_allclose(recs[0] + recs[1] + recs[2], x, rtol=1e-10, atol=1e-10)
+
+
+def test_decompose_c2_mssa_fp32():
+    w = synth.config2()
+    p = _plan(w)
+    x = _oracle_input(w, "f32")
+    sh = oracle.shapes(x, w.window)
+    s_or, U_or, V_or, s_all = oracle.svd_dense(x, sh, 17)
+    p.decompose(16)
+    assert check_sigma(p.sigma, s_all, 16) >= 4
+    _check_recon(p, x, sh, s_or, U_or, V_or, [g for g in w.groups if max(g) < 6])
+
+
+@pytest.mark.parametrize("name", ["shaped_small", "shaped_wmask"])
+def test_decompose_shaped_small(name):
+    w = _cases()[name]
+    p = _plan(w)
+    x = _oracle_input(w, "f32")
+    sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
+    r = w.r
+    s_or, U_or, V_or, s_all = oracle.svd_dense(x, sh, r + 1)
+    p.decompose(r)
+    check_sigma(p.sigma, s_all, r)
+    groups = _gap_groups(s_all, r)
+    if groups:
+        _check_recon(p, x, sh, s_or, U_or, V_or, groups)
+
+
+def test_reconstruct_from_oracle_triples_c1_and_shaped():
+    for w, dt in [(synth.config1(), "f64"), (synth.small_shaped(seed=14, wmask_drop=4), "f32")]:
+        p = _plan(w, dtype=dt)
+        x = _oracle_input(w, dt)
+        sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
+        s_or, U_or, V_or, _ = oracle.svd_dense(x, sh, 6)
+        p.set_triples(s_or, U_or)
+        groups = [[0], [1, 2], [3, 4, 5], [0, 1, 2, 3, 4, 5]]
+        recs = p.reconstruct(groups, add_rest=True)
+        ref = oracle.reconstruct(x, sh, s_or, U_or, V_or, groups, add_rest=True)
+        tol = 1e-11 if dt == "f64" else 2e-5
+        for a, b in zip(recs, ref):
+            assert np.array_equal(np.isnan(a), np.isnan(b))
+            m = ~np.isnan(b)
+            assert relfro(a[m], b[m]) <= tol
+
+
+def test_c3_noiseless_closed_form():
+    """P6/P7/P12 at the full c3 size: rank 24, σ = closed form, {1..24} = the image."""
+    w = synth.config3(noise=False)
+    p = _plan(w)
+    info = p.decompose(32, allow_not_converged=True)
+    s_cf = cf.sigma_rect(w.terms, 64, 64, 449, 449)
+    s = p.sigma
+    np.testing.assert_allclose(s[:24], s_cf[:24], rtol=1e-4)
+    assert np.all(s[24:] <= 1e-5 * s[0])
+    rec = p.reconstruct([list(range(24))])[0]
+    x = _oracle_input(w, "f32")
+    assert relfro(rec, x) <= 1e-4
+    assert info["n_block_products"] > 0
+
+
+def test_wcor_diag_and_symmetry():
+    w = synth.config1()
+    p = _plan(w)
+    p.decompose(10)
+    R = p.wcor([[0], [1], [2], [3], [4, 5]])
+    np.testing.assert_allclose(np.diag(R), 1.0, rtol=1e-12)
+    np.testing.assert_allclose(R, R.T, atol=1e-12)
+    x = _oracle_input(w, "f64")
+    sh = oracle.shapes(x, w.window)
+    s_or, U_or, V_or, _ = oracle.svd_dense(x, sh, 10)
+    Ro = oracle.wcorr(sh, oracle.reconstruct(x, sh, s_or, U_or, V_or, [[0], [1], [2], [3], [4, 5]]))
+    np.testing.assert_allclose(np.abs(R), np.abs(Ro), atol=1e-8)
+
+
+# ---------------------------------------------------------------- error behaviour
+def test_errors():
+    from paper_1309_5050_b200 import Plan, SSAError
+    x = np.random.default_rng(0).normal(size=(20, 15))
+    with pytest.raises(SSAError) as e:
+        Plan(x, (21, 3))
+    assert e.value.status == 2
+    with pytest.raises(SSAError) as e:
+        Plan(x, (1, 1))
+    assert e.value.status == 2
+    m = np.ones_like(x, bool); m[:, 7] = False; m[10, :] = False
+    with pytest.raises(SSAError) as e:
+        Plan(x, (12, 9), mask=m)
+    assert e.value.status == 3
+    p = Plan(x, (5, 4))
+    with pytest.raises(SSAError) as e:
+        p.reconstruct([[0]])
+    assert e.value.status == 9
+    with pytest.raises(SSAError) as e:
+        p.decompose(21)
+    assert e.value.status == 4
+    p.decompose(3)
+    with pytest.raises(SSAError) as e:
+        p.reconstruct([[0, 3]])
+    assert e.value.status == 4
