@@ -81,7 +81,7 @@ class ClockSampler:
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and "Active" in s[2 + i]})
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "n_samples": len(self.samples)}
 
@@ -112,14 +112,23 @@ def run_ours(args, rank, world, dist):
     mask_np = None if w.mask is None else np.asarray(w.mask)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
+    phases = []
+
     def step(host=False):
         with torch.cuda.stream(stream):
+            t0 = time.perf_counter()
             src = np.asarray(w.data) if host else img_dev
             p = Plan(src, w.window, mask=mask_np, wmask=w.wmask, dtype=w.dtype, block_k=w.block_k,
                      path=args.path, stream=stream.cuda_stream)
+            t1 = time.perf_counter()
             info = p.decompose(w.r, allow_not_converged=True)
+            t2 = time.perf_counter()
             recs = p.reconstruct(groups, add_rest=False, device=not host)
+            t3 = time.perf_counter()
             p.close()
+            t4 = time.perf_counter()
+        phases.append({"plan_ms": (t1 - t0) * 1e3, "decompose_ms": (t2 - t1) * 1e3,
+                       "reconstruct_ms": (t3 - t2) * 1e3, "destroy_ms": (t4 - t3) * 1e3})
         return info, recs, p
 
     # warm-up (also compiles nothing: the library is AOT-built)
@@ -132,6 +141,7 @@ def run_ours(args, rank, world, dist):
     torch.cuda.synchronize()
     times, infos = [], []
     launches0 = launch_count(reset=True)
+    phases.clear()
     with ClockSampler(dev.index) as clk:
         for _ in range(args.steps):
             flush.fill_(1)                         # flush L2 between timed iterations
@@ -144,6 +154,7 @@ def run_ours(args, rank, world, dist):
             times.append(e0.elapsed_time(e1))
             infos.append(info)
     launches = launch_count(reset=True)
+    timed_phases = {k: float(np.mean([ph[k] for ph in phases])) for k in phases[0]} if phases else {}
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -198,7 +209,9 @@ def run_ours(args, rank, world, dist):
                           "n_vector_products": infos[-1]["n_vector_products"],
                           "n_restarts": infos[-1]["n_restarts"], "n_converged": infos[-1]["n_converged"],
                           "max_rel_residual": infos[-1]["max_rel_residual"],
-                          "ms_products_per_step": ms_prod / args.steps},
+                          "ms_products_per_step": ms_prod / args.steps,
+                          "ms_ritz_per_step": float(np.sum([i["ms_ritz"] for i in infos])) / args.steps,
+                          "host_phases_ms": timed_phases},
         "e2e": {"value": e2e_value, "unit": "vector products/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": float(np.mean(e2e_times))},
         "gpu_launches": int(launches),

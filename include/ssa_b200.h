@@ -123,6 +123,7 @@ typedef struct {
     int64_t n_vector_products;        /* vectors pushed through the operator */
     double max_rel_residual;          /* max_i ||Xᵀu_i - σ_i v_i|| / σ_1 over i < r */
     double ms_products, ms_total;     /* device time in products; wall time of the call */
+    double ms_ritz;                   /* host time in the projected (Ritz) SVDs */
 } ssa_decomp_info;
 
 typedef struct ssa_plan_s *ssa_plan;
@@ -182,6 +183,13 @@ ssa_status ssa_reconstruct(ssa_plan p, const int32_t *grp_off, const int32_t *gr
  * rho (n_groups x n_groups, column-major double) = (X̃_a, X̃_b)_w / (‖X̃_a‖_w ‖X̃_b‖_w). */
 ssa_status ssa_wcor(ssa_plan p, const int32_t *grp_off, const int32_t *grp_idx,
                     int32_t n_groups, double *rho);
+
+/* The solver's projected-matrix SVD as a utility: one-sided
+ * Jacobi in fp64 on the device, one CTA, for m >= n and m*n*8 bytes <= ~220 KB
+ * (n <= 192).  A (host, m x n column-major) is overwritten with A·J whose
+ * columns are σ_j·y_j (unsorted); sweeps and device milliseconds are returned
+ * when the pointers are non-NULL.  SSA_ERR_ARG if the matrix does not fit. */
+ssa_status ssa_small_svd(int32_t m, int32_t n, double *A, int32_t *sweeps, double *ms);
 
 const char *ssa_last_error(void);
 const char *ssa_version(void);

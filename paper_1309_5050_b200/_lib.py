@@ -50,13 +50,14 @@ class ssa_plan_info_t(C.Structure):
 class ssa_decomp_info(C.Structure):
     _fields_ = [("r_requested", C.c_int32), ("n_converged", C.c_int32), ("block_k", C.c_int32),
                 ("n_restarts", C.c_int32), ("n_block_products", C.c_int64), ("n_vector_products", C.c_int64),
-                ("max_rel_residual", C.c_double), ("ms_products", C.c_double), ("ms_total", C.c_double)]
+                ("max_rel_residual", C.c_double), ("ms_products", C.c_double), ("ms_total", C.c_double),
+                ("ms_ritz", C.c_double)]
 
 
 EXPORTS = ["ssa_plan_create", "ssa_plan_destroy", "ssa_plan_info", "ssa_get_weights", "ssa_get_kmask",
            "ssa_matmul", "ssa_decompose", "ssa_get_rank", "ssa_get_sigma", "ssa_get_u", "ssa_get_v",
            "ssa_set_triples", "ssa_reconstruct", "ssa_wcor", "ssa_last_error", "ssa_version",
-           "ssa_launch_count"]
+           "ssa_launch_count", "ssa_small_svd"]
 
 _lib = None
 
@@ -96,6 +97,8 @@ def load(path: str = SO_PATH):
     L.ssa_last_error.argtypes = []; L.ssa_last_error.restype = C.c_char_p
     L.ssa_version.argtypes = []; L.ssa_version.restype = C.c_char_p
     L.ssa_launch_count.argtypes = [C.c_int]; L.ssa_launch_count.restype = i64
+    L.ssa_small_svd.argtypes = [i32, i32, p, C.POINTER(i32), C.POINTER(C.c_double)]
+    L.ssa_small_svd.restype = st
     _lib = L
     return L
 

@@ -17,6 +17,7 @@ static thread_local std::string g_err;
 static thread_local int64_t g_launches = 0;
 
 void count_launch(int n) { g_launches += n; }
+void ssa_set_error(const std::string &msg) { g_err = msg; }
 void after_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw Error(SSA_ERR_CUDA, std::string("launch of ") + what + ": " + cudaGetErrorString(e));

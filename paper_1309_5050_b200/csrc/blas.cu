@@ -71,14 +71,18 @@ gram_tn_kernel(int64_t M, const T *__restrict__ A, int64_t lda, int n1,
         for (int b = 0; b < 4; ++b) out[(4 * ti + a) + 64 * (4 * tj + b)] = accd[a][b];
 }
 
+// One warp per Gram entry: lanes sum strided partials, then a fixed shuffle tree
+// (deterministic order).
 __global__ void gram_reduce_kernel(const double *__restrict__ partials, int nparts, int n1, int n2,
                                    double *__restrict__ G) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (e >= n1 * n2) return;
     const int a = e % n1, b = e / n1;
     double s = 0.0;
-    for (int q = 0; q < nparts; ++q) s += partials[(int64_t)q * 4096 + a + 64 * b];
-    G[a + (int64_t)n1 * b] = s;
+    for (int q = lane; q < nparts; q += 32) s += partials[(int64_t)q * 4096 + a + 64 * b];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) G[a + (int64_t)n1 * b] = s;
 }
 
 static int gram_ctas(int64_t M) {
@@ -95,7 +99,7 @@ void gram_tn(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb
     SSA_REQUIRE((size_t)ctas * 4096 * sizeof(double) <= partial_bytes, SSA_ERR_ARG, "gram_tn: workspace");
     gram_tn_kernel<T><<<ctas, 256, 0, st>>>(M, A, lda, n1, B, ldb, n2, partials);
     after_launch("gram_tn");
-    gram_reduce_kernel<<<(unsigned)cdiv(n1 * n2, 256), 256, 0, st>>>(partials, ctas, n1, n2, G);
+    gram_reduce_kernel<<<(unsigned)cdiv((int64_t)n1 * n2 * 32, 256), 256, 0, st>>>(partials, ctas, n1, n2, G);
     after_launch("gram_reduce");
 }
 template void gram_tn<float>(int64_t, const float *, int64_t, int, const float *, int64_t, int, double *,
@@ -108,7 +112,7 @@ template void gram_tn<double>(int64_t, const double *, int64_t, int, const doubl
 template <typename T>
 __global__ void __launch_bounds__(128)
 gemm_small_kernel(int64_t M, const T *A, int64_t lda, int m, const double *__restrict__ C, int ldc,
-                  int n, double alpha, double beta, T *Out, int64_t ldo) {
+                  int n, double alpha, double beta, T *Out, int64_t ldo, bool inplace) {
     __shared__ T CS[64 * 64];
     for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
         const int a = idx % m, b = idx / m;
@@ -120,7 +124,9 @@ gemm_small_kernel(int64_t M, const T *A, int64_t lda, int m, const double *__res
     T a[64];
 #pragma unroll
     for (int c = 0; c < 64; ++c) a[c] = (c < m) ? A[row + lda * c] : T(0);
-    for (int b0 = 0; b0 < n; b0 += 16) {
+    // in-place (Out == A) needs one CTA column to own all outputs of its rows
+    const int bstep = inplace ? 16 : 16 * gridDim.y;
+    for (int b0 = inplace ? 0 : 16 * blockIdx.y; b0 < n; b0 += bstep) {
         T acc[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = T(0);
@@ -147,7 +153,11 @@ void gemm_small(int64_t M, const T *A, int64_t lda, int m, const double *C, int 
                 double alpha, double beta, T *Out, int64_t ldo, cudaStream_t st) {
     SSA_REQUIRE(m <= 64 && n <= 64, SSA_ERR_ARG, "gemm_small: at most 64x64");
     if (M <= 0 || n <= 0) return;
-    gemm_small_kernel<T><<<(unsigned)cdiv(M, 128), 128, 0, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
+    const bool inplace = (Out == A);
+    // small M: spread the column chunks over more CTAs (not in place)
+    const int gy = inplace ? 1 : (int)std::min<int64_t>(cdiv(n, 16), std::max<int64_t>(1, (2 * num_sms()) / cdiv(M, 128)));
+    dim3 grid((unsigned)cdiv(M, 128), gy);
+    gemm_small_kernel<T><<<grid, 128, 0, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo, inplace);
     after_launch("gemm_small");
 }
 template void gemm_small<float>(int64_t, const float *, int64_t, int, const double *, int, int, double,

@@ -68,5 +68,7 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 
 int num_sms();
+// set the thread-local message returned by ssa_last_error()
+void ssa_set_error(const std::string &msg);
 
 }  // namespace ssa

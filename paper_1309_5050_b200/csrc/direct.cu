@@ -51,8 +51,11 @@ corr_direct_kernel(CorrParams<T> P) {
     const int oy0 = (blockIdx.x / ntx) * TY;
     const int j0 = blockIdx.y * KV;
     const int split = blockIdx.z;
-    const int dy_lo = split * P.dy_split;
+    const int zx = split % P.nsx, zy = split / P.nsx;   // split-K over both reduction axes
+    const int dy_lo = zy * P.dy_split;
     const int dy_hi = min(P.dy, dy_lo + P.dy_split);
+    const int dx_lo = zx * P.dx_split;
+    const int dx_hi = min(P.dx, dx_lo + P.dx_split);
 
     const int tid = threadIdx.x;
     const int jg = tid % kJG;
@@ -67,7 +70,7 @@ corr_direct_kernel(CorrParams<T> P) {
         for (int j = 0; j < TN; ++j) acc[t][j] = T(0);
 
     for (int dy0 = dy_lo; dy0 < dy_hi; dy0 += CDY) {
-        for (int dx0 = 0; dx0 < P.dx; dx0 += CDX) {
+        for (int dx0 = dx_lo; dx0 < dx_hi; dx0 += CDX) {
             __syncthreads();
             // ---- stage the image tile: rows ox0+dx0 .. +XW, cols oy0+dy0 .. +YT
             for (int idx = tid; idx < XW * YT; idx += kThreads) {
@@ -84,7 +87,7 @@ corr_direct_kernel(CorrParams<T> P) {
                 const int gdx = dx0 + dxl, gdy = dy0 + dyl;
                 const int jj = j0 + jl;
                 T v = T(0);
-                if (gdx < P.dx && gdy < dy_hi && jj < P.k) {
+                if (gdx < dx_hi && gdy < dy_hi && jj < P.k) {
                     const int64_t box = gdx + (int64_t)P.dx * gdy;
                     const int64_t wi = P.wmap ? (int64_t)P.wmap[box] : box;
                     if (wi >= 0) v = P.W[wi + P.ldw * (int64_t)jj];
@@ -196,18 +199,30 @@ void corr_direct(CorrParams<T> P, T *ws_buf, size_t ws_bytes, cudaStream_t st) {
     if (P.k <= 0 || P.ox <= 0 || P.oy <= 0) return;
     P.px = choose_px(P.ox, P.oy, TM);
     const bool flat = (P.dy == 1);            // 1-row reduction box (MSSA X^T U): CDY = 1
-    const int cdy = flat ? 1 : 4;
+    const int cdy = flat ? 1 : 4, cdx = flat ? 128 : 32;
     const int PY = kPT / P.px;
     const int64_t tiles = cdiv(P.ox, TM * P.px) * cdiv(P.oy, PY) * cdiv(P.k, KV);
-    // split the reduction along d.y until the grid fills ~3 waves of 2 CTAs/SM
+    // split the reduction (first along d.y, then along d.x) until the grid fills
+    // ~3 waves of 2 CTAs/SM, bounded by the partial-sum workspace
     const int64_t want = 3 * 2 * (int64_t)num_sms();
-    int64_t nsplit = 1;
-    if (tiles < want) nsplit = std::min<int64_t>(cdiv(want, tiles), cdiv(P.dy, cdy));
     const int64_t nbox = (int64_t)P.ox * P.oy;
-    // bound the partial-sum workspace
-    while (nsplit > 1 && (size_t)nsplit * P.k * nbox * sizeof(T) > ws_bytes) --nsplit;
-    P.dy_split = (int)rup(cdiv(P.dy, nsplit), cdy);
-    nsplit = cdiv(P.dy, P.dy_split);
+    const int64_t max_ws_splits = std::max<int64_t>(1, (int64_t)(ws_bytes / ((size_t)P.k * nbox * sizeof(T))));
+    int64_t need = tiles < want ? cdiv(want, tiles) : 1;
+    need = std::min(need, max_ws_splits);
+    int64_t nsy = std::min<int64_t>(need, cdiv(P.dy, cdy));
+    int64_t nsx = std::min<int64_t>(cdiv(need, nsy), cdiv(P.dx, cdx));
+    if (nsx < 1) nsx = 1;
+    P.dy_split = (int)rup(cdiv(P.dy, nsy), cdy);
+    nsy = cdiv(P.dy, P.dy_split);
+    P.dx_split = (int)rup(cdiv(P.dx, nsx), cdx);
+    nsx = cdiv(P.dx, P.dx_split);
+    while (nsx * nsy > max_ws_splits && nsx > 1) {   // workspace bound after rounding
+        --nsx;
+        P.dx_split = (int)rup(cdiv(P.dx, nsx), cdx);
+        nsx = cdiv(P.dx, P.dx_split);
+    }
+    const int64_t nsplit = nsx * nsy;
+    P.nsx = (int)nsx;
     P.nsplit = (int)nsplit;
     P.ws = ws_buf;
     if (flat) launch_corr<T, 128, 1>(P, st);

@@ -15,7 +15,7 @@ struct CorrParams {
     T *out; int64_t ldo; const int *omap;       // output, compact; omap: box -> compact or -1 (null = identity)
     int k;                                   // number of filters
     // filled by the launcher
-    T *ws; int nsplit; int dy_split; int px; int xpitch;
+    T *ws; int nsplit; int nsx; int dy_split; int dx_split; int px; int xpitch;
 };
 
 template <typename T>

@@ -17,6 +17,7 @@
 // SVQB (eigen-decomposition of the column-scaled Gram, Stathopoulos & Wu) run
 // twice; numerically dependent directions are replaced by seeded random ones
 // (or zeroed once the space is exhausted).  V is recomputed as XᵀU/σ.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -29,25 +30,75 @@
 
 namespace ssa {
 
+// Pinned host staging + matching device ring for the small matrices exchanged
+// with the host (Gram results, projection coefficients).  Regions are never
+// reused before a stream synchronisation, so uploads need no sync of their own.
+struct Staging {
+    double *h = nullptr;
+    DevBuf d;
+    size_t cap = 0, off = 0;
+    cudaStream_t st = nullptr;
+    void init(size_t n_doubles, cudaStream_t s) {
+        // one pinned block per thread, allocated once and kept for the process
+        // lifetime (pinned allocation is slow; plans are cheap to create)
+        static thread_local double *pinned = nullptr;
+        static thread_local size_t pinned_cap = 0;
+        if (pinned_cap < n_doubles) {
+            if (pinned) cudaFreeHost(pinned);
+            SSA_CUDA(cudaMallocHost(&pinned, sizeof(double) * n_doubles));
+            pinned_cap = n_doubles;
+        }
+        st = s;
+        cap = n_doubles;
+        h = pinned;
+        d.alloc(sizeof(double) * cap, st);
+    }
+    // reserve n doubles; returns the index (host h[idx], device d[idx])
+    size_t take(size_t n) {
+        n = (n + 31) & ~size_t(31);
+        if (off + n > cap) {
+            SSA_CUDA(cudaStreamSynchronize(st));
+            off = 0;
+        }
+        SSA_REQUIRE(n <= cap, SSA_ERR_ARG, "staging buffer too small");
+        const size_t i = off;
+        off += n;
+        return i;
+    }
+    double *dev(size_t i) { return d.as<double>() + i; }
+    void sync() {
+        SSA_CUDA(cudaStreamSynchronize(st));
+        off = 0;
+    }
+};
+
+void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st);
+bool jacobi_blocked_fits(int m, int n);
+
 template <typename T>
 struct Gkl {
     PlanImpl &p;
     cudaStream_t st;
     int64_t L, K;
     int k, r, pk, nQmax;
-    DevBuf Pb, Qb, Ptmp, Qtmp;
+    DevBuf Pb, Qb, Ptmp, Qtmp, Jd;
+    Staging sg;
     int nP = 0, nQ = 0;
     std::vector<double> Tm;   // nQmax x nQmax host, column-major
     int ldT;
     std::vector<double> Alast;
     double anorm = 0.0;
+    double ms_ritz = 0.0;
     int64_t nblock = 0, nvec = 0;
     uint64_t sid = 1;
-    double thr_abs, thr_rel;
+    double thr_abs, thr_rel, thr_chol;
+    bool gpu_ritz = true;
 
     explicit Gkl(PlanImpl &pl) : p(pl), st(pl.st), L(pl.L), K(pl.K) {
         thr_abs = (sizeof(T) == 4) ? 1e-6 : 1e-14;
         thr_rel = (sizeof(T) == 4) ? 1e-10 : 1e-26;
+        thr_chol = (sizeof(T) == 4) ? 1e-6 : 1e-13;
+        sg.init(1 << 18, st);
     }
 
     T *P(int col) { return Pb.as<T>() + (int64_t)col * L; }
@@ -55,48 +106,52 @@ struct Gkl {
 
     bool kside_comm() const { return p.has_comm && p.comm.world > 1; }
 
-    // G (n1 x n2, host, column-major ld n1) = Aᵀ B; chunked by 64 columns.
+    // G (n1 x n2, host, column-major ld n1) = Aᵀ B; chunked by 64 columns, one sync.
     void gram(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb, int n2, double *G, bool kside) {
-        double *Gd = small_dev(p, 64 * 64);
-        std::vector<double> h(64 * 64);
+        struct Chunk { int a0, na, b0, nb; size_t idx; };
+        std::vector<Chunk> ch;
         for (int a0 = 0; a0 < n1; a0 += 64) {
             const int na = std::min(64, n1 - a0);
             for (int b0 = 0; b0 < n2; b0 += 64) {
                 const int nb = std::min(64, n2 - b0);
-                gram_tn<T>(M, A + lda * a0, lda, na, B + ldb * b0, ldb, nb, Gd, p.ws_gram.as<double>(),
+                const size_t idx = sg.take((size_t)na * nb);
+                gram_tn<T>(M, A + lda * a0, lda, na, B + ldb * b0, ldb, nb, sg.dev(idx), p.ws_gram.as<double>(),
                            p.ws_gram.bytes, st);
                 if (kside && kside_comm()) {
-                    if (p.comm.allreduce_sum(p.comm.user, Gd, (int64_t)na * nb, SSA_F64, st) != 0)
+                    if (p.comm.allreduce_sum(p.comm.user, sg.dev(idx), (int64_t)na * nb, SSA_F64, st) != 0)
                         throw Error(SSA_ERR_COMM, "allreduce of a K-side Gram failed");
                 }
-                SSA_CUDA(cudaMemcpyAsync(h.data(), Gd, sizeof(double) * na * nb, cudaMemcpyDeviceToHost, st));
-                SSA_CUDA(cudaStreamSynchronize(st));
-                for (int b = 0; b < nb; ++b)
-                    for (int a = 0; a < na; ++a) G[(a0 + a) + (int64_t)n1 * (b0 + b)] = h[a + (int64_t)na * b];
+                SSA_CUDA(cudaMemcpyAsync(sg.h + idx, sg.dev(idx), sizeof(double) * na * nb, cudaMemcpyDeviceToHost, st));
+                ch.push_back({a0, na, b0, nb, idx});
             }
         }
+        SSA_CUDA(cudaStreamSynchronize(st));
+        for (const Chunk &c : ch)
+            for (int b = 0; b < c.nb; ++b)
+                for (int a = 0; a < c.na; ++a)
+                    G[(c.a0 + a) + (int64_t)n1 * (c.b0 + b)] = sg.h[c.idx + a + (size_t)c.na * b];
+        sg.off = 0;   // everything staged so far has been consumed
     }
 
-    // Out[:, 0:n] = beta*Out + alpha * A[:, 0:m] * C (C: m x n host, ld ldc)
+    // Out[:, 0:n] = beta*Out + alpha * A[:, 0:m] * C (C: m x n host, ld ldc); no sync.
     void gemm(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha, double beta,
               T *Out, int64_t ldo) {
-        double *Cd = small_dev(p, 64 * 64);
-        std::vector<double> h(64 * 64);
         for (int c0 = 0; c0 < n; c0 += 64) {
             const int nc = std::min(64, n - c0);
             for (int m0 = 0; m0 < m; m0 += 64) {
                 const int mc = std::min(64, m - m0);
+                const size_t idx = sg.take((size_t)64 * nc);
+                double *h = sg.h + idx;
                 for (int b = 0; b < nc; ++b)
                     for (int a = 0; a < mc; ++a) h[a + 64 * b] = C[(m0 + a) + (int64_t)ldc * (c0 + b)];
-                SSA_CUDA(cudaMemcpyAsync(Cd, h.data(), sizeof(double) * 64 * nc, cudaMemcpyHostToDevice, st));
-                gemm_small<T>(M, A + lda * m0, lda, mc, Cd, 64, nc, alpha, (m0 == 0) ? beta : 1.0, Out + ldo * c0, ldo, st);
-                // h is reused: make sure the copy has consumed it
-                SSA_CUDA(cudaStreamSynchronize(st));
+                SSA_CUDA(cudaMemcpyAsync(sg.dev(idx), h, sizeof(double) * 64 * nc, cudaMemcpyHostToDevice, st));
+                gemm_small<T>(M, A + lda * m0, lda, mc, sg.dev(idx), 64, nc, alpha, (m0 == 0) ? beta : 1.0,
+                              Out + ldo * c0, ldo, st);
             }
         }
     }
 
-    // W -= Bm * (Bmᵀ W); returns the coefficients if coef != null (nb x kc, accumulated)
+    // W -= Bm * (Bmᵀ W); accumulates the coefficients into coef (nb x kc) if given
     void cgs(int64_t M, T *W, int kc, const T *Bm, int nb, bool kside, double *coef) {
         if (nb <= 0) return;
         std::vector<double> C((size_t)nb * kc);
@@ -106,38 +161,75 @@ struct Gkl {
             for (size_t t = 0; t < C.size(); ++t) coef[t] += C[t];
     }
 
-    // Orthonormalise W (M x kc) against `against` (na columns) and internally.
-    // Returns B (kc x kc, column-major) with W_in ≈ against·(·) + W_out·B.
+    // Cholesky G = RᵀR (R upper, column-major); false if a pivot is tiny (relative).
+    bool cholesky(int n, const double *G, std::vector<double> &R) {
+        R.assign((size_t)n * n, 0.0);
+        double dmax = 0.0;
+        for (int j = 0; j < n; ++j) dmax = std::max(dmax, G[j + (size_t)n * j]);
+        if (!(dmax > 0.0)) return false;
+        for (int j = 0; j < n; ++j) {
+            double s = G[j + (size_t)n * j];
+            for (int t = 0; t < j; ++t) s -= R[t + (size_t)n * j] * R[t + (size_t)n * j];
+            if (!(s > thr_chol * dmax) || !(std::sqrt(s) > thr_abs * anorm)) return false;
+            const double rjj = std::sqrt(s);
+            R[j + (size_t)n * j] = rjj;
+            for (int i = j + 1; i < n; ++i) {
+                double v = G[j + (size_t)n * i];
+                for (int t = 0; t < j; ++t) v -= R[t + (size_t)n * j] * R[t + (size_t)n * i];
+                R[j + (size_t)n * i] = v / rjj;
+            }
+        }
+        return true;
+    }
+
+    // Orthonormalise W (M x kc) against `against` (na columns) and internally:
+    // CholeskyQR2, with an SVQB pass (column-scaled Gram eigen-decomposition) when
+    // the Gram is ill-conditioned; numerically dependent directions are replaced by
+    // seeded random ones (zeroed when the space is exhausted).  Returns B
+    // (kc x kc, column-major) with W_in ≈ against·(·) + W_out·B.
     std::vector<double> orth(int64_t M, T *W, int kc, const T *against, int na, bool kside) {
         std::vector<double> B((size_t)kc * kc, 0.0);
         for (int i = 0; i < kc; ++i) B[i + (size_t)kc * i] = 1.0;
         std::vector<double> G((size_t)kc * kc), Gh((size_t)kc * kc), E((size_t)kc * kc), lam(kc);
-        std::vector<double> S((size_t)kc * kc), Bp((size_t)kc * kc), Bn((size_t)kc * kc);
-        for (int pass = 0; pass < 4; ++pass) {
+        std::vector<double> S((size_t)kc * kc), Bp((size_t)kc * kc), Bn((size_t)kc * kc), R;
+        for (int pass = 0; pass < 5; ++pass) {
             if (na > 0) cgs(M, W, kc, against, na, kside, nullptr);
             gram(M, W, M, kc, W, M, kc, G.data(), kside);
-            std::vector<double> d(kc);
-            std::vector<char> good(kc);
-            for (int j = 0; j < kc; ++j) {
-                d[j] = std::sqrt(std::max(G[j + (size_t)kc * j], 0.0));
-                good[j] = d[j] > thr_abs * std::max(anorm, 1e-300) && d[j] > 0.0;
-            }
-            for (int b = 0; b < kc; ++b)
-                for (int a = 0; a < kc; ++a)
-                    Gh[a + (size_t)kc * b] = (good[a] && good[b]) ? G[a + (size_t)kc * b] / (d[a] * d[b])
-                                                                   : (a == b ? 0.0 : 0.0);
-            sym_eig(kc, Gh.data(), lam.data(), E.data());
             std::vector<int> bad;
-            for (int j = 0; j < kc; ++j) {
-                const bool ok = lam[j] > thr_rel;
-                const double isq = ok ? 1.0 / std::sqrt(lam[j]) : 0.0;
-                const double sq = ok ? std::sqrt(lam[j]) : 0.0;
-                for (int a = 0; a < kc; ++a) {
-                    const double dinv = good[a] ? 1.0 / d[a] : 0.0;
-                    S[a + (size_t)kc * j] = dinv * E[a + (size_t)kc * j] * isq;          // D⁻¹ E Λ^{-1/2}
-                    Bp[j + (size_t)kc * a] = sq * E[a + (size_t)kc * j] * (good[a] ? d[a] : 0.0);  // Λ^{1/2} Eᵀ D
+            if (cholesky(kc, G.data(), R)) {
+                // S = R⁻¹ (upper triangular inverse), Bp = R
+                std::fill(S.begin(), S.end(), 0.0);
+                for (int j = 0; j < kc; ++j) {
+                    S[j + (size_t)kc * j] = 1.0 / R[j + (size_t)kc * j];
+                    for (int i = j - 1; i >= 0; --i) {
+                        double v = 0.0;
+                        for (int t = i + 1; t <= j; ++t) v += R[i + (size_t)kc * t] * S[t + (size_t)kc * j];
+                        S[i + (size_t)kc * j] = -v / R[i + (size_t)kc * i];
+                    }
                 }
-                if (!ok) bad.push_back(j);
+                Bp = R;
+            } else {
+                std::vector<double> d(kc);
+                std::vector<char> good(kc);
+                for (int j = 0; j < kc; ++j) {
+                    d[j] = std::sqrt(std::max(G[j + (size_t)kc * j], 0.0));
+                    good[j] = d[j] > thr_abs * std::max(anorm, 1e-300) && d[j] > 0.0;
+                }
+                for (int b = 0; b < kc; ++b)
+                    for (int a = 0; a < kc; ++a)
+                        Gh[a + (size_t)kc * b] = (good[a] && good[b]) ? G[a + (size_t)kc * b] / (d[a] * d[b]) : 0.0;
+                sym_eig(kc, Gh.data(), lam.data(), E.data());
+                for (int j = 0; j < kc; ++j) {
+                    const bool ok = lam[j] > thr_rel;
+                    const double isq = ok ? 1.0 / std::sqrt(lam[j]) : 0.0;
+                    const double sq = ok ? std::sqrt(lam[j]) : 0.0;
+                    for (int a = 0; a < kc; ++a) {
+                        const double dinv = good[a] ? 1.0 / d[a] : 0.0;
+                        S[a + (size_t)kc * j] = dinv * E[a + (size_t)kc * j] * isq;                    // D⁻¹ E Λ^{-1/2}
+                        Bp[j + (size_t)kc * a] = sq * E[a + (size_t)kc * j] * (good[a] ? d[a] : 0.0);  // Λ^{1/2} Eᵀ D
+                    }
+                    if (!ok) bad.push_back(j);
+                }
             }
             gemm(M, W, M, kc, S.data(), kc, kc, 1.0, 0.0, W, M);   // in place (kc <= 64)
             for (int b = 0; b < kc; ++b)
@@ -151,7 +243,7 @@ struct Gkl {
                 if (pass >= 1) break;
                 continue;
             }
-            if (pass >= 2) break;   // space exhausted: those columns stay zero
+            if (pass >= 3) break;   // space exhausted: those columns stay zero
             for (int j : bad) fill_normal<T>(M, W + M * j, M, 1, p.seed, 0x5eed0000ull + (sid++), st);
         }
         return B;
@@ -227,13 +319,66 @@ struct Gkl {
         nQ += k;
     }
 
+    // SVD of T[0:m, 0:n] (m >= n): th (n), Y (m x n), Z (n x n), descending.
+    void ritz_svd(int m, int n, std::vector<double> &th, std::vector<double> &Y, std::vector<double> &Z) {
+        const auto t0 = std::chrono::steady_clock::now();
+        th.assign(n, 0.0); Y.assign((size_t)m * n, 0.0); Z.assign((size_t)n * n, 0.0);
+        bool done = false;
+        if (gpu_ritz && jacobi_blocked_fits(m, n)) {
+            Jd.alloc(sizeof(double) * ((size_t)m * n + 80), st);
+            double *Ad = Jd.as<double>();
+            const size_t ia = sg.take((size_t)m * n);
+            for (int j = 0; j < n; ++j)
+                std::memcpy(sg.h + ia + (size_t)m * j, &Tm[(size_t)ldT * j], sizeof(double) * m);
+            SSA_CUDA(cudaMemcpyAsync(Ad, sg.h + ia, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
+            jacobi_svd_blocked(m, n, Ad, reinterpret_cast<int *>(Ad + (size_t)m * n + 8), nullptr, st);
+            std::vector<double> A((size_t)m * n);
+            SSA_CUDA(cudaMemcpyAsync(A.data(), Ad, sizeof(double) * m * n, cudaMemcpyDeviceToHost, st));
+            sg.sync();
+            std::vector<double> nrm(n);
+            for (int j = 0; j < n; ++j) {
+                double t = 0; for (int i = 0; i < m; ++i) t += A[i + (size_t)m * j] * A[i + (size_t)m * j];
+                nrm[j] = std::sqrt(t);
+            }
+            std::vector<int> idx(n);
+            for (int j = 0; j < n; ++j) idx[j] = j;
+            std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return nrm[a] > nrm[b]; });
+            for (int j = 0; j < n; ++j) {
+                const int c = idx[j];
+                th[j] = nrm[c];
+                const double inv = nrm[c] > 0 ? 1.0 / nrm[c] : 0.0;
+                for (int i = 0; i < m; ++i) Y[i + (size_t)m * j] = A[i + (size_t)m * c] * inv;
+            }
+            // right vectors of the kept triples: z_j = Tᵀ y_j / σ_j (needs σ_j well above 0)
+            const int need = std::min(n, std::max(pk, r));
+            const double floor_rel = (sizeof(T) == 4) ? 1e-9 : 1e-13;
+            if (th[need - 1] > floor_rel * th[0]) {
+                for (int j = 0; j < need; ++j) {
+                    const double inv = 1.0 / th[j];
+                    for (int c = 0; c < n; ++c) {
+                        double s = 0.0;
+                        const double *tc = &Tm[(size_t)ldT * c];
+                        const double *yj = &Y[(size_t)m * j];
+                        for (int i = 0; i < m; ++i) s += tc[i] * yj[i];
+                        Z[c + (size_t)n * j] = s * inv;
+                    }
+                }
+                done = true;
+            }
+        }
+        if (!done) svd_jacobi(m, n, Tm.data(), ldT, th.data(), Y.data(), Z.data());
+        ms_ritz += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+
     void run(int r_, ssa_decomp_info *info) {
         r = r_;
         const int64_t mn = std::min(L, K);
         k = std::max(1, std::min<int>(p.block_k, 64));
         if (k > mn) k = (int)mn;
         pk = (int)std::min<int64_t>(r + std::max(4, k / 2), mn);
-        const int mcyc = std::max(2, (int)cdiv(2 * r, k));
+        // blocks per restart cycle (the projected SVD runs on the device for n up to ~2000)
+        int mcyc = std::max(3, (int)cdiv(2 * pk, k));
+        while (mcyc > 2 && !jacobi_blocked_fits(pk + (mcyc + 1) * k, pk + mcyc * k)) --mcyc;
         nQmax = pk + k * (mcyc + 1);
         ldT = nQmax;
         Tm.assign((size_t)ldT * ldT, 0.0);
@@ -258,8 +403,7 @@ struct Gkl {
             if (nQ + k <= nQmax && nblock < maxprod) continue;
             // ---- Ritz extraction from T (nP x nc)
             const int nc = nQ - k;
-            th.assign(nc, 0.0); Y.assign((size_t)nP * nc, 0.0); Z.assign((size_t)nc * nc, 0.0);
-            svd_jacobi(nP, nc, Tm.data(), ldT, th.data(), Y.data(), Z.data());
+            ritz_svd(nP, nc, th, Y, Z);
             anorm = std::max(anorm, th[0]);
             res.assign(nc, 0.0);
             for (int i = 0; i < nc; ++i) {
@@ -298,13 +442,13 @@ struct Gkl {
             nQ = pk + k;
         }
         // sign convention: largest-|.| entry of each U_i positive
-        double *sg = small_dev(p, 64 * 64);
-        for (int c0 = 0; c0 < r; c0 += 4096) {
-            const int nc = std::min(4096, r - c0);
-            absmax_sign<T>(L, p.U.as<T>() + L * c0, L, nc, sg, st);
-            scale_columns<T>(L, p.U.as<T>() + L * c0, L, nc, sg, st);
+        for (int c0 = 0; c0 < r; c0 += 1024) {
+            const int nc = std::min(1024, r - c0);
+            const size_t idx = sg.take(nc);
+            absmax_sign<T>(L, p.U.as<T>() + L * c0, L, nc, sg.dev(idx), st);
+            scale_columns<T>(L, p.U.as<T>() + L * c0, L, nc, sg.dev(idx), st);
         }
-        SSA_CUDA(cudaStreamSynchronize(st));
+        sg.sync();
         p.v_valid = false;
         if (info) {
             info->r_requested = r;
@@ -315,6 +459,7 @@ struct Gkl {
             info->n_vector_products = nvec;
             info->max_rel_residual = maxres;
             info->ms_products = product_ms();
+            info->ms_ritz = ms_ritz;
         }
         if (nconv < r)
             throw Error(SSA_ERR_NOT_CONVERGED, "decomposition stopped at max_products with " + std::to_string(nconv) +
