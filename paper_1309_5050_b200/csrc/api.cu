@@ -286,7 +286,17 @@ static void reconstruct_impl(PlanImpl &p, const int32_t *off, const int32_t *idx
     SSA_CUDA(cudaMemcpyAsync(go.p, off, sizeof(int32_t) * (ng + 1), cudaMemcpyHostToDevice, p.st));
     if (nidx) SSA_CUDA(cudaMemcpyAsync(gi.p, idx, sizeof(int32_t) * nidx, cudaMemcpyHostToDevice, p.st));
     SSA_CUDA(cudaMemcpyAsync(sig.p, p.sigma.data(), sizeof(double) * p.r, cudaMemcpyHostToDevice, p.st));
-    if (ng > 0) {
+    if (ng > 0 && p.path == SSA_PATH_FFT && p.fft) {
+        // eigentriples referenced by the groups, and their slot in the batched spectra
+        std::vector<int> used, slot(p.r, -1);
+        for (int t = 0; t < nidx; ++t)
+            if (slot[idx[t]] < 0) { slot[idx[t]] = (int)used.size(); used.push_back(idx[t]); }
+        DevBuf ds;
+        ds.alloc(sizeof(int) * p.r, p.st);
+        SSA_CUDA(cudaMemcpyAsync(ds.p, slot.data(), sizeof(int) * p.r, cudaMemcpyHostToDevice, p.st));
+        fft_diagsums<T>(p, p.U.as<T>(), p.V.as<T>(), sig.as<double>(), go.as<int>(), gi.as<int>(), ng, used,
+                        ds.as<int>(), out_dev);
+    } else if (ng > 0) {
         AvgParams<T> a{};
         a.nx = p.nx; a.ny = p.ny;
         a.lx = p.lx; a.ly = p.ly; a.lmap = p.full_window ? nullptr : p.lmap.as<int>();

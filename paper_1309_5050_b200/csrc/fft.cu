@@ -1,19 +1,449 @@
-// FFT circular-correlation path (Alg. 1/3/5) — placeholder until the smem radix
-// FFT kernels land; fft_supported() reports false so AUTO picks the direct path.
+// FFT circular-correlation path for the trajectory-operator products and the
+// diagonal averaging (the method of Alg. 1/3/5,
+// P:3643-3665, re-derived for the device).
+//
+// Every product is one 2-D circular correlation of the image with a box array
+// evaluated on another box (reading Q1/Q2: the same formula serves X·V and XᵀU,
+// only the scatter box and the gather box swap):
+//
+//     out[p] = Σ_d x[p + d] a[d]  =  IDFT2( X̂ ⊙ conj(DFT2(a)) )[p]      (p in the output box)
+//
+// on an Mx x My grid (powers of two, Mx >= Nx, My >= Ny, so the gathered cells
+// never wrap).  The averaging numerator is a full 2-D convolution summed over a
+// group: num_g = IDFT2( Σ_{i∈I_g} σ_i DFT2(Ψ_i) ⊙ DFT2(Φ_i) ) (no conjugate).
+//
+// Three passes over HBM, each a batch of shared-memory Stockham FFTs
+// (radix 8 with one radix-2/4 stage) with zero-padding and output pruning:
+//   A  x-direction DFT of the input box columns (real -> half spectrum, Hx = Mx/2+1
+//      frequencies), written transposed as A[j][fx][col] so that B reads rows;
+//   B  per (j, fx) row: y-direction DFT of the ny_in nonzero entries, multiply by
+//      conj(X̂[fx, :]) (products) or accumulate Ψ̂·Φ̂ over a group (averaging),
+//      inverse y-DFT, keep the ny_out rows of the output box;
+//   C  per output column: Hermitian completion of the half spectrum, inverse
+//      x-DFT, keep the output box rows, scale, gather into the compact order
+//      (or divide by the hit counts 𝕎 for the averaging).
+// X̂ = DFT2(image) is computed once per plan (it "does not depend on L").
+#include <cmath>
+
 #include "common.h"
+#include "kernels.h"
 #include "plan.h"
 
 namespace ssa {
-struct FftOperator {};
-bool fft_supported(const PlanImpl &) { return false; }
-void fft_build(PlanImpl &) { throw Error(SSA_ERR_ARG, "FFT path not built"); }
+
+template <typename T> struct cplx { T x, y; };
+template <typename T> __device__ __forceinline__ cplx<T> cadd(cplx<T> a, cplx<T> b) { return {a.x + b.x, a.y + b.y}; }
+template <typename T> __device__ __forceinline__ cplx<T> csub(cplx<T> a, cplx<T> b) { return {a.x - b.x, a.y - b.y}; }
+template <typename T> __device__ __forceinline__ cplx<T> cmul(cplx<T> a, cplx<T> b) {
+    return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+template <typename T> __device__ __forceinline__ cplx<T> cmulconj(cplx<T> a, cplx<T> b) {   // a * conj(b)
+    return {a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y};
+}
+// multiply by DIR*i  (DIR = -1 forward, +1 inverse)
+template <typename T, int DIR> __device__ __forceinline__ cplx<T> mul_i(cplx<T> a) {
+    return DIR > 0 ? cplx<T>{-a.y, a.x} : cplx<T>{a.y, -a.x};
+}
+
+__device__ __forceinline__ void sincospi_t(float a, float *s, float *c) { sincospif(a, s, c); }
+__device__ __forceinline__ void sincospi_t(double a, double *s, double *c) { sincospi(a, s, c); }
+
+template <typename T, int DIR> __device__ __forceinline__ void dft2(cplx<T> *v) {
+    const cplx<T> a = v[0], b = v[1];
+    v[0] = cadd(a, b); v[1] = csub(a, b);
+}
+template <typename T, int DIR> __device__ __forceinline__ void dft4(cplx<T> *v) {
+    const cplx<T> t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+    const cplx<T> t2 = cadd(v[1], v[3]), t3 = mul_i<T, DIR>(csub(v[1], v[3]));
+    v[0] = cadd(t0, t2); v[2] = csub(t0, t2);
+    v[1] = cadd(t1, t3); v[3] = csub(t1, t3);
+}
+template <typename T, int DIR> __device__ __forceinline__ void dft8(cplx<T> *v) {
+    cplx<T> e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+    dft4<T, DIR>(e); dft4<T, DIR>(o);
+    const T h = (T)0.70710678118654752440;
+    // o[k] *= exp(DIR*2πi k/8)
+    o[1] = cplx<T>{h * (o[1].x - (T)DIR * o[1].y), h * (o[1].y + (T)DIR * o[1].x)};
+    o[2] = mul_i<T, DIR>(o[2]);
+    o[3] = cplx<T>{h * (-o[3].x - (T)DIR * o[3].y), h * (-o[3].y + (T)DIR * o[3].x)};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { v[k] = cadd(e[k], o[k]); v[k + 4] = csub(e[k], o[k]); }
+}
+
+// One Stockham radix-R stage for `nb` transforms of length N stored back to back.
+template <typename T, int DIR, int R>
+__device__ __forceinline__ void stockham_stage(const cplx<T> *__restrict__ x, cplx<T> *__restrict__ y, int N, int Ns,
+                                               int nbatch) {
+    constexpr int LR = R == 2 ? 1 : (R == 4 ? 2 : 3);
+    const int lgn = 31 - __clz(N);
+    const int nbf = N >> LR, lgb = lgn - LR;
+    for (int b = threadIdx.x; b < (nbatch << lgb); b += blockDim.x) {
+        const int t = b >> lgb, j = b & (nbf - 1);
+        const cplx<T> *xs = x + (size_t)t * N;
+        cplx<T> *ys = y + (size_t)t * N;
+        cplx<T> v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = xs[j + r * nbf];
+        const int k = j & (Ns - 1);
+        if (Ns > 1) {
+            T s, c;
+            sincospi_t((T)(2 * DIR) * (T)k / (T)(Ns * R), &s, &c);
+            const cplx<T> w1{c, s};
+            cplx<T> w = w1;
+#pragma unroll
+            for (int r = 1; r < R; ++r) { v[r] = cmul(v[r], w); w = cmul(w, w1); }
+        }
+        if (R == 2) dft2<T, DIR>(v);
+        else if (R == 4) dft4<T, DIR>(v);
+        else dft8<T, DIR>(v);
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) ys[base + r * Ns] = v[r];
+    }
+}
+
+// Batched in-place-by-ping-pong FFT of nbatch transforms of length N = 2^lg in
+// shared memory; returns the buffer that holds the result.  All threads of the
+// CTA take part; the caller has synchronised before the call.
+template <typename T, int DIR>
+__device__ cplx<T> *fft_batch(cplx<T> *x, cplx<T> *y, int lg, int nbatch) {
+    const int N = 1 << lg;
+    int Ns = 1;
+    const int rem = lg % 3;
+    if (rem == 1) { stockham_stage<T, DIR, 2>(x, y, N, Ns, nbatch); Ns *= 2; }
+    else if (rem == 2) { stockham_stage<T, DIR, 4>(x, y, N, Ns, nbatch); Ns *= 4; }
+    if (rem) { __syncthreads(); cplx<T> *t = x; x = y; y = t; }
+    while (Ns < N) {
+        stockham_stage<T, DIR, 8>(x, y, N, Ns, nbatch);
+        Ns *= 8;
+        __syncthreads();
+        cplx<T> *t = x; x = y; y = t;
+    }
+    return x;
+}
+
+// ---------------------------------------------------------------------------
+// Pass A: x-direction DFT of box columns.
+//   input : in[map(ix, col) + ld * j] (compact, map = box -> compact or -1), box bx x by,
+//           optional per-vector scale (σ_i for the averaging); the image when ld = 0 and map = null
+//   output: A[(j * Hx + fx) * by + col], fx < Hx
+// grid: (ceil(by / CB), k), CB columns per CTA.
+// ---------------------------------------------------------------------------
 template <typename T>
-void fft_xv(PlanImpl &, const T *, int64_t, T *, int64_t, int) { throw Error(SSA_ERR_ARG, "FFT path not built"); }
+__global__ void __launch_bounds__(256)
+fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, int bx, int by, int jsel_n,
+           const int *__restrict__ jsel, const double *__restrict__ scale, int lgx, int CB, cplx<T> *__restrict__ A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int Mx = 1 << lgx, Hx = Mx / 2 + 1;
+    cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
+    cplx<T> *b1 = b0 + (size_t)CB * Mx;
+    const int col0 = blockIdx.x * CB;
+    const int jo = blockIdx.y;                       // output vector slot
+    const int j = jsel ? jsel[jo] : jo;             // input vector index
+    const T sc = scale ? (T)scale[j] : T(1);
+    const int ncol = min(CB, by - col0);
+    for (int idx = threadIdx.x; idx < CB * Mx; idx += blockDim.x) {
+        const int c = idx >> lgx, ix = idx & (Mx - 1);
+        T v = T(0);
+        if (c < ncol && ix < bx) {
+            const int64_t box = ix + (int64_t)bx * (col0 + c);
+            const int64_t ci = map ? (int64_t)map[box] : box;
+            if (ci >= 0) v = sc * in[ci + ld * j];
+        }
+        b0[idx] = cplx<T>{v, T(0)};
+    }
+    __syncthreads();
+    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgx, CB);
+    // transposed write: consecutive threads -> consecutive columns
+    for (int idx = threadIdx.x; idx < Hx * CB; idx += blockDim.x) {
+        const int fx = idx / CB, c = idx - fx * CB;
+        if (c < ncol) A[((int64_t)jo * Hx + fx) * by + col0 + c] = res[(size_t)c * Mx + fx];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pass B (products): per (j, fx): y-DFT of A row (ny_in entries), multiply by
+// conj, inverse y-DFT, keep ny_out entries.  mode 0: Y = X̂ ⊙ conj(Â) (correlation);
+// mode 1: forward only, write all My entries (plan-time X̂).
+// grid: (ceil(Hx / RB), k)
+// ---------------------------------------------------------------------------
 template <typename T>
-void fft_xtu(PlanImpl &, const T *, int64_t, T *, int64_t, int) { throw Error(SSA_ERR_ARG, "FFT path not built"); }
+__global__ void __launch_bounds__(256)
+fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, const cplx<T> *__restrict__ Xh,
+           int mode, cplx<T> *__restrict__ B, int ny_out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int My = 1 << lgy;
+    cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
+    cplx<T> *b1 = b0 + (size_t)RB * My;
+    const int fx0 = blockIdx.x * RB;
+    const int j = blockIdx.y;
+    const int nrow = min(RB, Hx - fx0);
+    for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
+        const int rr = idx >> lgy, y = idx & (My - 1);
+        cplx<T> v{T(0), T(0)};
+        if (rr < nrow && y < ny_in) v = A[((int64_t)j * Hx + fx0 + rr) * ny_in + y];
+        b0[idx] = v;
+    }
+    __syncthreads();
+    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgy, RB);
+    cplx<T> *oth = (res == b0) ? b1 : b0;
+    if (mode == 1) {
+        for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
+            const int rr = idx >> lgy, y = idx & (My - 1);
+            if (rr < nrow) B[((int64_t)j * Hx + fx0 + rr) * My + y] = res[idx];
+        }
+        return;
+    }
+    for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
+        const int rr = idx >> lgy, y = idx & (My - 1);
+        const cplx<T> xh = (rr < nrow) ? Xh[(int64_t)(fx0 + rr) * My + y] : cplx<T>{T(0), T(0)};
+        res[idx] = cmulconj(xh, res[idx]);
+    }
+    __syncthreads();
+    cplx<T> *out = fft_batch<T, +1>(res, oth, lgy, RB);
+    for (int idx = threadIdx.x; idx < RB * ny_out; idx += blockDim.x) {
+        const int rr = idx / ny_out, y = idx - rr * ny_out;
+        if (rr < nrow) B[((int64_t)j * Hx + fx0 + rr) * ny_out + y] = out[(size_t)rr * My + y];
+    }
+}
+
+// Pass B (averaging): per (g, fx): Σ_{i∈I_g} DFT_y(AU_i row) ⊙ DFT_y(AV_i row), inverse, keep ny rows.
+template <typename T>
+__global__ void __launch_bounds__(256)
+fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restrict__ AV, int ky, const int *grp_off,
+                const int *grp_idx, const int *slot, int Hx, int lgy, int RB, cplx<T> *__restrict__ B, int ny_out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int My = 1 << lgy;
+    cplx<T> *acc = reinterpret_cast<cplx<T> *>(smem_raw);
+    cplx<T> *u0 = acc + (size_t)RB * My;
+    cplx<T> *u1 = u0 + (size_t)RB * My;
+    cplx<T> *v0 = u1 + (size_t)RB * My;
+    cplx<T> *v1 = v0 + (size_t)RB * My;
+    const int fx0 = blockIdx.x * RB;
+    const int g = blockIdx.y;
+    const int nrow = min(RB, Hx - fx0);
+    for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) acc[idx] = cplx<T>{T(0), T(0)};
+    for (int t = grp_off[g]; t < grp_off[g + 1]; ++t) {
+        const int s = slot[grp_idx[t]];
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
+            const int rr = idx >> lgy, y = idx & (My - 1);
+            cplx<T> a{T(0), T(0)}, b{T(0), T(0)};
+            if (rr < nrow) {
+                if (y < ly) a = AU[((int64_t)s * Hx + fx0 + rr) * ly + y];
+                if (y < ky) b = AV[((int64_t)s * Hx + fx0 + rr) * ky + y];
+            }
+            u0[idx] = a; v0[idx] = b;
+        }
+        __syncthreads();
+        cplx<T> *ru = fft_batch<T, -1>(u0, u1, lgy, RB);
+        cplx<T> *rv = fft_batch<T, -1>(v0, v1, lgy, RB);
+        for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) acc[idx] = cadd(acc[idx], cmul(ru[idx], rv[idx]));
+    }
+    __syncthreads();
+    cplx<T> *out = fft_batch<T, +1>(acc, u0, lgy, RB);
+    for (int idx = threadIdx.x; idx < RB * ny_out; idx += blockDim.x) {
+        const int rr = idx / ny_out, y = idx - rr * ny_out;
+        if (rr < nrow) B[((int64_t)g * Hx + fx0 + rr) * ny_out + y] = out[(size_t)rr * My + y];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pass C: per output column y: Hermitian completion, inverse x-DFT, keep ox rows.
+//   products : out[omap(x, y) + ldo * j] = Re(...) * inv   (omap: box -> compact or -1)
+//   averaging: out[x + ldo*y + stride*j] = Re(...) * inv / w  on w > 0, NaN elsewhere
+// grid: (ceil(oy / CB), k)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256)
+fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int ox, T inv, T *__restrict__ out,
+           int64_t ldo, const int *__restrict__ omap, const int *__restrict__ w, int64_t stride) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int Mx = 1 << lgx;
+    cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
+    cplx<T> *b1 = b0 + (size_t)CB * Mx;
+    const int y0 = blockIdx.x * CB;
+    const int j = blockIdx.y;
+    const int ncol = min(CB, oy - y0);
+    // coalesced transposing load of the half spectrum
+    for (int idx = threadIdx.x; idx < Hx * CB; idx += blockDim.x) {
+        const int fx = idx / CB, c = idx - fx * CB;
+        cplx<T> v{T(0), T(0)};
+        if (c < ncol) v = B[((int64_t)j * Hx + fx) * oy + y0 + c];
+        b0[(size_t)c * Mx + fx] = v;
+    }
+    __syncthreads();
+    // Hermitian completion: Z[Mx - f] = conj(Z[f]) for 0 < f < Mx/2
+    for (int idx = threadIdx.x; idx < CB * (Mx / 2 - 1); idx += blockDim.x) {
+        const int c = idx / (Mx / 2 - 1), f = 1 + idx - c * (Mx / 2 - 1);
+        const cplx<T> v = b0[(size_t)c * Mx + f];
+        b0[(size_t)c * Mx + Mx - f] = cplx<T>{v.x, -v.y};
+    }
+    __syncthreads();
+    cplx<T> *res = fft_batch<T, +1>(b0, b1, lgx, CB);
+    for (int idx = threadIdx.x; idx < CB * ox; idx += blockDim.x) {
+        const int c = idx / ox, x = idx - c * ox;
+        if (c >= ncol) continue;
+        const int y = y0 + c;
+        const T v = res[(size_t)c * Mx + x].x * inv;
+        if (w) {
+            const int wn = w[x + (int64_t)ox * y];
+            out[(int64_t)j * stride + x + ldo * y] = wn > 0 ? v / (T)wn : (T)NAN;
+        } else {
+            const int64_t box = x + (int64_t)ox * y;
+            const int64_t oi = omap ? (int64_t)omap[box] : box;
+            if (oi >= 0) out[oi + ldo * j] = v;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+struct FftOperator {
+    int lgx = 0, lgy = 0, Mx = 0, My = 0, Hx = 0;
+    DevBuf Xh;        // cplx[Hx][My]: DFT2 of the image
+    DevBuf bufA, bufB;
+    size_t capA = 0, capB = 0;
+};
+
+static int ilog2_ceil(int64_t n) {
+    int l = 0;
+    while ((int64_t(1) << l) < n) ++l;
+    return l;
+}
+
+bool fft_supported(const PlanImpl &p) {
+    // shared-memory Stockham sizes: up to 8192 points (fp32) / 2048 along y and 4096 along x (fp64)
+    const int lx = ilog2_ceil(p.nx), ly = ilog2_ceil(p.ny);
+    if (p.has_comm) return false;
+    return p.dt == SSA_F64 ? (lx <= 12 && ly <= 11) : (lx <= 13 && ly <= 13);
+}
+
+// transforms per CTA so that a CTA holds ~target complex points (2 buffers)
+static int batch_for(int lg, int target) { return std::max(1, target >> lg); }
+
+template <typename T>
+static size_t smem_ab(int lg, int nb) { return sizeof(cplx<T>) * 2 * ((size_t)nb << lg); }
+
+template <typename T>
+static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int bx, int by, int k, const int *jsel,
+                   const double *scale, cplx<T> *A, cudaStream_t st) {
+    const int CB = batch_for(f.lgx, 4096);
+    const size_t smem = smem_ab<T>(f.lgx, CB);
+    SSA_CUDA(cudaFuncSetAttribute(fft_pass_a<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fft_pass_a<T><<<dim3((unsigned)cdiv(by, CB), k), 256, smem, st>>>(in, ld, map, bx, by, k, jsel, scale, f.lgx, CB, A);
+    after_launch("fft_pass_a");
+}
+
+template <typename T>
+static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode, cplx<T> *B, int ny_out, cudaStream_t st) {
+    const int RB = batch_for(f.lgy, 4096);
+    const size_t smem = smem_ab<T>(f.lgy, RB);
+    SSA_CUDA(cudaFuncSetAttribute(fft_pass_b<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fft_pass_b<T><<<dim3((unsigned)cdiv(f.Hx, RB), k), 256, smem, st>>>(A, ny_in, f.Hx, f.lgy, RB,
+                                                                         f.Xh.as<cplx<T>>(), mode, B, ny_out);
+    after_launch("fft_pass_b");
+}
+
+template <typename T>
+static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *out, int64_t ldo, const int *omap,
+                   const int *w, int64_t stride, cudaStream_t st) {
+    const int CB = batch_for(f.lgx, 4096);
+    const size_t smem = smem_ab<T>(f.lgx, CB);
+    SSA_CUDA(cudaFuncSetAttribute(fft_pass_c<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const T inv = (T)(1.0 / ((double)f.Mx * (double)f.My));
+    fft_pass_c<T><<<dim3((unsigned)cdiv(oy, CB), k), 256, smem, st>>>(B, oy, f.Hx, f.lgx, CB, ox, inv, out, ldo, omap,
+                                                                       w, stride);
+    after_launch("fft_pass_c");
+}
+
+template <typename T>
+static void ensure(FftOperator &f, DevBuf &b, size_t &cap, size_t need, cudaStream_t st) {
+    if (need > cap) { b.alloc(need, st); cap = need; }
+}
+
+template <typename T>
+static void build_impl(PlanImpl &p) {
+    FftOperator &f = *p.fft;
+    f.lgx = ilog2_ceil(p.nx); f.lgy = ilog2_ceil(p.ny);
+    f.Mx = 1 << f.lgx; f.My = 1 << f.lgy; f.Hx = f.Mx / 2 + 1;
+    f.Xh.alloc(sizeof(cplx<T>) * (size_t)f.Hx * f.My, p.st);
+    DevBuf tmp;
+    tmp.alloc(sizeof(cplx<T>) * (size_t)f.Hx * p.ny, p.st);
+    // X̂: x-DFT of the image columns, then the full-length y-DFT (mode 1)
+    pass_a<T>(f, p.img.as<T>(), 0, nullptr, p.nx, p.ny, 1, nullptr, nullptr, tmp.as<cplx<T>>(), p.st);
+    pass_b<T>(f, tmp.as<cplx<T>>(), p.ny, 1, 1, f.Xh.as<cplx<T>>(), f.My, p.st);
+    SSA_CUDA(cudaStreamSynchronize(p.st));
+}
+
+void fft_build(PlanImpl &p) {
+    if (!p.fft) p.fft = new FftOperator();
+    if (p.dt == SSA_F64) build_impl<double>(p);
+    else build_impl<float>(p);
+}
+
+// out box (ox x oy) <- correlation of the image with the input box (bx x by)
+template <typename T>
+static void correlate(PlanImpl &p, const T *in, int64_t ldin, const int *imap, int bx, int by, T *out, int64_t ldo,
+                      const int *omap, int ox, int oy, int k) {
+    FftOperator &f = *p.fft;
+    for (int j0 = 0; j0 < k; j0 += 64) {
+        const int kc = std::min(64, k - j0);
+        ensure<T>(f, f.bufA, f.capA, sizeof(cplx<T>) * (size_t)kc * f.Hx * by, p.st);
+        ensure<T>(f, f.bufB, f.capB, sizeof(cplx<T>) * (size_t)kc * f.Hx * oy, p.st);
+        pass_a<T>(f, in + ldin * j0, ldin, imap, bx, by, kc, nullptr, nullptr, f.bufA.as<cplx<T>>(), p.st);
+        pass_b<T>(f, f.bufA.as<cplx<T>>(), by, kc, 0, f.bufB.as<cplx<T>>(), oy, p.st);
+        pass_c<T>(f, f.bufB.as<cplx<T>>(), oy, kc, ox, out + ldo * j0, ldo, omap, nullptr, 0, p.st);
+    }
+}
+
+template <typename T>
+void fft_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k) {
+    correlate<T>(p, V, ldv, p.full_k ? nullptr : p.kmap.as<int>(), p.kx, p.ky, U, ldu,
+                 p.full_window ? nullptr : p.lmap.as<int>(), p.lx, p.ly, k);
+}
+
+template <typename T>
+void fft_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k) {
+    correlate<T>(p, U, ldu, p.full_window ? nullptr : p.lmap.as<int>(), p.lx, p.ly, V, ldv,
+                 p.full_k ? nullptr : p.kmap.as<int>(), p.kx, p.ky, k);
+}
+
+// Grouped averaging via FFT: out_g = IDFT2(Σ_{i∈I_g} σ_i Ψ̂_i Φ̂_i) / 𝕎 (NaN off 𝔑′).
+template <typename T>
+void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, const int *grp_off_dev,
+                  const int *grp_idx_dev, int ng, const std::vector<int> &used, const int *slot_dev, T *out) {
+    FftOperator &f = *p.fft;
+    const int nu = (int)used.size();
+    DevBuf jsel, AU, AV, B;
+    jsel.alloc(sizeof(int) * std::max(nu, 1), p.st);
+    SSA_CUDA(cudaMemcpyAsync(jsel.p, used.data(), sizeof(int) * nu, cudaMemcpyHostToDevice, p.st));
+    AU.alloc(sizeof(cplx<T>) * (size_t)nu * f.Hx * p.ly, p.st);
+    AV.alloc(sizeof(cplx<T>) * (size_t)nu * f.Hx * p.ky, p.st);
+    B.alloc(sizeof(cplx<T>) * (size_t)ng * f.Hx * p.ny, p.st);
+    pass_a<T>(f, U, p.L, p.full_window ? nullptr : p.lmap.as<int>(), p.lx, p.ly, nu, jsel.as<int>(), sig_dev,
+              AU.as<cplx<T>>(), p.st);
+    pass_a<T>(f, V, p.K, p.full_k ? nullptr : p.kmap.as<int>(), p.kx, p.ky, nu, jsel.as<int>(), nullptr,
+              AV.as<cplx<T>>(), p.st);
+    const int RB = batch_for(f.lgy, 2048);
+    const size_t smem = sizeof(cplx<T>) * 5 * ((size_t)RB << f.lgy);
+    SSA_CUDA(cudaFuncSetAttribute(fft_pass_b_conv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fft_pass_b_conv<T><<<dim3((unsigned)cdiv(f.Hx, RB), ng), 256, smem, p.st>>>(
+        AU.as<cplx<T>>(), p.ly, AV.as<cplx<T>>(), p.ky, grp_off_dev, grp_idx_dev, slot_dev, f.Hx, f.lgy, RB,
+        B.as<cplx<T>>(), p.ny);
+    after_launch("fft_pass_b_conv");
+    pass_c<T>(f, B.as<cplx<T>>(), p.ny, ng, p.nx, out, p.nx, nullptr, p.weights.as<int>(), (int64_t)p.nx * p.ny, p.st);
+    SSA_CUDA(cudaStreamSynchronize(p.st));
+}
+
 template void fft_xv<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int);
 template void fft_xv<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int);
 template void fft_xtu<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int);
 template void fft_xtu<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int);
+template void fft_diagsums<float>(PlanImpl &, const float *, const float *, const double *, const int *, const int *,
+                                  int, const std::vector<int> &, const int *, float *);
+template void fft_diagsums<double>(PlanImpl &, const double *, const double *, const double *, const int *, const int *,
+                                   int, const std::vector<int> &, const int *, double *);
+
 void fft_destroy(FftOperator *f) { delete f; }
+
 }  // namespace ssa

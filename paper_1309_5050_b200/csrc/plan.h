@@ -71,6 +71,9 @@ template <typename T>
 void fft_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k);
 template <typename T>
 void fft_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k);
+template <typename T>
+void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, const int *grp_off_dev,
+                  const int *grp_idx_dev, int ng, const std::vector<int> &used, const int *slot_dev, T *out);
 void fft_destroy(FftOperator *f);
 
 }  // namespace ssa

@@ -95,12 +95,17 @@ def test_shapes_c4_full_size_bit_exact():
 
 
 # ---------------------------------------------------------------- products
+PATHS = ["direct", "fft"]
+
+
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name", ["shaped_small", "shaped_wmask", "shaped_tiny", "c1"])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("k", [1, 5, 37])
-def test_products_small(name, dtype, k):
+@pytest.mark.parametrize("k", [1, 5, 37, 70])
+def test_products_small(name, dtype, k, path):
     w = _cases()[name]
-    p = _plan(w, dtype=dtype, path="direct")
+    p = _plan(w, dtype=dtype, path=path)
+    assert p.path == path
     x = _oracle_input(w, dtype)
     sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
     rng = np.random.default_rng(k)
@@ -125,9 +130,10 @@ def test_products_device_tensors_and_ld():
     assert relfro(U.double().cpu().numpy(), ref) <= FP32_PROD_TOL
 
 
-def test_products_c2_mssa():
+@pytest.mark.parametrize("path", PATHS)
+def test_products_c2_mssa(path):
     w = synth.config2()
-    p = _plan(w, path="direct")
+    p = _plan(w, path=path)
     x = _oracle_input(w, "f32")
     sh = oracle.shapes(x, w.window)
     rng = np.random.default_rng(2)
@@ -137,11 +143,12 @@ def test_products_c2_mssa():
     assert relfro(p.matmul(U, transpose=True), oracle.xtu(x, sh, U)) <= FP32_PROD_TOL
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("cfg", ["c3", "c4"])
-def test_products_full_size_sampled(cfg):
+def test_products_full_size_sampled(cfg, path):
     """Full BASELINE sizes, block k = 32: sampled output rows against the oracle."""
     w = synth.get(cfg)
-    p = _plan(w, path="direct")
+    p = _plan(w, path=path)
     x = _oracle_input(w, "f32")
     sh = oracle.shapes(x, w.window, mask=w.mask)
     rng = np.random.default_rng(3)
@@ -162,10 +169,11 @@ def test_products_full_size_sampled(cfg):
     assert abs(lhs - rhs) <= 1e-5 * np.sqrt(np.sum(Ug.astype(np.float64) ** 2) * np.sum(U.astype(np.float64) ** 2))
 
 
-def test_products_closed_form_c3_twin():
+@pytest.mark.parametrize("path", PATHS)
+def test_products_closed_form_c3_twin(path):
     """P5: noiseless c3 geometry, products against the separable closed form."""
     w = synth.config3(noise=False)
-    p = _plan(w, path="direct")
+    p = _plan(w, path=path)
     from paper_1309_5050_b200 import Plan  # noqa: F401
     sh = oracle.shapes(w.data, w.window)
     rng = np.random.default_rng(4)
@@ -227,9 +235,10 @@ def _check_recon(p, x, sh, s_or, U_or, V_or, groups, tol=1e-4):
         assert relfro(a[npr], b[npr]) <= tol, (g, groups[g], relfro(a[npr], b[npr]))
 
 
-def test_decompose_c1_fp64():
+@pytest.mark.parametrize("path", PATHS)
+def test_decompose_c1_fp64(path):
     w = synth.config1()
-    p = _plan(w)
+    p = _plan(w, path=path)
     x = _oracle_input(w, "f64")
     sh = oracle.shapes(x, w.window)
     s_or, U_or, V_or, s_all = oracle.svd_dense(x, sh, 10)
@@ -243,9 +252,10 @@ def test_decompose_c1_fp64():
     np.testing.assert_allclose(recs[0] + recs[1] + recs[2], x, rtol=1e-10, atol=1e-10)
 
 
-def test_decompose_c2_mssa_fp32():
+@pytest.mark.parametrize("path", PATHS)
+def test_decompose_c2_mssa_fp32(path):
     w = synth.config2()
-    p = _plan(w)
+    p = _plan(w, path=path)
     x = _oracle_input(w, "f32")
     sh = oracle.shapes(x, w.window)
     s_or, U_or, V_or, s_all = oracle.svd_dense(x, sh, 17)
@@ -254,10 +264,11 @@ def test_decompose_c2_mssa_fp32():
     _check_recon(p, x, sh, s_or, U_or, V_or, [g for g in w.groups if max(g) < 6])
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name", ["shaped_small", "shaped_wmask"])
-def test_decompose_shaped_small(name):
+def test_decompose_shaped_small(name, path):
     w = _cases()[name]
-    p = _plan(w)
+    p = _plan(w, path=path)
     x = _oracle_input(w, "f32")
     sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
     r = w.r
@@ -269,9 +280,10 @@ def test_decompose_shaped_small(name):
         _check_recon(p, x, sh, s_or, U_or, V_or, groups)
 
 
-def test_reconstruct_from_oracle_triples_c1_and_shaped():
+@pytest.mark.parametrize("path", PATHS)
+def test_reconstruct_from_oracle_triples_c1_and_shaped(path):
     for w, dt in [(synth.config1(), "f64"), (synth.small_shaped(seed=14, wmask_drop=4), "f32")]:
-        p = _plan(w, dtype=dt)
+        p = _plan(w, dtype=dt, path=path)
         x = _oracle_input(w, dt)
         sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
         s_or, U_or, V_or, _ = oracle.svd_dense(x, sh, 6)
@@ -286,10 +298,11 @@ def test_reconstruct_from_oracle_triples_c1_and_shaped():
             assert relfro(a[m], b[m]) <= tol
 
 
-def test_c3_noiseless_closed_form():
+@pytest.mark.parametrize("path", PATHS)
+def test_c3_noiseless_closed_form(path):
     """P6/P7/P12 at the full c3 size: rank 24, σ = closed form, {1..24} = the image."""
     w = synth.config3(noise=False)
-    p = _plan(w)
+    p = _plan(w, path=path)
     info = p.decompose(32, allow_not_converged=True)
     s_cf = cf.sigma_rect(w.terms, 64, 64, 449, 449)
     s = p.sigma
