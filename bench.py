@@ -183,12 +183,40 @@ def run_ours(args, rank, world, dist):
     d2h = int(len(groups) * np.asarray(w.data).size * esz + 8 * w.r)
     e2e_value = info_h["n_vector_products"] / (np.mean(e2e_times) / 1e3) * world
 
-    # ---- roofline of the dominant kernel (the trajectory block product), timed live:
-    # the library brackets every block product with CUDA events on the plan's stream
-    flops_per_block = 2.0 * L * K * k
+    # ---- roofline of the trajectory block product (the kernel SURVEY §8(d) sizes), timed
+    # live: the library brackets every block product with CUDA events on the plan's stream
     avg_block_ms = ms_prod / max(nblk, 1)
-    achieved = flops_per_block / (avg_block_ms / 1e3) / 1e12
-    peak = FP64_PEAK_TFLOPS if w.dtype == "f64" else FFMA_PEAK_TFLOPS
+    peaks = _peaks()
+    if p.path == "fft":
+        # 3-pass model per vector: read the input box, write the output box,
+        # write+read the x-transformed input (Hx·by) and y-filtered output (Hx·oy), complex,
+        # plus the image spectrum once per block; identical for X·V and Xᵀ·U
+        esz = 8 if w.dtype == "f64" else 4
+        nx_, ny_ = np.asarray(w.data).shape
+        Mx = 1 << int(np.ceil(np.log2(nx_))); My = 1 << int(np.ceil(np.log2(max(ny_, 1))))
+        Hx = Mx // 2 + 1
+        kx_, ky_ = nx_ - w.window[0] + 1, ny_ - w.window[1] + 1
+        per_vec = esz * (K + L) + 2 * (2 * esz) * Hx * (ky_ + w.window[1])
+        alg = k * per_vec + (2 * esz) * Hx * My
+        achieved = alg / (avg_block_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": "FFT correlation block product (fft_pass_a/b/c)",
+                "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)",
+                "algorithmic_bytes_per_launch": alg}
+    else:
+        flops_per_block = 2.0 * L * K * k
+        achieved = flops_per_block / (avg_block_ms / 1e3) / 1e12
+        peak = FP64_PEAK_TFLOPS if w.dtype == "f64" else FFMA_PEAK_TFLOPS
+        roof = {"bound": "alu", "kernel": "corr_direct (X·V / Xᵀ·U block product, FFMA)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None,
+                "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md SM count,"
+                               " MEASURED_PEAKS sm_max_mhz); fp64 = 1/2",
+                "algorithmic_flops_per_launch": flops_per_block}
+    roof.update({"avg_launch_ms": avg_block_ms, "launches_per_step": nblk / args.steps,
+                 "share_of_step": ms_prod / max(ms_local, 1e-9),
+                 "note": "a 'launch' is one block product of k vectors (3 FFT passes or corr_direct + split-K reduce)"})
     res = {
         "metric": "trajectory products/s",
         "value": nvec_all / (ms_all / 1e3),
@@ -215,13 +243,7 @@ def run_ours(args, rank, world, dist):
         "e2e": {"value": e2e_value, "unit": "vector products/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": float(np.mean(e2e_times))},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "alu", "kernel": "corr_direct (X·V / Xᵀ·U block product)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": None,
-                     "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md SM count,"
-                                    " MEASURED_PEAKS sm_max_mhz); fp64 = 1/2",
-                     "algorithmic_flops_per_launch": flops_per_block, "avg_launch_ms": avg_block_ms,
-                     "share_of_step": ms_prod / max(ms_local, 1e-9)},
+        "roofline": roof,
         "clocks": clk.summary(),
     }
     return res, w
@@ -229,9 +251,10 @@ def run_ours(args, rank, world, dist):
 
 # ----------------------------------------------------------------------------- oracle (CPU)
 def oracle_products_per_s(w, budget_s=15.0):
-    """The oracle's naive X·V / Xᵀ·U (oracle/oracle_core.c) on a bounded sample of
-    the same workload: whole block products if they fit the budget, else sampled
-    output rows (scaled to products/s)."""
+    """The oracle's naive X·V / Xᵀ·U (oracle/oracle_core.c) on a bounded sample of the same
+    workload: whole block products (X·V then Xᵀ·U, k = block width) repeated until the time
+    budget is used, or, when one block would exceed the budget, sampled output rows of each
+    product scaled to whole blocks."""
     import oracle
     x = np.array(w.data, dtype=np.float64)
     if w.dtype == "f32":
@@ -240,16 +263,26 @@ def oracle_products_per_s(w, budget_s=15.0):
     rng = np.random.default_rng(0)
     k = w.block_k
     V = rng.normal(size=(sh.K, k)); U = rng.normal(size=(sh.L, k))
-    # time one output row of X·V to size the sample
     t0 = time.perf_counter(); oracle.xv_rows(x, sh, V, [0]); t_row = time.perf_counter() - t0
+    est_block = 2 * t_row * sh.L              # X·V rows cost ≈ Xᵀ·U rows in total (both L·K·k)
+    cores = len(os.sched_getaffinity(0))
+    if est_block <= budget_s / 2:
+        n, t_all = 0, 0.0
+        while t_all < budget_s and (n == 0 or t_all + t_all / n <= budget_s * 1.5):
+            t0 = time.perf_counter()
+            oracle.xv(x, sh, V)
+            oracle.xtu(x, sh, U)
+            t_all += time.perf_counter() - t0
+            n += 1
+        value = 2 * k * n / t_all
+        sample = f"{w.name}: {n} whole X·V + Xᵀ·U block pairs (k={k}), {t_all:.1f} s of CPU"
+        return value, cores, sample
     rows = int(max(1, min(sh.L, budget_s / 2 / max(t_row, 1e-6))))
     t0 = time.perf_counter(); oracle.xv_rows(x, sh, V, np.arange(rows)); t_xv = time.perf_counter() - t0
     kc = int(max(1, min(sh.K, rows * sh.K // sh.L)))
     t0 = time.perf_counter(); oracle.xtu(x, sh, U, kstart=0, kcount=kc); t_xtu = time.perf_counter() - t0
-    frac_xv, frac_xtu = rows / sh.L, kc / sh.K
-    t_block = t_xv / frac_xv + t_xtu / frac_xtu          # extrapolated time of one X·V + one Xᵀ·U block
+    t_block = t_xv * sh.L / rows + t_xtu * sh.K / kc
     value = 2 * k / t_block
-    cores = len(os.sched_getaffinity(0))
     sample = (f"{w.name}: X·V on {rows}/{sh.L} rows and Xᵀ·U on {kc}/{sh.K} rows of a k={k} block "
               f"({t_xv + t_xtu:.1f} s of CPU), scaled to whole blocks")
     return value, cores, sample

@@ -24,6 +24,19 @@ void after_launch(const char *what) {
     ++g_launches;
 }
 
+void pool_init() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    if (done_dev == dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;   // retain freed blocks for reuse by later plans
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_dev = dev;
+}
+
 int num_sms() {
     static int n = 0;
     if (n == 0) {

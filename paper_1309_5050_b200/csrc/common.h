@@ -37,7 +37,10 @@ void count_launch(int n = 1);
 // Check the last launch and count it.
 void after_launch(const char *what);
 
-// Owning device buffer (cudaMallocAsync on the plan's stream).
+// Owning device buffer from the stream-ordered pool allocator (cudaMallocAsync on the
+// plan's stream; the device's default pool keeps freed blocks cached, so creating and
+// destroying plans does not pay cudaMalloc/cudaFree each time).
+void pool_init();
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
@@ -54,12 +57,13 @@ struct DevBuf {
     void alloc(size_t n, cudaStream_t st) {
         if (n <= bytes && p) return;
         release();
+        pool_init();
         s = st;
-        SSA_CUDA(cudaMalloc(&p, n ? n : 16));
+        SSA_CUDA(cudaMallocAsync(&p, n ? n : 16, st));
         bytes = n;
     }
     void release() {
-        if (p) { cudaFree(p); p = nullptr; bytes = 0; }
+        if (p) { cudaFreeAsync(p, s); p = nullptr; bytes = 0; }
     }
     template <class T> T *as() const { return static_cast<T *>(p); }
 };

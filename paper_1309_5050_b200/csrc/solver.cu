@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -93,6 +95,8 @@ struct Gkl {
     uint64_t sid = 1;
     double thr_abs, thr_rel, thr_chol;
     bool gpu_ritz = true;
+    bool full_k_reorth = false;   // set when K < L (then the K side is the short one)
+    bool debug = std::getenv("SSA_DEBUG") != nullptr;
 
     explicit Gkl(PlanImpl &pl) : p(pl), st(pl.st), L(pl.L), K(pl.K) {
         thr_abs = (sizeof(T) == 4) ? 1e-6 : 1e-14;
@@ -161,16 +165,17 @@ struct Gkl {
             for (size_t t = 0; t < C.size(); ++t) coef[t] += C[t];
     }
 
-    // Cholesky G = RᵀR (R upper, column-major); false if a pivot is tiny (relative).
-    bool cholesky(int n, const double *G, std::vector<double> &R) {
+    // Cholesky (G + shift·I) = RᵀR (R upper, column-major); false if a pivot is not
+    // positive or tiny relative to the largest diagonal entry.
+    bool cholesky(int n, const double *G, double shift, double thr, std::vector<double> &R) {
         R.assign((size_t)n * n, 0.0);
         double dmax = 0.0;
         for (int j = 0; j < n; ++j) dmax = std::max(dmax, G[j + (size_t)n * j]);
         if (!(dmax > 0.0)) return false;
         for (int j = 0; j < n; ++j) {
-            double s = G[j + (size_t)n * j];
+            double s = G[j + (size_t)n * j] + shift;
             for (int t = 0; t < j; ++t) s -= R[t + (size_t)n * j] * R[t + (size_t)n * j];
-            if (!(s > thr_chol * dmax) || !(std::sqrt(s) > thr_abs * anorm)) return false;
+            if (!(s > thr * dmax)) return false;
             const double rjj = std::sqrt(s);
             R[j + (size_t)n * j] = rjj;
             for (int i = j + 1; i < n; ++i) {
@@ -182,69 +187,95 @@ struct Gkl {
         return true;
     }
 
-    // Orthonormalise W (M x kc) against `against` (na columns) and internally:
-    // CholeskyQR2, with an SVQB pass (column-scaled Gram eigen-decomposition) when
-    // the Gram is ill-conditioned; numerically dependent directions are replaced by
-    // seeded random ones (zeroed when the space is exhausted).  Returns B
-    // (kc x kc, column-major) with W_in ≈ against·(·) + W_out·B.
+    static void upper_inverse(int n, const std::vector<double> &R, std::vector<double> &S) {
+        S.assign((size_t)n * n, 0.0);
+        for (int j = 0; j < n; ++j) {
+            S[j + (size_t)n * j] = 1.0 / R[j + (size_t)n * j];
+            for (int i = j - 1; i >= 0; --i) {
+                double v = 0.0;
+                for (int t = i + 1; t <= j; ++t) v += R[i + (size_t)n * t] * S[t + (size_t)n * j];
+                S[i + (size_t)n * j] = -v / R[i + (size_t)n * i];
+            }
+        }
+    }
+
+    // Orthonormalise W (M x kc) against `against` (na orthonormal columns) and internally,
+    // by (shifted) CholeskyQR passes (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa:
+    // shifted CholeskyQR3): a pass whose Gram is too ill-conditioned for Cholesky uses
+    // G + s·I (s relative to the largest diagonal), which shrinks the condition number
+    // without losing directions; passes repeat until an unshifted pass succeeds after at
+    // least one full pass.  Zero columns (exact breakdown) are replaced by seeded random
+    // directions; when the space is exhausted they stay zero.  SVQB is the last resort.
+    // Returns B (kc x kc, column-major) with W_in ≈ against·(·) + W_out·B.
     std::vector<double> orth(int64_t M, T *W, int kc, const T *against, int na, bool kside) {
         std::vector<double> B((size_t)kc * kc, 0.0);
         for (int i = 0; i < kc; ++i) B[i + (size_t)kc * i] = 1.0;
         std::vector<double> G((size_t)kc * kc), Gh((size_t)kc * kc), E((size_t)kc * kc), lam(kc);
         std::vector<double> S((size_t)kc * kc), Bp((size_t)kc * kc), Bn((size_t)kc * kc), R;
-        for (int pass = 0; pass < 5; ++pass) {
+        const double shift_rel = (sizeof(T) == 4) ? 1e-6 : 1e-13;
+        int refills = 0;
+        for (int pass = 0; pass < 6; ++pass) {
             if (na > 0) cgs(M, W, kc, against, na, kside, nullptr);
             gram(M, W, M, kc, W, M, kc, G.data(), kside);
+            // exact breakdown: columns with (numerically) zero norm
+            std::vector<int> zero;
+            double dmax = 0.0;
+            for (int j = 0; j < kc; ++j) dmax = std::max(dmax, G[j + (size_t)kc * j]);
+            for (int j = 0; j < kc; ++j) {
+                // the absolute test (relative to ||X||) only makes sense on the raw input;
+                // after a pass the columns are normalised and only the relative test applies
+                const double d = std::sqrt(std::max(G[j + (size_t)kc * j], 0.0));
+                const bool tiny_abs = (pass == 0 && refills == 0) && !(d > thr_abs * std::max(anorm, 1e-300));
+                if (tiny_abs || !(d * d > 1e-24 * dmax) || !(dmax > 0.0)) zero.push_back(j);
+            }
+            if (!zero.empty() && refills < 2) {
+                ++refills;
+                for (int j : zero) {
+                    for (int i = 0; i < kc; ++i) B[j + (size_t)kc * i] = 0.0;   // W_in has no component there
+                    fill_normal<T>(M, W + M * j, M, 1, p.seed, 0x5eed0000ull + (sid++), st);
+                }
+                --pass;   // redo the pass with the refreshed columns (bounded by `refills`)
+                continue;
+            }
+            bool shifted = false, ok = cholesky(kc, G.data(), 0.0, thr_chol, R);
+            if (!ok) {
+                ok = cholesky(kc, G.data(), shift_rel * dmax, 1e-300, R);
+                shifted = ok;
+            }
             std::vector<int> bad;
-            if (cholesky(kc, G.data(), R)) {
-                // S = R⁻¹ (upper triangular inverse), Bp = R
-                std::fill(S.begin(), S.end(), 0.0);
-                for (int j = 0; j < kc; ++j) {
-                    S[j + (size_t)kc * j] = 1.0 / R[j + (size_t)kc * j];
-                    for (int i = j - 1; i >= 0; --i) {
-                        double v = 0.0;
-                        for (int t = i + 1; t <= j; ++t) v += R[i + (size_t)kc * t] * S[t + (size_t)kc * j];
-                        S[i + (size_t)kc * j] = -v / R[i + (size_t)kc * i];
-                    }
-                }
+            if (ok) {
+                upper_inverse(kc, R, S);
                 Bp = R;
-            } else {
+            } else {   // SVQB: eigen-decomposition of the column-scaled Gram
                 std::vector<double> d(kc);
-                std::vector<char> good(kc);
-                for (int j = 0; j < kc; ++j) {
-                    d[j] = std::sqrt(std::max(G[j + (size_t)kc * j], 0.0));
-                    good[j] = d[j] > thr_abs * std::max(anorm, 1e-300) && d[j] > 0.0;
-                }
+                for (int j = 0; j < kc; ++j) d[j] = std::sqrt(std::max(G[j + (size_t)kc * j], 0.0));
                 for (int b = 0; b < kc; ++b)
                     for (int a = 0; a < kc; ++a)
-                        Gh[a + (size_t)kc * b] = (good[a] && good[b]) ? G[a + (size_t)kc * b] / (d[a] * d[b]) : 0.0;
+                        Gh[a + (size_t)kc * b] = (d[a] > 0 && d[b] > 0) ? G[a + (size_t)kc * b] / (d[a] * d[b]) : 0.0;
                 sym_eig(kc, Gh.data(), lam.data(), E.data());
                 for (int j = 0; j < kc; ++j) {
-                    const bool ok = lam[j] > thr_rel;
-                    const double isq = ok ? 1.0 / std::sqrt(lam[j]) : 0.0;
-                    const double sq = ok ? std::sqrt(lam[j]) : 0.0;
+                    const bool good = lam[j] > thr_rel;
+                    const double isq = good ? 1.0 / std::sqrt(lam[j]) : 0.0;
+                    const double sq = good ? std::sqrt(lam[j]) : 0.0;
                     for (int a = 0; a < kc; ++a) {
-                        const double dinv = good[a] ? 1.0 / d[a] : 0.0;
-                        S[a + (size_t)kc * j] = dinv * E[a + (size_t)kc * j] * isq;                    // D⁻¹ E Λ^{-1/2}
-                        Bp[j + (size_t)kc * a] = sq * E[a + (size_t)kc * j] * (good[a] ? d[a] : 0.0);  // Λ^{1/2} Eᵀ D
+                        S[a + (size_t)kc * j] = (d[a] > 0 ? 1.0 / d[a] : 0.0) * E[a + (size_t)kc * j] * isq;
+                        Bp[j + (size_t)kc * a] = sq * E[a + (size_t)kc * j] * d[a];
                     }
-                    if (!ok) bad.push_back(j);
+                    if (!good) bad.push_back(j);
                 }
             }
+            if (debug)
+                std::fprintf(stderr, "[ssa] orth M=%lld pass=%d na=%d zero=%zu chol=%d shifted=%d bad=%zu anorm=%.3e\n",
+                             (long long)M, pass, na, zero.size(), (int)ok, (int)shifted, bad.size(), anorm);
             gemm(M, W, M, kc, S.data(), kc, kc, 1.0, 0.0, W, M);   // in place (kc <= 64)
             for (int b = 0; b < kc; ++b)
                 for (int a = 0; a < kc; ++a) {
-                    double s = 0.0;
-                    for (int t = 0; t < kc; ++t) s += Bp[a + (size_t)kc * t] * B[t + (size_t)kc * b];
-                    Bn[a + (size_t)kc * b] = s;
+                    double s2 = 0.0;
+                    for (int t = 0; t < kc; ++t) s2 += Bp[a + (size_t)kc * t] * B[t + (size_t)kc * b];
+                    Bn[a + (size_t)kc * b] = s2;
                 }
             B.swap(Bn);
-            if (bad.empty()) {
-                if (pass >= 1) break;
-                continue;
-            }
-            if (pass >= 3) break;   // space exhausted: those columns stay zero
-            for (int j : bad) fill_normal<T>(M, W + M * j, M, 1, p.seed, 0x5eed0000ull + (sid++), st);
+            if (ok && !shifted && pass >= 1 && bad.empty()) break;
         }
         return B;
     }
@@ -315,7 +346,20 @@ struct Gkl {
             gram(K, W, K, k, W, K, k, G.data(), true);
             for (int j = 0; j < k; ++j) anorm = std::max(anorm, std::sqrt(std::max(G[j + (size_t)k * j], 0.0)));
         }
-        Alast = orth(K, W, k, Q(0), nQ, true);
+        if (full_k_reorth || nQ == 0) {
+            Alast = orth(K, W, k, Q(0), nQ, true);
+        } else {
+            // One-sided reorthogonalisation (Simon & Zha 2000; as in IRLBA): the L side is
+            // kept orthonormal to working precision, so on the K side only the recurrence
+            // term is removed: W -= Qb · T[pc rows, :]ᵀ, whose only nonzero block is the
+            // B of the previous Q block (T row block of P_new), then W is orthonormalised.
+            const int qc = nQ - k;
+            std::vector<double> Bt((size_t)k * k);
+            for (int a = 0; a < k; ++a)
+                for (int b = 0; b < k; ++b) Bt[b + (size_t)k * a] = Tat(pc + a, qc + b);   // (T block)ᵀ
+            gemm(K, Q(qc), K, k, Bt.data(), k, k, -1.0, 1.0, W, K);
+            Alast = orth(K, W, k, nullptr, 0, true);
+        }
         nQ += k;
     }
 
@@ -367,12 +411,17 @@ struct Gkl {
             }
         }
         if (!done) svd_jacobi(m, n, Tm.data(), ldT, th.data(), Y.data(), Z.data());
-        ms_ritz += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        const double dt = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        ms_ritz += dt;
+        if (debug) std::fprintf(stderr, "[ssa] ritz_svd %dx%d %s %.3f ms\n", m, n, done ? "device" : "host", dt);
     }
 
     void run(int r_, ssa_decomp_info *info) {
         r = r_;
         const int64_t mn = std::min(L, K);
+        // one-sided reorthogonalisation (K side: recurrence term only) is experimental:
+        // with thick restarts it costs many more products, so full reorth is the default
+        full_k_reorth = (K < L) || std::getenv("SSA_ONESIDED") == nullptr;
         k = std::max(1, std::min<int>(p.block_k, 64));
         if (k > mn) k = (int)mn;
         pk = (int)std::min<int64_t>(r + std::max(4, k / 2), mn);
@@ -419,6 +468,15 @@ struct Gkl {
             for (int i = 0; i < std::min(r, nc); ++i) {
                 maxres = std::max(maxres, res[i] / th[0]);
                 if (res[i] <= tol * th[0]) ++nconv;
+            }
+            if (debug) {
+                double an = 0, bn = 0;
+                for (double v : Alast) an += v * v;
+                for (int b = 0; b < nc; ++b)
+                    for (int a = nP - k; a < nP; ++a) bn += Tat(a, b) * Tat(a, b);
+                std::fprintf(stderr, "[ssa] ritz nP=%d nc=%d prod=%lld th0=%.6e th[r-1]=%.6e res0=%.3e resr=%.3e |Alast|=%.3e |Tlast|=%.3e conv=%d\n",
+                             nP, nc, (long long)nblock, th[0], th[std::min(r, nc) - 1], res[0] / th[0],
+                             res[std::min(r, nc) - 1] / th[0], std::sqrt(an), std::sqrt(bn), nconv);
             }
             const bool done = (nconv >= r) || (nblock >= maxprod);
             if (done) {

@@ -15,7 +15,7 @@ def summarize(path, top=25):
             continue
         name = r[ki].split('(')[0][:70]
         v = float(r[mi].replace(',', ''))
-        v *= {'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3}.get(r[ui], 1.0)
+        v *= {'ns': 1e-3, 'nsecond': 1e-3, 'us': 1.0, 'usecond': 1.0, 'ms': 1e3, 'msecond': 1e3}.get(r[ui], 1.0)
         agg[name][0] += 1
         agg[name][1] += v
     tot = sum(v[1] for v in agg.values())

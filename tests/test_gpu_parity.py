@@ -185,6 +185,32 @@ def test_products_closed_form_c3_twin(path):
     assert relfro(p.matmul(U, transpose=True), Vcf) <= 2e-5
 
 
+def test_products_closed_form_c5_twin_sampled():
+    """P5 at the c5 size (4096², window 256², K ≈ 14.75M, k = 64), FFT path: sampled
+    output entries of both products against the separable closed form."""
+    w = synth.config5(noise=False)
+    p = _plan(w, path="fft")
+    import torch
+    rng = np.random.default_rng(5)
+    k = 64
+    V = torch.randn(p.K, k, device="cuda", dtype=torch.float32, generator=torch.Generator("cuda").manual_seed(1))
+    U = torch.randn(p.L, k, device="cuda", dtype=torch.float32, generator=torch.Generator("cuda").manual_seed(2))
+    Ug = p.matmul(V)[:, :4].double().cpu().numpy()
+    Vrows = rng.choice(p.K, 4096, replace=False)
+    Vg = p.matmul(U, transpose=True)[torch.as_tensor(Vrows, device="cuda")][:, :4].double().cpu().numpy()
+    lx, ly = np.meshgrid(np.arange(256), np.arange(256), indexing="ij")
+    lpos = (lx.reshape(-1, order="F"), ly.reshape(-1, order="F"))
+    kpos_all = (np.arange(p.K) % 3841, np.arange(p.K) // 3841)
+    Vh = V[:, :4].double().cpu().numpy()
+    Uh = U[:, :4].double().cpu().numpy()
+    Ucf = cf.products(w.terms, lpos, kpos_all, V=Vh)
+    Vcf = cf.products(w.terms, lpos, (kpos_all[0][Vrows], kpos_all[1][Vrows]), U=Uh)
+    # image values reach ~1e7 here (e^{±8} per axis): fp32 input rounding and fp32 FFT
+    # rounding are both relative to the largest entries
+    assert relfro(Ug, Ucf) <= 2e-5
+    assert relfro(Vg, Vcf) <= 2e-5
+
+
 # ---------------------------------------------------------------- decomposition + reconstruction
 def _relgaps(s_all, r):
     s = np.asarray(s_all, np.float64)
@@ -312,6 +338,19 @@ def test_c3_noiseless_closed_form(path):
     x = _oracle_input(w, "f32")
     assert relfro(rec, x) <= 1e-4
     assert info["n_block_products"] > 0
+
+
+def test_c5_noiseless_closed_form_sigma():
+    """P7 at the full c5 size (4096², window 256², K ≈ 14.75M, r = 50, k = 64): σ of the
+    noiseless twin against the closed form, with reading Q10's floor for fp32 products."""
+    w = synth.config5(noise=False)
+    p = _plan(w, path="fft")
+    p.decompose(50, allow_not_converged=True)
+    s = p.sigma
+    s_cf = np.concatenate([cf.sigma_rect(w.terms, 256, 256, 3841, 3841), np.zeros(8)])
+    assert cf.rank(w.terms) == 48
+    checked = check_sigma(s, s_cf, 50, tau=1e-5)
+    assert checked >= 8
 
 
 def test_wcor_diag_and_symmetry():
