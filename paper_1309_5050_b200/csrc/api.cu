@@ -259,7 +259,7 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
                                        (size_t)64 * p.lx * p.ly * (size_t)kmax * sizeof(T));
     p.ws_corr_bytes = std::max(p.ws_corr_bytes, (size_t)p.lx * p.ly * (size_t)kmax * sizeof(T) * 2);
     p.ws_corr.alloc(p.ws_corr_bytes, st);
-    p.ws_gram.alloc(gram_partial_bytes(std::max<int64_t>({p.L, p.K, nxy}), 64, 64), st);
+    p.ws_gram.alloc(gram_partial_bytes(std::max<int64_t>({p.L, p.K, nxy}), 512, 64), st);
     // product path
     if (p.path == SSA_PATH_FFT || p.path == SSA_PATH_AUTO) {
         if (fft_supported(p)) {

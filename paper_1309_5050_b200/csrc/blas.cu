@@ -26,6 +26,9 @@ gram_tn_kernel(int64_t M, const T *__restrict__ A, int64_t lda, int n1,
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) accd[a][b] = 0.0;
+    // grid.y selects a 64-column chunk of A (one launch for up to 64*gridDim.y columns)
+    A += lda * 64 * (int64_t)blockIdx.y;
+    n1 = min(64, n1 - 64 * (int)blockIdx.y);
     const bool active = (4 * ti < n1) && (4 * tj < n2);
     for (int64_t r0 = (int64_t)blockIdx.x * kGramRows; r0 < M; r0 += (int64_t)gridDim.x * kGramRows) {
         __syncthreads();
@@ -64,7 +67,7 @@ gram_tn_kernel(int64_t M, const T *__restrict__ A, int64_t lda, int n1,
         }
     }
     if (!active) return;
-    double *out = partials + (int64_t)blockIdx.x * 64 * 64;
+    double *out = partials + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 64 * 64;
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -78,8 +81,10 @@ __global__ void gram_reduce_kernel(const double *__restrict__ partials, int npar
     const int e = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (e >= n1 * n2) return;
     const int a = e % n1, b = e / n1;
+    const double *base = partials + (int64_t)(a / 64) * nparts * 4096;
+    const int al = a % 64;
     double s = 0.0;
-    for (int q = lane; q < nparts; q += 32) s += partials[(int64_t)q * 4096 + a + 64 * b];
+    for (int q = lane; q < nparts; q += 32) s += base[(int64_t)q * 4096 + al + 64 * b];
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) G[a + (int64_t)n1 * b] = s;
@@ -89,15 +94,18 @@ static int gram_ctas(int64_t M) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, 64), 2 * (int64_t)num_sms()));
 }
 
-size_t gram_partial_bytes(int64_t M, int, int) { return (size_t)gram_ctas(M) * 4096 * sizeof(double); }
+size_t gram_partial_bytes(int64_t M, int n1, int) {
+    return (size_t)gram_ctas(M) * 4096 * sizeof(double) * (size_t)cdiv(std::max(n1, 64), 64);
+}
 
 template <typename T>
 void gram_tn(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb, int n2,
              double *G, double *partials, size_t partial_bytes, cudaStream_t st) {
-    SSA_REQUIRE(n1 <= 64 && n2 <= 64, SSA_ERR_ARG, "gram_tn: at most 64 columns per call");
+    SSA_REQUIRE(n2 <= 64 && n1 <= 512, SSA_ERR_ARG, "gram_tn: at most 512 x 64 per call");
     const int ctas = gram_ctas(M);
-    SSA_REQUIRE((size_t)ctas * 4096 * sizeof(double) <= partial_bytes, SSA_ERR_ARG, "gram_tn: workspace");
-    gram_tn_kernel<T><<<ctas, 256, 0, st>>>(M, A, lda, n1, B, ldb, n2, partials);
+    const int ych = (int)cdiv(n1, 64);
+    SSA_REQUIRE((size_t)ctas * 4096 * sizeof(double) * ych <= partial_bytes, SSA_ERR_ARG, "gram_tn: workspace");
+    gram_tn_kernel<T><<<dim3(ctas, ych), 256, 0, st>>>(M, A, lda, n1, B, ldb, n2, partials);
     after_launch("gram_tn");
     gram_reduce_kernel<<<(unsigned)cdiv((int64_t)n1 * n2 * 32, 256), 256, 0, st>>>(partials, ctas, n1, n2, G);
     after_launch("gram_reduce");
@@ -164,6 +172,67 @@ template void gemm_small<float>(int64_t, const float *, int64_t, int, const doub
                                 double, float *, int64_t, cudaStream_t);
 template void gemm_small<double>(int64_t, const double *, int64_t, int, const double *, int, int, double,
                                  double, double *, int64_t, cudaStream_t);
+
+// Out (M x n) = beta*Out + alpha * A (M x m) * C (m x n); m <= 512, n <= 64, Out != A.
+// Thread per row: A streamed in 16-column chunks (one read of A), all n outputs in registers.
+template <typename T, int NMAX>
+__global__ void __launch_bounds__(128)
+gemm_acc_kernel(int64_t M, const T *__restrict__ A, int64_t lda, int m, const double *__restrict__ C, int ldc,
+                int n, double alpha, double beta, T *__restrict__ Out, int64_t ldo) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *CS = reinterpret_cast<T *>(smem_raw);   // [m][NMAX]
+    for (int idx = threadIdx.x; idx < m * NMAX; idx += blockDim.x) {
+        const int a = idx / NMAX, b = idx % NMAX;
+        CS[idx] = (b < n) ? (T)(alpha * C[a + (int64_t)ldc * b]) : T(0);
+    }
+    __syncthreads();
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= M) return;
+    T acc[NMAX];
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) acc[j] = T(0);
+    for (int c0 = 0; c0 < m; c0 += 16) {
+        T a[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) a[t] = (c0 + t < m) ? A[row + lda * (c0 + t)] : T(0);
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            if (c0 + t >= m) break;
+            const T *cr = CS + (c0 + t) * NMAX;
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) acc[j] = fma(a[t], cr[j], acc[j]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+        if (j < n) {
+            T *o = Out + row + ldo * j;
+            *o = (beta == 0.0) ? acc[j] : fma((T)beta, *o, acc[j]);
+        }
+    }
+}
+
+template <typename T>
+void gemm_acc(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
+              double beta, T *Out, int64_t ldo, cudaStream_t st) {
+    SSA_REQUIRE(m <= 512 && n <= 64, SSA_ERR_ARG, "gemm_acc: at most 512 x 64");
+    if (M <= 0 || n <= 0) return;
+    const unsigned grid = (unsigned)cdiv(M, 128);
+    if (n <= 32) {
+        const size_t smem = sizeof(T) * (size_t)m * 32;
+        SSA_CUDA(cudaFuncSetAttribute(gemm_acc_kernel<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        gemm_acc_kernel<T, 32><<<grid, 128, smem, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
+    } else {
+        const size_t smem = sizeof(T) * (size_t)m * 64;
+        SSA_CUDA(cudaFuncSetAttribute(gemm_acc_kernel<T, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        gemm_acc_kernel<T, 64><<<grid, 128, smem, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
+    }
+    after_launch("gemm_acc");
+}
+template void gemm_acc<float>(int64_t, const float *, int64_t, int, const double *, int, int, double, double,
+                              float *, int64_t, cudaStream_t);
+template void gemm_acc<double>(int64_t, const double *, int64_t, int, const double *, int, int, double, double,
+                               double *, int64_t, cudaStream_t);
 
 // ---- counter-based normal generator (splitmix64 + Box-Muller) -------------
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {

@@ -11,6 +11,7 @@
 #include "kernels.h"
 
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 namespace ssa {
 
@@ -138,7 +139,145 @@ jacobi_block_kernel(int m, int n, int nb, double *__restrict__ A, float tol, int
     if (c == 0 && tid == 0 && sweeps_out) *sweeps_out = sweep + 1;
 }
 
+// ---------------------------------------------------------------------------
+// Cluster variant (n <= 32·BW): the nb/2 CTAs of ONE thread-block cluster keep the
+// column blocks in shared memory for the whole factorisation.  With the circle
+// method, the transition from round t to t+1 is a systolic shift: CTA c's "+c" block
+// goes to CTA c-1, its "-c" block to CTA c+1 (CTA 0 keeps block nb-1; the last CTA
+// turns its "-c" block into its "+c" block).  Blocks are pushed into the neighbours'
+// next-round buffers through distributed shared memory and a cluster barrier replaces
+// the grid synchronisation (no global-memory round trip per round).
+// ---------------------------------------------------------------------------
+template <int MR, int BW>
+__global__ void __launch_bounds__(32 * BW, 1)
+jacobi_cluster_kernel(int m, int n, int nb, double *__restrict__ A, float tol, int max_sweeps,
+                      int *__restrict__ sweeps_out) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) double SM[];
+    __shared__ int flags[2];
+    const int ldc = m | 1;
+    const int blk = ldc * BW;                          // doubles per column block
+    double *buf[2] = {SM, SM + 2 * blk};                // [2 buffers][slot A | slot B]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = (int)cluster.block_rank(), ncta = nb / 2;
+    constexpr int NP = 2 * BW;
+    // initial blocks (round 0): CTA 0 -> (0, nb-1); CTA c -> (c, (nb-1-c) mod (nb-1))
+    {
+        const int ba = (c == 0) ? 0 : c % (nb - 1);
+        const int bb = (c == 0) ? nb - 1 : (nb - 1 - c) % (nb - 1);
+        for (int h = 0; h < 2; ++h) {
+            const int b = h ? bb : ba;
+            for (int idx = tid; idx < BW * m; idx += blockDim.x) {
+                const int jl = idx / m, i = idx - jl * m;
+                const int col = b * BW + jl;
+                buf[0][h * blk + i + ldc * jl] = col < n ? A[i + (int64_t)m * col] : 0.0;
+            }
+        }
+    }
+    if (tid == 0) { flags[0] = 0; flags[1] = 0; }
+    cluster.sync();
+    int cur = 0, t = 0, sweep = 0;
+    for (; sweep < max_sweeps; ++sweep) {
+        int rot = 0;
+        for (int round = 0; round < nb - 1; ++round, ++t) {
+            double *C = buf[cur];
+            // one inner sweep over the 2·BW columns held by this CTA
+            for (int ir = 0; ir < NP - 1; ++ir) {
+                int p, q;
+                if (warp == 0) { p = ir; q = NP - 1; }
+                else { p = (ir + warp) % (NP - 1); q = (ir - warp + (NP - 1)) % (NP - 1); }
+                if (jacobi_pair<MR>(C + ldc * p, C + ldc * q, m, lane, tol)) rot = 1;
+                __syncthreads();
+            }
+            // systolic shift into the neighbours' next buffers
+            double *nxt_local = buf[cur ^ 1];
+            if (ncta == 1) {
+                // single CTA: nothing moves
+                for (int idx = tid; idx < 2 * blk; idx += blockDim.x) nxt_local[idx] = C[idx];
+            } else {
+                double *dstA = nullptr, *dstB = nullptr;   // where my slot A / slot B go
+                int offA = 0, offB = 0;
+                if (c == 0) {
+                    dstA = cluster.map_shared_rank(buf[cur ^ 1], 1); offA = blk;    // -> CTA 1 slot B
+                    dstB = nxt_local; offB = blk;                                    // stays in slot B
+                } else {
+                    dstA = cluster.map_shared_rank(buf[cur ^ 1], c - 1); offA = 0;   // -> CTA c-1 slot A
+                    if (c + 1 < ncta) { dstB = cluster.map_shared_rank(buf[cur ^ 1], c + 1); offB = blk; }
+                    else { dstB = nxt_local; offB = 0; }                            // last CTA: B -> own A
+                }
+                for (int idx = tid; idx < blk; idx += blockDim.x) {
+                    dstA[offA + idx] = C[idx];
+                    dstB[offB + idx] = C[blk + idx];
+                }
+            }
+            cluster.sync();
+            cur ^= 1;
+        }
+        // sweep convergence: any CTA rotated?  (flags alternate with sweep parity)
+        if (__syncthreads_or(rot) && tid == 0) atomicOr(cluster.map_shared_rank(&flags[sweep & 1], 0), 1);
+        cluster.sync();
+        const int any = *cluster.map_shared_rank(&flags[sweep & 1], 0);
+        if (c == 0 && tid == 0) flags[(sweep + 1) & 1] = 0;
+        cluster.sync();
+        if (!any) break;
+    }
+    // write back: blocks held at round t
+    {
+        const int tt = t % (nb - 1);
+        const int ba = (c == 0) ? tt : (tt + c) % (nb - 1);
+        const int bb = (c == 0) ? nb - 1 : (tt - c + (nb - 1)) % (nb - 1);
+        for (int h = 0; h < 2; ++h) {
+            const int b = h ? bb : ba;
+            for (int idx = tid; idx < BW * m; idx += blockDim.x) {
+                const int jl = idx / m, i = idx - jl * m;
+                const int col = b * BW + jl;
+                if (col < n) A[i + (int64_t)m * col] = buf[cur][h * blk + i + ldc * jl];
+            }
+        }
+    }
+    if (c == 0 && tid == 0 && sweeps_out) *sweeps_out = sweep + 1;
+}
+
+template <int MR, int BW>
+static bool launch_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st) {
+    int nb = (int)cdiv(n, BW);
+    nb += nb & 1;
+    if (nb < 2) nb = 2;
+    const int ncta = nb / 2;
+    if (ncta > 16) return false;
+    const size_t smem = sizeof(double) * (size_t)(m | 1) * BW * 4;
+    if (smem > 200 * 1024) return false;
+    auto kern = jacobi_cluster_kernel<MR, BW>;
+    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (ncta > 8) SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ncta);
+    cfg.blockDim = dim3(32 * BW);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ncta; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr; cfg.numAttrs = 1;
+    float tol = 1e-12f;
+    int max_sweeps = 60;
+    SSA_CUDA(cudaLaunchKernelEx(&cfg, kern, m, n, nb, T, tol, max_sweeps, sweeps));
+    after_launch("jacobi_cluster");
+    return true;
+}
+
+// prefer the cluster kernel; fall back to the cooperative-grid kernel for large n
+static bool jacobi_try_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st) {
+    if (std::getenv("SSA_JACOBI_GRID")) return false;
+    if (m <= 128) return n <= 256 ? launch_cluster<4, 8>(m, n, T, sweeps, st) : launch_cluster<4, 16>(m, n, T, sweeps, st);
+    if (m <= 256) return n <= 256 ? launch_cluster<8, 8>(m, n, T, sweeps, st) : launch_cluster<8, 16>(m, n, T, sweeps, st);
+    if (m <= 512) return n <= 256 ? launch_cluster<16, 8>(m, n, T, sweeps, st) : launch_cluster<16, 16>(m, n, T, sweeps, st);
+    return false;
+}
+
 void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st) {
+    if (jacobi_try_cluster(m, n, T, sweeps, st)) return;
     int nb = (int)cdiv(n, kBW);
     nb += nb & 1;
     if (nb < 2) nb = 2;

@@ -45,7 +45,7 @@ void diagsums_direct(AvgParams<T> P, cudaStream_t st);
 struct FftPlan;   // opaque, defined in fft.cu
 
 // ---- small dense / tall-skinny helpers (blas.cu) -------------------------
-// G (n1 x n2, column-major, double, device) = Aᵀ B with A: M x n1, B: M x n2.
+// G (n1 x n2, column-major, double, device) = Aᵀ B with A: M x n1 (n1 <= 512), B: M x n2 (n2 <= 64).
 template <typename T>
 void gram_tn(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb, int n2,
              double *G, double *partials, size_t partial_bytes, cudaStream_t st);
@@ -56,6 +56,11 @@ size_t gram_partial_bytes(int64_t M, int n1, int n2);
 template <typename T>
 void gemm_small(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n,
                 double alpha, double beta, T *Out, int64_t ldo, cudaStream_t st);
+
+// Out (M x n) = beta*Out + alpha * A (M x m) * C (m x n); m <= 512, n <= 64, Out != A (one launch).
+template <typename T>
+void gemm_acc(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
+              double beta, T *Out, int64_t ldo, cudaStream_t st);
 
 // A[:, cols] = N(0,1) from a counter-based generator keyed by (seed, stream_id).
 template <typename T>

@@ -91,7 +91,7 @@ struct Gkl {
     std::vector<double> Alast;
     double anorm = 0.0;
     double ms_ritz = 0.0;
-    int64_t nblock = 0, nvec = 0;
+    int64_t nblock = 0, nvec = 0, n_cgs = 0;
     uint64_t sid = 1;
     double thr_abs, thr_rel, thr_chol;
     bool gpu_ritz = true;
@@ -110,12 +110,12 @@ struct Gkl {
 
     bool kside_comm() const { return p.has_comm && p.comm.world > 1; }
 
-    // G (n1 x n2, host, column-major ld n1) = Aᵀ B; chunked by 64 columns, one sync.
+    // G (n1 x n2, host, column-major ld n1) = Aᵀ B; one launch per 512 x 64 chunk, one sync.
     void gram(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb, int n2, double *G, bool kside) {
         struct Chunk { int a0, na, b0, nb; size_t idx; };
         std::vector<Chunk> ch;
-        for (int a0 = 0; a0 < n1; a0 += 64) {
-            const int na = std::min(64, n1 - a0);
+        for (int a0 = 0; a0 < n1; a0 += 512) {
+            const int na = std::min(512, n1 - a0);
             for (int b0 = 0; b0 < n2; b0 += 64) {
                 const int nb = std::min(64, n2 - b0);
                 const size_t idx = sg.take((size_t)na * nb);
@@ -138,19 +138,26 @@ struct Gkl {
     }
 
     // Out[:, 0:n] = beta*Out + alpha * A[:, 0:m] * C (C: m x n host, ld ldc); no sync.
+    // Not in place: one gemm_acc launch per 512 x 64 chunk; in place (Out == A, m = n <= 64): gemm_small.
     void gemm(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha, double beta,
               T *Out, int64_t ldo) {
+        const bool inplace = (Out == A);
+        const int mstep = inplace ? 64 : 512;
         for (int c0 = 0; c0 < n; c0 += 64) {
             const int nc = std::min(64, n - c0);
-            for (int m0 = 0; m0 < m; m0 += 64) {
-                const int mc = std::min(64, m - m0);
-                const size_t idx = sg.take((size_t)64 * nc);
+            for (int m0 = 0; m0 < m; m0 += mstep) {
+                const int mc = std::min(mstep, m - m0);
+                const size_t idx = sg.take((size_t)mc * nc);
                 double *h = sg.h + idx;
                 for (int b = 0; b < nc; ++b)
-                    for (int a = 0; a < mc; ++a) h[a + 64 * b] = C[(m0 + a) + (int64_t)ldc * (c0 + b)];
-                SSA_CUDA(cudaMemcpyAsync(sg.dev(idx), h, sizeof(double) * 64 * nc, cudaMemcpyHostToDevice, st));
-                gemm_small<T>(M, A + lda * m0, lda, mc, sg.dev(idx), 64, nc, alpha, (m0 == 0) ? beta : 1.0,
-                              Out + ldo * c0, ldo, st);
+                    for (int a = 0; a < mc; ++a) h[a + (size_t)mc * b] = C[(m0 + a) + (int64_t)ldc * (c0 + b)];
+                SSA_CUDA(cudaMemcpyAsync(sg.dev(idx), h, sizeof(double) * mc * nc, cudaMemcpyHostToDevice, st));
+                if (inplace)
+                    gemm_small<T>(M, A + lda * m0, lda, mc, sg.dev(idx), mc, nc, alpha, (m0 == 0) ? beta : 1.0,
+                                  Out + ldo * c0, ldo, st);
+                else
+                    gemm_acc<T>(M, A + lda * m0, lda, mc, sg.dev(idx), mc, nc, alpha, (m0 == 0) ? beta : 1.0,
+                                Out + ldo * c0, ldo, st);
             }
         }
     }
@@ -207,16 +214,43 @@ struct Gkl {
     // least one full pass.  Zero columns (exact breakdown) are replaced by seeded random
     // directions; when the space is exhausted they stay zero.  SVQB is the last resort.
     // Returns B (kc x kc, column-major) with W_in ≈ against·(·) + W_out·B.
-    std::vector<double> orth(int64_t M, T *W, int kc, const T *against, int na, bool kside) {
+    std::vector<double> orth(int64_t M, T *W, int kc, const T *against, int na, bool kside,
+                             double *coef = nullptr) {
         std::vector<double> B((size_t)kc * kc, 0.0);
         for (int i = 0; i < kc; ++i) B[i + (size_t)kc * i] = 1.0;
         std::vector<double> G((size_t)kc * kc), Gh((size_t)kc * kc), E((size_t)kc * kc), lam(kc);
         std::vector<double> S((size_t)kc * kc), Bp((size_t)kc * kc), Bn((size_t)kc * kc), R;
         const double shift_rel = (sizeof(T) == 4) ? 1e-6 : 1e-13;
+        // ---- projection against the basis: one CGS pass, a second only when DGKS asks
+        // (||w_after||² < ½||w_before||², with ||w_before||² = ||c||² + ||w_after||²)
+        auto project = [&](bool force_twice) {
+            std::vector<double> C((size_t)na * kc);
+            gram(M, against, M, na, W, M, kc, C.data(), kside);
+            gemm(M, against, M, na, C.data(), na, kc, -1.0, 1.0, W, M);
+            if (coef)
+                for (size_t t = 0; t < C.size(); ++t) coef[t] += C[t];
+            gram(M, W, M, kc, W, M, kc, G.data(), kside);
+            bool need = force_twice;
+            for (int j = 0; j < kc && !need; ++j) {
+                double c2 = 0.0;
+                for (int a2 = 0; a2 < na; ++a2) c2 += C[a2 + (size_t)na * j] * C[a2 + (size_t)na * j];
+                need = c2 > G[j + (size_t)kc * j];
+            }
+            if (need) {
+                gram(M, against, M, na, W, M, kc, C.data(), kside);
+                gemm(M, against, M, na, C.data(), na, kc, -1.0, 1.0, W, M);
+                if (coef)
+                    for (size_t t = 0; t < C.size(); ++t) coef[t] += C[t];
+                gram(M, W, M, kc, W, M, kc, G.data(), kside);
+            }
+            n_cgs += need ? 2 : 1;
+        };
+        bool have_gram = false;
+        if (na > 0) { project(false); have_gram = true; }
         int refills = 0;
         for (int pass = 0; pass < 6; ++pass) {
-            if (na > 0) cgs(M, W, kc, against, na, kside, nullptr);
-            gram(M, W, M, kc, W, M, kc, G.data(), kside);
+            if (!have_gram) gram(M, W, M, kc, W, M, kc, G.data(), kside);
+            have_gram = false;
             // exact breakdown: columns with (numerically) zero norm
             std::vector<int> zero;
             double dmax = 0.0;
@@ -234,6 +268,13 @@ struct Gkl {
                     for (int i = 0; i < kc; ++i) B[j + (size_t)kc * i] = 0.0;   // W_in has no component there
                     fill_normal<T>(M, W + M * j, M, 1, p.seed, 0x5eed0000ull + (sid++), st);
                 }
+                if (na > 0) {
+                    double *keep = coef;
+                    coef = nullptr;            // the random directions are not part of W_in
+                    project(true);
+                    coef = keep;
+                    have_gram = true;
+                }
                 --pass;   // redo the pass with the refreshed columns (bounded by `refills`)
                 continue;
             }
@@ -249,17 +290,17 @@ struct Gkl {
             } else {   // SVQB: eigen-decomposition of the column-scaled Gram
                 std::vector<double> d(kc);
                 for (int j = 0; j < kc; ++j) d[j] = std::sqrt(std::max(G[j + (size_t)kc * j], 0.0));
-                for (int b = 0; b < kc; ++b)
-                    for (int a = 0; a < kc; ++a)
-                        Gh[a + (size_t)kc * b] = (d[a] > 0 && d[b] > 0) ? G[a + (size_t)kc * b] / (d[a] * d[b]) : 0.0;
+                for (int b2 = 0; b2 < kc; ++b2)
+                    for (int a2 = 0; a2 < kc; ++a2)
+                        Gh[a2 + (size_t)kc * b2] = (d[a2] > 0 && d[b2] > 0) ? G[a2 + (size_t)kc * b2] / (d[a2] * d[b2]) : 0.0;
                 sym_eig(kc, Gh.data(), lam.data(), E.data());
                 for (int j = 0; j < kc; ++j) {
                     const bool good = lam[j] > thr_rel;
                     const double isq = good ? 1.0 / std::sqrt(lam[j]) : 0.0;
                     const double sq = good ? std::sqrt(lam[j]) : 0.0;
-                    for (int a = 0; a < kc; ++a) {
-                        S[a + (size_t)kc * j] = (d[a] > 0 ? 1.0 / d[a] : 0.0) * E[a + (size_t)kc * j] * isq;
-                        Bp[j + (size_t)kc * a] = sq * E[a + (size_t)kc * j] * d[a];
+                    for (int a2 = 0; a2 < kc; ++a2) {
+                        S[a2 + (size_t)kc * j] = (d[a2] > 0 ? 1.0 / d[a2] : 0.0) * E[a2 + (size_t)kc * j] * isq;
+                        Bp[j + (size_t)kc * a2] = sq * E[a2 + (size_t)kc * j] * d[a2];
                     }
                     if (!good) bad.push_back(j);
                 }
@@ -268,11 +309,11 @@ struct Gkl {
                 std::fprintf(stderr, "[ssa] orth M=%lld pass=%d na=%d zero=%zu chol=%d shifted=%d bad=%zu anorm=%.3e\n",
                              (long long)M, pass, na, zero.size(), (int)ok, (int)shifted, bad.size(), anorm);
             gemm(M, W, M, kc, S.data(), kc, kc, 1.0, 0.0, W, M);   // in place (kc <= 64)
-            for (int b = 0; b < kc; ++b)
-                for (int a = 0; a < kc; ++a) {
+            for (int b2 = 0; b2 < kc; ++b2)
+                for (int a2 = 0; a2 < kc; ++a2) {
                     double s2 = 0.0;
-                    for (int t = 0; t < kc; ++t) s2 += Bp[a + (size_t)kc * t] * B[t + (size_t)kc * b];
-                    Bn[a + (size_t)kc * b] = s2;
+                    for (int t = 0; t < kc; ++t) s2 += Bp[a2 + (size_t)kc * t] * B[t + (size_t)kc * b2];
+                    Bn[a2 + (size_t)kc * b2] = s2;
                 }
             B.swap(Bn);
             if (ok && !shifted && pass >= 1 && bad.empty()) break;
@@ -321,17 +362,17 @@ struct Gkl {
         const int qc = nQ - k;
         T *W = P(nP);
         product_xv(Q(qc), W, k);
-        std::vector<double> C((size_t)nP * k, 0.0);
-        cgs(L, W, k, P(0), nP, false, C.data());
-        cgs(L, W, k, P(0), nP, false, C.data());
-        for (int b = 0; b < k; ++b)
-            for (int a = 0; a < nP; ++a) Tat(a, qc + b) = C[a + (size_t)nP * b];
         if (anorm == 0.0) {
             std::vector<double> G((size_t)k * k);
             gram(L, W, L, k, W, L, k, G.data(), false);
             for (int j = 0; j < k; ++j) anorm = std::max(anorm, std::sqrt(std::max(G[j + (size_t)k * j], 0.0)));
         }
-        std::vector<double> B = orth(L, W, k, P(0), nP, false);
+        // full projection onto the L basis; all CGS coefficients go into T so that
+        // X·Qb = Pb·T holds exactly
+        std::vector<double> C((size_t)nP * k, 0.0);
+        std::vector<double> B = orth(L, W, k, P(0), nP, false, C.data());
+        for (int b = 0; b < k; ++b)
+            for (int a = 0; a < nP; ++a) Tat(a, qc + b) = C[a + (size_t)nP * b];
         for (int b = 0; b < k; ++b)
             for (int a = 0; a < k; ++a) Tat(nP + a, qc + b) = B[a + (size_t)k * b];
         nP += k;
@@ -346,20 +387,17 @@ struct Gkl {
             gram(K, W, K, k, W, K, k, G.data(), true);
             for (int j = 0; j < k; ++j) anorm = std::max(anorm, std::sqrt(std::max(G[j + (size_t)k * j], 0.0)));
         }
-        if (full_k_reorth || nQ == 0) {
-            Alast = orth(K, W, k, Q(0), nQ, true);
-        } else {
-            // One-sided reorthogonalisation (Simon & Zha 2000; as in IRLBA): the L side is
-            // kept orthonormal to working precision, so on the K side only the recurrence
-            // term is removed: W -= Qb · T[pc rows, :]ᵀ, whose only nonzero block is the
-            // B of the previous Q block (T row block of P_new), then W is orthonormalised.
+        if (nQ > 0) {
+            // remove the recurrence term first (W -= Q_prev·Bᵀ with B = T[P_new, Q_prev], known
+            // exactly), so that the full projection below only removes rounding-level
+            // components and one CGS pass normally suffices (DGKS test in orth)
             const int qc = nQ - k;
             std::vector<double> Bt((size_t)k * k);
             for (int a = 0; a < k; ++a)
                 for (int b = 0; b < k; ++b) Bt[b + (size_t)k * a] = Tat(pc + a, qc + b);   // (T block)ᵀ
             gemm(K, Q(qc), K, k, Bt.data(), k, k, -1.0, 1.0, W, K);
-            Alast = orth(K, W, k, nullptr, 0, true);
         }
+        Alast = orth(K, W, k, full_k_reorth ? Q(0) : nullptr, full_k_reorth ? nQ : 0, true);
         nQ += k;
     }
 
@@ -424,9 +462,12 @@ struct Gkl {
         full_k_reorth = (K < L) || std::getenv("SSA_ONESIDED") == nullptr;
         k = std::max(1, std::min<int>(p.block_k, 64));
         if (k > mn) k = (int)mn;
-        pk = (int)std::min<int64_t>(r + std::max(4, k / 2), mn);
+        int extra = std::max(k / 2, r);        // keep ~2r Ritz pairs (parameter sweep)
+        if (const char *e = std::getenv("SSA_PK_EXTRA")) extra = std::atoi(e);
+        pk = (int)std::min<int64_t>(r + extra, mn);
         // blocks per restart cycle (the projected SVD runs on the device for n up to ~2000)
-        int mcyc = std::max(3, (int)cdiv(2 * pk, k));
+        int mcyc = 4;
+        if (const char *e = std::getenv("SSA_MCYC")) mcyc = std::max(1, std::atoi(e));
         while (mcyc > 2 && !jacobi_blocked_fits(pk + (mcyc + 1) * k, pk + mcyc * k)) --mcyc;
         nQmax = pk + k * (mcyc + 1);
         ldT = nQmax;
