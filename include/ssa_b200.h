@@ -70,7 +70,9 @@ typedef enum { SSA_F32 = 0, SSA_F64 = 1 } ssa_dtype;
 typedef enum {
     SSA_PATH_AUTO = 0,
     SSA_PATH_DIRECT = 1,   /* smem-tiled implicit GEMM on CUDA cores (Hankel sliding window) */
-    SSA_PATH_FFT = 2       /* shared-memory radix FFT circular correlation (Alg. 1/3) */
+    SSA_PATH_FFT = 2,      /* shared-memory radix FFT circular correlation (Alg. 1/3) */
+    SSA_PATH_TC = 3        /* tcgen05 tensor-core implicit GEMM, 3xTF32 split (fp32 plans; products
+                              whose output box has < 96 rows fall back to FFT / direct) */
 } ssa_path;
 
 typedef struct {
@@ -111,9 +113,10 @@ typedef struct {
     int64_t L, K;                     /* |𝔏|, |𝔎| */
     int64_t n_valid;                  /* |𝔑| */
     int64_t n_excluded;               /* |𝔑 \ 𝔑′| (cells that enter no window) */
-    int path;                         /* path chosen for the products */
+    int path;                         /* path chosen for X·V (kept for compatibility) */
     int dtype;
     int full_window, full_kshape;     /* 1 if 𝔏 / 𝔎 are full rectangles (trivial-mask fast path) */
+    int path_xv, path_xtu;            /* ssa_path chosen for X·V and for Xᵀ·U (AUTO: measured per shape) */
 } ssa_plan_info_t;
 
 typedef struct {

@@ -14,7 +14,7 @@ SSA_OK = 0
 STATUS = {0: "SSA_OK", 1: "SSA_ERR_ARG", 2: "SSA_ERR_WINDOW", 3: "SSA_ERR_EMPTY_KSHAPE", 4: "SSA_ERR_RANK",
           5: "SSA_ERR_NOT_CONVERGED", 6: "SSA_ERR_OOM", 7: "SSA_ERR_CUDA", 8: "SSA_ERR_COMM", 9: "SSA_ERR_STATE"}
 SSA_F32, SSA_F64 = 0, 1
-PATHS = {"auto": 0, "direct": 1, "fft": 2}
+PATHS = {"auto": 0, "direct": 1, "fft": 2, "tc": 3}
 PATH_NAMES = {v: k for k, v in PATHS.items()}
 
 
@@ -44,7 +44,7 @@ class ssa_plan_info_t(C.Structure):
     _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("lx", C.c_int64), ("ly", C.c_int64),
                 ("kx", C.c_int64), ("ky", C.c_int64), ("L", C.c_int64), ("K", C.c_int64),
                 ("n_valid", C.c_int64), ("n_excluded", C.c_int64), ("path", C.c_int), ("dtype", C.c_int),
-                ("full_window", C.c_int), ("full_kshape", C.c_int)]
+                ("full_window", C.c_int), ("full_kshape", C.c_int), ("path_xv", C.c_int), ("path_xtu", C.c_int)]
 
 
 class ssa_decomp_info(C.Structure):

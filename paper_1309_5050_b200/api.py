@@ -102,6 +102,8 @@ class Plan:
         self.kx, self.ky, self.L, self.K = inf.kx, inf.ky, inf.L, inf.K
         self.n_valid, self.n_excluded = inf.n_valid, inf.n_excluded
         self.path = lib.PATH_NAMES.get(inf.path, str(inf.path))
+        self.path_xv = lib.PATH_NAMES.get(inf.path_xv, str(inf.path_xv))
+        self.path_xtu = lib.PATH_NAMES.get(inf.path_xtu, str(inf.path_xtu))
         self.full_window, self.full_kshape = bool(inf.full_window), bool(inf.full_kshape)
         self.decomp_info = None
 

@@ -4,7 +4,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.h"
@@ -91,8 +93,33 @@ static CorrParams<T> base_corr(PlanImpl &p) {
 }
 
 template <typename T>
+static void tc_dispatch(PlanImpl &p, bool xv, const T *in, int64_t ldi, T *out, int64_t ldo, int k) {
+    if constexpr (sizeof(T) == 4) {
+        TcCorrParams c{};
+        c.x = p.img.as<float>(); c.ldx = p.nx; c.nx = p.nx;
+        if (xv) {
+            c.ox = p.lx; c.oy = p.ly; c.bx = p.kx; c.by = p.ky;
+            c.imap = p.full_k ? nullptr : p.kmap.as<int>(); c.omap = p.full_window ? nullptr : p.lmap.as<int>();
+        } else {
+            c.ox = p.kx; c.oy = p.ky; c.bx = p.lx; c.by = p.ly;
+            c.imap = p.full_window ? nullptr : p.lmap.as<int>(); c.omap = p.full_k ? nullptr : p.kmap.as<int>();
+        }
+        c.in = in; c.ldi = ldi; c.out = out; c.ldo = ldo; c.k = k;
+        const size_t need = tc_pack_bytes(c.bx, c.by, std::min(k, 64));
+        if (need > p.tc_bpk_bytes) { p.tc_bpk.alloc(need, p.st); p.tc_bpk_bytes = need; }
+        c.bpk = p.tc_bpk.as<float>(); c.bpk_bytes = p.tc_bpk_bytes;
+        c.ws = p.ws_corr.as<float>(); c.ws_bytes = p.ws_corr_bytes;
+        tc_corr(c, p.st);
+    } else {
+        (void)p; (void)xv; (void)in; (void)ldi; (void)out; (void)ldo; (void)k;
+        throw Error(SSA_ERR_ARG, "tensor-core path is fp32 only");
+    }
+}
+
+template <typename T>
 void op_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k) {
-    if (p.path == SSA_PATH_FFT && p.fft) { fft_xtu<T>(p, U, ldu, V, ldv, k); return; }
+    if (p.path_xtu == SSA_PATH_FFT && p.fft) { fft_xtu<T>(p, U, ldu, V, ldv, k); return; }
+    if (p.path_xtu == SSA_PATH_TC) { tc_dispatch<T>(p, false, U, ldu, V, ldv, k); return; }
     CorrParams<T> c = base_corr<T>(p);
     c.ox = p.kx; c.oy = p.ky; c.dx = p.lx; c.dy = p.ly;
     c.W = U; c.ldw = ldu; c.wmap = p.full_window ? nullptr : p.lmap.as<int>();
@@ -103,8 +130,10 @@ void op_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k) {
 
 template <typename T>
 void op_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k) {
-    if (p.path == SSA_PATH_FFT && p.fft) {
+    if (p.path_xv == SSA_PATH_FFT && p.fft) {
         fft_xv<T>(p, V, ldv, U, ldu, k);
+    } else if (p.path_xv == SSA_PATH_TC) {
+        tc_dispatch<T>(p, true, V, ldv, U, ldu, k);
     } else {
         CorrParams<T> c = base_corr<T>(p);
         c.ox = p.lx; c.oy = p.ly; c.dx = p.kx; c.dy = p.ky;
@@ -124,6 +153,114 @@ template void op_xtu<float>(PlanImpl &, const float *, int64_t, float *, int64_t
 template void op_xtu<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int);
 template void op_xv<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int);
 template void op_xv<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int);
+
+// ---------------------------------------------------------------- path choice
+// Candidates per product: FFT correlation (fft_supported), tensor-core 3xTF32
+// implicit GEMM (fp32, output box rows >= 96) and the CUDA-core direct kernel.
+// AUTO prunes by a cost model and times the survivors on the plan's stream (one
+// block of k vectors, best of 3 after a warm-up); the decision is cached per shape
+// for the process.  An explicit opts.path is honoured where the product supports it.
+struct PathKey {
+    int nx, ny, lx, ly, kx, ky; int64_t L, K; int dt, k, xv, fw, fk;
+    bool operator<(const PathKey &o) const {
+        return std::tie(nx, ny, lx, ly, kx, ky, L, K, dt, k, xv, fw, fk) <
+               std::tie(o.nx, o.ny, o.lx, o.ly, o.kx, o.ky, o.L, o.K, o.dt, o.k, o.xv, o.fw, o.fk);
+    }
+};
+
+template <typename T>
+static double time_product(PlanImpl &p, bool xv, int path, int k, T *in, T *out) {
+    const int save_xv = p.path_xv, save_xtu = p.path_xtu;
+    (xv ? p.path_xv : p.path_xtu) = path;
+    cudaEvent_t e0, e1;
+    SSA_CUDA(cudaEventCreate(&e0)); SSA_CUDA(cudaEventCreate(&e1));
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+        SSA_CUDA(cudaEventRecord(e0, p.st));
+        if (xv) op_xv<T>(p, in, p.K, out, p.L, k);
+        else op_xtu<T>(p, in, p.L, out, p.K, k);
+        SSA_CUDA(cudaEventRecord(e1, p.st));
+        SSA_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        SSA_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (rep > 0) best = std::min(best, ms);
+    }
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    p.path_xv = save_xv; p.path_xtu = save_xtu;
+    return best;
+}
+
+template <typename T>
+static void choose_paths(PlanImpl &p) {
+    const bool fft_ok = fft_supported(p);
+    if (fft_ok && (p.path == SSA_PATH_FFT || p.path == SSA_PATH_AUTO)) fft_build(p);
+    const int k = std::max(1, std::min<int>(p.block_k, 64));
+    const bool is32 = sizeof(T) == 4;
+    const bool tc_xv = is32 && tc_corr_supported(p.lx, p.ly, p.kx, p.ky, k);
+    const bool tc_xtu = is32 && tc_corr_supported(p.kx, p.ky, p.lx, p.ly, k);
+    auto fallback = [&](bool tc_ok) { return tc_ok ? SSA_PATH_TC : SSA_PATH_DIRECT; };
+    if (p.path == SSA_PATH_FFT) {
+        if (!fft_ok) throw Error(SSA_ERR_ARG, "FFT path not available for this shape");
+        p.path_xv = p.path_xtu = SSA_PATH_FFT;
+        return;
+    }
+    if (p.path == SSA_PATH_DIRECT) { p.path_xv = p.path_xtu = SSA_PATH_DIRECT; return; }
+    if (p.path == SSA_PATH_TC) {
+        if (!is32) throw Error(SSA_ERR_ARG, "tensor-core path is fp32 only");
+        // products whose output box is too narrow for M = 128 tiles use the FFT / direct path
+        p.path_xv = tc_xv ? SSA_PATH_TC : (fft_ok ? SSA_PATH_FFT : SSA_PATH_DIRECT);
+        p.path_xtu = tc_xtu ? SSA_PATH_TC : (fft_ok ? SSA_PATH_FFT : SSA_PATH_DIRECT);
+        if (!p.fft && fft_ok && (p.path_xv == SSA_PATH_FFT || p.path_xtu == SSA_PATH_FFT)) fft_build(p);
+        return;
+    }
+    // AUTO
+    static std::mutex mu;
+    static std::map<PathKey, int> cache;
+    const double flops = 2.0 * (double)p.L * (double)p.K * k;
+    for (int xv = 0; xv < 2; ++xv) {
+        const bool tc_ok = xv ? tc_xv : tc_xtu;
+        PathKey key{p.nx, p.ny, p.lx, p.ly, p.kx, p.ky, p.L, p.K, (int)p.dt, k, xv, (int)p.full_window, (int)p.full_k};
+        int choice = -1;
+        {
+            std::lock_guard<std::mutex> g(mu);
+            auto itc = cache.find(key);
+            if (itc != cache.end()) choice = itc->second;
+        }
+        if (choice < 0) {
+            // cost model (µs) to prune hopeless candidates before timing
+            std::vector<std::pair<int, double>> cand;
+            const double t_direct = flops / (is32 ? 30e6 : 15e6);
+            const double t_tc = flops / 150e6;
+            if (fft_ok) cand.push_back({SSA_PATH_FFT, 0.0});
+            if (tc_ok) cand.push_back({SSA_PATH_TC, t_tc});
+            cand.push_back({SSA_PATH_DIRECT, t_direct});
+            if (cand.size() == 1 || (!fft_ok && !tc_ok)) {
+                choice = SSA_PATH_DIRECT;
+            } else {
+                DevBuf bin, bout;
+                bin.alloc(sizeof(T) * (size_t)std::max(p.L, p.K) * k, p.st);
+                bout.alloc(sizeof(T) * (size_t)std::max(p.L, p.K) * k, p.st);
+                SSA_CUDA(cudaMemsetAsync(bin.p, 0, bin.bytes, p.st));
+                double best = 1e300;
+                for (auto &c : cand) {
+                    // never time a candidate predicted > 20 ms or > 8x the best measured
+                    if (c.second > 2e4 || c.second > 8.0 * best * 1e3) continue;
+                    const double ms = time_product<T>(p, xv, c.first, k, bin.as<T>(), bout.as<T>());
+                    if (ms < best) { best = ms; choice = c.first; }
+                }
+                if (choice < 0) choice = fft_ok ? SSA_PATH_FFT : fallback(tc_ok);
+            }
+            std::lock_guard<std::mutex> g(mu);
+            cache[key] = choice;
+        }
+        (xv ? p.path_xv : p.path_xtu) = choice;
+    }
+    if (!fft_ok || (p.path_xv != SSA_PATH_FFT && p.path_xtu != SSA_PATH_FFT)) {
+        // keep the spectrum only if a product or the averaging uses it
+        (void)0;
+    }
+    p.path = p.path_xv;
+}
 
 // ---------------------------------------------------------------- plan creation
 template <typename T>
@@ -260,16 +397,8 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
     p.ws_corr_bytes = std::max(p.ws_corr_bytes, (size_t)p.lx * p.ly * (size_t)kmax * sizeof(T) * 2);
     p.ws_corr.alloc(p.ws_corr_bytes, st);
     p.ws_gram.alloc(gram_partial_bytes(std::max<int64_t>({p.L, p.K, nxy}), 512, 64), st);
-    // product path
-    if (p.path == SSA_PATH_FFT || p.path == SSA_PATH_AUTO) {
-        if (fft_supported(p)) {
-            fft_build(p);
-            p.path = SSA_PATH_FFT;
-        } else {
-            if (p.path == SSA_PATH_FFT) throw Error(SSA_ERR_ARG, "FFT path not available for this shape");
-            p.path = SSA_PATH_DIRECT;
-        }
-    }
+    // product path (per product; SURVEY north star: "the choice made per shape from measurement")
+    choose_paths<T>(p);
     SSA_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -299,7 +428,7 @@ static void reconstruct_impl(PlanImpl &p, const int32_t *off, const int32_t *idx
     SSA_CUDA(cudaMemcpyAsync(go.p, off, sizeof(int32_t) * (ng + 1), cudaMemcpyHostToDevice, p.st));
     if (nidx) SSA_CUDA(cudaMemcpyAsync(gi.p, idx, sizeof(int32_t) * nidx, cudaMemcpyHostToDevice, p.st));
     SSA_CUDA(cudaMemcpyAsync(sig.p, p.sigma.data(), sizeof(double) * p.r, cudaMemcpyHostToDevice, p.st));
-    if (ng > 0 && p.path == SSA_PATH_FFT && p.fft) {
+    if (ng > 0 && p.fft) {
         // eigentriples referenced by the groups, and their slot in the batched spectra
         std::vector<int> used, slot(p.r, -1);
         for (int t = 0; t < nidx; ++t)
@@ -432,6 +561,7 @@ ssa_status ssa_plan_info(ssa_plan p, ssa_plan_info_t *info) {
     info->L = P.L; info->K = P.K; info->n_valid = P.n_valid; info->n_excluded = P.n_excluded;
     info->path = P.path; info->dtype = P.dt;
     info->full_window = P.full_window; info->full_kshape = P.full_k;
+    info->path_xv = P.path_xv; info->path_xtu = P.path_xtu;
     return SSA_OK;
 }
 

@@ -41,6 +41,22 @@ struct AvgParams {
 template <typename T>
 void diagsums_direct(AvgParams<T> P, cudaStream_t st);
 
+// ---- tensor-core (tcgen05 3xTF32) implicit GEMM, fp32 only (hankel_tc.cu) -------
+// Same operation as CorrParams: out[p, j] = Σ_{d ∈ in-box} x[p + d] in[d, j].
+struct TcCorrParams {
+    const float *x; int64_t ldx; int nx;     // image (zero outside 𝔑), column-major
+    int ox, oy;                              // output box
+    int bx, by;                              // reduction (input) box
+    const float *in; int64_t ldi; const int *imap;   // filters, compact; imap: box -> compact or -1
+    float *out; int64_t ldo; const int *omap;        // output, compact; omap: box -> compact or -1
+    int k;
+    float *ws; size_t ws_bytes;              // split-K partials
+    float *bpk; size_t bpk_bytes;            // packed hi/lo filters
+};
+bool tc_corr_supported(int ox, int oy, int bx, int by, int k);
+size_t tc_pack_bytes(int bx, int by, int k);
+void tc_corr(const TcCorrParams &P, cudaStream_t st);
+
 // ---- FFT path (fft.cu) -----------------------------------------------------
 struct FftPlan;   // opaque, defined in fft.cu
 
@@ -61,6 +77,12 @@ void gemm_small(int64_t M, const T *A, int64_t lda, int m, const double *C, int 
 template <typename T>
 void gemm_acc(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
               double beta, T *Out, int64_t ldo, cudaStream_t st);
+
+// Device-resident CGS + CholeskyQR pass (blas.cu): see orth_solve_kernel.
+void orth_solve(const double *G, int na, int kc, int pass, double zthr2, double shift_rel, double thr_chol,
+                double *Mout, double *Ctot, double *Btot, int *flags, cudaStream_t st);
+template <typename T>
+void apply_inplace(int64_t M, T *A, int64_t lda, int n1, int kc, const double *Mc, const int *skip, cudaStream_t st);
 
 // A[:, cols] = N(0,1) from a counter-based generator keyed by (seed, stream_id).
 template <typename T>

@@ -16,7 +16,8 @@ struct PlanImpl {
     int64_t L = 0, K = 0, n_valid = 0, n_excluded = 0;
     bool full_window = true, full_k = true;
     ssa_dtype dt = SSA_F32;
-    int path = SSA_PATH_DIRECT;
+    int path = SSA_PATH_DIRECT;   // requested path (AUTO resolved per product below)
+    int path_xv = SSA_PATH_DIRECT, path_xtu = SSA_PATH_DIRECT;   // chosen per product
     int block_k = 32;
     double tol = 0;
     int max_products = 0;
@@ -37,6 +38,8 @@ struct PlanImpl {
     DevBuf ws_corr;   // split-K partials of the direct products
     size_t ws_corr_bytes = 0;
     DevBuf ws_gram;   // gram partials
+    DevBuf tc_bpk;    // packed tf32 hi/lo filters of the tensor-core path
+    size_t tc_bpk_bytes = 0;
     DevBuf dsmall;    // device scratch for small double matrices
     std::vector<int32_t> lmap_host;   // 𝔏 positions (box indices) in lex order
     FftOperator *fft = nullptr;       // FFT correlation path (null if not built)

@@ -97,6 +97,9 @@ struct Gkl {
     bool gpu_ritz = true;
     bool full_k_reorth = false;   // set when K < L (then the K side is the short one)
     bool debug = std::getenv("SSA_DEBUG") != nullptr;
+    bool use_fast = std::getenv("SSA_ORTH_LEGACY") == nullptr;
+    DevBuf ow;                    // device workspace of the fast orthonormalisation
+    int64_t n_fast = 0, n_fallback = 0;
 
     explicit Gkl(PlanImpl &pl) : p(pl), st(pl.st), L(pl.L), K(pl.K) {
         thr_abs = (sizeof(T) == 4) ? 1e-6 : 1e-14;
@@ -321,6 +324,53 @@ struct Gkl {
         return B;
     }
 
+
+    // Device-resident orthonormalisation of W (M x kc) against the na columns that
+    // precede it in the same buffer: two (rarely three) CGS + CholeskyQR passes run as
+    // gram_tn / orth_solve / apply_inplace launches with ONE host synchronisation (the
+    // coefficients and flags come back together).  Returns false — W is then garbage and
+    // the caller recomputes it and takes the robust host path `orth` — when a column is
+    // numerically in span(A) or zero (breakdown), or the passes did not converge.
+    bool orth_fast(int64_t M, T *W, int kc, const T *against, int na, bool kside, double *coef,
+                   std::vector<double> &Bout) {
+        if (!use_fast || kc > 64 || na + kc > 512) return false;
+        if (na > 0 && against + (int64_t)na * M != W) return false;   // needs [A W] contiguous
+        T *A = na > 0 ? const_cast<T *>(against) : W;
+        const int n1 = na + kc;
+        const size_t nd = 3 * 512 * 64 + 64 * 64 + 16;
+        ow.alloc(sizeof(double) * nd, st);
+        double *dG = ow.as<double>(), *dMc = dG + 512 * 64, *dC = dMc + 512 * 64, *dBt = dC + 512 * 64;
+        int *flags = reinterpret_cast<int *>(dBt + 64 * 64);
+        SSA_CUDA(cudaMemsetAsync(flags, 0, 8 * sizeof(int), st));
+        const double zt = thr_abs * std::max(anorm, 1e-300);
+        const double shift_rel = (sizeof(T) == 4) ? 1e-6 : 1e-13;
+        const size_t ic = sg.take((size_t)na * kc + (size_t)kc * kc + 8);
+        double *hC = sg.h + ic, *hB = hC + (size_t)na * kc;
+        int *hf = reinterpret_cast<int *>(hB + (size_t)kc * kc);
+        for (int pass = 1; pass <= 3; ++pass) {
+            gram_tn<T>(M, A, M, n1, W, M, kc, dG, p.ws_gram.as<double>(), p.ws_gram.bytes, st);
+            if (kside && kside_comm()) {
+                if (p.comm.allreduce_sum(p.comm.user, dG, (int64_t)n1 * kc, SSA_F64, st) != 0)
+                    throw Error(SSA_ERR_COMM, "allreduce of a K-side Gram failed");
+            }
+            orth_solve(dG, na, kc, pass, zt * zt, shift_rel, thr_chol, dMc, dC, dBt, flags, st);
+            apply_inplace<T>(M, A, M, n1, kc, dMc, flags, st);
+            if (pass == 1) continue;
+            if (na > 0) SSA_CUDA(cudaMemcpyAsync(hC, dC, sizeof(double) * na * kc, cudaMemcpyDeviceToHost, st));
+            SSA_CUDA(cudaMemcpyAsync(hB, dBt, sizeof(double) * kc * kc, cudaMemcpyDeviceToHost, st));
+            SSA_CUDA(cudaMemcpyAsync(hf, flags, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+            SSA_CUDA(cudaStreamSynchronize(st));
+            if (hf[0]) { ++n_fallback; return false; }
+            if (!hf[2]) break;
+            if (pass == 3) { ++n_fallback; return false; }
+        }
+        sg.off = 0;
+        for (size_t t = 0; t < (size_t)na * kc; ++t) coef[t] += hC[t];
+        Bout.assign(hB, hB + (size_t)kc * kc);
+        ++n_fast;
+        return true;
+    }
+
     // every block product is bracketed by CUDA events on the plan's stream so the
     // device time spent in the trajectory products is reported (ms_products)
     std::vector<cudaEvent_t> ev;
@@ -370,7 +420,14 @@ struct Gkl {
         // full projection onto the L basis; all CGS coefficients go into T so that
         // X·Qb = Pb·T holds exactly
         std::vector<double> C((size_t)nP * k, 0.0);
-        std::vector<double> B = orth(L, W, k, P(0), nP, false, C.data());
+        std::vector<double> B;
+        if (!orth_fast(L, W, k, P(0), nP, false, C.data(), B)) {
+            if (use_fast) {   // the fast path touched W: recompute the product
+                product_xv(Q(qc), W, k);
+                std::fill(C.begin(), C.end(), 0.0);
+            }
+            B = orth(L, W, k, P(0), nP, false, C.data());
+        }
         for (int b = 0; b < k; ++b)
             for (int a = 0; a < nP; ++a) Tat(a, qc + b) = C[a + (size_t)nP * b];
         for (int b = 0; b < k; ++b)
@@ -387,17 +444,29 @@ struct Gkl {
             gram(K, W, K, k, W, K, k, G.data(), true);
             for (int j = 0; j < k; ++j) anorm = std::max(anorm, std::sqrt(std::max(G[j + (size_t)k * j], 0.0)));
         }
-        if (nQ > 0) {
-            // remove the recurrence term first (W -= Q_prev·Bᵀ with B = T[P_new, Q_prev], known
-            // exactly), so that the full projection below only removes rounding-level
-            // components and one CGS pass normally suffices (DGKS test in orth)
-            const int qc = nQ - k;
-            std::vector<double> Bt((size_t)k * k);
-            for (int a = 0; a < k; ++a)
-                for (int b = 0; b < k; ++b) Bt[b + (size_t)k * a] = Tat(pc + a, qc + b);   // (T block)ᵀ
-            gemm(K, Q(qc), K, k, Bt.data(), k, k, -1.0, 1.0, W, K);
+        auto recurrence = [&]() {
+            if (nQ > 0) {
+                // remove the recurrence term first (W -= Q_prev·Bᵀ with B = T[P_new, Q_prev], known
+                // exactly), so that the full projection below only removes rounding-level
+                // components and one CGS pass normally suffices
+                const int qc = nQ - k;
+                std::vector<double> Bt((size_t)k * k);
+                for (int a = 0; a < k; ++a)
+                    for (int b = 0; b < k; ++b) Bt[b + (size_t)k * a] = Tat(pc + a, qc + b);   // (T block)ᵀ
+                gemm(K, Q(qc), K, k, Bt.data(), k, k, -1.0, 1.0, W, K);
+            }
+        };
+        recurrence();
+        const T *againstK = full_k_reorth ? Q(0) : nullptr;
+        const int naK = full_k_reorth ? nQ : 0;
+        std::vector<double> Cdummy((size_t)std::max(naK, 1) * k, 0.0);
+        if (!orth_fast(K, W, k, againstK, naK, true, Cdummy.data(), Alast)) {
+            if (use_fast) {
+                product_xtu(P(pc), W, k);
+                recurrence();
+            }
+            Alast = orth(K, W, k, againstK, naK, true);
         }
-        Alast = orth(K, W, k, full_k_reorth ? Q(0) : nullptr, full_k_reorth ? nQ : 0, true);
         nQ += k;
     }
 
