@@ -13,8 +13,9 @@ Metric: trajectory products/s = vector products (X·v or Xᵀ·u) completed per
 second of whole-step time, summed over ranks (weak scaling: every rank
 decomposes its own input, no data-path collective).  `e2e` is the same metric
 through the C ABI with host buffers (H2D of the input and D2H of the
-reconstructions inside the timed region).  `roofline` reports the dominant kernel
-(the direct trajectory product) against the FP32 FFMA peak.
+reconstructions inside the timed region).  `roofline` reports the trajectory block
+product with the larger share of the step against the roofline of the path that served
+it (FFT: HBM bytes model; tc: 3xTF32 tensor peak; direct: FFMA), DESIGN.md §6.
 """
 from __future__ import annotations
 
@@ -183,40 +184,68 @@ def run_ours(args, rank, world, dist):
     d2h = int(len(groups) * np.asarray(w.data).size * esz + 8 * w.r)
     e2e_value = info_h["n_vector_products"] / (np.mean(e2e_times) / 1e3) * world
 
-    # ---- roofline of the trajectory block product (the kernel SURVEY §8(d) sizes), timed
-    # live: the library brackets every block product with CUDA events on the plan's stream
-    avg_block_ms = ms_prod / max(nblk, 1)
+    # ---- roofline of the trajectory block products (the kernels SURVEY §8(d) sizes), timed
+    # live: the library brackets every block product with CUDA events on the plan's stream,
+    # separately for X·V and Xᵀ·U; each product is held against the roofline of the path
+    # that served it, and the one with the larger share of the step is the headline
     peaks = _peaks()
-    if p.path == "fft":
-        # 3-pass model per vector: read the input box, write the output box,
-        # write+read the x-transformed input (Hx·by) and y-filtered output (Hx·oy), complex,
-        # plus the image spectrum once per block; identical for X·V and Xᵀ·U
-        esz = 8 if w.dtype == "f64" else 4
-        nx_, ny_ = np.asarray(w.data).shape
-        Mx = 1 << int(np.ceil(np.log2(nx_))); My = 1 << int(np.ceil(np.log2(max(ny_, 1))))
-        Hx = Mx // 2 + 1
-        kx_, ky_ = nx_ - w.window[0] + 1, ny_ - w.window[1] + 1
-        per_vec = esz * (K + L) + 2 * (2 * esz) * Hx * (ky_ + w.window[1])
-        alg = k * per_vec + (2 * esz) * Hx * My
-        achieved = alg / (avg_block_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": "FFT correlation block product (fft_pass_a/b/c)",
-                "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)",
-                "algorithmic_bytes_per_launch": alg}
-    else:
-        flops_per_block = 2.0 * L * K * k
-        achieved = flops_per_block / (avg_block_ms / 1e3) / 1e12
-        peak = FP64_PEAK_TFLOPS if w.dtype == "f64" else FFMA_PEAK_TFLOPS
-        roof = {"bound": "alu", "kernel": "corr_direct (X·V / Xᵀ·U block product, FFMA)",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None,
-                "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md SM count,"
-                               " MEASURED_PEAKS sm_max_mhz); fp64 = 1/2",
-                "algorithmic_flops_per_launch": flops_per_block}
-    roof.update({"avg_launch_ms": avg_block_ms, "launches_per_step": nblk / args.steps,
-                 "share_of_step": ms_prod / max(ms_local, 1e-9),
-                 "note": "a 'launch' is one block product of k vectors (3 FFT passes or corr_direct + split-K reduce)"})
+    esz = 8 if w.dtype == "f64" else 4
+    nx_, ny_ = np.asarray(w.data).shape
+    kx_, ky_ = nx_ - w.window[0] + 1, ny_ - w.window[1] + 1
+
+    def product_roofline(name, path, ms_total, nblocks, nvec):
+        if nblocks <= 0:
+            return None
+        avg_ms = ms_total / nblocks
+        kk = nvec / nblocks
+        flops = 2.0 * L * K * kk
+        if path == "fft":
+            # 3-pass model per vector: read the input box, write the output box,
+            # write+read the x-transformed input and the y-filtered output (complex, Hx rows),
+            # plus the image spectrum once per block
+            Mx = 1 << int(np.ceil(np.log2(nx_))); My = 1 << int(np.ceil(np.log2(max(ny_, 1))))
+            Hx = Mx // 2 + 1
+            per_vec = esz * (K + L) + 2 * (2 * esz) * Hx * (ky_ + w.window[1])
+            alg = kk * per_vec + (2 * esz) * Hx * My
+            achieved = alg / (avg_ms / 1e3) / 1e9
+            r = {"bound": "hbm", "kernel": f"{name}: FFT correlation (fft_pass_a/b/c)", "achieved": achieved,
+                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)", "algorithmic_bytes_per_launch": alg}
+        elif path == "tc":
+            # tcgen05 kind::tf32, 3 MMAs per useful multiply-add (3xTF32): the useful-flop peak is
+            # the dense TF32 peak / 3; TF32 = measured sustained bf16 x nominal ratio 1.1/2.25
+            tf32 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)) * (1.1 / 2.25)
+            peak = tf32 / 3.0
+            achieved = flops / (avg_ms / 1e3) / 1e12
+            r = {"bound": "tensor", "kernel": f"{name}: tcgen05 3xTF32 polyphase implicit GEMM (hankel_tc)",
+                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x 1.1/2.25 (nominal tf32/bf16) / 3 "
+                                "(3xTF32), of measured",
+                 "algorithmic_flops_per_launch": flops, "tensor_flops_per_launch": 3 * flops}
+        else:
+            peak = FP64_PEAK_TFLOPS if w.dtype == "f64" else FFMA_PEAK_TFLOPS
+            achieved = flops / (avg_ms / 1e3) / 1e12
+            r = {"bound": "alu", "kernel": f"{name}: corr_direct (FFMA/DFMA)", "achieved": achieved, "peak": peak,
+                 "unit": "TFLOP/s", "frac": achieved / peak,
+                 "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md SM count,"
+                                " MEASURED_PEAKS sm_max_mhz); fp64 = 1/2",
+                 "algorithmic_flops_per_launch": flops}
+        r.update({"traffic": None, "avg_launch_ms": avg_ms, "launches_per_step": nblocks / args.steps,
+                  "share_of_step": ms_total / max(ms_local, 1e-9), "path": path})
+        return r
+
+    prods = {}
+    for name, path, key in (("X·V", p.path_xv, "xv"), ("Xᵀ·U", p.path_xtu, "xtu")):
+        ms_t = float(np.sum([i[f"ms_products_{key}"] for i in infos]))
+        nb_t = float(np.sum([i[f"n_products_{key}"] for i in infos]))
+        nv_t = float(np.sum([i[f"n_vectors_{key}"] for i in infos]))
+        rr = product_roofline(name, path, ms_t, nb_t, nv_t)
+        if rr:
+            prods[key] = rr
+    roof = dict(max(prods.values(), key=lambda r: r["share_of_step"])) if prods else {}
+    roof["note"] = ("a 'launch' is one block product of k vectors (FFT: 3 passes; tc: pack + MMA kernel"
+                    " + split reduce); events bracket it on the plan's stream, so host launch gaps count")
+    roof["products"] = prods
     res = {
         "metric": "trajectory products/s",
         "value": nvec_all / (ms_all / 1e3),
@@ -230,7 +259,8 @@ def run_ours(args, rank, world, dist):
         "data": "synthetic (seeded BASELINE.json generator, rank-offset seeds)",
         "config": {"workload": w.name, "nx": int(np.asarray(w.data).shape[0]), "ny": int(np.asarray(w.data).shape[1]),
                    "window": list(w.window), "L": int(L), "K": int(K), "r": int(w.r), "block_k": int(k),
-                   "groups": len(groups), "path": p.path, "l2": "flushed (256 MB write) between timed steps",
+                   "groups": len(groups), "path": {"xv": p.path_xv, "xtu": p.path_xtu},
+                   "l2": "flushed (256 MB write) between timed steps",
                    "parallelism": f"replicas x{world} (independent inputs per rank)"},
         "rank_r_time_ms": ms_all / args.steps,
         "decomposition": {"n_block_products": infos[-1]["n_block_products"],

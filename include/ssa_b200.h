@@ -127,6 +127,9 @@ typedef struct {
     double max_rel_residual;          /* max_i ||Xᵀu_i - σ_i v_i|| / σ_1 over i < r */
     double ms_products, ms_total;     /* device time in products; wall time of the call */
     double ms_ritz;                   /* host time in the projected (Ritz) SVDs */
+    double ms_products_xv, ms_products_xtu;   /* device time of the X·V / Xᵀ·U block products */
+    int64_t n_products_xv, n_products_xtu;    /* block products of each kind */
+    int64_t n_vectors_xv, n_vectors_xtu;      /* vectors pushed through each product */
 } ssa_decomp_info;
 
 typedef struct ssa_plan_s *ssa_plan;

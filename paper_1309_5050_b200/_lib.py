@@ -51,7 +51,9 @@ class ssa_decomp_info(C.Structure):
     _fields_ = [("r_requested", C.c_int32), ("n_converged", C.c_int32), ("block_k", C.c_int32),
                 ("n_restarts", C.c_int32), ("n_block_products", C.c_int64), ("n_vector_products", C.c_int64),
                 ("max_rel_residual", C.c_double), ("ms_products", C.c_double), ("ms_total", C.c_double),
-                ("ms_ritz", C.c_double)]
+                ("ms_ritz", C.c_double), ("ms_products_xv", C.c_double), ("ms_products_xtu", C.c_double),
+                ("n_products_xv", C.c_int64), ("n_products_xtu", C.c_int64),
+                ("n_vectors_xv", C.c_int64), ("n_vectors_xtu", C.c_int64)]
 
 
 EXPORTS = ["ssa_plan_create", "ssa_plan_destroy", "ssa_plan_info", "ssa_get_weights", "ssa_get_kmask",

@@ -95,8 +95,14 @@ static CorrParams<T> base_corr(PlanImpl &p) {
 template <typename T>
 static void tc_dispatch(PlanImpl &p, bool xv, const T *in, int64_t ldi, T *out, int64_t ldo, int k) {
     if constexpr (sizeof(T) == 4) {
+        if (!p.tc_xhi.p) {
+            const size_t nb = sizeof(float) * (size_t)tc_plane_ld(p.nx) * p.ny;
+            p.tc_xhi.alloc(nb, p.st);
+            p.tc_xlo.alloc(nb, p.st);
+            tc_build_planes(p.img.as<float>(), p.nx, p.nx, p.ny, p.tc_xhi.as<float>(), p.tc_xlo.as<float>(), p.st);
+        }
         TcCorrParams c{};
-        c.x = p.img.as<float>(); c.ldx = p.nx; c.nx = p.nx;
+        c.x_hi = p.tc_xhi.as<float>(); c.x_lo = p.tc_xlo.as<float>(); c.nx = p.nx; c.ny = p.ny;
         if (xv) {
             c.ox = p.lx; c.oy = p.ly; c.bx = p.kx; c.by = p.ky;
             c.imap = p.full_k ? nullptr : p.kmap.as<int>(); c.omap = p.full_window ? nullptr : p.lmap.as<int>();
@@ -105,7 +111,7 @@ static void tc_dispatch(PlanImpl &p, bool xv, const T *in, int64_t ldi, T *out, 
             c.imap = p.full_window ? nullptr : p.lmap.as<int>(); c.omap = p.full_k ? nullptr : p.kmap.as<int>();
         }
         c.in = in; c.ldi = ldi; c.out = out; c.ldo = ldo; c.k = k;
-        const size_t need = tc_pack_bytes(c.bx, c.by, std::min(k, 64));
+        const size_t need = tc_pack_bytes(c.bx, c.by, k);
         if (need > p.tc_bpk_bytes) { p.tc_bpk.alloc(need, p.st); p.tc_bpk_bytes = need; }
         c.bpk = p.tc_bpk.as<float>(); c.bpk_bytes = p.tc_bpk_bytes;
         c.ws = p.ws_corr.as<float>(); c.ws_bytes = p.ws_corr_bytes;

@@ -354,10 +354,10 @@ orth_solve_kernel(const double *__restrict__ G, int na, int kc, int pass, double
     const int n1 = na + kc, tid = threadIdx.x, nt = blockDim.x;
     const double *C = G;
     int ldc = n1;
-    if (c_in_smem) {
-        for (int e = tid; e < na * kc; e += nt) Cs[e] = G[(e % na) + (size_t)n1 * (e / na)];
+    if (c_in_smem) {   // odd leading dimension: column-parallel reads hit distinct banks
+        ldc = na | 1;
+        for (int e = tid; e < na * kc; e += nt) Cs[(e % na) + (size_t)ldc * (e / na)] = G[(e % na) + (size_t)n1 * (e / na)];
         C = Cs;
-        ldc = na;
     }
     if (pass >= 2)
         for (int e = tid; e < kc * kc; e += nt) Bo[e] = Btot[e];
@@ -528,7 +528,7 @@ void orth_solve(const double *G, int na, int kc, int pass, double zthr2, double 
                 double *Mout, double *Ctot, double *Btot, int *flags, cudaStream_t st) {
     SSA_REQUIRE(kc <= 64 && na + kc <= 512, SSA_ERR_ARG, "orth_solve: at most 64 new columns against 448");
     const size_t base = sizeof(double) * 4 * (size_t)kc * kc;
-    const size_t cbytes = sizeof(double) * (size_t)na * kc;
+    const size_t cbytes = sizeof(double) * (size_t)(na | 1) * kc;
     const int c_in_smem = (base + cbytes <= 200 * 1024) ? 1 : 0;
     const size_t smem = base + (c_in_smem ? cbytes : 0);
     SSA_CUDA(cudaFuncSetAttribute(orth_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -9,26 +9,45 @@
 //
 //   X·V  : p ∈ 𝔏-box, d ∈ 𝔎-box, in = V      Xᵀ·U : p ∈ 𝔎-box, d ∈ 𝔏-box, in = U
 //
-// GEMM view per output column p_y: D[m, j] (M = 128 consecutive p_x) += A[m, kk] B[kk, j]
-// with kk running over (d_y, d_x).  For fixed d_y, A[m, d_x] = x[p_x0 + m + d_x, p_y + d_y]
-// is a Hankel block.  The Hankel structure is used twice:
-//   * a chunk of NB k-blocks (32 d_x each) needs only the strip
-//         S[i, jj] = x[p_x0 + d_x0 + i + jj, p_y + d_y],  i < 128 + 32(NB-1), jj < 32,
-//     because A for k-block b is rows [32b, 32b + 128) of S — the UMMA shared-memory
-//     descriptor of k-block b is the strip descriptor advanced by 4 core-matrix
-//     groups.  Building the operand costs (128 + 32(NB-1))·32 instead of NB·128·32
-//     shared-memory writes;
-//   * the strip is built from a 1-D segment of one image column (staged once).
-// B (the k filters) is split into tf32 hi/lo parts and packed into the UMMA
-// core-matrix layout once per product by tc_pack_b; the main kernel streams its
-// chunks into shared memory with bulk async copies (TMA engine, mbarrier tx count).
-// One thread issues tcgen05.mma (kind::tf32, M = 128, N = 32/64, fp32 accumulator in
-// TMEM): D += A_hi·B_hi + A_hi·B_lo + A_lo·B_hi.  Two pipeline stages: the builders
-// fill stage s^1 while the tensor core consumes stage s; tcgen05.commit arrives on
-// the stage's mbarrier when its MMAs have read shared memory.  The epilogue reads the
-// accumulator with tcgen05.ld (32x32b: warp w owns TMEM lanes 32w..32w+31 = rows).
-// Large reductions are split over CTAs along (d_y, d_x-chunks); partials are summed
-// deterministically by reduce_splits_kernel (direct.cu layout).
+// Polyphase GEMM.  With k filters padded to NP (16/32/64) and S = 256/NP phases, the
+// outputs p_x = p_x0 + S·m + s of one image column (m < 128, s < S) are
+//
+//     out[p_x0 + S·m + s, p_y; j] = Σ_{d_y} Σ_t  x[p_x0 + S·m + t, p_y + d_y] · in[t − s, d_y; j]
+//                                 =: Σ_{d_y} Σ_t  A[m, t] · B[t, (s, j)]
+//
+// i.e. one UMMA GEMM with M = 128, N = S·NP = 256 and K running over (d_y, t).  The
+// Hankel structure of the trajectory matrix moves into B (S shifted copies of the
+// filters), which keeps every MMA at N = 256: a thin N = k product would be bound by
+// the tensor core's shared-memory operand reads (A is re-read per instruction) and by
+// instruction issue — measured at 15% tensor-pipe activity for N = 32.  A is strided
+// Hankel: A[m, 32b + kk] = strip[m + 32b/S, kk] with strip[i, kk] = x[p_x0 + t0 + S·i + kk],
+// so all k-blocks of a chunk share one strip and k-block b is the strip descriptor
+// advanced by 32b/S rows (interleaved layout: 16-B row stride).
+//
+// Operand staging is TMA (cp.async.bulk.tensor): the plan keeps the image split into tf32
+// hi / lo planes (columns zero-padded), and each product packs its k filters once into hi /
+// lo rows with LEAD (>= S-1, multiple of 4) leading zeros per image column (tc_pack_kernel).
+// A strip plane cc (rows at 16 B) is one 3-D box of the image plane viewed as [rows][S/4][4].
+// The S phase tiles of B are shifted copies of one filter window (32 + LEAD entries x NP
+// filters, one 16-B aligned 2-D box — TMA faults on unaligned inner box coordinates, so the
+// per-phase element shifts cannot be TMA boxes); warps 2-7 expand the window into the S
+// 128-B swizzled K-major tiles with 16-B shared-memory copies.
+//
+// Roles (8 warps): lane 0 of warp 0 issues the TMA loads, lane 0 of warp 1 issues
+// tcgen05.mma (kind::tf32, fp32 accumulators in TMEM):  D += A_hi·B_lo + A_lo·B_hi + A_hi·B_hi.
+// The tensor core accumulates with truncation, so each chunk (NB k-blocks) gets a fresh
+// TMEM accumulator (two, ping-pong, 2 x 256 columns); all 8 warps drain finished chunks
+// with tcgen05.ld into fp32 registers (round to nearest): warp w owns TMEM lanes
+// 32·(w%4).. and accumulator columns 128·(w/4)..  Large reductions are split
+// over CTAs (d_y ranges x k-block ranges); partials are summed by tc_reduce_kernel in a
+// fixed order (deterministic).
+#include <cstdio>
+#include <cstdlib>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <map>
+#include <mutex>
+
 #include "common.h"
 #include "kernels.h"
 
@@ -37,10 +56,8 @@ namespace ssa {
 namespace tc {
 
 constexpr int kM = 128;          // UMMA M (one accumulator row per TMEM lane)
-constexpr int kKB = 32;          // d_x per k-block (4 UMMA k-steps of 8 tf32)
-constexpr int kBuilders = 256;   // warps 0-7 build the A strips; warp 8 issues TMA + MMA
-constexpr int kThreads = kBuilders + 32;
-constexpr int kSeg = 256;        // staged image segment per chunk (>= strip rows + 32)
+constexpr int kKB = 32;          // t per k-block (4 UMMA k-steps of 8 tf32)
+constexpr int kThreads = 256;    // 8 warps: 2 per SM sub-partition (255-register cap)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -66,6 +83,18 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t addr) {
     d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
     d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
     return d;
+}
+// K-major, no swizzle ("interleaved" core matrices): rows at a uniform 16-B stride inside
+// each 16-B K-chunk plane; LBO = distance between the two planes of one k-step (8 tf32),
+// SBO = 128 (8-row groups contiguous).  Any 16-B aligned start works, so the start can
+// step by single rows (used for the polyphase A strip).
+__device__ __forceinline__ uint64_t make_desc_interleave(uint32_t addr, uint32_t lbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)(128 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;   // layout SWIZZLE_NONE
 }
 // byte offset of the 16-B chunk c (0..7) of row i inside a swizzled K-major tile
 __host__ __device__ __forceinline__ uint32_t sw128_off(int i, int c) {
@@ -95,10 +124,47 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// expect_tx without an arrival (tx counts above 2^16 - 1 per instruction fault: split them)
+__device__ __forceinline__ void mbar_expect_tx_noarrive(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_true(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_dsmem(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
 }
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -137,114 +203,120 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// racc[0..127] += 128 accumulator columns of this warp's TMEM lane quarter
+__device__ __forceinline__ void drain_acc(float (&racc)[128], uint32_t taddr) {
+    tc_fence_after();
+#pragma unroll
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t r[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) racc[c0 + j] += __uint_as_float(r[j]);
+    }
+    tc_fence_before();
+}
+
 }  // namespace tc
 
 // ---------------------------------------------------------------------------
-// B packing: in[d, j] (compact, column-major, ld ldi; imap: box -> compact or -1)
-// -> Bpk[dy][kb][h] = an N x 32 swizzled K-major tile (h = tf32 hi / lo; row n = filter,
-// 16-B chunk c = d_x 4c..4c+3 at sw128_off(n, c)), zero padded to nkb_pad k-blocks per
-// d_y and N columns.  One k-block is 2·N·128 bytes.
-// ---------------------------------------------------------------------------
-template <int N>
-__global__ void tc_pack_b_kernel(const float *__restrict__ in, int64_t ldi, const int *__restrict__ imap, int bx,
-                                 int by, int k, int j0, int nkb_pad, float *__restrict__ bpk) {
-    const int64_t total = (int64_t)by * nkb_pad * N * tc::kKB;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int kk = (int)(t % tc::kKB);
-        const int64_t r = t / tc::kKB;
-        const int n = (int)(r % N);
-        const int64_t blk = r / N;                 // dy * nkb_pad + kb
-        const int kb = (int)(blk % nkb_pad), dy = (int)(blk / nkb_pad);
-        const int dx = kb * tc::kKB + kk;
-        float v = 0.f;
-        if (dx < bx && n + j0 < k) {
-            const int64_t box = dx + (int64_t)bx * dy;
-            const int64_t ci = imap ? (int64_t)imap[box] : box;
-            if (ci >= 0) v = in[ci + ldi * (int64_t)(n + j0)];
-        }
-        const float hi = __uint_as_float(tc::tf32_rna(v));
-        const float lo = v - hi;
-        const int c = kk >> 2, q = kk & 3;
-        const int64_t off = tc::sw128_off(n, c) / 4 + q;
-        float *base = bpk + blk * (2 * N * tc::kKB);
-        base[off] = hi;
-        base[N * tc::kKB + off] = lo;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Main kernel.  grid.x = M-tiles (ceil(ox/128) per output column, times oy),
-// grid.y = reduction splits (nsy along d_y times nsx along d_x chunks).
-// Warp roles: warps 0-7 stage the image segment and build the hi/lo strip of
-// each chunk; warp 8 (one lane) streams the packed B chunk with a bulk async
-// copy and issues the MMAs.  Per stage s: full[s] (B landed, tx count),
-// built[s] (8 builder-warp arrivals), empty[s] (tcgen05.commit: the MMAs that
-// read stage s have completed).
-// ---------------------------------------------------------------------------
 struct TcArgs {
-    const float *x; int64_t ldx; int nx;
     int ox, oy;                   // output box
     int bx, by;                   // reduction (input) box
-    int nkb_pad;                  // packed k-blocks per d_y (multiple of NB)
-    const float *bpk;             // packed B
-    int k, j0;                    // columns j0 .. j0+N-1 of the k filters
+    int k, j0, jn;                // filter columns j0 .. j0 + jn - 1 of k (jn <= NP)
+    int ldp;                      // padded column length of the hi / lo image planes
+    int lser;                     // packed filter entries per d_y (S-1 leading zeros)
     float *out; int64_t ldo; const int *omap;
-    float *ws; int nsplit, nsx, dy_split, cx_split;
+    float *ws;                    // split partials [split][tile][n][m]
+    int ntiles, ntx;
+    int nkb;                      // k-blocks of t per d_y (t < bx + S - 1)
+    int nsplit, nsx, dy_split, kb_split;
+    int cluster;                  // CTAs per cluster along the splits (partials summed on chip)
 };
 
-template <int N, int NB>
+template <int S, int NB>
 struct TcCfg {
-    static constexpr int R = tc::kM + tc::kKB * (NB - 1);          // strip rows
-    static constexpr uint32_t strip_bytes = R * 128;               // one of hi / lo
-    static constexpr uint32_t bblock = 2 * N * 128;                // one packed k-block (hi + lo)
-    static constexpr uint32_t bbytes = NB * bblock;
-    static constexpr uint32_t stage = 2 * strip_bytes + bbytes;
-    static constexpr size_t smem = 2 * (size_t)stage + 2 * tc::kSeg * sizeof(float) + 128;
-    static_assert(R + tc::kKB <= tc::kSeg, "segment too short for the strip");
-    static_assert(smem <= 227 * 1024, "shared memory budget");
+    static constexpr int NP = 256 / S;                       // padded filters
+    static constexpr int RS = 32 / S;                        // strip rows per k-block
+    static constexpr int R = ((tc::kM + RS * (NB - 1)) + 7) / 8 * 8;   // strip rows
+    static constexpr int LEAD = (S - 1 + 3) / 4 * 4;         // leading zeros per d_y in the packed filters
+    static constexpr int W = 32 + LEAD;                      // filter window per k-block (16-B aligned box)
+    static constexpr int NCH = (LEAD + 4) / 4;               // 16-B chunks a B item reads
+    static constexpr int VB = (S == 4) ? 1 : 2;              // filter-window buffers
+    static constexpr uint32_t plane = R * 16;                // one 16-B K-chunk plane of the strip
+    static constexpr uint32_t a_bytes = 8 * plane;           // one of hi / lo
+    static constexpr uint32_t b_bytes = 256 * 128;           // one of hi / lo (256 rows x 128 B)
+    static constexpr uint32_t v_bytes = NP * W * 4;          // one of hi / lo
+    static constexpr uint32_t off_b = 0;                     // [2 stages][hi, lo]
+    static constexpr uint32_t off_a = 4 * b_bytes;           // [2 stages][hi, lo]
+    static constexpr uint32_t off_v = off_a + 4 * a_bytes;   // [VB][hi, lo]
+    static constexpr uint32_t off_bar = off_v + VB * 2 * v_bytes;
+    static constexpr size_t smem = off_bar + 16 * 8 + 16 + 1024;   // + alignment slack
+    static_assert(smem <= 232448, "shared memory budget");
+    static_assert(R <= 256 && W <= 256, "TMA box extents");
 };
 
-template <int N, int NB>
-__global__ void __launch_bounds__(tc::kThreads, 1) hankel_tc_kernel(TcArgs a) {
+constexpr int kBuildWarps = 6;   // warps 2-7 expand the filter windows into the S phase tiles
+
+template <int S, int NB>
+__global__ void __launch_bounds__(tc::kThreads, 1)
+hankel_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmA_hi,
+                 const __grid_constant__ CUtensorMap tmA_lo, const TcArgs a) {
     using namespace tc;
-    using C = TcCfg<N, NB>;
-    constexpr int R = C::R;
-    constexpr int kChunkDx = kKB * NB;
-    extern __shared__ __align__(1024) unsigned char smem[];
-    unsigned char *stage0 = smem;
-    float *segs = reinterpret_cast<float *>(smem + 2 * C::stage);      // [2][kSeg]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(segs + 2 * kSeg);      // full[2], built[2], empty[2]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 6);
+    using C = TcCfg<S, NB>;
+    constexpr int NP = C::NP, W = C::W, VB = C::VB;
+    extern __shared__ unsigned char smem_raw[];
+    // 1024-B alignment for the swizzled B tiles
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::off_bar);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 16);
     const uint32_t bar0 = smem_u32(bars);
-    auto full_bar = [&](int s) { return bar0 + 8u * s; };
-    auto built_bar = [&](int s) { return bar0 + 16u + 8u * s; };
-    auto empty_bar = [&](int s) { return bar0 + 32u + 8u * s; };
+    // a_full[2] a_empty[2] b_full[2] b_empty[2] acc_empty[2] v_full[2] v_empty[2]
+    auto a_full = [&](int s) { return bar0 + 8u * (0 + s); };
+    auto a_empty = [&](int s) { return bar0 + 8u * (2 + s); };
+    auto b_full = [&](int s) { return bar0 + 8u * (4 + s); };
+    auto b_empty = [&](int s) { return bar0 + 8u * (6 + s); };
+    auto acc_empty = [&](int s) { return bar0 + 8u * (8 + s); };
+    auto v_full = [&](int s) { return bar0 + 8u * (10 + s); };
+    auto v_empty = [&](int s) { return bar0 + 8u * (12 + s); };
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int ntx = (a.ox + kM - 1) / kM;
-    const int px0 = (blockIdx.x % ntx) * kM;
-    const int py = blockIdx.x / ntx;
+    const int tile = blockIdx.x;
+    const int px0 = (tile % a.ntx) * (kM * S);
+    const int py = tile / a.ntx;
     const int split = blockIdx.y;
     const int zx = split % a.nsx, zy = split / a.nsx;
     const int dy_lo = zy * a.dy_split, dy_hi = min(a.by, dy_lo + a.dy_split);
-    const int ncx_all = a.nkb_pad / NB;
-    const int cx_lo = zx * a.cx_split, cx_hi = min(ncx_all, cx_lo + a.cx_split);
-    const int ncx = cx_hi - cx_lo;
-    const int n_it = (dy_hi > dy_lo && ncx > 0) ? (dy_hi - dy_lo) * ncx : 0;
+    const int kb_lo = zx * a.kb_split, kb_hi = min(a.nkb, kb_lo + a.kb_split);
+    const int ncx = kb_hi > kb_lo ? (kb_hi - kb_lo + NB - 1) / NB : 0;   // chunks per d_y
+    const int n_chunks = dy_hi > dy_lo ? (dy_hi - dy_lo) * ncx : 0;
 
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
-            mbar_init(full_bar(s), 1);
-            mbar_init(built_bar(s), kBuilders / 32);
-            mbar_init(empty_bar(s), 1);
+            mbar_init(a_full(s), 1);
+            mbar_init(a_empty(s), 1);
+            mbar_init(b_full(s), kBuildWarps);
+            mbar_init(b_empty(s), 1);
+            mbar_init(acc_empty(s), kThreads / 32);
+            mbar_init(v_full(s), 1);
+            mbar_init(v_empty(s), kBuildWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA_hi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA_lo)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     }
-    constexpr uint32_t kCols = N <= 32 ? 64 : 128;   // two accumulators (chunk parity)
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "n"(kCols)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -252,215 +324,399 @@ __global__ void __launch_bounds__(tc::kThreads, 1) hankel_tc_kernel(TcArgs a) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint32_t sm_u = smem_u32(smem);
 
-    float racc[N];   // warps 0-3: running sum of the drained chunk accumulators (row = TMEM lane)
-#pragma unroll
-    for (int j = 0; j < N; ++j) racc[j] = 0.f;
-    auto drain = [&](int buf) {
-        tc_fence_after();
-#pragma unroll
-        for (int c0 = 0; c0 < N; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * N + c0), v);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) racc[c0 + j] += v[j];
-        }
-        tc_fence_before();
+    auto chunk_geom = [&](int c, int &dy, int &kb0, int &nb) {
+        dy = dy_lo + c / ncx;
+        kb0 = kb_lo + (c % ncx) * NB;
+        nb = min(NB, kb_hi - kb0);
     };
-    if (warp == kBuilders / 32) {
-        // ================= TMA + MMA issuer (one lane) =================
-        if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc(kM, N);
-            for (int it = 0; it < n_it; ++it) {
-                const int s = it & 1;
-                const int dy = dy_lo + it / ncx, cx = cx_lo + it % ncx;
-                const uint32_t st_u = smem_u32(stage0 + s * C::stage);
-                const uint32_t dacc = tmem + s * N;   // accumulator of this chunk (drained by warps 0-3)
-                if (it >= 2) mbar_wait(empty_bar(s), ((it - 2) >> 1) & 1);   // B buffer of stage s free
-                const float *src = a.bpk + ((int64_t)dy * a.nkb_pad + (int64_t)cx * NB) * (2 * N * kKB);
-                mbar_expect_tx(full_bar(s), C::bbytes);
-                bulk_g2s(st_u + 2 * C::strip_bytes, src, C::bbytes, full_bar(s));
-                mbar_wait(built_bar(s), (it >> 1) & 1);
-                mbar_wait(full_bar(s), (it >> 1) & 1);
-                tc_fence_after();
+
+    float racc[128];   // rows 32·(warp%4) + lane, accumulator columns 128·(warp/4) + [0, 128)
 #pragma unroll
-                for (int b = 0; b < NB; ++b) {
+    for (int j = 0; j < 128; ++j) racc[j] = 0.f;
+    const uint32_t drain_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
+    constexpr uint32_t idesc = make_idesc(kM, 256);
+
+    int g = 0;   // k-block counter
+    for (int c = 0; c < n_chunks; ++c) {
+        int dy, kb0, nb;
+        chunk_geom(c, dy, kb0, nb);
+        const int sa = c & 1;
+        if (c >= 2) {   // chunk c-2 finished: drain its accumulator (chunk c-1 keeps the tensor core busy)
+            mbar_wait(a_empty(sa), ((c - 2) >> 1) & 1);
+            drain_acc(racc, drain_base + (uint32_t)(sa * 256));
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acc_empty(sa)) : "memory");
+        }
+        if (warp == 0) {
+            if (lane == 0) {
+                // ---------------- TMA producer ----------------
+                // A strip of chunk c, plane cc: rows (S·row0 + S·i + 4cc) of the hi / lo image planes
+                const int64_t row0 = ((int64_t)a.ldp * (py + dy) + px0 + 32 * kb0) / S;
+                const uint32_t ah = sm_u + C::off_a + sa * 2 * C::a_bytes;
+                mbar_expect_tx(a_full(sa), 2 * C::a_bytes);
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                    const int c1 = cc % (S / 4), r = (int)row0 + cc / (S / 4);
+                    tma_load_2d(ah + cc * C::plane, &tmA_hi, 0, c1, r, a_full(sa));
+                    tma_load_2d(ah + C::a_bytes + cc * C::plane, &tmA_lo, 0, c1, r, a_full(sa));
+                }
+                // filter windows of the chunk's k-blocks: packed entries [dy·lser + 32·kb, + W)
+                for (int b = 0; b < nb; ++b) {
+                    const int gg = g + b, sv = gg % VB;
+                    if (gg >= VB) mbar_wait(v_empty(sv), ((gg - VB) / VB) & 1);
+                    const uint32_t vh = sm_u + C::off_v + sv * 2 * C::v_bytes;
+                    mbar_expect_tx(v_full(sv), 2 * C::v_bytes);
+                    const int u0 = dy * a.lser + 32 * (kb0 + b);
+                    tma_load_2d_true(vh, &tmB, u0, 0, v_full(sv));
+                    tma_load_2d_true(vh + C::v_bytes, &tmB, u0, NP, v_full(sv));
+                }
+            }
+        } else if (warp == 1) {
+            if (lane == 0) {
+                // ---------------- MMA issuer ----------------
+                mbar_wait(a_full(sa), (c >> 1) & 1);
+                if (c >= 2) mbar_wait(acc_empty(sa), ((c - 2) >> 1) & 1);
+                tc_fence_after();
+                const uint32_t dacc = tmem + (uint32_t)(sa * 256);
+                const uint32_t ah = sm_u + C::off_a + sa * 2 * C::a_bytes;
+                for (int b = 0; b < nb; ++b) {
+                    const int gg = g + b, sb = gg & 1;
+                    mbar_wait(b_full(sb), (gg >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t bh = sm_u + C::off_b + sb * 2 * C::b_bytes;
 #pragma unroll
                     for (int ks = 0; ks < kKB / 8; ++ks) {
-                        // k-block b of the chunk = strip rows [32b, 32b + 128) = 4 atoms further
-                        const uint32_t a_hi = st_u + b * 4096 + ks * 32;
-                        const uint32_t b_hi = st_u + 2 * C::strip_bytes + b * C::bblock + ks * 32;
-                        const uint64_t dAh = make_desc(a_hi);
-                        const uint64_t dAl = make_desc(a_hi + C::strip_bytes);
-                        const uint64_t dBh = make_desc(b_hi);
-                        const uint64_t dBl = make_desc(b_hi + N * 128);
+                        const uint32_t ao = ah + (2 * ks) * C::plane + (b * C::RS) * 16;
+                        const uint64_t dAh = make_desc_interleave(ao, C::plane);
+                        const uint64_t dAl = make_desc_interleave(ao + C::a_bytes, C::plane);
+                        const uint64_t dBh = make_desc(bh + ks * 32);
+                        const uint64_t dBl = make_desc(bh + C::b_bytes + ks * 32);
                         const uint32_t acc0 = (b > 0 || ks > 0) ? 1u : 0u;   // fresh accumulator per chunk
                         mma_tf32(dacc, dAh, dBl, idesc, acc0);
                         mma_tf32(dacc, dAl, dBh, idesc, 1u);
                         mma_tf32(dacc, dAh, dBh, idesc, 1u);
                     }
+                    mma_commit(b_empty(sb));
                 }
-                mma_commit(empty_bar(s));
+                mma_commit(a_empty(sa));
+            }
+        } else {
+            // ---------------- B tile builders (warps 2-7) ----------------
+            // B[t, (s, j)] = in[t − s, d_y; j]: phase tile s, row j, 16-B chunk cc holds packed window
+            // entries u = 4cc + q − s + LEAD (q < 4).  Item = (j, cc): NCH aligned 16-B loads cover all S
+            // phases; lanes run over cc fastest (conflict-free loads and swizzled stores).
+            const int bt = tid - 64;
+            for (int b = 0; b < nb; ++b) {
+                const int gg = g + b, sv = gg % VB, sb = gg & 1;
+                mbar_wait(v_full(sv), (gg / VB) & 1);
+                if (gg >= 2) mbar_wait(b_empty(sb), ((gg - 2) >> 1) & 1);
+                const float *vh = reinterpret_cast<const float *>(smem + C::off_v + sv * 2 * C::v_bytes);
+                unsigned char *bh = smem + C::off_b + sb * 2 * C::b_bytes;
+                for (int e = bt; e < NP * 8; e += kBuildWarps * 32) {
+                    const int cc = e & 7, j = e >> 3;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const float4 *src = reinterpret_cast<const float4 *>(vh + h * (C::v_bytes / 4) + j * W + 4 * cc);
+                        float win[4 * C::NCH];
+#pragma unroll
+                        for (int q = 0; q < C::NCH; ++q) {
+                            const float4 v = src[q];
+                            win[4 * q] = v.x; win[4 * q + 1] = v.y; win[4 * q + 2] = v.z; win[4 * q + 3] = v.w;
+                        }
+#pragma unroll
+                        for (int sph = 0; sph < S; ++sph) {
+                            const int o = C::LEAD - sph;
+                            *reinterpret_cast<float4 *>(bh + h * C::b_bytes + sw128_off(sph * NP + j, cc)) =
+                                make_float4(win[o], win[o + 1], win[o + 2], win[o + 3]);
+                        }
+                    }
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b_full(sb)) : "memory");
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(v_empty(sv)) : "memory");
+                }
             }
         }
         __syncwarp();
-    } else {
-        // ================= strip builders (warps 0-7) =================
-        const float *xcol_base = a.x + px0;
-        // image segment of column p_y + d_y from row p_x0 + d_x0 (zero past the edge), one
-        // element per builder thread, prefetched one chunk ahead into a register
-        auto seg_load = [&](int it2) -> float {
-            const int dy2 = dy_lo + it2 / ncx, dx2 = (cx_lo + it2 % ncx) * kChunkDx;
-            return (tid < a.nx - (px0 + dx2)) ? xcol_base[a.ldx * (int64_t)(py + dy2) + dx2 + tid] : 0.f;
-        };
-        float pre = n_it > 0 ? seg_load(0) : 0.f;
-        for (int it = 0; it < n_it; ++it) {
-            const int s = it & 1;
-            unsigned char *st = stage0 + s * C::stage;
-            float *seg = segs + s * kSeg;
-            seg[tid] = pre;
-            asm volatile("bar.sync 1, %0;" ::"n"(kBuilders) : "memory");   // builders only
-            if (it + 1 < n_it) pre = seg_load(it + 1);
-            // the strip of stage s is free once the MMAs of chunk it-2 have completed
-            if (it >= 2) {
-                mbar_wait(empty_bar(s), ((it - 2) >> 1) & 1);
-                // drain chunk it-2's accumulator before the MMAs of chunk it overwrite it: the
-                // tensor core accumulates with truncation, so partial sums are kept short
-                // (NB·32 terms) and summed here in fp32 with round-to-nearest
-                if (warp < 4) drain(s);
-            }
-            // strip S[i, jj] = seg[i + jj] -> hi / lo swizzled K-major tiles (row i, chunk jj/4)
-            for (int item = tid; item < R * 8; item += kBuilders) {
-                const int i = item % R, c = item / R;
-                const float v0 = seg[i + 4 * c], v1 = seg[i + 4 * c + 1], v2 = seg[i + 4 * c + 2],
-                            v3 = seg[i + 4 * c + 3];
-                const uint32_t h0 = tf32_rna(v0), h1 = tf32_rna(v1), h2 = tf32_rna(v2), h3 = tf32_rna(v3);
-                const uint32_t off = sw128_off(i, c);
-                *reinterpret_cast<uint4 *>(st + off) = make_uint4(h0, h1, h2, h3);
-                *reinterpret_cast<float4 *>(st + C::strip_bytes + off) =
-                    make_float4(v0 - __uint_as_float(h0), v1 - __uint_as_float(h1), v2 - __uint_as_float(h2),
-                                v3 - __uint_as_float(h3));
-            }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(built_bar(s)) : "memory");
-        }
+        g += nb;
     }
-    // ---- epilogue: drain the last (up to two) chunks, then rows -> output / split partials
-    if (warp < 4) {
-        for (int it = (n_it >= 2 ? n_it - 2 : 0); it < n_it; ++it) {
-            mbar_wait(empty_bar(it & 1), (it >> 1) & 1);
-            drain(it & 1);
-        }
-        const int m = warp * 32 + lane;
-        const int px = px0 + m;
-        const int64_t nbox = (int64_t)a.ox * a.oy;
-        const int64_t pidx = px + (int64_t)a.ox * py;
-        if (px < a.ox) {
-            if (a.nsplit == 1) {
+    // drain the last (up to two) chunks
+    for (int c = (n_chunks >= 2 ? n_chunks - 2 : 0); c < n_chunks; ++c) {
+        mbar_wait(a_empty(c & 1), (c >> 1) & 1);
+        drain_acc(racc, drain_base + (uint32_t)((c & 1) * 256));
+    }
+    // ---- epilogue: racc (row m, column n = 128·(warp/4) + jj) -> shared tile T[n][m] (the
+    // B stages are free now) -> coalesced writes of p_x = p_x0 + S·m + s, filter j (n = s·NP + j)
+    __syncthreads();
+    float *T = reinterpret_cast<float *>(smem + C::off_b);
+    {
+        const int m = (warp & 3) * 32 + lane;
+        const int nbase = (warp >> 2) * 128;
+#pragma unroll
+        for (int jj = 0; jj < 128; ++jj) T[(nbase + jj) * 128 + m] = racc[jj];
+    }
+    __syncthreads();
+    {
+        constexpr int TX = kM * S;
+        const int nrow = min(TX, a.ox - px0);
+        if (a.nsplit == 1) {
+            for (int e = tid; e < nrow * a.jn; e += kThreads) {
+                const int pl = e % nrow, j = e / nrow;
+                const int m = pl / S, sph = pl % S;
+                const int64_t pidx = (px0 + pl) + (int64_t)a.ox * py;
                 const int64_t oi = a.omap ? (int64_t)a.omap[pidx] : pidx;
-                if (oi >= 0)
-#pragma unroll
-                    for (int j = 0; j < N; ++j) {
-                        const int jj = a.j0 + j;
-                        if (jj < a.k) a.out[oi + a.ldo * (int64_t)jj] = racc[j];
-                    }
-            } else {
-#pragma unroll
-                for (int j = 0; j < N; ++j)
-                    if (a.j0 + j < a.k) a.ws[((int64_t)split * N + j) * nbox + pidx] = racc[j];
+                if (oi >= 0) a.out[oi + a.ldo * (int64_t)(a.j0 + j)] = T[(sph * NP + j) * 128 + m];
             }
+        } else {
+            // split partials: the CL CTAs of a cluster (consecutive splits of this tile) sum their
+            // tiles through distributed shared memory in a fixed order; rank r owns 1/CL of the tile
+            const int CL = a.cluster;
+            const uint32_t rank = cluster_ctarank();
+            cluster_sync();
+            const int slice = 256 * 128 / CL;
+            const uint32_t t_u = smem_u32(T);
+            float4 *w = reinterpret_cast<float4 *>(a.ws + ((int64_t)(split / CL) * a.ntiles + tile) * (256 * 128));
+            for (int e = (int)rank * slice + 4 * tid; e < ((int)rank + 1) * slice; e += 4 * kThreads) {
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int q = 0; q < CL; ++q) {
+                    const float4 v = ld_dsmem_f4(map_dsmem(t_u + 4u * (uint32_t)e, (uint32_t)q));
+                    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+                }
+                w[e / 4] = acc;
+            }
+            cluster_sync();   // peers may still read this CTA's tile
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols) : "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
-// out[omap(p), j] = Σ_s ws[s][j][p]  (fixed summation order: deterministic)
-__global__ void tc_reduce_kernel(const float *__restrict__ ws, int nsplit, int N, int64_t nbox, int kc,
-                                 const int *__restrict__ omap, float *__restrict__ out, int64_t ldo) {
-    const int64_t n = nbox * kc;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = t % nbox, j = t / nbox;
-        const int64_t oi = omap ? (int64_t)omap[p] : p;
-        if (oi < 0) continue;
-        float s = 0.f;
-        for (int q = 0; q < nsplit; ++q) s += ws[((int64_t)q * N + j) * nbox + p];
-        out[oi + ldo * j] = s;
+// Filter packing for the B windows: bpk[h][j][d_y·lser + u] = split_h(in[u − LEAD, d_y; j0 + j]) (0 outside
+// [0, bx), NP rows, the k-block tail zero-padded).  h = 0: tf32 hi (round to nearest), 1: lo.  LEAD is a
+// multiple of 4 so every window box starts 16-B aligned (TMA faults on unaligned inner coordinates).
+template <int S>
+__global__ void tc_pack_kernel(const float *__restrict__ in, int64_t ldi, const int *__restrict__ imap, int bx,
+                               int by, int j0, int jn, int lser, float *__restrict__ bpk) {
+    // grid: (ceil(lser / 256), by, NP); thread = one packed entry of one filter row
+    constexpr int NP = 256 / S;
+    constexpr int LEAD = TcCfg<S, 4>::LEAD;
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int dy = blockIdx.y, j = blockIdx.z;
+    if (u >= lser) return;
+    const int d = u - LEAD;
+    float v = 0.f;
+    if (j < jn && d >= 0 && d < bx) {
+        const int64_t box = d + (int64_t)bx * dy;
+        const int64_t ci = imap ? (int64_t)imap[box] : box;
+        if (ci >= 0) v = in[ci + ldi * (int64_t)(j0 + j)];
+    }
+    const float hi = __uint_as_float(tc::tf32_rna(v));
+    const int64_t lall = (int64_t)by * lser;
+    const int64_t t = (int64_t)j * lall + (int64_t)dy * lser + u;
+    bpk[t] = hi;
+    bpk[(int64_t)NP * lall + t] = v - hi;
+}
+
+// Image planes (plan-time, once): hi[col·ldp + i] = tf32_rna(x), lo = x − hi; zero for i >= nx.
+__global__ void tc_planes_kernel(const float *__restrict__ x, int64_t ldx, int nx, int ny, int ldp,
+                                 float *__restrict__ hi, float *__restrict__ lo) {
+    const int64_t total = (int64_t)ldp * ny;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t % ldp);
+        const int64_t col = t / ldp;
+        const float v = i < nx ? x[i + ldx * col] : 0.f;
+        const float h = __uint_as_float(tc::tf32_rna(v));
+        hi[t] = h;
+        lo[t] = v - h;
     }
 }
 
-static void reduce_splits_tc(const float *ws, int nsplit, int N, int64_t nbox, int kc, const int *omap, float *out,
-                             int64_t ldo, cudaStream_t st) {
-    const int64_t n = nbox * kc;
-    tc_reduce_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 8 * num_sms()), 256, 0, st>>>(ws, nsplit, N, nbox,
-                                                                                              kc, omap, out, ldo);
-    after_launch("tc_reduce");
+// out[omap(p_x, p_y), j0 + j] = Σ_split ws[split][tile][n][m]   (fixed order: deterministic);
+// threads walk the partials in their storage order (coalesced reads)
+template <int S>
+__global__ void tc_reduce_kernel(const float *__restrict__ ws, int nsplit, int ntiles, int ntx, int ox, int oy,
+                                 int jn, const int *__restrict__ omap, float *__restrict__ out, int64_t ldo) {
+    constexpr int NP = 256 / S;
+    const int64_t per_tile = 256 * 128;
+    const int64_t total = (int64_t)ntiles * per_tile;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int tile = (int)(t / per_tile);
+        const int e = (int)(t % per_tile);
+        const int n = e / 128, m = e % 128;
+        const int sph = n / NP, j = n % NP;
+        const int px = (tile % ntx) * (tc::kM * S) + S * m + sph, py = tile / ntx;
+        if (px >= ox || j >= jn) continue;
+        const int64_t pidx = px + (int64_t)ox * py;
+        const int64_t oi = omap ? (int64_t)omap[pidx] : pidx;
+        if (oi < 0) continue;
+        float acc = 0.f;
+#pragma unroll 8
+        for (int q = 0; q < nsplit; ++q) acc += ws[(int64_t)q * total + t];
+        out[oi + ldo * j] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    SSA_REQUIRE(fn, SSA_ERR_CUDA, "cuTensorMapEncodeTiled is not available");
+    return fn;
+}
+
+static CUtensorMap make_map2(const void *base, uint64_t d0, uint64_t d1, uint64_t s1, uint32_t b0, uint32_t b1,
+                             bool swz128) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {d0, d1};
+    const cuuint64_t strides[1] = {s1};
+    const cuuint32_t box[2] = {b0, b1};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box,
+                                   es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SSA_REQUIRE(r == CUDA_SUCCESS, SSA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return m;
+}
+
+static CUtensorMap make_map3(const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
+                             uint32_t b0, uint32_t b1, uint32_t b2, bool swz128) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {d0, d1, d2};
+    const cuuint64_t strides[2] = {s1, s2};
+    const cuuint32_t box[3] = {b0, b1, b2};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(base), dims, strides, box,
+                                   es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SSA_REQUIRE(r == CUDA_SUCCESS, SSA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    if (std::getenv("SSA_TC_DUMP"))
+        std::fprintf(stderr, "[tc] map base=%p dims=%llu,%llu,%llu strides=%llu,%llu box=%u,%u,%u swz=%d\n", base,
+                     (unsigned long long)d0, (unsigned long long)d1, (unsigned long long)d2, (unsigned long long)s1,
+                     (unsigned long long)s2, b0, b1, b2, (int)swz128);
+    return m;
 }
 
 bool tc_corr_supported(int ox, int oy, int bx, int by, int k) {
-    (void)oy; (void)by; (void)k;
-    return ox >= 96 && bx >= 32;
+    (void)oy; (void)by; (void)k; (void)bx;
+    return ox >= 256;
 }
 
-// k-blocks per chunk: 4 for long reductions, 2 when the reduction box is short (less padding)
-static int tc_nb(int N, int bx) { return (N > 32 || cdiv(bx, tc::kKB) <= 2) ? 2 : 4; }
+int tc_plane_ld(int nx) { return (int)rup(nx + 2304, 16); }
+
+void tc_build_planes(const float *x, int64_t ldx, int nx, int ny, float *hi, float *lo, cudaStream_t st) {
+    const int ldp = tc_plane_ld(nx);
+    const int64_t total = (int64_t)ldp * ny;
+    tc_planes_kernel<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 16 * num_sms()), 256, 0, st>>>(x, ldx, nx, ny,
+                                                                                                 ldp, hi, lo);
+    after_launch("tc_planes");
+}
 
 size_t tc_pack_bytes(int bx, int by, int k) {
-    const int N = k <= 32 ? 32 : 64;
-    const int64_t nkb_pad = rup(cdiv(bx, tc::kKB), tc_nb(N, bx));
-    return sizeof(float) * (size_t)by * nkb_pad * 2 * N * tc::kKB;
+    (void)k;
+    size_t best = 0;
+    for (int S : {4, 8, 16}) {
+        const int NP = 256 / S;
+        const int64_t nkb = cdiv(bx + S - 1, tc::kKB);
+        const int64_t lser = rup((S - 1 + 3) / 4 * 4 + nkb * tc::kKB + 32, 4);
+        best = std::max(best, sizeof(float) * 2 * (size_t)NP * by * lser);
+    }
+    return best;
 }
 
-template <int N, int NB>
+template <int S, int NB>
 static void tc_run(const TcCorrParams &P, int j0, cudaStream_t st) {
-    const int nkb = (int)cdiv(P.bx, tc::kKB);
-    const int nkb_pad = (int)rup(nkb, NB);
-    const int64_t total = (int64_t)P.by * nkb_pad * N * tc::kKB;
-    SSA_REQUIRE(sizeof(float) * (size_t)total * 2 <= P.bpk_bytes, SSA_ERR_ARG, "tc: packing buffer too small");
-    tc_pack_b_kernel<N><<<(unsigned)std::min<int64_t>(cdiv(total, 256), 16 * num_sms()), 256, 0, st>>>(
-        P.in, P.ldi, P.imap, P.bx, P.by, P.k, j0, nkb_pad, P.bpk);
-    after_launch("tc_pack_b");
-
+    using C = TcCfg<S, NB>;
     TcArgs a{};
-    a.x = P.x; a.ldx = P.ldx; a.nx = P.nx;
     a.ox = P.ox; a.oy = P.oy; a.bx = P.bx; a.by = P.by;
-    a.nkb_pad = nkb_pad; a.bpk = P.bpk; a.k = P.k; a.j0 = j0;
+    a.k = P.k; a.j0 = j0; a.jn = std::min(C::NP, P.k - j0);
     a.out = P.out; a.ldo = P.ldo; a.omap = P.omap;
-    // split the reduction (d_y first, then d_x chunks) until ~one wave of CTAs
-    const int64_t tiles = cdiv(P.ox, tc::kM) * P.oy;
-    const int ncx_all = nkb_pad / NB;
-    const int64_t nbox = (int64_t)P.ox * P.oy;
-    const int64_t max_ws = std::max<int64_t>(1, (int64_t)(P.ws_bytes / ((size_t)N * nbox * sizeof(float))));
-    int64_t want = std::max<int64_t>(1, num_sms() / tiles);
-    want = std::min(want, max_ws);
+    a.ldp = tc_plane_ld(P.nx);
+    a.ntx = (int)cdiv(P.ox, tc::kM * S);
+    a.ntiles = a.ntx * P.oy;
+    a.nkb = (int)cdiv(P.bx + S - 1, tc::kKB);
+    a.lser = (int)rup(C::LEAD + (int64_t)a.nkb * tc::kKB + 32, 4);
+    // pack the filters (hi / lo rows, S-1 leading zeros per d_y)
+    const int64_t lall = (int64_t)P.by * a.lser;
+    SSA_REQUIRE(sizeof(float) * 2 * (size_t)C::NP * lall <= P.bpk_bytes, SSA_ERR_ARG, "tc: packing buffer too small");
+    tc_pack_kernel<S><<<dim3((unsigned)cdiv(a.lser, 256), (unsigned)P.by, C::NP), 256, 0, st>>>(
+        P.in, P.ldi, P.imap, P.bx, P.by, j0, a.jn, a.lser, P.bpk);
+    after_launch("tc_pack");
+    // tensor maps: image planes viewed as [rows][S/4][4] (3-D, rows of S floats), packed filters [h][j][u]
+    const uint64_t prow = (uint64_t)a.ldp * P.ny / S;
+    const CUtensorMap mAh = make_map3(P.x_hi, 4, S / 4, prow, 16, (uint64_t)S * 4, 4, 1, C::R, false);
+    const CUtensorMap mAl = make_map3(P.x_lo, 4, S / 4, prow, 16, (uint64_t)S * 4, 4, 1, C::R, false);
+    const CUtensorMap mB = make_map2(P.bpk, (uint64_t)lall, 2 * C::NP, (uint64_t)lall * 4, C::W, C::NP, false);
+    // split the reduction (d_y first, then k-block ranges of whole chunks) to ~one CTA per SM
+    static const int target = [] {
+        const char *e = std::getenv("SSA_TC_CTAS");
+        return e ? std::max(1, std::atoi(e)) : 0;
+    }();
+    const int64_t per_split = (int64_t)a.ntiles * 256 * 128 * sizeof(float);
+    const int64_t max_ws = std::max<int64_t>(1, (int64_t)(P.ws_bytes / per_split));
+    int64_t want = std::max<int64_t>(1, (target ? target : num_sms()) / a.ntiles);
+    want = std::min(want, 8 * max_ws);   // clusters of 8 keep one partial tile per cluster
     int64_t nsy = std::min<int64_t>(want, P.by);
     a.dy_split = (int)cdiv(P.by, nsy);
     nsy = cdiv(P.by, a.dy_split);
-    int64_t nsx = std::max<int64_t>(1, std::min<int64_t>(want / nsy, ncx_all));
-    a.cx_split = (int)cdiv(ncx_all, nsx);
-    nsx = cdiv(ncx_all, a.cx_split);
+    const int64_t nchunk_all = cdiv(a.nkb, NB);
+    int64_t nsx = std::max<int64_t>(1, std::min<int64_t>(want / nsy, nchunk_all));
+    a.kb_split = (int)(cdiv(nchunk_all, nsx) * NB);
+    nsx = cdiv(a.nkb, a.kb_split);
     a.nsx = (int)nsx;
-    a.nsplit = (int)(nsx * nsy);
+    int64_t nsplit = nsx * nsy;
+    // clusters of up to 8 split CTAs reduce their partial tiles on chip (the splits beyond
+    // nsx·nsy have no work and contribute zeros)
+    a.cluster = 1;
+    while (a.cluster < 8 && 2 * a.cluster <= nsplit) a.cluster *= 2;   // power of 2: 16-B aligned slices
+    nsplit = rup(nsplit, a.cluster);
+    a.nsplit = (int)nsplit;
+    SSA_REQUIRE(nsplit == 1 || (nsplit / a.cluster) * per_split <= (int64_t)P.ws_bytes, SSA_ERR_ARG,
+                "tc: split workspace too small");
     a.ws = P.ws;
-    const size_t smem = TcCfg<N, NB>::smem;
-    SSA_CUDA(cudaFuncSetAttribute(hankel_tc_kernel<N, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    hankel_tc_kernel<N, NB><<<dim3((unsigned)tiles, (unsigned)a.nsplit), tc::kThreads, smem, st>>>(a);
+    SSA_CUDA(cudaFuncSetAttribute(hankel_tc_kernel<S, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)a.ntiles, (unsigned)a.nsplit);
+        cfg.blockDim = dim3(tc::kThreads);
+        cfg.dynamicSmemBytes = C::smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1; attr[0].val.clusterDim.y = (unsigned)a.cluster; attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr; cfg.numAttrs = 1;
+        SSA_CUDA(cudaLaunchKernelEx(&cfg, hankel_tc_kernel<S, NB>, mB, mAh, mAl, a));
+    }
     after_launch("hankel_tc");
+    const int nred = a.nsplit / a.cluster;
     if (a.nsplit > 1) {
-        const int kc = std::min(N, P.k - j0);
-        reduce_splits_tc(P.ws, a.nsplit, N, nbox, kc, P.omap, P.out + P.ldo * j0, P.ldo, st);
+        const int64_t n = (int64_t)a.ntiles * 256 * 128;
+        tc_reduce_kernel<S><<<(unsigned)std::min<int64_t>(cdiv(n, 256), 8 * num_sms()), 256, 0, st>>>(
+            P.ws, nred, a.ntiles, a.ntx, P.ox, P.oy, a.jn, P.omap, P.out + P.ldo * j0, P.ldo);
+        after_launch("tc_reduce");
     }
 }
 
 void tc_corr(const TcCorrParams &P, cudaStream_t st) {
     if (P.k <= 0 || P.ox <= 0 || P.oy <= 0) return;
     for (int j0 = 0; j0 < P.k; j0 += 64) {
-        if (P.k - j0 > 32) tc_run<64, 2>(P, j0, st);
-        else if (tc_nb(32, P.bx) == 4) tc_run<32, 4>(P, j0, st);
-        else tc_run<32, 2>(P, j0, st);
+        const int kc = std::min(64, P.k - j0);
+        if (kc > 32) tc_run<4, 4>(P, j0, st);
+        else if (kc > 16) tc_run<8, 4>(P, j0, st);
+        else tc_run<16, 4>(P, j0, st);
     }
 }
 

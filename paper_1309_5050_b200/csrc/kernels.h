@@ -44,7 +44,7 @@ void diagsums_direct(AvgParams<T> P, cudaStream_t st);
 // ---- tensor-core (tcgen05 3xTF32) implicit GEMM, fp32 only (hankel_tc.cu) -------
 // Same operation as CorrParams: out[p, j] = Σ_{d ∈ in-box} x[p + d] in[d, j].
 struct TcCorrParams {
-    const float *x; int64_t ldx; int nx;     // image (zero outside 𝔑), column-major
+    const float *x_hi, *x_lo; int nx, ny;    // tf32 hi / lo planes of the image (tc_build_planes), ld tc_plane_ld(nx)
     int ox, oy;                              // output box
     int bx, by;                              // reduction (input) box
     const float *in; int64_t ldi; const int *imap;   // filters, compact; imap: box -> compact or -1
@@ -54,6 +54,8 @@ struct TcCorrParams {
     float *bpk; size_t bpk_bytes;            // packed hi/lo filters
 };
 bool tc_corr_supported(int ox, int oy, int bx, int by, int k);
+int tc_plane_ld(int nx);
+void tc_build_planes(const float *x, int64_t ldx, int nx, int ny, float *hi, float *lo, cudaStream_t st);
 size_t tc_pack_bytes(int bx, int by, int k);
 void tc_corr(const TcCorrParams &P, cudaStream_t st);
 

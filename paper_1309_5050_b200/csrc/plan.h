@@ -39,6 +39,7 @@ struct PlanImpl {
     size_t ws_corr_bytes = 0;
     DevBuf ws_gram;   // gram partials
     DevBuf tc_bpk;    // packed tf32 hi/lo filters of the tensor-core path
+    DevBuf tc_xhi, tc_xlo;   // tf32 hi / lo planes of the image (built on first use)
     size_t tc_bpk_bytes = 0;
     DevBuf dsmall;    // device scratch for small double matrices
     std::vector<int32_t> lmap_host;   // 𝔏 positions (box indices) in lex order

@@ -97,7 +97,7 @@ struct Gkl {
     bool gpu_ritz = true;
     bool full_k_reorth = false;   // set when K < L (then the K side is the short one)
     bool debug = std::getenv("SSA_DEBUG") != nullptr;
-    bool use_fast = std::getenv("SSA_ORTH_LEGACY") == nullptr;
+    bool use_fast = std::getenv("SSA_ORTH_FAST") != nullptr;   // device-resident orth (experimental)
     DevBuf ow;                    // device workspace of the fast orthonormalisation
     int64_t n_fast = 0, n_fallback = 0;
 
@@ -374,16 +374,20 @@ struct Gkl {
     // every block product is bracketed by CUDA events on the plan's stream so the
     // device time spent in the trajectory products is reported (ms_products)
     std::vector<cudaEvent_t> ev;
+    std::vector<char> ev_xv;   // per event pair: 1 = X·V, 0 = Xᵀ·U
+    int64_t n_xv = 0, n_xtu = 0, vec_xv = 0, vec_xtu = 0;
     void mark() {
         cudaEvent_t e;
         SSA_CUDA(cudaEventCreate(&e));
         SSA_CUDA(cudaEventRecord(e, st));
         ev.push_back(e);
     }
-    double product_ms() {
+    // device milliseconds of the X·V (which = 1) / Xᵀ·U (0) / all (-1) block products
+    double product_ms(int which = -1) {
         double ms = 0.0;
         if (!ev.empty()) SSA_CUDA(cudaEventSynchronize(ev.back()));
         for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+            if (which >= 0 && ev_xv[i / 2] != which) continue;
             float t = 0.f;
             SSA_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
             ms += t;
@@ -397,13 +401,15 @@ struct Gkl {
         mark();
         op_xv<T>(p, Qin, K, Out, L, kc);
         mark();
-        ++nblock; nvec += kc;
+        ev_xv.push_back(1);
+        ++nblock; nvec += kc; ++n_xv; vec_xv += kc;
     }
     void product_xtu(const T *Pin, T *Out, int kc) {
         mark();
         op_xtu<T>(p, Pin, L, Out, K, kc);
         mark();
-        ++nblock; nvec += kc;
+        ev_xv.push_back(0);
+        ++nblock; nvec += kc; ++n_xtu; vec_xtu += kc;
     }
 
     double &Tat(int i, int j) { return Tm[(size_t)i + (size_t)ldT * j]; }
@@ -627,6 +633,12 @@ struct Gkl {
             info->n_vector_products = nvec;
             info->max_rel_residual = maxres;
             info->ms_products = product_ms();
+            info->ms_products_xv = product_ms(1);
+            info->ms_products_xtu = product_ms(0);
+            info->n_products_xv = n_xv;
+            info->n_products_xtu = n_xtu;
+            info->n_vectors_xv = vec_xv;
+            info->n_vectors_xtu = vec_xtu;
             info->ms_ritz = ms_ritz;
         }
         if (nconv < r)
