@@ -76,6 +76,7 @@ struct Staging {
 
 void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st);
 bool jacobi_blocked_fits(int m, int n);
+bool jacobi_smem_fits(int m, int n);
 
 template <typename T>
 struct Gkl {
@@ -543,6 +544,12 @@ struct Gkl {
         // blocks per restart cycle (the projected SVD runs on the device for n up to ~2000)
         int mcyc = 4;
         if (const char *e = std::getenv("SSA_MCYC")) mcyc = std::max(1, std::atoi(e));
+        // prefer cycles whose projected matrix fits the single-CTA shared-memory Jacobi
+        if (!std::getenv("SSA_MCYC") && std::getenv("SSA_JACOBI_SMEM")) {
+            int m2 = mcyc;
+            while (m2 > 2 && !jacobi_smem_fits(pk + (m2 + 1) * k, pk + m2 * k)) --m2;
+            if (jacobi_smem_fits(pk + (m2 + 1) * k, pk + m2 * k)) mcyc = m2;
+        }
         while (mcyc > 2 && !jacobi_blocked_fits(pk + (mcyc + 1) * k, pk + mcyc * k)) --mcyc;
         nQmax = pk + k * (mcyc + 1);
         ldT = nQmax;
