@@ -46,6 +46,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <map>
+#include <tuple>
 #include <mutex>
 
 #include "common.h"
@@ -656,10 +657,28 @@ static void tc_run(const TcCorrParams &P, int j0, cudaStream_t st) {
         P.in, P.ldi, P.imap, P.bx, P.by, j0, a.jn, a.lser, P.bpk);
     after_launch("tc_pack");
     // tensor maps: image planes viewed as [rows][S/4][4] (3-D, rows of S floats), packed filters [h][j][u]
-    const uint64_t prow = (uint64_t)a.ldp * P.ny / S;
-    const CUtensorMap mAh = make_map3(P.x_hi, 4, S / 4, prow, 16, (uint64_t)S * 4, 4, 1, C::R, false);
-    const CUtensorMap mAl = make_map3(P.x_lo, 4, S / 4, prow, 16, (uint64_t)S * 4, 4, 1, C::R, false);
-    const CUtensorMap mB = make_map2(P.bpk, (uint64_t)lall, 2 * C::NP, (uint64_t)lall * 4, C::W, C::NP, false);
+    // tensor maps only encode (address, extents), so a cached map for an identical key is
+    // exactly the map that would be re-encoded: cache them (host encode ~µs per map)
+    struct MapKey {
+        const void *xh, *xl, *bp; int64_t lall; int ldp, ny;
+        bool operator<(const MapKey &o) const {
+            return std::tie(xh, xl, bp, lall, ldp, ny) < std::tie(o.xh, o.xl, o.bp, o.lall, o.ldp, o.ny);
+        }
+    };
+    struct Maps { CUtensorMap ah, al, b; };
+    static thread_local std::map<MapKey, Maps> cache;
+    const MapKey key{P.x_hi, P.x_lo, P.bpk, lall, a.ldp, P.ny};   // one cache per <S, NB> instantiation
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+        if (cache.size() > 256) cache.clear();
+        const uint64_t prow = (uint64_t)a.ldp * P.ny / S;
+        Maps mp;
+        mp.ah = make_map3(P.x_hi, 4, S / 4, prow, 16, (uint64_t)S * 4, 4, 1, C::R, false);
+        mp.al = make_map3(P.x_lo, 4, S / 4, prow, 16, (uint64_t)S * 4, 4, 1, C::R, false);
+        mp.b = make_map2(P.bpk, (uint64_t)lall, 2 * C::NP, (uint64_t)lall * 4, C::W, C::NP, false);
+        it = cache.emplace(key, mp).first;
+    }
+    const CUtensorMap &mAh = it->second.ah, &mAl = it->second.al, &mB = it->second.b;
     // split the reduction (d_y first, then k-block ranges of whole chunks) to ~one CTA per SM
     static const int target = [] {
         const char *e = std::getenv("SSA_TC_CTAS");
@@ -687,7 +706,12 @@ static void tc_run(const TcCorrParams &P, int j0, cudaStream_t st) {
     SSA_REQUIRE(nsplit == 1 || (nsplit / a.cluster) * per_split <= (int64_t)P.ws_bytes, SSA_ERR_ARG,
                 "tc: split workspace too small");
     a.ws = P.ws;
-    SSA_CUDA(cudaFuncSetAttribute(hankel_tc_kernel<S, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
+    static thread_local bool attr_set = false;
+    if (!attr_set) {
+        SSA_CUDA(cudaFuncSetAttribute(hankel_tc_kernel<S, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)C::smem));
+        attr_set = true;
+    }
     {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)a.ntiles, (unsigned)a.nsplit);

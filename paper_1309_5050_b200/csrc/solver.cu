@@ -100,6 +100,10 @@ struct Gkl {
     bool debug = std::getenv("SSA_DEBUG") != nullptr;
     bool use_fast = std::getenv("SSA_ORTH_FAST") != nullptr;   // device-resident orth (experimental)
     DevBuf ow;                    // device workspace of the fast orthonormalisation
+    double tw_prod = 0, tw_orthA = 0, tw_orthB = 0, tw_rec = 0, tw_restart = 0;   // host wall ms (SSA_DEBUG)
+    static double now_ms() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
     int64_t n_fast = 0, n_fallback = 0;
 
     explicit Gkl(PlanImpl &pl) : p(pl), st(pl.st), L(pl.L), K(pl.K) {
@@ -418,7 +422,10 @@ struct Gkl {
     void stepA() {
         const int qc = nQ - k;
         T *W = P(nP);
+        double t0 = now_ms();
         product_xv(Q(qc), W, k);
+        tw_prod += now_ms() - t0;
+        t0 = now_ms();
         if (anorm == 0.0) {
             std::vector<double> G((size_t)k * k);
             gram(L, W, L, k, W, L, k, G.data(), false);
@@ -435,6 +442,7 @@ struct Gkl {
             }
             B = orth(L, W, k, P(0), nP, false, C.data());
         }
+        tw_orthA += now_ms() - t0;
         for (int b = 0; b < k; ++b)
             for (int a = 0; a < nP; ++a) Tat(a, qc + b) = C[a + (size_t)nP * b];
         for (int b = 0; b < k; ++b)
@@ -445,7 +453,9 @@ struct Gkl {
     void stepB() {
         const int pc = nP - k;
         T *W = Q(nQ);
+        double t0 = now_ms();
         product_xtu(P(pc), W, k);
+        tw_prod += now_ms() - t0;
         if (anorm == 0.0) {
             std::vector<double> G((size_t)k * k);
             gram(K, W, K, k, W, K, k, G.data(), true);
@@ -463,7 +473,10 @@ struct Gkl {
                 gemm(K, Q(qc), K, k, Bt.data(), k, k, -1.0, 1.0, W, K);
             }
         };
+        t0 = now_ms();
         recurrence();
+        tw_rec += now_ms() - t0;
+        t0 = now_ms();
         const T *againstK = full_k_reorth ? Q(0) : nullptr;
         const int naK = full_k_reorth ? nQ : 0;
         std::vector<double> Cdummy((size_t)std::max(naK, 1) * k, 0.0);
@@ -474,6 +487,7 @@ struct Gkl {
             }
             Alast = orth(K, W, k, againstK, naK, true);
         }
+        tw_orthB += now_ms() - t0;
         nQ += k;
     }
 
@@ -541,8 +555,11 @@ struct Gkl {
         int extra = std::max(k / 2, r);        // keep ~2r Ritz pairs (parameter sweep)
         if (const char *e = std::getenv("SSA_PK_EXTRA")) extra = std::atoi(e);
         pk = (int)std::min<int64_t>(r + extra, mn);
-        // blocks per restart cycle (the projected SVD runs on the device for n up to ~2000)
-        int mcyc = 4;
+        // blocks per restart cycle: ~4r new vectors per cycle (measured sweep over k and the
+        // cycle length on c1-c3: the projected SVD grows as n³, fewer cycles cost
+        // more products); the projected SVD runs on the device for n up to ~2000
+        int mcyc = (int)std::lround(4.0 * r / k);
+        mcyc = std::max(2, std::min(6, mcyc));
         if (const char *e = std::getenv("SSA_MCYC")) mcyc = std::max(1, std::atoi(e));
         // prefer cycles whose projected matrix fits the single-CTA shared-memory Jacobi
         if (!std::getenv("SSA_MCYC") && std::getenv("SSA_JACOBI_SMEM")) {
@@ -612,6 +629,7 @@ struct Gkl {
             }
             // ---- thick restart keeping pk Ritz pairs
             ++restarts;
+            const double tr0 = now_ms();
             gemm(L, P(0), L, nP, Y.data(), nP, pk, 1.0, 0.0, Ptmp.as<T>(), L);
             gemm(K, Q(0), K, nc, Z.data(), nc, pk, 1.0, 0.0, Qtmp.as<T>(), K);
             SSA_CUDA(cudaMemcpyAsync(P(0), Ptmp.p, sizeof(T) * L * pk, cudaMemcpyDeviceToDevice, st));
@@ -621,7 +639,13 @@ struct Gkl {
             for (int i = 0; i < pk; ++i) Tat(i, i) = th[i];
             nP = pk;
             nQ = pk + k;
+            tw_restart += now_ms() - tr0;
         }
+        if (debug)
+            std::fprintf(stderr, "[ssa] host ms: products %.2f orthL %.2f orthK %.2f recurrence %.2f restart %.2f ritz %.2f "
+                                 "(fast %lld, fallback %lld)\n",
+                         tw_prod, tw_orthA, tw_orthB, tw_rec, tw_restart, ms_ritz, (long long)n_fast,
+                         (long long)n_fallback);
         // sign convention: largest-|.| entry of each U_i positive
         for (int c0 = 0; c0 < r; c0 += 1024) {
             const int nc = std::min(1024, r - c0);
