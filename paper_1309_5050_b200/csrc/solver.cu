@@ -585,11 +585,20 @@ struct Gkl {
         stepB();
         std::vector<double> th, Y, Z, res;
         int nconv = 0, restarts = 0;
+        bool checked_once = false;
+        int first_blocks = (3 * r + k - 1) / k;   // first check once ~3r Ritz vectors exist
+        if (const char *e = std::getenv("SSA_FIRST_BLOCKS")) first_blocks = std::max(1, std::atoi(e));
+        if (first_blocks >= mcyc) checked_once = true;
         double maxres = 0.0;
         for (;;) {
             stepA();
             stepB();
-            if (nQ + k <= nQmax && nblock < maxprod) continue;
+            // the first cycle checks convergence early (after first_blocks blocks): well-separated
+            // signals converge there without paying for a full cycle (c4)
+            const bool cycle_end = !(nQ + k <= nQmax && nblock < maxprod);
+            const bool first_check = (restarts == 0 && !checked_once && nQ >= first_blocks * k + k);
+            if (!first_check && !cycle_end) continue;
+            checked_once = true;
             // ---- Ritz extraction from T (nP x nc)
             const int nc = nQ - k;
             ritz_svd(nP, nc, th, Y, Z);
@@ -627,6 +636,7 @@ struct Gkl {
                 p.r = r;
                 break;
             }
+            if (!cycle_end) continue;   // early check only: keep growing the Krylov basis
             // ---- thick restart keeping pk Ritz pairs
             ++restarts;
             const double tr0 = now_ms();
