@@ -557,3 +557,52 @@ template void apply_inplace<float>(int64_t, float *, int64_t, int, int, const do
 template void apply_inplace<double>(int64_t, double *, int64_t, int, int, const double *, const int *, cudaStream_t);
 
 }  // namespace ssa
+
+namespace ssa {
+// Out (M x n) = A (M x m) · C (m x n, device double), Out != A: thread per (row, group of
+// 8 output columns), grid (ceil(M/128), ceil(n/8)) — enough CTAs for short bases (L side).
+template <typename T>
+__global__ void __launch_bounds__(128)
+gemm_cols_kernel(int64_t M, const T *__restrict__ A, int64_t lda, int m, const double *__restrict__ C, int ldc, int n,
+                 T *__restrict__ Out, int64_t ldo) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *CS = reinterpret_cast<T *>(smem_raw);   // [m][8]
+    const int c0 = blockIdx.y * 8;
+    for (int idx = threadIdx.x; idx < m * 8; idx += blockDim.x) {
+        const int a = idx / 8, b = idx % 8;
+        CS[idx] = (c0 + b < n) ? (T)C[a + (int64_t)ldc * (c0 + b)] : T(0);
+    }
+    __syncthreads();
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= M) return;
+    T acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = T(0);
+    const T *ar = A + row;
+#pragma unroll 4
+    for (int a = 0; a < m; ++a) {
+        const T v = ar[lda * a];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fma(v, CS[a * 8 + j], acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (c0 + j < n) Out[row + ldo * (c0 + j)] = acc[j];
+}
+
+template <typename T>
+void gemm_cols(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, T *Out, int64_t ldo,
+               cudaStream_t st) {
+    if (M <= 0 || n <= 0) return;
+    const size_t smem = sizeof(T) * (size_t)m * 8;
+    SSA_REQUIRE(smem <= 200 * 1024, SSA_ERR_ARG, "gemm_cols: too many input columns");
+    SSA_CUDA(cudaFuncSetAttribute(gemm_cols_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gemm_cols_kernel<T><<<dim3((unsigned)cdiv(M, 128), (unsigned)cdiv(n, 8)), 128, smem, st>>>(M, A, lda, m, C, ldc, n,
+                                                                                            Out, ldo);
+    after_launch("gemm_cols");
+}
+template void gemm_cols<float>(int64_t, const float *, int64_t, int, const double *, int, int, float *, int64_t,
+                               cudaStream_t);
+template void gemm_cols<double>(int64_t, const double *, int64_t, int, const double *, int, int, double *, int64_t,
+                                cudaStream_t);
+}  // namespace ssa

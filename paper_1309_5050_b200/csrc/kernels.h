@@ -80,6 +80,11 @@ template <typename T>
 void gemm_acc(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
               double beta, T *Out, int64_t ldo, cudaStream_t st);
 
+// Out (M x n) = A (M x m) · C (device double); Out != A; column groups across CTAs (short bases).
+template <typename T>
+void gemm_cols(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, T *Out, int64_t ldo,
+               cudaStream_t st);
+
 // Device-resident CGS + CholeskyQR pass (blas.cu): see orth_solve_kernel.
 void orth_solve(const double *G, int na, int kc, int pass, double zthr2, double shift_rel, double thr_chol,
                 double *Mout, double *Ctot, double *Btot, int *flags, cudaStream_t st);

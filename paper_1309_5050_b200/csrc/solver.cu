@@ -376,6 +376,135 @@ struct Gkl {
         return true;
     }
 
+
+    // Orthonormalisation with one host round trip per pass (the default path).  W (M x kc)
+    // follows the na orthonormal columns `against` in the same buffer, so one Gram launch
+    // gives G = [A W]ᵀ W; the host forms C = G[0:na], Gp = WᵀW − CᵀC (= W'ᵀW' for W' = W − A C),
+    // its Cholesky factor R (shifted when needed) and M = [−C R⁻¹; R⁻¹]; one launch applies
+    // W ← [A W]·M.  Pass 2 repeats on the result (CGS2 + CholeskyQR2); a pass 3 runs only if
+    // pass 2 was shifted or its Gram was far from the identity.  Breakdown (a column whose
+    // projected norm is below thr_abs·‖X‖ or numerically zero) is detected on pass 1's Gram,
+    // before W is touched, and handed to the robust `orth` (random refills, SVQB).
+    // Returns B with W_in = A·coef + W_out·B (coef accumulated, as in `orth`).
+    std::vector<double> orth2(int64_t M, T *W, int kc, const T *against, int na, bool kside, double *coef) {
+        // opt-in (SSA_ORTH2=1): measured no faster than `orth` on c2/c3 (the Gram / update
+        // kernels, not the host round trips, dominate the K side), DESIGN.md §5
+        if (kc > 64 || na + kc > 512 || (na > 0 && against + (int64_t)na * M != W) || !std::getenv("SSA_ORTH2"))
+            return orth(M, W, kc, against, na, kside, coef);
+        T *A = na > 0 ? const_cast<T *>(against) : W;
+        const int n1 = na + kc;
+        std::vector<double> G((size_t)n1 * kc), Gp((size_t)kc * kc), R, Sinv, Mc((size_t)n1 * kc);
+        std::vector<double> Ctot((size_t)na * kc, 0.0), Btot((size_t)kc * kc, 0.0);
+        const double shift_rel = (sizeof(T) == 4) ? 1e-6 : 1e-13;
+        bool prev_shifted = false;
+        for (int pass = 1; pass <= 3; ++pass) {
+            gram(M, A, M, n1, W, M, kc, G.data(), kside);
+            double dmax = 0.0, dev = 0.0;
+            for (int b = 0; b < kc; ++b)
+                for (int a = 0; a <= b; ++a) {
+                    double v = G[na + a + (size_t)n1 * b];
+                    for (int t = 0; t < na; ++t) v -= G[t + (size_t)n1 * a] * G[t + (size_t)n1 * b];
+                    Gp[a + (size_t)kc * b] = v;
+                    Gp[b + (size_t)kc * a] = v;
+                }
+            for (int j = 0; j < kc; ++j) dmax = std::max(dmax, Gp[j + (size_t)kc * j]);
+            for (int b = 0; b < kc; ++b)
+                for (int a = 0; a < kc; ++a) dev = std::max(dev, std::fabs(Gp[a + (size_t)kc * b] - (a == b ? 1.0 : 0.0)));
+            bool trouble = !(dmax > 0.0) || !std::isfinite(dmax);
+            if (pass == 1)
+                for (int j = 0; j < kc && !trouble; ++j) {
+                    const double d = Gp[j + (size_t)kc * j];
+                    const double nrm = std::sqrt(std::max(d, 0.0));
+                    trouble = !(nrm > thr_abs * std::max(anorm, 1e-300)) || !(d > 1e-24 * dmax) ||
+                              !(d > (sizeof(T) == 4 ? 1e-12 : 1e-24) * G[na + j + (size_t)n1 * j]);   // cancellation
+                }
+            if (trouble) {
+                if (pass == 1) { ++n_fallback; return orth(M, W, kc, against, na, kside, coef); }
+                break;   // W is a valid block already: finish with the robust path below
+            }
+            bool shifted = false, ok = cholesky(kc, Gp.data(), 0.0, thr_chol, R);
+            if (!ok) { ok = cholesky(kc, Gp.data(), shift_rel * dmax, 1e-300, R); shifted = ok; }
+            if (!ok) break;
+            upper_inverse(kc, R, Sinv);
+            for (int b = 0; b < kc; ++b) {
+                for (int t = 0; t < na; ++t) {
+                    double v = 0.0;
+                    for (int a = 0; a <= b; ++a) v -= G[t + (size_t)n1 * a] * Sinv[a + (size_t)kc * b];
+                    Mc[t + (size_t)n1 * b] = v;
+                }
+                for (int a = 0; a < kc; ++a) Mc[na + a + (size_t)n1 * b] = Sinv[a + (size_t)kc * b];
+            }
+            apply(M, A, n1, kc, Mc.data());
+            // coefficients: W_in = A·Ctot + W·Btot
+            if (pass == 1) {
+                for (int b = 0; b < kc; ++b)
+                    for (int t = 0; t < na; ++t) Ctot[t + (size_t)na * b] = G[t + (size_t)n1 * b];
+                Btot = R;
+            } else {
+                for (int b = 0; b < kc; ++b)
+                    for (int t = 0; t < na; ++t) {
+                        double v = 0.0;
+                        for (int a = 0; a < kc; ++a) v += G[t + (size_t)n1 * a] * Btot[a + (size_t)kc * b];
+                        Ctot[t + (size_t)na * b] += v;
+                    }
+                std::vector<double> Bn((size_t)kc * kc, 0.0);
+                for (int b = 0; b < kc; ++b)
+                    for (int a = 0; a < kc; ++a) {
+                        double v = 0.0;
+                        for (int t = a; t < kc; ++t) v += R[a + (size_t)kc * t] * Btot[t + (size_t)kc * b];
+                        Bn[a + (size_t)kc * b] = v;
+                    }
+                Btot.swap(Bn);
+            }
+            const bool good = pass >= 2 && !shifted && !prev_shifted && dev <= 0.1;
+            prev_shifted = shifted;
+            if (good) {
+                if (coef)
+                    for (size_t t = 0; t < Ctot.size(); ++t) coef[t] += Ctot[t];
+                ++n_fast;
+                return Btot;
+            }
+        }
+        // not converged in three passes (or a later pass broke down): the robust path finishes
+        // from the current W; compose its coefficients with the ones gathered so far
+        ++n_fallback;
+        std::vector<double> C2((size_t)na * kc, 0.0);
+        std::vector<double> B2 = orth(M, W, kc, against, na, kside, C2.data());
+        if (coef)
+            for (int b = 0; b < kc; ++b)
+                for (int t = 0; t < na; ++t) {
+                    double v = Ctot[t + (size_t)na * b];
+                    for (int a = 0; a < kc; ++a) v += C2[t + (size_t)na * a] * Btot[a + (size_t)kc * b];
+                    coef[t + (size_t)na * b] += v;
+                }
+        std::vector<double> Bn((size_t)kc * kc, 0.0);
+        for (int b = 0; b < kc; ++b)
+            for (int a = 0; a < kc; ++a) {
+                double v = 0.0;
+                for (int t = 0; t < kc; ++t) v += B2[a + (size_t)kc * t] * Btot[t + (size_t)kc * b];
+                Bn[a + (size_t)kc * b] = v;
+            }
+        return Bn;
+    }
+
+    // W (= the last kc of the n1 columns of A) ← A[:, 0:n1] · Mc (n1 x kc, host).  Large M:
+    // in place, thread per row; small M: out of place into scratch with column groups across
+    // CTAs (enough parallelism), then copied back.
+    DevBuf oop;
+    void apply(int64_t M, T *A, int n1, int kc, const double *Mc) {
+        const size_t idx = sg.take((size_t)n1 * kc);
+        std::memcpy(sg.h + idx, Mc, sizeof(double) * n1 * kc);
+        SSA_CUDA(cudaMemcpyAsync(sg.dev(idx), sg.h + idx, sizeof(double) * n1 * kc, cudaMemcpyHostToDevice, st));
+        T *W = A + M * (int64_t)(n1 - kc);
+        if (M >= 32768) {
+            apply_inplace<T>(M, A, M, n1, kc, sg.dev(idx), nullptr, st);
+        } else {
+            oop.alloc(sizeof(T) * M * kc, st);
+            gemm_cols<T>(M, A, M, n1, sg.dev(idx), n1, kc, oop.as<T>(), M, st);
+            SSA_CUDA(cudaMemcpyAsync(W, oop.p, sizeof(T) * M * kc, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+
     // every block product is bracketed by CUDA events on the plan's stream so the
     // device time spent in the trajectory products is reported (ms_products)
     std::vector<cudaEvent_t> ev;
@@ -440,7 +569,7 @@ struct Gkl {
                 product_xv(Q(qc), W, k);
                 std::fill(C.begin(), C.end(), 0.0);
             }
-            B = orth(L, W, k, P(0), nP, false, C.data());
+            B = orth2(L, W, k, P(0), nP, false, C.data());
         }
         tw_orthA += now_ms() - t0;
         for (int b = 0; b < k; ++b)
@@ -485,7 +614,7 @@ struct Gkl {
                 product_xtu(P(pc), W, k);
                 recurrence();
             }
-            Alast = orth(K, W, k, againstK, naK, true);
+            Alast = orth2(K, W, k, againstK, naK, true, nullptr);
         }
         tw_orthB += now_ms() - t0;
         nQ += k;
