@@ -24,6 +24,8 @@
 //      (or divide by the hit counts 𝕎 for the averaging).
 // X̂ = DFT2(image) is computed once per plan (it "does not depend on L").
 #include <cmath>
+#include <cstdlib>
+#include <vector>
 
 #include "common.h"
 #include "kernels.h"
@@ -70,52 +72,62 @@ template <typename T, int DIR> __device__ __forceinline__ void dft8(cplx<T> *v) 
     for (int k = 0; k < 4; ++k) { v[k] = cadd(e[k], o[k]); v[k + 4] = csub(e[k], o[k]); }
 }
 
-// One Stockham radix-R stage for `nb` transforms of length N stored back to back.
+// Shared-memory index padding: one spare element per 16 keeps the radix-8 Stockham
+// stores (stride R) and the transposed column accesses free of bank conflicts.
+__device__ __forceinline__ int sp(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr size_t sp_size(size_t n) { return n + (n >> 4) + 1; }
+
+// Twiddle table (per plan, fp64-accurate values rounded to T): tw[t] = exp(−2πi t / 2^lgtw).
+// exp(DIR·2πi·m / 2^lg) = tw[m << (lgtw − lg)] (conjugated for DIR = +1).
+template <typename T, int DIR>
+__device__ __forceinline__ cplx<T> twiddle(const cplx<T> *__restrict__ tw, int idx) {
+    cplx<T> w = tw[idx];
+    if (DIR > 0) w.y = -w.y;
+    return w;
+}
+
+// One Stockham radix-R stage for `nbatch` transforms of length N = 2^lgn stored back to
+// back (padded indices); Ns = 2^lgs is the current span.
 template <typename T, int DIR, int R>
-__device__ __forceinline__ void stockham_stage(const cplx<T> *__restrict__ x, cplx<T> *__restrict__ y, int N, int Ns,
-                                               int nbatch) {
+__device__ __forceinline__ void stockham_stage(const cplx<T> *__restrict__ x, cplx<T> *__restrict__ y, int lgn, int lgs,
+                                               int nbatch, const cplx<T> *__restrict__ tw, int lgtw) {
     constexpr int LR = R == 2 ? 1 : (R == 4 ? 2 : 3);
-    const int lgn = 31 - __clz(N);
-    const int nbf = N >> LR, lgb = lgn - LR;
+    const int N = 1 << lgn, nbf = N >> LR, lgb = lgn - LR;
+    const int Ns = 1 << lgs;
+    const int tsh = lgtw - lgs - LR;
     for (int b = threadIdx.x; b < (nbatch << lgb); b += blockDim.x) {
         const int t = b >> lgb, j = b & (nbf - 1);
-        const cplx<T> *xs = x + (size_t)t * N;
-        cplx<T> *ys = y + (size_t)t * N;
+        const int base_in = t * N;
         cplx<T> v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = xs[j + r * nbf];
+        for (int r = 0; r < R; ++r) v[r] = x[sp(base_in + j + r * nbf)];
         const int k = j & (Ns - 1);
         if (Ns > 1) {
-            T s, c;
-            sincospi_t((T)(2 * DIR) * (T)k / (T)(Ns * R), &s, &c);
-            const cplx<T> w1{c, s};
-            cplx<T> w = w1;
 #pragma unroll
-            for (int r = 1; r < R; ++r) { v[r] = cmul(v[r], w); w = cmul(w, w1); }
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], twiddle<T, DIR>(tw, (k * r) << tsh));
         }
         if (R == 2) dft2<T, DIR>(v);
         else if (R == 4) dft4<T, DIR>(v);
         else dft8<T, DIR>(v);
-        const int base = (j - k) * R + k;
+        const int base = base_in + (j - k) * R + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) ys[base + r * Ns] = v[r];
+        for (int r = 0; r < R; ++r) y[sp(base + r * Ns)] = v[r];
     }
 }
 
 // Batched in-place-by-ping-pong FFT of nbatch transforms of length N = 2^lg in
-// shared memory; returns the buffer that holds the result.  All threads of the
-// CTA take part; the caller has synchronised before the call.
+// shared memory (padded indices); returns the buffer that holds the result.  All
+// threads of the CTA take part; the caller has synchronised before the call.
 template <typename T, int DIR>
-__device__ cplx<T> *fft_batch(cplx<T> *x, cplx<T> *y, int lg, int nbatch) {
-    const int N = 1 << lg;
-    int Ns = 1;
+__device__ cplx<T> *fft_batch(cplx<T> *x, cplx<T> *y, int lg, int nbatch, const cplx<T> *__restrict__ tw, int lgtw) {
+    int lgs = 0;
     const int rem = lg % 3;
-    if (rem == 1) { stockham_stage<T, DIR, 2>(x, y, N, Ns, nbatch); Ns *= 2; }
-    else if (rem == 2) { stockham_stage<T, DIR, 4>(x, y, N, Ns, nbatch); Ns *= 4; }
+    if (rem == 1) { stockham_stage<T, DIR, 2>(x, y, lg, lgs, nbatch, tw, lgtw); lgs += 1; }
+    else if (rem == 2) { stockham_stage<T, DIR, 4>(x, y, lg, lgs, nbatch, tw, lgtw); lgs += 2; }
     if (rem) { __syncthreads(); cplx<T> *t = x; x = y; y = t; }
-    while (Ns < N) {
-        stockham_stage<T, DIR, 8>(x, y, N, Ns, nbatch);
-        Ns *= 8;
+    while (lgs < lg) {
+        stockham_stage<T, DIR, 8>(x, y, lg, lgs, nbatch, tw, lgtw);
+        lgs += 3;
         __syncthreads();
         cplx<T> *t = x; x = y; y = t;
     }
@@ -132,11 +144,12 @@ __device__ cplx<T> *fft_batch(cplx<T> *x, cplx<T> *y, int lg, int nbatch) {
 template <typename T>
 __global__ void __launch_bounds__(256)
 fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, int bx, int by, int jsel_n,
-           const int *__restrict__ jsel, const double *__restrict__ scale, int lgx, int CB, cplx<T> *__restrict__ A) {
+           const int *__restrict__ jsel, const double *__restrict__ scale, int lgx, int CB, cplx<T> *__restrict__ A,
+           const cplx<T> *__restrict__ tw, int lgtw) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int Mx = 1 << lgx, Hx = Mx / 2 + 1;
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
-    cplx<T> *b1 = b0 + (size_t)CB * Mx;
+    cplx<T> *b1 = b0 + sp_size((size_t)CB * Mx);
     const int col0 = blockIdx.x * CB;
     const int jo = blockIdx.y;                       // output vector slot
     const int j = jsel ? jsel[jo] : jo;             // input vector index
@@ -150,14 +163,14 @@ fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, in
             const int64_t ci = map ? (int64_t)map[box] : box;
             if (ci >= 0) v = sc * in[ci + ld * j];
         }
-        b0[idx] = cplx<T>{v, T(0)};
+        b0[sp(idx)] = cplx<T>{v, T(0)};
     }
     __syncthreads();
-    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgx, CB);
+    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgx, CB, tw, lgtw);
     // transposed write: consecutive threads -> consecutive columns
     for (int idx = threadIdx.x; idx < Hx * CB; idx += blockDim.x) {
         const int fx = idx / CB, c = idx - fx * CB;
-        if (c < ncol) A[((int64_t)jo * Hx + fx) * by + col0 + c] = res[(size_t)c * Mx + fx];
+        if (c < ncol) A[((int64_t)jo * Hx + fx) * by + col0 + c] = res[sp(c * Mx + fx)];
     }
 }
 
@@ -170,11 +183,11 @@ fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, in
 template <typename T>
 __global__ void __launch_bounds__(256)
 fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, const cplx<T> *__restrict__ Xh,
-           int mode, cplx<T> *__restrict__ B, int ny_out) {
+           int mode, cplx<T> *__restrict__ B, int ny_out, const cplx<T> *__restrict__ tw, int lgtw) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int My = 1 << lgy;
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
-    cplx<T> *b1 = b0 + (size_t)RB * My;
+    cplx<T> *b1 = b0 + sp_size((size_t)RB * My);
     const int fx0 = blockIdx.x * RB;
     const int j = blockIdx.y;
     const int nrow = min(RB, Hx - fx0);
@@ -182,28 +195,28 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
         const int rr = idx >> lgy, y = idx & (My - 1);
         cplx<T> v{T(0), T(0)};
         if (rr < nrow && y < ny_in) v = A[((int64_t)j * Hx + fx0 + rr) * ny_in + y];
-        b0[idx] = v;
+        b0[sp(idx)] = v;
     }
     __syncthreads();
-    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgy, RB);
+    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgy, RB, tw, lgtw);
     cplx<T> *oth = (res == b0) ? b1 : b0;
     if (mode == 1) {
         for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
             const int rr = idx >> lgy, y = idx & (My - 1);
-            if (rr < nrow) B[((int64_t)j * Hx + fx0 + rr) * My + y] = res[idx];
+            if (rr < nrow) B[((int64_t)j * Hx + fx0 + rr) * My + y] = res[sp(idx)];
         }
         return;
     }
     for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
         const int rr = idx >> lgy, y = idx & (My - 1);
         const cplx<T> xh = (rr < nrow) ? Xh[(int64_t)(fx0 + rr) * My + y] : cplx<T>{T(0), T(0)};
-        res[idx] = cmulconj(xh, res[idx]);
+        res[sp(idx)] = cmulconj(xh, res[sp(idx)]);
     }
     __syncthreads();
-    cplx<T> *out = fft_batch<T, +1>(res, oth, lgy, RB);
+    cplx<T> *out = fft_batch<T, +1>(res, oth, lgy, RB, tw, lgtw);
     for (int idx = threadIdx.x; idx < RB * ny_out; idx += blockDim.x) {
         const int rr = idx / ny_out, y = idx - rr * ny_out;
-        if (rr < nrow) B[((int64_t)j * Hx + fx0 + rr) * ny_out + y] = out[(size_t)rr * My + y];
+        if (rr < nrow) B[((int64_t)j * Hx + fx0 + rr) * ny_out + y] = out[sp(rr * My + y)];
     }
 }
 
@@ -211,18 +224,20 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
 template <typename T>
 __global__ void __launch_bounds__(256)
 fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restrict__ AV, int ky, const int *grp_off,
-                const int *grp_idx, const int *slot, int Hx, int lgy, int RB, cplx<T> *__restrict__ B, int ny_out) {
+                const int *grp_idx, const int *slot, int Hx, int lgy, int RB, cplx<T> *__restrict__ B, int ny_out,
+                const cplx<T> *__restrict__ tw, int lgtw) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int My = 1 << lgy;
+    const size_t bs = sp_size((size_t)RB * My);
     cplx<T> *acc = reinterpret_cast<cplx<T> *>(smem_raw);
-    cplx<T> *u0 = acc + (size_t)RB * My;
-    cplx<T> *u1 = u0 + (size_t)RB * My;
-    cplx<T> *v0 = u1 + (size_t)RB * My;
-    cplx<T> *v1 = v0 + (size_t)RB * My;
+    cplx<T> *u0 = acc + bs;
+    cplx<T> *u1 = u0 + bs;
+    cplx<T> *v0 = u1 + bs;
+    cplx<T> *v1 = v0 + bs;
     const int fx0 = blockIdx.x * RB;
     const int g = blockIdx.y;
     const int nrow = min(RB, Hx - fx0);
-    for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) acc[idx] = cplx<T>{T(0), T(0)};
+    for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) acc[sp(idx)] = cplx<T>{T(0), T(0)};
     for (int t = grp_off[g]; t < grp_off[g + 1]; ++t) {
         const int s = slot[grp_idx[t]];
         __syncthreads();
@@ -233,18 +248,19 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
                 if (y < ly) a = AU[((int64_t)s * Hx + fx0 + rr) * ly + y];
                 if (y < ky) b = AV[((int64_t)s * Hx + fx0 + rr) * ky + y];
             }
-            u0[idx] = a; v0[idx] = b;
+            u0[sp(idx)] = a; v0[sp(idx)] = b;
         }
         __syncthreads();
-        cplx<T> *ru = fft_batch<T, -1>(u0, u1, lgy, RB);
-        cplx<T> *rv = fft_batch<T, -1>(v0, v1, lgy, RB);
-        for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) acc[idx] = cadd(acc[idx], cmul(ru[idx], rv[idx]));
+        cplx<T> *ru = fft_batch<T, -1>(u0, u1, lgy, RB, tw, lgtw);
+        cplx<T> *rv = fft_batch<T, -1>(v0, v1, lgy, RB, tw, lgtw);
+        for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x)
+            acc[sp(idx)] = cadd(acc[sp(idx)], cmul(ru[sp(idx)], rv[sp(idx)]));
     }
     __syncthreads();
-    cplx<T> *out = fft_batch<T, +1>(acc, u0, lgy, RB);
+    cplx<T> *out = fft_batch<T, +1>(acc, u0, lgy, RB, tw, lgtw);
     for (int idx = threadIdx.x; idx < RB * ny_out; idx += blockDim.x) {
         const int rr = idx / ny_out, y = idx - rr * ny_out;
-        if (rr < nrow) B[((int64_t)g * Hx + fx0 + rr) * ny_out + y] = out[(size_t)rr * My + y];
+        if (rr < nrow) B[((int64_t)g * Hx + fx0 + rr) * ny_out + y] = out[sp(rr * My + y)];
     }
 }
 
@@ -257,11 +273,12 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
 template <typename T>
 __global__ void __launch_bounds__(256)
 fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int ox, T inv, T *__restrict__ out,
-           int64_t ldo, const int *__restrict__ omap, const int *__restrict__ w, int64_t stride) {
+           int64_t ldo, const int *__restrict__ omap, const int *__restrict__ w, int64_t stride,
+           const cplx<T> *__restrict__ tw, int lgtw) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int Mx = 1 << lgx;
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
-    cplx<T> *b1 = b0 + (size_t)CB * Mx;
+    cplx<T> *b1 = b0 + sp_size((size_t)CB * Mx);
     const int y0 = blockIdx.x * CB;
     const int j = blockIdx.y;
     const int ncol = min(CB, oy - y0);
@@ -270,22 +287,22 @@ fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int o
         const int fx = idx / CB, c = idx - fx * CB;
         cplx<T> v{T(0), T(0)};
         if (c < ncol) v = B[((int64_t)j * Hx + fx) * oy + y0 + c];
-        b0[(size_t)c * Mx + fx] = v;
+        b0[sp(c * Mx + fx)] = v;
     }
     __syncthreads();
     // Hermitian completion: Z[Mx - f] = conj(Z[f]) for 0 < f < Mx/2
     for (int idx = threadIdx.x; idx < CB * (Mx / 2 - 1); idx += blockDim.x) {
         const int c = idx / (Mx / 2 - 1), f = 1 + idx - c * (Mx / 2 - 1);
-        const cplx<T> v = b0[(size_t)c * Mx + f];
-        b0[(size_t)c * Mx + Mx - f] = cplx<T>{v.x, -v.y};
+        const cplx<T> v = b0[sp(c * Mx + f)];
+        b0[sp(c * Mx + Mx - f)] = cplx<T>{v.x, -v.y};
     }
     __syncthreads();
-    cplx<T> *res = fft_batch<T, +1>(b0, b1, lgx, CB);
+    cplx<T> *res = fft_batch<T, +1>(b0, b1, lgx, CB, tw, lgtw);
     for (int idx = threadIdx.x; idx < CB * ox; idx += blockDim.x) {
         const int c = idx / ox, x = idx - c * ox;
         if (c >= ncol) continue;
         const int y = y0 + c;
-        const T v = res[(size_t)c * Mx + x].x * inv;
+        const T v = res[sp(c * Mx + x)].x * inv;
         if (w) {
             const int wn = w[x + (int64_t)ox * y];
             out[(int64_t)j * stride + x + ldo * y] = wn > 0 ? v / (T)wn : (T)NAN;
@@ -300,6 +317,8 @@ fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int o
 // ---------------------------------------------------------------------------
 struct FftOperator {
     int lgx = 0, lgy = 0, Mx = 0, My = 0, Hx = 0;
+    int lgtw = 0;
+    DevBuf tw;        // cplx[2^lgtw]: exp(−2πi t / 2^lgtw), fp64-accurate
     DevBuf Xh;        // cplx[Hx][My]: DFT2 of the image
     DevBuf bufA, bufB;
     size_t capA = 0, capB = 0;
@@ -319,40 +338,46 @@ bool fft_supported(const PlanImpl &p) {
 }
 
 // transforms per CTA so that a CTA holds ~target complex points (2 buffers)
-static int batch_for(int lg, int target) { return std::max(1, target >> lg); }
+static int batch_for(int lg, int target) {
+    static const int scale = [] { const char *e = std::getenv("SSA_FFT_BATCH"); return e ? std::atoi(e) : 0; }();
+    if (scale > 0) target = scale;
+    return std::max(1, target >> lg);
+}
 
 template <typename T>
-static size_t smem_ab(int lg, int nb) { return sizeof(cplx<T>) * 2 * ((size_t)nb << lg); }
+static size_t smem_ab(int lg, int nb) { return sizeof(cplx<T>) * 2 * sp_size((size_t)nb << lg); }
 
 template <typename T>
 static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int bx, int by, int k, const int *jsel,
                    const double *scale, cplx<T> *A, cudaStream_t st) {
-    const int CB = batch_for(f.lgx, 4096);
+    const int CB = batch_for(f.lgx, 2048);
     const size_t smem = smem_ab<T>(f.lgx, CB);
     SSA_CUDA(cudaFuncSetAttribute(fft_pass_a<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fft_pass_a<T><<<dim3((unsigned)cdiv(by, CB), k), 256, smem, st>>>(in, ld, map, bx, by, k, jsel, scale, f.lgx, CB, A);
+    fft_pass_a<T><<<dim3((unsigned)cdiv(by, CB), k), 256, smem, st>>>(in, ld, map, bx, by, k, jsel, scale, f.lgx, CB, A,
+                                                                        f.tw.as<cplx<T>>(), f.lgtw);
     after_launch("fft_pass_a");
 }
 
 template <typename T>
 static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode, cplx<T> *B, int ny_out, cudaStream_t st) {
-    const int RB = batch_for(f.lgy, 4096);
+    const int RB = batch_for(f.lgy, 2048);
     const size_t smem = smem_ab<T>(f.lgy, RB);
     SSA_CUDA(cudaFuncSetAttribute(fft_pass_b<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fft_pass_b<T><<<dim3((unsigned)cdiv(f.Hx, RB), k), 256, smem, st>>>(A, ny_in, f.Hx, f.lgy, RB,
-                                                                         f.Xh.as<cplx<T>>(), mode, B, ny_out);
+                                                                         f.Xh.as<cplx<T>>(), mode, B, ny_out,
+                                                                         f.tw.as<cplx<T>>(), f.lgtw);
     after_launch("fft_pass_b");
 }
 
 template <typename T>
 static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *out, int64_t ldo, const int *omap,
                    const int *w, int64_t stride, cudaStream_t st) {
-    const int CB = batch_for(f.lgx, 4096);
+    const int CB = batch_for(f.lgx, 2048);
     const size_t smem = smem_ab<T>(f.lgx, CB);
     SSA_CUDA(cudaFuncSetAttribute(fft_pass_c<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const T inv = (T)(1.0 / ((double)f.Mx * (double)f.My));
     fft_pass_c<T><<<dim3((unsigned)cdiv(oy, CB), k), 256, smem, st>>>(B, oy, f.Hx, f.lgx, CB, ox, inv, out, ldo, omap,
-                                                                       w, stride);
+                                                                       w, stride, f.tw.as<cplx<T>>(), f.lgtw);
     after_launch("fft_pass_c");
 }
 
@@ -366,6 +391,18 @@ static void build_impl(PlanImpl &p) {
     FftOperator &f = *p.fft;
     f.lgx = ilog2_ceil(p.nx); f.lgy = ilog2_ceil(p.ny);
     f.Mx = 1 << f.lgx; f.My = 1 << f.lgy; f.Hx = f.Mx / 2 + 1;
+    f.lgtw = std::max(f.lgx, f.lgy);
+    {
+        const size_t nt = (size_t)1 << f.lgtw;
+        std::vector<cplx<T>> h(nt);
+        for (size_t t = 0; t < nt; ++t) {
+            const double a = -2.0 * M_PI * (double)t / (double)nt;
+            h[t] = cplx<T>{(T)std::cos(a), (T)std::sin(a)};
+        }
+        f.tw.alloc(sizeof(cplx<T>) * nt, p.st);
+        SSA_CUDA(cudaMemcpyAsync(f.tw.p, h.data(), sizeof(cplx<T>) * nt, cudaMemcpyHostToDevice, p.st));
+        SSA_CUDA(cudaStreamSynchronize(p.st));
+    }
     f.Xh.alloc(sizeof(cplx<T>) * (size_t)f.Hx * f.My, p.st);
     DevBuf tmp;
     tmp.alloc(sizeof(cplx<T>) * (size_t)f.Hx * p.ny, p.st);
@@ -425,11 +462,11 @@ void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, co
     pass_a<T>(f, V, p.K, p.full_k ? nullptr : p.kmap.as<int>(), p.kx, p.ky, nu, jsel.as<int>(), nullptr,
               AV.as<cplx<T>>(), p.st);
     const int RB = batch_for(f.lgy, 2048);
-    const size_t smem = sizeof(cplx<T>) * 5 * ((size_t)RB << f.lgy);
+    const size_t smem = sizeof(cplx<T>) * 5 * sp_size((size_t)RB << f.lgy);
     SSA_CUDA(cudaFuncSetAttribute(fft_pass_b_conv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fft_pass_b_conv<T><<<dim3((unsigned)cdiv(f.Hx, RB), ng), 256, smem, p.st>>>(
         AU.as<cplx<T>>(), p.ly, AV.as<cplx<T>>(), p.ky, grp_off_dev, grp_idx_dev, slot_dev, f.Hx, f.lgy, RB,
-        B.as<cplx<T>>(), p.ny);
+        B.as<cplx<T>>(), p.ny, f.tw.as<cplx<T>>(), f.lgtw);
     after_launch("fft_pass_b_conv");
     pass_c<T>(f, B.as<cplx<T>>(), p.ny, ng, p.nx, out, p.nx, nullptr, p.weights.as<int>(), (int64_t)p.nx * p.ny, p.st);
     SSA_CUDA(cudaStreamSynchronize(p.st));
