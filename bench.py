@@ -5,7 +5,7 @@ One STEP = one pass of the whole hot path over one
 synthetic input: plan (embedding: shapes, 𝔎, weights), block-Lanczos rank-r
 decomposition driven by X·V / Xᵀ·U block products, and the grouped diagonal-
 averaging reconstruction.  Default workload: BASELINE.json configs[1] (c2, MSSA
-8 x 4096, L = 1024, r = 16, block k = 16); --config c1..c5 selects another.
+8 x 4096, L = 1024, r = 16, block k = 32); --config c1..c5 selects another.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
 

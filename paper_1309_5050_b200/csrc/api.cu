@@ -250,7 +250,7 @@ static void choose_paths(PlanImpl &p) {
                 double best = 1e300;
                 for (auto &c : cand) {
                     // never time a candidate predicted > 20 ms or > 8x the best measured
-                    if (c.second > 2e4 || c.second > 8.0 * best * 1e3) continue;
+                    if (c.second > 2e4 || c.second > 3.0 * best * 1e3) continue;
                     const double ms = time_product<T>(p, xv, c.first, k, bin.as<T>(), bout.as<T>());
                     if (ms < best) { best = ms; choice = c.first; }
                 }

@@ -149,28 +149,44 @@ fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, in
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int Mx = 1 << lgx, Hx = Mx / 2 + 1;
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
-    cplx<T> *b1 = b0 + sp_size((size_t)CB * Mx);
+    cplx<T> *b1 = b0 + sp_size((size_t)(CB >> 1) * Mx);   // CB/2 complex transforms
+    // two real columns per complex transform (NT = CB/2 transforms): z = x_a + i·x_b,
+    // X_a[f] = (Z[f] + conj Z[-f]) / 2,  X_b[f] = (Z[f] - conj Z[-f]) / (2i)
+    const int NT = CB >> 1;
     const int col0 = blockIdx.x * CB;
     const int jo = blockIdx.y;                       // output vector slot
     const int j = jsel ? jsel[jo] : jo;             // input vector index
     const T sc = scale ? (T)scale[j] : T(1);
     const int ncol = min(CB, by - col0);
-    for (int idx = threadIdx.x; idx < CB * Mx; idx += blockDim.x) {
-        const int c = idx >> lgx, ix = idx & (Mx - 1);
-        T v = T(0);
-        if (c < ncol && ix < bx) {
-            const int64_t box = ix + (int64_t)bx * (col0 + c);
-            const int64_t ci = map ? (int64_t)map[box] : box;
-            if (ci >= 0) v = sc * in[ci + ld * j];
+    #pragma unroll 8
+    for (int idx = threadIdx.x; idx < NT * Mx; idx += blockDim.x) {
+        const int t = idx >> lgx, ix = idx & (Mx - 1);
+        T v[2] = {T(0), T(0)};
+        if (ix < bx) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = 2 * t + h;
+                if (c < ncol) {
+                    const int64_t box = ix + (int64_t)bx * (col0 + c);
+                    const int64_t ci = map ? (int64_t)map[box] : box;
+                    if (ci >= 0) v[h] = sc * in[ci + ld * j];
+                }
+            }
         }
-        b0[sp(idx)] = cplx<T>{v, T(0)};
+        b0[sp(idx)] = cplx<T>{v[0], v[1]};
     }
     __syncthreads();
-    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgx, CB, tw, lgtw);
+    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgx, NT, tw, lgtw);
     // transposed write: consecutive threads -> consecutive columns
+    #pragma unroll 8
     for (int idx = threadIdx.x; idx < Hx * CB; idx += blockDim.x) {
         const int fx = idx / CB, c = idx - fx * CB;
-        if (c < ncol) A[((int64_t)jo * Hx + fx) * by + col0 + c] = res[sp(c * Mx + fx)];
+        if (c >= ncol) continue;
+        const int t = c >> 1;
+        const cplx<T> z = res[sp(t * Mx + fx)], zm = res[sp(t * Mx + ((Mx - fx) & (Mx - 1)))];
+        const cplx<T> out = (c & 1) ? cplx<T>{(z.y + zm.y) * T(0.5), (zm.x - z.x) * T(0.5)}
+                                    : cplx<T>{(z.x + zm.x) * T(0.5), (z.y - zm.y) * T(0.5)};
+        A[((int64_t)jo * Hx + fx) * by + col0 + c] = out;
     }
 }
 
@@ -191,6 +207,7 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
     const int fx0 = blockIdx.x * RB;
     const int j = blockIdx.y;
     const int nrow = min(RB, Hx - fx0);
+    #pragma unroll 8
     for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
         const int rr = idx >> lgy, y = idx & (My - 1);
         cplx<T> v{T(0), T(0)};
@@ -201,12 +218,14 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
     cplx<T> *res = fft_batch<T, -1>(b0, b1, lgy, RB, tw, lgtw);
     cplx<T> *oth = (res == b0) ? b1 : b0;
     if (mode == 1) {
+        #pragma unroll 8
         for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
             const int rr = idx >> lgy, y = idx & (My - 1);
             if (rr < nrow) B[((int64_t)j * Hx + fx0 + rr) * My + y] = res[sp(idx)];
         }
         return;
     }
+    #pragma unroll 8
     for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
         const int rr = idx >> lgy, y = idx & (My - 1);
         const cplx<T> xh = (rr < nrow) ? Xh[(int64_t)(fx0 + rr) * My + y] : cplx<T>{T(0), T(0)};
@@ -214,6 +233,7 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
     }
     __syncthreads();
     cplx<T> *out = fft_batch<T, +1>(res, oth, lgy, RB, tw, lgtw);
+    #pragma unroll 8
     for (int idx = threadIdx.x; idx < RB * ny_out; idx += blockDim.x) {
         const int rr = idx / ny_out, y = idx - rr * ny_out;
         if (rr < nrow) B[((int64_t)j * Hx + fx0 + rr) * ny_out + y] = out[sp(rr * My + y)];
@@ -241,6 +261,7 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
     for (int t = grp_off[g]; t < grp_off[g + 1]; ++t) {
         const int s = slot[grp_idx[t]];
         __syncthreads();
+        #pragma unroll 8
         for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
             const int rr = idx >> lgy, y = idx & (My - 1);
             cplx<T> a{T(0), T(0)}, b{T(0), T(0)};
@@ -258,6 +279,7 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
     }
     __syncthreads();
     cplx<T> *out = fft_batch<T, +1>(acc, u0, lgy, RB, tw, lgtw);
+    #pragma unroll 8
     for (int idx = threadIdx.x; idx < RB * ny_out; idx += blockDim.x) {
         const int rr = idx / ny_out, y = idx - rr * ny_out;
         if (rr < nrow) B[((int64_t)g * Hx + fx0 + rr) * ny_out + y] = out[sp(rr * My + y)];
@@ -278,31 +300,33 @@ fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int o
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int Mx = 1 << lgx;
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
-    cplx<T> *b1 = b0 + sp_size((size_t)CB * Mx);
+    cplx<T> *b1 = b0 + sp_size((size_t)(CB >> 1) * Mx);   // CB/2 complex transforms
+    // two output columns per complex inverse transform (NT = CB/2): Z = Y_a + i·Y_b over the
+    // full spectrum (Hermitian completion of each half spectrum), Re z = y_a, Im z = y_b
+    const int NT = CB >> 1;
     const int y0 = blockIdx.x * CB;
     const int j = blockIdx.y;
     const int ncol = min(CB, oy - y0);
-    // coalesced transposing load of the half spectrum
-    for (int idx = threadIdx.x; idx < Hx * CB; idx += blockDim.x) {
-        const int fx = idx / CB, c = idx - fx * CB;
-        cplx<T> v{T(0), T(0)};
-        if (c < ncol) v = B[((int64_t)j * Hx + fx) * oy + y0 + c];
-        b0[sp(c * Mx + fx)] = v;
+    #pragma unroll 8
+    for (int idx = threadIdx.x; idx < Hx * NT; idx += blockDim.x) {
+        const int fx = idx / NT, t = idx - fx * NT;
+        cplx<T> ya{T(0), T(0)}, yb{T(0), T(0)};
+        const int64_t base = ((int64_t)j * Hx + fx) * oy + y0 + 2 * t;
+        if (2 * t < ncol) ya = B[base];
+        if (2 * t + 1 < ncol) yb = B[base + 1];
+        if (fx == 0 || fx == Mx / 2) { ya.y = T(0); yb.y = T(0); }   // real signals: these bins are real
+        b0[sp(t * Mx + fx)] = cplx<T>{ya.x - yb.y, ya.y + yb.x};
+        if (fx > 0 && fx < Mx / 2) b0[sp(t * Mx + Mx - fx)] = cplx<T>{ya.x + yb.y, yb.x - ya.y};
     }
     __syncthreads();
-    // Hermitian completion: Z[Mx - f] = conj(Z[f]) for 0 < f < Mx/2
-    for (int idx = threadIdx.x; idx < CB * (Mx / 2 - 1); idx += blockDim.x) {
-        const int c = idx / (Mx / 2 - 1), f = 1 + idx - c * (Mx / 2 - 1);
-        const cplx<T> v = b0[sp(c * Mx + f)];
-        b0[sp(c * Mx + Mx - f)] = cplx<T>{v.x, -v.y};
-    }
-    __syncthreads();
-    cplx<T> *res = fft_batch<T, +1>(b0, b1, lgx, CB, tw, lgtw);
+    cplx<T> *res = fft_batch<T, +1>(b0, b1, lgx, NT, tw, lgtw);
+    #pragma unroll 8
     for (int idx = threadIdx.x; idx < CB * ox; idx += blockDim.x) {
         const int c = idx / ox, x = idx - c * ox;
         if (c >= ncol) continue;
         const int y = y0 + c;
-        const T v = res[sp(c * Mx + x)].x * inv;
+        const cplx<T> z = res[sp((c >> 1) * Mx + x)];
+        const T v = ((c & 1) ? z.y : z.x) * inv;
         if (w) {
             const int wn = w[x + (int64_t)ox * y];
             out[(int64_t)j * stride + x + ldo * y] = wn > 0 ? v / (T)wn : (T)NAN;
@@ -350,8 +374,8 @@ static size_t smem_ab(int lg, int nb) { return sizeof(cplx<T>) * 2 * sp_size((si
 template <typename T>
 static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int bx, int by, int k, const int *jsel,
                    const double *scale, cplx<T> *A, cudaStream_t st) {
-    const int CB = batch_for(f.lgx, 2048);
-    const size_t smem = smem_ab<T>(f.lgx, CB);
+    const int CB = 2 * batch_for(f.lgx, 2048);   // real columns (two per complex transform)
+    const size_t smem = smem_ab<T>(f.lgx, CB / 2);
     SSA_CUDA(cudaFuncSetAttribute(fft_pass_a<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fft_pass_a<T><<<dim3((unsigned)cdiv(by, CB), k), 256, smem, st>>>(in, ld, map, bx, by, k, jsel, scale, f.lgx, CB, A,
                                                                         f.tw.as<cplx<T>>(), f.lgtw);
@@ -372,8 +396,8 @@ static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode,
 template <typename T>
 static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *out, int64_t ldo, const int *omap,
                    const int *w, int64_t stride, cudaStream_t st) {
-    const int CB = batch_for(f.lgx, 2048);
-    const size_t smem = smem_ab<T>(f.lgx, CB);
+    const int CB = 2 * batch_for(f.lgx, 2048);   // output columns (two per complex transform)
+    const size_t smem = smem_ab<T>(f.lgx, CB / 2);
     SSA_CUDA(cudaFuncSetAttribute(fft_pass_c<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const T inv = (T)(1.0 / ((double)f.Mx * (double)f.My));
     fft_pass_c<T><<<dim3((unsigned)cdiv(oy, CB), k), 256, smem, st>>>(B, oy, f.Hx, f.lgx, CB, ox, inv, out, ldo, omap,

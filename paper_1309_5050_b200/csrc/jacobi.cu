@@ -240,7 +240,7 @@ jacobi_cluster_kernel(int m, int n, int nb, double *__restrict__ A, float tol, i
 }
 
 template <int MR, int BW>
-static bool launch_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st) {
+static bool launch_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st, float tol) {
     int nb = (int)cdiv(n, BW);
     nb += nb & 1;
     if (nb < 2) nb = 2;
@@ -260,7 +260,6 @@ static bool launch_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = ncta; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr; cfg.numAttrs = 1;
-    float tol = 1e-12f;
     int max_sweeps = 60;
     SSA_CUDA(cudaLaunchKernelEx(&cfg, kern, m, n, nb, T, tol, max_sweeps, sweeps));
     after_launch("jacobi_cluster");
@@ -268,11 +267,12 @@ static bool launch_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st
 }
 
 // prefer the cluster kernel; fall back to the cooperative-grid kernel for large n
-static bool jacobi_try_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st) {
+static bool jacobi_try_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st, float tol) {
     if (std::getenv("SSA_JACOBI_GRID")) return false;
-    if (m <= 128) return n <= 256 ? launch_cluster<4, 8>(m, n, T, sweeps, st) : launch_cluster<4, 16>(m, n, T, sweeps, st);
-    if (m <= 256) return n <= 256 ? launch_cluster<8, 8>(m, n, T, sweeps, st) : launch_cluster<8, 16>(m, n, T, sweeps, st);
-    if (m <= 512) return n <= 256 ? launch_cluster<16, 8>(m, n, T, sweeps, st) : launch_cluster<16, 16>(m, n, T, sweeps, st);
+    if (m <= 128) return n <= 256 ? launch_cluster<4, 8>(m, n, T, sweeps, st, tol) : launch_cluster<4, 16>(m, n, T, sweeps, st, tol);
+    if (m <= 192) return n <= 256 ? launch_cluster<6, 8>(m, n, T, sweeps, st, tol) : launch_cluster<6, 16>(m, n, T, sweeps, st, tol);
+    if (m <= 256) return n <= 256 ? launch_cluster<8, 8>(m, n, T, sweeps, st, tol) : launch_cluster<8, 16>(m, n, T, sweeps, st, tol);
+    if (m <= 512) return n <= 256 ? launch_cluster<16, 8>(m, n, T, sweeps, st, tol) : launch_cluster<16, 16>(m, n, T, sweeps, st, tol);
     return false;
 }
 
@@ -369,9 +369,10 @@ static bool jacobi_try_smem(int m, int n, double *T, int *sweeps, cudaStream_t s
     return true;
 }
 
-void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st) {
+void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st, double tol_d) {
+    const float tol = (float)tol_d;
     if (jacobi_try_smem(m, n, T, sweeps, st)) return;
-    if (jacobi_try_cluster(m, n, T, sweeps, st)) return;
+    if (jacobi_try_cluster(m, n, T, sweeps, st, tol)) return;
     int nb = (int)cdiv(n, kBW);
     nb += nb & 1;
     if (nb < 2) nb = 2;
@@ -380,9 +381,9 @@ void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cud
     SSA_REQUIRE(grid <= num_sms() && smem <= 200 * 1024 && m <= 32 * 24, SSA_ERR_ARG,
                 "projected matrix too large for the device Jacobi");
     SSA_CUDA(cudaMemsetAsync(counters, 0, sizeof(int) * 64, st));
-    float tol = 1e-12f;
     int max_sweeps = 60;
-    void *args[] = {&m, &n, &nb, &T, &tol, &max_sweeps, &counters, &sweeps};
+    float tol_arg = tol;
+    void *args[] = {&m, &n, &nb, &T, &tol_arg, &max_sweeps, &counters, &sweeps};
     void *kern = m <= 32 * 4 ? (void *)jacobi_block_kernel<4>
                : m <= 32 * 8 ? (void *)jacobi_block_kernel<8>
                : m <= 32 * 16 ? (void *)jacobi_block_kernel<16> : (void *)jacobi_block_kernel<24>;
@@ -413,7 +414,7 @@ extern "C" ssa_status ssa_small_svd(int32_t m, int32_t n, double *A, int32_t *sw
         cudaEvent_t e0, e1;
         SSA_CUDA(cudaEventCreate(&e0)); SSA_CUDA(cudaEventCreate(&e1));
         SSA_CUDA(cudaEventRecord(e0, nullptr));
-        jacobi_svd_blocked(m, n, d.as<double>(), dc, ds, nullptr);
+        jacobi_svd_blocked(m, n, d.as<double>(), dc, ds, nullptr, 1e-12);
         SSA_CUDA(cudaEventRecord(e1, nullptr));
         SSA_CUDA(cudaEventSynchronize(e1));
         float t = 0.f;

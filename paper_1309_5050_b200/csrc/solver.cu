@@ -74,7 +74,7 @@ struct Staging {
     }
 };
 
-void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st);
+void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st, double tol);
 bool jacobi_blocked_fits(int m, int n);
 bool jacobi_smem_fits(int m, int n);
 
@@ -632,7 +632,11 @@ struct Gkl {
             for (int j = 0; j < n; ++j)
                 std::memcpy(sg.h + ia + (size_t)m * j, &Tm[(size_t)ldT * j], sizeof(double) * m);
             SSA_CUDA(cudaMemcpyAsync(Ad, sg.h + ia, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
-            jacobi_svd_blocked(m, n, Ad, reinterpret_cast<int *>(Ad + (size_t)m * n + 8), nullptr, st);
+            // off-diagonal tolerance: fp32 products resolve ~1e-7 relative, so 1e-9 (fp32) / 1e-12
+            // (fp64) leaves the Ritz values exact to rounding and saves the last Jacobi sweep(s)
+            static const double jtol = [] { const char *e = std::getenv("SSA_JACOBI_TOL"); return e ? std::atof(e) : 0.0; }();
+            const double tolj = jtol > 0 ? jtol : (sizeof(T) == 4 ? 1e-9 : 1e-12);
+            jacobi_svd_blocked(m, n, Ad, reinterpret_cast<int *>(Ad + (size_t)m * n + 8), nullptr, st, tolj);
             std::vector<double> A((size_t)m * n);
             SSA_CUDA(cudaMemcpyAsync(A.data(), Ad, sizeof(double) * m * n, cudaMemcpyDeviceToHost, st));
             sg.sync();
@@ -684,11 +688,10 @@ struct Gkl {
         int extra = std::max(k / 2, r);        // keep ~2r Ritz pairs (parameter sweep)
         if (const char *e = std::getenv("SSA_PK_EXTRA")) extra = std::atoi(e);
         pk = (int)std::min<int64_t>(r + extra, mn);
-        // blocks per restart cycle: ~4r new vectors per cycle (measured sweep over k and the
-        // cycle length on c1-c3: the projected SVD grows as n³, fewer cycles cost
-        // more products); the projected SVD runs on the device for n up to ~2000
-        int mcyc = (int)std::lround(4.0 * r / k);
-        mcyc = std::max(2, std::min(6, mcyc));
+        // blocks per restart cycle (measured sweep over k and the cycle length on c1-c4, DESIGN.md §5:
+        // the projected SVD grows as n³, fewer cycles cost more products); the projected SVD runs
+        // on the device for n up to ~2000
+        int mcyc = 4;
         if (const char *e = std::getenv("SSA_MCYC")) mcyc = std::max(1, std::atoi(e));
         // prefer cycles whose projected matrix fits the single-CTA shared-memory Jacobi
         if (!std::getenv("SSA_MCYC") && std::getenv("SSA_JACOBI_SMEM")) {

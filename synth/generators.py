@@ -83,7 +83,7 @@ def config1(seed: int = 1, noise: bool = True) -> Workload:
     sig = 0.5 if noise else 0.0
     if noise:
         img = img + rng.normal(0.0, 0.5, size=(nx, ny))
-    return Workload("c1", img, (16, 16), r=10, block_k=8, dtype="f64",
+    return Workload("c1", img, (16, 16), r=10, block_k=16, dtype="f64",
                     groups=[[0, 1, 2, 3], [4, 5]], terms=terms, noise_sigma=sig, seed=seed)
 
 
@@ -96,7 +96,7 @@ def config2(seed: int = 2, noise: bool = True, n: int = 4096, s: int = 8, L: int
         + 0.5 * np.sin(TWO_PI * t / 11.0) + 0.001 * t * c
     if noise:
         x = x + rng.normal(0.0, 0.3, size=(n, s))
-    return Workload("c2", x, (L, 1), r=16, block_k=16, dtype="f32",
+    return Workload("c2", x, (L, 1), r=16, block_k=32, dtype="f32",
                     groups=[[0], [1, 2], [3], [4, 5], [0, 1, 2, 3, 4, 5]],
                     noise_sigma=0.3 if noise else 0.0, seed=seed)
 
