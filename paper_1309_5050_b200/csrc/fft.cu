@@ -77,11 +77,23 @@ template <typename T, int DIR> __device__ __forceinline__ void dft8(cplx<T> *v) 
 __device__ __forceinline__ int sp(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr size_t sp_size(size_t n) { return n + (n >> 4) + 1; }
 
-// Twiddle table (per plan, fp64-accurate values rounded to T): tw[t] = exp(−2πi t / 2^lgtw).
+// Twiddles: the plan keeps tw[t] = exp(−2πi t / 2^lgtw) (fp64-accurate values rounded to T);
+// each CTA stages a two-level copy in shared memory — fine[f] = tw[f] (f < 2^lo) and
+// coarse[c] = tw[c·2^lo] (lo = lgtw/2) — and forms tw[m] = coarse[m >> lo]·fine[m mod 2^lo]
+// (one extra complex multiply, ≤ 2 ulp).  A full table in L1 competes with the FFT buffers for
+// the SM's shared storage and its loads missed to L2 (long-scoreboard stalls, ncu).
 // exp(DIR·2πi·m / 2^lg) = tw[m << (lgtw − lg)] (conjugated for DIR = +1).
+__host__ __device__ constexpr size_t tw_count(int lgtw) { return ((size_t)1 << (lgtw >> 1)) + ((size_t)1 << (lgtw - (lgtw >> 1))); }
+template <typename T>
+__device__ __forceinline__ void stage_twiddles(cplx<T> *tws, const cplx<T> *__restrict__ gtw, int lgtw) {
+    const int lo = lgtw >> 1, nf = 1 << lo, nc = 1 << (lgtw - lo);
+    for (int i = threadIdx.x; i < nf + nc; i += blockDim.x) tws[i] = i < nf ? gtw[i] : gtw[(size_t)(i - nf) << lo];
+}
 template <typename T, int DIR>
-__device__ __forceinline__ cplx<T> twiddle(const cplx<T> *__restrict__ tw, int idx) {
-    cplx<T> w = tw[idx];
+__device__ __forceinline__ cplx<T> twiddle(const cplx<T> *__restrict__ tws, int lgtw, int m) {
+    const int lo = lgtw >> 1;
+    const cplx<T> f = tws[m & ((1 << lo) - 1)], c = tws[(1 << lo) + (m >> lo)];
+    cplx<T> w = cmul(c, f);
     if (DIR > 0) w.y = -w.y;
     return w;
 }
@@ -104,7 +116,7 @@ __device__ __forceinline__ void stockham_stage(const cplx<T> *__restrict__ x, cp
         const int k = j & (Ns - 1);
         if (Ns > 1) {
 #pragma unroll
-            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], twiddle<T, DIR>(tw, (k * r) << tsh));
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], twiddle<T, DIR>(tw, lgtw, (k * r) << tsh));
         }
         if (R == 2) dft2<T, DIR>(v);
         else if (R == 4) dft4<T, DIR>(v);
@@ -150,6 +162,8 @@ fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, in
     const int Mx = 1 << lgx, Hx = Mx / 2 + 1;
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
     cplx<T> *b1 = b0 + sp_size((size_t)(CB >> 1) * Mx);   // CB/2 complex transforms
+    cplx<T> *tws = b1 + sp_size((size_t)(CB >> 1) * Mx);
+    stage_twiddles(tws, tw, lgtw);
     // two real columns per complex transform (NT = CB/2 transforms): z = x_a + i·x_b,
     // X_a[f] = (Z[f] + conj Z[-f]) / 2,  X_b[f] = (Z[f] - conj Z[-f]) / (2i)
     const int NT = CB >> 1;
@@ -176,7 +190,7 @@ fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, in
         b0[sp(idx)] = cplx<T>{v[0], v[1]};
     }
     __syncthreads();
-    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgx, NT, tw, lgtw);
+    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgx, NT, tws, lgtw);
     // transposed write: consecutive threads -> consecutive columns
     #pragma unroll 8
     for (int idx = threadIdx.x; idx < Hx * CB; idx += blockDim.x) {
@@ -204,8 +218,13 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
     const int My = 1 << lgy;
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
     cplx<T> *b1 = b0 + sp_size((size_t)RB * My);
-    const int fx0 = blockIdx.x * RB;
-    const int j = blockIdx.y;
+    cplx<T> *tws = b1 + sp_size((size_t)RB * My);
+    stage_twiddles(tws, tw, lgtw);
+    // grid (k, Hx/RB): the k CTAs that multiply by the same X̂ rows run back to back, so
+    // X̂ stays in L2 while the (much larger) A stream passes (c5: 4.3 GB of X̂ re-reads from
+    // DRAM with the transposed grid order, ncu)
+    const int fx0 = blockIdx.y * RB;
+    const int j = blockIdx.x;
     const int nrow = min(RB, Hx - fx0);
     #pragma unroll 8
     for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
@@ -215,7 +234,7 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
         b0[sp(idx)] = v;
     }
     __syncthreads();
-    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgy, RB, tw, lgtw);
+    cplx<T> *res = fft_batch<T, -1>(b0, b1, lgy, RB, tws, lgtw);
     cplx<T> *oth = (res == b0) ? b1 : b0;
     if (mode == 1) {
         #pragma unroll 8
@@ -232,7 +251,7 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
         res[sp(idx)] = cmulconj(xh, res[sp(idx)]);
     }
     __syncthreads();
-    cplx<T> *out = fft_batch<T, +1>(res, oth, lgy, RB, tw, lgtw);
+    cplx<T> *out = fft_batch<T, +1>(res, oth, lgy, RB, tws, lgtw);
     #pragma unroll 8
     for (int idx = threadIdx.x; idx < RB * ny_out; idx += blockDim.x) {
         const int rr = idx / ny_out, y = idx - rr * ny_out;
@@ -254,6 +273,8 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
     cplx<T> *u1 = u0 + bs;
     cplx<T> *v0 = u1 + bs;
     cplx<T> *v1 = v0 + bs;
+    cplx<T> *tws = v1 + bs;
+    stage_twiddles(tws, tw, lgtw);
     const int fx0 = blockIdx.x * RB;
     const int g = blockIdx.y;
     const int nrow = min(RB, Hx - fx0);
@@ -272,13 +293,13 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
             u0[sp(idx)] = a; v0[sp(idx)] = b;
         }
         __syncthreads();
-        cplx<T> *ru = fft_batch<T, -1>(u0, u1, lgy, RB, tw, lgtw);
-        cplx<T> *rv = fft_batch<T, -1>(v0, v1, lgy, RB, tw, lgtw);
+        cplx<T> *ru = fft_batch<T, -1>(u0, u1, lgy, RB, tws, lgtw);
+        cplx<T> *rv = fft_batch<T, -1>(v0, v1, lgy, RB, tws, lgtw);
         for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x)
             acc[sp(idx)] = cadd(acc[sp(idx)], cmul(ru[sp(idx)], rv[sp(idx)]));
     }
     __syncthreads();
-    cplx<T> *out = fft_batch<T, +1>(acc, u0, lgy, RB, tw, lgtw);
+    cplx<T> *out = fft_batch<T, +1>(acc, u0, lgy, RB, tws, lgtw);
     #pragma unroll 8
     for (int idx = threadIdx.x; idx < RB * ny_out; idx += blockDim.x) {
         const int rr = idx / ny_out, y = idx - rr * ny_out;
@@ -301,6 +322,8 @@ fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int o
     const int Mx = 1 << lgx;
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
     cplx<T> *b1 = b0 + sp_size((size_t)(CB >> 1) * Mx);   // CB/2 complex transforms
+    cplx<T> *tws = b1 + sp_size((size_t)(CB >> 1) * Mx);
+    stage_twiddles(tws, tw, lgtw);
     // two output columns per complex inverse transform (NT = CB/2): Z = Y_a + i·Y_b over the
     // full spectrum (Hermitian completion of each half spectrum), Re z = y_a, Im z = y_b
     const int NT = CB >> 1;
@@ -319,7 +342,7 @@ fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int o
         if (fx > 0 && fx < Mx / 2) b0[sp(t * Mx + Mx - fx)] = cplx<T>{ya.x + yb.y, yb.x - ya.y};
     }
     __syncthreads();
-    cplx<T> *res = fft_batch<T, +1>(b0, b1, lgx, NT, tw, lgtw);
+    cplx<T> *res = fft_batch<T, +1>(b0, b1, lgx, NT, tws, lgtw);
     #pragma unroll 8
     for (int idx = threadIdx.x; idx < CB * ox; idx += blockDim.x) {
         const int c = idx / ox, x = idx - c * ox;
@@ -369,13 +392,15 @@ static int batch_for(int lg, int target) {
 }
 
 template <typename T>
-static size_t smem_ab(int lg, int nb) { return sizeof(cplx<T>) * 2 * sp_size((size_t)nb << lg); }
+static size_t smem_ab(int lg, int nb, int lgtw) {
+    return sizeof(cplx<T>) * (2 * sp_size((size_t)nb << lg) + tw_count(lgtw));
+}
 
 template <typename T>
 static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int bx, int by, int k, const int *jsel,
                    const double *scale, cplx<T> *A, cudaStream_t st) {
     const int CB = 2 * batch_for(f.lgx, 2048);   // real columns (two per complex transform)
-    const size_t smem = smem_ab<T>(f.lgx, CB / 2);
+    const size_t smem = smem_ab<T>(f.lgx, CB / 2, f.lgtw);
     SSA_CUDA(cudaFuncSetAttribute(fft_pass_a<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fft_pass_a<T><<<dim3((unsigned)cdiv(by, CB), k), 256, smem, st>>>(in, ld, map, bx, by, k, jsel, scale, f.lgx, CB, A,
                                                                         f.tw.as<cplx<T>>(), f.lgtw);
@@ -385,9 +410,9 @@ static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int 
 template <typename T>
 static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode, cplx<T> *B, int ny_out, cudaStream_t st) {
     const int RB = batch_for(f.lgy, 2048);
-    const size_t smem = smem_ab<T>(f.lgy, RB);
+    const size_t smem = smem_ab<T>(f.lgy, RB, f.lgtw);
     SSA_CUDA(cudaFuncSetAttribute(fft_pass_b<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fft_pass_b<T><<<dim3((unsigned)cdiv(f.Hx, RB), k), 256, smem, st>>>(A, ny_in, f.Hx, f.lgy, RB,
+    fft_pass_b<T><<<dim3(k, (unsigned)cdiv(f.Hx, RB)), 256, smem, st>>>(A, ny_in, f.Hx, f.lgy, RB,
                                                                          f.Xh.as<cplx<T>>(), mode, B, ny_out,
                                                                          f.tw.as<cplx<T>>(), f.lgtw);
     after_launch("fft_pass_b");
@@ -397,7 +422,7 @@ template <typename T>
 static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *out, int64_t ldo, const int *omap,
                    const int *w, int64_t stride, cudaStream_t st) {
     const int CB = 2 * batch_for(f.lgx, 2048);   // output columns (two per complex transform)
-    const size_t smem = smem_ab<T>(f.lgx, CB / 2);
+    const size_t smem = smem_ab<T>(f.lgx, CB / 2, f.lgtw);
     SSA_CUDA(cudaFuncSetAttribute(fft_pass_c<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const T inv = (T)(1.0 / ((double)f.Mx * (double)f.My));
     fft_pass_c<T><<<dim3((unsigned)cdiv(oy, CB), k), 256, smem, st>>>(B, oy, f.Hx, f.lgx, CB, ox, inv, out, ldo, omap,
@@ -486,7 +511,7 @@ void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, co
     pass_a<T>(f, V, p.K, p.full_k ? nullptr : p.kmap.as<int>(), p.kx, p.ky, nu, jsel.as<int>(), nullptr,
               AV.as<cplx<T>>(), p.st);
     const int RB = batch_for(f.lgy, 2048);
-    const size_t smem = sizeof(cplx<T>) * 5 * sp_size((size_t)RB << f.lgy);
+    const size_t smem = sizeof(cplx<T>) * (5 * sp_size((size_t)RB << f.lgy) + tw_count(f.lgtw));
     SSA_CUDA(cudaFuncSetAttribute(fft_pass_b_conv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fft_pass_b_conv<T><<<dim3((unsigned)cdiv(f.Hx, RB), ng), 256, smem, p.st>>>(
         AU.as<cplx<T>>(), p.ly, AV.as<cplx<T>>(), p.ky, grp_off_dev, grp_idx_dev, slot_dev, f.Hx, f.lgy, RB,
