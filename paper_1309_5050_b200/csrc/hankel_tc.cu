@@ -251,16 +251,17 @@ struct TcCfg {
     static constexpr int LEAD = (S - 1 + 3) / 4 * 4;         // leading zeros per d_y in the packed filters
     static constexpr int W = 32 + LEAD;                      // filter window per k-block (16-B aligned box)
     static constexpr int NCH = (LEAD + 4) / 4;               // 16-B chunks a B item reads
-    static constexpr int VB = (S == 4) ? 1 : 2;              // filter-window buffers
+    static constexpr int VB = (S == 4) ? 2 : 4;              // filter-window buffers (TMA prefetch depth)
     static constexpr uint32_t plane = R * 16;                // one 16-B K-chunk plane of the strip
     static constexpr uint32_t a_bytes = 8 * plane;           // one of hi / lo
     static constexpr uint32_t b_bytes = 256 * 128;           // one of hi / lo (256 rows x 128 B)
-    static constexpr uint32_t v_bytes = NP * W * 4;          // one of hi / lo
+    static constexpr uint32_t v_bytes = NP * W * 4;          // raw fp32 window (split on chip)
     static constexpr uint32_t off_b = 0;                     // [2 stages][hi, lo]
     static constexpr uint32_t off_a = 4 * b_bytes;           // [2 stages][hi, lo]
     static constexpr uint32_t off_v = off_a + 4 * a_bytes;   // [VB][hi, lo]
-    static constexpr uint32_t off_bar = off_v + VB * 2 * v_bytes;
-    static constexpr size_t smem = off_bar + 16 * 8 + 16 + 1024;   // + alignment slack
+    static constexpr uint32_t off_bar = off_v + VB * ((v_bytes + 127) / 128 * 128);
+    static constexpr uint32_t v_stride = (v_bytes + 127) / 128 * 128;
+    static constexpr size_t smem = off_bar + 24 * 8 + 16 + 1024;   // + alignment slack
     static_assert(smem <= 232448, "shared memory budget");
     static_assert(R <= 256 && W <= 256, "TMA box extents");
 };
@@ -279,16 +280,16 @@ hankel_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant_
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::off_bar);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 16);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 24);
     const uint32_t bar0 = smem_u32(bars);
-    // a_full[2] a_empty[2] b_full[2] b_empty[2] acc_empty[2] v_full[2] v_empty[2]
+    // a_full[2] a_empty[2] b_full[2] b_empty[2] acc_empty[2] v_full[VB] v_empty[VB]
     auto a_full = [&](int s) { return bar0 + 8u * (0 + s); };
     auto a_empty = [&](int s) { return bar0 + 8u * (2 + s); };
     auto b_full = [&](int s) { return bar0 + 8u * (4 + s); };
     auto b_empty = [&](int s) { return bar0 + 8u * (6 + s); };
     auto acc_empty = [&](int s) { return bar0 + 8u * (8 + s); };
     auto v_full = [&](int s) { return bar0 + 8u * (10 + s); };
-    auto v_empty = [&](int s) { return bar0 + 8u * (12 + s); };
+    auto v_empty = [&](int s) { return bar0 + 8u * (10 + VB + s); };
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int tile = blockIdx.x;
@@ -308,6 +309,8 @@ hankel_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant_
             mbar_init(b_full(s), kBuildWarps);
             mbar_init(b_empty(s), 1);
             mbar_init(acc_empty(s), kThreads / 32);
+        }
+        for (int s = 0; s < VB; ++s) {
             mbar_init(v_full(s), 1);
             mbar_init(v_empty(s), kBuildWarps);
         }
@@ -367,11 +370,10 @@ hankel_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant_
                 for (int b = 0; b < nb; ++b) {
                     const int gg = g + b, sv = gg % VB;
                     if (gg >= VB) mbar_wait(v_empty(sv), ((gg - VB) / VB) & 1);
-                    const uint32_t vh = sm_u + C::off_v + sv * 2 * C::v_bytes;
-                    mbar_expect_tx(v_full(sv), 2 * C::v_bytes);
+                    const uint32_t vh = sm_u + C::off_v + sv * C::v_stride;
+                    mbar_expect_tx(v_full(sv), C::v_bytes);
                     const int u0 = dy * a.lser + 32 * (kb0 + b);
                     tma_load_2d_true(vh, &tmB, u0, 0, v_full(sv));
-                    tma_load_2d_true(vh + C::v_bytes, &tmB, u0, NP, v_full(sv));
                 }
             }
         } else if (warp == 1) {
@@ -413,25 +415,29 @@ hankel_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant_
                 const int gg = g + b, sv = gg % VB, sb = gg & 1;
                 mbar_wait(v_full(sv), (gg / VB) & 1);
                 if (gg >= 2) mbar_wait(b_empty(sb), ((gg - 2) >> 1) & 1);
-                const float *vh = reinterpret_cast<const float *>(smem + C::off_v + sv * 2 * C::v_bytes);
+                const float *vh = reinterpret_cast<const float *>(smem + C::off_v + sv * C::v_stride);
                 unsigned char *bh = smem + C::off_b + sb * 2 * C::b_bytes;
                 for (int e = bt; e < NP * 8; e += kBuildWarps * 32) {
                     const int cc = e & 7, j = e >> 3;
+                    const float4 *src = reinterpret_cast<const float4 *>(vh + j * W + 4 * cc);
+                    float hi[4 * C::NCH], lo[4 * C::NCH];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const float4 *src = reinterpret_cast<const float4 *>(vh + h * (C::v_bytes / 4) + j * W + 4 * cc);
-                        float win[4 * C::NCH];
+                    for (int q = 0; q < C::NCH; ++q) {
+                        const float4 v = src[q];
+                        const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                        for (int q = 0; q < C::NCH; ++q) {
-                            const float4 v = src[q];
-                            win[4 * q] = v.x; win[4 * q + 1] = v.y; win[4 * q + 2] = v.z; win[4 * q + 3] = v.w;
+                        for (int u = 0; u < 4; ++u) {
+                            hi[4 * q + u] = __uint_as_float(tf32_rna(vv[u]));
+                            lo[4 * q + u] = vv[u] - hi[4 * q + u];
                         }
+                    }
 #pragma unroll
-                        for (int sph = 0; sph < S; ++sph) {
-                            const int o = C::LEAD - sph;
-                            *reinterpret_cast<float4 *>(bh + h * C::b_bytes + sw128_off(sph * NP + j, cc)) =
-                                make_float4(win[o], win[o + 1], win[o + 2], win[o + 3]);
-                        }
+                    for (int sph = 0; sph < S; ++sph) {
+                        const int o = C::LEAD - sph;
+                        const uint32_t off = sw128_off(sph * NP + j, cc);
+                        *reinterpret_cast<float4 *>(bh + off) = make_float4(hi[o], hi[o + 1], hi[o + 2], hi[o + 3]);
+                        *reinterpret_cast<float4 *>(bh + C::b_bytes + off) =
+                            make_float4(lo[o], lo[o + 1], lo[o + 2], lo[o + 3]);
                     }
                 }
                 fence_proxy_async();
@@ -497,14 +503,13 @@ hankel_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant_
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
-// Filter packing for the B windows: bpk[h][j][d_y·lser + u] = split_h(in[u − LEAD, d_y; j0 + j]) (0 outside
-// [0, bx), NP rows, the k-block tail zero-padded).  h = 0: tf32 hi (round to nearest), 1: lo.  LEAD is a
-// multiple of 4 so every window box starts 16-B aligned (TMA faults on unaligned inner coordinates).
+// Filter packing for the B windows: bpk[j][d_y·lser + u] = in[u − LEAD, d_y; j0 + j] (0 outside [0, bx),
+// NP rows, the k-block tail zero-padded; the tf32 hi / lo split happens on chip).  LEAD is a multiple
+// of 4 so every window box starts 16-B aligned (TMA faults on unaligned inner coordinates).
 template <int S>
 __global__ void tc_pack_kernel(const float *__restrict__ in, int64_t ldi, const int *__restrict__ imap, int bx,
                                int by, int j0, int jn, int lser, float *__restrict__ bpk) {
     // grid: (ceil(lser / 256), by, NP); thread = one packed entry of one filter row
-    constexpr int NP = 256 / S;
     constexpr int LEAD = TcCfg<S, 4>::LEAD;
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
     const int dy = blockIdx.y, j = blockIdx.z;
@@ -516,11 +521,8 @@ __global__ void tc_pack_kernel(const float *__restrict__ in, int64_t ldi, const 
         const int64_t ci = imap ? (int64_t)imap[box] : box;
         if (ci >= 0) v = in[ci + ldi * (int64_t)(j0 + j)];
     }
-    const float hi = __uint_as_float(tc::tf32_rna(v));
     const int64_t lall = (int64_t)by * lser;
-    const int64_t t = (int64_t)j * lall + (int64_t)dy * lser + u;
-    bpk[t] = hi;
-    bpk[(int64_t)NP * lall + t] = v - hi;
+    bpk[(int64_t)j * lall + (int64_t)dy * lser + u] = v;
 }
 
 // Image planes (plan-time, once): hi[col·ldp + i] = tf32_rna(x), lo = x − hi; zero for i >= nx.
@@ -633,7 +635,7 @@ size_t tc_pack_bytes(int bx, int by, int k) {
         const int NP = 256 / S;
         const int64_t nkb = cdiv(bx + S - 1, tc::kKB);
         const int64_t lser = rup((S - 1 + 3) / 4 * 4 + nkb * tc::kKB + 32, 4);
-        best = std::max(best, sizeof(float) * 2 * (size_t)NP * by * lser);
+        best = std::max(best, sizeof(float) * (size_t)NP * by * lser);
     }
     return best;
 }
@@ -652,7 +654,7 @@ static void tc_run(const TcCorrParams &P, int j0, cudaStream_t st) {
     a.lser = (int)rup(C::LEAD + (int64_t)a.nkb * tc::kKB + 32, 4);
     // pack the filters (hi / lo rows, S-1 leading zeros per d_y)
     const int64_t lall = (int64_t)P.by * a.lser;
-    SSA_REQUIRE(sizeof(float) * 2 * (size_t)C::NP * lall <= P.bpk_bytes, SSA_ERR_ARG, "tc: packing buffer too small");
+    SSA_REQUIRE(sizeof(float) * (size_t)C::NP * lall <= P.bpk_bytes, SSA_ERR_ARG, "tc: packing buffer too small");
     tc_pack_kernel<S><<<dim3((unsigned)cdiv(a.lser, 256), (unsigned)P.by, C::NP), 256, 0, st>>>(
         P.in, P.ldi, P.imap, P.bx, P.by, j0, a.jn, a.lser, P.bpk);
     after_launch("tc_pack");
@@ -675,7 +677,7 @@ static void tc_run(const TcCorrParams &P, int j0, cudaStream_t st) {
         Maps mp;
         mp.ah = make_map3(P.x_hi, 4, S / 4, prow, 16, (uint64_t)S * 4, 4, 1, C::R, false);
         mp.al = make_map3(P.x_lo, 4, S / 4, prow, 16, (uint64_t)S * 4, 4, 1, C::R, false);
-        mp.b = make_map2(P.bpk, (uint64_t)lall, 2 * C::NP, (uint64_t)lall * 4, C::W, C::NP, false);
+        mp.b = make_map2(P.bpk, (uint64_t)lall, C::NP, (uint64_t)lall * 4, C::W, C::NP, false);
         it = cache.emplace(key, mp).first;
     }
     const CUtensorMap &mAh = it->second.ah, &mAl = it->second.al, &mB = it->second.b;

@@ -269,6 +269,12 @@ static bool launch_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st
 // prefer the cluster kernel; fall back to the cooperative-grid kernel for large n
 static bool jacobi_try_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st, float tol) {
     if (std::getenv("SSA_JACOBI_GRID")) return false;
+    static const int bw16 = std::getenv("SSA_JACOBI_BW16") ? 1 : 0;
+    if (bw16 && n <= 256) {
+        if (m <= 128) return launch_cluster<4, 16>(m, n, T, sweeps, st, tol);
+        if (m <= 192) return launch_cluster<6, 16>(m, n, T, sweeps, st, tol);
+        if (m <= 256) return launch_cluster<8, 16>(m, n, T, sweeps, st, tol);
+    }
     if (m <= 128) return n <= 256 ? launch_cluster<4, 8>(m, n, T, sweeps, st, tol) : launch_cluster<4, 16>(m, n, T, sweeps, st, tol);
     if (m <= 192) return n <= 256 ? launch_cluster<6, 8>(m, n, T, sweeps, st, tol) : launch_cluster<6, 16>(m, n, T, sweeps, st, tol);
     if (m <= 256) return n <= 256 ? launch_cluster<8, 8>(m, n, T, sweeps, st, tol) : launch_cluster<8, 16>(m, n, T, sweeps, st, tol);
