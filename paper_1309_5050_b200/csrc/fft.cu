@@ -153,8 +153,8 @@ __device__ cplx<T> *fft_batch(cplx<T> *x, cplx<T> *y, int lg, int nbatch, const 
 //   output: A[(j * Hx + fx) * by + col], fx < Hx
 // grid: (ceil(by / CB), k), CB columns per CTA.
 // ---------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(256)
+template <typename T, int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 2)
 fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, int bx, int by, int jsel_n,
            const int *__restrict__ jsel, const double *__restrict__ scale, int lgx, int CB, cplx<T> *__restrict__ A,
            const cplx<T> *__restrict__ tw, int lgtw) {
@@ -210,8 +210,8 @@ fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, in
 // mode 1: forward only, write all My entries (plan-time X̂).
 // grid: (ceil(Hx / RB), k)
 // ---------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(256)
+template <typename T, int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 2)
 fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, const cplx<T> *__restrict__ Xh,
            int mode, cplx<T> *__restrict__ B, int ny_out, const cplx<T> *__restrict__ tw, int lgtw) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -260,8 +260,8 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
 }
 
 // Pass B (averaging): per (g, fx): Σ_{i∈I_g} DFT_y(AU_i row) ⊙ DFT_y(AV_i row), inverse, keep ny rows.
-template <typename T>
-__global__ void __launch_bounds__(256)
+template <typename T, int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 2)
 fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restrict__ AV, int ky, const int *grp_off,
                 const int *grp_idx, const int *slot, int Hx, int lgy, int RB, cplx<T> *__restrict__ B, int ny_out,
                 const cplx<T> *__restrict__ tw, int lgtw) {
@@ -313,8 +313,8 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
 //   averaging: out[x + ldo*y + stride*j] = Re(...) * inv / w  on w > 0, NaN elsewhere
 // grid: (ceil(oy / CB), k)
 // ---------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(256)
+template <typename T, int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 2)
 fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int ox, T inv, T *__restrict__ out,
            int64_t ldo, const int *__restrict__ omap, const int *__restrict__ w, int64_t stride,
            const cplx<T> *__restrict__ tw, int lgtw) {
@@ -385,6 +385,15 @@ bool fft_supported(const PlanImpl &p) {
 }
 
 // transforms per CTA so that a CTA holds ~target complex points (2 buffers)
+// threads per CTA: one radix-8 butterfly per thread per stage, 128..512 (long transforms get
+// more threads: the stages are latency chains, so parallel butterflies shorten each one)
+// (measured: 512 threads help short grids such as the c2 4096-point columns, 256 are better for
+// grids of many waves such as c5 pass B, where occupancy hides the latency instead)
+static int threads_for(int lg, int nb, int64_t nctas) {
+    const int64_t cap = nctas >= 4 * (int64_t)num_sms() ? 256 : 512;
+    return (int)std::min<int64_t>(cap, std::max<int64_t>(128, ((int64_t)nb << lg) / 8));
+}
+
 static int batch_for(int lg, int target) {
     static const int scale = [] { const char *e = std::getenv("SSA_FFT_BATCH"); return e ? std::atoi(e) : 0; }();
     if (scale > 0) target = scale;
@@ -401,8 +410,10 @@ static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int 
                    const double *scale, cplx<T> *A, cudaStream_t st) {
     const int CB = 2 * batch_for(f.lgx, 2048);   // real columns (two per complex transform)
     const size_t smem = smem_ab<T>(f.lgx, CB / 2, f.lgtw);
-    SSA_CUDA(cudaFuncSetAttribute(fft_pass_a<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fft_pass_a<T><<<dim3((unsigned)cdiv(by, CB), k), 256, smem, st>>>(in, ld, map, bx, by, k, jsel, scale, f.lgx, CB, A,
+    const int nth = threads_for(f.lgx, CB / 2, cdiv(by, CB) * k);
+    auto kern = nth <= 256 ? fft_pass_a<T, 256> : fft_pass_a<T, 512>;
+    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<dim3((unsigned)cdiv(by, CB), k), nth, smem, st>>>(in, ld, map, bx, by, k, jsel, scale, f.lgx, CB, A,
                                                                         f.tw.as<cplx<T>>(), f.lgtw);
     after_launch("fft_pass_a");
 }
@@ -411,8 +422,10 @@ template <typename T>
 static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode, cplx<T> *B, int ny_out, cudaStream_t st) {
     const int RB = batch_for(f.lgy, 2048);
     const size_t smem = smem_ab<T>(f.lgy, RB, f.lgtw);
-    SSA_CUDA(cudaFuncSetAttribute(fft_pass_b<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fft_pass_b<T><<<dim3(k, (unsigned)cdiv(f.Hx, RB)), 256, smem, st>>>(A, ny_in, f.Hx, f.lgy, RB,
+    const int nth = threads_for(f.lgy, RB, cdiv(f.Hx, RB) * k);
+    auto kern = nth <= 256 ? fft_pass_b<T, 256> : fft_pass_b<T, 512>;
+    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<dim3(k, (unsigned)cdiv(f.Hx, RB)), nth, smem, st>>>(A, ny_in, f.Hx, f.lgy, RB,
                                                                          f.Xh.as<cplx<T>>(), mode, B, ny_out,
                                                                          f.tw.as<cplx<T>>(), f.lgtw);
     after_launch("fft_pass_b");
@@ -423,9 +436,11 @@ static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *o
                    const int *w, int64_t stride, cudaStream_t st) {
     const int CB = 2 * batch_for(f.lgx, 2048);   // output columns (two per complex transform)
     const size_t smem = smem_ab<T>(f.lgx, CB / 2, f.lgtw);
-    SSA_CUDA(cudaFuncSetAttribute(fft_pass_c<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int nth = threads_for(f.lgx, CB / 2, cdiv(oy, CB) * k);
+    auto kern = nth <= 256 ? fft_pass_c<T, 256> : fft_pass_c<T, 512>;
+    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const T inv = (T)(1.0 / ((double)f.Mx * (double)f.My));
-    fft_pass_c<T><<<dim3((unsigned)cdiv(oy, CB), k), 256, smem, st>>>(B, oy, f.Hx, f.lgx, CB, ox, inv, out, ldo, omap,
+    kern<<<dim3((unsigned)cdiv(oy, CB), k), nth, smem, st>>>(B, oy, f.Hx, f.lgx, CB, ox, inv, out, ldo, omap,
                                                                        w, stride, f.tw.as<cplx<T>>(), f.lgtw);
     after_launch("fft_pass_c");
 }
@@ -512,8 +527,10 @@ void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, co
               AV.as<cplx<T>>(), p.st);
     const int RB = batch_for(f.lgy, 2048);
     const size_t smem = sizeof(cplx<T>) * (5 * sp_size((size_t)RB << f.lgy) + tw_count(f.lgtw));
-    SSA_CUDA(cudaFuncSetAttribute(fft_pass_b_conv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fft_pass_b_conv<T><<<dim3((unsigned)cdiv(f.Hx, RB), ng), 256, smem, p.st>>>(
+    const int nth = threads_for(f.lgy, RB, cdiv(f.Hx, RB) * ng);
+    auto kern = nth <= 256 ? fft_pass_b_conv<T, 256> : fft_pass_b_conv<T, 512>;
+    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<dim3((unsigned)cdiv(f.Hx, RB), ng), nth, smem, p.st>>>(
         AU.as<cplx<T>>(), p.ly, AV.as<cplx<T>>(), p.ky, grp_off_dev, grp_idx_dev, slot_dev, f.Hx, f.lgy, RB,
         B.as<cplx<T>>(), p.ny, f.tw.as<cplx<T>>(), f.lgtw);
     after_launch("fft_pass_b_conv");
