@@ -177,6 +177,8 @@ struct PathKey {
 template <typename T>
 static double time_product(PlanImpl &p, bool xv, int path, int k, T *in, T *out) {
     const int save_xv = p.path_xv, save_xtu = p.path_xtu;
+    const bool save_comm = p.has_comm;
+    p.has_comm = false;   // time the local product only: no collective during the choice
     (xv ? p.path_xv : p.path_xtu) = path;
     cudaEvent_t e0, e1;
     SSA_CUDA(cudaEventCreate(&e0)); SSA_CUDA(cudaEventCreate(&e1));
@@ -193,6 +195,7 @@ static double time_product(PlanImpl &p, bool xv, int path, int k, T *in, T *out)
     }
     cudaEventDestroy(e0); cudaEventDestroy(e1);
     p.path_xv = save_xv; p.path_xtu = save_xtu;
+    p.has_comm = save_comm;
     return best;
 }
 

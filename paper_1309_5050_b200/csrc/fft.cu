@@ -378,9 +378,9 @@ static int ilog2_ceil(int64_t n) {
 }
 
 bool fft_supported(const PlanImpl &p) {
-    // shared-memory Stockham sizes: up to 8192 points (fp32) / 2048 along y and 4096 along x (fp64)
+    // shared-memory Stockham sizes: up to 8192 points (fp32) / 2048 along y and 4096 along x (fp64).
+    // Bands (multi-GPU) are fine: the band's 𝔎 enters through the compaction map like any shape.
     const int lx = ilog2_ceil(p.nx), ly = ilog2_ceil(p.ny);
-    if (p.has_comm) return false;
     return p.dt == SSA_F64 ? (lx <= 12 && ly <= 11) : (lx <= 13 && ly <= 13);
 }
 

@@ -76,3 +76,19 @@ class TorchComm:
         if self._struct is None:
             self._struct = lib.ssa_comm(self.rank, self.world, None, self._fn)
         return self._struct
+
+
+class LocalComm:
+    """A stand-in `ssa_comm` for one process that plays rank `rank` of `world` with an identity
+    all-reduce: the library then computes exactly the band-local operator (X·V partial of the
+    band, band-local Xᵀ·U), which is what the single-GPU band tests check against the oracle."""
+
+    def __init__(self, rank: int = 0, world: int = 2):
+        self.rank, self.world = rank, world
+        self._fn = lib.ALLREDUCE_FN(lambda user, ptr, count, dtype, stream: 0)
+        self._struct = None
+
+    def struct(self) -> lib.ssa_comm:
+        if self._struct is None:
+            self._struct = lib.ssa_comm(self.rank, self.world, None, self._fn)
+        return self._struct

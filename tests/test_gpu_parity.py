@@ -392,3 +392,33 @@ def test_errors():
     with pytest.raises(SSAError) as e:
         p.reconstruct([[0, 3]])
     assert e.value.status == 4
+
+
+# ---------------------------------------------------------------- band partition (row a12) on one GPU
+@pytest.mark.parametrize("path", ["direct", "fft", "tc"])
+def test_band_products_and_decomposition(path):
+    """The multi-GPU band plan on one GPU with an identity all-reduce: X·V is the
+    band's partial sum and Xᵀ·U the band-local product (both against the oracle on the band's
+    𝔎), and the decomposition is the SVD of the band operator X[:, κ ∈ band]."""
+    from paper_1309_5050_b200.dist import LocalComm, band_bounds
+    w = synth.small_shaped(seed=51, nx=700, ny=10, window=(300, 3), n_holes=2) if path == "tc" else \
+        synth.small_shaped(seed=52, nx=40, ny=33, window=(7, 5), wmask_drop=3)
+    x = _oracle_input(w, "f32")
+    sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
+    y0, y1 = band_bounds(sh.ky, 2, 1)
+    band = oracle.Shapes(sh.nx, sh.ny, sh.lx, sh.ly, sh.nmask, sh.wmask, sh.kmask.copy(order="F"), sh.weights)
+    band.kmask[:, :y0] = 0
+    band.kmask[:, y1:] = 0
+    from paper_1309_5050_b200 import Plan
+    p = Plan(w.data, w.window, mask=w.mask, wmask=w.wmask, dtype="f32", path=path, block_k=8,
+             comm=LocalComm(1, 2), band=(y0, y1))
+    kb = int(band.kmask.sum())
+    assert p.K == kb
+    rng = np.random.default_rng(8)
+    V = rng.normal(size=(kb, 5)).astype(np.float32).astype(np.float64)
+    U = rng.normal(size=(sh.L, 5)).astype(np.float32).astype(np.float64)
+    assert relfro(p.matmul(V), oracle.xv(x, band, V)) <= FP32_PROD_TOL
+    assert relfro(p.matmul(U, transpose=True), oracle.xtu(x, band, U)) <= FP32_PROD_TOL
+    s_or, _, _, s_all = oracle.svd_dense(x, band, 5)
+    p.decompose(4)
+    check_sigma(p.sigma, s_all, 4)
