@@ -98,52 +98,112 @@ __device__ __forceinline__ cplx<T> twiddle(const cplx<T> *__restrict__ tws, int 
     return w;
 }
 
-// One Stockham radix-R stage for `nbatch` transforms of length N = 2^lgn stored back to
-// back (padded indices); Ns = 2^lgs is the current span.
-template <typename T, int DIR, int R>
-__device__ __forceinline__ void stockham_stage(const cplx<T> *__restrict__ x, cplx<T> *__restrict__ y, int lgn, int lgs,
-                                               int nbatch, const cplx<T> *__restrict__ tw, int lgtw) {
+// One Stockham radix-R stage for `nbatch` transforms of length N = 2^LGN stored back to back
+// (padded indices); NS = 2^LGS is the current span.  Sizes are template constants so the index
+// arithmetic folds (the generic version spent half of its instructions on integer address
+// math, ncu); loads use one padded base plus constant strides, and the R-1 twiddles of a
+// butterfly come from 3 table lookups (w, w², w⁴) and 4 multiplies.
+template <typename T, int DIR, int R, int LGN, int LGS>
+__device__ __forceinline__ void stage_t(const cplx<T> *__restrict__ x, cplx<T> *__restrict__ y, int nbatch,
+                                        const cplx<T> *__restrict__ tws, int lgtw) {
     constexpr int LR = R == 2 ? 1 : (R == 4 ? 2 : 3);
-    const int N = 1 << lgn, nbf = N >> LR, lgb = lgn - LR;
-    const int Ns = 1 << lgs;
-    const int tsh = lgtw - lgs - LR;
-    for (int b = threadIdx.x; b < (nbatch << lgb); b += blockDim.x) {
-        const int t = b >> lgb, j = b & (nbf - 1);
-        const int base_in = t * N;
+    constexpr int N = 1 << LGN, NBF = N >> LR, LGB = LGN - LR, NS = 1 << LGS;
+    const int tsh = lgtw - LGS - LR;
+    for (int b = threadIdx.x; b < (nbatch << LGB); b += blockDim.x) {
+        const int t = b >> LGB, j = b & (NBF - 1);
+        const int a = t * N + j;
         cplx<T> v[R];
+        if constexpr (NBF % 16 == 0) {
+            const int pa = sp(a);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = x[sp(base_in + j + r * nbf)];
-        const int k = j & (Ns - 1);
-        if (Ns > 1) {
+            for (int r = 0; r < R; ++r) v[r] = x[pa + r * (NBF + NBF / 16)];
+        } else {
 #pragma unroll
-            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], twiddle<T, DIR>(tw, lgtw, (k * r) << tsh));
+            for (int r = 0; r < R; ++r) v[r] = x[sp(a + r * NBF)];
         }
-        if (R == 2) dft2<T, DIR>(v);
-        else if (R == 4) dft4<T, DIR>(v);
+        const int k = j & (NS - 1);
+        if constexpr (NS > 1) {
+            const cplx<T> w1 = twiddle<T, DIR>(tws, lgtw, k << tsh);
+            if constexpr (R == 2) {
+                v[1] = cmul(v[1], w1);
+            } else {
+                const cplx<T> w2 = twiddle<T, DIR>(tws, lgtw, (2 * k) << tsh);
+                const cplx<T> w3 = cmul(w2, w1);
+                v[1] = cmul(v[1], w1); v[2] = cmul(v[2], w2); v[3] = cmul(v[3], w3);
+                if constexpr (R == 8) {
+                    const cplx<T> w4 = twiddle<T, DIR>(tws, lgtw, (4 * k) << tsh);
+                    v[4] = cmul(v[4], w4);
+                    v[5] = cmul(v[5], cmul(w4, w1));
+                    v[6] = cmul(v[6], cmul(w4, w2));
+                    v[7] = cmul(v[7], cmul(w4, w3));
+                }
+            }
+        }
+        if constexpr (R == 2) dft2<T, DIR>(v);
+        else if constexpr (R == 4) dft4<T, DIR>(v);
         else dft8<T, DIR>(v);
-        const int base = base_in + (j - k) * R + k;
+        const int base = t * N + (j - k) * R + k;
+        if constexpr (NS % 16 == 0) {
+            const int pb = sp(base);
 #pragma unroll
-        for (int r = 0; r < R; ++r) y[sp(base + r * Ns)] = v[r];
+            for (int r = 0; r < R; ++r) y[pb + r * (NS + NS / 16)] = v[r];
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) y[sp(base + r * NS)] = v[r];
+        }
     }
 }
 
-// Batched in-place-by-ping-pong FFT of nbatch transforms of length N = 2^lg in
-// shared memory (padded indices); returns the buffer that holds the result.  All
-// threads of the CTA take part; the caller has synchronised before the call.
-template <typename T, int DIR>
-__device__ cplx<T> *fft_batch(cplx<T> *x, cplx<T> *y, int lg, int nbatch, const cplx<T> *__restrict__ tw, int lgtw) {
-    int lgs = 0;
-    const int rem = lg % 3;
-    if (rem == 1) { stockham_stage<T, DIR, 2>(x, y, lg, lgs, nbatch, tw, lgtw); lgs += 1; }
-    else if (rem == 2) { stockham_stage<T, DIR, 4>(x, y, lg, lgs, nbatch, tw, lgtw); lgs += 2; }
-    if (rem) { __syncthreads(); cplx<T> *t = x; x = y; y = t; }
-    while (lgs < lg) {
-        stockham_stage<T, DIR, 8>(x, y, lg, lgs, nbatch, tw, lgtw);
-        lgs += 3;
+template <typename T, int DIR, int LG, int LGS>
+__device__ __forceinline__ cplx<T> *stages_from(cplx<T> *x, cplx<T> *y, int nbatch, const cplx<T> *__restrict__ tws,
+                                                int lgtw) {
+    if constexpr (LGS >= LG) {
+        return x;
+    } else {
+        stage_t<T, DIR, 8, LG, LGS>(x, y, nbatch, tws, lgtw);
         __syncthreads();
-        cplx<T> *t = x; x = y; y = t;
+        return stages_from<T, DIR, LG, LGS + 3>(y, x, nbatch, tws, lgtw);
     }
-    return x;
+}
+
+// Batched ping-pong FFT of nbatch transforms of length 2^LG in shared memory (padded
+// indices); returns the buffer that holds the result.  All threads of the CTA take part;
+// the caller has synchronised before the call.
+template <typename T, int DIR, int LG>
+__device__ __forceinline__ cplx<T> *fft_batch_t(cplx<T> *x, cplx<T> *y, int nbatch, const cplx<T> *__restrict__ tws,
+                                                int lgtw) {
+    constexpr int REM = LG % 3;
+    if constexpr (REM == 1) {
+        stage_t<T, DIR, 2, LG, 0>(x, y, nbatch, tws, lgtw);
+        __syncthreads();
+        return stages_from<T, DIR, LG, 1>(y, x, nbatch, tws, lgtw);
+    } else if constexpr (REM == 2) {
+        stage_t<T, DIR, 4, LG, 0>(x, y, nbatch, tws, lgtw);
+        __syncthreads();
+        return stages_from<T, DIR, LG, 2>(y, x, nbatch, tws, lgtw);
+    } else {
+        return stages_from<T, DIR, LG, 0>(x, y, nbatch, tws, lgtw);
+    }
+}
+
+template <typename T, int DIR>
+__device__ cplx<T> *fft_batch(cplx<T> *x, cplx<T> *y, int lg, int nbatch, const cplx<T> *__restrict__ tws, int lgtw) {
+    switch (lg) {
+    case 0: return x;   // length-1 transforms are the identity
+    case 1: return fft_batch_t<T, DIR, 1>(x, y, nbatch, tws, lgtw);
+    case 2: return fft_batch_t<T, DIR, 2>(x, y, nbatch, tws, lgtw);
+    case 3: return fft_batch_t<T, DIR, 3>(x, y, nbatch, tws, lgtw);
+    case 4: return fft_batch_t<T, DIR, 4>(x, y, nbatch, tws, lgtw);
+    case 5: return fft_batch_t<T, DIR, 5>(x, y, nbatch, tws, lgtw);
+    case 6: return fft_batch_t<T, DIR, 6>(x, y, nbatch, tws, lgtw);
+    case 7: return fft_batch_t<T, DIR, 7>(x, y, nbatch, tws, lgtw);
+    case 8: return fft_batch_t<T, DIR, 8>(x, y, nbatch, tws, lgtw);
+    case 9: return fft_batch_t<T, DIR, 9>(x, y, nbatch, tws, lgtw);
+    case 10: return fft_batch_t<T, DIR, 10>(x, y, nbatch, tws, lgtw);
+    case 11: return fft_batch_t<T, DIR, 11>(x, y, nbatch, tws, lgtw);
+    case 12: return fft_batch_t<T, DIR, 12>(x, y, nbatch, tws, lgtw);
+    default: return fft_batch_t<T, DIR, 13>(x, y, nbatch, tws, lgtw);
+    }
 }
 
 // ---------------------------------------------------------------------------
