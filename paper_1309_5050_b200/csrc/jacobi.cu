@@ -239,6 +239,294 @@ jacobi_cluster_kernel(int m, int n, int nb, double *__restrict__ A, float tol, i
     if (c == 0 && tid == 0 && sweeps_out) *sweeps_out = sweep + 1;
 }
 
+// ---------------------------------------------------------------------------
+// Gram-based cluster variant (the default).  Same block circle schedule and systolic
+// DSMEM shift as jacobi_cluster_kernel, but one inner sweep over the NC = 2·BW columns
+// a CTA holds is run on their NC x NC Gram matrix instead of on the m-long columns:
+//   1. G = CᵀC on the fp64 tensor cores (DMMA m8n8k4, fp64 accumulate);
+//   2. one cyclic two-sided Jacobi sweep on G (NC-1 steps of NC/2 disjoint rotations,
+//      the same fp32-angle / fp64-rotation rule and skip test as jacobi_pair, applied to
+//      the current G) accumulating V = J_1 J_2 ... (exactly orthogonal up to rounding);
+//   3. C ← C·V on the tensor cores, the result tiles stored straight into the
+//      neighbours' next-round buffers (the systolic shift fused into the epilogue).
+// The rotations are those the column-wise inner sweep would apply (G carries the same
+// inner products), but each step costs O(NC) instead of an m-long dot product plus a
+// warp reduction.  Gram rounding only perturbs the angles at ε·|c_p||c_q| (a pair may
+// need another visit); σ_j are still the column norms of the rotated T.  Column buffers
+// use ld ≡ 4 (mod 16) doubles with zero padding rows (conflict-free fragment loads).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+template <int NC>
+struct GramCfg {
+    static constexpr int BW = NC / 2;
+    static constexpr int NT = 256;                        // threads per CTA
+    static constexpr int TILES = (NC / 8) * (NC / 8);     // 8x8 Gram tiles
+    static constexpr int KSPLIT = TILES >= 8 ? 1 : 8 / TILES;
+    static constexpr int LDG = NC + 1;
+    __host__ __device__ static int ldc(int m) { return (m + 15) / 16 * 16 + 4; }
+    static size_t smem(int m) {
+        return sizeof(double) * ((size_t)2 * NC * ldc(m) + 4 * (size_t)NC * LDG + (size_t)KSPLIT * NC * NC);
+    }
+};
+
+// Rotation of the pair (p, q) from al = |C_p|², be = |C_q|², ga = C_pᵀC_q (the rule of
+// jacobi_pair: skip unless ga² > tol²·al·be, ζ = (be−al)/(2ga), t = sign(ζ)/(|ζ|+√(1+ζ²)),
+// c = 1/√(1+t²), s = c·t).  The test is in fp64; the angle in fp32 on operands scaled
+// by an exact power of two (no fp32 overflow for any fp64 input); c, s in fp64.
+__device__ __forceinline__ float rcp_approx(float x) { float r; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+__device__ __forceinline__ float sqrt_approx(float x) { float r; asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+
+__device__ __forceinline__ bool pair_rotation(double al, double be, double ga, double tol2, double &c, double &s,
+                                              float &mrel) {
+    c = 1.0; s = 0.0;
+    if (!(ga * ga > tol2 * al * be)) return false;
+    mrel = fmaxf(mrel, (float)(fabs(ga) * rsqrt(al * be)));   // relative off-diagonal (early stop)
+    // 2^-e with e the exponent of max(al, be): scaled operands are <= 1 in magnitude
+    const int hi = __double2hiint(fmax(al, be));
+    const double scale = __hiloint2double(((2046 - ((hi >> 20) & 2047)) & 2047) << 20, 0);
+    const float fa = (float)(al * scale), fb = (float)(be * scale), fg = (float)(ga * scale);
+    const float zeta = (fb - fa) * 0.5f * rcp_approx(fg);
+    float tf = copysignf(1.0f, zeta) * rcp_approx(fabsf(zeta) + sqrt_approx(fmaf(zeta, zeta, 1.0f)));
+    if (!isfinite(zeta)) tf = 0.0f;
+    const double t = (double)tf;
+    c = rsqrt(fma(t, t, 1.0));
+    s = c * t;
+    return true;
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256, 1)
+jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, float early, int max_sweeps,
+                   int *__restrict__ sweeps_out) {
+    using Cfg = GramCfg<NC>;
+    constexpr int BW = Cfg::BW, LDG = Cfg::LDG;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) double SM[];
+    __shared__ int flags[2];
+    __shared__ int rot_sh, mrel_sh, mflags[2];
+    const int ldc = Cfg::ldc(m);
+    const int blk = ldc * BW;                               // doubles per column block (slot)
+    double *const bufs = SM;                                // [2][NC][ldc]
+    double *const Gs = SM + 2 * NC * ldc;                   // [2][NC][LDG] ping-pong Gram
+    double *const Vs = Gs + 2 * NC * LDG;                   // [2][NC][LDG] ping-pong V (row-major V[x][y])
+    double *const Gp = Vs + 2 * NC * LDG;                   // [KSPLIT][NC][NC] partial Grams
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = (int)cluster.block_rank(), ncta = nb / 2;
+    const int m4 = (m + 3) & ~3, m8 = (m + 7) & ~7;
+    for (int idx = tid; idx < 2 * NC * ldc; idx += Cfg::NT) bufs[idx] = 0.0;
+    // step schedule.  A round pairs slot A (columns 0..BW-1) with slot B (BW..NC-1): BW "cross"
+    // steps s with pairs (i, BW + (i+s) mod BW).  The first round of a sweep is preceded by BW-1
+    // "intra" steps (circle method inside each slot), so every column pair is visited exactly
+    // once per sweep, as in the cyclic ordering.  Steps 0..BW-2: intra, BW-1..NC-2: cross.
+    //   tab[step][x] = partner | pair index << 8 | (x is the 'p' of its pair) << 16
+    //   ptab[step][w] = p | q << 8
+    __shared__ int tab[(NC - 1) * NC];
+    __shared__ int ptab[(NC - 1) * (NC / 2)];
+    for (int idx = tid; idx < (NC - 1) * (NC / 2); idx += Cfg::NT) {
+        const int st = idx / (NC / 2), w = idx - st * (NC / 2);
+        int p, q;
+        if (st < BW - 1) {                       // intra: circle over BW players in slot w / (BW/2)
+            constexpr int M1 = BW - 1;
+            const int h = w / (BW / 2), v = w - h * (BW / 2);
+            p = (v == 0) ? st : (st + v) % M1;
+            q = (v == 0) ? M1 : (st - v + M1) % M1;
+            p += h * BW; q += h * BW;
+        } else {                                 // cross
+            const int sx = st - (BW - 1);
+            p = w;
+            q = BW + (w + sx) % BW;
+        }
+        ptab[idx] = p | (q << 8);
+        tab[st * NC + p] = q | (w << 8) | (1 << 16);
+        tab[st * NC + q] = p | (w << 8);
+    }
+    const double tol2 = (double)tol * (double)tol;
+    __syncthreads();
+    {
+        const int ba = (c == 0) ? 0 : c % (nb - 1);
+        const int bb = (c == 0) ? nb - 1 : (nb - 1 - c) % (nb - 1);
+        for (int h = 0; h < 2; ++h) {
+            const int b = h ? bb : ba;
+            for (int idx = tid; idx < BW * m; idx += Cfg::NT) {
+                const int jl = idx / m, i = idx - jl * m;
+                const int col = b * BW + jl;
+                bufs[h * blk + i + ldc * jl] = col < n ? A[i + (int64_t)m * col] : 0.0;
+            }
+        }
+    }
+    if (tid == 0) { flags[0] = 0; flags[1] = 0; mflags[0] = 0; mflags[1] = 0; }
+    cluster.sync();
+    int cur = 0, t = 0, sweep = 0;
+    for (; sweep < max_sweeps; ++sweep) {
+        if (tid == 0) { rot_sh = 0; mrel_sh = 0; }
+        for (int round = 0; round < nb - 1; ++round, ++t) {
+            const double *C = bufs + cur * NC * ldc;
+            // ---- 1. Gram G = CᵀC (tensor cores), k split over warps when there are few tiles
+            {
+                const int ks = warp % Cfg::KSPLIT;
+                for (int tile = warp / Cfg::KSPLIT; tile < Cfg::TILES; tile += 8 / Cfg::KSPLIT) {
+                    const int ta = tile / (NC / 8), tb = tile % (NC / 8);
+                    const double *ca = C + ldc * (8 * ta + (lane >> 2)) + (lane & 3);
+                    const double *cb = C + ldc * (8 * tb + (lane >> 2)) + (lane & 3);
+                    double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;   // two accumulator chains
+                    int k0 = 4 * ks;
+                    for (; k0 + 4 * Cfg::KSPLIT < m4; k0 += 8 * Cfg::KSPLIT) {
+                        dmma884(d0, d1, ca[k0], cb[k0]);
+                        dmma884(e0, e1, ca[k0 + 4 * Cfg::KSPLIT], cb[k0 + 4 * Cfg::KSPLIT]);
+                    }
+                    if (k0 < m4) dmma884(d0, d1, ca[k0], cb[k0]);
+                    d0 += e0;
+                    d1 += e1;
+                    double *gp = Gp + ks * NC * NC + NC * (8 * ta + (lane >> 2)) + 8 * tb + 2 * (lane & 3);
+                    gp[0] = d0;
+                    gp[1] = d1;
+                }
+            }
+            __syncthreads();
+            for (int e = tid; e < NC * NC; e += Cfg::NT) {
+                double s = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < Cfg::KSPLIT; ++ks) s += Gp[ks * NC * NC + e];
+                const int x = e / NC, y = e - x * NC;
+                Gs[x * LDG + y] = s;
+                Vs[x * LDG + y] = (x == y) ? 1.0 : 0.0;
+            }
+            __syncthreads();
+            // ---- 2. Jacobi steps on G, V accumulated: G_new = Jᵀ G J, V_new = V J (ping-pong
+            // buffers, one barrier per step).  Every warp computes the NC/2 rotations of the step
+            // (lane w -> pair w; identical on every warp) and hands them to the lanes owning
+            // entries (x, y) by shuffles.
+            int gi = 0;
+            {
+                int rot = 0;
+                float mrel = 0.f;
+                for (int st = (round == 0 ? 0 : BW - 1); st < NC - 1; ++st) {
+                    const double *G0 = Gs + gi * NC * LDG;
+                    const double *V0 = Vs + gi * NC * LDG;
+                    double *G1 = Gs + (gi ^ 1) * NC * LDG;
+                    double *V1 = Vs + (gi ^ 1) * NC * LDG;
+                    double cw, sw;
+                    {
+                        const int pq = ptab[st * (NC / 2) + lane % (NC / 2)];
+                        const int p = pq & 255, q = pq >> 8;
+                        rot |= pair_rotation(G0[p * LDG + p], G0[q * LDG + q], G0[p * LDG + q], tol2, cw, sw, mrel);
+                    }
+#pragma unroll
+                    for (int j = 0; j < NC * NC / Cfg::NT; ++j) {
+                        const int e = tid + Cfg::NT * j;
+                        const int x = e / NC, y = e - x * NC;
+                        const int tx = tab[st * NC + x], ty = tab[st * NC + y];
+                        const int xb = tx & 255, yb = ty & 255;
+                        const double cxx = __shfl_sync(0xffffffffu, cw, (tx >> 8) & 255);
+                        const double sx0 = __shfl_sync(0xffffffffu, sw, (tx >> 8) & 255);
+                        const double cyy = __shfl_sync(0xffffffffu, cw, (ty >> 8) & 255);
+                        const double sy0 = __shfl_sync(0xffffffffu, sw, (ty >> 8) & 255);
+                        // C'_p = c C_p - s C_q,  C'_q = s C_p + c C_q
+                        const double sxx = (tx >> 16) ? -sx0 : sx0, syy = (ty >> 16) ? -sy0 : sy0;
+                        const double g = cxx * (cyy * G0[x * LDG + y] + syy * G0[x * LDG + yb]) +
+                                         sxx * (cyy * G0[xb * LDG + y] + syy * G0[xb * LDG + yb]);
+                        G1[x * LDG + y] = g;
+                        V1[x * LDG + y] = V0[x * LDG + y] * cyy + V0[x * LDG + yb] * syy;
+                    }
+                    __syncthreads();
+                    gi ^= 1;
+                }
+                if (rot) rot_sh = 1;   // benign races: every writer stores 1 / a larger value
+                if (lane == 0 && mrel > 0.f) atomicMax(&mrel_sh, __float_as_int(mrel));
+            }
+            // ---- 3. C·V on the tensor cores, stored into the next-round buffers
+            {
+                const double *V = Vs + gi * NC * LDG;
+                double *nxt_local = bufs + (cur ^ 1) * NC * ldc;
+                double *dstA, *dstB;
+                if (ncta == 1) { dstA = nxt_local; dstB = nxt_local + blk; }
+                else if (c == 0) { dstA = cluster.map_shared_rank(nxt_local, 1) + blk; dstB = nxt_local + blk; }
+                else {
+                    dstA = cluster.map_shared_rank(nxt_local, c - 1);
+                    dstB = (c + 1 < ncta) ? cluster.map_shared_rank(nxt_local, c + 1) + blk : nxt_local;
+                }
+                const int ntiles = (m8 / 8) * (NC / 8);
+                for (int tile = warp; tile < ntiles; tile += 8) {
+                    const int it = tile / (NC / 8), jt = tile - it * (NC / 8);
+                    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                    for (int k0 = 0; k0 < NC; k0 += 4) {
+                        const double a = C[ldc * (k0 + (lane & 3)) + 8 * it + (lane >> 2)];
+                        const double b = V[(k0 + (lane & 3)) * LDG + 8 * jt + (lane >> 2)];
+                        dmma884(d0, d1, a, b);
+                    }
+                    const int row = 8 * it + (lane >> 2);
+                    const int col = 8 * jt + 2 * (lane & 3);   // col, col+1 in the same slot (BW % 8 == 0)
+                    double *dst = (col < BW) ? dstA + ldc * col : dstB + ldc * (col - BW);
+                    dst[row] = d0;
+                    dst[row + ldc] = d1;
+                }
+            }
+            cluster.sync();
+            cur ^= 1;
+        }
+        // convergence: no rotation anywhere, or the largest relative off-diagonal rotated in this
+        // sweep was below `early` (Jacobi converges quadratically: the next sweep would start
+        // from ~early², below the rotation threshold)
+        if (tid == 0 && rot_sh) atomicOr(cluster.map_shared_rank(&flags[sweep & 1], 0), 1);
+        if (tid == 0 && mrel_sh) atomicMax(cluster.map_shared_rank(&mflags[sweep & 1], 0), mrel_sh);
+        cluster.sync();
+        const int any = *cluster.map_shared_rank(&flags[sweep & 1], 0);
+        const float mx = __int_as_float(*cluster.map_shared_rank(&mflags[sweep & 1], 0));
+        if (c == 0 && tid == 0) { flags[(sweep + 1) & 1] = 0; mflags[(sweep + 1) & 1] = 0; }
+        cluster.sync();
+        if (!any || mx < early) break;
+    }
+    {
+        const int tt = t % (nb - 1);
+        const int ba = (c == 0) ? tt : (tt + c) % (nb - 1);
+        const int bb = (c == 0) ? nb - 1 : (tt - c + (nb - 1)) % (nb - 1);
+        const double *C = bufs + cur * NC * ldc;
+        for (int h = 0; h < 2; ++h) {
+            const int b = h ? bb : ba;
+            for (int idx = tid; idx < BW * m; idx += Cfg::NT) {
+                const int jl = idx / m, i = idx - jl * m;
+                const int col = b * BW + jl;
+                if (col < n) A[i + (int64_t)m * col] = C[h * blk + i + ldc * jl];
+            }
+        }
+    }
+    if (c == 0 && tid == 0 && sweeps_out) *sweeps_out = sweep + 1;
+}
+
+template <int NC>
+static bool launch_gram(int m, int n, double *T, int *sweeps, cudaStream_t st, float tol, float early) {
+    using Cfg = GramCfg<NC>;
+    int nb = (int)cdiv(n, Cfg::BW);
+    nb += nb & 1;
+    if (nb < 2) nb = 2;
+    const int ncta = nb / 2;
+    if (ncta > 16) return false;
+    const size_t smem = Cfg::smem(m);
+    if (smem > 220 * 1024) return false;
+    auto kern = jacobi_gram_kernel<NC>;
+    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (ncta > 8) SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ncta);
+    cfg.blockDim = dim3(Cfg::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ncta; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr; cfg.numAttrs = 1;
+    int max_sweeps = 60;
+    SSA_CUDA(cudaLaunchKernelEx(&cfg, kern, m, n, nb, T, tol, early, max_sweeps, sweeps));
+    after_launch("jacobi_gram");
+    return true;
+}
+
 template <int MR, int BW>
 static bool launch_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st, float tol) {
     int nb = (int)cdiv(n, BW);
@@ -267,8 +555,11 @@ static bool launch_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st
 }
 
 // prefer the cluster kernel; fall back to the cooperative-grid kernel for large n
-static bool jacobi_try_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st, float tol) {
+static bool jacobi_try_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st, float tol, float early) {
     if (std::getenv("SSA_JACOBI_GRID")) return false;
+    static const int nc_env = [] { const char *e = std::getenv("SSA_JACOBI_NC"); return e ? std::atoi(e) : 16; }();
+    if (nc_env == 16 && launch_gram<16>(m, n, T, sweeps, st, tol, early)) return true;
+    if ((nc_env == 16 || nc_env == 32) && launch_gram<32>(m, n, T, sweeps, st, tol, early)) return true;
     static const int bw16 = std::getenv("SSA_JACOBI_BW16") ? 1 : 0;
     if (bw16 && n <= 256) {
         if (m <= 128) return launch_cluster<4, 16>(m, n, T, sweeps, st, tol);
@@ -375,10 +666,11 @@ static bool jacobi_try_smem(int m, int n, double *T, int *sweeps, cudaStream_t s
     return true;
 }
 
-void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st, double tol_d) {
+void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st, double tol_d,
+                        double early) {
     const float tol = (float)tol_d;
     if (jacobi_try_smem(m, n, T, sweeps, st)) return;
-    if (jacobi_try_cluster(m, n, T, sweeps, st, tol)) return;
+    if (jacobi_try_cluster(m, n, T, sweeps, st, tol, (float)early)) return;
     int nb = (int)cdiv(n, kBW);
     nb += nb & 1;
     if (nb < 2) nb = 2;
@@ -396,6 +688,34 @@ void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cud
     SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SSA_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(32 * kBW), args, smem, st));
     after_launch("jacobi_block");
+}
+
+// After the Jacobi: nrm[j] = ||A_j|| (the singular values) and W = T0ᵀ·A (n x n), from which
+// the caller forms the right vectors z_j = T0ᵀ y_j / θ_j = W[:, j] / θ_j² without a host
+// pass over T.  Block j: warp 0 the norm, then the 8 warps over the rows i of W[:, j].
+__global__ void __launch_bounds__(256)
+ritz_tn_kernel(int m, int n, const double *__restrict__ T0, const double *__restrict__ A, double *__restrict__ W,
+               double *__restrict__ nrm) {
+    const int j = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double *aj = A + (int64_t)m * j;
+    if (warp == 0) {
+        double s = 0.0;
+        for (int k = lane; k < m; k += 32) s = fma(aj[k], aj[k], s);
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) nrm[j] = sqrt(s);
+    }
+    for (int i = warp; i < n; i += 8) {
+        const double *ti = T0 + (int64_t)m * i;
+        double s = 0.0;
+        for (int k = lane; k < m; k += 32) s = fma(ti[k], aj[k], s);
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) W[i + (int64_t)n * j] = s;
+    }
+}
+
+void ritz_tn(int m, int n, const double *T0, const double *A, double *W, double *nrm, cudaStream_t st) {
+    ritz_tn_kernel<<<n, 256, 0, st>>>(m, n, T0, A, W, nrm);
+    after_launch("ritz_tn");
 }
 
 bool jacobi_blocked_fits(int m, int n) {
@@ -420,7 +740,7 @@ extern "C" ssa_status ssa_small_svd(int32_t m, int32_t n, double *A, int32_t *sw
         cudaEvent_t e0, e1;
         SSA_CUDA(cudaEventCreate(&e0)); SSA_CUDA(cudaEventCreate(&e1));
         SSA_CUDA(cudaEventRecord(e0, nullptr));
-        jacobi_svd_blocked(m, n, d.as<double>(), dc, ds, nullptr, 1e-12);
+        jacobi_svd_blocked(m, n, d.as<double>(), dc, ds, nullptr, 1e-12, 1e-6);
         SSA_CUDA(cudaEventRecord(e1, nullptr));
         SSA_CUDA(cudaEventSynchronize(e1));
         float t = 0.f;

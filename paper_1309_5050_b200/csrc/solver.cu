@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "common.h"
@@ -74,8 +75,9 @@ struct Staging {
     }
 };
 
-void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st, double tol);
+void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st, double tol, double early);
 bool jacobi_blocked_fits(int m, int n);
+void ritz_tn(int m, int n, const double *T0, const double *A, double *W, double *nrm, cudaStream_t st);
 bool jacobi_smem_fits(int m, int n);
 
 template <typename T>
@@ -92,6 +94,8 @@ struct Gkl {
     std::vector<double> Alast;
     double anorm = 0.0;
     double ms_ritz = 0.0;
+    int last_sweeps = 0;
+    float last_kernel_ms = 0.f;
     int64_t nblock = 0, nvec = 0, n_cgs = 0;
     uint64_t sid = 1;
     double thr_abs, thr_rel, thr_chol;
@@ -626,25 +630,58 @@ struct Gkl {
         th.assign(n, 0.0); Y.assign((size_t)m * n, 0.0); Z.assign((size_t)n * n, 0.0);
         bool done = false;
         if (gpu_ritz && jacobi_blocked_fits(m, n)) {
-            Jd.alloc(sizeof(double) * ((size_t)m * n + 80), st);
-            double *Ad = Jd.as<double>();
-            const size_t ia = sg.take((size_t)m * n);
+            // device layout: A (m x n, rotated in place) | T0 (copy of T) | W (n x n) | nrm (n) | ints
+            const size_t mn = (size_t)m * n;
+            Jd.alloc(sizeof(double) * (2 * mn + (size_t)n * n + n + 80), st);
+            double *Ad = Jd.as<double>(), *T0d = Ad + mn, *Wd = T0d + mn, *nrmd = Wd + (size_t)n * n;
+            int *dints = reinterpret_cast<int *>(nrmd + n + 8);
+            const size_t ia = sg.take(mn);
             for (int j = 0; j < n; ++j)
                 std::memcpy(sg.h + ia + (size_t)m * j, &Tm[(size_t)ldT * j], sizeof(double) * m);
-            SSA_CUDA(cudaMemcpyAsync(Ad, sg.h + ia, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
+            SSA_CUDA(cudaMemcpyAsync(Ad, sg.h + ia, sizeof(double) * mn, cudaMemcpyHostToDevice, st));
+            SSA_CUDA(cudaMemcpyAsync(T0d, Ad, sizeof(double) * mn, cudaMemcpyDeviceToDevice, st));
             // off-diagonal tolerance: fp32 products resolve ~1e-7 relative, so 1e-9 (fp32) / 1e-12
             // (fp64) leaves the Ritz values exact to rounding and saves the last Jacobi sweep(s)
             static const double jtol = [] { const char *e = std::getenv("SSA_JACOBI_TOL"); return e ? std::atof(e) : 0.0; }();
             const double tolj = jtol > 0 ? jtol : (sizeof(T) == 4 ? 1e-9 : 1e-12);
-            jacobi_svd_blocked(m, n, Ad, reinterpret_cast<int *>(Ad + (size_t)m * n + 8), nullptr, st, tolj);
-            std::vector<double> A((size_t)m * n);
-            SSA_CUDA(cudaMemcpyAsync(A.data(), Ad, sizeof(double) * m * n, cudaMemcpyDeviceToHost, st));
-            sg.sync();
-            std::vector<double> nrm(n);
-            for (int j = 0; j < n; ++j) {
-                double t = 0; for (int i = 0; i < m; ++i) t += A[i + (size_t)m * j] * A[i + (size_t)m * j];
-                nrm[j] = std::sqrt(t);
+            if (const char *dump = std::getenv("SSA_DUMP_T")) {   // debug: projected matrices for offline study
+                static int ndump = 0;
+                const std::string fn = std::string(dump) + "_" + std::to_string(ndump++) + ".bin";
+                if (FILE *f = std::fopen(fn.c_str(), "wb")) {
+                    const int32_t hdr[2] = {m, n};
+                    std::fwrite(hdr, sizeof(hdr), 1, f);
+                    std::fwrite(sg.h + ia, sizeof(double), mn, f);
+                    std::fclose(f);
+                }
             }
+            int *dsw = dints + 64;
+            cudaEvent_t je0 = nullptr, je1 = nullptr;
+            if (debug) {
+                SSA_CUDA(cudaEventCreate(&je0)); SSA_CUDA(cudaEventCreate(&je1));
+                SSA_CUDA(cudaEventRecord(je0, st));
+            }
+            // early stop once a sweep's largest rotated relative off-diagonal is below 1e-4 (fp32) /
+            // 1e-6 (fp64): the columns then end orthogonal to ~1e-8 / 1e-12 (quadratic convergence)
+            static const double jearly = [] { const char *e = std::getenv("SSA_JACOBI_EARLY"); return e ? std::atof(e) : -1.0; }();
+            const double early = jearly >= 0 ? jearly : (sizeof(T) == 4 ? 1e-4 : 1e-6);
+            jacobi_svd_blocked(m, n, Ad, dints, debug ? dsw : nullptr, st, tolj, early);
+            if (debug) {
+                SSA_CUDA(cudaEventRecord(je1, st));
+                SSA_CUDA(cudaMemcpyAsync(&last_sweeps, dsw, sizeof(int), cudaMemcpyDeviceToHost, st));
+            }
+            ritz_tn(m, n, T0d, Ad, Wd, nrmd, st);
+            // A | T0 | W | nrm: fetch A, then W and nrm (contiguous)
+            std::vector<double> A(mn), Wn((size_t)n * n + n);
+            SSA_CUDA(cudaMemcpyAsync(A.data(), Ad, sizeof(double) * mn, cudaMemcpyDeviceToHost, st));
+            SSA_CUDA(cudaMemcpyAsync(Wn.data(), Wd, sizeof(double) * ((size_t)n * n + n), cudaMemcpyDeviceToHost, st));
+            sg.sync();
+            if (debug) {
+                float jms = 0.f;
+                SSA_CUDA(cudaEventElapsedTime(&jms, je0, je1));
+                last_kernel_ms = jms;
+                cudaEventDestroy(je0); cudaEventDestroy(je1);
+            }
+            const double *nrm = Wn.data() + (size_t)n * n;
             std::vector<int> idx(n);
             for (int j = 0; j < n; ++j) idx[j] = j;
             std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return nrm[a] > nrm[b]; });
@@ -654,19 +691,14 @@ struct Gkl {
                 const double inv = nrm[c] > 0 ? 1.0 / nrm[c] : 0.0;
                 for (int i = 0; i < m; ++i) Y[i + (size_t)m * j] = A[i + (size_t)m * c] * inv;
             }
-            // right vectors of the kept triples: z_j = Tᵀ y_j / σ_j (needs σ_j well above 0)
+            // right vectors of the kept triples: z_j = Tᵀ y_j / θ_j = W[:, c] / θ_j² (needs θ_j well above 0)
             const int need = std::min(n, std::max(pk, r));
             const double floor_rel = (sizeof(T) == 4) ? 1e-9 : 1e-13;
             if (th[need - 1] > floor_rel * th[0]) {
                 for (int j = 0; j < need; ++j) {
-                    const double inv = 1.0 / th[j];
-                    for (int c = 0; c < n; ++c) {
-                        double s = 0.0;
-                        const double *tc = &Tm[(size_t)ldT * c];
-                        const double *yj = &Y[(size_t)m * j];
-                        for (int i = 0; i < m; ++i) s += tc[i] * yj[i];
-                        Z[c + (size_t)n * j] = s * inv;
-                    }
+                    const double inv2 = 1.0 / (th[j] * th[j]);
+                    const double *wc = Wn.data() + (size_t)n * idx[j];
+                    for (int c = 0; c < n; ++c) Z[c + (size_t)n * j] = wc[c] * inv2;
                 }
                 done = true;
             }
@@ -674,7 +706,8 @@ struct Gkl {
         if (!done) svd_jacobi(m, n, Tm.data(), ldT, th.data(), Y.data(), Z.data());
         const double dt = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         ms_ritz += dt;
-        if (debug) std::fprintf(stderr, "[ssa] ritz_svd %dx%d %s %.3f ms\n", m, n, done ? "device" : "host", dt);
+        if (debug) std::fprintf(stderr, "[ssa] ritz_svd %dx%d %s %.3f ms (kernel %.3f ms, %d sweeps)\n", m, n, done ? "device" : "host", dt,
+                                last_kernel_ms, last_sweeps);
     }
 
     void run(int r_, ssa_decomp_info *info) {
