@@ -191,11 +191,21 @@ ssa_status ssa_wcor(ssa_plan p, const int32_t *grp_off, const int32_t *grp_idx,
                     int32_t n_groups, double *rho);
 
 /* The solver's projected-matrix SVD as a utility: one-sided
- * Jacobi in fp64 on the device, one CTA, for m >= n and m*n*8 bytes <= ~220 KB
- * (n <= 192).  A (host, m x n column-major) is overwritten with A·J whose
- * columns are σ_j·y_j (unsorted); sweeps and device milliseconds are returned
- * when the pointers are non-NULL.  SSA_ERR_ARG if the matrix does not fit. */
+ * block Jacobi in fp64 on the device (one thread-block cluster for n <= 256, a
+ * cooperative grid above), for m >= n, m <= 768.  A (host, m x n column-major)
+ * is overwritten with A·J whose columns are σ_j·y_j (unsorted); sweeps and
+ * device milliseconds are returned when the pointers are non-NULL.
+ * SSA_ERR_ARG if the matrix does not fit. */
 ssa_status ssa_small_svd(int32_t m, int32_t n, double *A, int32_t *sweeps, double *ms);
+
+/* Micro-benchmark of the solver's tall-skinny fp32 kernels on seeded device data
+ * (test / tuning hook, no host data): which = 0 times the Gram G = AᵀB (A: M x n1,
+ * B: M x n2, n1 <= 512, n2 <= 64), which = 1 the update W -= A·C (A: M x n1,
+ * W: M x n2).  Leading dimension M rounded up to 32 (the solver's layout).
+ * *ms = average device milliseconds over `reps` launches after one warm-up;
+ * *check = a checksum of the result (Σ|G| or Σ|W|).  SSA_ERR_ARG on bad sizes. */
+ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32_t n2, int32_t reps, double *ms,
+                          double *check);
 
 const char *ssa_last_error(void);
 const char *ssa_version(void);

@@ -150,8 +150,10 @@ void op_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k) {
     }
     // window-position band partition: sum the L x k partials
     if (p.has_comm && p.comm.world > 1) {
-        if (ldu != p.L) throw Error(SSA_ERR_ARG, "multi-GPU X·V needs a packed output");
-        if (p.comm.allreduce_sum(p.comm.user, U, p.L * (int64_t)k, p.dt, p.st) != 0)
+        // one allreduce over the k columns as stored (ldu >= L; rows L..ldu-1 between the
+        // columns are the solver's zero padding, identical on every rank, or caller scratch)
+        if (ldu < p.L) throw Error(SSA_ERR_ARG, "X·V output leading dimension below L");
+        if (p.comm.allreduce_sum(p.comm.user, U, ldu * (int64_t)(k - 1) + p.L, p.dt, p.st) != 0)
             throw Error(SSA_ERR_COMM, "allreduce of X·V partials failed");
     }
 }

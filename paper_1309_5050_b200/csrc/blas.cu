@@ -3,6 +3,9 @@
 // right-multiplications A·C, column scaling, and a counter-based normal RNG.
 // All are HBM-bound streaming kernels over M = L or K rows.
 #include "common.h"
+#include <cstdlib>
+#include <cmath>
+#include <vector>
 #include "kernels.h"
 
 namespace ssa {
@@ -90,6 +93,11 @@ __global__ void gram_reduce_kernel(const double *__restrict__ partials, int npar
     if (lane == 0) G[a + (int64_t)n1 * b] = s;
 }
 
+void gram_reduce(const double *partials, int nparts, int n1, int n2, double *G, cudaStream_t st) {
+    gram_reduce_kernel<<<(unsigned)cdiv((int64_t)n1 * n2 * 32, 256), 256, 0, st>>>(partials, nparts, n1, n2, G);
+    after_launch("gram_reduce");
+}
+
 static int gram_ctas(int64_t M) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, 64), 2 * (int64_t)num_sms()));
 }
@@ -98,10 +106,192 @@ size_t gram_partial_bytes(int64_t M, int n1, int) {
     return (size_t)gram_ctas(M) * 4096 * sizeof(double) * (size_t)cdiv(std::max(n1, 64), 64);
 }
 
+// ---------------------------------------------------------------------------
+// Streaming fp32 Gram for tall-skinny column-major blocks (the K-side CGS / CholeskyQR
+// Grams): G (n1 x n2) = AᵀB over M rows, 16-byte aligned columns (lda, ldb % 4 == 0).
+// A CTA (256 threads, one per SM) walks 32-row chunks c, c + G, ... of all n1p (<= 256)
+// columns of A and NB columns of B, staged by a 4-deep cp.async pipeline into
+// column-major smem tiles (row pitch 36 floats: 16-byte rows of 4, pitch/4 odd).
+// Thread tile: 8 A columns (ti + 8a) x 4 B columns (tj + NB/4·b) — strided so the 8
+// threads of an LDS.128 phase hit distinct bank groups for A and broadcast B — each
+// step consuming 4 rows (12 LDS.128, 128 FFMA).  fp32 partial sums per 32 rows are
+// folded into fp64 accumulators; row groups (when n1 is small) are combined through
+// shared memory; per-CTA partials go to gram_reduce (fixed order, deterministic).
+// ---------------------------------------------------------------------------
+namespace gram2 {
+constexpr int R = 32, LDR = 36, STAGES = 4, NT = 256;
+__device__ __forceinline__ void cp_async16(float *dst, const float *src, int src_bytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+}  // namespace gram2
+
+template <int NB>
+__global__ void __launch_bounds__(256, 1)
+gram_stream_kernel(int64_t M, const float *__restrict__ A, int64_t lda, int n1, const float *__restrict__ B,
+                   int64_t ldb, int n2, int YG, int contig, double *__restrict__ partials) {
+    using namespace gram2;
+    extern __shared__ __align__(16) unsigned char gs_raw[];
+    float *sm = reinterpret_cast<float *>(gs_raw);
+    constexpr int TPT = 8 * (NB / 4);                  // threads per 64 x NB tile
+    const int tid = threadIdx.x;
+    const int RG = (NT / TPT) / YG;                     // row groups
+    const int ncolA = 64 * YG;                          // A columns staged per CTA
+    const int stage_f = (ncolA + NB) * LDR;             // floats per stage
+    A += lda * (int64_t)(ncolA * blockIdx.y);
+    const int n1c = min(ncolA, n1 - ncolA * (int)blockIdx.y);
+    const int g = tid / TPT, yg = g % YG, rg = g / YG;
+    const int ti = tid % 8, tj = (tid / 8) % (NB / 4);
+    const int64_t nchunks = (M + R - 1) / R;
+    // ---- loader: (n1c + n2) columns x R/4 float4 per stage
+    auto load = [&](int64_t chunk, int buf) {
+        float *As = sm + buf * stage_f, *Bs = As + ncolA * LDR;
+        const int64_t r0 = chunk * R;
+        const int tot = (n1c + n2) * (R / 4);
+        for (int idx = tid; idx < tot; idx += NT) {
+            const int col = idx / (R / 4), q = idx % (R / 4);
+            const int64_t row = r0 + 4 * q;
+            const int64_t rem = M - row;
+            const int bytes = rem >= 4 ? 16 : (rem > 0 ? 4 * (int)rem : 0);
+            if (col < n1c) cp_async16(As + col * LDR + 4 * q, A + lda * col + (bytes ? row : 0), bytes);
+            else {
+                const int cb = col - n1c;
+                cp_async16(Bs + cb * LDR + 4 * q, B + ldb * cb + (bytes ? row : 0), bytes);
+            }
+        }
+    };
+    // zero the column padding once (columns n1c..ncolA-1 and n2..NB-1 stay zero)
+    for (int idx = tid; idx < STAGES * stage_f; idx += NT) sm[idx] = 0.f;
+    __syncthreads();
+    // chunks of this CTA: a contiguous range (contig) or every gridDim.x-th chunk
+    int64_t c0, cstep, my;
+    if (contig) {
+        const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+        c0 = blockIdx.x * per; cstep = 1;
+        my = max((int64_t)0, min(per, nchunks - c0));
+    } else {
+        c0 = blockIdx.x; cstep = gridDim.x;
+        my = (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    }
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < my) load(c0 + (int64_t)s * cstep, s);
+        cp_commit();
+    }
+    double accd[8][4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) accd[a][b] = 0.0;
+    const int colA0 = 64 * yg + ti;
+    for (int64_t i = 0; i < my; ++i) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int64_t nx = i + STAGES - 1;
+            if (nx < my) load(c0 + nx * cstep, (int)(nx % STAGES));
+            cp_commit();
+        }
+        const float *As = sm + (int)(i % STAGES) * stage_f, *Bs = As + ncolA * LDR;
+        float acc[8][4];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+        for (int q = rg; q < R / 4; q += RG) {
+            float4 av[8], bv[4];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) av[a] = *reinterpret_cast<const float4 *>(As + (colA0 + 8 * a) * LDR + 4 * q);
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bv[b] = *reinterpret_cast<const float4 *>(Bs + (tj + (NB / 4) * b) * LDR + 4 * q);
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    acc[a][b] = fmaf(av[a].x, bv[b].x, acc[a][b]);
+                    acc[a][b] = fmaf(av[a].y, bv[b].y, acc[a][b]);
+                    acc[a][b] = fmaf(av[a].z, bv[b].z, acc[a][b]);
+                    acc[a][b] = fmaf(av[a].w, bv[b].w, acc[a][b]);
+                }
+        }
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) accd[a][b] += (double)acc[a][b];
+    }
+    cp_wait<0>();
+    __syncthreads();
+    // ---- combine row groups (fixed order) and write this CTA's partial tiles
+    double *red = reinterpret_cast<double *>(sm);        // [RG][YG][64][NB]
+    if (RG > 1) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                red[((rg * YG + yg) * 64 + ti + 8 * a) * NB + tj + (NB / 4) * b] = accd[a][b];
+        __syncthreads();
+        if (rg == 0) {
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    double s = accd[a][b];
+                    for (int r2 = 1; r2 < RG; ++r2) s += red[((r2 * YG + yg) * 64 + ti + 8 * a) * NB + tj + (NB / 4) * b];
+                    accd[a][b] = s;
+                }
+        }
+    }
+    if (rg != 0) return;
+    const int ych = (int)blockIdx.y * YG + yg;          // global 64-column chunk of A
+    if (64 * yg >= n1c) return;
+    double *out = partials + ((int64_t)ych * gridDim.x + blockIdx.x) * 4096;
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int al = ti + 8 * a, bl = tj + (NB / 4) * b;
+            if (bl < n2) out[al + 64 * bl] = accd[a][b];
+        }
+}
+
+static bool gram_stream(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2,
+                        double *G, double *partials, size_t partial_bytes, cudaStream_t st) {
+    static const bool off = std::getenv("SSA_GRAM_OLD") != nullptr;
+    if (off || M < 4096 || (lda & 3) || (ldb & 3) || ((uintptr_t)A & 15) || ((uintptr_t)B & 15) || n2 > 64) return false;
+    const int NB = n2 <= 32 ? 32 : 64;
+    const int tiles = (NB == 32) ? 4 : 2;               // 64 x NB tiles computed in parallel per CTA
+    const int ych = (int)cdiv(n1, 64);
+    const int YG = std::min(ych, tiles);
+    const int gy = (int)cdiv(ych, YG);
+    const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, gram2::R));
+    static const int contig = [] { const char *e = std::getenv("SSA_GRAM_CONTIG"); return e ? std::atoi(e) : 1; }();
+    if ((size_t)ctas * 4096 * sizeof(double) * (size_t)ych > partial_bytes) return false;
+    // pipeline stages; reused at the end for the row-group combine ([RG][YG][64][NB] doubles)
+    const size_t smem = std::max(sizeof(float) * (size_t)gram2::STAGES * (64 * YG + NB) * gram2::LDR,
+                                 sizeof(double) * (size_t)tiles * 64 * NB);
+    if (NB == 32) {
+        SSA_CUDA(cudaFuncSetAttribute(gram_stream_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        gram_stream_kernel<32><<<dim3(ctas, gy), 256, smem, st>>>(M, A, lda, n1, B, ldb, n2, YG, contig, partials);
+    } else {
+        SSA_CUDA(cudaFuncSetAttribute(gram_stream_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        gram_stream_kernel<64><<<dim3(ctas, gy), 256, smem, st>>>(M, A, lda, n1, B, ldb, n2, YG, contig, partials);
+    }
+    after_launch("gram_stream");
+    gram_reduce_kernel<<<(unsigned)cdiv((int64_t)n1 * n2 * 32, 256), 256, 0, st>>>(partials, ctas, n1, n2, G);
+    after_launch("gram_reduce");
+    return true;
+}
+
 template <typename T>
 void gram_tn(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb, int n2,
              double *G, double *partials, size_t partial_bytes, cudaStream_t st) {
     SSA_REQUIRE(n2 <= 64 && n1 <= 512, SSA_ERR_ARG, "gram_tn: at most 512 x 64 per call");
+    if constexpr (sizeof(T) == 4) {
+        if (gram_tc(M, A, lda, n1, B, ldb, n2, G, partials, partial_bytes, st)) return;
+        if (gram_stream(M, A, lda, n1, B, ldb, n2, G, partials, partial_bytes, st)) return;
+    }
     const int ctas = gram_ctas(M);
     const int ych = (int)cdiv(n1, 64);
     SSA_REQUIRE((size_t)ctas * 4096 * sizeof(double) * ych <= partial_bytes, SSA_ERR_ARG, "gram_tn: workspace");
@@ -156,11 +346,152 @@ gemm_small_kernel(int64_t M, const T *A, int64_t lda, int m, const double *__res
     }
 }
 
+// ---------------------------------------------------------------------------
+// Streaming fp32 update for tall-skinny blocks (CGS projections, recurrence terms,
+// CholeskyQR applies): Out (M x n) = beta·Out + alpha·A (M x m)·C (m x n), n <= NC, Out may
+// equal A (in place: every row tile is read completely before it is written).
+// 128 threads per CTA, one CTA per SM walking 256-row tiles; each tile streams its m columns
+// in 32-column chunks through a 3-deep cp.async pipeline ([32 cols][256 rows] smem tiles).
+// Thread t owns rows 2t, 2t+1 of the tile and all NC outputs (2·NC fp32 accumulators):
+// per column one LDS.64 of A and NC/4 broadcast LDS.128 of alpha·C (fp32, in smem).
+// ---------------------------------------------------------------------------
+namespace upd2 {
+constexpr int ROWS = 256, KC = 32, STAGES = 3, NT = 128;
+}
+
+template <int NC>
+__global__ void __launch_bounds__(128, 1)
+tall_update_kernel(int64_t M, const float *A, int64_t lda, int m, const double *__restrict__ C, int ldc, int n,
+                   double alpha, double beta, float *Out, int64_t ldo) {
+    using namespace upd2;
+    using gram2::cp_async16;
+    using gram2::cp_commit;
+    using gram2::cp_wait;
+    extern __shared__ __align__(16) unsigned char us_raw[];
+    float *Cs = reinterpret_cast<float *>(us_raw);                 // [m][NC] alpha·C
+    float *St = Cs + (size_t)m * NC;                                 // [STAGES][KC][ROWS]
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < m * NC; idx += NT) {
+        const int a = idx / NC, b = idx % NC;
+        Cs[idx] = (b < n) ? (float)(alpha * C[a + (int64_t)ldc * b]) : 0.f;
+    }
+    const int nchk = (m + KC - 1) / KC;
+    const int64_t ntiles = (M + ROWS - 1) / ROWS;
+    // work items (tile, chunk) of this CTA, in order
+    const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t nitems = my_tiles * nchk;
+    auto load = [&](int64_t it, int buf) {
+        const int64_t tile = blockIdx.x + (it / nchk) * gridDim.x;
+        const int ch = (int)(it % nchk);
+        const int64_t r0 = tile * ROWS;
+        float *dst = St + (size_t)buf * KC * ROWS;
+        const int ncol = min(KC, m - ch * KC);
+        for (int idx = tid; idx < KC * (ROWS / 4); idx += NT) {
+            const int c = idx / (ROWS / 4), q = idx % (ROWS / 4);
+            const int64_t row = r0 + 4 * q;
+            const int64_t rem = M - row;
+            const int bytes = (c < ncol) ? (rem >= 4 ? 16 : (rem > 0 ? 4 * (int)rem : 0)) : 0;
+            cp_async16(dst + c * ROWS + 4 * q, A + lda * (int64_t)(ch * KC + (c < ncol ? c : 0)) + (bytes ? row : 0), bytes);
+        }
+    };
+#pragma unroll
+    for (int st = 0; st < STAGES - 1; ++st) {
+        if (st < nitems) load(st, st);
+        cp_commit();
+    }
+    __syncthreads();   // Cs ready
+    float acc0[NC], acc1[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) { acc0[j] = 0.f; acc1[j] = 0.f; }
+    for (int64_t it = 0; it < nitems; ++it) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int64_t nx = it + STAGES - 1;
+            if (nx < nitems) load(nx, (int)(nx % STAGES));
+            cp_commit();
+        }
+        const int ch = (int)(it % nchk);
+        const float *Sb = St + (size_t)(it % STAGES) * KC * ROWS;
+        const int ncol = min(KC, m - ch * KC);
+        for (int c = 0; c < ncol; ++c) {
+            const float2 a = *reinterpret_cast<const float2 *>(Sb + c * ROWS + 2 * tid);
+            const float4 *cr = reinterpret_cast<const float4 *>(Cs + (size_t)(ch * KC + c) * NC);
+#pragma unroll
+            for (int j4 = 0; j4 < NC / 4; ++j4) {
+                const float4 cv = cr[j4];
+                acc0[4 * j4 + 0] = fmaf(a.x, cv.x, acc0[4 * j4 + 0]);
+                acc0[4 * j4 + 1] = fmaf(a.x, cv.y, acc0[4 * j4 + 1]);
+                acc0[4 * j4 + 2] = fmaf(a.x, cv.z, acc0[4 * j4 + 2]);
+                acc0[4 * j4 + 3] = fmaf(a.x, cv.w, acc0[4 * j4 + 3]);
+                acc1[4 * j4 + 0] = fmaf(a.y, cv.x, acc1[4 * j4 + 0]);
+                acc1[4 * j4 + 1] = fmaf(a.y, cv.y, acc1[4 * j4 + 1]);
+                acc1[4 * j4 + 2] = fmaf(a.y, cv.z, acc1[4 * j4 + 2]);
+                acc1[4 * j4 + 3] = fmaf(a.y, cv.w, acc1[4 * j4 + 3]);
+            }
+        }
+        if (ch == nchk - 1) {
+            // tile complete: every column of these rows has been read (cp.async data consumed
+            // above); write the outputs, then reset the accumulators
+            const int64_t tile = blockIdx.x + (it / nchk) * gridDim.x;
+            const int64_t row = tile * ROWS + 2 * tid;
+            const float fb = (float)beta;
+#pragma unroll
+            for (int j = 0; j < NC; ++j) {
+                if (j < n) {
+                    float *o = Out + row + ldo * (int64_t)j;
+                    if (row + 1 < M) {
+                        float2 v = make_float2(acc0[j], acc1[j]);
+                        if (beta != 0.0) {
+                            const float2 old = *reinterpret_cast<const float2 *>(o);
+                            v.x = fmaf(fb, old.x, v.x);
+                            v.y = fmaf(fb, old.y, v.y);
+                        }
+                        *reinterpret_cast<float2 *>(o) = v;
+                    } else if (row < M) {
+                        o[0] = (beta != 0.0) ? fmaf(fb, o[0], acc0[j]) : acc0[j];
+                    }
+                }
+                acc0[j] = 0.f;
+                acc1[j] = 0.f;
+            }
+        }
+    }
+    cp_wait<0>();
+}
+
+// true when handled (fp32, aligned columns, M large); Out == A allowed
+static bool tall_update(int64_t M, const float *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
+                        double beta, float *Out, int64_t ldo, cudaStream_t st) {
+    // measured (scripts/bench_tall.py): faster than the thread-per-row kernel only for wide
+    // blocks (m >= 256, n > 32: 4.2 vs 7.1 ms at M = 1.8M, m = 356, n = 64); SSA_UPD=1 forces it
+    static const int mode = [] { const char *e = std::getenv("SSA_UPD"); return e ? std::atoi(e) : -1; }();
+    if (mode == 0 || (mode < 0 && !(m >= 256 && n > 32))) return false;
+    if (M < 8192 || n > 64 || m > 512 || (lda & 3) || (ldo & 1) || ((uintptr_t)A & 15) || ((uintptr_t)Out & 7))
+        return false;
+    const int NC = n <= 32 ? 32 : 64;
+    const size_t smem = sizeof(float) * ((size_t)m * NC + (size_t)upd2::STAGES * upd2::KC * upd2::ROWS);
+    if (smem > 220 * 1024) return false;
+    const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, upd2::ROWS));
+    if (NC == 32) {
+        SSA_CUDA(cudaFuncSetAttribute(tall_update_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        tall_update_kernel<32><<<ctas, upd2::NT, smem, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
+    } else {
+        SSA_CUDA(cudaFuncSetAttribute(tall_update_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        tall_update_kernel<64><<<ctas, upd2::NT, smem, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
+    }
+    after_launch("tall_update");
+    return true;
+}
+
 template <typename T>
 void gemm_small(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n,
                 double alpha, double beta, T *Out, int64_t ldo, cudaStream_t st) {
     SSA_REQUIRE(m <= 64 && n <= 64, SSA_ERR_ARG, "gemm_small: at most 64x64");
     if (M <= 0 || n <= 0) return;
+    if constexpr (sizeof(T) == 4) {
+        if (tall_update(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo, st)) return;
+    }
     const bool inplace = (Out == A);
     // small M: spread the column chunks over more CTAs (not in place)
     const int gy = inplace ? 1 : (int)std::min<int64_t>(cdiv(n, 16), std::max<int64_t>(1, (2 * num_sms()) / cdiv(M, 128)));
@@ -217,6 +548,9 @@ void gemm_acc(int64_t M, const T *A, int64_t lda, int m, const double *C, int ld
               double beta, T *Out, int64_t ldo, cudaStream_t st) {
     SSA_REQUIRE(m <= 512 && n <= 64, SSA_ERR_ARG, "gemm_acc: at most 512 x 64");
     if (M <= 0 || n <= 0) return;
+    if constexpr (sizeof(T) == 4) {
+        if (tall_update(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo, st)) return;
+    }
     const unsigned grid = (unsigned)cdiv(M, 128);
     if (n <= 32) {
         const size_t smem = sizeof(T) * (size_t)m * 32;
@@ -606,3 +940,78 @@ template void gemm_cols<float>(int64_t, const float *, int64_t, int, const doubl
 template void gemm_cols<double>(int64_t, const double *, int64_t, int, const double *, int, int, double *, int64_t,
                                 cudaStream_t);
 }  // namespace ssa
+
+// read-bandwidth probe for the column-major tall-skinny layout (ssa_bench_tall which = 2):
+// CTA c streams a contiguous row range of all ncols columns, rch rows per column at a time
+__global__ void colread_kernel(int64_t M, const float *__restrict__ A, int64_t lda, int ncols, int rch, float *out) {
+    const int64_t per = ((M + gridDim.x - 1) / gridDim.x + 3) & ~3;
+    const int64_t r0 = blockIdx.x * per, r1 = min(M, r0 + per);
+    float acc = 0.f;
+    for (int64_t rb = r0; rb < r1; rb += rch) {
+        const int nr4 = (int)((min(r1, rb + rch) - rb) / 4);
+        for (int idx = threadIdx.x; idx < ncols * nr4; idx += blockDim.x) {
+            const int c = idx / nr4, q = idx % nr4;
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(A + lda * c + rb) + q);
+            acc += v.x + v.y + v.z + v.w;
+        }
+    }
+    if (acc == 123.456f) out[0] = acc;
+}
+
+// ---- ABI test hook: timing of the tall-skinny kernels on seeded device data
+extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32_t n2, int32_t reps, double *ms,
+                                     double *check) {
+    using namespace ssa;
+    try {
+        if (M < 1 || n1 < 1 || n1 > 512 || n2 < 1 || n2 > 64 || reps < 1 || which < 0 || which > 2)
+            throw Error(SSA_ERR_ARG, "ssa_bench_tall: bad sizes");
+        const int64_t ld = (M + 31) / 32 * 32;
+        DevBuf a, b, g, ws, c;
+        a.alloc(sizeof(float) * ld * n1, nullptr);
+        b.alloc(sizeof(float) * ld * n2, nullptr);
+        g.alloc(sizeof(double) * 512 * 64, nullptr);
+        c.alloc(sizeof(double) * 512 * 64, nullptr);
+        const size_t wsb = gram_partial_bytes(M, 512, 64);
+        ws.alloc(wsb, nullptr);
+        SSA_CUDA(cudaMemset(a.p, 0, sizeof(float) * ld * n1));
+        SSA_CUDA(cudaMemset(b.p, 0, sizeof(float) * ld * n2));
+        fill_normal<float>(M, a.as<float>(), ld, n1, 7, 1, nullptr);
+        fill_normal<float>(M, b.as<float>(), ld, n2, 7, 2, nullptr);
+        std::vector<double> hc((size_t)n1 * n2);
+        for (size_t t = 0; t < hc.size(); ++t) hc[t] = 1e-3 * (double)((t * 7919) % 1000) / 1000.0;
+        SSA_CUDA(cudaMemcpy(c.p, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice));
+        auto run = [&]() {
+            if (which == 2) colread_kernel<<<num_sms() * 2, 512>>>(M, a.as<float>(), ld, n1, 32 * n2, b.as<float>());
+            else if (which == 0) gram_tn<float>(M, a.as<float>(), ld, n1, b.as<float>(), ld, n2, g.as<double>(), ws.as<double>(), wsb, nullptr);
+            else gemm_acc<float>(M, a.as<float>(), ld, n1, c.as<double>(), n1, n2, -1.0, 1.0, b.as<float>(), ld, nullptr);
+        };
+        run();
+        cudaEvent_t e0, e1;
+        SSA_CUDA(cudaEventCreate(&e0)); SSA_CUDA(cudaEventCreate(&e1));
+        SSA_CUDA(cudaEventRecord(e0, nullptr));
+        for (int i = 0; i < reps; ++i) run();
+        SSA_CUDA(cudaEventRecord(e1, nullptr));
+        SSA_CUDA(cudaEventSynchronize(e1));
+        float t = 0.f;
+        SSA_CUDA(cudaEventElapsedTime(&t, e0, e1));
+        cudaEventDestroy(e0); cudaEventDestroy(e1);
+        if (ms) *ms = t / reps;
+        if (check) {
+            double s = 0.0;
+            if (which == 0) {
+                std::vector<double> hg((size_t)n1 * n2);
+                SSA_CUDA(cudaMemcpy(hg.data(), g.p, sizeof(double) * hg.size(), cudaMemcpyDeviceToHost));
+                for (double v : hg) s += std::fabs(v);
+            } else {
+                std::vector<float> hw((size_t)ld * n2);
+                SSA_CUDA(cudaMemcpy(hw.data(), b.p, sizeof(float) * hw.size(), cudaMemcpyDeviceToHost));
+                for (float v : hw) s += std::fabs((double)v);
+            }
+            *check = s;
+        }
+        return SSA_OK;
+    } catch (const Error &e) {
+        ssa_set_error(e.what());
+        return e.code;
+    }
+}

@@ -68,6 +68,10 @@ template <typename T>
 void gram_tn(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb, int n2,
              double *G, double *partials, size_t partial_bytes, cudaStream_t st);
 size_t gram_partial_bytes(int64_t M, int n1, int n2);
+void gram_reduce(const double *partials, int nparts, int n1, int n2, double *G, cudaStream_t st);
+// tcgen05 3xTF32 Gram (tall_tc.cu); false when the layout is unsupported
+bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2, double *G,
+             double *partials, size_t partial_bytes, cudaStream_t st);
 
 // Out (M x n) = beta*Out + alpha * A (M x m) * C (m x n, device double, column-major).
 // In-place (Out == A, with m == n) is allowed.

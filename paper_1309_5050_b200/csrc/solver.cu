@@ -117,8 +117,12 @@ struct Gkl {
         sg.init(1 << 18, st);
     }
 
-    T *P(int col) { return Pb.as<T>() + (int64_t)col * L; }
-    T *Q(int col) { return Qb.as<T>() + (int64_t)col * K; }
+    // basis leading dimensions: L and K rounded up to 32 elements (16-byte aligned columns for
+    // vector / async copies); the padding rows are zero and never written
+    int64_t ldP = 0, ldQ = 0;
+    int64_t LD(int64_t M) const { return M == K ? ldQ : ldP; }
+    T *P(int col) { return Pb.as<T>() + (int64_t)col * ldP; }
+    T *Q(int col) { return Qb.as<T>() + (int64_t)col * ldQ; }
 
     bool kside_comm() const { return p.has_comm && p.comm.world > 1; }
 
@@ -178,8 +182,8 @@ struct Gkl {
     void cgs(int64_t M, T *W, int kc, const T *Bm, int nb, bool kside, double *coef) {
         if (nb <= 0) return;
         std::vector<double> C((size_t)nb * kc);
-        gram(M, Bm, M, nb, W, M, kc, C.data(), kside);
-        gemm(M, Bm, M, nb, C.data(), nb, kc, -1.0, 1.0, W, M);
+        gram(M, Bm, LD(M), nb, W, LD(M), kc, C.data(), kside);
+        gemm(M, Bm, LD(M), nb, C.data(), nb, kc, -1.0, 1.0, W, LD(M));
         if (coef)
             for (size_t t = 0; t < C.size(); ++t) coef[t] += C[t];
     }
@@ -237,11 +241,11 @@ struct Gkl {
         // (||w_after||² < ½||w_before||², with ||w_before||² = ||c||² + ||w_after||²)
         auto project = [&](bool force_twice) {
             std::vector<double> C((size_t)na * kc);
-            gram(M, against, M, na, W, M, kc, C.data(), kside);
-            gemm(M, against, M, na, C.data(), na, kc, -1.0, 1.0, W, M);
+            gram(M, against, LD(M), na, W, LD(M), kc, C.data(), kside);
+            gemm(M, against, LD(M), na, C.data(), na, kc, -1.0, 1.0, W, LD(M));
             if (coef)
                 for (size_t t = 0; t < C.size(); ++t) coef[t] += C[t];
-            gram(M, W, M, kc, W, M, kc, G.data(), kside);
+            gram(M, W, LD(M), kc, W, LD(M), kc, G.data(), kside);
             bool need = force_twice;
             for (int j = 0; j < kc && !need; ++j) {
                 double c2 = 0.0;
@@ -249,11 +253,11 @@ struct Gkl {
                 need = c2 > G[j + (size_t)kc * j];
             }
             if (need) {
-                gram(M, against, M, na, W, M, kc, C.data(), kside);
-                gemm(M, against, M, na, C.data(), na, kc, -1.0, 1.0, W, M);
+                gram(M, against, LD(M), na, W, LD(M), kc, C.data(), kside);
+                gemm(M, against, LD(M), na, C.data(), na, kc, -1.0, 1.0, W, LD(M));
                 if (coef)
                     for (size_t t = 0; t < C.size(); ++t) coef[t] += C[t];
-                gram(M, W, M, kc, W, M, kc, G.data(), kside);
+                gram(M, W, LD(M), kc, W, LD(M), kc, G.data(), kside);
             }
             n_cgs += need ? 2 : 1;
         };
@@ -261,7 +265,7 @@ struct Gkl {
         if (na > 0) { project(false); have_gram = true; }
         int refills = 0;
         for (int pass = 0; pass < 6; ++pass) {
-            if (!have_gram) gram(M, W, M, kc, W, M, kc, G.data(), kside);
+            if (!have_gram) gram(M, W, LD(M), kc, W, LD(M), kc, G.data(), kside);
             have_gram = false;
             // exact breakdown: columns with (numerically) zero norm
             std::vector<int> zero;
@@ -278,7 +282,7 @@ struct Gkl {
                 ++refills;
                 for (int j : zero) {
                     for (int i = 0; i < kc; ++i) B[j + (size_t)kc * i] = 0.0;   // W_in has no component there
-                    fill_normal<T>(M, W + M * j, M, 1, p.seed, 0x5eed0000ull + (sid++), st);
+                    fill_normal<T>(M, W + LD(M) * j, LD(M), 1, p.seed, 0x5eed0000ull + (sid++), st);
                 }
                 if (na > 0) {
                     double *keep = coef;
@@ -320,7 +324,7 @@ struct Gkl {
             if (debug)
                 std::fprintf(stderr, "[ssa] orth M=%lld pass=%d na=%d zero=%zu chol=%d shifted=%d bad=%zu anorm=%.3e\n",
                              (long long)M, pass, na, zero.size(), (int)ok, (int)shifted, bad.size(), anorm);
-            gemm(M, W, M, kc, S.data(), kc, kc, 1.0, 0.0, W, M);   // in place (kc <= 64)
+            gemm(M, W, LD(M), kc, S.data(), kc, kc, 1.0, 0.0, W, LD(M));   // in place (kc <= 64)
             for (int b2 = 0; b2 < kc; ++b2)
                 for (int a2 = 0; a2 < kc; ++a2) {
                     double s2 = 0.0;
@@ -343,7 +347,7 @@ struct Gkl {
     bool orth_fast(int64_t M, T *W, int kc, const T *against, int na, bool kside, double *coef,
                    std::vector<double> &Bout) {
         if (!use_fast || kc > 64 || na + kc > 512) return false;
-        if (na > 0 && against + (int64_t)na * M != W) return false;   // needs [A W] contiguous
+        if (na > 0 && against + (int64_t)na * LD(M) != W) return false;   // needs [A W] contiguous
         T *A = na > 0 ? const_cast<T *>(against) : W;
         const int n1 = na + kc;
         const size_t nd = 3 * 512 * 64 + 64 * 64 + 16;
@@ -357,13 +361,13 @@ struct Gkl {
         double *hC = sg.h + ic, *hB = hC + (size_t)na * kc;
         int *hf = reinterpret_cast<int *>(hB + (size_t)kc * kc);
         for (int pass = 1; pass <= 3; ++pass) {
-            gram_tn<T>(M, A, M, n1, W, M, kc, dG, p.ws_gram.as<double>(), p.ws_gram.bytes, st);
+            gram_tn<T>(M, A, LD(M), n1, W, LD(M), kc, dG, p.ws_gram.as<double>(), p.ws_gram.bytes, st);
             if (kside && kside_comm()) {
                 if (p.comm.allreduce_sum(p.comm.user, dG, (int64_t)n1 * kc, SSA_F64, st) != 0)
                     throw Error(SSA_ERR_COMM, "allreduce of a K-side Gram failed");
             }
             orth_solve(dG, na, kc, pass, zt * zt, shift_rel, thr_chol, dMc, dC, dBt, flags, st);
-            apply_inplace<T>(M, A, M, n1, kc, dMc, flags, st);
+            apply_inplace<T>(M, A, LD(M), n1, kc, dMc, flags, st);
             if (pass == 1) continue;
             if (na > 0) SSA_CUDA(cudaMemcpyAsync(hC, dC, sizeof(double) * na * kc, cudaMemcpyDeviceToHost, st));
             SSA_CUDA(cudaMemcpyAsync(hB, dBt, sizeof(double) * kc * kc, cudaMemcpyDeviceToHost, st));
@@ -393,7 +397,7 @@ struct Gkl {
     std::vector<double> orth2(int64_t M, T *W, int kc, const T *against, int na, bool kside, double *coef) {
         // opt-in (SSA_ORTH2=1): measured no faster than `orth` on c2/c3 (the Gram / update
         // kernels, not the host round trips, dominate the K side), DESIGN.md §5
-        if (kc > 64 || na + kc > 512 || (na > 0 && against + (int64_t)na * M != W) || !std::getenv("SSA_ORTH2"))
+        if (kc > 64 || na + kc > 512 || (na > 0 && against + (int64_t)na * LD(M) != W) || !std::getenv("SSA_ORTH2"))
             return orth(M, W, kc, against, na, kside, coef);
         T *A = na > 0 ? const_cast<T *>(against) : W;
         const int n1 = na + kc;
@@ -402,7 +406,7 @@ struct Gkl {
         const double shift_rel = (sizeof(T) == 4) ? 1e-6 : 1e-13;
         bool prev_shifted = false;
         for (int pass = 1; pass <= 3; ++pass) {
-            gram(M, A, M, n1, W, M, kc, G.data(), kside);
+            gram(M, A, LD(M), n1, W, LD(M), kc, G.data(), kside);
             double dmax = 0.0, dev = 0.0;
             for (int b = 0; b < kc; ++b)
                 for (int a = 0; a <= b; ++a) {
@@ -499,13 +503,15 @@ struct Gkl {
         const size_t idx = sg.take((size_t)n1 * kc);
         std::memcpy(sg.h + idx, Mc, sizeof(double) * n1 * kc);
         SSA_CUDA(cudaMemcpyAsync(sg.dev(idx), sg.h + idx, sizeof(double) * n1 * kc, cudaMemcpyHostToDevice, st));
-        T *W = A + M * (int64_t)(n1 - kc);
+        const int64_t ld = LD(M);
+        T *W = A + ld * (int64_t)(n1 - kc);
         if (M >= 32768) {
-            apply_inplace<T>(M, A, M, n1, kc, sg.dev(idx), nullptr, st);
+            apply_inplace<T>(M, A, ld, n1, kc, sg.dev(idx), nullptr, st);
         } else {
             oop.alloc(sizeof(T) * M * kc, st);
-            gemm_cols<T>(M, A, M, n1, sg.dev(idx), n1, kc, oop.as<T>(), M, st);
-            SSA_CUDA(cudaMemcpyAsync(W, oop.p, sizeof(T) * M * kc, cudaMemcpyDeviceToDevice, st));
+            gemm_cols<T>(M, A, ld, n1, sg.dev(idx), n1, kc, oop.as<T>(), M, st);
+            SSA_CUDA(cudaMemcpy2DAsync(W, sizeof(T) * ld, oop.p, sizeof(T) * M, sizeof(T) * M, kc,
+                                       cudaMemcpyDeviceToDevice, st));
         }
     }
 
@@ -537,14 +543,14 @@ struct Gkl {
     }
     void product_xv(const T *Qin, T *Out, int kc) {
         mark();
-        op_xv<T>(p, Qin, K, Out, L, kc);
+        op_xv<T>(p, Qin, ldQ, Out, ldP, kc);
         mark();
         ev_xv.push_back(1);
         ++nblock; nvec += kc; ++n_xv; vec_xv += kc;
     }
     void product_xtu(const T *Pin, T *Out, int kc) {
         mark();
-        op_xtu<T>(p, Pin, L, Out, K, kc);
+        op_xtu<T>(p, Pin, ldP, Out, ldQ, kc);
         mark();
         ev_xv.push_back(0);
         ++nblock; nvec += kc; ++n_xtu; vec_xtu += kc;
@@ -561,7 +567,7 @@ struct Gkl {
         t0 = now_ms();
         if (anorm == 0.0) {
             std::vector<double> G((size_t)k * k);
-            gram(L, W, L, k, W, L, k, G.data(), false);
+            gram(L, W, ldP, k, W, ldP, k, G.data(), false);
             for (int j = 0; j < k; ++j) anorm = std::max(anorm, std::sqrt(std::max(G[j + (size_t)k * j], 0.0)));
         }
         // full projection onto the L basis; all CGS coefficients go into T so that
@@ -591,7 +597,7 @@ struct Gkl {
         tw_prod += now_ms() - t0;
         if (anorm == 0.0) {
             std::vector<double> G((size_t)k * k);
-            gram(K, W, K, k, W, K, k, G.data(), true);
+            gram(K, W, ldQ, k, W, ldQ, k, G.data(), true);
             for (int j = 0; j < k; ++j) anorm = std::max(anorm, std::sqrt(std::max(G[j + (size_t)k * j], 0.0)));
         }
         auto recurrence = [&]() {
@@ -603,7 +609,7 @@ struct Gkl {
                 std::vector<double> Bt((size_t)k * k);
                 for (int a = 0; a < k; ++a)
                     for (int b = 0; b < k; ++b) Bt[b + (size_t)k * a] = Tat(pc + a, qc + b);   // (T block)ᵀ
-                gemm(K, Q(qc), K, k, Bt.data(), k, k, -1.0, 1.0, W, K);
+                gemm(K, Q(qc), ldQ, k, Bt.data(), k, k, -1.0, 1.0, W, ldQ);
             }
         };
         t0 = now_ms();
@@ -724,7 +730,10 @@ struct Gkl {
         // blocks per restart cycle (measured sweep over k and the cycle length on c1-c4, DESIGN.md §5:
         // the projected SVD grows as n³, fewer cycles cost more products); the projected SVD runs
         // on the device for n up to ~2000
-        int mcyc = 4;
+        // cycle length: the warm-decomposition sweep (scripts/sweep_warm.py) has
+        // c2-sized operators (L·K ~ 2.5e7) fastest at 4 blocks per cycle and c3-sized ones
+        // (L·K ~ 8e8, products and K-side Grams dominate) at 6
+        int mcyc = ((double)L * (double)K >= 1e8) ? 6 : 4;
         if (const char *e = std::getenv("SSA_MCYC")) mcyc = std::max(1, std::atoi(e));
         // prefer cycles whose projected matrix fits the single-CTA shared-memory Jacobi
         if (!std::getenv("SSA_MCYC") && std::getenv("SSA_JACOBI_SMEM")) {
@@ -736,37 +745,60 @@ struct Gkl {
         nQmax = pk + k * (mcyc + 1);
         ldT = nQmax;
         Tm.assign((size_t)ldT * ldT, 0.0);
-        Pb.alloc(sizeof(T) * L * nQmax, st);
-        Qb.alloc(sizeof(T) * K * nQmax, st);
-        Ptmp.alloc(sizeof(T) * L * pk, st);
-        Qtmp.alloc(sizeof(T) * K * pk, st);
+        ldP = (L + 31) / 32 * 32;
+        ldQ = (K + 31) / 32 * 32;
+        Pb.alloc(sizeof(T) * ldP * nQmax, st);
+        Qb.alloc(sizeof(T) * ldQ * nQmax, st);
+        Ptmp.alloc(sizeof(T) * ldP * pk, st);
+        Qtmp.alloc(sizeof(T) * ldQ * pk, st);
+        // zero only the padding rows (L..ldP-1, K..ldQ-1) of every column
+        auto zero_pad = [&](void *base, int64_t rows, int64_t ld, int64_t cols) {
+            if (ld > rows)
+                SSA_CUDA(cudaMemset2DAsync(static_cast<T *>(base) + rows, sizeof(T) * ld, 0, sizeof(T) * (ld - rows),
+                                           (size_t)cols, st));
+        };
+        zero_pad(Pb.p, L, ldP, nQmax);
+        zero_pad(Qb.p, K, ldQ, nQmax);
+        zero_pad(Ptmp.p, L, ldP, pk);
+        zero_pad(Qtmp.p, K, ldQ, pk);
         const double tol = p.tol > 0 ? p.tol : (sizeof(T) == 4 ? 1e-6 : 1e-10);
         const int64_t maxprod = p.max_products > 0 ? p.max_products : std::max<int64_t>(400, 40 * (nQmax / k));
 
         // P_1 = orth(random)
-        fill_normal<T>(L, P(0), L, k, p.seed, 0, st);
+        fill_normal<T>(L, P(0), ldP, k, p.seed, 0, st);
         orth(L, P(0), k, nullptr, 0, false);
         nP = k;
         stepB();
         std::vector<double> th, Y, Z, res;
         int nconv = 0, restarts = 0;
         bool checked_once = false;
+        double t_block = 0.0, t_ritz = 0.0;   // host wall ms of the last block pair / Ritz step
+        static const bool near_ok = std::getenv("SSA_NO_NEAR_CHECK") == nullptr;
         int first_blocks = (3 * r + k - 1) / k;   // first check once ~3r Ritz vectors exist
         if (const char *e = std::getenv("SSA_FIRST_BLOCKS")) first_blocks = std::max(1, std::atoi(e));
         if (first_blocks >= mcyc) checked_once = true;
         double maxres = 0.0;
         for (;;) {
+            const double tb0 = now_ms();
             stepA();
             stepB();
+            t_block = now_ms() - tb0;
             // the first cycle checks convergence early (after first_blocks blocks): well-separated
             // signals converge there without paying for a full cycle (c4)
             const bool cycle_end = !(nQ + k <= nQmax && nblock < maxprod);
             const bool first_check = (restarts == 0 && !checked_once && nQ >= first_blocks * k + k);
-            if (!first_check && !cycle_end) continue;
+            // when a block step costs clearly more than a Ritz step (c4, c5: large operators, few
+            // blocks to convergence), check after every block once the basis holds r vectors;
+            // cheap blocks (c2, c3) wait for the first early check / the cycle end
+            const double tr_est = t_ritz > 0.0 ? t_ritz : 1.0;
+            const bool costly_blocks = near_ok && nQ - k >= r && t_block >= 1.5 * tr_est;
+            if (!first_check && !cycle_end && !costly_blocks) continue;
             checked_once = true;
             // ---- Ritz extraction from T (nP x nc)
             const int nc = nQ - k;
+            const double tr = ms_ritz;
             ritz_svd(nP, nc, th, Y, Z);
+            t_ritz = ms_ritz - tr;
             anorm = std::max(anorm, th[0]);
             res.assign(nc, 0.0);
             for (int i = 0; i < nc; ++i) {
@@ -796,7 +828,7 @@ struct Gkl {
             if (done) {
                 // U = Pb · Y[:, 0:r]
                 p.U.alloc(sizeof(T) * L * r, st);
-                gemm(L, P(0), L, nP, Y.data(), nP, r, 1.0, 0.0, p.U.as<T>(), L);
+                gemm(L, P(0), ldP, nP, Y.data(), nP, r, 1.0, 0.0, p.U.as<T>(), L);
                 p.sigma.assign(th.begin(), th.begin() + r);
                 p.r = r;
                 break;
@@ -805,11 +837,11 @@ struct Gkl {
             // ---- thick restart keeping pk Ritz pairs
             ++restarts;
             const double tr0 = now_ms();
-            gemm(L, P(0), L, nP, Y.data(), nP, pk, 1.0, 0.0, Ptmp.as<T>(), L);
-            gemm(K, Q(0), K, nc, Z.data(), nc, pk, 1.0, 0.0, Qtmp.as<T>(), K);
-            SSA_CUDA(cudaMemcpyAsync(P(0), Ptmp.p, sizeof(T) * L * pk, cudaMemcpyDeviceToDevice, st));
-            SSA_CUDA(cudaMemcpyAsync(Q(pk), Q(nc), sizeof(T) * K * k, cudaMemcpyDeviceToDevice, st));
-            SSA_CUDA(cudaMemcpyAsync(Q(0), Qtmp.p, sizeof(T) * K * pk, cudaMemcpyDeviceToDevice, st));
+            gemm(L, P(0), ldP, nP, Y.data(), nP, pk, 1.0, 0.0, Ptmp.as<T>(), ldP);
+            gemm(K, Q(0), ldQ, nc, Z.data(), nc, pk, 1.0, 0.0, Qtmp.as<T>(), ldQ);
+            SSA_CUDA(cudaMemcpyAsync(P(0), Ptmp.p, sizeof(T) * ldP * pk, cudaMemcpyDeviceToDevice, st));
+            SSA_CUDA(cudaMemcpyAsync(Q(pk), Q(nc), sizeof(T) * ldQ * k, cudaMemcpyDeviceToDevice, st));
+            SSA_CUDA(cudaMemcpyAsync(Q(0), Qtmp.p, sizeof(T) * ldQ * pk, cudaMemcpyDeviceToDevice, st));
             std::fill(Tm.begin(), Tm.end(), 0.0);
             for (int i = 0; i < pk; ++i) Tat(i, i) = th[i];
             nP = pk;

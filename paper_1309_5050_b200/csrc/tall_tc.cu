@@ -1,0 +1,282 @@
+// Tensor-core (tcgen05 kind::tf32, 3xTF32) Gram of tall-skinny fp32 blocks for the
+// block Lanczos solver (CGS / CholeskyQR Grams against the K-side
+// basis, the largest HBM streams of the decomposition after the products):
+//
+//     G (n1 x n2, fp64) = Aᵀ B,   A: M x n1, B: M x n2, column-major, M ≫ n1, n2.
+//
+// The reduction runs over the M rows, which are contiguous in memory, so both UMMA
+// operands are K-major straight from TMA: a 32-row chunk of 128 columns of A is one
+// 128-B swizzled box [128 cols][32 rows] (A_op: M = columns of A, K = rows), a chunk of
+// B likewise [N cols][32 rows] (B_op: N = columns of B).  Each CTA walks a contiguous
+// range of chunks (one CTA per SM); per chunk:
+//
+//   TMA (warp 0) -> converter warps 4-7 split the raw fp32 tiles in place into
+//   hi = rna_tf32(x) and lo = x − hi (same swizzled offsets) -> MMA thread (warp 1):
+//   for each k-step kk (8 rows) and M-tile: D[kk] = A_lo·B_hi; D[kk] += A_hi·B_lo;
+//   D[kk] += A_hi·B_hi (the large term last: one truncating accumulation at full
+//   magnitude per 8-row partial) -> warps 8-15 drain the 4 k-step accumulators of the
+//   chunk (tcgen05.ld), sum them in fp32 and fold them into compensated fp32 sums.
+//
+// TMEM holds two chunks of accumulators (ping-pong), so the tensor core works on chunk
+// c+1 while chunk c drains.  Converters (warps 4-7) and drainers (warps 8-15) are separate
+// warps so the split of chunk c+2, the MMAs of c+1 and the drain of c overlap.  Per-CTA fp64 partials are summed by gram_reduce_kernel in a
+// fixed order (deterministic).  Accuracy: 3xTF32 products (~2^-21 relative per term)
+// and one fp32 truncation per 8-row partial, comparable to the fp32 FFMA Gram.
+#include <map>
+#include <tuple>
+
+#include "common.h"
+#include "kernels.h"
+#include "tc_common.h"
+
+namespace ssa {
+
+namespace tallg {
+constexpr int R = 32;                 // rows per chunk (128 B per column: one swizzled row)
+constexpr int KS = R / 8;             // UMMA k-steps per chunk
+constexpr int NTHR = 512;            // warps 0 TMA, 1 MMA, 4-7 convert, 8-15 drain
+
+template <int NM, int NN>
+struct Cfg {
+    static constexpr int a_bytes = NM * 128 * 128;          // raw/hi A tiles (NM x 16 KB)
+    static constexpr int b_bytes = NN * 128;
+    static constexpr int stage = 2 * a_bytes + 2 * b_bytes; // hi + lo of A and B
+    static constexpr int STAGES = (220 * 1024) / stage > 4 ? 4 : (220 * 1024) / stage;
+    static constexpr int off_bar = STAGES * stage;
+    static constexpr int smem = off_bar + 256 + 1024;       // barriers + alignment slack
+    static constexpr int acc_cols = NM * KS * NN;           // one chunk's accumulators
+    static constexpr int tmem_cols = 2 * acc_cols;          // ping-pong
+};
+}  // namespace tallg
+
+template <int NM, int NN>
+__global__ void __launch_bounds__(tallg::NTHR, 1)
+gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
+               int n1, int n2, double *__restrict__ partials) {
+    using namespace tc;
+    using C = tallg::Cfg<NM, NN>;
+    constexpr int S = C::STAGES, KS = tallg::KS;
+    static_assert(C::tmem_cols == 256 || C::tmem_cols == 512, "TMEM allocation must be 256 or 512 columns");
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::off_bar);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 24);
+    const uint32_t bar0 = smem_u32(bars);
+    auto full = [&](int s) { return bar0 + 8u * s; };             // TMA landed
+    auto conv = [&](int s) { return bar0 + 8u * (4 + s); };       // hi/lo split done (4 warps)
+    auto empty = [&](int s) { return bar0 + 8u * (8 + s); };      // MMAs of the stage done
+    auto accf = [&](int b) { return bar0 + 8u * (12 + b); };      // accumulators ready
+    auto acce = [&](int b) { return bar0 + 8u * (14 + b); };      // accumulators drained (4 warps)
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t nchunks = (M + tallg::R - 1) / tallg::R;
+    const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+    const int64_t c0 = (int64_t)blockIdx.x * per;
+    const int nmy = (int)max((int64_t)0, min(per, nchunks - c0));
+    const int col0 = (int)blockIdx.y * NM * 128;                  // first A column of this CTA
+
+    if (tid == 0) {
+        for (int s = 0; s < 4; ++s) {
+            mbar_init(full(s), 1);
+            mbar_init(conv(s), 4);
+            mbar_init(empty(s), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(accf(b), 1);
+            mbar_init(acce(b), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(C::tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sm_u = smem_u32(smem);
+    auto a_hi = [&](int s) { return sm_u + (uint32_t)(s * C::stage); };
+    auto a_lo = [&](int s) { return a_hi(s) + C::a_bytes; };
+    auto b_hi = [&](int s) { return a_hi(s) + 2 * C::a_bytes; };
+    auto b_lo = [&](int s) { return b_hi(s) + C::b_bytes; };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer ----------------
+            for (int i = 0; i < nmy; ++i) {
+                const int s = i % S;
+                if (i >= S) mbar_wait(empty(s), ((i / S) - 1) & 1);
+                const int r0 = (int)((c0 + i) * tallg::R);
+                mbar_expect_tx(full(s), C::a_bytes + C::b_bytes);
+#pragma unroll
+                for (int mt = 0; mt < NM; ++mt) tma_load_2d_true(a_hi(s) + mt * 16384, &tmA, r0, col0 + 128 * mt, full(s));
+                tma_load_2d_true(b_hi(s), &tmB, r0, 0, full(s));
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer ----------------
+            constexpr uint32_t idesc = make_idesc(128, NN);
+            for (int i = 0; i < nmy; ++i) {
+                const int s = i % S, b = i & 1;
+                mbar_wait(conv(s), (i / S) & 1);
+                if (i >= 2) mbar_wait(acce(b), ((i >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t dbase = tmem + (uint32_t)(b * C::acc_cols);
+#pragma unroll
+                for (int kk = 0; kk < KS; ++kk) {
+                    const uint64_t dBh = make_desc(b_hi(s) + kk * 32), dBl = make_desc(b_lo(s) + kk * 32);
+#pragma unroll
+                    for (int mt = 0; mt < NM; ++mt) {
+                        const uint32_t d = dbase + (uint32_t)((mt * KS + kk) * NN);
+                        const uint64_t dAh = make_desc(a_hi(s) + mt * 16384 + kk * 32);
+                        const uint64_t dAl = make_desc(a_lo(s) + mt * 16384 + kk * 32);
+                        mma_tf32(d, dAl, dBh, idesc, 0u);
+                        mma_tf32(d, dAh, dBl, idesc, 1u);
+                        mma_tf32(d, dAh, dBh, idesc, 1u);
+                    }
+                }
+                mma_commit(empty(s));
+                mma_commit(accf(b));
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ---------------- converters (warps 4-7): raw -> hi in place, lo alongside ----------------
+        const int ct = tid - 128;
+        for (int i = 0; i < nmy; ++i) {
+            const int s = i % S;
+            mbar_wait(full(s), (i / S) & 1);
+            float4 *ah = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage);
+            float4 *al = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + C::a_bytes);
+            float4 *bh = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + 2 * C::a_bytes);
+            float4 *bl = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + 2 * C::a_bytes + C::b_bytes);
+            constexpr int na4 = C::a_bytes / 16, nt4 = (C::a_bytes + C::b_bytes) / 16;
+#pragma unroll 4
+            for (int e = ct; e < nt4; e += 128) {
+                float4 *src = e < na4 ? ah + e : bh + (e - na4);
+                float4 *dlo = e < na4 ? al + e : bl + (e - na4);
+                const float4 x = *src;
+                float4 hh, l;
+                hh.x = __uint_as_float(tf32_rna(x.x)); l.x = x.x - hh.x;
+                hh.y = __uint_as_float(tf32_rna(x.y)); l.y = x.y - hh.y;
+                hh.z = __uint_as_float(tf32_rna(x.z)); l.z = x.z - hh.z;
+                hh.w = __uint_as_float(tf32_rna(x.w)); l.w = x.w - hh.w;
+                *src = hh;
+                *dlo = l;
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv(s)) : "memory");
+        }
+    } else if (warp >= 8) {
+        // ---------------- drain (warps 8-15) ----------------
+        // warp w reads TMEM lanes 32·(w%4).. (A columns) and the 32-column unit h = (w-8)/4 of
+        // the chunk's NM x NN accumulator columns (M-tile h, or columns 32h..).  The 4 k-step
+        // partials are summed in fp32 and folded into a compensated (Kahan) fp32 running sum.
+        constexpr int UNITS = NM * NN / 32;
+        const int h = (warp - 8) >> 2;
+        const int mt_u = (NM == 2) ? h : 0, n0_u = (NM == 2) ? 0 : 32 * h;
+        const bool has_unit = h < UNITS;
+        float ks[32], kc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) { ks[j] = 0.f; kc[j] = 0.f; }
+        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        for (int i = 0; i < nmy; ++i) {
+            const int b = i & 1;
+            mbar_wait(accf(b), (i >> 1) & 1);
+            tc_fence_after();
+            if (has_unit) {
+#pragma unroll
+                for (int hv = 0; hv < 2; ++hv) {
+                    float sum[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) sum[j] = 0.f;
+#pragma unroll
+                    for (int kk = 0; kk < KS; ++kk) {
+                        float v[16];
+                        tmem_ld16(lane_base + (uint32_t)(b * C::acc_cols + (mt_u * KS + kk) * NN + n0_u + 16 * hv), v);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) sum[j] += v[j];
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int q = 16 * hv + j;
+                        const float y = sum[j] - kc[q];
+                        const float t = ks[q] + y;
+                        kc[q] = (t - ks[q]) - y;
+                        ks[q] = t;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
+        }
+        // ---- per-CTA partials in gram_reduce's layout: [64-column block][cta][64 x 64]
+        if (has_unit) {
+            const int nparts = gridDim.x;
+            const int a = col0 + 128 * mt_u + (warp & 3) * 32 + lane;
+            if (a < n1) {
+                double *base = partials + ((int64_t)(a / 64) * nparts + blockIdx.x) * 4096 + (a % 64);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (n0_u + j < n2) base[64 * (n0_u + j)] = (double)ks[j] - (double)kc[j];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::tmem_cols) : "memory");
+}
+
+// tensor maps cached per (pointer, rows, columns, ld, box columns)
+static const CUtensorMap &tall_map(const float *base, int64_t M, int ncols, int64_t ld, int boxc) {
+    using Key = std::tuple<const float *, int64_t, int, int64_t, int>;
+    static thread_local std::map<Key, CUtensorMap> cache;
+    const Key key{base, M, ncols, ld, boxc};
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (cache.size() > 256) cache.clear();
+    return cache[key] = make_map2(base, (uint64_t)M, (uint64_t)ncols, (uint64_t)ld * 4, tallg::R, (uint32_t)boxc, true);
+}
+
+template <int NM, int NN>
+static void launch_gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2,
+                           double *partials, int ctas, cudaStream_t st) {
+    using C = tallg::Cfg<NM, NN>;
+    const CUtensorMap &ma = tall_map(A, M, n1, lda, 128);
+    const CUtensorMap &mb = tall_map(B, M, n2, ldb, NN);
+    auto kern = gram_tc_kernel<NM, NN>;
+    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem));
+    const int gy = (int)cdiv(n1, NM * 128);
+    kern<<<dim3(ctas, gy), tallg::NTHR, C::smem, st>>>(ma, mb, M, n1, n2, partials);
+    after_launch("gram_tc");
+}
+
+// Returns false when the shape / layout is not supported (the caller uses the CUDA-core path).
+bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2, double *G,
+             double *partials, size_t partial_bytes, cudaStream_t st) {
+    static const int mode = [] { const char *e = std::getenv("SSA_GRAM_TC"); return e ? std::atoi(e) : 1; }();
+    if (!mode || M < 8192 || n2 > 64 || n1 > 512 || (lda & 3) || (ldb & 3) || ((uintptr_t)A & 15) ||
+        ((uintptr_t)B & 15) || M > INT32_MAX)
+        return false;
+    const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallg::R));
+    if ((size_t)ctas * 4096 * sizeof(double) * (size_t)cdiv(n1, 64) > partial_bytes) return false;
+    if (n2 <= 32) {
+        if (n1 <= 128) launch_gram_tc<1, 32>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+        else launch_gram_tc<2, 32>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+    } else {
+        launch_gram_tc<1, 64>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+    }
+    gram_reduce(partials, ctas, n1, n2, G, st);
+    return true;
+}
+
+}  // namespace ssa

@@ -4,3 +4,4 @@ python bench.py --steps 5 --warmup 3 > gpurun_out/bench_c2.json 2> gpurun_out/be
 for c in c1 c3 c4; do python bench.py --steps 3 --warmup 3 --config $c --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo "bench $c exit $?"; done
 python bench.py --steps 2 --warmup 3 --config c5 --no-cpu-baseline > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo "bench c5 exit $?"
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref exit $?"
+for c in c1 c2 c3 c4 c5; do python -c "import json;d=json.load(open('gpurun_out/bench_$c.json'));print('$c', round(d['ms_per_step'],2), round(d['value'],1), d['unit'], d['roofline']['frac'], d['config']['path'], d['e2e']['value'])"; done
