@@ -72,6 +72,9 @@ void gram_reduce(const double *partials, int nparts, int n1, int n2, double *G, 
 // tcgen05 3xTF32 Gram (tall_tc.cu); false when the layout is unsupported
 bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2, double *G,
              double *partials, size_t partial_bytes, cudaStream_t st);
+// tcgen05 3xTF32 update Out = beta·Out + alpha·A·C (tall_tc.cu); false when unsupported
+bool update_tc(int64_t M, const float *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
+               double beta, float *Out, int64_t ldo, cudaStream_t st);
 
 // Out (M x n) = beta*Out + alpha * A (M x m) * C (m x n, device double, column-major).
 // In-place (Out == A, with m == n) is allowed.

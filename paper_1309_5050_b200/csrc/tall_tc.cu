@@ -10,7 +10,7 @@
 // B likewise [N cols][32 rows] (B_op: N = columns of B).  Each CTA walks a contiguous
 // range of chunks (one CTA per SM); per chunk:
 //
-//   TMA (warp 0) -> converter warps 4-7 split the raw fp32 tiles in place into
+//   TMA (warp 0) -> converter warps 2-7 split the raw fp32 tiles in place into
 //   hi = rna_tf32(x) and lo = x − hi (same swizzled offsets) -> MMA thread (warp 1):
 //   for each k-step kk (8 rows) and M-tile: D[kk] = A_lo·B_hi; D[kk] += A_hi·B_lo;
 //   D[kk] += A_hi·B_hi (the large term last: one truncating accumulation at full
@@ -18,7 +18,7 @@
 //   chunk (tcgen05.ld), sum them in fp32 and fold them into compensated fp32 sums.
 //
 // TMEM holds two chunks of accumulators (ping-pong), so the tensor core works on chunk
-// c+1 while chunk c drains.  Converters (warps 4-7) and drainers (warps 8-15) are separate
+// c+1 while chunk c drains.  Converters (warps 2-7) and drainers (warps 8-15) are separate
 // warps so the split of chunk c+2, the MMAs of c+1 and the drain of c overlap.  Per-CTA fp64 partials are summed by gram_reduce_kernel in a
 // fixed order (deterministic).  Accuracy: 3xTF32 products (~2^-21 relative per term)
 // and one fp32 truncation per 8-row partial, comparable to the fp32 FFMA Gram.
@@ -34,7 +34,7 @@ namespace ssa {
 namespace tallg {
 constexpr int R = 32;                 // rows per chunk (128 B per column: one swizzled row)
 constexpr int KS = R / 8;             // UMMA k-steps per chunk
-constexpr int NTHR = 512;            // warps 0 TMA, 1 MMA, 4-7 convert, 8-15 drain
+constexpr int NTHR = 512;            // warps 0 TMA, 1 MMA, 2-7 convert, 8-15 drain
 
 template <int NM, int NN>
 struct Cfg {
@@ -79,7 +79,7 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (tid == 0) {
         for (int s = 0; s < 4; ++s) {
             mbar_init(full(s), 1);
-            mbar_init(conv(s), 4);
+            mbar_init(conv(s), 6);
             mbar_init(empty(s), 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -146,9 +146,9 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 mma_commit(accf(b));
             }
         }
-    } else if (warp >= 4 && warp < 8) {
-        // ---------------- converters (warps 4-7): raw -> hi in place, lo alongside ----------------
-        const int ct = tid - 128;
+    } else if (warp >= 2 && warp < 8) {
+        // ---------------- converters (warps 2-7): raw -> hi in place, lo alongside ----------------
+        const int ct = tid - 64;
         for (int i = 0; i < nmy; ++i) {
             const int s = i % S;
             mbar_wait(full(s), (i / S) & 1);
@@ -157,8 +157,8 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             float4 *bh = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + 2 * C::a_bytes);
             float4 *bl = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + 2 * C::a_bytes + C::b_bytes);
             constexpr int na4 = C::a_bytes / 16, nt4 = (C::a_bytes + C::b_bytes) / 16;
-#pragma unroll 4
-            for (int e = ct; e < nt4; e += 128) {
+#pragma unroll 8
+            for (int e = ct; e < nt4; e += 192) {
                 float4 *src = e < na4 ? ah + e : bh + (e - na4);
                 float4 *dlo = e < na4 ? al + e : bl + (e - na4);
                 const float4 x = *src;
@@ -236,6 +236,191 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::tmem_cols) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core update  Out (M x n) = beta·Out + A (M x m)·(alpha·C) (m x n), n <= NN, fp32, Out may equal
+// A (in place: a 128-row tile is written only after all of its chunks were loaded).  The contraction
+// runs over the columns of A, so A is the MN-major operand: one 3-D TMA box {32 rows, 32 columns,
+// 4 row groups} of the column-major A lands as four 32-row groups of 32 swizzled 128-B column rows =
+// the canonical MN-major SW128 layout (LBO 4096 B between row groups, SBO 1024 B between 8-column
+// k-groups).  B_op = (alpha·C)ᵀ chunk, K-major, built in shared memory by the converter warps from
+// the fp64 coefficients (hi / lo tf32).  Per (tile, 32-column chunk): D = A_lo·B_hi + A_hi·B_lo +
+// A_hi·B_hi over 4 k-steps into a fresh TMEM accumulator (≤ 12 truncating accumulations), drained by
+// warps 8-15 into fp32 registers (round to nearest) and written with the tile's last chunk.
+// ---------------------------------------------------------------------------
+namespace tallu {
+constexpr int ROWS = 128, KC = 32, NBUF = 4, NTHR = 512;
+template <int NN>
+struct Cfg {
+    static constexpr int a_bytes = ROWS * KC * 4;            // 16 KB
+    static constexpr int b_bytes = NN * KC * 4;
+    static constexpr int stage = 2 * a_bytes + 2 * b_bytes;
+    static constexpr int STAGES = 4;
+    static constexpr int off_bar = STAGES * stage;
+    static constexpr int smem = off_bar + 256 + 1024;
+    static constexpr int tmem_cols = NBUF * NN <= 256 ? 256 : 512;
+};
+}  // namespace tallu
+
+template <int NN>
+__global__ void __launch_bounds__(tallu::NTHR, 1)
+update_tc_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, const float *__restrict__ Bpk, int n,
+                 double beta, float *Out, int64_t ldo) {
+    using namespace tc;
+    using Cf = tallu::Cfg<NN>;
+    constexpr int S = Cf::STAGES, NBUF = tallu::NBUF, KC = tallu::KC;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + Cf::off_bar);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 28);
+    const uint32_t bar0 = smem_u32(bars);
+    auto full = [&](int s) { return bar0 + 8u * s; };
+    auto conv = [&](int s) { return bar0 + 8u * (4 + s); };
+    auto empty = [&](int s) { return bar0 + 8u * (8 + s); };
+    auto accf = [&](int b) { return bar0 + 8u * (12 + b); };
+    auto acce = [&](int b) { return bar0 + 8u * (16 + b); };
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nchk = (m + KC - 1) / KC;
+    const int64_t ntiles = (M + tallu::ROWS - 1) / tallu::ROWS;
+    const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * per;
+    const int64_t mytiles = max((int64_t)0, min(per, ntiles - t0));
+    const int nitems = (int)(mytiles * nchk);
+
+    if (tid == 0) {
+        for (int s = 0; s < 4; ++s) {
+            mbar_init(full(s), 1);
+            mbar_init(conv(s), 6);
+            mbar_init(empty(s), 1);
+            mbar_init(accf(s), 1);
+            mbar_init(acce(s), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(Cf::tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sm_u = smem_u32(smem);
+    auto a_hi = [&](int s) { return sm_u + (uint32_t)(s * Cf::stage); };
+    auto a_lo = [&](int s) { return a_hi(s) + Cf::a_bytes; };
+    auto b_hi = [&](int s) { return a_hi(s) + 2 * Cf::a_bytes; };
+    auto b_lo = [&](int s) { return b_hi(s) + Cf::b_bytes; };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < nitems; ++i) {
+                const int s = i % S;
+                if (i >= S) mbar_wait(empty(s), ((i / S) - 1) & 1);
+                const int64_t tile = t0 + i / nchk;
+                const int ch = i % nchk;
+                mbar_expect_tx(full(s), Cf::a_bytes + 2 * Cf::b_bytes);
+                tma_load_2d(a_hi(s), &tmA, 0, ch * KC, (int)(tile * (tallu::ROWS / 32)), full(s));
+                bulk_g2s(b_hi(s), Bpk + (size_t)ch * 2 * (Cf::b_bytes / 4), 2 * Cf::b_bytes, full(s));
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc_amn(128, NN);
+            for (int i = 0; i < nitems; ++i) {
+                const int s = i % S, b = i % NBUF;
+                mbar_wait(conv(s), (i / S) & 1);
+                if (i >= NBUF) mbar_wait(acce(b), ((i / NBUF) - 1) & 1);
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(b * NN);
+#pragma unroll
+                for (int q = 0; q < KC / 8; ++q) {
+                    const uint64_t dAh = make_desc_mn(a_hi(s) + q * 1024, 4096, 512, 1);
+                    const uint64_t dAl = make_desc_mn(a_lo(s) + q * 1024, 4096, 512, 1);
+                    const uint64_t dBh = make_desc(b_hi(s) + q * 32), dBl = make_desc(b_lo(s) + q * 32);
+                    mma_tf32(d, dAl, dBh, idesc, q > 0 ? 1u : 0u);
+                    mma_tf32(d, dAh, dBl, idesc, 1u);
+                    mma_tf32(d, dAh, dBh, idesc, 1u);
+                }
+                mma_commit(empty(s));
+                mma_commit(accf(b));
+            }
+        }
+    } else if (warp >= 2 && warp < 8) {
+        // ---------------- converters (warps 2-7): A raw -> hi in place + lo ----------------
+        const int ct = tid - 64;
+        for (int i = 0; i < nitems; ++i) {
+            const int s = i % S;
+            mbar_wait(full(s), (i / S) & 1);
+            float4 *ah = reinterpret_cast<float4 *>(smem + (size_t)s * Cf::stage);
+            float4 *al = reinterpret_cast<float4 *>(smem + (size_t)s * Cf::stage + Cf::a_bytes);
+#pragma unroll 6
+            for (int e = ct; e < Cf::a_bytes / 16; e += 192) {
+                const float4 x = ah[e];
+                float4 hh, l;
+                hh.x = __uint_as_float(tf32_rna(x.x)); l.x = x.x - hh.x;
+                hh.y = __uint_as_float(tf32_rna(x.y)); l.y = x.y - hh.y;
+                hh.z = __uint_as_float(tf32_rna(x.z)); l.z = x.z - hh.z;
+                hh.w = __uint_as_float(tf32_rna(x.w)); l.w = x.w - hh.w;
+                ah[e] = hh;
+                al[e] = l;
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv(s)) : "memory");
+        }
+    } else if (warp >= 8) {
+        // ---------------- drain + epilogue: warp w: rows 32·(w%4).., output columns 32·((w-8)/4).. ----------------
+        const int h = (warp - 8) >> 2;
+        const bool has = 32 * h < NN;
+        float acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(32 * h);
+        const float fb = (float)beta;
+        for (int i = 0; i < nitems; ++i) {
+            const int b = i % NBUF;
+            mbar_wait(accf(b), (i / NBUF) & 1);
+            tc_fence_after();
+            if (has) {
+                float v[32];
+                tmem_ld32(lane_base + (uint32_t)(b * NN), v);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[j] += v[j];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
+            if (i % nchk == nchk - 1) {
+                const int64_t row = (t0 + i / nchk) * tallu::ROWS + (warp & 3) * 32 + lane;
+                if (has && row < M) {
+                    // all old values first (independent loads in flight), then the stores
+                    float old[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = 32 * h + j;
+                        old[j] = (beta != 0.0 && col < n) ? __ldcg(Out + row + ldo * (int64_t)col) : 0.f;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = 32 * h + j;
+                        if (col < n) Out[row + ldo * (int64_t)col] = fmaf(fb, old[j], acc[j]);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cf::tmem_cols) : "memory");
+}
+
 // tensor maps cached per (pointer, rows, columns, ld, box columns)
 static const CUtensorMap &tall_map(const float *base, int64_t M, int ncols, int64_t ld, int boxc) {
     using Key = std::tuple<const float *, int64_t, int, int64_t, int>;
@@ -244,7 +429,9 @@ static const CUtensorMap &tall_map(const float *base, int64_t M, int ncols, int6
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     if (cache.size() > 256) cache.clear();
-    return cache[key] = make_map2(base, (uint64_t)M, (uint64_t)ncols, (uint64_t)ld * 4, tallg::R, (uint32_t)boxc, true);
+    static const bool p256 = [] { const char *e = std::getenv("SSA_L2P"); return !e || std::atoi(e) == 256; }();
+    return cache[key] = make_map2(base, (uint64_t)M, (uint64_t)ncols, (uint64_t)ld * 4, tallg::R, (uint32_t)boxc, true,
+                                  p256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
 }
 
 template <int NM, int NN>
@@ -258,6 +445,65 @@ static void launch_gram_tc(int64_t M, const float *A, int64_t lda, int n1, const
     const int gy = (int)cdiv(n1, NM * 128);
     kern<<<dim3(ctas, gy), tallg::NTHR, C::smem, st>>>(ma, mb, M, n1, n2, partials);
     after_launch("gram_tc");
+}
+
+// B tiles of all 32-column chunks, packed once per update as the exact shared-memory images
+// (K-major, 128-B swizzle): Bpk[chunk][hi | lo][NN rows j][32 columns c] = split(alpha·C[c, j])
+template <int NN>
+__global__ void coef_pack_kernel(int m, const double *__restrict__ C, int ldc, int n, double alpha, float *Bpk) {
+    const int ch = blockIdx.x;
+    float *hi = Bpk + (size_t)ch * 2 * NN * 32, *lo = hi + NN * 32;
+    for (int e = threadIdx.x; e < NN * 32; e += blockDim.x) {
+        const int j = e / 32, cc = e % 32, c = ch * 32 + cc;
+        const float v = (j < n && c < m) ? (float)(alpha * C[c + (int64_t)ldc * j]) : 0.f;
+        const float hv = __uint_as_float(tc::tf32_rna(v));
+        const uint32_t off = (tc::sw128_off(j, cc >> 2) + 4 * (cc & 3)) / 4;
+        hi[off] = hv;
+        lo[off] = v - hv;
+    }
+}
+
+template <int NN>
+static void launch_update_tc(const CUtensorMap &ma, int64_t M, int m, const double *C, int ldc, int n, double alpha,
+                             double beta, float *Out, int64_t ldo, cudaStream_t st) {
+    using Cf = tallu::Cfg<NN>;
+    const int nchk = (m + 31) / 32;
+    static thread_local DevBuf bpk;
+    const size_t need = sizeof(float) * (size_t)nchk * 2 * NN * 32;
+    if (bpk.bytes < need) bpk.alloc(need, st);
+    coef_pack_kernel<NN><<<nchk, 256, 0, st>>>(m, C, ldc, n, alpha, bpk.as<float>());
+    after_launch("coef_pack");
+    auto kern = update_tc_kernel<NN>;
+    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::smem));
+    const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallu::ROWS));
+    kern<<<ctas, tallu::NTHR, Cf::smem, st>>>(ma, M, m, bpk.as<float>(), n, beta, Out, ldo);
+    after_launch("update_tc");
+}
+
+// Out = beta·Out + alpha·A·C on the tensor cores; false when unsupported (caller: CUDA cores).
+// Needs lda a multiple of 32 with lda >= M rounded up to 32 (the solver's padded bases), 16-B
+// aligned A, M < 2^31 · 32.
+bool update_tc(int64_t M, const float *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
+               double beta, float *Out, int64_t ldo, cudaStream_t st) {
+    static const int mode = [] { const char *e = std::getenv("SSA_UPD_TC"); return e ? std::atoi(e) : 1; }();
+    // measured (scripts/bench_tall.py, M = 201,601): 85 µs vs 171 µs (FFMA) at m = 224, 60 vs 81 at m = 96,
+    // but 40 vs 29 at m = 32 — narrow updates stay on the CUDA cores
+    if (!mode || M < 8192 || n > 64 || m > 4096 || (mode == 1 && m < 64) || (lda & 31) || lda < (M + 31) / 32 * 32 ||
+        ((uintptr_t)A & 127))
+        return false;
+    using Key = std::tuple<const float *, int64_t, int, int64_t>;
+    static thread_local std::map<Key, CUtensorMap> cache;
+    const Key key{A, M, m, lda};
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+        if (cache.size() > 256) cache.clear();
+        it = cache.emplace(key, make_map3(A, 32, (uint64_t)m, (uint64_t)((M + 31) / 32), (uint64_t)lda * 4, 128, 32,
+                                          32, 4, false, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B)).first;
+    }
+    if (n <= 32) launch_update_tc<32>(it->second, M, m, C, ldc, n, alpha, beta, Out, ldo, st);
+    else launch_update_tc<64>(it->second, M, m, C, ldc, n, alpha, beta, Out, ldo, st);
+    return true;
 }
 
 // Returns false when the shape / layout is not supported (the caller uses the CUDA-core path).

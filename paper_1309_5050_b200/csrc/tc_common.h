@@ -61,6 +61,24 @@ __host__ __device__ __forceinline__ uint32_t sw128_off(int i, int c) {
     return (uint32_t)((i >> 3) * 1024 + (i & 7) * 128 + ((c ^ (i & 7)) << 4));
 }
 
+// UMMA descriptor, MN-major.  layout 2 = SWIZZLE_128B (canonical ((8,n),(8,k)):((1,LBO),(8,SBO)) in
+// 16-B units: 32 M elements x 8 K rows per 1024-B atom); layout 1 = SWIZZLE_128B_BASE32B, the only
+// MN-major layout for tf32 (Swizzle<2,5,2>: 32-B granules, 4 K rows per 512-B atom).  lbo = byte
+// stride between 32-element M groups, sbo = byte stride between K-row groups.
+__device__ __forceinline__ uint64_t make_desc_mn(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)layout << 61;
+    return d;
+}
+// Instruction descriptor, kind::tf32, A MN-major (bit 15), B K-major.
+__host__ __device__ constexpr uint32_t make_idesc_amn(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 // Instruction descriptor, kind::tf32: D fp32, A/B tf32, both K-major, M x N.
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -216,7 +234,7 @@ static inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 static inline CUtensorMap make_map2(const void *base, uint64_t d0, uint64_t d1, uint64_t s1, uint32_t b0, uint32_t b1,
-                             bool swz128) {
+                             bool swz128, CUtensorMapL2promotion l2p = CU_TENSOR_MAP_L2_PROMOTION_L2_128B) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {d0, d1};
     const cuuint64_t strides[1] = {s1};
@@ -225,13 +243,15 @@ static inline CUtensorMap make_map2(const void *base, uint64_t d0, uint64_t d1, 
     const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box,
                                    es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                    swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                   l2p, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     SSA_REQUIRE(r == CUDA_SUCCESS, SSA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return m;
 }
 
 static inline CUtensorMap make_map3(const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
-                             uint32_t b0, uint32_t b1, uint32_t b2, bool swz128) {
+                             uint32_t b0, uint32_t b1, uint32_t b2, bool swz128,
+                             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CUtensorMapL2promotion l2p = CU_TENSOR_MAP_L2_PROMOTION_L2_128B) {
     CUtensorMap m;
     const cuuint64_t dims[3] = {d0, d1, d2};
     const cuuint64_t strides[2] = {s1, s2};
@@ -239,8 +259,8 @@ static inline CUtensorMap make_map3(const void *base, uint64_t d0, uint64_t d1, 
     const cuuint32_t es[3] = {1, 1, 1};
     const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(base), dims, strides, box,
                                    es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                   swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                   swz != CU_TENSOR_MAP_SWIZZLE_NONE ? swz : (swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE),
+                                   l2p, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     SSA_REQUIRE(r == CUDA_SUCCESS, SSA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     if (std::getenv("SSA_TC_DUMP"))
         std::fprintf(stderr, "[tc] map base=%p dims=%llu,%llu,%llu strides=%llu,%llu box=%u,%u,%u swz=%d\n", base,

@@ -15,4 +15,4 @@ for which in (0, 1):
         byts = 4 * M * (n1 + n2) if which == 0 else 4 * M * (n1 + 2 * n2)
         fl = 2.0 * M * n1 * n2
         print(f"{'gram' if which == 0 else 'upd '} M={M:9d} n1={n1:3d} n2={n2:2d}: {ms.value * 1e3:8.1f} us  "
-              f"{byts / ms.value / 1e6:7.0f} GB/s  {fl / ms.value / 1e9:6.1f} TFLOP/s  check {ck.value:.6e}")
+              f"{byts / ms.value / 1e6:7.0f} GB/s  {fl / ms.value / 1e9:6.1f} TFLOP/s  check {ck.value:.3e}")
