@@ -595,7 +595,10 @@ __global__ void fill_normal_kernel(int64_t M, T *A, int64_t lda, int ncols, uint
         const uint64_t h = mix64(seed ^ mix64(sid * 0x100000001B3ull + (uint64_t)col) ^ (uint64_t)row * 0xD6E8FEB86659FD93ull);
         const double u1 = ((h >> 11) + 1.0) * (1.0 / 9007199254740993.0);
         const double u2 = (double)(mix64(h) >> 11) * (1.0 / 9007199254740992.0);
-        A[row + lda * col] = (T)(sqrt(-2.0 * log(u1)) * cospi(2.0 * u2));
+        if constexpr (sizeof(T) == 4)   // fp32 plans: fp32 transcendentals (the fp64 ones made this HBM write compute-bound)
+            A[row + lda * col] = sqrtf(-2.0f * logf((float)u1)) * cospif(2.0f * (float)u2);
+        else
+            A[row + lda * col] = (T)(sqrt(-2.0 * log(u1)) * cospi(2.0 * u2));
     }
 }
 

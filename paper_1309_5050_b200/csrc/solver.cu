@@ -774,7 +774,9 @@ struct Gkl {
         bool checked_once = false;
         double t_block = 0.0, t_ritz = 0.0;   // host wall ms of the last block pair / Ritz step
         static const bool near_ok = std::getenv("SSA_NO_NEAR_CHECK") == nullptr;
-        int first_blocks = (3 * r + k - 1) / k;   // first check once ~3r Ritz vectors exist
+        // an early check in the first cycle (SSA_FIRST_BLOCKS = blocks before it) is off by default:
+        // with the cost-aware per-block checks below it only cost c2/c3 a Ritz step (measured)
+        int first_blocks = 1 << 20;
         if (const char *e = std::getenv("SSA_FIRST_BLOCKS")) first_blocks = std::max(1, std::atoi(e));
         if (first_blocks >= mcyc) checked_once = true;
         double maxres = 0.0;
