@@ -495,6 +495,132 @@ struct Gkl {
         return Bn;
     }
 
+    // Projection + CholeskyQR2 with two host round trips (the default).  W (M x kc) follows the
+    // na orthonormal columns `against` in the same buffer:
+    //   1. one Gram [A W]ᵀW gives C = AᵀW and WᵀW; the projected Gram is Gp = WᵀW − CᵀC
+    //      (= W'ᵀW' for W' = W − A C); its Cholesky factor R gives the fused update
+    //      W ← [A W]·[−C R⁻¹; R⁻¹] (one streaming pass, tile-level in place);
+    //   2. CholeskyQR on W alone (Gram WᵀW, W ← W R₂⁻¹), repeated once more only if a pass was
+    //      shifted or far from orthonormal.
+    // DGKS (P:… standard CGS safeguard): if projection removed more than half of a column's
+    // norm (Gp_jj < ½ (WᵀW)_jj), or a column is numerically zero, or Cholesky fails, W is left
+    // untouched and the robust `orth` (second projection, shifts, refills, SVQB) takes over.
+    // Returns B with W_in = A·coef + W_out·B (coef accumulated, as in `orth`).
+    std::vector<double> orth3(int64_t M, T *W, int kc, const T *against, int na, bool kside, double *coef) {
+        static const bool legacy = std::getenv("SSA_ORTH_LEGACY") != nullptr;
+        const int64_t ld = LD(M);
+        if (legacy || kc > 64 || na <= 0 || na + kc > 512 || against + (int64_t)na * ld != W)
+            return orth2(M, W, kc, against, na, kside, coef);
+        T *A = const_cast<T *>(against);
+        const int n1 = na + kc;
+        std::vector<double> G((size_t)n1 * kc), Gp((size_t)kc * kc), R, Sinv, Mc((size_t)n1 * kc);
+        std::vector<double> Ctot((size_t)na * kc, 0.0), Btot, Bn((size_t)kc * kc);
+        const double shift_rel = (sizeof(T) == 4) ? 1e-6 : 1e-13;
+        bool project = true, reproject = false;
+        for (int pass = 1; pass <= 4; ++pass) {
+            const int nn = project ? n1 : kc;                       // Gram columns: [A W] or W
+            T *Ab = project ? A : W;
+            gram(M, Ab, ld, nn, W, ld, kc, G.data(), kside);
+            const int off = project ? na : 0;
+            for (int bb = 0; bb < kc; ++bb)
+                for (int aa = 0; aa <= bb; ++aa) {
+                    double v = G[off + aa + (size_t)nn * bb];
+                    if (project)
+                        for (int t = 0; t < na; ++t) v -= G[t + (size_t)nn * aa] * G[t + (size_t)nn * bb];
+                    Gp[aa + (size_t)kc * bb] = v;
+                    Gp[bb + (size_t)kc * aa] = v;
+                }
+            double dmax = 0.0, dev = 0.0;
+            for (int j = 0; j < kc; ++j) dmax = std::max(dmax, Gp[j + (size_t)kc * j]);
+            for (int bb = 0; bb < kc; ++bb)
+                for (int aa = 0; aa < kc; ++aa)
+                    dev = std::max(dev, std::fabs(Gp[aa + (size_t)kc * bb] - (aa == bb ? 1.0 : 0.0)));
+            if (pass == 1) {
+                // breakdown (numerically zero column) -> robust path, W untouched
+                bool zero = !(dmax > 0.0) || !std::isfinite(dmax);
+                for (int j = 0; j < kc && !zero; ++j) {
+                    const double d = Gp[j + (size_t)kc * j], h = G[na + j + (size_t)n1 * j];
+                    zero = !(std::sqrt(std::max(d, 0.0)) > thr_abs * std::max(anorm, 1e-300)) || !(d > 1e-24 * dmax) ||
+                           !(d > (sizeof(T) == 4 ? 1e-12 : 1e-24) * h);
+                    reproject = reproject || !(d > 0.5 * h);   // DGKS: "twice is enough"
+                }
+                if (zero) { ++n_fallback; return orth(M, W, kc, against, na, kside, coef); }
+            }
+            bool shifted = false, ok = cholesky(kc, Gp.data(), 0.0, thr_chol, R);
+            if (!ok) { ok = cholesky(kc, Gp.data(), shift_rel * dmax, 1e-300, R); shifted = ok; }
+            if (!ok) {
+                if (pass == 1) { ++n_fallback; return orth(M, W, kc, against, na, kside, coef); }
+                break;
+            }
+            upper_inverse(kc, R, Sinv);
+            if (project) {
+                // W ← [A W]·[−C R⁻¹; R⁻¹]; coefficients W_in = A·(Ctot + C·Btot) + W_new·(R·Btot)
+                for (int bb = 0; bb < kc; ++bb) {
+                    for (int t = 0; t < na; ++t) {
+                        double v = 0.0;
+                        for (int aa = 0; aa <= bb; ++aa) v -= G[t + (size_t)n1 * aa] * Sinv[aa + (size_t)kc * bb];
+                        Mc[t + (size_t)n1 * bb] = v;
+                    }
+                    for (int aa = 0; aa < kc; ++aa) Mc[na + aa + (size_t)n1 * bb] = Sinv[aa + (size_t)kc * bb];
+                }
+                gemm(M, A, ld, n1, Mc.data(), n1, kc, 1.0, 0.0, W, ld);
+                for (int bb = 0; bb < kc; ++bb)
+                    for (int t = 0; t < na; ++t) {
+                        double v = 0.0;
+                        if (Btot.empty()) v = G[t + (size_t)n1 * bb];
+                        else
+                            for (int aa = 0; aa < kc; ++aa) v += G[t + (size_t)n1 * aa] * Btot[aa + (size_t)kc * bb];
+                        Ctot[t + (size_t)na * bb] += v;
+                    }
+            } else {
+                gemm(M, W, ld, kc, Sinv.data(), kc, kc, 1.0, 0.0, W, ld);   // in place
+            }
+            if (Btot.empty()) Btot = R;
+            else {
+                for (int bb = 0; bb < kc; ++bb)
+                    for (int aa = 0; aa < kc; ++aa) {
+                        double v = 0.0;
+                        for (int t = aa; t < kc; ++t) v += R[aa + (size_t)kc * t] * Btot[t + (size_t)kc * bb];
+                        Bn[aa + (size_t)kc * bb] = v;
+                    }
+                Btot.swap(Bn);
+            }
+            const bool was_projection = project;
+            project = (pass == 1 && reproject);
+            if (pass >= 2 && !project && !shifted && !was_projection && dev <= 0.1) {
+                if (coef)
+                    for (size_t t = 0; t < Ctot.size(); ++t) coef[t] += Ctot[t];
+                ++n_fast;
+                return Btot;
+            }
+            if (pass >= 2 && !project && !shifted && was_projection && dev <= 1e-3) {
+                // the second projection pass already left W orthonormal
+                if (coef)
+                    for (size_t t = 0; t < Ctot.size(); ++t) coef[t] += Ctot[t];
+                ++n_fast;
+                return Btot;
+            }
+        }
+        // not orthonormal after the passes: the robust path finishes from the current W
+        ++n_fallback;
+        std::vector<double> C2((size_t)na * kc, 0.0);
+        std::vector<double> B2 = orth(M, W, kc, against, na, kside, C2.data());
+        if (coef)
+            for (int bb = 0; bb < kc; ++bb)
+                for (int t = 0; t < na; ++t) {
+                    double v = Ctot[t + (size_t)na * bb];
+                    for (int aa = 0; aa < kc; ++aa) v += C2[t + (size_t)na * aa] * Btot[aa + (size_t)kc * bb];
+                    coef[t + (size_t)na * bb] += v;
+                }
+        for (int bb = 0; bb < kc; ++bb)
+            for (int aa = 0; aa < kc; ++aa) {
+                double v = 0.0;
+                for (int t = 0; t < kc; ++t) v += B2[aa + (size_t)kc * t] * Btot[t + (size_t)kc * bb];
+                Bn[aa + (size_t)kc * bb] = v;
+            }
+        return Bn;
+    }
+
     // W (= the last kc of the n1 columns of A) ← A[:, 0:n1] · Mc (n1 x kc, host).  Large M:
     // in place, thread per row; small M: out of place into scratch with column groups across
     // CTAs (enough parallelism), then copied back.
@@ -579,7 +705,7 @@ struct Gkl {
                 product_xv(Q(qc), W, k);
                 std::fill(C.begin(), C.end(), 0.0);
             }
-            B = orth2(L, W, k, P(0), nP, false, C.data());
+            B = orth3(L, W, k, P(0), nP, false, C.data());
         }
         tw_orthA += now_ms() - t0;
         for (int b = 0; b < k; ++b)
@@ -624,7 +750,7 @@ struct Gkl {
                 product_xtu(P(pc), W, k);
                 recurrence();
             }
-            Alast = orth2(K, W, k, againstK, naK, true, nullptr);
+            Alast = orth3(K, W, k, againstK, naK, true, nullptr);
         }
         tw_orthB += now_ms() - t0;
         nQ += k;
