@@ -977,11 +977,13 @@ extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32
                                      double *check) {
     using namespace ssa;
     try {
-        if (M < 1 || n1 < 1 || n1 > 512 || n2 < 1 || n2 > 64 || reps < 1 || which < 0 || which > 2)
+        if (M < 1 || n1 < 1 || n1 > 512 || n2 < 1 || (n2 > 64 && which != 4) || reps < 1 || which < 0 || which > 4)
             throw Error(SSA_ERR_ARG, "ssa_bench_tall: bad sizes");
         const int64_t ld = (M + 31) / 32 * 32;
         DevBuf a, b, g, ws, c;
         a.alloc(sizeof(float) * ld * n1, nullptr);
+        const int probe_code = n2;   // which = 4: box columns + 256 x row groups; B unused
+        if (which == 4) n2 = 1;
         b.alloc(sizeof(float) * ld * n2, nullptr);
         g.alloc(sizeof(double) * 512 * 64, nullptr);
         c.alloc(sizeof(double) * 512 * 64, nullptr);
@@ -997,6 +999,8 @@ extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32
         auto run = [&]() {
             if (which == 2) colread_kernel<<<num_sms() * 2, 512>>>(M, a.as<float>(), ld, n1, 32 * n2, b.as<float>());
             else if (which == 0) gram_tn<float>(M, a.as<float>(), ld, n1, b.as<float>(), ld, n2, g.as<double>(), ws.as<double>(), wsb, nullptr);
+            else if (which == 4) tma_probe(a.as<float>(), M, n1, ld, probe_code & 255, (probe_code >> 8) ? (probe_code >> 8) : 1, nullptr);
+            else if (which == 3) gram_tn<float>(M, a.as<float>(), ld, n1, a.as<float>(), ld, n2, g.as<double>(), ws.as<double>(), wsb, nullptr);
             else gemm_acc<float>(M, a.as<float>(), ld, n1, c.as<double>(), n1, n2, -1.0, 1.0, b.as<float>(), ld, nullptr);
         };
         run();
@@ -1030,7 +1034,7 @@ extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32
             *check = emax / std::max(ref_max, 1e-300);
         } else if (check) {
             double s = 0.0;
-            if (which == 0) {
+            if (which == 0 || which == 3) {
                 std::vector<double> hg((size_t)n1 * n2);
                 SSA_CUDA(cudaMemcpy(hg.data(), g.p, sizeof(double) * hg.size(), cudaMemcpyDeviceToHost));
                 for (double v : hg) s += std::fabs(v);

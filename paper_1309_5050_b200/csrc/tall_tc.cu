@@ -31,43 +31,61 @@
 
 namespace ssa {
 
+// debug timeline of CTA 0 (SSA_GRAM_TRACE): [role][chunk] globaltimer ns
+__device__ unsigned long long *g_gram_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace(int role, int i) {
+    if (g_gram_trace && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) g_gram_trace[role * 64 + i] = gtimer();
+}
+
 namespace tallg {
 constexpr int R = 32;                 // rows per chunk (128 B per column: one swizzled row)
 constexpr int KS = R / 8;             // UMMA k-steps per chunk
 constexpr int NTHR = 512;            // warps 0 TMA, 1 MMA, 2-7 convert, 8-15 drain
 
-template <int NM, int NN>
+template <int NM, int NN, int BA = 128>
 struct Cfg {
-    static constexpr int a_bytes = NM * 128 * 128;          // raw/hi A tiles (NM x 16 KB)
+    static constexpr int a_bytes = NM * BA * 128;           // raw/hi A tiles (NM x BA rows of 128 B)
     static constexpr int b_bytes = NN * 128;
     static constexpr int stage = 2 * a_bytes + 2 * b_bytes; // hi + lo of A and B
-    static constexpr int STAGES = (220 * 1024) / stage > 4 ? 4 : (220 * 1024) / stage;
+    // as many chunks in flight as fit (the pipeline is latency-bound per chunk)
+    static constexpr int STAGES = (220 * 1024) / stage > 8 ? 8 : (220 * 1024) / stage;
     static constexpr int off_bar = STAGES * stage;
-    static constexpr int smem = off_bar + 256 + 1024;       // barriers + alignment slack
+    static constexpr int smem = off_bar + 320 + 1024;       // barriers + alignment slack
     static constexpr int acc_cols = NM * KS * NN;           // one chunk's accumulators
-    static constexpr int tmem_cols = 2 * acc_cols;          // ping-pong
+    static constexpr int ACCB = 512 / acc_cols >= 4 ? 4 : 2; // accumulator buffers (MMA runs ACCB chunks ahead)
+    static constexpr int tmem_cols = ACCB * acc_cols;
 };
 }  // namespace tallg
 
-template <int NM, int NN>
+template <int NM, int NN, int BA>
 __global__ void __launch_bounds__(tallg::NTHR, 1)
 gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
-               int n1, int n2, double *__restrict__ partials) {
+               int n1, int n2, int self_b, double *__restrict__ partials) {
+    constexpr int boxa = BA;
+    // BA: A columns per TMA box (a multiple of 32, <= 128; rows beyond it in the tile are stale and
+    // only feed discarded accumulator rows); self_b: B is the first n2 columns of A (AᵀA): no B load,
+    // the B operand descriptors point into the A tile
     using namespace tc;
-    using C = tallg::Cfg<NM, NN>;
+    using C = tallg::Cfg<NM, NN, BA>;
     constexpr int S = C::STAGES, KS = tallg::KS;
     static_assert(C::tmem_cols == 256 || C::tmem_cols == 512, "TMEM allocation must be 256 or 512 columns");
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::off_bar);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 24);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 32);
     const uint32_t bar0 = smem_u32(bars);
-    auto full = [&](int s) { return bar0 + 8u * s; };             // TMA landed
-    auto conv = [&](int s) { return bar0 + 8u * (4 + s); };       // hi/lo split done (4 warps)
-    auto empty = [&](int s) { return bar0 + 8u * (8 + s); };      // MMAs of the stage done
-    auto accf = [&](int b) { return bar0 + 8u * (12 + b); };      // accumulators ready
-    auto acce = [&](int b) { return bar0 + 8u * (14 + b); };      // accumulators drained (4 warps)
+    auto full = [&](int s) { return bar0 + 8u * s; };             // TMA landed            [8]
+    auto conv = [&](int s) { return bar0 + 8u * (8 + s); };       // hi/lo split done      [8]
+    auto empty = [&](int s) { return bar0 + 8u * (16 + s); };     // MMAs of the stage done [8]
+    auto accf = [&](int b) { return bar0 + 8u * (24 + b); };      // accumulators ready     [4]
+    auto acce = [&](int b) { return bar0 + 8u * (28 + b); };      // accumulators drained   [4]
+    constexpr int AB = C::ACCB;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t nchunks = (M + tallg::R - 1) / tallg::R;
@@ -77,12 +95,12 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int col0 = (int)blockIdx.y * NM * 128;                  // first A column of this CTA
 
     if (tid == 0) {
-        for (int s = 0; s < 4; ++s) {
+        for (int s = 0; s < S; ++s) {
             mbar_init(full(s), 1);
             mbar_init(conv(s), 6);
             mbar_init(empty(s), 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < AB; ++b) {
             mbar_init(accf(b), 1);
             mbar_init(acce(b), 8);
         }
@@ -113,10 +131,11 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 const int s = i % S;
                 if (i >= S) mbar_wait(empty(s), ((i / S) - 1) & 1);
                 const int r0 = (int)((c0 + i) * tallg::R);
-                mbar_expect_tx(full(s), C::a_bytes + C::b_bytes);
+                mbar_expect_tx(full(s), NM * boxa * 128 + (self_b ? 0 : C::b_bytes));
 #pragma unroll
                 for (int mt = 0; mt < NM; ++mt) tma_load_2d_true(a_hi(s) + mt * 16384, &tmA, r0, col0 + 128 * mt, full(s));
-                tma_load_2d_true(b_hi(s), &tmB, r0, 0, full(s));
+                if (!self_b) tma_load_2d_true(b_hi(s), &tmB, r0, 0, full(s));
+                trace(0, i);
             }
         }
     } else if (warp == 1) {
@@ -124,14 +143,15 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             // ---------------- MMA issuer ----------------
             constexpr uint32_t idesc = make_idesc(128, NN);
             for (int i = 0; i < nmy; ++i) {
-                const int s = i % S, b = i & 1;
+                const int s = i % S, b = i % AB;
                 mbar_wait(conv(s), (i / S) & 1);
-                if (i >= 2) mbar_wait(acce(b), ((i >> 1) - 1) & 1);
+                if (i >= AB) mbar_wait(acce(b), ((i / AB) - 1) & 1);
                 tc_fence_after();
                 const uint32_t dbase = tmem + (uint32_t)(b * C::acc_cols);
 #pragma unroll
                 for (int kk = 0; kk < KS; ++kk) {
-                    const uint64_t dBh = make_desc(b_hi(s) + kk * 32), dBl = make_desc(b_lo(s) + kk * 32);
+                    const uint64_t dBh = make_desc((self_b ? a_hi(s) : b_hi(s)) + kk * 32);
+                    const uint64_t dBl = make_desc((self_b ? a_lo(s) : b_lo(s)) + kk * 32);
 #pragma unroll
                     for (int mt = 0; mt < NM; ++mt) {
                         const uint32_t d = dbase + (uint32_t)((mt * KS + kk) * NN);
@@ -144,6 +164,7 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
                 mma_commit(empty(s));
                 mma_commit(accf(b));
+                trace(2, i);
             }
         }
     } else if (warp >= 2 && warp < 8) {
@@ -152,15 +173,13 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int i = 0; i < nmy; ++i) {
             const int s = i % S;
             mbar_wait(full(s), (i / S) & 1);
+            if (warp == 2 && lane == 0) trace(4, i);
             float4 *ah = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage);
             float4 *al = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + C::a_bytes);
             float4 *bh = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + 2 * C::a_bytes);
             float4 *bl = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + 2 * C::a_bytes + C::b_bytes);
-            constexpr int na4 = C::a_bytes / 16, nt4 = (C::a_bytes + C::b_bytes) / 16;
-#pragma unroll 8
-            for (int e = ct; e < nt4; e += 192) {
-                float4 *src = e < na4 ? ah + e : bh + (e - na4);
-                float4 *dlo = e < na4 ? al + e : bl + (e - na4);
+            // loaded bytes only: NM tiles of boxa rows (+ the B tile unless B aliases A)
+            auto split = [](float4 *src, float4 *dlo) {
                 const float4 x = *src;
                 float4 hh, l;
                 hh.x = __uint_as_float(tf32_rna(x.x)); l.x = x.x - hh.x;
@@ -169,10 +188,20 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 hh.w = __uint_as_float(tf32_rna(x.w)); l.w = x.w - hh.w;
                 *src = hh;
                 *dlo = l;
+            };
+            constexpr int rows4 = boxa * 8;                           // float4 per M-tile
+            constexpr int na4 = NM * rows4, nt4 = na4 + C::b_bytes / 16;
+            const int nt = self_b ? na4 : nt4;
+#pragma unroll 8
+            for (int e = ct; e < nt; e += 192) {
+                const int ea = (e / rows4) * 1024 + (e % rows4);       // M-tile stride 16 KB = 1024 float4
+                if (e < na4) split(ah + ea, al + ea);
+                else split(bh + (e - na4), bl + (e - na4));
             }
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv(s)) : "memory");
+            if (warp == 2 && lane == 0) trace(1, i);
         }
     } else if (warp >= 8) {
         // ---------------- drain (warps 8-15) ----------------
@@ -188,21 +217,25 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int j = 0; j < 32; ++j) { ks[j] = 0.f; kc[j] = 0.f; }
         const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         for (int i = 0; i < nmy; ++i) {
-            const int b = i & 1;
-            mbar_wait(accf(b), (i >> 1) & 1);
+            const int b = i % AB;
+            mbar_wait(accf(b), (i / AB) & 1);
             tc_fence_after();
             if (has_unit) {
 #pragma unroll
                 for (int hv = 0; hv < 2; ++hv) {
+                    // the KS k-step partials of 16 columns: all loads in flight, one wait
+                    uint32_t r[KS][16];
+#pragma unroll
+                    for (int kk = 0; kk < KS; ++kk)
+                        tmem_ld16_nowait(lane_base + (uint32_t)(b * C::acc_cols + (mt_u * KS + kk) * NN + n0_u + 16 * hv), r[kk]);
+                    tmem_wait_ld();
                     float sum[16];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) sum[j] = 0.f;
+                    for (int j = 0; j < 16; ++j) {
+                        float t = 0.f;
 #pragma unroll
-                    for (int kk = 0; kk < KS; ++kk) {
-                        float v[16];
-                        tmem_ld16(lane_base + (uint32_t)(b * C::acc_cols + (mt_u * KS + kk) * NN + n0_u + 16 * hv), v);
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) sum[j] += v[j];
+                        for (int kk = 0; kk < KS; ++kk) t += __uint_as_float(r[kk][j]);
+                        sum[j] = t;
                     }
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
@@ -217,6 +250,7 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
+            if (warp == 8 && lane == 0) trace(3, i);
         }
         // ---- per-CTA partials in gram_reduce's layout: [64-column block][cta][64 x 64]
         if (has_unit) {
@@ -421,6 +455,54 @@ update_tc_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, cons
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cf::tmem_cols) : "memory");
 }
 
+// ---- TMA streaming probe (ssa_bench_tall which = 4 / 5): one thread per CTA streams 3-D boxes
+// {32 rows, bc columns, rg row groups} of a column-major M x n block through 8 smem stages, no
+// consumer work — the achievable TMA read rate for the Gram's access pattern.
+__global__ void __launch_bounds__(32, 1) tma_probe_kernel(const __grid_constant__ CUtensorMap tm, int64_t M, int n,
+                                                          int bc, int rg) {
+    using namespace tc;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int box = bc * 128 * rg;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 8 * box);
+    const uint32_t bar0 = smem_u32(bars);
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < 8; ++s) mbar_init(bar0 + 8u * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int64_t nrg = (M + 31) / 32;
+    const int64_t nchunks = (nrg + rg - 1) / rg;
+    const int ncb = (n + bc - 1) / bc;
+    const int64_t items = nchunks * ncb;
+    const int64_t per = (items + gridDim.x - 1) / gridDim.x;
+    const int64_t i0 = blockIdx.x * per, i1 = min(items, i0 + per);
+    for (int64_t i = i0; i < i1; ++i) {
+        const int s = (int)((i - i0) % 8);
+        if (i - i0 >= 8) mbar_wait(bar0 + 8u * s, (uint32_t)((((i - i0) / 8) - 1) & 1));
+        mbar_expect_tx(bar0 + 8u * s, box);
+        const int64_t ch = i / ncb;
+        const int cb = (int)(i % ncb);
+        tma_load_2d(smem_u32(smem) + s * box, &tm, 0, cb * bc, (int)(ch * rg), bar0 + 8u * s);
+    }
+    for (int64_t i = max(i0, i1 - 8); i < i1; ++i) {
+        const int s = (int)((i - i0) % 8);
+        mbar_wait(bar0 + 8u * s, (uint32_t)(((i - i0) / 8) & 1));
+    }
+}
+
+void tma_probe(const float *A, int64_t M, int n, int64_t ld, int bc, int rg, cudaStream_t st) {
+    static std::map<std::tuple<const float *, int64_t, int, int>, CUtensorMap> cache;
+    auto key = std::make_tuple(A, M, bc, rg);
+    auto it = cache.find(key);
+    if (it == cache.end())
+        it = cache.emplace(key, make_map3(A, 32, (uint64_t)n, (uint64_t)((M + 31) / 32), (uint64_t)ld * 4, 128, 32,
+                                          (uint32_t)bc, (uint32_t)rg, true)).first;
+    const int smem = 8 * bc * 128 * rg + 128 + 1024;
+    SSA_CUDA(cudaFuncSetAttribute(tma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    tma_probe_kernel<<<num_sms(), 32, smem, st>>>(it->second, M, n, bc, rg);
+    after_launch("tma_probe");
+}
+
 // tensor maps cached per (pointer, rows, columns, ld, box columns)
 static const CUtensorMap &tall_map(const float *base, int64_t M, int ncols, int64_t ld, int boxc) {
     using Key = std::tuple<const float *, int64_t, int, int64_t, int>;
@@ -434,16 +516,17 @@ static const CUtensorMap &tall_map(const float *base, int64_t M, int ncols, int6
                                   p256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
 }
 
-template <int NM, int NN>
+template <int NM, int NN, int BA>
 static void launch_gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2,
                            double *partials, int ctas, cudaStream_t st) {
-    using C = tallg::Cfg<NM, NN>;
-    const CUtensorMap &ma = tall_map(A, M, n1, lda, 128);
+    using C = tallg::Cfg<NM, NN, BA>;
+    const int self_b = (B == A && ldb == lda && n2 <= n1 && NN <= BA && NM == 1) ? 1 : 0;
+    const CUtensorMap &ma = tall_map(A, M, n1, lda, BA);
     const CUtensorMap &mb = tall_map(B, M, n2, ldb, NN);
-    auto kern = gram_tc_kernel<NM, NN>;
+    auto kern = gram_tc_kernel<NM, NN, BA>;
     SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem));
     const int gy = (int)cdiv(n1, NM * 128);
-    kern<<<dim3(ctas, gy), tallg::NTHR, C::smem, st>>>(ma, mb, M, n1, n2, partials);
+    kern<<<dim3(ctas, gy), tallg::NTHR, C::smem, st>>>(ma, mb, M, n1, n2, self_b, partials);
     after_launch("gram_tc");
 }
 
@@ -515,13 +598,33 @@ bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int
         return false;
     const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallg::R));
     if ((size_t)ctas * 4096 * sizeof(double) * (size_t)cdiv(n1, 64) > partial_bytes) return false;
+    static unsigned long long *trace_buf = nullptr;
+    if (std::getenv("SSA_GRAM_TRACE") && !trace_buf) {
+        SSA_CUDA(cudaMalloc(&trace_buf, 5 * 64 * 8));
+        SSA_CUDA(cudaMemset(trace_buf, 0, 5 * 64 * 8));
+        SSA_CUDA(cudaMemcpyToSymbol(g_gram_trace, &trace_buf, sizeof(trace_buf)));
+    }
+    // narrow blocks (n1 <= 64, e.g. the CholeskyQR Gram WᵀW): a 64-column A box, B read from the A tile
     if (n2 <= 32) {
-        if (n1 <= 128) launch_gram_tc<1, 32>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
-        else launch_gram_tc<2, 32>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+        if (n1 <= 64) launch_gram_tc<1, 32, 64>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+        else if (n1 <= 128) launch_gram_tc<1, 32, 128>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+        else launch_gram_tc<2, 32, 128>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
     } else {
-        launch_gram_tc<1, 64>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+        if (n1 <= 64) launch_gram_tc<1, 64, 64>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+        else launch_gram_tc<1, 64, 128>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
     }
     gram_reduce(partials, ctas, n1, n2, G, st);
+    if (trace_buf) {
+        unsigned long long h[5 * 64];
+        SSA_CUDA(cudaStreamSynchronize(st));
+        SSA_CUDA(cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[gram trace] M=%lld n1=%d n2=%d (us from first TMA): chunk tma wait conv mma drain\n",
+                     (long long)M, n1, n2);
+        for (int i = 0; i < 12; ++i)
+            std::fprintf(stderr, "  %2d %8.2f %8.2f %8.2f %8.2f %8.2f\n", i, (h[i] - h[0]) * 1e-3, (h[4 * 64 + i] - h[0]) * 1e-3,
+                         (h[64 + i] - h[0]) * 1e-3, (h[128 + i] - h[0]) * 1e-3, (h[192 + i] - h[0]) * 1e-3);
+        std::fprintf(stderr, "  last(42): tma %.2f drain %.2f\n", (h[42] - h[0]) * 1e-3, (h[192 + 42] - h[0]) * 1e-3);
+    }
     return true;
 }
 

@@ -6,6 +6,10 @@ from paper_1309_5050_b200 import _lib
 L = _lib.load()
 shapes = [(201601, 32, 32), (201601, 96, 32), (201601, 192, 32), (201601, 224, 32), (24584, 192, 32), (4096, 192, 32),
           (14753281 // 8, 64, 64), (14753281 // 8, 356, 64)]
+for (M, n1, n2) in [(201601, 32, 32), (1844160, 64, 64)]:
+    ms = C.c_double(); ck = C.c_double()
+    assert L.ssa_bench_tall(3, M, n1, n2, 5, C.byref(ms), C.byref(ck)) == 0
+    print(f"self M={M:9d} n1={n1:3d} n2={n2:2d}: {ms.value * 1e3:8.1f} us  {4 * M * n1 / ms.value / 1e6:7.0f} GB/s  check {ck.value:.3e}")
 for which in (0, 1):
     for (M, n1, n2) in shapes:
         ms = C.c_double(); ck = C.c_double()
