@@ -286,6 +286,21 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
     const int fx0 = blockIdx.y * RB;
     const int j = blockIdx.x;
     const int nrow = min(RB, Hx - fx0);
+    // X̂ rows of this CTA: fetched asynchronously into shared memory at the start so their L2
+    // latency overlaps the forward transforms (ncu: the multiply waited on these loads)
+    cplx<T> *xs = reinterpret_cast<cplx<T> *>((reinterpret_cast<uintptr_t>(tws + tw_count(lgtw)) + 15) & ~uintptr_t(15));
+    if (mode == 0) {
+        constexpr int PER = 16 / sizeof(cplx<T>);            // complex values per 16-B copy
+        const uint32_t xs_u = (uint32_t)__cvta_generic_to_shared(xs);
+        for (int q = threadIdx.x; q < (RB * My) / PER; q += blockDim.x) {
+            const int idx = q * PER, rr = idx >> lgy;
+            const int bytes = rr < nrow ? 16 : 0;
+            const cplx<T> *src = Xh + (int64_t)(fx0 + (rr < nrow ? rr : 0)) * My + (idx & (My - 1));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(xs_u + (uint32_t)(16 * q)), "l"(src),
+                         "r"(bytes));
+        }
+        asm volatile("cp.async.commit_group;");
+    }
     #pragma unroll 8
     for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
         const int rr = idx >> lgy, y = idx & (My - 1);
@@ -304,12 +319,10 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
         }
         return;
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
     #pragma unroll 8
-    for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
-        const int rr = idx >> lgy, y = idx & (My - 1);
-        const cplx<T> xh = (rr < nrow) ? Xh[(int64_t)(fx0 + rr) * My + y] : cplx<T>{T(0), T(0)};
-        res[sp(idx)] = cmulconj(xh, res[sp(idx)]);
-    }
+    for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) res[sp(idx)] = cmulconj(xs[idx], res[sp(idx)]);
     __syncthreads();
     cplx<T> *out = fft_batch<T, +1>(res, oth, lgy, RB, tws, lgtw);
     #pragma unroll 8
@@ -481,7 +494,8 @@ static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int 
 template <typename T>
 static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode, cplx<T> *B, int ny_out, cudaStream_t st) {
     const int RB = batch_for(f.lgy, 2048);
-    const size_t smem = smem_ab<T>(f.lgy, RB, f.lgtw);
+    // + the CTA's X̂ rows (prefetched, mode 0)
+    const size_t smem = smem_ab<T>(f.lgy, RB, f.lgtw) + sizeof(cplx<T>) * ((size_t)RB << f.lgy) + 16;
     const int nth = threads_for(f.lgy, RB, cdiv(f.Hx, RB) * k);
     auto kern = nth <= 256 ? fft_pass_b<T, 256> : fft_pass_b<T, 512>;
     SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
