@@ -272,10 +272,10 @@ static bool gram_stream(int64_t M, const float *A, int64_t lda, int n1, const fl
     const size_t smem = std::max(sizeof(float) * (size_t)gram2::STAGES * (64 * YG + NB) * gram2::LDR,
                                  sizeof(double) * (size_t)tiles * 64 * NB);
     if (NB == 32) {
-        SSA_CUDA(cudaFuncSetAttribute(gram_stream_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set_max_smem(gram_stream_kernel<32>);
         gram_stream_kernel<32><<<dim3(ctas, gy), 256, smem, st>>>(M, A, lda, n1, B, ldb, n2, YG, contig, partials);
     } else {
-        SSA_CUDA(cudaFuncSetAttribute(gram_stream_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set_max_smem(gram_stream_kernel<64>);
         gram_stream_kernel<64><<<dim3(ctas, gy), 256, smem, st>>>(M, A, lda, n1, B, ldb, n2, YG, contig, partials);
     }
     after_launch("gram_stream");
@@ -479,10 +479,10 @@ static bool tall_update(int64_t M, const float *A, int64_t lda, int m, const dou
     if (smem > 220 * 1024) return false;
     const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, upd2::ROWS));
     if (NC == 32) {
-        SSA_CUDA(cudaFuncSetAttribute(tall_update_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set_max_smem(tall_update_kernel<32>);
         tall_update_kernel<32><<<ctas, upd2::NT, smem, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
     } else {
-        SSA_CUDA(cudaFuncSetAttribute(tall_update_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set_max_smem(tall_update_kernel<64>);
         tall_update_kernel<64><<<ctas, upd2::NT, smem, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
     }
     after_launch("tall_update");
@@ -565,11 +565,11 @@ void gemm_acc(int64_t M, const T *A, int64_t lda, int m, const double *C, int ld
     const unsigned grid = (unsigned)cdiv(M, 128);
     if (n <= 32) {
         const size_t smem = sizeof(T) * (size_t)m * 32;
-        SSA_CUDA(cudaFuncSetAttribute(gemm_acc_kernel<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set_max_smem(gemm_acc_kernel<T, 32>);
         gemm_acc_kernel<T, 32><<<grid, 128, smem, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
     } else {
         const size_t smem = sizeof(T) * (size_t)m * 64;
-        SSA_CUDA(cudaFuncSetAttribute(gemm_acc_kernel<T, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set_max_smem(gemm_acc_kernel<T, 64>);
         gemm_acc_kernel<T, 64><<<grid, 128, smem, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
     }
     after_launch("gemm_acc");
@@ -879,7 +879,7 @@ void orth_solve(const double *G, int na, int kc, int pass, double zthr2, double 
     const size_t cbytes = sizeof(double) * (size_t)(na | 1) * kc;
     const int c_in_smem = (base + cbytes <= 200 * 1024) ? 1 : 0;
     const size_t smem = base + (c_in_smem ? cbytes : 0);
-    SSA_CUDA(cudaFuncSetAttribute(orth_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(orth_solve_kernel);
     orth_solve_kernel<<<1, 256, smem, st>>>(G, na, kc, pass, zthr2, shift_rel, thr_chol, c_in_smem, Mout, Ctot, Btot,
                                             flags);
     after_launch("orth_solve");
@@ -892,11 +892,11 @@ void apply_inplace(int64_t M, T *A, int64_t lda, int n1, int kc, const double *M
     const unsigned grid = (unsigned)cdiv(M, 128);
     if (kc <= 32) {
         const size_t smem = sizeof(T) * (size_t)n1 * 32;
-        SSA_CUDA(cudaFuncSetAttribute(apply_inplace_kernel<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set_max_smem(apply_inplace_kernel<T, 32>);
         apply_inplace_kernel<T, 32><<<grid, 128, smem, st>>>(M, A, lda, n1, kc, Mc, skip);
     } else {
         const size_t smem = sizeof(T) * (size_t)n1 * 64;
-        SSA_CUDA(cudaFuncSetAttribute(apply_inplace_kernel<T, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set_max_smem(apply_inplace_kernel<T, 64>);
         apply_inplace_kernel<T, 64><<<grid, 128, smem, st>>>(M, A, lda, n1, kc, Mc, skip);
     }
     after_launch("apply_inplace");
@@ -944,7 +944,7 @@ void gemm_cols(int64_t M, const T *A, int64_t lda, int m, const double *C, int l
     if (M <= 0 || n <= 0) return;
     const size_t smem = sizeof(T) * (size_t)m * 8;
     SSA_REQUIRE(smem <= 200 * 1024, SSA_ERR_ARG, "gemm_cols: too many input columns");
-    SSA_CUDA(cudaFuncSetAttribute(gemm_cols_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(gemm_cols_kernel<T>);
     gemm_cols_kernel<T><<<dim3((unsigned)cdiv(M, 128), (unsigned)cdiv(n, 8)), 128, smem, st>>>(M, A, lda, m, C, ldc, n,
                                                                                             Out, ldo);
     after_launch("gemm_cols");

@@ -72,6 +72,11 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 
 int num_sms();
+// Raise a kernel's dynamic shared-memory cap to the sm_100 maximum once per function (the
+// attribute call costs host time on every launch otherwise; the launch's own size still decides
+// the carve-out).
+void set_max_smem_impl(const void *fn);
+template <typename F> inline void set_max_smem(F *fn) { set_max_smem_impl(reinterpret_cast<const void *>(fn)); }
 // set the thread-local message returned by ssa_last_error()
 void ssa_set_error(const std::string &msg);
 

@@ -174,7 +174,7 @@ static void launch_corr(CorrParams<T> P, cudaStream_t st) {
     const int YT = TY + CDY - 1;
     const size_t smem = sizeof(T) * ((size_t)CDX * CDY * KV + (size_t)P.xpitch * YT);
     auto kern = corr_direct_kernel<T, CDX, CDY>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(kern);
     const int ntx = (int)cdiv(P.ox, TX), nty = (int)cdiv(P.oy, TY);
     dim3 grid(ntx * nty, (unsigned)cdiv(P.k, KV), P.nsplit);
     kern<<<grid, kThreads, smem, st>>>(P);
@@ -378,7 +378,7 @@ void diagsums_direct(AvgParams<T> P, cudaStream_t st) {
     const int BYT = TY + CLY - 1;
     const size_t smem = sizeof(T) * ((size_t)CLX * CLY + (size_t)P.bpitch * BYT);
     auto kern = diagsums_kernel<T, CLX, CLY>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(kern);
     dim3 grid((unsigned)(cdiv(P.nx, TX) * cdiv(P.ny, TY)), P.ngroups);
     kern<<<grid, 256, smem, st>>>(P);
     after_launch("diagsums_direct");

@@ -485,7 +485,7 @@ static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int 
     const size_t smem = smem_ab<T>(f.lgx, CB / 2, f.lgtw);
     const int nth = threads_for(f.lgx, CB / 2, cdiv(by, CB) * k);
     auto kern = nth <= 256 ? fft_pass_a<T, 256> : fft_pass_a<T, 512>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(kern);
     kern<<<dim3((unsigned)cdiv(by, CB), k), nth, smem, st>>>(in, ld, map, bx, by, k, jsel, scale, f.lgx, CB, A,
                                                                         f.tw.as<cplx<T>>(), f.lgtw);
     after_launch("fft_pass_a");
@@ -498,7 +498,7 @@ static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode,
     const size_t smem = smem_ab<T>(f.lgy, RB, f.lgtw) + sizeof(cplx<T>) * ((size_t)RB << f.lgy) + 16;
     const int nth = threads_for(f.lgy, RB, cdiv(f.Hx, RB) * k);
     auto kern = nth <= 256 ? fft_pass_b<T, 256> : fft_pass_b<T, 512>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(kern);
     kern<<<dim3(k, (unsigned)cdiv(f.Hx, RB)), nth, smem, st>>>(A, ny_in, f.Hx, f.lgy, RB,
                                                                          f.Xh.as<cplx<T>>(), mode, B, ny_out,
                                                                          f.tw.as<cplx<T>>(), f.lgtw);
@@ -512,7 +512,7 @@ static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *o
     const size_t smem = smem_ab<T>(f.lgx, CB / 2, f.lgtw);
     const int nth = threads_for(f.lgx, CB / 2, cdiv(oy, CB) * k);
     auto kern = nth <= 256 ? fft_pass_c<T, 256> : fft_pass_c<T, 512>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(kern);
     const T inv = (T)(1.0 / ((double)f.Mx * (double)f.My));
     kern<<<dim3((unsigned)cdiv(oy, CB), k), nth, smem, st>>>(B, oy, f.Hx, f.lgx, CB, ox, inv, out, ldo, omap,
                                                                        w, stride, f.tw.as<cplx<T>>(), f.lgtw);
@@ -603,7 +603,7 @@ void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, co
     const size_t smem = sizeof(cplx<T>) * (5 * sp_size((size_t)RB << f.lgy) + tw_count(f.lgtw));
     const int nth = threads_for(f.lgy, RB, cdiv(f.Hx, RB) * ng);
     auto kern = nth <= 256 ? fft_pass_b_conv<T, 256> : fft_pass_b_conv<T, 512>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(kern);
     kern<<<dim3((unsigned)cdiv(f.Hx, RB), ng), nth, smem, p.st>>>(
         AU.as<cplx<T>>(), p.ly, AV.as<cplx<T>>(), p.ky, grp_off_dev, grp_idx_dev, slot_dev, f.Hx, f.lgy, RB,
         B.as<cplx<T>>(), p.ny, f.tw.as<cplx<T>>(), f.lgtw);

@@ -491,8 +491,7 @@ static void tc_run(const TcCorrParams &P, int j0, cudaStream_t st) {
     a.ws = P.ws;
     static thread_local bool attr_set = false;
     if (!attr_set) {
-        SSA_CUDA(cudaFuncSetAttribute(hankel_tc_kernel<S, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)C::smem));
+        set_max_smem(hankel_tc_kernel<S, NB>);
         attr_set = true;
     }
     {

@@ -510,7 +510,7 @@ static bool launch_gram(int m, int n, double *T, int *sweeps, cudaStream_t st, f
     const size_t smem = Cfg::smem(m);
     if (smem > 220 * 1024) return false;
     auto kern = jacobi_gram_kernel<NC>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(kern);
     if (ncta > 8) SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ncta);
@@ -537,7 +537,7 @@ static bool launch_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st
     const size_t smem = sizeof(double) * (size_t)(m | 1) * BW * 4;
     if (smem > 200 * 1024) return false;
     auto kern = jacobi_cluster_kernel<MR, BW>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(kern);
     if (ncta > 8) SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ncta);
@@ -657,7 +657,7 @@ static bool jacobi_try_smem(int m, int n, double *T, int *sweeps, cudaStream_t s
     const size_t smem = jacobi_smem_bytes(m, n);
     void *kern = m <= 32 * 4 ? (void *)jacobi_smem_kernel<4> : m <= 32 * 6 ? (void *)jacobi_smem_kernel<6>
                                                                             : (void *)jacobi_smem_kernel<8>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(kern);
     double tol = 1e-12;
     int max_sweeps = 60;
     void *args[] = {&m, &n, &T, &tol, &max_sweeps, &sweeps};
@@ -685,7 +685,7 @@ void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cud
     void *kern = m <= 32 * 4 ? (void *)jacobi_block_kernel<4>
                : m <= 32 * 8 ? (void *)jacobi_block_kernel<8>
                : m <= 32 * 16 ? (void *)jacobi_block_kernel<16> : (void *)jacobi_block_kernel<24>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_smem(kern);
     SSA_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(32 * kBW), args, smem, st));
     after_launch("jacobi_block");
 }

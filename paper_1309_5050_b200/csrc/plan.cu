@@ -1,9 +1,30 @@
 // Plan-time kernels: shape ingestion, 𝔎 selection,
 // compaction maps, rectangular weights, and small elementwise epilogues.
+#include <mutex>
+#include <set>
+
 #include "common.h"
 #include "kernels.h"
 
 namespace ssa {
+
+void set_max_smem_impl(const void *fn) {
+    static std::mutex mu;
+    static std::set<const void *> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(fn)) return;
+    // opt-in per-block maximum minus the kernel's static shared memory
+    static int optin = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        return v;
+    }();
+    cudaFuncAttributes fa{};
+    SSA_CUDA(cudaFuncGetAttributes(&fa, fn));
+    SSA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+    done.insert(fn);
+}
 
 // a1: 𝔑 = {finite cells} ∩ mask; cells outside 𝔑 are set to 0
 // (they never enter 𝒯(𝕏) because every κ ∈ 𝔎 keeps its window inside 𝔑).

@@ -33,6 +33,22 @@
 
 namespace ssa {
 
+// Host wait for everything queued on `st`: an event polled in a tight loop (the solver waits
+// ~60 times per decomposition for small Gram results; a blocking stream synchronisation adds
+// the OS wake-up latency to every one of these round trips).  SSA_BLOCKING_SYNC=1 restores
+// cudaStreamSynchronize.
+static void stream_wait(cudaStream_t st) {
+    static const bool blocking = std::getenv("SSA_BLOCKING_SYNC") != nullptr;
+    if (blocking) { SSA_CUDA(cudaStreamSynchronize(st)); return; }
+    static thread_local cudaEvent_t ev = nullptr;
+    if (!ev) SSA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SSA_CUDA(cudaEventRecord(ev, st));
+    cudaError_t e;
+    while ((e = cudaEventQuery(ev)) == cudaErrorNotReady) {
+    }
+    SSA_CUDA(e);
+}
+
 // Pinned host staging + matching device ring for the small matrices exchanged
 // with the host (Gram results, projection coefficients).  Regions are never
 // reused before a stream synchronisation, so uploads need no sync of their own.
@@ -60,7 +76,7 @@ struct Staging {
     size_t take(size_t n) {
         n = (n + 31) & ~size_t(31);
         if (off + n > cap) {
-            SSA_CUDA(cudaStreamSynchronize(st));
+            stream_wait(st);
             off = 0;
         }
         SSA_REQUIRE(n <= cap, SSA_ERR_ARG, "staging buffer too small");
@@ -70,7 +86,7 @@ struct Staging {
     }
     double *dev(size_t i) { return d.as<double>() + i; }
     void sync() {
-        SSA_CUDA(cudaStreamSynchronize(st));
+        stream_wait(st);
         off = 0;
     }
 };
@@ -145,7 +161,7 @@ struct Gkl {
                 ch.push_back({a0, na, b0, nb, idx});
             }
         }
-        SSA_CUDA(cudaStreamSynchronize(st));
+        stream_wait(st);
         for (const Chunk &c : ch)
             for (int b = 0; b < c.nb; ++b)
                 for (int a = 0; a < c.na; ++a)

@@ -498,7 +498,7 @@ void tma_probe(const float *A, int64_t M, int n, int64_t ld, int bc, int rg, cud
         it = cache.emplace(key, make_map3(A, 32, (uint64_t)n, (uint64_t)((M + 31) / 32), (uint64_t)ld * 4, 128, 32,
                                           (uint32_t)bc, (uint32_t)rg, true)).first;
     const int smem = 8 * bc * 128 * rg + 128 + 1024;
-    SSA_CUDA(cudaFuncSetAttribute(tma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    set_max_smem(tma_probe_kernel);
     tma_probe_kernel<<<num_sms(), 32, smem, st>>>(it->second, M, n, bc, rg);
     after_launch("tma_probe");
 }
@@ -524,7 +524,7 @@ static void launch_gram_tc(int64_t M, const float *A, int64_t lda, int n1, const
     const CUtensorMap &ma = tall_map(A, M, n1, lda, BA);
     const CUtensorMap &mb = tall_map(B, M, n2, ldb, NN);
     auto kern = gram_tc_kernel<NM, NN, BA>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem));
+    set_max_smem(kern);
     const int gy = (int)cdiv(n1, NM * 128);
     kern<<<dim3(ctas, gy), tallg::NTHR, C::smem, st>>>(ma, mb, M, n1, n2, self_b, partials);
     after_launch("gram_tc");
@@ -557,7 +557,7 @@ static void launch_update_tc(const CUtensorMap &ma, int64_t M, int m, const doub
     coef_pack_kernel<NN><<<nchk, 256, 0, st>>>(m, C, ldc, n, alpha, bpk.as<float>());
     after_launch("coef_pack");
     auto kern = update_tc_kernel<NN>;
-    SSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::smem));
+    set_max_smem(kern);
     const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallu::ROWS));
     kern<<<ctas, tallu::NTHR, Cf::smem, st>>>(ma, M, m, bpk.as<float>(), n, beta, Out, ldo);
     after_launch("update_tc");
