@@ -36,6 +36,19 @@ FFMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 TF: 148 SM x 128 FP32
 FP64_PEAK_TFLOPS = FFMA_PEAK_TFLOPS / 2               # B200 non-tensor FP64 = 1/2 FP32 rate
 
 
+def _traffic(config, product, path, k):
+    """DRAM bytes per block product from the committed ncu capture (profiles/r01/traffic.json), or None."""
+    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic.json")
+    try:
+        with open(f) as fh:
+            for e in json.load(fh)["entries"]:
+                if (e["config"], e["product"], e["path"], e["k"]) == (config, product, path, k):
+                    return e["traffic_bytes"]
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -193,7 +206,7 @@ def run_ours(args, rank, world, dist):
     nx_, ny_ = np.asarray(w.data).shape
     kx_, ky_ = nx_ - w.window[0] + 1, ny_ - w.window[1] + 1
 
-    def product_roofline(name, path, ms_total, nblocks, nvec):
+    def product_roofline(name, path, ms_total, nblocks, nvec, name_key=""):
         if nblocks <= 0:
             return None
         avg_ms = ms_total / nblocks
@@ -230,8 +243,12 @@ def run_ours(args, rank, world, dist):
                  "peak_source": "derived: 148 SM x 128 FP32 FMA/clk x 2 x 1.965 GHz (B200_PROFILING.md SM count,"
                                 " MEASURED_PEAKS sm_max_mhz); fp64 = 1/2",
                  "algorithmic_flops_per_launch": flops}
-        r.update({"traffic": None, "avg_launch_ms": avg_ms, "launches_per_step": nblocks / args.steps,
+        tr = _traffic(args.config, name_key, path, int(round(kk)))
+        r.update({"traffic": tr, "avg_launch_ms": avg_ms, "launches_per_step": nblocks / args.steps,
                   "share_of_step": ms_total / max(ms_local, 1e-9), "path": path})
+        if tr is not None:
+            r["traffic_source"] = ("profiles/r01/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of "
+                                   "the block product's kernels, one ncu capture (cold caches)")
         return r
 
     prods = {}
@@ -239,7 +256,7 @@ def run_ours(args, rank, world, dist):
         ms_t = float(np.sum([i[f"ms_products_{key}"] for i in infos]))
         nb_t = float(np.sum([i[f"n_products_{key}"] for i in infos]))
         nv_t = float(np.sum([i[f"n_vectors_{key}"] for i in infos]))
-        rr = product_roofline(name, path, ms_t, nb_t, nv_t)
+        rr = product_roofline(name, path, ms_t, nb_t, nv_t, key)
         if rr:
             prods[key] = rr
     roof = dict(max(prods.values(), key=lambda r: r["share_of_step"])) if prods else {}
