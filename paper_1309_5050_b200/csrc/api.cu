@@ -328,6 +328,33 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
         SSA_CUDA(cudaMemsetAsync(p.kmask.p, 1, nk, st));
         p.full_k = true;
         p.K = nk;
+    } else if (p.full_window && !std::getenv("SSA_PLAN_CORR")) {
+        // rectangular window: 𝔎 by separable box sums of 1_𝔑 (exact int32; same set as the
+        // correlation below, without an L·K-flop kernel)
+        DevBuf tmp;
+        tmp.alloc(sizeof(int32_t) * (size_t)p.kx * p.ny, st);
+        box_kmask(p.nmask.as<uint8_t>(), p.nx, p.ny, p.lx, p.ly, p.kmask.as<uint8_t>(), tmp.as<int32_t>(), st);
+        if (p.has_comm) {
+            clear_band_kernel<<<(unsigned)std::min<int64_t>(cdiv(nk, 256), 16 * num_sms()), 256, 0, st>>>(
+                p.kmask.as<uint8_t>(), p.kx, p.ky, p.band_y0, p.band_y1);
+            after_launch("clear_band");
+        }
+        DevBuf cc;
+        cc.alloc(sizeof(int32_t) * (p.ky + 1), st);
+        column_counts(p.kmask.as<uint8_t>(), p.kx, p.ky, cc.as<int32_t>(), st);
+        std::vector<int32_t> h(p.ky + 1, 0);
+        SSA_CUDA(cudaMemcpyAsync(h.data(), cc.p, sizeof(int32_t) * p.ky, cudaMemcpyDeviceToHost, st));
+        SSA_CUDA(cudaStreamSynchronize(st));
+        int64_t tot = 0;
+        for (int j = 0; j < p.ky; ++j) { const int32_t c0 = h[j]; h[j] = (int32_t)tot; tot += c0; }
+        p.K = tot;
+        p.full_k = (tot == nk);
+        if (!p.full_k) {
+            SSA_CUDA(cudaMemcpyAsync(cc.p, h.data(), sizeof(int32_t) * p.ky, cudaMemcpyHostToDevice, st));
+            p.kmap.alloc(sizeof(int32_t) * nk, st);
+            compact_map(p.kmask.as<uint8_t>(), p.kx, p.ky, cc.as<int32_t>(), p.kmap.as<int32_t>(), nullptr, p.nx, st);
+        }
+        SSA_CUDA(cudaStreamSynchronize(st));
     } else {
         DevBuf ind, ones, cnt, ws;
         ind.alloc(sizeof(T) * nxy, st);
@@ -378,6 +405,17 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
         weights_rect(p.nx, p.ny, p.lx, p.ly, p.weights.as<int32_t>(), st);
         p.n_excluded = p.n_valid - nxy;   // all cells valid in this case -> 0
         if (p.n_excluded < 0) p.n_excluded = 0;
+    } else if (p.full_window && !std::getenv("SSA_PLAN_CORR")) {
+        // 𝕎 = box sum of 1_𝔎 over the window (exact int32)
+        DevBuf tmp;
+        tmp.alloc(sizeof(int32_t) * (size_t)p.nx * p.ky, st);
+        box_weights(p.kmask.as<uint8_t>(), p.nx, p.ny, p.lx, p.ly, p.weights.as<int32_t>(), tmp.as<int32_t>(), st);
+        std::vector<int32_t> wh(nxy);
+        SSA_CUDA(cudaMemcpyAsync(wh.data(), p.weights.p, sizeof(int32_t) * nxy, cudaMemcpyDeviceToHost, st));
+        SSA_CUDA(cudaStreamSynchronize(st));
+        int64_t np = 0;
+        for (int64_t t = 0; t < nxy; ++t) np += wh[t] > 0;
+        p.n_excluded = p.has_comm ? 0 : p.n_valid - np;
     } else {
         DevBuf num, go, gi;
         num.alloc(sizeof(T) * nxy, st);

@@ -72,6 +72,8 @@ void gram_reduce(const double *partials, int nparts, int n1, int n2, double *G, 
 // tcgen05 3xTF32 Gram (tall_tc.cu); false when the layout is unsupported
 bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2, double *G,
              double *partials, size_t partial_bytes, cudaStream_t st);
+void box_kmask(const uint8_t *nmask, int nx, int ny, int lx, int ly, uint8_t *kmask, int32_t *tmp, cudaStream_t st);
+void box_weights(const uint8_t *kmask, int nx, int ny, int lx, int ly, int32_t *w, int32_t *tmp, cudaStream_t st);
 void tma_probe(const float *A, int64_t M, int n, int64_t ld, int bc, int rg, cudaStream_t st);
 // tcgen05 3xTF32 update Out = beta·Out + alpha·A·C (tall_tc.cu); false when unsupported
 bool update_tc(int64_t M, const float *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,

@@ -137,6 +137,75 @@ void weights_rect(int nx, int ny, int lx, int ly, int32_t *w, cudaStream_t st) {
     after_launch("weights_rect");
 }
 
+// Separable box sums for full rectangular windows (a2/a3 without a correlation kernel):
+// 𝔎 = {κ : Σ_{d ∈ 𝔏} 1_𝔑(κ + d) = |𝔏|} (Alg. 6) and 𝕎(p) = #{κ ∈ 𝔎 : p − κ ∈ 𝔏}
+// (Alg. 4 step 1) are 2-D box filters of 0/1 images; each pass is a sliding-window sum along one
+// axis (one thread per line, exact int32).
+// forward window: out[i, j] = Σ_{d < w} in[i + d, j] for i < no   (lines along the fast axis)
+__global__ void box_fwd_x_kernel(const uint8_t *__restrict__ in, int nin, int ny, int w, int no, int32_t *__restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= ny) return;
+    const uint8_t *r = in + (int64_t)nin * j;
+    int32_t s = 0;
+    for (int d = 0; d < w - 1 && d < nin; ++d) s += r[d];
+    for (int i = 0; i < no; ++i) {
+        s += r[i + w - 1];
+        out[i + (int64_t)no * j] = s;
+        s -= r[i];
+    }
+}
+// forward window along the slow axis, thresholded: mask[i, j] = (Σ_{d < w} in[i, j + d] == full)
+__global__ void box_fwd_y_kernel(const int32_t *__restrict__ in, int nx, int w, int no, int32_t full, uint8_t *__restrict__ mask) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nx) return;
+    int32_t s = 0;
+    for (int d = 0; d < w - 1; ++d) s += in[i + (int64_t)nx * d];
+    for (int j = 0; j < no; ++j) {
+        s += in[i + (int64_t)nx * (j + w - 1)];
+        mask[i + (int64_t)nx * j] = (s == full) ? 1 : 0;
+        s -= in[i + (int64_t)nx * j];
+    }
+}
+// backward window along the fast axis: out[x, j] = Σ_{d < w, 0 <= x - d < nin} in[x - d, j], x < nout
+__global__ void box_bwd_x_kernel(const uint8_t *__restrict__ in, int nin, int ny, int w, int nout, int32_t *__restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= ny) return;
+    const uint8_t *r = in + (int64_t)nin * j;
+    int32_t s = 0;
+    for (int x = 0; x < nout; ++x) {
+        if (x < nin) s += r[x];
+        if (x - w >= 0 && x - w < nin) s -= r[x - w];
+        out[x + (int64_t)nout * j] = s;
+    }
+}
+// backward window along the slow axis: out[x, y] = Σ_{d < w, 0 <= y - d < nin} in[x, y - d], y < nout
+__global__ void box_bwd_y_kernel(const int32_t *__restrict__ in, int nx, int nin, int w, int nout, int32_t *__restrict__ out) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= nx) return;
+    int32_t s = 0;
+    for (int y = 0; y < nout; ++y) {
+        if (y < nin) s += in[x + (int64_t)nx * y];
+        if (y - w >= 0 && y - w < nin) s -= in[x + (int64_t)nx * (y - w)];
+        out[x + (int64_t)nx * y] = s;
+    }
+}
+
+void box_kmask(const uint8_t *nmask, int nx, int ny, int lx, int ly, uint8_t *kmask, int32_t *tmp, cudaStream_t st) {
+    const int kx = nx - lx + 1, ky = ny - ly + 1;
+    box_fwd_x_kernel<<<(unsigned)cdiv(ny, 128), 128, 0, st>>>(nmask, nx, ny, lx, kx, tmp);
+    after_launch("box_fwd_x");
+    box_fwd_y_kernel<<<(unsigned)cdiv(kx, 128), 128, 0, st>>>(tmp, kx, ly, ky, lx * ly, kmask);
+    after_launch("box_fwd_y");
+}
+
+void box_weights(const uint8_t *kmask, int nx, int ny, int lx, int ly, int32_t *w, int32_t *tmp, cudaStream_t st) {
+    const int kx = nx - lx + 1, ky = ny - ly + 1;
+    box_bwd_x_kernel<<<(unsigned)cdiv(ky, 128), 128, 0, st>>>(kmask, kx, ky, lx, nx, tmp);
+    after_launch("box_bwd_x");
+    box_bwd_y_kernel<<<(unsigned)cdiv(nx, 128), 128, 0, st>>>(tmp, nx, ky, ly, ny, w);
+    after_launch("box_bwd_y");
+}
+
 // "rest" group of eq. P:440-443: 𝕏 − Σ_g X̃_g on 𝔑′ (NaN elsewhere).
 template <typename T>
 __global__ void rest_kernel(const T *x, const int32_t *w, const T *groups, int ng, int64_t stride, int64_t n, T *rest) {
