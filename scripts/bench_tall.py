@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import ctypes as C
 from paper_1309_5050_b200 import _lib
 L = _lib.load()
-shapes = [(201601, 32, 32), (201601, 96, 32), (201601, 192, 32), (201601, 224, 32), (24584, 192, 32), (4096, 192, 32),
+shapes = [(1024, 32, 32), (1024, 224, 32), (4096, 32, 32), (4096, 224, 32), (201601, 32, 32), (201601, 96, 32), (201601, 192, 32), (201601, 224, 32), (24584, 192, 32), (4096, 192, 32),
           (14753281 // 8, 64, 64), (14753281 // 8, 356, 64)]
 for (M, n1, n2) in [(201601, 32, 32), (1844160, 64, 64)]:
     ms = C.c_double(); ck = C.c_double()

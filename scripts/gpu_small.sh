@@ -1,0 +1,3 @@
+timeout 300 python scripts/bench_tall.py 2>&1 | grep "upd" | head -5
+timeout 900 python -m pytest tests/ -m gpu -x -q -k "decompose or edge or reconstruct or band or c3_noiseless or c1" > gpurun_out/pytest_q.log 2>&1; echo "pytest $?"; tail -2 gpurun_out/pytest_q.log
+timeout 900 python scripts/sweep_warm.py c1,c2,c3 d d
