@@ -451,23 +451,52 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
     SSA_CUDA(cudaStreamSynchronize(st));
 }
 
+// V_i = Xᵀu_i / σ_i, computed on demand: all r columns (ssa_get_v), or only the columns a
+// reconstruction references (c5: 6 of 50 — one Xᵀ·U block of 6 instead of 50 vectors)
 template <typename T>
-static void get_v(PlanImpl &p) {
+static void get_v(PlanImpl &p, const std::vector<int> *need = nullptr) {
     if (p.v_valid) return;
-    p.V.alloc(sizeof(T) * p.K * std::max(p.r, 1), p.st);
-    op_xtu<T>(p, p.U.as<T>(), p.L, p.V.as<T>(), p.K, p.r);
-    std::vector<double> inv(p.r);
-    for (int i = 0; i < p.r; ++i) inv[i] = p.sigma[i] > 0 ? 1.0 / p.sigma[i] : 0.0;
-    double *d = small_dev(p, std::max(p.r, 1));
-    SSA_CUDA(cudaMemcpyAsync(d, inv.data(), sizeof(double) * p.r, cudaMemcpyHostToDevice, p.st));
-    scale_columns<T>(p.K, p.V.as<T>(), p.K, p.r, d, p.st);
-    SSA_CUDA(cudaStreamSynchronize(p.st));
-    p.v_valid = true;
+    if ((int)p.v_have.size() != p.r) {
+        p.v_have.assign(p.r, 0);
+        p.V.alloc(sizeof(T) * p.K * std::max(p.r, 1), p.st);
+    }
+    std::vector<int> miss;
+    for (int i = 0; i < p.r; ++i)
+        if (!p.v_have[i] && (!need || std::find(need->begin(), need->end(), i) != need->end())) miss.push_back(i);
+    if (!miss.empty()) {
+        const int nm = (int)miss.size();
+        std::vector<double> inv(nm);
+        for (int t = 0; t < nm; ++t) inv[t] = p.sigma[miss[t]] > 0 ? 1.0 / p.sigma[miss[t]] : 0.0;
+        double *d = small_dev(p, std::max(nm, 1));
+        SSA_CUDA(cudaMemcpyAsync(d, inv.data(), sizeof(double) * nm, cudaMemcpyHostToDevice, p.st));
+        if (nm == p.r) {
+            op_xtu<T>(p, p.U.as<T>(), p.L, p.V.as<T>(), p.K, p.r);
+            scale_columns<T>(p.K, p.V.as<T>(), p.K, p.r, d, p.st);
+        } else {
+            DevBuf ut, vt;
+            ut.alloc(sizeof(T) * p.L * nm, p.st);
+            vt.alloc(sizeof(T) * p.K * nm, p.st);
+            for (int t = 0; t < nm; ++t)
+                SSA_CUDA(cudaMemcpyAsync(ut.as<T>() + p.L * t, p.U.as<T>() + p.L * miss[t], sizeof(T) * p.L,
+                                         cudaMemcpyDeviceToDevice, p.st));
+            op_xtu<T>(p, ut.as<T>(), p.L, vt.as<T>(), p.K, nm);
+            scale_columns<T>(p.K, vt.as<T>(), p.K, nm, d, p.st);
+            for (int t = 0; t < nm; ++t)
+                SSA_CUDA(cudaMemcpyAsync(p.V.as<T>() + p.K * miss[t], vt.as<T>() + p.K * t, sizeof(T) * p.K,
+                                         cudaMemcpyDeviceToDevice, p.st));
+        }
+        SSA_CUDA(cudaStreamSynchronize(p.st));
+        for (int i : miss) p.v_have[i] = 1;
+    }
+    if (std::all_of(p.v_have.begin(), p.v_have.end(), [](char c) { return c != 0; })) p.v_valid = true;
 }
 
 template <typename T>
 static void reconstruct_impl(PlanImpl &p, const int32_t *off, const int32_t *idx, int ng, int add_rest, T *out_dev) {
-    get_v<T>(p);
+    {
+        std::vector<int> need(idx, idx + off[ng]);
+        get_v<T>(p, &need);
+    }
     const int64_t nxy = (int64_t)p.nx * p.ny;
     DevBuf go, gi, sig;
     const int nidx = off[ng];
@@ -746,6 +775,7 @@ ssa_status ssa_set_triples(ssa_plan p, int32_t r, const double *sigma, const voi
     P.sigma.assign(sigma, sigma + r);
     P.r = r;
     P.v_valid = false;
+    P.v_have.clear();
     if (V) {
         P.V.alloc(es * P.K * r, P.st);
         SSA_CUDA(cudaMemcpyAsync(P.V.p, V, es * P.K * r, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P.st));

@@ -214,7 +214,7 @@ __device__ cplx<T> *fft_batch(cplx<T> *x, cplx<T> *y, int lg, int nbatch, const 
 // grid: (ceil(by / CB), k), CB columns per CTA.
 // ---------------------------------------------------------------------------
 template <typename T, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 2)
+__global__ void __launch_bounds__(MAXT, sizeof(T) == 4 ? (MAXT <= 256 ? 6 : 3) : (MAXT <= 256 ? 4 : 2))
 fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, int bx, int by, int jsel_n,
            const int *__restrict__ jsel, const double *__restrict__ scale, int lgx, int CB, cplx<T> *__restrict__ A,
            const cplx<T> *__restrict__ tw, int lgtw) {
@@ -271,7 +271,7 @@ fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, in
 // grid: (ceil(Hx / RB), k)
 // ---------------------------------------------------------------------------
 template <typename T, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 2)
+__global__ void __launch_bounds__(MAXT, sizeof(T) == 4 ? (MAXT <= 256 ? 6 : 3) : (MAXT <= 256 ? 4 : 2))
 fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, const cplx<T> *__restrict__ Xh,
            int mode, cplx<T> *__restrict__ B, int ny_out, const cplx<T> *__restrict__ tw, int lgtw) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -334,7 +334,7 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
 
 // Pass B (averaging): per (g, fx): Σ_{i∈I_g} DFT_y(AU_i row) ⊙ DFT_y(AV_i row), inverse, keep ny rows.
 template <typename T, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 2)
+__global__ void __launch_bounds__(MAXT, sizeof(T) == 4 ? (MAXT <= 256 ? 6 : 3) : (MAXT <= 256 ? 4 : 2))
 fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restrict__ AV, int ky, const int *grp_off,
                 const int *grp_idx, const int *slot, int Hx, int lgy, int RB, cplx<T> *__restrict__ B, int ny_out,
                 const cplx<T> *__restrict__ tw, int lgtw) {
@@ -387,7 +387,7 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
 // grid: (ceil(oy / CB), k)
 // ---------------------------------------------------------------------------
 template <typename T, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 2)
+__global__ void __launch_bounds__(MAXT, sizeof(T) == 4 ? (MAXT <= 256 ? 6 : 3) : (MAXT <= 256 ? 4 : 2))
 fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int ox, T inv, T *__restrict__ out,
            int64_t ldo, const int *__restrict__ omap, const int *__restrict__ w, int64_t stride,
            const cplx<T> *__restrict__ tw, int lgtw) {

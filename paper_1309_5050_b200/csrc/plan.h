@@ -51,6 +51,7 @@ struct PlanImpl {
     DevBuf U;          // T[L*r]
     DevBuf V;          // T[K*r] (valid if v_valid)
     bool v_valid = false;
+    std::vector<char> v_have;   // per-column validity of V when !v_valid (reconstruction computes only used columns)
     ssa_decomp_info last_info{};
 
     size_t elem() const { return dt == SSA_F64 ? 8 : 4; }

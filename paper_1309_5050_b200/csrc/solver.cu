@@ -1006,6 +1006,7 @@ struct Gkl {
         }
         sg.sync();
         p.v_valid = false;
+        p.v_have.clear();
         if (info) {
             info->r_requested = r;
             info->n_converged = nconv;
