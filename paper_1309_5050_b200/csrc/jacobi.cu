@@ -283,12 +283,13 @@ __device__ __forceinline__ float sqrt_approx(float x) { float r; asm("sqrt.appro
 __device__ __forceinline__ bool pair_rotation(double al, double be, double ga, double tol2, double &c, double &s,
                                               float &mrel) {
     c = 1.0; s = 0.0;
-    if (!(ga * ga > tol2 * al * be)) return false;
-    mrel = fmaxf(mrel, (float)(fabs(ga) * rsqrt(al * be)));   // relative off-diagonal (early stop)
-    // 2^-e with e the exponent of max(al, be): scaled operands are <= 1 in magnitude
+    // 2^-e with e the exponent of max(al, be): scaled operands are <= 1 in magnitude, so the skip
+    // test and the angle run in fp32 without overflow (fewer dependent fp64 ops per step)
     const int hi = __double2hiint(fmax(al, be));
     const double scale = __hiloint2double(((2046 - ((hi >> 20) & 2047)) & 2047) << 20, 0);
     const float fa = (float)(al * scale), fb = (float)(be * scale), fg = (float)(ga * scale);
+    if (!(fg * fg > (float)tol2 * fa * fb)) return false;
+    mrel = fmaxf(mrel, fabsf(fg) * rsqrtf(fa * fb));   // relative off-diagonal (early stop)
     const float zeta = (fb - fa) * 0.5f * rcp_approx(fg);
     float tf = copysignf(1.0f, zeta) * rcp_approx(fabsf(zeta) + sqrt_approx(fmaf(zeta, zeta, 1.0f)));
     if (!isfinite(zeta)) tf = 0.0f;
