@@ -203,7 +203,10 @@ ssa_status ssa_small_svd(int32_t m, int32_t n, double *A, int32_t *sweeps, doubl
  * B: M x n2, n1 <= 512, n2 <= 64), which = 1 the update W -= A·C (A: M x n1,
  * W: M x n2).  Leading dimension M rounded up to 32 (the solver's layout).
  * *ms = average device milliseconds over `reps` launches after one warm-up;
- * *check = a checksum of the result (Σ|G| or Σ|W|).  SSA_ERR_ARG on bad sizes. */
+ * *check = max relative error against an fp64 host evaluation (update: on ~1000 sampled
+ * rows; Gram: all entries when M·n1·n2 <= 5e8, else the checksum Σ|G|).  which = 3 times
+ * the self Gram AᵀA[:, :n2]; which = 4 is a TMA streaming probe (n2 = box columns + 256 x row
+ * groups).  SSA_ERR_ARG on bad sizes. */
 ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32_t n2, int32_t reps, double *ms,
                           double *check);
 

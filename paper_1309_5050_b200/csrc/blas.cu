@@ -1037,7 +1037,24 @@ extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32
             if (which == 0 || which == 3) {
                 std::vector<double> hg((size_t)n1 * n2);
                 SSA_CUDA(cudaMemcpy(hg.data(), g.p, sizeof(double) * hg.size(), cudaMemcpyDeviceToHost));
-                for (double v : hg) s += std::fabs(v);
+                if ((double)M * n1 * n2 <= 5e8) {
+                    // max relative error against an fp64 host Gram of the same fp32 data
+                    std::vector<float> ha((size_t)ld * n1), hb((size_t)ld * n2);
+                    SSA_CUDA(cudaMemcpy(ha.data(), a.p, sizeof(float) * ha.size(), cudaMemcpyDeviceToHost));
+                    SSA_CUDA(cudaMemcpy(hb.data(), b.p, sizeof(float) * hb.size(), cudaMemcpyDeviceToHost));
+                    const std::vector<float> &hB = (which == 3) ? ha : hb;
+                    double emax = 0.0, gmax = 0.0;
+                    for (int j = 0; j < n2; ++j)
+                        for (int i = 0; i < n1; ++i) {
+                            double v = 0.0;
+                            for (int64_t r = 0; r < M; ++r) v += (double)ha[r + ld * i] * (double)hB[r + ld * j];
+                            emax = std::max(emax, std::fabs(v - hg[i + (size_t)n1 * j]));
+                            gmax = std::max(gmax, std::fabs(v));
+                        }
+                    s = emax / std::max(gmax, 1e-300);
+                } else {
+                    for (double v : hg) s += std::fabs(v);
+                }
             } else {
                 std::vector<float> hw((size_t)ld * n2);
                 SSA_CUDA(cudaMemcpy(hw.data(), b.p, sizeof(float) * hw.size(), cudaMemcpyDeviceToHost));
