@@ -490,6 +490,10 @@ static bool tall_update(int64_t M, const float *A, int64_t lda, int m, const dou
 }
 
 template <typename T>
+static bool gemm_split(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
+                       double beta, T *Out, int64_t ldo, cudaStream_t st);
+
+template <typename T>
 void gemm_small(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n,
                 double alpha, double beta, T *Out, int64_t ldo, cudaStream_t st) {
     SSA_REQUIRE(m <= 64 && n <= 64, SSA_ERR_ARG, "gemm_small: at most 64x64");
@@ -498,6 +502,7 @@ void gemm_small(int64_t M, const T *A, int64_t lda, int m, const double *C, int 
         if (update_tc(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo, st)) return;
         if (tall_update(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo, st)) return;
     }
+    if (gemm_split<T>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo, st)) return;   // small M, in place ok
     const bool inplace = (Out == A);
     // small M: spread the column chunks over more CTAs (not in place)
     const int gy = inplace ? 1 : (int)std::min<int64_t>(cdiv(n, 16), std::max<int64_t>(1, (2 * num_sms()) / cdiv(M, 128)));
@@ -553,6 +558,81 @@ gemm_acc_kernel(int64_t M, const T *__restrict__ A, int64_t lda, int m, const do
         if (j < n) Out[row + ldo * j] = acc[j];
 }
 
+// Small-M variant (M < 16384, the L side): the m-long reduction of a row is split over the 8
+// warps of a CTA (warp w: columns w, w+8, ...; lane = row), partial sums meet in shared memory.
+// 4x the CTAs and 1/8 of the dependent loop of the thread-per-row kernel (33 µs -> see DESIGN).
+// A CTA owns its 32 rows, so Out may be the trailing columns of A (all reads precede the
+// reduction barrier, all writes follow it).
+template <typename T, int NMAX>
+__global__ void __launch_bounds__(256)
+gemm_acc_split_kernel(int64_t M, const T *A, int64_t lda, int m, const double *__restrict__ C, int ldc, int n,
+                      double alpha, double beta, T *Out, int64_t ldo) {
+    extern __shared__ __align__(16) unsigned char ss_raw[];
+    T *CS = reinterpret_cast<T *>(ss_raw);          // [m][NMAX] alpha·C
+    T *red = CS + (size_t)m * NMAX;                   // [8][32][NMAX + 1] partial sums
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+#pragma unroll 4
+    for (int idx = tid; idx < m * NMAX; idx += 256) {
+        const int b = idx / m, a = idx - b * m;       // a (row of C) fastest: coalesced reads of C
+        CS[a * NMAX + b] = (b < n) ? (T)(alpha * C[a + (int64_t)ldc * b]) : T(0);
+    }
+    __syncthreads();
+    const int64_t row = (int64_t)blockIdx.x * 32 + lane;
+    T acc[NMAX];
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) acc[j] = T(0);
+    if (row < M) {
+        int c = w;
+        for (; c + 8 < m; c += 16) {                  // two columns per iteration: loads in flight
+            const T a0 = A[row + lda * (int64_t)c], a1 = A[row + lda * (int64_t)(c + 8)];
+            const T *c0 = CS + c * NMAX, *c1 = CS + (c + 8) * NMAX;
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) acc[j] = fma(a1, c1[j], fma(a0, c0[j], acc[j]));
+        }
+        if (c < m) {
+            const T a0 = A[row + lda * (int64_t)c];
+            const T *c0 = CS + c * NMAX;
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) acc[j] = fma(a0, c0[j], acc[j]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) red[(w * 32 + lane) * (NMAX + 1) + j] = acc[j];
+    __syncthreads();
+    // thread -> (row lane', outputs j = jg, jg + 8, ...): fixed summation order over the warps
+    const int rl = tid & 31, jg = tid >> 5;
+    const int64_t r = (int64_t)blockIdx.x * 32 + rl;
+    if (r >= M) return;
+    for (int j = jg; j < n; j += 8) {
+        T s = T(0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += red[(q * 32 + rl) * (NMAX + 1) + j];
+        T *o = Out + r + ldo * (int64_t)j;
+        *o = (beta == 0.0) ? s : fma((T)beta, *o, s);
+    }
+}
+
+template <typename T>
+static bool gemm_split(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
+                       double beta, T *Out, int64_t ldo, cudaStream_t st) {
+    static const bool split_off = std::getenv("SSA_SPLIT_OFF") != nullptr;
+    if (M >= 16384 || split_off || n > 64) return false;
+    const unsigned g = (unsigned)cdiv(M, 32);
+    if (n <= 32) {
+        const size_t smem = sizeof(T) * ((size_t)m * 32 + 8 * 32 * 33);
+        if (smem > 200 * 1024) return false;
+        set_max_smem(gemm_acc_split_kernel<T, 32>);
+        gemm_acc_split_kernel<T, 32><<<g, 256, smem, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
+    } else {
+        const size_t smem = sizeof(T) * ((size_t)m * 64 + 8 * 32 * 65);
+        if (smem > 200 * 1024) return false;
+        set_max_smem(gemm_acc_split_kernel<T, 64>);
+        gemm_acc_split_kernel<T, 64><<<g, 256, smem, st>>>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo);
+    }
+    after_launch("gemm_acc_split");
+    return true;
+}
+
 template <typename T>
 void gemm_acc(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
               double beta, T *Out, int64_t ldo, cudaStream_t st) {
@@ -562,6 +642,7 @@ void gemm_acc(int64_t M, const T *A, int64_t lda, int m, const double *C, int ld
         if (update_tc(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo, st)) return;
         if (tall_update(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo, st)) return;
     }
+    if (gemm_split<T>(M, A, lda, m, C, ldc, n, alpha, beta, Out, ldo, st)) return;
     const unsigned grid = (unsigned)cdiv(M, 128);
     if (n <= 32) {
         const size_t smem = sizeof(T) * (size_t)m * 32;
