@@ -299,6 +299,17 @@ __device__ __forceinline__ bool pair_rotation(double al, double be, double ga, d
     return true;
 }
 
+// debug timeline (SSA_JACOBI_TRACE): CTA 0 thread 0 globaltimer at the phase boundaries of the
+// first 32 rounds: [round][0 start, 1 Gram done, 2 steps done, 3 C·V done, 4 cluster barrier done]
+__device__ unsigned long long *g_jac_trace = nullptr;
+__device__ __forceinline__ void jtrace(int round, int ph) {
+    if (g_jac_trace && blockIdx.x == 0 && threadIdx.x == 0 && round < 32) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_jac_trace[round * 5 + ph] = t;
+    }
+}
+
 template <int NC>
 __global__ void __launch_bounds__(256, 1)
 jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, float early, int max_sweeps,
@@ -367,6 +378,7 @@ jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, floa
         if (tid == 0) { rot_sh = 0; mrel_sh = 0; }
         for (int round = 0; round < nb - 1; ++round, ++t) {
             const double *C = bufs + cur * NC * ldc;
+            if (sweep == 0) jtrace(round, 0);
             // ---- 1. Gram G = CᵀC (tensor cores), k split over warps when there are few tiles
             {
                 const int ks = warp % Cfg::KSPLIT;
@@ -374,15 +386,15 @@ jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, floa
                     const int ta = tile / (NC / 8), tb = tile % (NC / 8);
                     const double *ca = C + ldc * (8 * ta + (lane >> 2)) + (lane & 3);
                     const double *cb = C + ldc * (8 * tb + (lane >> 2)) + (lane & 3);
-                    double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;   // two accumulator chains
-                    int k0 = 4 * ks;
-                    for (; k0 + 4 * Cfg::KSPLIT < m4; k0 += 8 * Cfg::KSPLIT) {
-                        dmma884(d0, d1, ca[k0], cb[k0]);
-                        dmma884(e0, e1, ca[k0 + 4 * Cfg::KSPLIT], cb[k0 + 4 * Cfg::KSPLIT]);
+                    double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};   // four accumulator chains
+                    constexpr int KS4 = 4 * Cfg::KSPLIT;
+                    for (int k0 = 4 * ks; k0 < m4; k0 += 4 * KS4) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)   // warp-uniform guard, constant chain index
+                            if (k0 + q * KS4 < m4) dmma884(d[q][0], d[q][1], ca[k0 + q * KS4], cb[k0 + q * KS4]);
                     }
-                    if (k0 < m4) dmma884(d0, d1, ca[k0], cb[k0]);
-                    d0 += e0;
-                    d1 += e1;
+                    const double d0 = (d[0][0] + d[1][0]) + (d[2][0] + d[3][0]);
+                    const double d1 = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
                     double *gp = Gp + ks * NC * NC + NC * (8 * ta + (lane >> 2)) + 8 * tb + 2 * (lane & 3);
                     gp[0] = d0;
                     gp[1] = d1;
@@ -398,6 +410,7 @@ jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, floa
                 Vs[x * LDG + y] = (x == y) ? 1.0 : 0.0;
             }
             __syncthreads();
+            if (sweep == 0) jtrace(round, 1);
             // ---- 2. Jacobi steps on G, V accumulated: G_new = Jᵀ G J, V_new = V J (ping-pong
             // buffers, one barrier per step).  Every warp computes the NC/2 rotations of the step
             // (lane w -> pair w; identical on every warp) and hands them to the lanes owning
@@ -440,6 +453,7 @@ jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, floa
                 if (rot) rot_sh = 1;   // benign races: every writer stores 1 / a larger value
                 if (lane == 0 && mrel > 0.f) atomicMax(&mrel_sh, __float_as_int(mrel));
             }
+            if (sweep == 0) jtrace(round, 2);
             // ---- 3. C·V on the tensor cores, stored into the next-round buffers
             {
                 const double *V = Vs + gi * NC * LDG;
@@ -451,24 +465,46 @@ jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, floa
                     dstA = cluster.map_shared_rank(nxt_local, c - 1);
                     dstB = (c + 1 < ncta) ? cluster.map_shared_rank(nxt_local, c + 1) + blk : nxt_local;
                 }
-                const int ntiles = (m8 / 8) * (NC / 8);
-                for (int tile = warp; tile < ntiles; tile += 8) {
-                    const int it = tile / (NC / 8), jt = tile - it * (NC / 8);
-                    double d0 = 0.0, d1 = 0.0;
+                // a warp takes two 8-row tiles at a time and all NC/8 column tiles: the row fragments
+                // are loaded once per k-step and 2·NC/8 independent DMMA chains overlap their latency
+                constexpr int NJ = NC / 8;
+                const int nit = m8 / 8;
+                for (int it0 = warp; it0 < nit; it0 += 16) {
+                    const bool two = it0 + 8 < nit;        // warp-uniform
+                    double acc[2][NJ][2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int jt = 0; jt < NJ; ++jt) acc[h][jt][0] = acc[h][jt][1] = 0.0;
 #pragma unroll
                     for (int k0 = 0; k0 < NC; k0 += 4) {
-                        const double a = C[ldc * (k0 + (lane & 3)) + 8 * it + (lane >> 2)];
-                        const double b = V[(k0 + (lane & 3)) * LDG + 8 * jt + (lane >> 2)];
-                        dmma884(d0, d1, a, b);
+                        const double *cr = C + ldc * (k0 + (lane & 3)) + (lane >> 2);
+                        const double a0 = cr[8 * it0];
+                        const double a1 = two ? cr[8 * (it0 + 8)] : 0.0;
+#pragma unroll
+                        for (int jt = 0; jt < NJ; ++jt) {
+                            const double b = V[(k0 + (lane & 3)) * LDG + 8 * jt + (lane >> 2)];
+                            dmma884(acc[0][jt][0], acc[0][jt][1], a0, b);
+                            if (two) dmma884(acc[1][jt][0], acc[1][jt][1], a1, b);
+                        }
                     }
-                    const int row = 8 * it + (lane >> 2);
-                    const int col = 8 * jt + 2 * (lane & 3);   // col, col+1 in the same slot (BW % 8 == 0)
-                    double *dst = (col < BW) ? dstA + ldc * col : dstB + ldc * (col - BW);
-                    dst[row] = d0;
-                    dst[row + ldc] = d1;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (h == 1 && !two) break;
+                        const int row = 8 * (it0 + 8 * h) + (lane >> 2);
+#pragma unroll
+                        for (int jt = 0; jt < NJ; ++jt) {
+                            const int col = 8 * jt + 2 * (lane & 3);   // col, col+1 in the same slot (BW % 8 == 0)
+                            double *dst = (col < BW) ? dstA + ldc * col : dstB + ldc * (col - BW);
+                            dst[row] = acc[h][jt][0];
+                            dst[row + ldc] = acc[h][jt][1];
+                        }
+                    }
                 }
             }
+            if (sweep == 0) jtrace(round, 3);
             cluster.sync();
+            if (sweep == 0) jtrace(round, 4);
             cur ^= 1;
         }
         // convergence: no rotation anywhere, or the largest relative off-diagonal rotated in this
@@ -523,8 +559,24 @@ static bool launch_gram(int m, int n, double *T, int *sweeps, cudaStream_t st, f
     attr[0].val.clusterDim.x = ncta; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr; cfg.numAttrs = 1;
     int max_sweeps = 60;
+    static unsigned long long *tb = nullptr;
+    if (std::getenv("SSA_JACOBI_TRACE") && !tb) {
+        SSA_CUDA(cudaMalloc(&tb, 32 * 5 * 8));
+        SSA_CUDA(cudaMemset(tb, 0, 32 * 5 * 8));
+        SSA_CUDA(cudaMemcpyToSymbol(g_jac_trace, &tb, sizeof(tb)));
+    }
     SSA_CUDA(cudaLaunchKernelEx(&cfg, kern, m, n, nb, T, tol, early, max_sweeps, sweeps));
     after_launch("jacobi_gram");
+    if (tb) {
+        unsigned long long h[32 * 5];
+        SSA_CUDA(cudaStreamSynchronize(st));
+        SSA_CUDA(cudaMemcpy(h, tb, sizeof(h), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[jacobi trace] m=%d n=%d nb=%d (us per phase: gram steps cv sync)\n", m, n, nb);
+        for (int r = 0; r < std::min(nb - 1, 6); ++r)
+            std::fprintf(stderr, "  round %d: %.2f %.2f %.2f %.2f\n", r, (h[r * 5 + 1] - h[r * 5]) * 1e-3,
+                         (h[r * 5 + 2] - h[r * 5 + 1]) * 1e-3, (h[r * 5 + 3] - h[r * 5 + 2]) * 1e-3,
+                         (h[r * 5 + 4] - h[r * 5 + 3]) * 1e-3);
+    }
     return true;
 }
 
