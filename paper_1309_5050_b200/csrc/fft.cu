@@ -390,7 +390,8 @@ template <typename T, int MAXT>
 __global__ void __launch_bounds__(MAXT, sizeof(T) == 4 ? (MAXT <= 256 ? 6 : 3) : (MAXT <= 256 ? 4 : 2))
 fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int ox, T inv, T *__restrict__ out,
            int64_t ldo, const int *__restrict__ omap, const int *__restrict__ w, int64_t stride,
-           const cplx<T> *__restrict__ tw, int lgtw) {
+           const cplx<T> *__restrict__ tw, int lgtw, const cplx<T> *__restrict__ Afu, int ny_in,
+           const cplx<T> *__restrict__ gk, int lgy) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int Mx = 1 << lgx;
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
@@ -407,9 +408,24 @@ fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int o
     for (int idx = threadIdx.x; idx < Hx * NT; idx += blockDim.x) {
         const int fx = idx / NT, t = idx - fx * NT;
         cplx<T> ya{T(0), T(0)}, yb{T(0), T(0)};
-        const int64_t base = ((int64_t)j * Hx + fx) * oy + y0 + 2 * t;
-        if (2 * t < ncol) ya = B[base];
-        if (2 * t + 1 < ncol) yb = B[base + 1];
+        if (Afu) {
+            // pass B folded in (few rows on both sides, MSSA): the y-correlation with the image as
+            // B[fx, y] = Σ_{y'} conj(A[fx, y']) · g[fx, (y + y') mod My], g = unnormalised inverse
+            // y-DFT of the X̂ row (plan time)
+            const int My = 1 << lgy;
+            const cplx<T> *ar = Afu + ((int64_t)j * Hx + fx) * ny_in;
+            const cplx<T> *gr = gk + (int64_t)fx * My;
+            const int ya_i = y0 + 2 * t;
+            for (int yp = 0; yp < ny_in; ++yp) {
+                const cplx<T> a = ar[yp];
+                if (2 * t < ncol) ya = cadd(ya, cmulconj(gr[(ya_i + yp) & (My - 1)], a));
+                if (2 * t + 1 < ncol) yb = cadd(yb, cmulconj(gr[(ya_i + 1 + yp) & (My - 1)], a));
+            }
+        } else {
+            const int64_t base = ((int64_t)j * Hx + fx) * oy + y0 + 2 * t;
+            if (2 * t < ncol) ya = B[base];
+            if (2 * t + 1 < ncol) yb = B[base + 1];
+        }
         if (fx == 0 || fx == Mx / 2) { ya.y = T(0); yb.y = T(0); }   // real signals: these bins are real
         b0[sp(t * Mx + fx)] = cplx<T>{ya.x - yb.y, ya.y + yb.x};
         if (fx > 0 && fx < Mx / 2) b0[sp(t * Mx + Mx - fx)] = cplx<T>{ya.x + yb.y, yb.x - ya.y};
@@ -440,6 +456,7 @@ struct FftOperator {
     int lgtw = 0;
     DevBuf tw;        // cplx[2^lgtw]: exp(−2πi t / 2^lgtw), fp64-accurate
     DevBuf Xh;        // cplx[Hx][My]: DFT2 of the image
+    DevBuf gk;        // cplx[Hx][My]: unnormalised inverse y-DFT of each X̂ row (small My: folded pass B)
     DevBuf bufA, bufB;
     size_t capA = 0, capB = 0;
 };
@@ -507,7 +524,7 @@ static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode,
 
 template <typename T>
 static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *out, int64_t ldo, const int *omap,
-                   const int *w, int64_t stride, cudaStream_t st) {
+                   const int *w, int64_t stride, cudaStream_t st, const cplx<T> *Afu = nullptr, int ny_in = 0) {
     const int CB = 2 * batch_for(f.lgx, 2048);   // output columns (two per complex transform)
     const size_t smem = smem_ab<T>(f.lgx, CB / 2, f.lgtw);
     const int nth = threads_for(f.lgx, CB / 2, cdiv(oy, CB) * k);
@@ -515,13 +532,33 @@ static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *o
     set_max_smem(kern);
     const T inv = (T)(1.0 / ((double)f.Mx * (double)f.My));
     kern<<<dim3((unsigned)cdiv(oy, CB), k), nth, smem, st>>>(B, oy, f.Hx, f.lgx, CB, ox, inv, out, ldo, omap,
-                                                                       w, stride, f.tw.as<cplx<T>>(), f.lgtw);
+                                                                       w, stride, f.tw.as<cplx<T>>(), f.lgtw, Afu,
+                                                                       ny_in, Afu ? f.gk.as<cplx<T>>() : nullptr, f.lgy);
     after_launch("fft_pass_c");
 }
 
 template <typename T>
 static void ensure(FftOperator &f, DevBuf &b, size_t &cap, size_t need, cudaStream_t st) {
     if (need > cap) { b.alloc(need, st); cap = need; }
+}
+
+// g[fx, d] = Σ_fy X̂[fx, fy]·exp(+2πi fy d / My), accumulated in fp64 (plan time, small My only)
+template <typename T>
+__global__ void gk_kernel(const cplx<T> *__restrict__ Xh, int Hx, int lgy, cplx<T> *__restrict__ g) {
+    const int My = 1 << lgy;
+    const int64_t n = (int64_t)Hx * My;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int fx = (int)(t >> lgy), d = (int)(t & (My - 1));
+        double sr = 0.0, si = 0.0;
+        for (int fy = 0; fy < My; ++fy) {
+            double sn, cs;
+            sincospi(2.0 * (double)((fy * d) & (My - 1)) / (double)My, &sn, &cs);
+            const cplx<T> x = Xh[(int64_t)fx * My + fy];
+            sr += (double)x.x * cs - (double)x.y * sn;
+            si += (double)x.x * sn + (double)x.y * cs;
+        }
+        g[t] = cplx<T>{(T)sr, (T)si};
+    }
 }
 
 template <typename T>
@@ -547,6 +584,12 @@ static void build_impl(PlanImpl &p) {
     // X̂: x-DFT of the image columns, then the full-length y-DFT (mode 1)
     pass_a<T>(f, p.img.as<T>(), 0, nullptr, p.nx, p.ny, 1, nullptr, nullptr, tmp.as<cplx<T>>(), p.st);
     pass_b<T>(f, tmp.as<cplx<T>>(), p.ny, 1, 1, f.Xh.as<cplx<T>>(), f.My, p.st);
+    if (f.My <= 64) {
+        f.gk.alloc(sizeof(cplx<T>) * (size_t)f.Hx * f.My, p.st);
+        gk_kernel<T><<<(unsigned)cdiv((int64_t)f.Hx * f.My, 256), 256, 0, p.st>>>(f.Xh.as<cplx<T>>(), f.Hx, f.lgy,
+                                                                                   f.gk.as<cplx<T>>());
+        after_launch("fft_gk");
+    }
     SSA_CUDA(cudaStreamSynchronize(p.st));
 }
 
@@ -566,8 +609,14 @@ static void correlate(PlanImpl &p, const T *in, int64_t ldin, const int *imap, i
         ensure<T>(f, f.bufA, f.capA, sizeof(cplx<T>) * (size_t)kc * f.Hx * by, p.st);
         ensure<T>(f, f.bufB, f.capB, sizeof(cplx<T>) * (size_t)kc * f.Hx * oy, p.st);
         pass_a<T>(f, in + ldin * j0, ldin, imap, bx, by, kc, nullptr, nullptr, f.bufA.as<cplx<T>>(), p.st);
-        pass_b<T>(f, f.bufA.as<cplx<T>>(), by, kc, 0, f.bufB.as<cplx<T>>(), oy, p.st);
-        pass_c<T>(f, f.bufB.as<cplx<T>>(), oy, kc, ox, out + ldo * j0, ldo, omap, nullptr, 0, p.st);
+        static const bool nofold = std::getenv("SSA_FFT_NOFOLD") != nullptr;
+        if (f.gk.p && !nofold && by <= 2 && (int64_t)by * oy <= 64) {
+            // MSSA-like shapes (few rows in and out): pass B folded into pass C
+            pass_c<T>(f, nullptr, oy, kc, ox, out + ldo * j0, ldo, omap, nullptr, 0, p.st, f.bufA.as<cplx<T>>(), by);
+        } else {
+            pass_b<T>(f, f.bufA.as<cplx<T>>(), by, kc, 0, f.bufB.as<cplx<T>>(), oy, p.st);
+            pass_c<T>(f, f.bufB.as<cplx<T>>(), oy, kc, ox, out + ldo * j0, ldo, omap, nullptr, 0, p.st);
+        }
     }
 }
 
