@@ -416,7 +416,22 @@ jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, floa
             // (lane w -> pair w; identical on every warp) and hands them to the lanes owning
             // entries (x, y) by shuffles.
             int gi = 0;
+            // skip the steps when none of the pairs this round visits (cross pairs; intra-slot pairs in
+            // round 0) exceeds the rotation threshold on the fresh Gram: no step would rotate then
+            // (late sweeps; the CTA still does the C·V = C copy of the systolic shift)
+            bool work;
             {
+                bool need = false;
+                for (int e = tid; e < NC * NC; e += Cfg::NT) {
+                    const int x = e / NC, y = e - x * NC;
+                    if (x < y && (round == 0 || (x < BW) != (y < BW))) {
+                        const double g = Gs[x * LDG + y], a = Gs[x * LDG + x], b = Gs[y * LDG + y];
+                        need = need || (g * g > tol2 * a * b);
+                    }
+                }
+                work = __syncthreads_or(need) != 0;
+            }
+            if (work) {
                 int rot = 0;
                 float mrel = 0.f;
                 for (int st = (round == 0 ? 0 : BW - 1); st < NC - 1; ++st) {
