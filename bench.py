@@ -345,6 +345,90 @@ def oracle_products_per_s(w, budget_s=15.0):
     return value, cores, sample
 
 
+def run_sharded(args, rank, world, dist):
+    """--shard: ONE decomposition of the config split over the ranks (strong scaling):
+    rank r owns the window positions κ_y ∈ [r·ky/N, (r+1)·ky/N) (a band plan, halo rows implied by the
+    full image every rank holds); X·V partials and K-side Grams are summed with an NCCL all-reduce
+    through the library's communicator hook (dist.TorchComm).  Reconstruction of a band plan is left
+    to the caller, so a step is plan + decompose.  Not measured at N > 1 in this round (one GPU per
+    gpurun call); at N = 1 it is the full problem without a communicator."""
+    import torch
+    from paper_1309_5050_b200 import Plan, launch_count
+    from paper_1309_5050_b200.dist import TorchComm
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    w = workload(args.config, seed_offset=0)          # the same problem on every rank
+    stream = torch.cuda.Stream(device=dev)
+    dt_torch = torch.float64 if w.dtype == "f64" else torch.float32
+    img_dev = torch.as_tensor(np.asarray(w.data), dtype=dt_torch, device=dev)
+    mask_np = None if w.mask is None else np.asarray(w.mask)
+    ny = np.asarray(w.data).shape[1]
+    ky = ny - w.window[1] + 1
+    band = (rank * ky // world, (rank + 1) * ky // world)
+    comm = TorchComm(device="cuda") if world > 1 else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(host=False):
+        with torch.cuda.stream(stream):
+            src = np.asarray(w.data) if host else img_dev
+            kw = dict(comm=comm, band=band) if comm is not None else {}
+            p = Plan(src, w.window, mask=mask_np, wmask=w.wmask, dtype=w.dtype, block_k=w.block_k,
+                     path=args.path, stream=stream.cuda_stream, **kw)
+            info = p.decompose(w.r, allow_not_converged=True)
+            sig = np.array(p.sigma)
+            p.close()
+        return info, sig
+
+    for _ in range(args.warmup):
+        info, _ = step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    times = []
+    launch_count(reset=True)
+    with ClockSampler(dev.index) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            info, sig = step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = launch_count(reset=True)
+    ms = float(np.sum(times))
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    e2e = []
+    for _ in range(max(1, min(args.steps, 3))):
+        flush.fill_(1); torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        step(host=True)
+        torch.cuda.synchronize()
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    nvec = float(info["n_vector_products"])               # one decomposition: not summed over ranks
+    esz = 8 if w.dtype == "f64" else 4
+    res = {"metric": "trajectory products/s", "value": nvec / (ms / args.steps / 1e3), "unit": "vector products/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": w.dtype,
+           "data": "synthetic (seeded BASELINE.json generator)",
+           "config": {"workload": w.name, "window": list(w.window), "r": w.r, "block_k": w.block_k,
+                      "parallelism": f"bands{world} (window positions along y, NCCL all-reduce)",
+                      "band_of_rank0": list(band), "l2": "flushed (256 MB write) between timed steps"},
+           "e2e": {"value": nvec / (np.mean(e2e) / 1e3), "unit": "vector products/s",
+                   "h2d_bytes_per_step": int(np.asarray(w.data).size * esz), "d2h_bytes_per_step": 8 * w.r},
+           "gpu_launches": int(launches), "clocks": clk.summary(), "sigma_head": [float(x) for x in sig[:4]],
+           "decomposition": {k2: info[k2] for k2 in ("n_block_products", "n_restarts", "n_converged")}}
+    return res, w
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -365,6 +449,8 @@ def main():
     ap.add_argument("--path", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--shard", action="store_true",
+                    help="one decomposition split over the ranks by window-position bands (strong scaling)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -401,9 +487,9 @@ def main():
         import torch.distributed as tdist
         tdist.init_process_group("nccl")
         dist = tdist
-    res, w = run_ours(args, rank, world, dist)
+    res, w = (run_sharded if args.shard else run_ours)(args, rank, world, dist)
     if rank == 0:
-        if not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1 and not args.shard:
             v, cores, sample = oracle_products_per_s(w, budget_s=args.cpu_budget)
             res["cpu_baseline"] = {"value": v, "unit": "vector products/s", "cores": cores, "kind": "oracle",
                                    "sample": sample, "cpu": cpu_model()}
