@@ -296,9 +296,14 @@ struct Gkl {
             }
             if (!zero.empty() && refills < 2) {
                 ++refills;
-                for (int j : zero) {
+                for (int j : zero)
                     for (int i = 0; i < kc; ++i) B[j + (size_t)kc * i] = 0.0;   // W_in has no component there
-                    fill_normal<T>(M, W + LD(M) * j, LD(M), 1, p.seed, 0x5eed0000ull + (sid++), st);
+                // one launch per run of consecutive zero columns (c5: ~130 refilled columns per decomposition)
+                for (size_t a = 0; a < zero.size();) {
+                    size_t b = a + 1;
+                    while (b < zero.size() && zero[b] == zero[b - 1] + 1) ++b;
+                    fill_normal<T>(M, W + LD(M) * zero[a], LD(M), (int)(b - a), p.seed, 0x5eed0000ull + (sid++), st);
+                    a = b;
                 }
                 if (na > 0) {
                     double *keep = coef;
