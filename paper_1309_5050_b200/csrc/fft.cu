@@ -77,38 +77,36 @@ template <typename T, int DIR> __device__ __forceinline__ void dft8(cplx<T> *v) 
 __device__ __forceinline__ int sp(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr size_t sp_size(size_t n) { return n + (n >> 4) + 1; }
 
-// Twiddles: the plan keeps tw[t] = exp(−2πi t / 2^lgtw) (fp64-accurate values rounded to T);
-// each CTA stages a two-level copy in shared memory — fine[f] = tw[f] (f < 2^lo) and
-// coarse[c] = tw[c·2^lo] (lo = lgtw/2) — and forms tw[m] = coarse[m >> lo]·fine[m mod 2^lo]
-// (one extra complex multiply, ≤ 2 ulp).  A full table in L1 competes with the FFT buffers for
-// the SM's shared storage and its loads missed to L2 (long-scoreboard stalls, ncu).
-// exp(DIR·2πi·m / 2^lg) = tw[m << (lgtw − lg)] (conjugated for DIR = +1).
-__host__ __device__ constexpr size_t tw_count(int lgtw) { return ((size_t)1 << (lgtw >> 1)) + ((size_t)1 << (lgtw - (lgtw >> 1))); }
-template <typename T>
-__device__ __forceinline__ void stage_twiddles(cplx<T> *tws, const cplx<T> *__restrict__ gtw, int lgtw) {
-    const int lo = lgtw >> 1, nf = 1 << lo, nc = 1 << (lgtw - lo);
-    for (int i = threadIdx.x; i < nf + nc; i += blockDim.x) tws[i] = i < nf ? gtw[i] : gtw[(size_t)(i - nf) << lo];
+// Twiddles: per transform size 2^LG the plan keeps one table per radix-8 stage with span
+// NS = 2^LGS > 1 — w1[k] = exp(−2πi k / (8·NS)), k < NS (fp64-accurate, rounded to T) — concatenated
+// (stab_off(LG, LGS) = position of the stage's table; 584 entries for LG = 12).  Each CTA stages
+// the table of its transform size in shared memory; a butterfly reads w1 once and forms
+// w2 = w1², w3 = w2·w1, w4 = w2², w5..w7 = w4·w1..w3 (the previous two-level table cost three
+// lookups with a complex multiply each: ~20% of the stage's instructions, ncu).
+__host__ __device__ constexpr int stab_off(int LG, int LGS) {
+    int off = 0;
+    for (int l = LG % 3; l < LGS; l += 3)
+        if (l > 0) off += 1 << l;
+    return off;
 }
-template <typename T, int DIR>
-__device__ __forceinline__ cplx<T> twiddle(const cplx<T> *__restrict__ tws, int lgtw, int m) {
-    const int lo = lgtw >> 1;
-    const cplx<T> f = tws[m & ((1 << lo) - 1)], c = tws[(1 << lo) + (m >> lo)];
-    cplx<T> w = cmul(c, f);
-    if (DIR > 0) w.y = -w.y;
-    return w;
+__host__ __device__ constexpr size_t stab_count(int lg) { return (size_t)stab_off(lg, lg); }
+template <typename T>
+__device__ __forceinline__ void stage_stab(cplx<T> *tws, const cplx<T> *__restrict__ g, int lg) {
+    const int n = (int)stab_count(lg);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) tws[i] = g[i];
 }
 
 // One Stockham radix-R stage for `nbatch` transforms of length N = 2^LGN stored back to back
 // (padded indices); NS = 2^LGS is the current span.  Sizes are template constants so the index
 // arithmetic folds (the generic version spent half of its instructions on integer address
 // math, ncu); loads use one padded base plus constant strides, and the R-1 twiddles of a
-// butterfly come from 3 table lookups (w, w², w⁴) and 4 multiplies.
+// butterfly come from one per-stage table lookup and 6 multiplies.
 template <typename T, int DIR, int R, int LGN, int LGS>
 __device__ __forceinline__ void stage_t(const cplx<T> *__restrict__ x, cplx<T> *__restrict__ y, int nbatch,
                                         const cplx<T> *__restrict__ tws, int lgtw) {
     constexpr int LR = R == 2 ? 1 : (R == 4 ? 2 : 3);
     constexpr int N = 1 << LGN, NBF = N >> LR, LGB = LGN - LR, NS = 1 << LGS;
-    const int tsh = lgtw - LGS - LR;
+    static_assert(NS == 1 || R == 8, "only the first stage may be radix 2/4");
     for (int b = threadIdx.x; b < (nbatch << LGB); b += blockDim.x) {
         const int t = b >> LGB, j = b & (NBF - 1);
         const int a = t * N + j;
@@ -123,20 +121,18 @@ __device__ __forceinline__ void stage_t(const cplx<T> *__restrict__ x, cplx<T> *
         }
         const int k = j & (NS - 1);
         if constexpr (NS > 1) {
-            const cplx<T> w1 = twiddle<T, DIR>(tws, lgtw, k << tsh);
-            if constexpr (R == 2) {
-                v[1] = cmul(v[1], w1);
-            } else {
-                const cplx<T> w2 = twiddle<T, DIR>(tws, lgtw, (2 * k) << tsh);
-                const cplx<T> w3 = cmul(w2, w1);
-                v[1] = cmul(v[1], w1); v[2] = cmul(v[2], w2); v[3] = cmul(v[3], w3);
-                if constexpr (R == 8) {
-                    const cplx<T> w4 = twiddle<T, DIR>(tws, lgtw, (4 * k) << tsh);
-                    v[4] = cmul(v[4], w4);
-                    v[5] = cmul(v[5], cmul(w4, w1));
-                    v[6] = cmul(v[6], cmul(w4, w2));
-                    v[7] = cmul(v[7], cmul(w4, w3));
-                }
+            // radix-8 stages only (the radix-2/4 stage, if any, is the first one: NS = 1)
+            cplx<T> w1 = tws[stab_off(LGN, LGS) + k];
+            if (DIR > 0) w1.y = -w1.y;
+            const cplx<T> w2 = cmul(w1, w1);
+            const cplx<T> w3 = cmul(w2, w1);
+            v[1] = cmul(v[1], w1); v[2] = cmul(v[2], w2); v[3] = cmul(v[3], w3);
+            if constexpr (R == 8) {
+                const cplx<T> w4 = cmul(w2, w2);
+                v[4] = cmul(v[4], w4);
+                v[5] = cmul(v[5], cmul(w4, w1));
+                v[6] = cmul(v[6], cmul(w4, w2));
+                v[7] = cmul(v[7], cmul(w4, w3));
             }
         }
         if constexpr (R == 2) dft2<T, DIR>(v);
@@ -223,7 +219,7 @@ fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, in
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
     cplx<T> *b1 = b0 + sp_size((size_t)(CB >> 1) * Mx);   // CB/2 complex transforms
     cplx<T> *tws = b1 + sp_size((size_t)(CB >> 1) * Mx);
-    stage_twiddles(tws, tw, lgtw);
+    stage_stab(tws, tw, lgtw);
     // two real columns per complex transform (NT = CB/2 transforms): z = x_a + i·x_b,
     // X_a[f] = (Z[f] + conj Z[-f]) / 2,  X_b[f] = (Z[f] - conj Z[-f]) / (2i)
     const int NT = CB >> 1;
@@ -279,7 +275,7 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
     cplx<T> *b1 = b0 + sp_size((size_t)RB * My);
     cplx<T> *tws = b1 + sp_size((size_t)RB * My);
-    stage_twiddles(tws, tw, lgtw);
+    stage_stab(tws, tw, lgtw);
     // grid (k, Hx/RB): the k CTAs that multiply by the same X̂ rows run back to back, so
     // X̂ stays in L2 while the (much larger) A stream passes (c5: 4.3 GB of X̂ re-reads from
     // DRAM with the transposed grid order, ncu)
@@ -288,7 +284,7 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
     const int nrow = min(RB, Hx - fx0);
     // X̂ rows of this CTA: fetched asynchronously into shared memory at the start so their L2
     // latency overlaps the forward transforms (ncu: the multiply waited on these loads)
-    cplx<T> *xs = reinterpret_cast<cplx<T> *>((reinterpret_cast<uintptr_t>(tws + tw_count(lgtw)) + 15) & ~uintptr_t(15));
+    cplx<T> *xs = reinterpret_cast<cplx<T> *>((reinterpret_cast<uintptr_t>(tws + stab_count(lgtw)) + 15) & ~uintptr_t(15));
     if (mode == 0) {
         constexpr int PER = 16 / sizeof(cplx<T>);            // complex values per 16-B copy
         const uint32_t xs_u = (uint32_t)__cvta_generic_to_shared(xs);
@@ -347,7 +343,7 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
     cplx<T> *v0 = u1 + bs;
     cplx<T> *v1 = v0 + bs;
     cplx<T> *tws = v1 + bs;
-    stage_twiddles(tws, tw, lgtw);
+    stage_stab(tws, tw, lgtw);
     const int fx0 = blockIdx.x * RB;
     const int g = blockIdx.y;
     const int nrow = min(RB, Hx - fx0);
@@ -397,7 +393,7 @@ fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int o
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
     cplx<T> *b1 = b0 + sp_size((size_t)(CB >> 1) * Mx);   // CB/2 complex transforms
     cplx<T> *tws = b1 + sp_size((size_t)(CB >> 1) * Mx);
-    stage_twiddles(tws, tw, lgtw);
+    stage_stab(tws, tw, lgtw);
     // two output columns per complex inverse transform (NT = CB/2): Z = Y_a + i·Y_b over the
     // full spectrum (Hermitian completion of each half spectrum), Re z = y_a, Im z = y_b
     const int NT = CB >> 1;
@@ -454,7 +450,7 @@ fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int o
 struct FftOperator {
     int lgx = 0, lgy = 0, Mx = 0, My = 0, Hx = 0;
     int lgtw = 0;
-    DevBuf tw;        // cplx[2^lgtw]: exp(−2πi t / 2^lgtw), fp64-accurate
+    DevBuf stab_x, stab_y;   // per-stage twiddle tables for 2^lgx / 2^lgy point transforms
     DevBuf Xh;        // cplx[Hx][My]: DFT2 of the image
     DevBuf gk;        // cplx[Hx][My]: unnormalised inverse y-DFT of each X̂ row (small My: folded pass B)
     DevBuf bufA, bufB;
@@ -491,20 +487,20 @@ static int batch_for(int lg, int target) {
 }
 
 template <typename T>
-static size_t smem_ab(int lg, int nb, int lgtw) {
-    return sizeof(cplx<T>) * (2 * sp_size((size_t)nb << lg) + tw_count(lgtw));
+static size_t smem_ab(int lg, int nb, int /*unused*/) {
+    return sizeof(cplx<T>) * (2 * sp_size((size_t)nb << lg) + stab_count(lg));
 }
 
 template <typename T>
 static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int bx, int by, int k, const int *jsel,
                    const double *scale, cplx<T> *A, cudaStream_t st) {
     const int CB = 2 * batch_for(f.lgx, 2048);   // real columns (two per complex transform)
-    const size_t smem = smem_ab<T>(f.lgx, CB / 2, f.lgtw);
+    const size_t smem = smem_ab<T>(f.lgx, CB / 2, 0);
     const int nth = threads_for(f.lgx, CB / 2, cdiv(by, CB) * k);
     auto kern = nth <= 256 ? fft_pass_a<T, 256> : fft_pass_a<T, 512>;
     set_max_smem(kern);
     kern<<<dim3((unsigned)cdiv(by, CB), k), nth, smem, st>>>(in, ld, map, bx, by, k, jsel, scale, f.lgx, CB, A,
-                                                                        f.tw.as<cplx<T>>(), f.lgtw);
+                                                                        f.stab_x.as<cplx<T>>(), f.lgx);
     after_launch("fft_pass_a");
 }
 
@@ -512,13 +508,13 @@ template <typename T>
 static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode, cplx<T> *B, int ny_out, cudaStream_t st) {
     const int RB = batch_for(f.lgy, 2048);
     // + the CTA's X̂ rows (prefetched, mode 0)
-    const size_t smem = smem_ab<T>(f.lgy, RB, f.lgtw) + sizeof(cplx<T>) * ((size_t)RB << f.lgy) + 16;
+    const size_t smem = smem_ab<T>(f.lgy, RB, 0) + sizeof(cplx<T>) * ((size_t)RB << f.lgy) + 16;
     const int nth = threads_for(f.lgy, RB, cdiv(f.Hx, RB) * k);
     auto kern = nth <= 256 ? fft_pass_b<T, 256> : fft_pass_b<T, 512>;
     set_max_smem(kern);
     kern<<<dim3(k, (unsigned)cdiv(f.Hx, RB)), nth, smem, st>>>(A, ny_in, f.Hx, f.lgy, RB,
                                                                          f.Xh.as<cplx<T>>(), mode, B, ny_out,
-                                                                         f.tw.as<cplx<T>>(), f.lgtw);
+                                                                         f.stab_y.as<cplx<T>>(), f.lgy);
     after_launch("fft_pass_b");
 }
 
@@ -526,13 +522,13 @@ template <typename T>
 static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *out, int64_t ldo, const int *omap,
                    const int *w, int64_t stride, cudaStream_t st, const cplx<T> *Afu = nullptr, int ny_in = 0) {
     const int CB = 2 * batch_for(f.lgx, 2048);   // output columns (two per complex transform)
-    const size_t smem = smem_ab<T>(f.lgx, CB / 2, f.lgtw);
+    const size_t smem = smem_ab<T>(f.lgx, CB / 2, 0);
     const int nth = threads_for(f.lgx, CB / 2, cdiv(oy, CB) * k);
     auto kern = nth <= 256 ? fft_pass_c<T, 256> : fft_pass_c<T, 512>;
     set_max_smem(kern);
     const T inv = (T)(1.0 / ((double)f.Mx * (double)f.My));
     kern<<<dim3((unsigned)cdiv(oy, CB), k), nth, smem, st>>>(B, oy, f.Hx, f.lgx, CB, ox, inv, out, ldo, omap,
-                                                                       w, stride, f.tw.as<cplx<T>>(), f.lgtw, Afu,
+                                                                       w, stride, f.stab_x.as<cplx<T>>(), f.lgx, Afu,
                                                                        ny_in, Afu ? f.gk.as<cplx<T>>() : nullptr, f.lgy);
     after_launch("fft_pass_c");
 }
@@ -567,17 +563,24 @@ static void build_impl(PlanImpl &p) {
     f.lgx = ilog2_ceil(p.nx); f.lgy = ilog2_ceil(p.ny);
     f.Mx = 1 << f.lgx; f.My = 1 << f.lgy; f.Hx = f.Mx / 2 + 1;
     f.lgtw = std::max(f.lgx, f.lgy);
-    {
-        const size_t nt = (size_t)1 << f.lgtw;
-        std::vector<cplx<T>> h(nt);
-        for (size_t t = 0; t < nt; ++t) {
-            const double a = -2.0 * M_PI * (double)t / (double)nt;
-            h[t] = cplx<T>{(T)std::cos(a), (T)std::sin(a)};
+    // per-stage twiddle tables (see stab_off): stage l (radix 8, span 2^l > 1), w1[k] = exp(−2πi k / 2^(l+3))
+    auto build_stab = [&](int lg, DevBuf &buf) {
+        std::vector<cplx<T>> h(std::max<size_t>(stab_count(lg), 1));
+        size_t o = 0;
+        for (int l = lg % 3; l < lg; l += 3) {
+            if (l == 0) continue;
+            const int ns = 1 << l;
+            for (int k = 0; k < ns; ++k) {
+                const double a = -2.0 * M_PI * (double)k / (double)(8 * ns);
+                h[o++] = cplx<T>{(T)std::cos(a), (T)std::sin(a)};
+            }
         }
-        f.tw.alloc(sizeof(cplx<T>) * nt, p.st);
-        SSA_CUDA(cudaMemcpyAsync(f.tw.p, h.data(), sizeof(cplx<T>) * nt, cudaMemcpyHostToDevice, p.st));
+        buf.alloc(sizeof(cplx<T>) * h.size(), p.st);
+        SSA_CUDA(cudaMemcpyAsync(buf.p, h.data(), sizeof(cplx<T>) * h.size(), cudaMemcpyHostToDevice, p.st));
         SSA_CUDA(cudaStreamSynchronize(p.st));
-    }
+    };
+    build_stab(f.lgx, f.stab_x);
+    build_stab(f.lgy, f.stab_y);
     f.Xh.alloc(sizeof(cplx<T>) * (size_t)f.Hx * f.My, p.st);
     DevBuf tmp;
     tmp.alloc(sizeof(cplx<T>) * (size_t)f.Hx * p.ny, p.st);
@@ -649,13 +652,13 @@ void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, co
     pass_a<T>(f, V, p.K, p.full_k ? nullptr : p.kmap.as<int>(), p.kx, p.ky, nu, jsel.as<int>(), nullptr,
               AV.as<cplx<T>>(), p.st);
     const int RB = batch_for(f.lgy, 2048);
-    const size_t smem = sizeof(cplx<T>) * (5 * sp_size((size_t)RB << f.lgy) + tw_count(f.lgtw));
+    const size_t smem = sizeof(cplx<T>) * (5 * sp_size((size_t)RB << f.lgy) + stab_count(f.lgy));
     const int nth = threads_for(f.lgy, RB, cdiv(f.Hx, RB) * ng);
     auto kern = nth <= 256 ? fft_pass_b_conv<T, 256> : fft_pass_b_conv<T, 512>;
     set_max_smem(kern);
     kern<<<dim3((unsigned)cdiv(f.Hx, RB), ng), nth, smem, p.st>>>(
         AU.as<cplx<T>>(), p.ly, AV.as<cplx<T>>(), p.ky, grp_off_dev, grp_idx_dev, slot_dev, f.Hx, f.lgy, RB,
-        B.as<cplx<T>>(), p.ny, f.tw.as<cplx<T>>(), f.lgtw);
+        B.as<cplx<T>>(), p.ny, f.stab_y.as<cplx<T>>(), f.lgy);
     after_launch("fft_pass_b_conv");
     pass_c<T>(f, B.as<cplx<T>>(), p.ny, ng, p.nx, out, p.nx, nullptr, p.weights.as<int>(), (int64_t)p.nx * p.ny, p.st);
     SSA_CUDA(cudaStreamSynchronize(p.st));
