@@ -247,10 +247,11 @@ fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, in
     }
     __syncthreads();
     cplx<T> *res = fft_batch<T, -1>(b0, b1, lgx, NT, tws, lgtw);
+    const int lcb = __ffs(CB) - 1;
     // transposed write: consecutive threads -> consecutive columns
     #pragma unroll 8
     for (int idx = threadIdx.x; idx < Hx * CB; idx += blockDim.x) {
-        const int fx = idx / CB, c = idx - fx * CB;
+        const int fx = idx >> lcb, c = idx & (CB - 1);   // CB is a power of two
         if (c >= ncol) continue;
         const int t = c >> 1;
         const cplx<T> z = res[sp(t * Mx + fx)], zm = res[sp(t * Mx + ((Mx - fx) & (Mx - 1)))];
@@ -396,13 +397,13 @@ fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int o
     stage_stab(tws, tw, lgtw);
     // two output columns per complex inverse transform (NT = CB/2): Z = Y_a + i·Y_b over the
     // full spectrum (Hermitian completion of each half spectrum), Re z = y_a, Im z = y_b
-    const int NT = CB >> 1;
+    const int NT = CB >> 1, lnt = __ffs(NT) - 1;
     const int y0 = blockIdx.x * CB;
     const int j = blockIdx.y;
     const int ncol = min(CB, oy - y0);
     #pragma unroll 8
     for (int idx = threadIdx.x; idx < Hx * NT; idx += blockDim.x) {
-        const int fx = idx / NT, t = idx - fx * NT;
+        const int fx = idx >> lnt, t = idx & (NT - 1);   // NT is a power of two
         cplx<T> ya{T(0), T(0)}, yb{T(0), T(0)};
         if (Afu) {
             // pass B folded in (few rows on both sides, MSSA): the y-correlation with the image as
