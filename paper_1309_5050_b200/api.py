@@ -206,10 +206,17 @@ class Plan:
             idx = np.zeros(1, dtype=np.int32)
         return off, idx
 
-    def reconstruct(self, groups, add_rest=False, device=False):
-        """List of (Nx, Ny) arrays X̃_g (NaN off 𝔑′); with add_rest a final residual array."""
+    def reconstruct(self, groups, add_rest=False, device=False, out=None):
+        """List of (Nx, Ny) arrays X̃_g (NaN off 𝔑′); with add_rest a final residual array.
+        Host results go to `out` when given: a C-contiguous (n, Ny, Nx) array of the plan's dtype
+        (e.g. the numpy view of a pinned torch tensor), otherwise to a new array."""
         off, idx = self._csr(groups)
         n = len(groups) + (1 if add_rest else 0)
+        if out is not None and not device:
+            assert out.shape == (n, self.ny, self.nx) and out.dtype == self._np_dtype and out.flags["C_CONTIGUOUS"]
+            lib.check(self._L.ssa_reconstruct(self._h, off.ctypes.data, idx.ctypes.data, len(groups),
+                                              int(add_rest), out.ctypes.data, 0))
+            return [out[g].T for g in range(n)]
         if device:
             torch = _torch()
             td = torch.float64 if self.dtype == "f64" else torch.float32
