@@ -38,8 +38,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-__device__ __forceinline__ void trace(int role, int i) {
-    if (g_gram_trace && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) g_gram_trace[role * 64 + i] = gtimer();
+// (the pointer is read once per kernel into `tr`: a global load per call sat on the issue path)
+__device__ __forceinline__ void trace(unsigned long long *tr, int role, int i) {
+    if (tr && blockIdx.x == 0 && blockIdx.y == 0 && i < 64 && role < 8) tr[role * 64 + i] = gtimer();
 }
 
 namespace tallg {
@@ -47,7 +48,7 @@ constexpr int R = 32;                 // rows per chunk (128 B per column: one s
 constexpr int KS = R / 8;             // UMMA k-steps per chunk
 constexpr int NTHR = 512;            // warps 0 TMA, 1 MMA, 2-7 convert, 8-15 drain
 
-template <int NM, int NN, int BA = 128>
+template <int NM, int NN, int BA = 128, int KA = KS>
 struct Cfg {
     static constexpr int a_bytes = NM * BA * 128;           // raw/hi A tiles (NM x BA rows of 128 B)
     static constexpr int b_bytes = NN * 128;
@@ -56,13 +57,13 @@ struct Cfg {
     static constexpr int STAGES = (220 * 1024) / stage > 8 ? 8 : (220 * 1024) / stage;
     static constexpr int off_bar = STAGES * stage;
     static constexpr int smem = off_bar + 320 + 1024;       // barriers + alignment slack
-    static constexpr int acc_cols = NM * KS * NN;           // one chunk's accumulators
+    static constexpr int acc_cols = NM * KA * NN;           // one chunk's accumulators (KA per M-tile)
     static constexpr int ACCB = 512 / acc_cols >= 4 ? 4 : 2; // accumulator buffers (MMA runs ACCB chunks ahead)
     static constexpr int tmem_cols = ACCB * acc_cols;
 };
 }  // namespace tallg
 
-template <int NM, int NN, int BA>
+template <int NM, int NN, int BA, int KA>
 __global__ void __launch_bounds__(tallg::NTHR, 1)
 gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
                int n1, int n2, int self_b, double *__restrict__ partials) {
@@ -71,9 +72,10 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // only feed discarded accumulator rows); self_b: B is the first n2 columns of A (AᵀA): no B load,
     // the B operand descriptors point into the A tile
     using namespace tc;
-    using C = tallg::Cfg<NM, NN, BA>;
-    constexpr int S = C::STAGES, KS = tallg::KS;
-    static_assert(C::tmem_cols == 256 || C::tmem_cols == 512, "TMEM allocation must be 256 or 512 columns");
+    using C = tallg::Cfg<NM, NN, BA, KA>;
+    constexpr int S = C::STAGES, KS = tallg::KS, KG = KS / KA;   // KG k-steps per accumulator
+    static_assert(C::tmem_cols >= 32 && C::tmem_cols <= 512 && (C::tmem_cols & (C::tmem_cols - 1)) == 0,
+                  "TMEM allocation must be a power of two in [32, 512] columns");
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -87,6 +89,7 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     auto acce = [&](int b) { return bar0 + 8u * (28 + b); };      // accumulators drained   [4]
     constexpr int AB = C::ACCB;
 
+    unsigned long long *const tr = g_gram_trace;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t nchunks = (M + tallg::R - 1) / tallg::R;
     const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
@@ -135,7 +138,7 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
                 for (int mt = 0; mt < NM; ++mt) tma_load_2d_true(a_hi(s) + mt * 16384, &tmA, r0, col0 + 128 * mt, full(s));
                 if (!self_b) tma_load_2d_true(b_hi(s), &tmB, r0, 0, full(s));
-                trace(0, i);
+                trace(tr, 0, i);
             }
         }
     } else if (warp == 1) {
@@ -154,17 +157,17 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     const uint64_t dBl = make_desc((self_b ? a_lo(s) : b_lo(s)) + kk * 32);
 #pragma unroll
                     for (int mt = 0; mt < NM; ++mt) {
-                        const uint32_t d = dbase + (uint32_t)((mt * KS + kk) * NN);
+                        const uint32_t d = dbase + (uint32_t)((mt * KA + kk / KG) * NN);
                         const uint64_t dAh = make_desc(a_hi(s) + mt * 16384 + kk * 32);
                         const uint64_t dAl = make_desc(a_lo(s) + mt * 16384 + kk * 32);
-                        mma_tf32(d, dAl, dBh, idesc, 0u);
+                        mma_tf32(d, dAl, dBh, idesc, kk % KG ? 1u : 0u);
                         mma_tf32(d, dAh, dBl, idesc, 1u);
                         mma_tf32(d, dAh, dBh, idesc, 1u);
                     }
                 }
                 mma_commit(empty(s));
                 mma_commit(accf(b));
-                trace(2, i);
+                trace(tr, 2, i);
             }
         }
     } else if (warp >= 2 && warp < 8) {
@@ -173,7 +176,7 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int i = 0; i < nmy; ++i) {
             const int s = i % S;
             mbar_wait(full(s), (i / S) & 1);
-            if (warp == 2 && lane == 0) trace(4, i);
+            if (warp == 2 && lane == 0) trace(tr, 4, i);
             float4 *ah = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage);
             float4 *al = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + C::a_bytes);
             float4 *bh = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + 2 * C::a_bytes);
@@ -201,7 +204,7 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv(s)) : "memory");
-            if (warp == 2 && lane == 0) trace(1, i);
+            if (warp == 2 && lane == 0) trace(tr, 1, i);
         }
     } else if (warp >= 8) {
         // ---------------- drain (warps 8-15) ----------------
@@ -224,17 +227,17 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
                 for (int hv = 0; hv < 2; ++hv) {
                     // the KS k-step partials of 16 columns: all loads in flight, one wait
-                    uint32_t r[KS][16];
+                    uint32_t r[KA][16];
 #pragma unroll
-                    for (int kk = 0; kk < KS; ++kk)
-                        tmem_ld16_nowait(lane_base + (uint32_t)(b * C::acc_cols + (mt_u * KS + kk) * NN + n0_u + 16 * hv), r[kk]);
+                    for (int kk = 0; kk < KA; ++kk)
+                        tmem_ld16_nowait(lane_base + (uint32_t)(b * C::acc_cols + (mt_u * KA + kk) * NN + n0_u + 16 * hv), r[kk]);
                     tmem_wait_ld();
                     float sum[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         float t = 0.f;
 #pragma unroll
-                        for (int kk = 0; kk < KS; ++kk) t += __uint_as_float(r[kk][j]);
+                        for (int kk = 0; kk < KA; ++kk) t += __uint_as_float(r[kk][j]);
                         sum[j] = t;
                     }
 #pragma unroll
@@ -250,7 +253,7 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
-            if (warp == 8 && lane == 0) trace(3, i);
+            if (warp == 8 && lane == 0) trace(tr, 3, i);
         }
         // ---- per-CTA partials in gram_reduce's layout: [64-column block][cta][64 x 64]
         if (has_unit) {
@@ -268,6 +271,287 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     __syncthreads();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::tmem_cols) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Gram v3 (default): A operand in tensor memory.  Thin-N MMAs (N = k <= 64) with both operands in
+// shared memory were bound by the shared-memory port and the chunk pipeline, not the tensor pipe:
+// per 8-row k-step the three 3xTF32 MMAs read A three times plus B, and the in-smem hi/lo split
+// read and wrote every element once more (v1 timeline: ~1 µs per 16 KB chunk with the TMA idle).
+// Here a stage is RC 32-row sub-chunks; converter warps 4-7 (one per TMEM lane quarter) read a
+// landed raw A row (one A column = one TMEM lane), split it and tcgen05.st hi / lo into TMEM (the
+// A-from-TMEM `.kind::tf32` MMA: row m -> lane m, k -> column); then warps 2-7 split the thin B tile
+// into shared memory, and the raw slot is released at once (the ring of raw slots takes the rest
+// of shared memory).  Per accumulator (KG k-steps) the small terms A_lo·B_hi, A_hi·B_lo are
+// accumulated first and the exact A_hi·B_hi products last: each truncating accumulation at full
+// magnitude adds one large term.  TMEM: accumulators in columns [0, 256), A hi | lo buffers in
+// [256, 512).
+// ---------------------------------------------------------------------------
+namespace tallg3 {
+constexpr int MAXR = 24;
+constexpr int SMEM = 226 * 1024;        // 227 KB opt-in − 1 KB reserved per CTA
+template <int NM, int NN, int BA, int RC, int KG>
+struct Cfg {
+    static constexpr int OPB = 2;                           // operand buffers (TMEM A + shared B)
+    static constexpr int KS = 4 * RC;                       // 8-row k-steps per stage
+    static constexpr int KA = KS / KG;                      // accumulators per M-tile per stage
+    static constexpr int a_raw = NM * BA * 128;             // A bytes per 32-row sub-chunk
+    static constexpr int b_raw = NN * 128;
+    static constexpr int bop = RC * 2 * b_raw;              // B [sub-chunk][hi | lo]
+    static constexpr int acols = 64 * RC;                   // TMEM columns of one M-tile's A (hi | lo)
+    static constexpr int off_raw = OPB * bop;
+    static constexpr int off_bar = SMEM - 2048;             // 1 KB barriers + 1 KB alignment slack
+    static constexpr int ring = off_bar - off_raw;
+    static constexpr int acc_cols = NM * KA * NN;
+    static constexpr int ACCB = 256 / acc_cols >= 4 ? 4 : 256 / acc_cols;
+    static_assert(KS % KG == 0, "KG must divide the k-steps of a stage");
+    static_assert(ACCB >= 2, "at least two accumulator buffers");
+    static_assert(OPB * NM * acols <= 256, "A buffers exceed TMEM columns [256, 512)");
+};
+}  // namespace tallg3
+
+template <int NM, int NN, int BA, int RC, int KG>
+__global__ void __launch_bounds__(tallg::NTHR, 1)
+gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
+                int n1, int n2, int self_b, double *__restrict__ partials) {
+    using namespace tc;
+    using C = tallg3::Cfg<NM, NN, BA, RC, KG>;
+    constexpr int KS = C::KS, KA = C::KA, OPB = C::OPB, AB = C::ACCB;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::off_bar);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 64);
+    const uint32_t bar0 = smem_u32(bars);
+    auto full = [&](int r) { return bar0 + 8u * r; };             // raw stage landed        [24]
+    auto rawe = [&](int r) { return bar0 + 8u * (24 + r); };      // raw slot consumed       [24]
+    auto conv = [&](int o) { return bar0 + 8u * (48 + o); };      // operands split          [2]
+    auto ope = [&](int o) { return bar0 + 8u * (52 + o); };       // operand MMAs done       [2]
+    auto accf = [&](int b) { return bar0 + 8u * (56 + b); };      // accumulators ready      [4]
+    auto acce = [&](int b) { return bar0 + 8u * (60 + b); };      // accumulators drained    [4]
+
+    const int unit = C::a_raw + (self_b ? 0 : C::b_raw);          // raw bytes per sub-chunk
+    const int raw_bytes = RC * unit;
+    const int RS = min(tallg3::MAXR, C::ring / raw_bytes);
+    unsigned long long *const tr = g_gram_trace;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t nchunks = (M + 32 * RC - 1) / (32 * RC);
+    const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+    const int64_t c0 = (int64_t)blockIdx.x * per;
+    const int nmy = (int)max((int64_t)0, min(per, nchunks - c0));
+    const int col0 = (int)blockIdx.y * NM * 128;
+
+    if (tid == 0) {
+        for (int r = 0; r < RS; ++r) {
+            mbar_init(full(r), 1);
+            mbar_init(rawe(r), 6);
+        }
+        for (int o = 0; o < OPB; ++o) {
+            mbar_init(conv(o), 6);
+            mbar_init(ope(o), 1);
+        }
+        for (int b = 0; b < AB; ++b) {
+            mbar_init(accf(b), 1);
+            mbar_init(acce(b), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sm_u = smem_u32(smem);
+    auto b_hi = [&](int o, int rc) { return sm_u + (uint32_t)(o * C::bop + rc * 2 * C::b_raw); };
+    auto a_col = [&](int o, int mt) { return (uint32_t)(256 + (o * NM + mt) * C::acols); };   // hi; lo at +32·RC
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer: raw ring ----------------
+            for (int i = 0; i < nmy; ++i) {
+                const int r = i % RS;
+                if (i >= RS) mbar_wait(rawe(r), ((i / RS) - 1) & 1);
+                const uint32_t dst = sm_u + (uint32_t)(C::off_raw + r * raw_bytes);
+                mbar_expect_tx(full(r), raw_bytes);
+#pragma unroll
+                for (int rc = 0; rc < RC; ++rc) {
+                    const int r0 = (int)((c0 + i) * 32 * RC + 32 * rc);
+#pragma unroll
+                    for (int mt = 0; mt < NM; ++mt)
+                        tma_load_2d_true(dst + rc * unit + mt * BA * 128, &tmA, r0, col0 + 128 * mt, full(r));
+                    if (!self_b) tma_load_2d_true(dst + rc * unit + C::a_raw, &tmB, r0, 0, full(r));
+                }
+                trace(tr, 0, i);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer ----------------
+            constexpr uint32_t idesc = make_idesc(128, NN);
+            for (int i = 0; i < nmy; ++i) {
+                const int o = i % OPB, b = i % AB;
+                mbar_wait(conv(o), (i / OPB) & 1);
+                if (i >= AB) mbar_wait(acce(b), ((i / AB) - 1) & 1);
+                tc_fence_after();
+                trace(tr, 6, i);
+                const uint32_t dbase = tmem + (uint32_t)(b * C::acc_cols);
+                const uint64_t bh0 = make_desc(b_hi(o, 0));
+                constexpr uint64_t b_lo_step = (uint64_t)(C::b_raw >> 4), rc_step = (uint64_t)((2 * C::b_raw) >> 4);
+#pragma unroll
+                for (int g = 0; g < KA; ++g) {
+#pragma unroll
+                    for (int mt = 0; mt < NM; ++mt) {
+                        const uint32_t d = dbase + (uint32_t)((mt * KA + g) * NN);
+                        const uint32_t ah = tmem + a_col(o, mt), al = ah + 32 * RC;
+#pragma unroll
+                        for (int q = 0; q < KG; ++q) {
+                            const int kk = g * KG + q;
+                            const uint64_t bh = bh0 + (uint64_t)(kk >> 2) * rc_step + (uint64_t)(2 * (kk & 3));
+                            mma_tf32_ts(d, al + 8 * kk, bh, idesc, q ? 1u : 0u);
+                            mma_tf32_ts(d, ah + 8 * kk, bh + b_lo_step, idesc, 1u);
+                        }
+#pragma unroll
+                        for (int q = 0; q < KG; ++q) {
+                            const int kk = g * KG + q;
+                            const uint64_t bh = bh0 + (uint64_t)(kk >> 2) * rc_step + (uint64_t)(2 * (kk & 3));
+                            mma_tf32_ts(d, ah + 8 * kk, bh, idesc, 1u);
+                        }
+                    }
+                }
+                mma_commit(ope(o));
+                mma_commit(accf(b));
+                trace(tr, 2, i);
+            }
+        }
+    } else if (warp < 8) {
+        // ---------------- converters, warps 2-7 ----------------
+        // warps 4-7 first move the A rows of their TMEM lane quarter (one A column per lane) into TMEM
+        // as hi / lo; then all six warps split the thin B tile (or A's first NN rows) into shared memory
+        const int q = warp & 3, m = 32 * q + lane;
+        const bool a_warp = warp >= 4 && 32 * q < BA;
+        const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+        const int ct = tid - 64;
+        constexpr int nb4 = C::b_raw / 16;
+        for (int i = 0; i < nmy; ++i) {
+            const int r = i % RS, o = i % OPB;
+            mbar_wait(full(r), (i / RS) & 1);
+            if (i >= OPB) mbar_wait(ope(o), ((i / OPB) - 1) & 1);
+            tc_fence_after();
+            if (warp == 4 && lane == 0) trace(tr, 4, i);
+            const unsigned char *rawp = smem + C::off_raw + (size_t)r * raw_bytes;
+            if (a_warp) {
+#pragma unroll
+                for (int rc = 0; rc < RC; ++rc) {
+#pragma unroll
+                    for (int mt = 0; mt < NM; ++mt) {
+                        const unsigned char *row = rawp + rc * unit + mt * BA * 128 + m * 128;
+                        uint32_t hi[32], lo[32];
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            const float4 x = *reinterpret_cast<const float4 *>(row + ((c ^ (m & 7)) << 4));
+                            const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t h = tf32_rna(xs[u]);
+                                hi[4 * c + u] = h;
+                                lo[4 * c + u] = __float_as_uint(xs[u] - __uint_as_float(h));
+                            }
+                        }
+                        tmem_st32(tmem + lane_off + a_col(o, mt) + 32 * rc, hi);
+                        tmem_st32(tmem + lane_off + a_col(o, mt) + 32 * RC + 32 * rc, lo);
+                    }
+                }
+                tmem_wait_st();
+            }
+            if (warp == 4 && lane == 0) trace(tr, 1, i);
+#pragma unroll
+            for (int rc = 0; rc < RC; ++rc) {
+                const float4 *src = reinterpret_cast<const float4 *>(rawp + rc * unit + (self_b ? 0 : C::a_raw));
+                float4 *dh = reinterpret_cast<float4 *>(smem + (size_t)o * C::bop + rc * 2 * C::b_raw);
+#pragma unroll 2
+                for (int e = ct; e < nb4; e += 192) {
+                    const float4 x = src[e];
+                    float4 hh, l;
+                    hh.x = __uint_as_float(tf32_rna(x.x)); l.x = x.x - hh.x;
+                    hh.y = __uint_as_float(tf32_rna(x.y)); l.y = x.y - hh.y;
+                    hh.z = __uint_as_float(tf32_rna(x.z)); l.z = x.z - hh.z;
+                    hh.w = __uint_as_float(tf32_rna(x.w)); l.w = x.w - hh.w;
+                    dh[e] = hh;
+                    dh[e + nb4] = l;
+                }
+            }
+            fence_proxy_async();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rawe(r)) : "memory");
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv(o)) : "memory");
+            }
+            if (warp == 2 && lane == 0) trace(tr, 5, i);
+            if (warp == 7 && lane == 0) trace(tr, 7, i);
+        }
+    } else {
+        // ---------------- drain (warps 8-15): KA accumulators summed in fp32, Kahan across stages ----------------
+        constexpr int UNITS = NM * NN / 32;
+        const int h = (warp - 8) >> 2;
+        const int mt_u = (NM == 2) ? h : 0, n0_u = (NM == 2) ? 0 : 32 * h;
+        const bool has_unit = h < UNITS;
+        float ks[32], kc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) { ks[j] = 0.f; kc[j] = 0.f; }
+        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        for (int i = 0; i < nmy; ++i) {
+            const int b = i % AB;
+            mbar_wait(accf(b), (i / AB) & 1);
+            tc_fence_after();
+            if (has_unit) {
+#pragma unroll
+                for (int hv = 0; hv < 2; ++hv) {
+                    uint32_t rr[KA][16];
+#pragma unroll
+                    for (int g = 0; g < KA; ++g)
+                        tmem_ld16_nowait(lane_base + (uint32_t)(b * C::acc_cols + (mt_u * KA + g) * NN + n0_u + 16 * hv), rr[g]);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        float t = 0.f;
+#pragma unroll
+                        for (int g = 0; g < KA; ++g) t += __uint_as_float(rr[g][j]);
+                        const int qq = 16 * hv + j;
+                        const float y = t - kc[qq];
+                        const float u = ks[qq] + y;
+                        kc[qq] = (u - ks[qq]) - y;
+                        ks[qq] = u;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
+            if (warp == 8 && lane == 0) trace(tr, 3, i);
+        }
+        if (has_unit) {
+            const int nparts = gridDim.x;
+            const int a = col0 + 128 * mt_u + (warp & 3) * 32 + lane;
+            if (a < n1) {
+                double *base = partials + ((int64_t)(a / 64) * nparts + blockIdx.x) * 4096 + (a % 64);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (n0_u + j < n2) base[64 * (n0_u + j)] = (double)ks[j] - (double)kc[j];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -516,18 +800,49 @@ static const CUtensorMap &tall_map(const float *base, int64_t M, int ncols, int6
                                   p256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
 }
 
-template <int NM, int NN, int BA>
-static void launch_gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2,
-                           double *partials, int ctas, cudaStream_t st) {
-    using C = tallg::Cfg<NM, NN, BA>;
+template <int NM, int NN, int BA, int KA>
+static void launch_gram_tc_ka(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2,
+                              double *partials, int ctas, cudaStream_t st) {
+    using C = tallg::Cfg<NM, NN, BA, KA>;
     const int self_b = (B == A && ldb == lda && n2 <= n1 && NN <= BA && NM == 1) ? 1 : 0;
     const CUtensorMap &ma = tall_map(A, M, n1, lda, BA);
     const CUtensorMap &mb = tall_map(B, M, n2, ldb, NN);
-    auto kern = gram_tc_kernel<NM, NN, BA>;
+    auto kern = gram_tc_kernel<NM, NN, BA, KA>;
     set_max_smem(kern);
     const int gy = (int)cdiv(n1, NM * 128);
     kern<<<dim3(ctas, gy), tallg::NTHR, C::smem, st>>>(ma, mb, M, n1, n2, self_b, partials);
     after_launch("gram_tc");
+}
+
+template <int NM, int NN, int BA, int RC, int KG>
+static void launch_gram_tc3(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2,
+                            double *partials, int ctas, cudaStream_t st) {
+    const int self_b = (B == A && ldb == lda && n2 <= n1 && NN <= BA && NM == 1) ? 1 : 0;
+    const CUtensorMap &ma = tall_map(A, M, n1, lda, BA);
+    const CUtensorMap &mb = tall_map(B, M, n2, ldb, NN);
+    auto kern = gram_tc3_kernel<NM, NN, BA, RC, KG>;
+    set_max_smem(kern);
+    const int gy = (int)cdiv(n1, NM * 128);
+    kern<<<dim3(ctas, gy), tallg::NTHR, tallg3::SMEM, st>>>(ma, mb, M, n1, n2, self_b, partials);
+    after_launch("gram_tc3");
+}
+
+template <int NM, int NN, int BA>
+static void launch_gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2,
+                           double *partials, int ctas, cudaStream_t st) {
+    static const int ver = [] { const char *e = std::getenv("SSA_GRAM_V"); return e ? std::atoi(e) : 3; }();
+    if (ver == 3) {
+        // RC = 2 (64-row stages) where the TMEM A buffers allow it; KG = 4 k-steps per accumulator
+        static const int rc = [] { const char *e = std::getenv("SSA_GRAM_RC"); return e ? std::atoi(e) : 2; }();
+        if constexpr (NM == 1) {
+            if (rc == 2) launch_gram_tc3<NM, NN, BA, 2, 4>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+            else launch_gram_tc3<NM, NN, BA, 1, 2>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+        } else {
+            launch_gram_tc3<NM, NN, BA, 1, 2>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+        }
+        return;
+    }
+    launch_gram_tc_ka<NM, NN, BA, 4>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
 }
 
 // B tiles of all 32-column chunks, packed once per update as the exact shared-memory images
@@ -600,8 +915,8 @@ bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int
     if ((size_t)ctas * 4096 * sizeof(double) * (size_t)cdiv(n1, 64) > partial_bytes) return false;
     static unsigned long long *trace_buf = nullptr;
     if (std::getenv("SSA_GRAM_TRACE") && !trace_buf) {
-        SSA_CUDA(cudaMalloc(&trace_buf, 5 * 64 * 8));
-        SSA_CUDA(cudaMemset(trace_buf, 0, 5 * 64 * 8));
+        SSA_CUDA(cudaMalloc(&trace_buf, 8 * 64 * 8));
+        SSA_CUDA(cudaMemset(trace_buf, 0, 8 * 64 * 8));
         SSA_CUDA(cudaMemcpyToSymbol(g_gram_trace, &trace_buf, sizeof(trace_buf)));
     }
     // narrow blocks (n1 <= 64, e.g. the CholeskyQR Gram WᵀW): a 64-column A box, B read from the A tile
@@ -615,14 +930,15 @@ bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int
     }
     gram_reduce(partials, ctas, n1, n2, G, st);
     if (trace_buf) {
-        unsigned long long h[5 * 64];
+        unsigned long long h[8 * 64];
         SSA_CUDA(cudaStreamSynchronize(st));
         SSA_CUDA(cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost));
-        std::fprintf(stderr, "[gram trace] M=%lld n1=%d n2=%d (us from first TMA): chunk tma wait conv mma drain\n",
+        std::fprintf(stderr, "[gram trace] M=%lld n1=%d n2=%d (us from first TMA): chunk tma wait convA convB2 convB3 mma0 mma drain\n",
                      (long long)M, n1, n2);
+        auto us = [&](int k) { return h[k] ? (double)(h[k] - h[0]) * 1e-3 : -1.0; };
         for (int i = 0; i < 12; ++i)
-            std::fprintf(stderr, "  %2d %8.2f %8.2f %8.2f %8.2f %8.2f\n", i, (h[i] - h[0]) * 1e-3, (h[4 * 64 + i] - h[0]) * 1e-3,
-                         (h[64 + i] - h[0]) * 1e-3, (h[128 + i] - h[0]) * 1e-3, (h[192 + i] - h[0]) * 1e-3);
+            std::fprintf(stderr, "  %2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", i, us(i), us(4 * 64 + i), us(64 + i),
+                         us(5 * 64 + i), us(7 * 64 + i), us(6 * 64 + i), us(128 + i), us(192 + i));
         std::fprintf(stderr, "  last(42): tma %.2f drain %.2f\n", (h[42] - h[0]) * 1e-3, (h[192 + 42] - h[0]) * 1e-3);
     }
     return true;
