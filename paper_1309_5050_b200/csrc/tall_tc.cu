@@ -739,6 +739,210 @@ update_tc_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, cons
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cf::tmem_cols) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Update v2 (default): Out = beta·Out + A·(alpha·C) with the A operand in tensor memory.  The
+// contraction runs over A's columns, so an A row (one output row) is one TMEM lane: converter
+// warps 4-7 read the landed raw tile [32 columns][128 rows] (plain TMA box, no swizzle: a warp
+// reads 128 contiguous bytes per column), split it into tf32 hi / lo and tcgen05.st them as a
+// K-major TMEM operand; the raw slot is released at once (ring of up to 12 raw tiles).  The
+// pre-split coefficient tiles (B = (alpha·C)ᵀ chunk, K-major SW128 images) are bulk-copied from L2
+// by warp 2 into OPB slots that the MMAs release.  Per (tile, chunk) one fresh accumulator: the
+// small terms A_lo·B_hi, A_hi·B_lo of the 4 k-steps first, then the exact A_hi·B_hi products.
+// Drain / epilogue as in update_tc_kernel (fp32 register sums across chunks, RMW of the tile).
+// ---------------------------------------------------------------------------
+namespace tallu2 {
+constexpr int ROWS = 128, KC = 32, OPB = 4, NBUF = 4, MAXR = 12, NTHR = 512;
+constexpr int SMEM = 226 * 1024;
+template <int NN>
+struct Cfg {
+    static constexpr int a_raw = ROWS * KC * 4;             // 16 KB
+    static constexpr int b_bytes = 2 * NN * KC * 4;         // hi | lo
+    static constexpr int off_raw = OPB * b_bytes;
+    static constexpr int off_bar = SMEM - 2048;
+    static constexpr int RS = (off_bar - off_raw) / a_raw < MAXR ? (off_bar - off_raw) / a_raw : MAXR;
+    static_assert(NBUF * NN <= 256 && OPB * 64 <= 256, "TMEM budget");
+};
+}  // namespace tallu2
+
+template <int NN>
+__global__ void __launch_bounds__(tallu2::NTHR, 1)
+update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, const float *__restrict__ Bpk, int n,
+                  double beta, float *Out, int64_t ldo) {
+    using namespace tc;
+    using Cf = tallu2::Cfg<NN>;
+    constexpr int RS = Cf::RS, OPB = tallu2::OPB, NBUF = tallu2::NBUF, KC = tallu2::KC;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + Cf::off_bar);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 64);
+    const uint32_t bar0 = smem_u32(bars);
+    auto fulla = [&](int r) { return bar0 + 8u * r; };            // raw A landed          [12]
+    auto rawe = [&](int r) { return bar0 + 8u * (12 + r); };      // raw A converted       [12]
+    auto fullb = [&](int o) { return bar0 + 8u * (24 + o); };     // coefficients landed   [4]
+    auto conv = [&](int o) { return bar0 + 8u * (28 + o); };      // A in TMEM             [4]
+    auto ope = [&](int o) { return bar0 + 8u * (32 + o); };       // MMAs of slot o done   [4]
+    auto accf = [&](int b) { return bar0 + 8u * (36 + b); };      // accumulator ready     [4]
+    auto acce = [&](int b) { return bar0 + 8u * (40 + b); };      // accumulator drained   [4]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nchk = (m + KC - 1) / KC;
+    const int64_t ntiles = (M + tallu2::ROWS - 1) / tallu2::ROWS;
+    const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * per;
+    const int64_t mytiles = max((int64_t)0, min(per, ntiles - t0));
+    const int nitems = (int)(mytiles * nchk);
+
+    if (tid == 0) {
+        for (int r = 0; r < RS; ++r) {
+            mbar_init(fulla(r), 1);
+            mbar_init(rawe(r), 4);
+        }
+        for (int o = 0; o < OPB; ++o) {
+            mbar_init(fullb(o), 1);
+            mbar_init(conv(o), 4);
+            mbar_init(ope(o), 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(accf(b), 1);
+            mbar_init(acce(b), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sm_u = smem_u32(smem);
+    auto bslot = [&](int o) { return sm_u + (uint32_t)(o * Cf::b_bytes); };
+    auto raw = [&](int r) { return sm_u + (uint32_t)(Cf::off_raw + r * Cf::a_raw); };
+    auto a_col = [&](int o) { return (uint32_t)(256 + 64 * o); };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < nitems; ++i) {
+                const int r = i % RS;
+                if (i >= RS) mbar_wait(rawe(r), ((i / RS) - 1) & 1);
+                const int64_t tile = t0 + i / nchk;
+                mbar_expect_tx(fulla(r), Cf::a_raw);
+                tma_load_2d_true(raw(r), &tmA, (int)(tile * tallu2::ROWS), (i % nchk) * KC, fulla(r));
+            }
+        }
+    } else if (warp == 2) {
+        if (lane == 0) {
+            for (int i = 0; i < nitems; ++i) {
+                const int o = i % OPB;
+                if (i >= OPB) mbar_wait(ope(o), ((i / OPB) - 1) & 1);
+                mbar_expect_tx(fullb(o), Cf::b_bytes);
+                bulk_g2s(bslot(o), Bpk + (size_t)(i % nchk) * (Cf::b_bytes / 4), Cf::b_bytes, fullb(o));
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc(128, NN);
+            for (int i = 0; i < nitems; ++i) {
+                const int o = i % OPB, b = i % NBUF;
+                mbar_wait(conv(o), (i / OPB) & 1);
+                mbar_wait(fullb(o), (i / OPB) & 1);
+                if (i >= NBUF) mbar_wait(acce(b), ((i / NBUF) - 1) & 1);
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(b * NN);
+                const uint32_t ah = tmem + a_col(o), al = ah + 32;
+                const uint64_t bh = make_desc(bslot(o)), bl = bh + (uint64_t)((NN * KC * 4) >> 4);
+#pragma unroll
+                for (int q = 0; q < KC / 8; ++q) {
+                    mma_tf32_ts(d, al + 8 * q, bh + 2 * q, idesc, q > 0 ? 1u : 0u);
+                    mma_tf32_ts(d, ah + 8 * q, bl + 2 * q, idesc, 1u);
+                }
+#pragma unroll
+                for (int q = 0; q < KC / 8; ++q) mma_tf32_ts(d, ah + 8 * q, bh + 2 * q, idesc, 1u);
+                mma_commit(ope(o));
+                mma_commit(accf(b));
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ---------------- converters: row r of the tile -> TMEM lane r (hi | lo) ----------------
+        const int q = warp & 3, r_l = 32 * q + lane;
+        const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+        for (int i = 0; i < nitems; ++i) {
+            const int r = i % RS, o = i % OPB;
+            mbar_wait(fulla(r), (i / RS) & 1);
+            if (i >= OPB) mbar_wait(ope(o), ((i / OPB) - 1) & 1);
+            tc_fence_after();
+            const float *src = reinterpret_cast<const float *>(smem + Cf::off_raw + (size_t)r * Cf::a_raw) + r_l;
+            uint32_t hi[32], lo[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const float x = src[c * tallu2::ROWS];
+                const uint32_t h = tf32_rna(x);
+                hi[c] = h;
+                lo[c] = __float_as_uint(x - __uint_as_float(h));
+            }
+            tmem_st32(tmem + lane_off + a_col(o), hi);
+            tmem_st32(tmem + lane_off + a_col(o) + 32, lo);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rawe(r)) : "memory");
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv(o)) : "memory");
+            }
+        }
+    } else if (warp >= 8) {
+        // ---------------- drain + epilogue: warp w: rows 32·(w%4).., output columns 32·((w-8)/4).. ----------------
+        const int h = (warp - 8) >> 2;
+        const bool has = 32 * h < NN;
+        float acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(32 * h);
+        const float fb = (float)beta;
+        for (int i = 0; i < nitems; ++i) {
+            const int b = i % NBUF;
+            mbar_wait(accf(b), (i / NBUF) & 1);
+            tc_fence_after();
+            if (has) {
+                float v[32];
+                tmem_ld32(lane_base + (uint32_t)(b * NN), v);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[j] += v[j];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
+            if (i % nchk == nchk - 1) {
+                const int64_t row = (t0 + i / nchk) * tallu2::ROWS + (warp & 3) * 32 + lane;
+                if (has && row < M) {
+                    float old[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = 32 * h + j;
+                        old[j] = (beta != 0.0 && col < n) ? __ldcg(Out + row + ldo * (int64_t)col) : 0.f;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = 32 * h + j;
+                        if (col < n) Out[row + ldo * (int64_t)col] = fmaf(fb, old[j], acc[j]);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512) : "memory");
+}
+
 // ---- TMA streaming probe (ssa_bench_tall which = 4 / 5): one thread per CTA streams 3-D boxes
 // {32 rows, bc columns, rg row groups} of a column-major M x n block through 8 smem stages, no
 // consumer work — the achievable TMA read rate for the Gram's access pattern.
@@ -878,6 +1082,31 @@ static void launch_update_tc(const CUtensorMap &ma, int64_t M, int m, const doub
     after_launch("update_tc");
 }
 
+template <int NN>
+static void launch_update_tc2(const float *A, int64_t lda, int64_t M, int m, const double *C, int ldc, int n,
+                              double alpha, double beta, float *Out, int64_t ldo, cudaStream_t st) {
+    using Key = std::tuple<const float *, int64_t, int, int64_t>;
+    static thread_local std::map<Key, CUtensorMap> cache;
+    const Key key{A, M, m, lda};
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+        if (cache.size() > 256) cache.clear();
+        it = cache.emplace(key, make_map2(A, (uint64_t)M, (uint64_t)m, (uint64_t)lda * 4, tallu2::ROWS, tallu2::KC,
+                                          false, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)).first;
+    }
+    const int nchk = (m + 31) / 32;
+    static thread_local DevBuf bpk;
+    const size_t need = sizeof(float) * (size_t)nchk * 2 * NN * 32;
+    if (bpk.bytes < need) bpk.alloc(need, st);
+    coef_pack_kernel<NN><<<nchk, 256, 0, st>>>(m, C, ldc, n, alpha, bpk.as<float>());
+    after_launch("coef_pack");
+    auto kern = update_tc2_kernel<NN>;
+    set_max_smem(kern);
+    const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallu2::ROWS));
+    kern<<<ctas, tallu2::NTHR, tallu2::SMEM, st>>>(it->second, M, m, bpk.as<float>(), n, beta, Out, ldo);
+    after_launch("update_tc2");
+}
+
 // Out = beta·Out + alpha·A·C on the tensor cores; false when unsupported (caller: CUDA cores).
 // Needs lda a multiple of 32 with lda >= M rounded up to 32 (the solver's padded bases), 16-B
 // aligned A, M < 2^31 · 32.
@@ -889,6 +1118,12 @@ bool update_tc(int64_t M, const float *A, int64_t lda, int m, const double *C, i
     if (!mode || M < 8192 || n > 64 || m > 4096 || (mode == 1 && m < 64) || (lda & 31) || lda < (M + 31) / 32 * 32 ||
         ((uintptr_t)A & 127))
         return false;
+    static const int ver = [] { const char *e = std::getenv("SSA_UPD_V"); return e ? std::atoi(e) : 2; }();
+    if (ver == 2) {
+        if (n <= 32) launch_update_tc2<32>(A, lda, M, m, C, ldc, n, alpha, beta, Out, ldo, st);
+        else launch_update_tc2<64>(A, lda, M, m, C, ldc, n, alpha, beta, Out, ldo, st);
+        return true;
+    }
     using Key = std::tuple<const float *, int64_t, int, int64_t>;
     static thread_local std::map<Key, CUtensorMap> cache;
     const Key key{A, M, m, lda};
