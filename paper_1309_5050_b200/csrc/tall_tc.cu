@@ -313,7 +313,7 @@ struct Cfg {
 template <int NM, int NN, int BA, int RC, int KG>
 __global__ void __launch_bounds__(tallg::NTHR, 1)
 gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
-                int n1, int n2, int self_b, double *__restrict__ partials) {
+                int n1, int n2, int self_b, double *__restrict__ partials, int dbg) {
     using namespace tc;
     using C = tallg3::Cfg<NM, NN, BA, RC, KG>;
     constexpr int KS = C::KS, KA = C::KA, OPB = C::OPB, AB = C::ACCB;
@@ -403,6 +403,7 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 trace(tr, 6, i);
                 const uint32_t dbase = tmem + (uint32_t)(b * C::acc_cols);
                 const uint64_t bh0 = make_desc(b_hi(o, 0));
+                if (!(dbg & 2)) {
                 constexpr uint64_t b_lo_step = (uint64_t)(C::b_raw >> 4), rc_step = (uint64_t)((2 * C::b_raw) >> 4);
 #pragma unroll
                 for (int g = 0; g < KA; ++g) {
@@ -425,6 +426,7 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         }
                     }
                 }
+                }
                 mma_commit(ope(o));
                 mma_commit(accf(b));
                 trace(tr, 2, i);
@@ -446,7 +448,7 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             tc_fence_after();
             if (warp == 4 && lane == 0) trace(tr, 4, i);
             const unsigned char *rawp = smem + C::off_raw + (size_t)r * raw_bytes;
-            if (a_warp) {
+            if (a_warp && !(dbg & 1)) {
 #pragma unroll
                 for (int rc = 0; rc < RC; ++rc) {
 #pragma unroll
@@ -472,7 +474,7 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
             if (warp == 4 && lane == 0) trace(tr, 1, i);
 #pragma unroll
-            for (int rc = 0; rc < RC; ++rc) {
+            for (int rc = 0; rc < (dbg & 1 ? 0 : RC); ++rc) {
                 const float4 *src = reinterpret_cast<const float4 *>(rawp + rc * unit + (self_b ? 0 : C::a_raw));
                 float4 *dh = reinterpret_cast<float4 *>(smem + (size_t)o * C::bop + rc * 2 * C::b_raw);
 #pragma unroll 2
@@ -1027,7 +1029,8 @@ static void launch_gram_tc3(int64_t M, const float *A, int64_t lda, int n1, cons
     auto kern = gram_tc3_kernel<NM, NN, BA, RC, KG>;
     set_max_smem(kern);
     const int gy = (int)cdiv(n1, NM * 128);
-    kern<<<dim3(ctas, gy), tallg::NTHR, tallg3::SMEM, st>>>(ma, mb, M, n1, n2, self_b, partials);
+    static const int dbg = [] { const char *e = std::getenv("SSA_GRAM_DBG"); return e ? std::atoi(e) : 0; }();
+    kern<<<dim3(ctas, gy), tallg::NTHR, tallg3::SMEM, st>>>(ma, mb, M, n1, n2, self_b, partials, dbg);
     after_launch("gram_tc3");
 }
 
