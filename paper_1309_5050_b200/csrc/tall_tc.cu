@@ -906,8 +906,20 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
         for (int j = 0; j < 32; ++j) acc[j] = 0.f;
         const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(32 * h);
         const float fb = (float)beta;
+        float old[32];
         for (int i = 0; i < nitems; ++i) {
             const int b = i % NBUF;
+            const int64_t row = (t0 + i / nchk) * tallu2::ROWS + (warp & 3) * 32 + lane;
+            if (i % nchk == 0) {
+                // the tile's old output values, loaded a whole tile ahead of the epilogue (their
+                // latency used to stall the drain, and with it the MMAs, once per tile); in place
+                // (Out = A) is safe: these rows are written only by this thread, at the tile's end
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int col = 32 * h + j;
+                    old[j] = (has && row < M && beta != 0.0 && col < n) ? __ldcg(Out + row + ldo * (int64_t)col) : 0.f;
+                }
+            }
             mbar_wait(accf(b), (i / NBUF) & 1);
             tc_fence_after();
             if (has) {
@@ -920,14 +932,7 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
             if (i % nchk == nchk - 1) {
-                const int64_t row = (t0 + i / nchk) * tallu2::ROWS + (warp & 3) * 32 + lane;
                 if (has && row < M) {
-                    float old[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int col = 32 * h + j;
-                        old[j] = (beta != 0.0 && col < n) ? __ldcg(Out + row + ldo * (int64_t)col) : 0.f;
-                    }
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const int col = 32 * h + j;

@@ -1,4 +1,4 @@
-for cfg in "1 1" "2 1" "2 2"; do set -- $cfg; echo "UPD_V=$1 UPD_TC=$2"; SSA_UPD_V=$1 SSA_UPD_TC=$2 timeout 120 python - <<'PY'
+for cfg in "2 1"; do set -- $cfg; echo "UPD_V=$1 UPD_TC=$2"; SSA_UPD_V=$1 SSA_UPD_TC=$2 timeout 120 python - <<'PY'
 import ctypes as C, sys
 sys.path.insert(0, '.')
 from paper_1309_5050_b200 import _lib
