@@ -45,3 +45,34 @@ def test_self_gram_matches_fp64(lib, M, n1, n2):
                                      (70000, 512, 64), (3000, 224, 32)])
 def test_update_matches_fp64(lib, M, n1, n2):
     assert _run(lib, 1, M, n1, n2) <= TOL
+
+
+_V1_SCRIPT = r"""
+import ctypes as C, sys
+sys.path.insert(0, sys.argv[1])
+from paper_1309_5050_b200 import _lib
+L = _lib.load()
+worst = 0.0
+for which, (M, n1, n2) in [(0, (8200, 65, 33)), (0, (20001, 300, 64)), (3, (12345, 64, 64)), (1, (8200, 100, 64)),
+                           (1, (20001, 300, 64))]:
+    ms, ck = C.c_double(), C.c_double()
+    assert L.ssa_bench_tall(which, M, n1, n2, 1, C.byref(ms), C.byref(ck)) == 0, L.ssa_last_error()
+    worst = max(worst, ck.value)
+print(worst)
+"""
+
+
+@pytest.mark.parametrize("env", [{"SSA_GRAM_V": "1", "SSA_UPD_V": "1"}, {"SSA_GRAM_RC": "1"},
+                                 {"SSA_UPD_TC": "2"}])
+def test_kernel_variants_match_fp64(lib, env):
+    """The env-selected variants (v1 Gram / update with both operands in shared memory, 32-row Gram stages,
+    tensor-core update for narrow m) stay correct: the switches are read once per process, so each runs in
+    a subprocess."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _V1_SCRIPT, root], env={**os.environ, **env}, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= TOL
