@@ -543,14 +543,36 @@ struct Gkl {
             T *Ab = project ? A : W;
             gram(M, Ab, ld, nn, W, ld, kc, G.data(), kside);
             const int off = project ? na : 0;
-            for (int bb = 0; bb < kc; ++bb)
-                for (int aa = 0; aa <= bb; ++aa) {
-                    double v = G[off + aa + (size_t)nn * bb];
-                    if (project)
-                        for (int t = 0; t < na; ++t) v -= G[t + (size_t)nn * aa] * G[t + (size_t)nn * bb];
-                    Gp[aa + (size_t)kc * bb] = v;
-                    Gp[bb + (size_t)kc * aa] = v;
+            // (host loops over na ≤ 448 run several independent chains / axpys at once: as scalar
+            // dependent-FMA chains they were a large part of a small-M block step)
+            // four independent chains (aa .. aa+3), each in the original t order (bit-identical)
+            for (int bb = 0; bb < kc; ++bb) {
+                const double *gb = G.data() + (size_t)nn * bb;
+                for (int aa = 0; aa <= bb; aa += 4) {
+                    const int na4 = std::min(4, bb + 1 - aa);
+                    double v[4];
+                    for (int q = 0; q < na4; ++q) v[q] = G[off + aa + q + (size_t)nn * bb];
+                    if (project) {
+                        const double *g0 = G.data() + (size_t)nn * aa;
+                        if (na4 == 4) {
+                            const double *g1 = g0 + nn, *g2 = g1 + nn, *g3 = g2 + nn;
+                            for (int t = 0; t < na; ++t) {
+                                const double x = gb[t];
+                                v[0] -= g0[t] * x; v[1] -= g1[t] * x; v[2] -= g2[t] * x; v[3] -= g3[t] * x;
+                            }
+                        } else {
+                            for (int q = 0; q < na4; ++q) {
+                                const double *gq = g0 + (size_t)nn * q;
+                                for (int t = 0; t < na; ++t) v[q] -= gq[t] * gb[t];
+                            }
+                        }
+                    }
+                    for (int q = 0; q < na4; ++q) {
+                        Gp[aa + q + (size_t)kc * bb] = v[q];
+                        Gp[bb + (size_t)kc * (aa + q)] = v[q];
+                    }
                 }
+            }
             double dmax = 0.0, dev = 0.0;
             for (int j = 0; j < kc; ++j) dmax = std::max(dmax, Gp[j + (size_t)kc * j]);
             for (int bb = 0; bb < kc; ++bb)
@@ -577,22 +599,32 @@ struct Gkl {
             if (project) {
                 // W ← [A W]·[−C R⁻¹; R⁻¹]; coefficients W_in = A·(Ctot + C·Btot) + W_new·(R·Btot)
                 for (int bb = 0; bb < kc; ++bb) {
-                    for (int t = 0; t < na; ++t) {
-                        double v = 0.0;
-                        for (int aa = 0; aa <= bb; ++aa) v -= G[t + (size_t)n1 * aa] * Sinv[aa + (size_t)kc * bb];
-                        Mc[t + (size_t)n1 * bb] = v;
+                    double *mc = Mc.data() + (size_t)n1 * bb;
+                    for (int t = 0; t < na; ++t) mc[t] = 0.0;
+                    for (int aa = 0; aa <= bb; ++aa) {
+                        const double sv = Sinv[aa + (size_t)kc * bb], *ga = G.data() + (size_t)n1 * aa;
+#pragma omp simd
+                        for (int t = 0; t < na; ++t) mc[t] -= ga[t] * sv;
                     }
-                    for (int aa = 0; aa < kc; ++aa) Mc[na + aa + (size_t)n1 * bb] = Sinv[aa + (size_t)kc * bb];
+                    for (int aa = 0; aa < kc; ++aa) mc[na + aa] = Sinv[aa + (size_t)kc * bb];
                 }
                 gemm(M, A, ld, n1, Mc.data(), n1, kc, 1.0, 0.0, W, ld);
-                for (int bb = 0; bb < kc; ++bb)
-                    for (int t = 0; t < na; ++t) {
-                        double v = 0.0;
-                        if (Btot.empty()) v = G[t + (size_t)n1 * bb];
-                        else
-                            for (int aa = 0; aa < kc; ++aa) v += G[t + (size_t)n1 * aa] * Btot[aa + (size_t)kc * bb];
-                        Ctot[t + (size_t)na * bb] += v;
+                std::vector<double> cv((size_t)std::max(na, 1));
+                for (int bb = 0; bb < kc; ++bb) {
+                    double *ct = Ctot.data() + (size_t)na * bb;
+                    if (Btot.empty()) {
+                        const double *gb = G.data() + (size_t)n1 * bb;
+                        for (int t = 0; t < na; ++t) ct[t] += gb[t];
+                        continue;
                     }
+                    for (int t = 0; t < na; ++t) cv[t] = 0.0;
+                    for (int aa = 0; aa < kc; ++aa) {
+                        const double bv = Btot[aa + (size_t)kc * bb], *ga = G.data() + (size_t)n1 * aa;
+#pragma omp simd
+                        for (int t = 0; t < na; ++t) cv[t] += ga[t] * bv;
+                    }
+                    for (int t = 0; t < na; ++t) ct[t] += cv[t];
+                }
             } else {
                 gemm(M, W, ld, kc, Sinv.data(), kc, kc, 1.0, 0.0, W, ld);   // in place
             }
@@ -608,6 +640,13 @@ struct Gkl {
             }
             const bool was_projection = project;
             project = (pass == 1 && reproject);
+            static const bool onepass = std::getenv("SSA_ORTH3_ONEPASS") != nullptr;   // timing experiment only
+            if (onepass && !project && !shifted) {
+                if (coef)
+                    for (size_t t = 0; t < Ctot.size(); ++t) coef[t] += Ctot[t];
+                ++n_fast;
+                return Btot;
+            }
             if (pass >= 2 && !project && !shifted && !was_projection && dev <= 0.1) {
                 if (coef)
                     for (size_t t = 0; t < Ctot.size(); ++t) coef[t] += Ctot[t];
@@ -940,7 +979,8 @@ struct Gkl {
             // blocks to convergence), check after every block once the basis holds r vectors;
             // cheap blocks (c2, c3) wait for the first early check / the cycle end
             const double tr_est = t_ritz > 0.0 ? t_ritz : 1.0;
-            const bool costly_blocks = near_ok && nQ - k >= r && t_block >= 1.5 * tr_est;
+            static const double cost_ratio = [] { const char *e = std::getenv("SSA_CHECK_RATIO"); return e ? std::atof(e) : 1.0; }();
+            const bool costly_blocks = near_ok && nQ - k >= r && t_block >= cost_ratio * tr_est;
             if (!first_check && !cycle_end && !costly_blocks) continue;
             checked_once = true;
             // ---- Ritz extraction from T (nP x nc)
