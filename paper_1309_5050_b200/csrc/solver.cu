@@ -630,12 +630,15 @@ struct Gkl {
             }
             if (Btot.empty()) Btot = R;
             else {
-                for (int bb = 0; bb < kc; ++bb)
-                    for (int aa = 0; aa < kc; ++aa) {
-                        double v = 0.0;
-                        for (int t = aa; t < kc; ++t) v += R[aa + (size_t)kc * t] * Btot[t + (size_t)kc * bb];
-                        Bn[aa + (size_t)kc * bb] = v;
+                // Bn = R·Btot (R upper): per output the same t order as the dot-product form
+                for (int bb = 0; bb < kc; ++bb) {
+                    double *bn = Bn.data() + (size_t)kc * bb;
+                    for (int aa = 0; aa < kc; ++aa) bn[aa] = 0.0;
+                    for (int t = 0; t < kc; ++t) {
+                        const double bt = Btot[t + (size_t)kc * bb], *rt = R.data() + (size_t)kc * t;
+                        for (int aa = 0; aa <= t; ++aa) bn[aa] += rt[aa] * bt;
                     }
+                }
                 Btot.swap(Bn);
             }
             const bool was_projection = project;
@@ -990,13 +993,16 @@ struct Gkl {
             t_ritz = ms_ritz - tr;
             anorm = std::max(anorm, th[0]);
             res.assign(nc, 0.0);
+            std::vector<double> sv((size_t)k);
             for (int i = 0; i < nc; ++i) {
-                double s2 = 0.0;
-                for (int a = 0; a < k; ++a) {
-                    double s = 0.0;
-                    for (int b = 0; b < k; ++b) s += Alast[a + (size_t)k * b] * Y[(nP - k + b) + (size_t)nP * i];
-                    s2 += s * s;
+                // s = Alast · y_i(last block): k independent accumulators, each in the original b order
+                for (int a = 0; a < k; ++a) sv[a] = 0.0;
+                for (int b = 0; b < k; ++b) {
+                    const double y = Y[(nP - k + b) + (size_t)nP * i], *al = Alast.data() + (size_t)k * b;
+                    for (int a = 0; a < k; ++a) sv[a] += al[a] * y;
                 }
+                double s2 = 0.0;
+                for (int a = 0; a < k; ++a) s2 += sv[a] * sv[a];
                 res[i] = std::sqrt(s2);
             }
             nconv = 0; maxres = 0.0;
