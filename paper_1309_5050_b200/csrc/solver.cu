@@ -28,6 +28,7 @@
 
 #include "common.h"
 #include "dense.h"
+#include "hostla.h"
 #include "kernels.h"
 #include "plan.h"
 
@@ -121,6 +122,7 @@ struct Gkl {
     bool use_fast = std::getenv("SSA_ORTH_FAST") != nullptr;   // device-resident orth (experimental)
     DevBuf ow;                    // device workspace of the fast orthonormalisation
     double tw_prod = 0, tw_orthA = 0, tw_orthB = 0, tw_rec = 0, tw_restart = 0;   // host wall ms (SSA_DEBUG)
+    double tw_o3_gram[2] = {0, 0}, tw_o3_host[2] = {0, 0}, tw_o3_apply[2] = {0, 0};   // orth3 split [L, K side]
     static double now_ms() {
         return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
     }
@@ -208,34 +210,12 @@ struct Gkl {
     // positive or tiny relative to the largest diagonal entry.
     bool cholesky(int n, const double *G, double shift, double thr, std::vector<double> &R) {
         R.assign((size_t)n * n, 0.0);
-        double dmax = 0.0;
-        for (int j = 0; j < n; ++j) dmax = std::max(dmax, G[j + (size_t)n * j]);
-        if (!(dmax > 0.0)) return false;
-        for (int j = 0; j < n; ++j) {
-            double s = G[j + (size_t)n * j] + shift;
-            for (int t = 0; t < j; ++t) s -= R[t + (size_t)n * j] * R[t + (size_t)n * j];
-            if (!(s > thr * dmax)) return false;
-            const double rjj = std::sqrt(s);
-            R[j + (size_t)n * j] = rjj;
-            for (int i = j + 1; i < n; ++i) {
-                double v = G[j + (size_t)n * i];
-                for (int t = 0; t < j; ++t) v -= R[t + (size_t)n * j] * R[t + (size_t)n * i];
-                R[j + (size_t)n * i] = v / rjj;
-            }
-        }
-        return true;
+        return hostla::cholesky_upper(n, G, shift, thr, R.data());
     }
 
     static void upper_inverse(int n, const std::vector<double> &R, std::vector<double> &S) {
         S.assign((size_t)n * n, 0.0);
-        for (int j = 0; j < n; ++j) {
-            S[j + (size_t)n * j] = 1.0 / R[j + (size_t)n * j];
-            for (int i = j - 1; i >= 0; --i) {
-                double v = 0.0;
-                for (int t = i + 1; t <= j; ++t) v += R[i + (size_t)n * t] * S[t + (size_t)n * j];
-                S[i + (size_t)n * j] = -v / R[i + (size_t)n * i];
-            }
-        }
+        hostla::upper_inverse(n, R.data(), S.data());
     }
 
     // Orthonormalise W (M x kc) against `against` (na orthonormal columns) and internally,
@@ -541,37 +521,18 @@ struct Gkl {
         for (int pass = 1; pass <= 4; ++pass) {
             const int nn = project ? n1 : kc;                       // Gram columns: [A W] or W
             T *Ab = project ? A : W;
+            const double tg0 = now_ms();
             gram(M, Ab, ld, nn, W, ld, kc, G.data(), kside);
+            const double tg1 = now_ms();
+            tw_o3_gram[kside] += tg1 - tg0;
             const int off = project ? na : 0;
-            // (host loops over na ≤ 448 run several independent chains / axpys at once: as scalar
-            // dependent-FMA chains they were a large part of a small-M block step)
-            // four independent chains (aa .. aa+3), each in the original t order (bit-identical)
-            for (int bb = 0; bb < kc; ++bb) {
-                const double *gb = G.data() + (size_t)nn * bb;
-                for (int aa = 0; aa <= bb; aa += 4) {
-                    const int na4 = std::min(4, bb + 1 - aa);
-                    double v[4];
-                    for (int q = 0; q < na4; ++q) v[q] = G[off + aa + q + (size_t)nn * bb];
-                    if (project) {
-                        const double *g0 = G.data() + (size_t)nn * aa;
-                        if (na4 == 4) {
-                            const double *g1 = g0 + nn, *g2 = g1 + nn, *g3 = g2 + nn;
-                            for (int t = 0; t < na; ++t) {
-                                const double x = gb[t];
-                                v[0] -= g0[t] * x; v[1] -= g1[t] * x; v[2] -= g2[t] * x; v[3] -= g3[t] * x;
-                            }
-                        } else {
-                            for (int q = 0; q < na4; ++q) {
-                                const double *gq = g0 + (size_t)nn * q;
-                                for (int t = 0; t < na; ++t) v[q] -= gq[t] * gb[t];
-                            }
-                        }
-                    }
-                    for (int q = 0; q < na4; ++q) {
-                        Gp[aa + q + (size_t)kc * bb] = v[q];
-                        Gp[bb + (size_t)kc * (aa + q)] = v[q];
-                    }
-                }
+            // (the na-long host loops run vectorised in hostla.cpp: as scalar dependent-FMA chains
+            // they were a large part of a small-M block step)
+            if (project) {
+                hostla::gram_minus_ctc(kc, na, nn, off, G.data(), Gp.data());
+            } else {
+                for (int bb = 0; bb < kc; ++bb)
+                    for (int aa = 0; aa < kc; ++aa) Gp[aa + (size_t)kc * bb] = G[off + std::min(aa, bb) + (size_t)nn * std::max(aa, bb)];
             }
             double dmax = 0.0, dev = 0.0;
             for (int j = 0; j < kc; ++j) dmax = std::max(dmax, Gp[j + (size_t)kc * j]);
@@ -596,19 +557,14 @@ struct Gkl {
                 break;
             }
             upper_inverse(kc, R, Sinv);
+            double ta0 = 0.0;
             if (project) {
                 // W ← [A W]·[−C R⁻¹; R⁻¹]; coefficients W_in = A·(Ctot + C·Btot) + W_new·(R·Btot)
-                for (int bb = 0; bb < kc; ++bb) {
-                    double *mc = Mc.data() + (size_t)n1 * bb;
-                    for (int t = 0; t < na; ++t) mc[t] = 0.0;
-                    for (int aa = 0; aa <= bb; ++aa) {
-                        const double sv = Sinv[aa + (size_t)kc * bb], *ga = G.data() + (size_t)n1 * aa;
-#pragma omp simd
-                        for (int t = 0; t < na; ++t) mc[t] -= ga[t] * sv;
-                    }
-                    for (int aa = 0; aa < kc; ++aa) mc[na + aa] = Sinv[aa + (size_t)kc * bb];
-                }
+                hostla::proj_coef(kc, na, n1, G.data(), Sinv.data(), Mc.data());
+                ta0 = now_ms();
+                tw_o3_host[kside] += ta0 - tg1;
                 gemm(M, A, ld, n1, Mc.data(), n1, kc, 1.0, 0.0, W, ld);
+                tw_o3_apply[kside] += now_ms() - ta0;
                 std::vector<double> cv((size_t)std::max(na, 1));
                 for (int bb = 0; bb < kc; ++bb) {
                     double *ct = Ctot.data() + (size_t)na * bb;
@@ -626,7 +582,10 @@ struct Gkl {
                     for (int t = 0; t < na; ++t) ct[t] += cv[t];
                 }
             } else {
+                ta0 = now_ms();
+                tw_o3_host[kside] += ta0 - tg1;
                 gemm(M, W, ld, kc, Sinv.data(), kc, kc, 1.0, 0.0, W, ld);   // in place
+                tw_o3_apply[kside] += now_ms() - ta0;
             }
             if (Btot.empty()) Btot = R;
             else {
@@ -1048,6 +1007,9 @@ struct Gkl {
                                  "(fast %lld, fallback %lld)\n",
                          tw_prod, tw_orthA, tw_orthB, tw_rec, tw_restart, ms_ritz, (long long)n_fast,
                          (long long)n_fallback);
+        if (debug)
+            std::fprintf(stderr, "[ssa] orth3 host ms: L gram(wait) %.2f host %.2f apply(launch) %.2f | K gram %.2f host %.2f apply %.2f\n",
+                         tw_o3_gram[0], tw_o3_host[0], tw_o3_apply[0], tw_o3_gram[1], tw_o3_host[1], tw_o3_apply[1]);
         // sign convention: largest-|.| entry of each U_i positive
         for (int c0 = 0; c0 < r; c0 += 1024) {
             const int nc = std::min(1024, r - c0);
