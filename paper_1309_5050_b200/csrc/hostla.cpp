@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -105,7 +106,8 @@ SSA_HOSTLA_BODY
 }
 #pragma GCC pop_options
 bool use_avx2() {
-    static const bool v = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma");
+    static const bool v = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma") &&
+                          std::getenv("SSA_HOSTLA_GENERIC") == nullptr;   // (tests force the baseline build)
     return v;
 }
 #else
