@@ -131,4 +131,9 @@ void scale_columns(int64_t M, T *A, int64_t lda, int n, const double *s, cudaStr
 template <typename T>
 void absmax_sign(int64_t M, const T *A, int64_t lda, int n, double *sgn, cudaStream_t st);
 
+// one CholeskyQR pass (G = WᵀW, RᵀR = G, W ← W R⁻¹) in a single cooperative launch (cholqr.cu)
+size_t cholqr_ws_bytes(int kc);
+bool cholqr_fused(int64_t M, float *W, int64_t ld, int kc, double shift_rel, double thr_chol, double *ws, size_t ws_bytes,
+                  double *out, cudaStream_t st);
+
 }  // namespace ssa

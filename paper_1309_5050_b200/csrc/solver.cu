@@ -519,73 +519,100 @@ struct Gkl {
         const double shift_rel = (sizeof(T) == 4) ? 1e-6 : 1e-13;
         bool project = true, reproject = false;
         for (int pass = 1; pass <= 4; ++pass) {
-            const int nn = project ? n1 : kc;                       // Gram columns: [A W] or W
-            T *Ab = project ? A : W;
-            const double tg0 = now_ms();
-            gram(M, Ab, ld, nn, W, ld, kc, G.data(), kside);
-            const double tg1 = now_ms();
-            tw_o3_gram[kside] += tg1 - tg0;
-            const int off = project ? na : 0;
-            // (the na-long host loops run vectorised in hostla.cpp: as scalar dependent-FMA chains
-            // they were a large part of a small-M block step)
-            if (project) {
-                hostla::gram_minus_ctc(kc, na, nn, off, G.data(), Gp.data());
-            } else {
+            // plain CholeskyQR passes (no projection) of fp32 blocks whose row slices fit in shared
+            // memory run as one cooperative kernel (Gram, factor, apply; cholqr.cu): one launch and
+            // one small read-back instead of Gram + reduction + round trip + upload + update
+            bool shifted = false, fused = false;
+            double dev = 0.0;
+            if (!project && sizeof(T) == 4 && !(kside && kside_comm())) {
+                const size_t io = sg.take((size_t)kc * kc + 4);
+                const double tf0 = now_ms();
+                if (cholqr_fused(M, reinterpret_cast<float *>(W), ld, kc, shift_rel, thr_chol, p.ws_gram.template as<double>(),
+                                 p.ws_gram.bytes, sg.dev(io), st)) {
+                    SSA_CUDA(cudaMemcpyAsync(sg.h + io, sg.dev(io), sizeof(double) * ((size_t)kc * kc + 4),
+                                             cudaMemcpyDeviceToHost, st));
+                    stream_wait(st);
+                    sg.off = 0;
+                    const double *ho = sg.h + io;
+                    tw_o3_gram[kside] += now_ms() - tf0;
+                    if (ho[(size_t)kc * kc] == 0.0) break;   // factorisation failed, W untouched: robust path
+                    R.assign(ho, ho + (size_t)kc * kc);
+                    shifted = ho[(size_t)kc * kc + 1] != 0.0;
+                    dev = ho[(size_t)kc * kc + 2];
+                    fused = true;
+                }
+            }
+            if (!fused) {
+                const int nn = project ? n1 : kc;                       // Gram columns: [A W] or W
+                T *Ab = project ? A : W;
+                const double tg0 = now_ms();
+                gram(M, Ab, ld, nn, W, ld, kc, G.data(), kside);
+                const double tg1 = now_ms();
+                tw_o3_gram[kside] += tg1 - tg0;
+                const int off = project ? na : 0;
+                // (the na-long host loops run vectorised in hostla.cpp: as scalar dependent-FMA chains
+                // they were a large part of a small-M block step)
+                if (project) {
+                    hostla::gram_minus_ctc(kc, na, nn, off, G.data(), Gp.data());
+                } else {
+                    for (int bb = 0; bb < kc; ++bb)
+                        for (int aa = 0; aa < kc; ++aa) Gp[aa + (size_t)kc * bb] = G[off + std::min(aa, bb) + (size_t)nn * std::max(aa, bb)];
+                }
+                double dmax = 0.0;
+                dev = 0.0;
+                for (int j = 0; j < kc; ++j) dmax = std::max(dmax, Gp[j + (size_t)kc * j]);
                 for (int bb = 0; bb < kc; ++bb)
-                    for (int aa = 0; aa < kc; ++aa) Gp[aa + (size_t)kc * bb] = G[off + std::min(aa, bb) + (size_t)nn * std::max(aa, bb)];
-            }
-            double dmax = 0.0, dev = 0.0;
-            for (int j = 0; j < kc; ++j) dmax = std::max(dmax, Gp[j + (size_t)kc * j]);
-            for (int bb = 0; bb < kc; ++bb)
-                for (int aa = 0; aa < kc; ++aa)
-                    dev = std::max(dev, std::fabs(Gp[aa + (size_t)kc * bb] - (aa == bb ? 1.0 : 0.0)));
-            if (pass == 1) {
-                // breakdown (numerically zero column) -> robust path, W untouched
-                bool zero = !(dmax > 0.0) || !std::isfinite(dmax);
-                for (int j = 0; j < kc && !zero; ++j) {
-                    const double d = Gp[j + (size_t)kc * j], h = G[na + j + (size_t)n1 * j];
-                    zero = !(std::sqrt(std::max(d, 0.0)) > thr_abs * std::max(anorm, 1e-300)) || !(d > 1e-24 * dmax) ||
-                           !(d > (sizeof(T) == 4 ? 1e-12 : 1e-24) * h);
-                    reproject = reproject || !(d > 0.5 * h);   // DGKS: "twice is enough"
-                }
-                if (zero) { ++n_fallback; return orth(M, W, kc, against, na, kside, coef); }
-            }
-            bool shifted = false, ok = cholesky(kc, Gp.data(), 0.0, thr_chol, R);
-            if (!ok) { ok = cholesky(kc, Gp.data(), shift_rel * dmax, 1e-300, R); shifted = ok; }
-            if (!ok) {
-                if (pass == 1) { ++n_fallback; return orth(M, W, kc, against, na, kside, coef); }
-                break;
-            }
-            upper_inverse(kc, R, Sinv);
-            double ta0 = 0.0;
-            if (project) {
-                // W ← [A W]·[−C R⁻¹; R⁻¹]; coefficients W_in = A·(Ctot + C·Btot) + W_new·(R·Btot)
-                hostla::proj_coef(kc, na, n1, G.data(), Sinv.data(), Mc.data());
-                ta0 = now_ms();
-                tw_o3_host[kside] += ta0 - tg1;
-                gemm(M, A, ld, n1, Mc.data(), n1, kc, 1.0, 0.0, W, ld);
-                tw_o3_apply[kside] += now_ms() - ta0;
-                std::vector<double> cv((size_t)std::max(na, 1));
-                for (int bb = 0; bb < kc; ++bb) {
-                    double *ct = Ctot.data() + (size_t)na * bb;
-                    if (Btot.empty()) {
-                        const double *gb = G.data() + (size_t)n1 * bb;
-                        for (int t = 0; t < na; ++t) ct[t] += gb[t];
-                        continue;
+                    for (int aa = 0; aa < kc; ++aa)
+                        dev = std::max(dev, std::fabs(Gp[aa + (size_t)kc * bb] - (aa == bb ? 1.0 : 0.0)));
+                if (pass == 1) {
+                    // breakdown (numerically zero column) -> robust path, W untouched
+                    bool zero = !(dmax > 0.0) || !std::isfinite(dmax);
+                    for (int j = 0; j < kc && !zero; ++j) {
+                        const double d = Gp[j + (size_t)kc * j], h = G[na + j + (size_t)n1 * j];
+                        zero = !(std::sqrt(std::max(d, 0.0)) > thr_abs * std::max(anorm, 1e-300)) || !(d > 1e-24 * dmax) ||
+                               !(d > (sizeof(T) == 4 ? 1e-12 : 1e-24) * h);
+                        reproject = reproject || !(d > 0.5 * h);   // DGKS: "twice is enough"
                     }
-                    for (int t = 0; t < na; ++t) cv[t] = 0.0;
-                    for (int aa = 0; aa < kc; ++aa) {
-                        const double bv = Btot[aa + (size_t)kc * bb], *ga = G.data() + (size_t)n1 * aa;
-#pragma omp simd
-                        for (int t = 0; t < na; ++t) cv[t] += ga[t] * bv;
-                    }
-                    for (int t = 0; t < na; ++t) ct[t] += cv[t];
+                    if (zero) { ++n_fallback; return orth(M, W, kc, against, na, kside, coef); }
                 }
-            } else {
-                ta0 = now_ms();
-                tw_o3_host[kside] += ta0 - tg1;
-                gemm(M, W, ld, kc, Sinv.data(), kc, kc, 1.0, 0.0, W, ld);   // in place
-                tw_o3_apply[kside] += now_ms() - ta0;
+                shifted = false;
+                bool ok = cholesky(kc, Gp.data(), 0.0, thr_chol, R);
+                if (!ok) { ok = cholesky(kc, Gp.data(), shift_rel * dmax, 1e-300, R); shifted = ok; }
+                if (!ok) {
+                    if (pass == 1) { ++n_fallback; return orth(M, W, kc, against, na, kside, coef); }
+                    break;
+                }
+                upper_inverse(kc, R, Sinv);
+                double ta0 = 0.0;
+                if (project) {
+                    // W ← [A W]·[−C R⁻¹; R⁻¹]; coefficients W_in = A·(Ctot + C·Btot) + W_new·(R·Btot)
+                    hostla::proj_coef(kc, na, n1, G.data(), Sinv.data(), Mc.data());
+                    ta0 = now_ms();
+                    tw_o3_host[kside] += ta0 - tg1;
+                    gemm(M, A, ld, n1, Mc.data(), n1, kc, 1.0, 0.0, W, ld);
+                    tw_o3_apply[kside] += now_ms() - ta0;
+                    std::vector<double> cv((size_t)std::max(na, 1));
+                    for (int bb = 0; bb < kc; ++bb) {
+                        double *ct = Ctot.data() + (size_t)na * bb;
+                        if (Btot.empty()) {
+                            const double *gb = G.data() + (size_t)n1 * bb;
+                            for (int t = 0; t < na; ++t) ct[t] += gb[t];
+                            continue;
+                        }
+                        for (int t = 0; t < na; ++t) cv[t] = 0.0;
+                        for (int aa = 0; aa < kc; ++aa) {
+                            const double bv = Btot[aa + (size_t)kc * bb], *ga = G.data() + (size_t)n1 * aa;
+    #pragma omp simd
+                            for (int t = 0; t < na; ++t) cv[t] += ga[t] * bv;
+                        }
+                        for (int t = 0; t < na; ++t) ct[t] += cv[t];
+                    }
+                } else {
+                    ta0 = now_ms();
+                    tw_o3_host[kside] += ta0 - tg1;
+                    gemm(M, W, ld, kc, Sinv.data(), kc, kc, 1.0, 0.0, W, ld);   // in place
+                    tw_o3_apply[kside] += now_ms() - ta0;
+                }
             }
             if (Btot.empty()) Btot = R;
             else {
