@@ -670,16 +670,31 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 
 template <typename T>
 __global__ void fill_normal_kernel(int64_t M, T *A, int64_t lda, int ncols, uint64_t seed, uint64_t sid) {
-    const int64_t n = M * ncols;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = t % M, col = t / M;
-        const uint64_t h = mix64(seed ^ mix64(sid * 0x100000001B3ull + (uint64_t)col) ^ (uint64_t)row * 0xD6E8FEB86659FD93ull);
-        const double u1 = ((h >> 11) + 1.0) * (1.0 / 9007199254740993.0);
-        const double u2 = (double)(mix64(h) >> 11) * (1.0 / 9007199254740992.0);
-        if constexpr (sizeof(T) == 4)   // fp32 plans: fp32 transcendentals (the fp64 ones made this HBM write compute-bound)
-            A[row + lda * col] = sqrtf(-2.0f * logf((float)u1)) * cospif(2.0f * (float)u2);
-        else
+    if constexpr (sizeof(T) == 4) {
+        // fp32 plans: one hash per Box–Muller pair (rows 2i, 2i+1 get r·cos, r·sin), 24-bit uniforms
+        // and fp32 transcendentals (c5's random refills of 14.75M-row columns were compute bound)
+        const int64_t mp = (M + 1) / 2, n = mp * ncols;
+        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t pr = t % mp, col = t / mp;
+            const uint64_t h = mix64(seed ^ mix64(sid * 0x100000001B3ull + (uint64_t)col) ^ (uint64_t)pr * 0xD6E8FEB86659FD93ull);
+            const float u1 = (float)((uint32_t)(h >> 40) + 1u) * 0x1p-24f;              // (0, 1]
+            const float u2 = (float)(uint32_t)((h >> 8) & 0xFFFFFFu) * 0x1p-24f;         // [0, 1)
+            const float r = sqrtf(-2.0f * logf(u1));
+            float sn, cs;
+            sincospif(2.0f * u2, &sn, &cs);
+            const int64_t row = 2 * pr;
+            A[row + lda * col] = r * cs;
+            if (row + 1 < M) A[row + 1 + lda * col] = r * sn;
+        }
+    } else {
+        const int64_t n = M * ncols;
+        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t row = t % M, col = t / M;
+            const uint64_t h = mix64(seed ^ mix64(sid * 0x100000001B3ull + (uint64_t)col) ^ (uint64_t)row * 0xD6E8FEB86659FD93ull);
+            const double u1 = ((h >> 11) + 1.0) * (1.0 / 9007199254740993.0);
+            const double u2 = (double)(mix64(h) >> 11) * (1.0 / 9007199254740992.0);
             A[row + lda * col] = (T)(sqrt(-2.0 * log(u1)) * cospi(2.0 * u2));
+        }
     }
 }
 
