@@ -753,15 +753,15 @@ update_tc_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, cons
 // Drain / epilogue as in update_tc_kernel (fp32 register sums across chunks, RMW of the tile).
 // ---------------------------------------------------------------------------
 namespace tallu2 {
-constexpr int ROWS = 128, KC = 32, OPB = 4, NBUF = 4, MAXR = 12, NTHR = 512;
+constexpr int ROWS = 128, KC = 32, OPB = 4, NBUF = 4, MAXR = 12, MAXB = 24, NTHR = 512;
 constexpr int SMEM = 226 * 1024;
+constexpr int BRES = 96 * 1024;      // coefficient tiles of all chunks kept resident up to this size
+constexpr int BRING = 8;             // otherwise a ring of this many tiles, released by the MMAs
 template <int NN>
 struct Cfg {
     static constexpr int a_raw = ROWS * KC * 4;             // 16 KB
     static constexpr int b_bytes = 2 * NN * KC * 4;         // hi | lo
-    static constexpr int off_raw = OPB * b_bytes;
     static constexpr int off_bar = SMEM - 2048;
-    static constexpr int RS = (off_bar - off_raw) / a_raw < MAXR ? (off_bar - off_raw) / a_raw : MAXR;
     static_assert(NBUF * NN <= 256 && OPB * 64 <= 256, "TMEM budget");
 };
 }  // namespace tallu2
@@ -769,26 +769,34 @@ struct Cfg {
 template <int NN>
 __global__ void __launch_bounds__(tallu2::NTHR, 1)
 update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, const float *__restrict__ Bpk, int n,
-                  double beta, float *Out, int64_t ldo) {
+                  double beta, float *Out, int64_t ldo, int dbg) {
     using namespace tc;
     using Cf = tallu2::Cfg<NN>;
-    constexpr int RS = Cf::RS, OPB = tallu2::OPB, NBUF = tallu2::NBUF, KC = tallu2::KC;
+    constexpr int OPB = tallu2::OPB, NBUF = tallu2::NBUF, KC = tallu2::KC;
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + Cf::off_bar);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 64);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 96);   // after the 88 barriers
     const uint32_t bar0 = smem_u32(bars);
     auto fulla = [&](int r) { return bar0 + 8u * r; };            // raw A landed          [12]
     auto rawe = [&](int r) { return bar0 + 8u * (12 + r); };      // raw A converted       [12]
-    auto fullb = [&](int o) { return bar0 + 8u * (24 + o); };     // coefficients landed   [4]
-    auto conv = [&](int o) { return bar0 + 8u * (28 + o); };      // A in TMEM             [4]
-    auto ope = [&](int o) { return bar0 + 8u * (32 + o); };       // MMAs of slot o done   [4]
-    auto accf = [&](int b) { return bar0 + 8u * (36 + b); };      // accumulator ready     [4]
-    auto acce = [&](int b) { return bar0 + 8u * (40 + b); };      // accumulator drained   [4]
+    auto conv = [&](int o) { return bar0 + 8u * (24 + o); };      // A in TMEM             [4]
+    auto ope = [&](int o) { return bar0 + 8u * (28 + o); };       // MMAs of A buffer o done [4]
+    auto accf = [&](int b) { return bar0 + 8u * (32 + b); };      // accumulator ready     [4]
+    auto acce = [&](int b) { return bar0 + 8u * (36 + b); };      // accumulator drained   [4]
+    auto fullb = [&](int q) { return bar0 + 8u * (40 + q); };     // coefficient slot landed [24]
+    auto bemp = [&](int q) { return bar0 + 8u * (64 + q); };      // coefficient slot free   [24]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nchk = (m + KC - 1) / KC;
+    // coefficient tiles: all nchk resident (loaded once, reused by every row tile) when they fit,
+    // else a ring of BRING slots that runs ahead of the MMAs (a per-item reload from L2 tied to
+    // the A buffers had put the L2 latency on the item cadence)
+    const bool bres = nchk * Cf::b_bytes <= tallu2::BRES && nchk <= tallu2::MAXB;
+    const int BS = bres ? nchk : tallu2::BRING;
+    const int off_raw = BS * Cf::b_bytes;
+    const int RS = min(tallu2::MAXR, (Cf::off_bar - off_raw) / Cf::a_raw);
     const int64_t ntiles = (M + tallu2::ROWS - 1) / tallu2::ROWS;
     const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * per;
@@ -801,9 +809,12 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
             mbar_init(rawe(r), 4);
         }
         for (int o = 0; o < OPB; ++o) {
-            mbar_init(fullb(o), 1);
             mbar_init(conv(o), 4);
             mbar_init(ope(o), 1);
+        }
+        for (int q = 0; q < BS; ++q) {
+            mbar_init(fullb(q), 1);
+            mbar_init(bemp(q), 1);
         }
         for (int b = 0; b < NBUF; ++b) {
             mbar_init(accf(b), 1);
@@ -823,8 +834,8 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t sm_u = smem_u32(smem);
-    auto bslot = [&](int o) { return sm_u + (uint32_t)(o * Cf::b_bytes); };
-    auto raw = [&](int r) { return sm_u + (uint32_t)(Cf::off_raw + r * Cf::a_raw); };
+    auto bslot = [&](int q) { return sm_u + (uint32_t)(q * Cf::b_bytes); };
+    auto raw = [&](int r) { return sm_u + (uint32_t)(off_raw + r * Cf::a_raw); };
     auto a_col = [&](int o) { return (uint32_t)(256 + 64 * o); };
 
     if (warp == 0) {
@@ -839,25 +850,33 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
         }
     } else if (warp == 2) {
         if (lane == 0) {
-            for (int i = 0; i < nitems; ++i) {
-                const int o = i % OPB;
-                if (i >= OPB) mbar_wait(ope(o), ((i / OPB) - 1) & 1);
-                mbar_expect_tx(fullb(o), Cf::b_bytes);
-                bulk_g2s(bslot(o), Bpk + (size_t)(i % nchk) * (Cf::b_bytes / 4), Cf::b_bytes, fullb(o));
+            if (bres) {
+                for (int ch = 0; ch < nchk && nitems > 0; ++ch) {
+                    mbar_expect_tx(fullb(ch), Cf::b_bytes);
+                    bulk_g2s(bslot(ch), Bpk + (size_t)ch * (Cf::b_bytes / 4), Cf::b_bytes, fullb(ch));
+                }
+            } else {
+                for (int i = 0; i < nitems; ++i) {
+                    const int q = i % BS;
+                    if (i >= BS) mbar_wait(bemp(q), ((i / BS) - 1) & 1);
+                    mbar_expect_tx(fullb(q), Cf::b_bytes);
+                    bulk_g2s(bslot(q), Bpk + (size_t)(i % nchk) * (Cf::b_bytes / 4), Cf::b_bytes, fullb(q));
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = make_idesc(128, NN);
             for (int i = 0; i < nitems; ++i) {
-                const int o = i % OPB, b = i % NBUF;
+                const int o = i % OPB, b = i % NBUF, q = bres ? i % nchk : i % BS;
                 mbar_wait(conv(o), (i / OPB) & 1);
-                mbar_wait(fullb(o), (i / OPB) & 1);
+                mbar_wait(fullb(q), bres ? 0u : (uint32_t)((i / BS) & 1));
                 if (i >= NBUF) mbar_wait(acce(b), ((i / NBUF) - 1) & 1);
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(b * NN);
                 const uint32_t ah = tmem + a_col(o), al = ah + 32;
-                const uint64_t bh = make_desc(bslot(o)), bl = bh + (uint64_t)((NN * KC * 4) >> 4);
+                const uint64_t bh = make_desc(bslot(q)), bl = bh + (uint64_t)((NN * KC * 4) >> 4);
+                if (!(dbg & 2)) {
 #pragma unroll
                 for (int q = 0; q < KC / 8; ++q) {
                     mma_tf32_ts(d, al + 8 * q, bh + 2 * q, idesc, q > 0 ? 1u : 0u);
@@ -865,8 +884,10 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
                 }
 #pragma unroll
                 for (int q = 0; q < KC / 8; ++q) mma_tf32_ts(d, ah + 8 * q, bh + 2 * q, idesc, 1u);
+                }
                 mma_commit(ope(o));
                 mma_commit(accf(b));
+                if (!bres) mma_commit(bemp(q));
             }
         }
     } else if (warp >= 4 && warp < 8) {
@@ -878,7 +899,8 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
             mbar_wait(fulla(r), (i / RS) & 1);
             if (i >= OPB) mbar_wait(ope(o), ((i / OPB) - 1) & 1);
             tc_fence_after();
-            const float *src = reinterpret_cast<const float *>(smem + Cf::off_raw + (size_t)r * Cf::a_raw) + r_l;
+            const float *src = reinterpret_cast<const float *>(smem + off_raw + (size_t)r * Cf::a_raw) + r_l;
+            if (!(dbg & 1)) {
             uint32_t hi[32], lo[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
@@ -890,6 +912,7 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
             tmem_st32(tmem + lane_off + a_col(o), hi);
             tmem_st32(tmem + lane_off + a_col(o) + 32, lo);
             tmem_wait_st();
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -1111,7 +1134,8 @@ static void launch_update_tc2(const float *A, int64_t lda, int64_t M, int m, con
     auto kern = update_tc2_kernel<NN>;
     set_max_smem(kern);
     const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallu2::ROWS));
-    kern<<<ctas, tallu2::NTHR, tallu2::SMEM, st>>>(it->second, M, m, bpk.as<float>(), n, beta, Out, ldo);
+    static const int dbg = [] { const char *e = std::getenv("SSA_UPD_DBG"); return e ? std::atoi(e) : 0; }();
+    kern<<<ctas, tallu2::NTHR, tallu2::SMEM, st>>>(it->second, M, m, bpk.as<float>(), n, beta, Out, ldo, dbg);
     after_launch("update_tc2");
 }
 
