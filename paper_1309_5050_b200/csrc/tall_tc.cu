@@ -753,16 +753,16 @@ update_tc_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, cons
 // Drain / epilogue as in update_tc_kernel (fp32 register sums across chunks, RMW of the tile).
 // ---------------------------------------------------------------------------
 namespace tallu2 {
-constexpr int ROWS = 128, KC = 32, OPB = 4, NBUF = 4, MAXR = 12, MAXB = 24, NTHR = 512;
+constexpr int ROWS = 128, KC = 64, OPB = 2, NBUF = 4, MAXR = 12, MAXB = 24, NTHR = 512;   // KC: A columns per item
 constexpr int SMEM = 226 * 1024;
 constexpr int BRES = 96 * 1024;      // coefficient tiles of all chunks kept resident up to this size
 constexpr int BRING = 8;             // otherwise a ring of this many tiles, released by the MMAs
 template <int NN>
 struct Cfg {
-    static constexpr int a_raw = ROWS * KC * 4;             // 16 KB
-    static constexpr int b_bytes = 2 * NN * KC * 4;         // hi | lo
+    static constexpr int a_raw = ROWS * KC * 4;             // 32 KB
+    static constexpr int b_bytes = 2 * NN * KC * 4;         // two packed 32-column chunks, each hi | lo
     static constexpr int off_bar = SMEM - 2048;
-    static_assert(NBUF * NN <= 256 && OPB * 64 <= 256, "TMEM budget");
+    static_assert(NBUF * NN <= 256 && OPB * 2 * KC <= 256, "TMEM budget");
 };
 }  // namespace tallu2
 
@@ -794,7 +794,7 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
     // else a ring of BRING slots that runs ahead of the MMAs (a per-item reload from L2 tied to
     // the A buffers had put the L2 latency on the item cadence)
     const bool bres = nchk * Cf::b_bytes <= tallu2::BRES && nchk <= tallu2::MAXB;
-    const int BS = bres ? nchk : tallu2::BRING;
+    const int BS = bres ? nchk : max(2, min(tallu2::BRING, (Cf::off_bar - 3 * Cf::a_raw) / Cf::b_bytes));
     const int off_raw = BS * Cf::b_bytes;
     const int RS = min(tallu2::MAXR, (Cf::off_bar - off_raw) / Cf::a_raw);
     const int64_t ntiles = (M + tallu2::ROWS - 1) / tallu2::ROWS;
@@ -836,7 +836,7 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
     const uint32_t sm_u = smem_u32(smem);
     auto bslot = [&](int q) { return sm_u + (uint32_t)(q * Cf::b_bytes); };
     auto raw = [&](int r) { return sm_u + (uint32_t)(off_raw + r * Cf::a_raw); };
-    auto a_col = [&](int o) { return (uint32_t)(256 + 64 * o); };
+    auto a_col = [&](int o) { return (uint32_t)(256 + 2 * KC * o); };   // hi [KC] | lo [KC]
 
     if (warp == 0) {
         if (lane == 0) {
@@ -874,16 +874,22 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
                 if (i >= NBUF) mbar_wait(acce(b), ((i / NBUF) - 1) & 1);
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(b * NN);
-                const uint32_t ah = tmem + a_col(o), al = ah + 32;
-                const uint64_t bh = make_desc(bslot(q)), bl = bh + (uint64_t)((NN * KC * 4) >> 4);
+                const uint32_t ah = tmem + a_col(o), al = ah + KC;
+                // B slot = two 32-column chunks [hi | lo] of NN x 32 each; k-step k: chunk k / 4, k % 4 within
+                const uint64_t b0 = make_desc(bslot(q));
+                constexpr uint64_t lo_step = (uint64_t)((NN * 32 * 4) >> 4), ch_step = 2 * lo_step;
                 if (!(dbg & 2)) {
 #pragma unroll
-                for (int q = 0; q < KC / 8; ++q) {
-                    mma_tf32_ts(d, al + 8 * q, bh + 2 * q, idesc, q > 0 ? 1u : 0u);
-                    mma_tf32_ts(d, ah + 8 * q, bl + 2 * q, idesc, 1u);
+                for (int k = 0; k < KC / 8; ++k) {
+                    const uint64_t bh = b0 + (uint64_t)(k >> 2) * ch_step + (uint64_t)(2 * (k & 3));
+                    mma_tf32_ts(d, al + 8 * k, bh, idesc, k > 0 ? 1u : 0u);
+                    mma_tf32_ts(d, ah + 8 * k, bh + lo_step, idesc, 1u);
                 }
 #pragma unroll
-                for (int q = 0; q < KC / 8; ++q) mma_tf32_ts(d, ah + 8 * q, bh + 2 * q, idesc, 1u);
+                for (int k = 0; k < KC / 8; ++k) {
+                    const uint64_t bh = b0 + (uint64_t)(k >> 2) * ch_step + (uint64_t)(2 * (k & 3));
+                    mma_tf32_ts(d, ah + 8 * k, bh, idesc, 1u);
+                }
                 }
                 mma_commit(ope(o));
                 mma_commit(accf(b));
@@ -901,16 +907,19 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
             tc_fence_after();
             const float *src = reinterpret_cast<const float *>(smem + off_raw + (size_t)r * Cf::a_raw) + r_l;
             if (!(dbg & 1)) {
-            uint32_t hi[32], lo[32];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const float x = src[c * tallu2::ROWS];
-                const uint32_t h = tf32_rna(x);
-                hi[c] = h;
-                lo[c] = __float_as_uint(x - __uint_as_float(h));
+            for (int hh = 0; hh < KC / 32; ++hh) {
+                uint32_t hi[32], lo[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const float x = src[(32 * hh + c) * tallu2::ROWS];
+                    const uint32_t h = tf32_rna(x);
+                    hi[c] = h;
+                    lo[c] = __float_as_uint(x - __uint_as_float(h));
+                }
+                tmem_st32(tmem + lane_off + a_col(o) + 32 * hh, hi);
+                tmem_st32(tmem + lane_off + a_col(o) + KC + 32 * hh, lo);
             }
-            tmem_st32(tmem + lane_off + a_col(o), hi);
-            tmem_st32(tmem + lane_off + a_col(o) + 32, lo);
             tmem_wait_st();
             }
             tc_fence_before();
@@ -1125,7 +1134,7 @@ static void launch_update_tc2(const float *A, int64_t lda, int64_t M, int m, con
         it = cache.emplace(key, make_map2(A, (uint64_t)M, (uint64_t)m, (uint64_t)lda * 4, tallu2::ROWS, tallu2::KC,
                                           false, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)).first;
     }
-    const int nchk = (m + 31) / 32;
+    const int nchk = (m + tallu2::KC - 1) / tallu2::KC * (tallu2::KC / 32);   // 32-column chunks, zero padded
     static thread_local DevBuf bpk;
     const size_t need = sizeof(float) * (size_t)nchk * 2 * NN * 32;
     if (bpk.bytes < need) bpk.alloc(need, st);
