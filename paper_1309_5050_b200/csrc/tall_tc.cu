@@ -1195,10 +1195,13 @@ bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int
         SSA_CUDA(cudaMemset(trace_buf, 0, 8 * 64 * 8));
         SSA_CUDA(cudaMemcpyToSymbol(g_gram_trace, &trace_buf, sizeof(trace_buf)));
     }
+    static const bool nm2 = [] { const char *e = std::getenv("SSA_GRAM_NM2"); return !e || std::atoi(e) != 0; }();
     // narrow blocks (n1 <= 64, e.g. the CholeskyQR Gram WᵀW): a 64-column A box, B read from the A tile
     if (n2 <= 32) {
         if (n1 <= 64) launch_gram_tc<1, 32, 64>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
-        else if (n1 <= 128) launch_gram_tc<1, 32, 128>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+        // two M-tiles per CTA (B read once per 256 columns) up to 256 columns; above that a second
+        // nearly empty y-block made it slower than 128-column CTAs (n1 = 288: 136 vs 107 µs)
+        else if (n1 <= 128 || n1 > 256 || !nm2) launch_gram_tc<1, 32, 128>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
         else launch_gram_tc<2, 32, 128>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
     } else {
         if (n1 <= 64) launch_gram_tc<1, 64, 64>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
