@@ -629,13 +629,6 @@ struct Gkl {
             }
             const bool was_projection = project;
             project = (pass == 1 && reproject);
-            static const bool onepass = std::getenv("SSA_ORTH3_ONEPASS") != nullptr;   // timing experiment only
-            if (onepass && !project && !shifted) {
-                if (coef)
-                    for (size_t t = 0; t < Ctot.size(); ++t) coef[t] += Ctot[t];
-                ++n_fast;
-                return Btot;
-            }
             if (pass >= 2 && !project && !shifted && !was_projection && dev <= 0.1) {
                 if (coef)
                     for (size_t t = 0; t < Ctot.size(); ++t) coef[t] += Ctot[t];
