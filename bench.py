@@ -277,6 +277,14 @@ def run_ours(args, rank, world, dist):
     roof["note"] = ("a 'launch' is one block product of k vectors (FFT: 3 passes; tc: pack + MMA kernel"
                     " + split reduce); events bracket it on the plan's stream, so host launch gaps count")
     roof["products"] = prods
+    # where the rest of the step goes (the products are the kernels SURVEY §8(d) sizes; on the small
+    # configs the Ritz SVD and the orthonormalisation take more of the step)
+    ms_ritz_step = float(np.sum([i["ms_ritz"] for i in infos])) / args.steps
+    ms_step = ms_all / args.steps
+    prod_share = float(sum(r["share_of_step"] for r in prods.values()))
+    roof["step_shares"] = {"products": prod_share,
+                           "ritz_svd (jacobi_gram_kernel, latency bound)": ms_ritz_step / max(ms_step, 1e-9),
+                           "orthonormalisation + host": max(0.0, 1.0 - prod_share - ms_ritz_step / max(ms_step, 1e-9))}
     res = {
         "metric": "trajectory products/s",
         "value": nvec_all / (ms_all / 1e3),
