@@ -169,7 +169,9 @@ def run_ours(args, rank, world, dist):
         with torch.cuda.stream(stream):
             t0 = time.perf_counter()
             src = host_src if host else img_dev
-            msk = (mask_pin.t().numpy() if mask_pin is not None else None) if host else mask_np
+            # the ABI takes the 𝔑 mask from host memory on both paths: the pinned, column-major copy
+            # (a C-ordered numpy mask cost a host transpose-copy per step: c4 11.3 vs 10.2 ms)
+            msk = mask_pin.t().numpy() if mask_pin is not None else None
             p = Plan(src, w.window, mask=msk, wmask=w.wmask, dtype=w.dtype, block_k=w.block_k,
                      path=args.path, stream=stream.cuda_stream)
             t1 = time.perf_counter()
