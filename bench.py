@@ -68,39 +68,14 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
-    def _nvml_sampler(self):
-        # in-process NVML queries: spawning nvidia-smi inside the timed region cost host time that
-        # the host-bound small configs felt (same fields as the nvidia-smi query)
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
-            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
-            bits = (0x8, 0x40, 0x20, 0x4)   # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
-
-            def sample():
-                r = get_reasons(h)
-                return [str(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
-                        str(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))] + \
-                       ["Active" if r & b else "Not Active" for b in bits]
-            sample()
-            return sample
-        except Exception:
-            return None
-
     def _run(self):
-        sample = self._nvml_sampler()
         while not self._stop.is_set():
             try:
-                if sample is not None:
-                    self.samples.append(sample())
-                else:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([s.strip() for s in out.split(",")])
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
             self._stop.wait(0.2)
