@@ -845,9 +845,19 @@ struct Gkl {
             }
             ritz_tn(m, n, T0d, Ad, Wd, nrmd, st);
             // A | T0 | W | nrm: fetch A, then W and nrm (contiguous)
-            std::vector<double> A(mn), Wn((size_t)n * n + n);
-            SSA_CUDA(cudaMemcpyAsync(A.data(), Ad, sizeof(double) * mn, cudaMemcpyDeviceToHost, st));
-            SSA_CUDA(cudaMemcpyAsync(Wn.data(), Wd, sizeof(double) * ((size_t)n * n + n), cudaMemcpyDeviceToHost, st));
+            // read-back into a grow-only pinned block kept per thread (pageable / freshly allocated
+            // host buffers cost page faults and bounce-buffer copies on every Ritz step)
+            static thread_local double *rpin = nullptr;
+            static thread_local size_t rcap = 0;
+            const size_t need_d = mn + (size_t)n * n + n;
+            if (rcap < need_d) {
+                if (rpin) SSA_CUDA(cudaFreeHost(rpin));
+                rcap = std::max(need_d, 2 * rcap);
+                SSA_CUDA(cudaMallocHost(&rpin, sizeof(double) * rcap));
+            }
+            double *const A = rpin, *const Wn = rpin + mn;
+            SSA_CUDA(cudaMemcpyAsync(A, Ad, sizeof(double) * mn, cudaMemcpyDeviceToHost, st));
+            SSA_CUDA(cudaMemcpyAsync(Wn, Wd, sizeof(double) * ((size_t)n * n + n), cudaMemcpyDeviceToHost, st));
             sg.sync();
             if (debug) {
                 float jms = 0.f;
@@ -855,7 +865,7 @@ struct Gkl {
                 last_kernel_ms = jms;
                 cudaEventDestroy(je0); cudaEventDestroy(je1);
             }
-            const double *nrm = Wn.data() + (size_t)n * n;
+            const double *nrm = Wn + (size_t)n * n;
             std::vector<int> idx(n);
             for (int j = 0; j < n; ++j) idx[j] = j;
             std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return nrm[a] > nrm[b]; });
@@ -871,7 +881,7 @@ struct Gkl {
             if (th[need - 1] > floor_rel * th[0]) {
                 for (int j = 0; j < need; ++j) {
                     const double inv2 = 1.0 / (th[j] * th[j]);
-                    const double *wc = Wn.data() + (size_t)n * idx[j];
+                    const double *wc = Wn + (size_t)n * idx[j];
                     for (int c = 0; c < n; ++c) Z[c + (size_t)n * j] = wc[c] * inv2;
                 }
                 done = true;
