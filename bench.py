@@ -4,18 +4,22 @@
 One STEP = one pass of the whole hot path over one
 synthetic input: plan (embedding: shapes, 𝔎, weights), block-Lanczos rank-r
 decomposition driven by X·V / Xᵀ·U block products, and the grouped diagonal-
-averaging reconstruction.  Default workload: BASELINE.json configs[1] (c2, MSSA
-8 x 4096, L = 1024, r = 16, block k = 32); --config c1..c5 selects another.
+averaging reconstruction.  Default workload: c5 (BASELINE.json configs[4], the
+north star's largest config: 2D-SSA 4096² fp32, window 256², r = 50, block k = 64)
+at N = 1; --config c1..c5 selects another.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
 Metric: trajectory products/s = vector products (X·v or Xᵀ·u) completed per
 second of whole-step time, summed over ranks (weak scaling: every rank
-decomposes its own input, no data-path collective).  `e2e` is the same metric
-through the C ABI with host buffers (H2D of the input and D2H of the
-reconstructions inside the timed region).  `roofline` reports the trajectory block
-product with the larger share of the step against the roofline of the path that served
-it (FFT: HBM bytes model; tc: 3xTF32 tensor peak; direct: FFMA), DESIGN.md §6.
+decomposes its own input, no data-path collective).  `rank_r_time_ms` is the
+device time of the decomposition alone (plan and reconstruction
+are reported beside it, §8(d)(3-4)); `products_only` is the metric over the
+block products' device time alone.  `e2e` is the same metric through the C ABI
+with host buffers (H2D of the input and D2H of the reconstructions inside the
+timed region).  `roofline` reports the trajectory block product with the larger
+share of the step against the roofline of the path that served it (FFT: HBM bytes
+model; tc: measured tcgen05 tf32 peak / 3; direct: FFMA), DESIGN.md §6.
 """
 from __future__ import annotations
 
@@ -36,9 +40,12 @@ FFMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 TF: 148 SM x 128 FP32
 FP64_PEAK_TFLOPS = FFMA_PEAK_TFLOPS / 2               # B200 non-tensor FP64 = 1/2 FP32 rate
 
 
+TRAFFIC_FILE = os.path.join("profiles", "r02", "traffic.json")
+
+
 def _traffic(config, product, path, k):
-    """DRAM bytes per block product from the committed ncu capture (profiles/r01/traffic.json), or None."""
-    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic.json")
+    """DRAM bytes per block product from the committed ncu capture (profiles/r02/traffic.json), or None."""
+    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), TRAFFIC_FILE)
     try:
         with open(f) as fh:
             for e in json.load(fh)["entries"]:
@@ -100,6 +107,16 @@ class ClockSampler:
                 "reasons": reasons, "n_samples": len(self.samples)}
 
 
+def measured_tf32_peak():
+    """Dense tcgen05 kind::tf32 TFLOP/s measured on this GPU (library microbenchmark)."""
+    import ctypes
+    from paper_1309_5050_b200 import _lib
+    L = _lib.load()
+    ms, tf = ctypes.c_double(), ctypes.c_double()
+    _lib.check(L.ssa_bench_mma(100000, 0, ctypes.byref(ms), ctypes.byref(tf)))
+    return float(tf.value)
+
+
 def workload(name, seed_offset=0):
     import synth
     fn = synth.CONFIGS[name]
@@ -140,8 +157,13 @@ def run_ours(args, rank, world, dist):
         mask_pin.copy_(torch.as_tensor(np.ascontiguousarray(mask_np.T.astype(np.uint8))))
     out_pin = torch.empty((len(groups), ny_, nx_), dtype=dt_torch, pin_memory=True)
 
-    def step(host=False):
+    phase_dev = []   # device ms of (plan, decompose, reconstruct) per timed step
+
+    def step(host=False, events=False):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if events else None
         with torch.cuda.stream(stream):
+            if ev:
+                ev[0].record(stream)
             t0 = time.perf_counter()
             src = host_src if host else img_dev
             # the ABI takes the 𝔑 mask from host memory on both paths: the pinned, column-major copy
@@ -150,15 +172,24 @@ def run_ours(args, rank, world, dist):
             p = Plan(src, w.window, mask=msk, wmask=w.wmask, dtype=w.dtype, block_k=w.block_k,
                      path=args.path, stream=stream.cuda_stream)
             t1 = time.perf_counter()
+            if ev:
+                ev[1].record(stream)
             info = p.decompose(w.r, allow_not_converged=True)
+            if ev:
+                ev[2].record(stream)
             t2 = time.perf_counter()
             recs = (p.reconstruct(groups, add_rest=False, device=False, out=out_pin.numpy()) if host
                     else p.reconstruct(groups, add_rest=False, device=True))
+            if ev:
+                ev[3].record(stream)
             t3 = time.perf_counter()
             p.close()
             t4 = time.perf_counter()
         phases.append({"plan_ms": (t1 - t0) * 1e3, "decompose_ms": (t2 - t1) * 1e3,
                        "reconstruct_ms": (t3 - t2) * 1e3, "destroy_ms": (t4 - t3) * 1e3})
+        if ev:
+            ev[3].synchronize()
+            phase_dev.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])])
         return info, recs, p
 
     # warm-up (also compiles nothing: the library is AOT-built)
@@ -178,7 +209,7 @@ def run_ours(args, rank, world, dist):
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            info, recs, _ = step()
+            info, recs, _ = step(events=True)
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
@@ -218,6 +249,7 @@ def run_ours(args, rank, world, dist):
     # separately for X·V and Xᵀ·U; each product is held against the roofline of the path
     # that served it, and the one with the larger share of the step is the headline
     peaks = _peaks()
+    tf32_measured = measured_tf32_peak()
     esz = 8 if w.dtype == "f64" else 4
     nx_, ny_ = np.asarray(w.data).shape
     kx_, ky_ = nx_ - w.window[0] + 1, ny_ - w.window[1] + 1
@@ -241,15 +273,13 @@ def run_ours(args, rank, world, dist):
                  "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)", "algorithmic_bytes_per_launch": alg}
         elif path == "tc":
-            # tcgen05 kind::tf32, 3 MMAs per useful multiply-add (3xTF32): the useful-flop peak is
-            # the dense TF32 peak / 3; TF32 = measured sustained bf16 x nominal ratio 1.1/2.25
-            tf32 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)) * (1.1 / 2.25)
-            peak = tf32 / 3.0
+            # tcgen05 kind::tf32, 3 MMAs per useful multiply-add (3xTF32): the useful-flop peak is the
+            # dense TF32 peak / 3, with the TF32 peak measured in this run (ssa_bench_mma)
+            peak = tf32_measured / 3.0
             achieved = flops / (avg_ms / 1e3) / 1e12
             r = {"bound": "tensor", "kernel": f"{name}: tcgen05 3xTF32 polyphase implicit GEMM (hankel_tc)",
                  "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x 1.1/2.25 (nominal tf32/bf16) / 3 "
-                                "(3xTF32), of measured",
+                 "peak_source": "measured: ssa_bench_mma tcgen05 kind::tf32 M128 N256 back-to-back, / 3 (3xTF32)",
                  "algorithmic_flops_per_launch": flops, "tensor_flops_per_launch": 3 * flops}
         else:
             peak = FP64_PEAK_TFLOPS if w.dtype == "f64" else FFMA_PEAK_TFLOPS
@@ -287,6 +317,8 @@ def run_ours(args, rank, world, dist):
     roof["step_shares"] = {"products": prod_share,
                            "ritz_svd (jacobi_gram_kernel, latency bound)": ms_ritz_step / max(ms_step, 1e-9),
                            "orthonormalisation + host": max(0.0, 1.0 - prod_share - ms_ritz_step / max(ms_step, 1e-9))}
+    ph = np.mean(np.array(phase_dev), axis=0) if phase_dev else [float("nan")] * 3
+    nvec_step = nvec_local / args.steps
     res = {
         "metric": "trajectory products/s",
         "value": nvec_all / (ms_all / 1e3),
@@ -303,7 +335,14 @@ def run_ours(args, rank, world, dist):
                    "groups": len(groups), "path": {"xv": p.path_xv, "xtu": p.path_xtu},
                    "l2": "flushed (256 MB write) between timed steps",
                    "parallelism": f"replicas x{world} (independent inputs per rank)"},
-        "rank_r_time_ms": ms_all / args.steps,
+        "rank_r_time_ms": float(ph[1]),
+        "phases_device_ms": {"plan": float(ph[0]), "decompose": float(ph[1]), "reconstruct": float(ph[2]),
+                             "note": "CUDA events on the plan's stream between the synchronous ABI calls; "
+                                     "rank_r_time_ms = decompose (SURVEY §8(d)(2)), plan and reconstruction "
+                                     "reported beside it (§8(d)(3-4))"},
+        "products_only": {"value": nvec_step / (ms_prod / args.steps / 1e3), "unit": "vector products/s",
+                          "ms_per_step": ms_prod / args.steps,
+                          "note": "vector products over the device time of the block products alone"},
         "decomposition": {"n_block_products": infos[-1]["n_block_products"],
                           "n_vector_products": infos[-1]["n_vector_products"],
                           "n_restarts": infos[-1]["n_restarts"], "n_converged": infos[-1]["n_converged"],
@@ -315,6 +354,8 @@ def run_ours(args, rank, world, dist):
                 "d2h_bytes_per_step": d2h, "ms_per_step": float(np.mean(e2e_times))},
         "gpu_launches": int(launches),
         "roofline": roof,
+        "peaks_measured_here": {"tf32_dense_tflops": tf32_measured,
+                                "source": "ssa_bench_mma: 148 CTAs x 100k tcgen05.mma kind::tf32 128x256x8"},
         "clocks": clk.summary(),
     }
     return res, w
@@ -330,7 +371,10 @@ def oracle_products_per_s(w, budget_s=15.0):
     x = np.array(w.data, dtype=np.float64)
     if w.dtype == "f32":
         x = x.astype(np.float32).astype(np.float64)
-    sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
+    if w.mask is None and w.wmask is None and np.all(np.isfinite(x)) and x.size > (1 << 22):
+        sh = oracle.shapes_rect(*x.shape, *w.window)   # full rectangle: the brute-force 𝔎 scan is infeasible at c5
+    else:
+        sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
     rng = np.random.default_rng(0)
     k = w.block_k
     V = rng.normal(size=(sh.K, k)); U = rng.normal(size=(sh.L, k))
@@ -468,7 +512,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")

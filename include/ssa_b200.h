@@ -72,7 +72,7 @@ typedef enum {
     SSA_PATH_DIRECT = 1,   /* smem-tiled implicit GEMM on CUDA cores (Hankel sliding window) */
     SSA_PATH_FFT = 2,      /* shared-memory radix FFT circular correlation (Alg. 1/3) */
     SSA_PATH_TC = 3        /* tcgen05 tensor-core implicit GEMM, 3xTF32 split (fp32 plans; products
-                              whose output box has < 96 rows fall back to FFT / direct) */
+                              whose output box has < 256 rows fall back to FFT / direct) */
 } ssa_path;
 
 typedef struct {
@@ -105,7 +105,12 @@ typedef struct {
     int max_products;      /* cap on block products in ssa_decompose (0 = auto) */
     uint64_t seed;         /* seed of the Lanczos start block (counter-based RNG) */
     const ssa_comm *comm;  /* NULL = single GPU */
-    int64_t band_y0, band_y1; /* this rank's κy range [y0, y1) of 𝔎 when comm != NULL */
+    int64_t band_y0, band_y1; /* band plans (comm != NULL, world > 1): this rank's global origin columns
+                                 [y0, y1); x is then the sub-image of global columns [y0, y1 + Ly − 1)
+                                 (band + (Ly−1)-column halo) */
+    int precision;         /* arithmetic type of the plan: 0 = the input's dtype, 1 = fp32, 2 = fp64
+                              (the input is cast once at plan creation); SSA_ERR_ARG otherwise */
+    int64_t ny_global;     /* band plans: number of columns of the global image */
 } ssa_opts;
 
 typedef struct {
@@ -130,6 +135,13 @@ typedef struct {
     double ms_products_xv, ms_products_xtu;   /* device time of the X·V / Xᵀ·U block products */
     int64_t n_products_xv, n_products_xtu;    /* block products of each kind */
     int64_t n_vectors_xv, n_vectors_xtu;      /* vectors pushed through each product */
+    /* reading Q10: the σ floor τ of the product path (σ_i < τ·σ_1 cannot be resolved
+     * in the path's arithmetic; τ measured on the noiseless twins) and how many returned triples lie
+     * below it */
+    double sigma_floor_rel;
+    int32_t n_below_floor;
+    int32_t warm_start_cols;          /* start-block columns taken from the previous decomposition */
+    double drop_norm_rel;             /* norm of block columns discarded as numerically zero, / ||X|| */
 } ssa_decomp_info;
 
 typedef struct ssa_plan_s *ssa_plan;
@@ -159,9 +171,12 @@ ssa_status ssa_matmul(ssa_plan p, int transpose, const void *in, int64_t ldin,
                       void *out, int64_t ldout, int64_t k, int on_device);
 
 /* Step 2: top-r eigentriples (σ_i, U_i, V_i) of X by block Golub-Kahan-Lanczos
- * bidiagonalisation with thick restarts, σ descending.
- * Continues from the stored basis when called again with a larger r.
- * info may be NULL. */
+ * bidiagonalisation with thick restarts, σ descending.  Converged means
+ * ||Xᵀu_i − σ_i v_i|| <= tol·σ_1 for all i < r (residual bounds: ssa_get_residuals).  Called again
+ * on a plan that holds a decomposition (e.g. with a larger r), the Lanczos start block is warm-started
+ * from the stored eigenvectors U_1..U_min(r_prev, k) ("automatically continued").
+ * SSA_ERR_NOT_CONVERGED when max_products is reached first (the r triples are still returned,
+ * with their residual bounds).  info may be NULL. */
 ssa_status ssa_decompose(ssa_plan p, int32_t r, ssa_decomp_info *info);
 
 /* Getters (valid after ssa_decompose or ssa_set_triples).  sigma: r doubles.
@@ -169,6 +184,8 @@ ssa_status ssa_decompose(ssa_plan p, int32_t r, ssa_decomp_info *info);
  * P:1720-1723).  Signs: the largest-|.| entry of each U_i is positive. */
 ssa_status ssa_get_rank(ssa_plan p, int32_t *r);
 ssa_status ssa_get_sigma(ssa_plan p, double *sigma);
+/* Per-triple residual bounds ||Xᵀu_i − σ_i v_i|| (r doubles, absolute) of the last decomposition. */
+ssa_status ssa_get_residuals(ssa_plan p, double *res);
 ssa_status ssa_get_u(ssa_plan p, void *U, int on_device);
 ssa_status ssa_get_v(ssa_plan p, void *V, int on_device);
 
@@ -181,14 +198,18 @@ ssa_status ssa_set_triples(ssa_plan p, int32_t r, const double *sigma, const voi
  * 0-based eigentriple indices < r.  out: (n_groups + add_rest) arrays of nx*ny
  * (column-major, ld = nx), each  X̃_g = diagsums(Σ_{i∈I_g} σ_i U_i V_iᵀ) / 𝕎  on 𝔑′
  * and NaN elsewhere (Alg. 4; values exist only inside 𝔑′,
- * P:3214-3217).  add_rest appends 𝕏 − Σ_g X̃_g on 𝔑′ (eq. P:440-443). */
+ * P:3214-3217).  add_rest appends 𝕏 − Σ_g X̃_g on 𝔑′ (eq. P:440-443).
+ * A group index >= the computed rank continues the decomposition first (decompose(max index + 1),
+ * P:869-873); SSA_ERR_RANK if an index is >= min(L, K). */
 ssa_status ssa_reconstruct(ssa_plan p, const int32_t *grp_off, const int32_t *grp_idx,
                            int32_t n_groups, int add_rest, void *out, int on_device);
 
 /* w-correlation matrix of the groups' reconstructions:
- * rho (n_groups x n_groups, column-major double) = (X̃_a, X̃_b)_w / (‖X̃_a‖_w ‖X̃_b‖_w). */
+ * rho (n_groups x n_groups, column-major double) = (X̃_a, X̃_b)_w / (‖X̃_a‖_w ‖X̃_b‖_w), with the
+ * weighted inner product (Y, Z)_w = Σ_n w_n y_n z_n; and, when contrib is non-NULL,
+ * the contributions ‖X̃_g‖²_w / ‖𝕏‖²_w (n_groups doubles).  1 <= n_groups <= 63. */
 ssa_status ssa_wcor(ssa_plan p, const int32_t *grp_off, const int32_t *grp_idx,
-                    int32_t n_groups, double *rho);
+                    int32_t n_groups, double *rho, double *contrib);
 
 /* The solver's projected-matrix SVD as a utility: one-sided
  * block Jacobi in fp64 on the device (one thread-block cluster for n <= 256, a
@@ -205,10 +226,14 @@ ssa_status ssa_small_svd(int32_t m, int32_t n, double *A, int32_t *sweeps, doubl
  * *ms = average device milliseconds over `reps` launches after one warm-up;
  * *check = max relative error against an fp64 host evaluation (update: on ~1000 sampled
  * rows; Gram: all entries when M·n1·n2 <= 5e8, else the checksum Σ|G|).  which = 3 times
- * the self Gram AᵀA[:, :n2]; which = 4 is a TMA streaming probe (n2 = box columns + 256 x row
- * groups).  SSA_ERR_ARG on bad sizes. */
+ * the self Gram AᵀA[:, :n2].  SSA_ERR_ARG on bad sizes. */
 ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32_t n2, int32_t reps, double *ms,
                           double *check);
+
+/* Measured tensor-core peak (roofline denominator of the tcgen05 kernels): `ctas` CTAs (0 = one per
+ * SM) each issue `iters` back-to-back tcgen05.mma kind::tf32 M=128 N=256 K=8 from shared memory.
+ * *ms = device time, *tflops = dense tf32 TFLOP/s (2·128·256·8 per MMA). */
+ssa_status ssa_bench_mma(int32_t iters, int32_t ctas, double *ms, double *tflops);
 
 const char *ssa_last_error(void);
 const char *ssa_version(void);

@@ -136,6 +136,20 @@ def shapes(img, window, mask=None, wmask=None) -> Shapes:
     return Shapes(nx, ny, lx, ly, nmask, wm, kmask, w)
 
 
+def shapes_rect(nx, ny, lx, ly) -> Shapes:
+    """Shapes of a full Nx x Ny array with the full Lx x Ly window, without the brute-force scan
+    (for sizes where it is infeasible, e.g. c5): every origin is valid (eq. P:3004-3005 with 𝔑 the
+    whole grid), and the weights are the product of the 1-D hit counts w_i = min(i+1, L, K, N−i)
+    (P:3702-3704 per axis; for rectangles 𝕎 = w_x ⊗ w_y, pin P3)."""
+    def w1(n, l):
+        k = n - l + 1
+        i = np.arange(n)
+        return np.minimum(np.minimum(i + 1, n - i), min(l, k))
+    w = np.asfortranarray(np.outer(w1(nx, lx), w1(ny, ly)).astype(np.int32))
+    return Shapes(nx, ny, lx, ly, np.ones((nx, ny), np.uint8, order="F"), np.ones((lx, ly), np.uint8, order="F"),
+                  np.ones((nx - lx + 1, ny - ly + 1), np.uint8, order="F"), w)
+
+
 def _image(img, sh: Shapes):
     """Image with cells outside 𝔑 set to 0 (they never enter 𝒯(𝕏))."""
     x = np.array(img, dtype=np.float64, copy=True)
@@ -276,6 +290,15 @@ def reconstruct_cells(sh: Shapes, sigma, U, V, group, cells):
     ok = w > 0
     out[ok] = num[ok] / w[ok]
     return out
+
+
+def contributions(sh: Shapes, recs, img):
+    """Contributions of reconstructed components: ||X̃_j||²_w / ||X||²_w with the
+    weighted norm ||Y||²_w = Σ_n w_n y_n² (w_n = 0 off 𝔑′, cells outside 𝔑 are 0)."""
+    w = sh.weights.astype(np.float64)
+    x = np.where(sh.nmask.astype(bool), np.nan_to_num(np.asarray(img, dtype=np.float64)), 0.0)
+    den = np.sum(w * x * x)
+    return np.array([np.sum(w * np.nan_to_num(r) ** 2) for r in recs]) / den
 
 
 def wcorr(sh: Shapes, recs):

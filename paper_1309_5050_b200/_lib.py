@@ -37,7 +37,8 @@ class ssa_comm(C.Structure):
 class ssa_opts(C.Structure):
     _fields_ = [("stream", C.c_void_p), ("path", C.c_int), ("block_k", C.c_int), ("tol", C.c_double),
                 ("max_products", C.c_int), ("seed", C.c_uint64), ("comm", C.POINTER(ssa_comm)),
-                ("band_y0", C.c_int64), ("band_y1", C.c_int64)]
+                ("band_y0", C.c_int64), ("band_y1", C.c_int64), ("precision", C.c_int),
+                ("ny_global", C.c_int64)]
 
 
 class ssa_plan_info_t(C.Structure):
@@ -53,13 +54,15 @@ class ssa_decomp_info(C.Structure):
                 ("max_rel_residual", C.c_double), ("ms_products", C.c_double), ("ms_total", C.c_double),
                 ("ms_ritz", C.c_double), ("ms_products_xv", C.c_double), ("ms_products_xtu", C.c_double),
                 ("n_products_xv", C.c_int64), ("n_products_xtu", C.c_int64),
-                ("n_vectors_xv", C.c_int64), ("n_vectors_xtu", C.c_int64)]
+                ("n_vectors_xv", C.c_int64), ("n_vectors_xtu", C.c_int64),
+                ("sigma_floor_rel", C.c_double), ("n_below_floor", C.c_int32), ("warm_start_cols", C.c_int32),
+                ("drop_norm_rel", C.c_double)]
 
 
 EXPORTS = ["ssa_plan_create", "ssa_plan_destroy", "ssa_plan_info", "ssa_get_weights", "ssa_get_kmask",
-           "ssa_matmul", "ssa_decompose", "ssa_get_rank", "ssa_get_sigma", "ssa_get_u", "ssa_get_v",
+           "ssa_matmul", "ssa_decompose", "ssa_get_rank", "ssa_get_sigma", "ssa_get_residuals", "ssa_get_u", "ssa_get_v",
            "ssa_set_triples", "ssa_reconstruct", "ssa_wcor", "ssa_last_error", "ssa_version",
-           "ssa_launch_count", "ssa_small_svd", "ssa_bench_tall"]
+           "ssa_launch_count", "ssa_small_svd", "ssa_bench_tall", "ssa_bench_mma"]
 
 _lib = None
 
@@ -91,11 +94,12 @@ def load(path: str = SO_PATH):
     L.ssa_decompose.argtypes = [p, i32, C.POINTER(ssa_decomp_info)]; L.ssa_decompose.restype = st
     L.ssa_get_rank.argtypes = [p, C.POINTER(i32)]; L.ssa_get_rank.restype = st
     L.ssa_get_sigma.argtypes = [p, p]; L.ssa_get_sigma.restype = st
+    L.ssa_get_residuals.argtypes = [p, p]; L.ssa_get_residuals.restype = st
     L.ssa_get_u.argtypes = [p, p, C.c_int]; L.ssa_get_u.restype = st
     L.ssa_get_v.argtypes = [p, p, C.c_int]; L.ssa_get_v.restype = st
     L.ssa_set_triples.argtypes = [p, i32, p, p, p, C.c_int]; L.ssa_set_triples.restype = st
     L.ssa_reconstruct.argtypes = [p, p, p, i32, C.c_int, p, C.c_int]; L.ssa_reconstruct.restype = st
-    L.ssa_wcor.argtypes = [p, p, p, i32, p]; L.ssa_wcor.restype = st
+    L.ssa_wcor.argtypes = [p, p, p, i32, p, p]; L.ssa_wcor.restype = st
     L.ssa_last_error.argtypes = []; L.ssa_last_error.restype = C.c_char_p
     L.ssa_version.argtypes = []; L.ssa_version.restype = C.c_char_p
     L.ssa_launch_count.argtypes = [C.c_int]; L.ssa_launch_count.restype = i64
@@ -103,6 +107,8 @@ def load(path: str = SO_PATH):
     L.ssa_small_svd.restype = st
     L.ssa_bench_tall.argtypes = [i32, C.c_int64, i32, i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.ssa_bench_tall.restype = st
+    L.ssa_bench_mma.argtypes = [i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.ssa_bench_mma.restype = st
     _lib = L
     return L
 

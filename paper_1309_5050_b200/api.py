@@ -41,7 +41,10 @@ class Plan:
     """An embedding of one array (step 1) with its device-side operator data."""
 
     def __init__(self, x, window, mask=None, wmask=None, *, dtype=None, path="auto", block_k=0,
-                 tol=0.0, max_products=0, seed=0, stream=None, comm=None, band=None):
+                 tol=0.0, max_products=0, seed=0, stream=None, comm=None, band=None, ny_global=None,
+                 precision=None):
+        """`comm`/`band`/`ny_global`: a band plan of the window-position partition (see
+        dist.band_plan): x is this rank's sub-image = global columns [band[0], band[1] + Ly − 1)."""
         self._L = lib.load()
         self._h = C.c_void_p()
         lx, ly = int(window[0]), int(window[1])
@@ -89,10 +92,16 @@ class Plan:
         o.tol = float(tol)
         o.max_products = int(max_products)
         o.seed = int(seed)
+        # arithmetic type of the plan when it differs from the input's ("f32" / "f64")
+        o.precision = {None: 0, "f32": 1, "f64": 2}[precision]
+        if precision is not None:
+            self.dtype = precision
+            self._np_dtype = np.float64 if precision == "f64" else np.float32
         if comm is not None:
             self._comm = comm
             o.comm = C.pointer(comm.struct())
             o.band_y0, o.band_y1 = band
+            o.ny_global = int(ny_global) if ny_global is not None else 0
         self._opts = o
         lib.check(self._L.ssa_plan_create(C.byref(arr), C.byref(win), mptr, C.byref(o), C.byref(self._h)))
         self._keep = []  # the plan deep-copied its inputs
@@ -106,6 +115,9 @@ class Plan:
         self.path_xtu = lib.PATH_NAMES.get(inf.path_xtu, str(inf.path_xtu))
         self.full_window, self.full_kshape = bool(inf.full_window), bool(inf.full_kshape)
         self.decomp_info = None
+        # band plans reconstruct the global image (the ranks' bands assembled)
+        self.band = tuple(band) if (comm is not None and comm.world > 1) else None
+        self.ny_out = int(ny_global) if self.band else self.ny
 
     # ------------------------------------------------------------ lifetime
     def close(self):
@@ -178,15 +190,31 @@ class Plan:
         lib.check(self._L.ssa_get_sigma(self._h, s.ctypes.data))
         return s
 
-    def U(self) -> np.ndarray:
-        u = np.zeros((self.L, self.r), dtype=self._np_dtype, order="F")
-        lib.check(self._L.ssa_get_u(self._h, u.ctypes.data, 0))
-        return u
+    @property
+    def residuals(self) -> np.ndarray:
+        """Residual bounds ||Xᵀu_i − σ_i v_i|| of the last decomposition (absolute)."""
+        s = np.zeros(self.r, dtype=np.float64)
+        lib.check(self._L.ssa_get_residuals(self._h, s.ctypes.data))
+        return s
 
-    def V(self) -> np.ndarray:
-        v = np.zeros((self.K, self.r), dtype=self._np_dtype, order="F")
-        lib.check(self._L.ssa_get_v(self._h, v.ctypes.data, 0))
-        return v
+    def _getter(self, fn, n, device):
+        if device:
+            torch = _torch()
+            td = torch.float64 if self.dtype == "f64" else torch.float32
+            o = torch.empty((self.r, n), dtype=td, device="cuda")
+            lib.check(fn(self._h, o.data_ptr(), 1))
+            return o.t()
+        o = np.zeros((n, self.r), dtype=self._np_dtype, order="F")
+        lib.check(fn(self._h, o.ctypes.data, 0))
+        return o
+
+    def U(self, device=False):
+        """Eigenvectors U (L x r, 𝔏-lex order); a CUDA tensor with device=True."""
+        return self._getter(self._L.ssa_get_u, self.L, device)
+
+    def V(self, device=False):
+        """Factor vectors V_i = Xᵀ U_i / σ_i (K x r, 𝔎-lex order)."""
+        return self._getter(self._L.ssa_get_v, self.K, device)
 
     def set_triples(self, sigma, U, V=None):
         s = np.ascontiguousarray(sigma, dtype=np.float64)
@@ -213,28 +241,32 @@ class Plan:
         off, idx = self._csr(groups)
         n = len(groups) + (1 if add_rest else 0)
         if out is not None and not device:
-            assert out.shape == (n, self.ny, self.nx) and out.dtype == self._np_dtype and out.flags["C_CONTIGUOUS"]
+            assert out.shape == (n, self.ny_out, self.nx) and out.dtype == self._np_dtype and out.flags["C_CONTIGUOUS"]
             lib.check(self._L.ssa_reconstruct(self._h, off.ctypes.data, idx.ctypes.data, len(groups),
                                               int(add_rest), out.ctypes.data, 0))
             return [out[g].T for g in range(n)]
         if device:
             torch = _torch()
             td = torch.float64 if self.dtype == "f64" else torch.float32
-            o = torch.empty((n, self.ny, self.nx), dtype=td, device="cuda")
+            o = torch.empty((n, self.ny_out, self.nx), dtype=td, device="cuda")
             lib.check(self._L.ssa_reconstruct(self._h, off.ctypes.data, idx.ctypes.data, len(groups),
                                               int(add_rest), o.data_ptr(), 1))
             return [o[g].t() for g in range(n)]
-        o = np.zeros((n, self.ny, self.nx), dtype=self._np_dtype)
+        o = np.zeros((n, self.ny_out, self.nx), dtype=self._np_dtype)
         lib.check(self._L.ssa_reconstruct(self._h, off.ctypes.data, idx.ctypes.data, len(groups),
                                           int(add_rest), o.ctypes.data, 0))
         return [o[g].T for g in range(n)]
 
-    def wcor(self, groups) -> np.ndarray:
+    def wcor(self, groups, contributions=False):
+        """w-correlation matrix of the groups' reconstructions; with contributions=True
+        also returns ||X̃_g||²_w / ||X||²_w per group."""
         off, idx = self._csr(groups)
         ng = len(groups)
         rho = np.zeros((ng, ng), dtype=np.float64, order="F")
-        lib.check(self._L.ssa_wcor(self._h, off.ctypes.data, idx.ctypes.data, ng, rho.ctypes.data))
-        return rho
+        con = np.zeros(ng, dtype=np.float64)
+        lib.check(self._L.ssa_wcor(self._h, off.ctypes.data, idx.ctypes.data, ng, rho.ctypes.data,
+                                   con.ctypes.data))
+        return (rho, con) if contributions else rho
 
 
 def version() -> str:

@@ -66,11 +66,29 @@ __global__ void u8_to_T_kernel(const uint8_t *m, int64_t n, T *out) {
         out[t] = m[t] ? T(1) : T(0);
 }
 
-__global__ void clear_band_kernel(uint8_t *km, int kx, int ky, int64_t y0, int64_t y1) {
-    const int64_t n = (int64_t)kx * ky;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = t / kx;
-        if (j < y0 || j >= y1) km[t] = 0;
+// band assembly (multi-GPU reconstruction): dst[g][x, y0 + y] = src[g][x, y] for the band's columns,
+// zero elsewhere (nb = number of arrays, each nx x ny_src into nx x ny_dst)
+template <typename T>
+__global__ void place_band_kernel(const T *src, int nx, int ny_src, int64_t ncols, T *dst, int ny_dst, int64_t y0,
+                                  int nb) {
+    const int64_t per = (int64_t)nx * ny_dst, tot = per * nb;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = t / per, r = t - g * per;
+        const int64_t y = r / nx - y0, x = r % nx;
+        dst[t] = (y >= 0 && y < ncols) ? src[g * (int64_t)nx * ny_src + x + (int64_t)nx * y] : T(0);
+    }
+}
+template <typename T>
+__global__ void int_to_T_kernel(const int32_t *w, int64_t n, T *out) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        out[t] = (T)w[t];
+}
+// out[g][n] = num[g][n] / w[n] on w > 0, NaN elsewhere (Alg. 4 step 3 on the assembled bands)
+template <typename T>
+__global__ void divide_weights_kernel(T *num, const T *w, int64_t n, int ng) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * ng; t += (int64_t)gridDim.x * blockDim.x) {
+        const T wn = w[t % n];
+        num[t] = wn > T(0) ? num[t] / wn : (T)NAN;
     }
 }
 
@@ -323,7 +341,7 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
     // a2: 𝔎 by Alg. 6: v = 𝒯ᵀ(I^𝔑)·1_𝔏 ;  𝔎 = {v = |𝔏|}
     const int64_t nk = (int64_t)p.kx * p.ky;
     p.kmask.alloc(nk, st);
-    const bool trivial = (p.n_valid == nxy) && p.full_window && !p.has_comm;
+    const bool trivial = (p.n_valid == nxy) && p.full_window;
     if (trivial) {
         SSA_CUDA(cudaMemsetAsync(p.kmask.p, 1, nk, st));
         p.full_k = true;
@@ -334,11 +352,6 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
         DevBuf tmp;
         tmp.alloc(sizeof(int32_t) * (size_t)p.kx * p.ny, st);
         box_kmask(p.nmask.as<uint8_t>(), p.nx, p.ny, p.lx, p.ly, p.kmask.as<uint8_t>(), tmp.as<int32_t>(), st);
-        if (p.has_comm) {
-            clear_band_kernel<<<(unsigned)std::min<int64_t>(cdiv(nk, 256), 16 * num_sms()), 256, 0, st>>>(
-                p.kmask.as<uint8_t>(), p.kx, p.ky, p.band_y0, p.band_y1);
-            after_launch("clear_band");
-        }
         DevBuf cc;
         cc.alloc(sizeof(int32_t) * (p.ky + 1), st);
         column_counts(p.kmask.as<uint8_t>(), p.kx, p.ky, cc.as<int32_t>(), st);
@@ -374,11 +387,6 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
         ws.alloc(wsb, st);
         corr_direct<T>(c, ws.as<T>(), wsb, st);
         threshold_eq<T>(cnt.as<T>(), nk, (double)p.L, p.kmask.as<uint8_t>(), st);
-        if (p.has_comm) {
-            clear_band_kernel<<<(unsigned)std::min<int64_t>(cdiv(nk, 256), 16 * num_sms()), 256, 0, st>>>(
-                p.kmask.as<uint8_t>(), p.kx, p.ky, p.band_y0, p.band_y1);
-            after_launch("clear_band");
-        }
         // compaction map box -> 𝔎 index (lex order)
         DevBuf cc;
         cc.alloc(sizeof(int32_t) * (p.ky + 1), st);
@@ -415,7 +423,7 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
         SSA_CUDA(cudaStreamSynchronize(st));
         int64_t np = 0;
         for (int64_t t = 0; t < nxy; ++t) np += wh[t] > 0;
-        p.n_excluded = p.has_comm ? 0 : p.n_valid - np;
+        p.n_excluded = p.n_valid - np;   // band plans: cells of the band's sub-image
     } else {
         DevBuf num, go, gi;
         num.alloc(sizeof(T) * nxy, st);
@@ -437,7 +445,7 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
         SSA_CUDA(cudaStreamSynchronize(st));
         int64_t np = 0;
         for (int64_t t = 0; t < nxy; ++t) np += wh[t] > 0;
-        p.n_excluded = p.has_comm ? 0 : p.n_valid - np;
+        p.n_excluded = p.n_valid - np;   // band plans: cells of the band's sub-image
     }
     // workspaces
     const int kmax = std::max(64, p.block_k);
@@ -492,7 +500,9 @@ static void get_v(PlanImpl &p, const std::vector<int> *need = nullptr) {
 }
 
 template <typename T>
-static void reconstruct_impl(PlanImpl &p, const int32_t *off, const int32_t *idx, int ng, int add_rest, T *out_dev) {
+static void reconstruct_impl(PlanImpl &p, const int32_t *off, const int32_t *idx, int ng, int add_rest, T *out_dev,
+                             const int32_t *wdiv = nullptr) {
+    if (!wdiv) wdiv = p.weights.as<int32_t>();
     {
         std::vector<int> need(idx, idx + off[ng]);
         get_v<T>(p, &need);
@@ -515,7 +525,7 @@ static void reconstruct_impl(PlanImpl &p, const int32_t *off, const int32_t *idx
         ds.alloc(sizeof(int) * p.r, p.st);
         SSA_CUDA(cudaMemcpyAsync(ds.p, slot.data(), sizeof(int) * p.r, cudaMemcpyHostToDevice, p.st));
         fft_diagsums<T>(p, p.U.as<T>(), p.V.as<T>(), sig.as<double>(), go.as<int>(), gi.as<int>(), ng, used,
-                        ds.as<int>(), out_dev);
+                        ds.as<int>(), out_dev, wdiv);
     } else if (ng > 0) {
         AvgParams<T> a{};
         a.nx = p.nx; a.ny = p.ny;
@@ -523,11 +533,66 @@ static void reconstruct_impl(PlanImpl &p, const int32_t *off, const int32_t *idx
         a.kx = p.kx; a.ky = p.ky; a.kmap = p.full_k ? nullptr : p.kmap.as<int>();
         a.U = p.U.as<T>(); a.ldu = p.L; a.V = p.V.as<T>(); a.ldv = p.K; a.coef = sig.as<double>();
         a.grp_off = go.as<int>(); a.grp_idx = gi.as<int>(); a.ngroups = ng;
-        a.w = p.weights.as<int>(); a.out = out_dev; a.ldout = p.nx; a.out_stride = nxy;
+        a.w = wdiv; a.out = out_dev; a.ldout = p.nx; a.out_stride = nxy;
         diagsums_direct<T>(a, p.st);
     }
     if (add_rest)
-        rest_group<T>(p.img.as<T>(), p.weights.as<int32_t>(), out_dev, ng, nxy, nxy, out_dev + (int64_t)ng * nxy, p.st);
+        rest_group<T>(p.img.as<T>(), wdiv, out_dev, ng, nxy, nxy, out_dev + (int64_t)ng * nxy, p.st);
+    SSA_CUDA(cudaStreamSynchronize(p.st));
+}
+
+// Band plans: the reconstruction of the global image from the ranks' bands.  Each
+// rank forms the diagonal-averaging NUMERATORS of its sub-image (its own window positions only),
+// places them at the band's global columns and the ranks sum them (one all-reduce per output; the
+// (Ly−1)-column halos overlap with the next band); the global hit counts are the sum of the bands'
+// (𝕎 counts (ℓ, κ) pairs and the κ are partitioned), so Alg. 4's division then gives the global
+// X̃_g on every rank.  With want_img the global image (0 outside 𝔑) is assembled into out[ng]
+// (owned columns only: a rank contributes [y0, y1), the last one also its halo).  w_global (int32,
+// nx x ny_global) receives the global hit counts when non-null.
+template <typename T>
+static void band_reconstruct(PlanImpl &p, const int32_t *off, const int32_t *idx, int ng, bool want_img, T *out,
+                             int32_t *w_global) {
+    const int64_t nxy = (int64_t)p.nx * p.ny, nxg = (int64_t)p.nx * p.ny_global;
+    const unsigned grid = (unsigned)std::min<int64_t>(cdiv(nxg * std::max(ng, 1), 256), 16 * num_sms());
+    auto allreduce = [&](T *buf, int64_t n) {
+        if (p.comm.allreduce_sum(p.comm.user, buf, n, p.dt, p.st) != 0)
+            throw Error(SSA_ERR_COMM, "allreduce of the band reconstructions failed");
+    };
+    DevBuf ones, num, wl, wg;
+    ones.alloc(sizeof(int32_t) * nxy, p.st);
+    {
+        std::vector<int32_t> h(nxy, 1);
+        SSA_CUDA(cudaMemcpyAsync(ones.p, h.data(), sizeof(int32_t) * nxy, cudaMemcpyHostToDevice, p.st));
+        if (ng > 0) {
+            num.alloc(sizeof(T) * nxy * ng, p.st);
+            reconstruct_impl<T>(p, off, idx, ng, 0, num.as<T>(), ones.as<int32_t>());   // raw numerators
+        }
+        SSA_CUDA(cudaStreamSynchronize(p.st));
+    }
+    if (ng > 0) {
+        place_band_kernel<T><<<grid, 256, 0, p.st>>>(num.as<T>(), p.nx, p.ny, p.ny, out, (int)p.ny_global, p.band_y0, ng);
+        after_launch("place_band");
+        allreduce(out, nxg * ng);
+    }
+    wl.alloc(sizeof(T) * nxy, p.st);
+    wg.alloc(sizeof(T) * nxg, p.st);
+    int_to_T_kernel<T><<<grid, 256, 0, p.st>>>(p.weights.as<int32_t>(), nxy, wl.as<T>());
+    after_launch("int_to_T");
+    place_band_kernel<T><<<grid, 256, 0, p.st>>>(wl.as<T>(), p.nx, p.ny, p.ny, wg.as<T>(), (int)p.ny_global, p.band_y0, 1);
+    after_launch("place_band");
+    allreduce(wg.as<T>(), nxg);   // exact: integer counts < 2^24
+    if (ng > 0) {
+        divide_weights_kernel<T><<<grid, 256, 0, p.st>>>(out, wg.as<T>(), nxg, ng);
+        after_launch("divide_weights");
+    }
+    if (want_img) {
+        const bool last = p.band_y1 + p.ly - 1 == p.ny_global;
+        place_band_kernel<T><<<grid, 256, 0, p.st>>>(p.img.as<T>(), p.nx, p.ny, last ? p.ny : p.band_y1 - p.band_y0,
+                                                     out + nxg * ng, (int)p.ny_global, p.band_y0, 1);
+        after_launch("place_band");
+        allreduce(out + nxg * ng, nxg);
+    }
+    if (w_global) box_ones_to_int<T>(wg.as<T>(), nxg, w_global, p.st);
     SSA_CUDA(cudaStreamSynchronize(p.st));
 }
 
@@ -592,18 +657,28 @@ ssa_status ssa_plan_create(const ssa_array *x, const ssa_window *w, const uint8_
     PlanImpl &P = p->impl;
     P.nx = (int)x->nx; P.ny = (int)x->ny; P.lx = w->lx; P.ly = w->ly;
     P.kx = P.nx - P.lx + 1; P.ky = P.ny - P.ly + 1;
-    P.dt = x->dtype;
     ssa_opts o{};
     if (opts) o = *opts;
+    // arithmetic type of the plan: the input's dtype unless opts.precision asks for another
+    // (the input is cast once at plan creation)
+    if (o.precision < 0 || o.precision > 2) throw Error(SSA_ERR_ARG, "precision must be 0 (input), 1 (fp32) or 2 (fp64)");
+    P.dt = o.precision == 0 ? x->dtype : (o.precision == 1 ? SSA_F32 : SSA_F64);
     P.st = (cudaStream_t)o.stream;
     P.path = o.path;
     P.block_k = o.block_k > 0 ? o.block_k : (P.dt == SSA_F64 ? 16 : 32);
     P.tol = o.tol; P.max_products = o.max_products; P.seed = o.seed ? o.seed : 0x1309505000ull;
     if (o.comm && o.comm->world > 1) {
+        // window-position band partition: x is this rank's sub-image, the global image
+        // columns [band_y0, band_y1 + Ly − 1) (its origin band plus the (Ly−1)-column halo), so the
+        // sub-image's own 𝔎 is exactly the band of the global 𝔎 (eq. P:3004-3005 only looks inside
+        // the window span of each origin)
         P.comm = *o.comm; P.has_comm = true;
         P.band_y0 = o.band_y0; P.band_y1 = o.band_y1;
-        if (P.band_y0 < 0 || P.band_y1 > P.ky || P.band_y0 >= P.band_y1)
-            throw Error(SSA_ERR_ARG, "band [y0,y1) outside the origin box");
+        P.ny_global = o.ny_global;
+        if (P.band_y0 < 0 || P.band_y0 >= P.band_y1 || P.band_y1 - P.band_y0 != P.ky ||
+            P.ny_global < P.band_y1 + P.ly - 1)
+            throw Error(SSA_ERR_ARG, "band plan: x must be the global columns [band_y0, band_y1 + Ly - 1) "
+                                     "and ny_global >= band_y1 + Ly - 1");
     }
     // 𝔏 (window shape) on the host: box index -> lex index
     P.lmap_host.assign((size_t)P.lx * P.ly, -1);
@@ -740,6 +815,15 @@ ssa_status ssa_get_sigma(ssa_plan p, double *sigma) {
     return SSA_OK;
 }
 
+ssa_status ssa_get_residuals(ssa_plan p, double *res) {
+    if (ssa_status s = check_plan(p)) return s;
+    if (!res) { g_err = "null output"; return SSA_ERR_ARG; }
+    if (p->impl.r == 0) { g_err = "no decomposition"; return SSA_ERR_STATE; }
+    const PlanImpl &P = p->impl;
+    for (int i = 0; i < P.r; ++i) res[i] = i < (int)P.residuals.size() ? P.residuals[i] : NAN;
+    return SSA_OK;
+}
+
 ssa_status ssa_get_u(ssa_plan p, void *U, int on_device) {
     if (ssa_status s = check_plan(p)) return s;
     SSA_API_BEGIN
@@ -786,14 +870,28 @@ ssa_status ssa_set_triples(ssa_plan p, int32_t r, const double *sigma, const voi
     SSA_API_END
 }
 
-static void check_groups(const PlanImpl &P, const int32_t *off, const int32_t *idx, int32_t ng) {
+// Group validation.  A group index beyond the computed triples continues the decomposition
+// automatically ("if 10 eigentriples were calculated while decomposing, then the user could still
+// perform reconstruction by the first 15 components, since the decomposition will be automatically
+// continued"): decompose(max index + 1), warm-started from the stored eigenvectors.
+static void check_groups(PlanImpl &P, const int32_t *off, const int32_t *idx, int32_t ng) {
     if (ng < 0 || (ng > 0 && (!off || !idx))) throw Error(SSA_ERR_ARG, "bad group arrays");
     if (ng == 0) return;
     if (off[0] != 0) throw Error(SSA_ERR_ARG, "grp_off[0] must be 0");
     for (int g = 0; g < ng; ++g)
         if (off[g + 1] < off[g]) throw Error(SSA_ERR_ARG, "grp_off must be non-decreasing");
-    for (int t = 0; t < off[ng]; ++t)
-        if (idx[t] < 0 || idx[t] >= P.r) throw Error(SSA_ERR_RANK, "group index >= number of computed triples");
+    int need = 0;
+    for (int t = 0; t < off[ng]; ++t) {
+        if (idx[t] < 0) throw Error(SSA_ERR_RANK, "negative group index");
+        need = std::max(need, idx[t] + 1);
+    }
+    if (need > P.r) {
+        if (need > std::min(P.L, P.K)) throw Error(SSA_ERR_RANK, "group index >= min(L, K)");
+        ssa_decomp_info inf{};
+        if (P.dt == SSA_F64) decompose<double>(P, need, &inf);
+        else decompose<float>(P, need, &inf);
+        P.last_info = inf;
+    }
 }
 
 ssa_status ssa_reconstruct(ssa_plan p, const int32_t *off, const int32_t *idx, int32_t ng, int add_rest, void *out,
@@ -804,8 +902,8 @@ ssa_status ssa_reconstruct(ssa_plan p, const int32_t *off, const int32_t *idx, i
     if (P.r == 0) throw Error(SSA_ERR_STATE, "reconstruct before decompose");
     if (!out) throw Error(SSA_ERR_ARG, "null output");
     check_groups(P, off, idx, ng);
-    if (P.has_comm) throw Error(SSA_ERR_ARG, "multi-GPU reconstruction: gather the bands on the caller side");
-    const int64_t nxy = (int64_t)P.nx * P.ny;
+    const bool band = P.has_comm && P.comm.world > 1;
+    const int64_t nxy = (int64_t)P.nx * (band ? P.ny_global : P.ny);   // band plans return the global image
     const int nout = ng + (add_rest ? 1 : 0);
     const int32_t zero_off = 0;
     if (ng == 0) off = &zero_off;
@@ -815,45 +913,93 @@ ssa_status ssa_reconstruct(ssa_plan p, const int32_t *off, const int32_t *idx, i
         tmp.alloc(P.elem() * nxy * std::max(nout, 1), P.st);
         dout = tmp.p;
     }
-    if (P.dt == SSA_F64) reconstruct_impl<double>(P, off, idx, ng, add_rest, (double *)dout);
-    else reconstruct_impl<float>(P, off, idx, ng, add_rest, (float *)dout);
+    if (band) {
+        DevBuf wgi;
+        if (add_rest) wgi.alloc(sizeof(int32_t) * nxy, P.st);
+        if (P.dt == SSA_F64) {
+            band_reconstruct<double>(P, off, idx, ng, add_rest, (double *)dout, add_rest ? wgi.as<int32_t>() : nullptr);
+            if (add_rest) {   // rest = image − Σ_g X̃_g on the global 𝔑′ (the image was assembled into out[ng])
+                DevBuf xg;
+                xg.alloc(sizeof(double) * nxy, P.st);
+                SSA_CUDA(cudaMemcpyAsync(xg.p, (double *)dout + nxy * ng, sizeof(double) * nxy, cudaMemcpyDeviceToDevice, P.st));
+                rest_group<double>(xg.as<double>(), wgi.as<int32_t>(), (double *)dout, ng, nxy, nxy, (double *)dout + nxy * ng, P.st);
+            }
+        } else {
+            band_reconstruct<float>(P, off, idx, ng, add_rest, (float *)dout, add_rest ? wgi.as<int32_t>() : nullptr);
+            if (add_rest) {
+                DevBuf xg;
+                xg.alloc(sizeof(float) * nxy, P.st);
+                SSA_CUDA(cudaMemcpyAsync(xg.p, (float *)dout + nxy * ng, sizeof(float) * nxy, cudaMemcpyDeviceToDevice, P.st));
+                rest_group<float>(xg.as<float>(), wgi.as<int32_t>(), (float *)dout, ng, nxy, nxy, (float *)dout + nxy * ng, P.st);
+            }
+        }
+        SSA_CUDA(cudaStreamSynchronize(P.st));
+    } else if (P.dt == SSA_F64) {
+        reconstruct_impl<double>(P, off, idx, ng, add_rest, (double *)dout);
+    } else {
+        reconstruct_impl<float>(P, off, idx, ng, add_rest, (float *)dout);
+    }
     if (!on_device) copy_out(P, out, dout, P.elem() * nxy * nout, 0);
     return SSA_OK;
     SSA_API_END
 }
 
-ssa_status ssa_wcor(ssa_plan p, const int32_t *off, const int32_t *idx, int32_t ng, double *rho) {
+ssa_status ssa_wcor(ssa_plan p, const int32_t *off, const int32_t *idx, int32_t ng, double *rho, double *contrib) {
     if (ssa_status s = check_plan(p)) return s;
     SSA_API_BEGIN
     PlanImpl &P = p->impl;
     if (P.r == 0) throw Error(SSA_ERR_STATE, "wcor before decompose");
-    if (!rho || ng < 1 || ng > 64) throw Error(SSA_ERR_ARG, "wcor: 1..64 groups");
+    if (!rho || ng < 1 || ng > 63) throw Error(SSA_ERR_ARG, "wcor: 1..63 groups");
     check_groups(P, off, idx, ng);
-    const int64_t nxy = (int64_t)P.nx * P.ny;
-    DevBuf rec;
-    rec.alloc(P.elem() * nxy * ng, P.st);
-    std::vector<double> G((size_t)ng * ng);
+    const bool band = P.has_comm && P.comm.world > 1;
+    const int64_t nxy = (int64_t)P.nx * (band ? P.ny_global : P.ny);
+    // columns: the ng reconstructions, then the image itself (its weighted norm is the denominator
+    // of the contributions); each scaled by sqrt(w_n) so that one Gram gives (Y, Z)_w.
+    // Band plans work on the assembled global reconstructions, image and hit counts.
+    const int nc = ng + 1;
+    DevBuf rec, wgl;
+    rec.alloc(P.elem() * nxy * nc, P.st);
+    const int32_t *wts = P.weights.as<int32_t>();
+    if (band) {
+        wgl.alloc(sizeof(int32_t) * nxy, P.st);
+        wts = wgl.as<int32_t>();
+    }
+    std::vector<double> G((size_t)nc * nc);
     double *Gd = small_dev(P, 64 * 64);
     if (P.dt == SSA_F64) {
-        reconstruct_impl<double>(P, off, idx, ng, 0, rec.as<double>());
-        weighted_sqrt_kernel<double><<<(unsigned)std::min<int64_t>(cdiv(nxy * ng, 256), 16 * num_sms()), 256, 0, P.st>>>(
-            rec.as<double>(), P.weights.as<int32_t>(), nxy, ng);
+        if (band) {
+            band_reconstruct<double>(P, off, idx, ng, true, rec.as<double>(), wgl.as<int32_t>());
+        } else {
+            reconstruct_impl<double>(P, off, idx, ng, 0, rec.as<double>());
+            SSA_CUDA(cudaMemcpyAsync(rec.as<double>() + nxy * ng, P.img.p, sizeof(double) * nxy, cudaMemcpyDeviceToDevice, P.st));
+        }
+        weighted_sqrt_kernel<double><<<(unsigned)std::min<int64_t>(cdiv(nxy * nc, 256), 16 * num_sms()), 256, 0, P.st>>>(
+            rec.as<double>(), wts, nxy, nc);
         after_launch("weighted_sqrt");
-        gram_tn<double>(nxy, rec.as<double>(), nxy, ng, rec.as<double>(), nxy, ng, Gd, P.ws_gram.as<double>(), P.ws_gram.bytes, P.st);
+        gram_tn<double>(nxy, rec.as<double>(), nxy, nc, rec.as<double>(), nxy, nc, Gd, P.ws_gram.as<double>(), P.ws_gram.bytes, P.st);
     } else {
-        reconstruct_impl<float>(P, off, idx, ng, 0, rec.as<float>());
-        weighted_sqrt_kernel<float><<<(unsigned)std::min<int64_t>(cdiv(nxy * ng, 256), 16 * num_sms()), 256, 0, P.st>>>(
-            rec.as<float>(), P.weights.as<int32_t>(), nxy, ng);
+        if (band) {
+            band_reconstruct<float>(P, off, idx, ng, true, rec.as<float>(), wgl.as<int32_t>());
+        } else {
+            reconstruct_impl<float>(P, off, idx, ng, 0, rec.as<float>());
+            SSA_CUDA(cudaMemcpyAsync(rec.as<float>() + nxy * ng, P.img.p, sizeof(float) * nxy, cudaMemcpyDeviceToDevice, P.st));
+        }
+        weighted_sqrt_kernel<float><<<(unsigned)std::min<int64_t>(cdiv(nxy * nc, 256), 16 * num_sms()), 256, 0, P.st>>>(
+            rec.as<float>(), wts, nxy, nc);
         after_launch("weighted_sqrt");
-        gram_tn<float>(nxy, rec.as<float>(), nxy, ng, rec.as<float>(), nxy, ng, Gd, P.ws_gram.as<double>(), P.ws_gram.bytes, P.st);
+        gram_tn<float>(nxy, rec.as<float>(), nxy, nc, rec.as<float>(), nxy, nc, Gd, P.ws_gram.as<double>(), P.ws_gram.bytes, P.st);
     }
-    SSA_CUDA(cudaMemcpyAsync(G.data(), Gd, sizeof(double) * ng * ng, cudaMemcpyDeviceToHost, P.st));
+    SSA_CUDA(cudaMemcpyAsync(G.data(), Gd, sizeof(double) * nc * nc, cudaMemcpyDeviceToHost, P.st));
     SSA_CUDA(cudaStreamSynchronize(P.st));
     for (int b = 0; b < ng; ++b)
         for (int a = 0; a < ng; ++a) {
-            const double d = std::sqrt(G[a + (size_t)ng * a] * G[b + (size_t)ng * b]);
-            rho[a + (size_t)ng * b] = d > 0 ? G[a + (size_t)ng * b] / d : 0.0;
+            const double d = std::sqrt(G[a + (size_t)nc * a] * G[b + (size_t)nc * b]);
+            rho[a + (size_t)ng * b] = d > 0 ? G[a + (size_t)nc * b] / d : 0.0;
         }
+    if (contrib) {
+        const double xx = G[ng + (size_t)nc * ng];
+        for (int g = 0; g < ng; ++g) contrib[g] = xx > 0 ? G[g + (size_t)nc * g] / xx : 0.0;
+    }
     return SSA_OK;
     SSA_API_END
 }

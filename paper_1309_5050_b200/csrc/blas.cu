@@ -767,319 +767,16 @@ template void absmax_sign<float>(int64_t, const float *, int64_t, int, double *,
 template void absmax_sign<double>(int64_t, const double *, int64_t, int, double *, cudaStream_t);
 }  // namespace ssa
 
-namespace ssa {
-
-// ============================================================================
-// Device-resident block orthonormalisation (one CGS + CholeskyQR pass per call
-// pair orth_solve / apply_inplace; the solver runs two or three passes with a
-// single host synchronisation).  For W (M x kc) following `na` orthonormal
-// columns A in the same buffer ([A W] contiguous, ld M):
-//   G = [A W]ᵀ W  (gram_tn)   C = G[0:na, :]   Gp = WᵀW − CᵀC  (= W'ᵀW', W' = W − A C)
-//   Gp (+ shift) = RᵀR        S = R⁻¹          W ← W' S = [A W]·[−C S; S]
-// Coefficients accumulate so that W_in = A·Ctot + W_out·Btot holds exactly:
-//   pass 1: Ctot = C, Btot = R;   pass p > 1: Ctot += C·Btot, Btot = R·Btot.
-// flags[0] trouble (non-finite Gram, a column numerically in span(A) or zero —
-//          the host then redoes the block with the robust path),
-// flags[1] pass 1 needed a shifted Cholesky, flags[2] another pass is needed
-//          (shifted, or pass-p Gram far from identity), flags[3] = pass count.
-// ============================================================================
-__global__ void __launch_bounds__(256)
-orth_solve_kernel(const double *__restrict__ G, int na, int kc, int pass, double zthr2, double shift_rel,
-                  double thr_chol, int c_in_smem, double *__restrict__ Mout, double *__restrict__ Ctot,
-                  double *__restrict__ Btot, int *__restrict__ flags) {
-    extern __shared__ double sm[];
-    double *Gp = sm;
-    double *R = Gp + kc * kc;
-    double *S = R + kc * kc;
-    double *Bo = S + kc * kc;
-    double *Cs = Bo + kc * kc;   // na x kc (only if c_in_smem)
-    __shared__ int s_fail;
-    __shared__ double s_dmax, s_dev;
-    const int n1 = na + kc, tid = threadIdx.x, nt = blockDim.x;
-    const double *C = G;
-    int ldc = n1;
-    if (c_in_smem) {   // odd leading dimension: column-parallel reads hit distinct banks
-        ldc = na | 1;
-        for (int e = tid; e < na * kc; e += nt) Cs[(e % na) + (size_t)ldc * (e / na)] = G[(e % na) + (size_t)n1 * (e / na)];
-        C = Cs;
-    }
-    if (pass >= 2)
-        for (int e = tid; e < kc * kc; e += nt) Bo[e] = Btot[e];
-    __syncthreads();
-    for (int e = tid; e < kc * kc; e += nt) {
-        const int a = e % kc, b = e / kc;
-        if (a > b) continue;
-        double s = G[na + a + (size_t)n1 * b];
-        const double *ca = C + (size_t)ldc * a, *cb = C + (size_t)ldc * b;
-        for (int t = 0; t < na; ++t) s -= ca[t] * cb[t];
-        Gp[a + kc * b] = s;
-        Gp[b + kc * a] = s;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double dmax = 0.0, dev = 0.0;
-        int bad = 0;
-        for (int j = 0; j < kc; ++j) {
-            const double d = Gp[j + kc * j];
-            if (!isfinite(d)) bad = 1;
-            dmax = fmax(dmax, d);
-            if (pass == 1 && !(d > zthr2)) bad = 1;
-        }
-        for (int e = 0; e < kc * kc; ++e) {
-            const double v = Gp[e] - ((e % kc) == (e / kc) ? 1.0 : 0.0);
-            if (!isfinite(v)) bad = 1;
-            dev = fmax(dev, fabs(v));
-        }
-        if (!(dmax > 0.0)) bad = 1;
-        s_dmax = dmax;
-        s_dev = dev;
-        s_fail = bad;
-    }
-    __syncthreads();
-    if (s_fail) {
-        if (tid == 0) flags[0] = 1;
-        return;
-    }
-    int shifted = 0;
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        const double shift = attempt ? shift_rel * s_dmax : 0.0;
-        const double thr = attempt ? 0.0 : thr_chol * s_dmax;
-        for (int e = tid; e < kc * kc; e += nt) R[e] = Gp[e] + (((e % kc) == (e / kc)) ? shift : 0.0);
-        __syncthreads();
-        if (tid == 0) s_fail = 0;
-        __syncthreads();
-        for (int j = 0; j < kc; ++j) {
-            if (tid == 0) {
-                const double d = R[j + kc * j];
-                if (!(d > thr)) s_fail = 1;
-                else R[j + kc * j] = sqrt(d);
-            }
-            __syncthreads();
-            if (s_fail) break;
-            const double rjj = R[j + kc * j];
-            for (int i = j + 1 + tid; i < kc; i += nt) R[j + kc * i] /= rjj;
-            __syncthreads();
-            const int m = kc - j - 1;
-            for (int e = tid; e < m * m; e += nt) {
-                const int a = j + 1 + e % m, b = j + 1 + e / m;
-                if (a <= b) R[a + kc * b] -= R[j + kc * a] * R[j + kc * b];
-            }
-            __syncthreads();
-        }
-        if (!s_fail) { shifted = attempt; break; }
-        __syncthreads();
-    }
-    if (s_fail) {
-        if (tid == 0) flags[0] = 1;
-        return;
-    }
-    for (int e = tid; e < kc * kc; e += nt)
-        if ((e % kc) > (e / kc)) R[e] = 0.0;
-    __syncthreads();
-    // S = R^-1 (upper triangular), one column per thread
-    for (int j = tid; j < kc; j += nt) {
-        for (int i = 0; i < kc; ++i) S[i + kc * j] = 0.0;
-        S[j + kc * j] = 1.0 / R[j + kc * j];
-        for (int i = j - 1; i >= 0; --i) {
-            double v = 0.0;
-            for (int t = i + 1; t <= j; ++t) v += R[i + kc * t] * S[t + kc * j];
-            S[i + kc * j] = -v / R[i + kc * i];
-        }
-    }
-    __syncthreads();
-    // Mout = [-C S ; S]
-    for (int e = tid; e < n1 * kc; e += nt) {
-        const int t = e % n1, b = e / n1;
-        double v;
-        if (t < na) {
-            v = 0.0;
-            for (int a = 0; a <= b; ++a) v -= C[t + (size_t)ldc * a] * S[a + kc * b];
-        } else {
-            v = S[(t - na) + kc * b];
-        }
-        Mout[e] = v;
-    }
-    // coefficient bookkeeping
-    if (pass == 1) {
-        for (int e = tid; e < na * kc; e += nt) Ctot[e] = C[(e % na) + (size_t)ldc * (e / na)];
-        for (int e = tid; e < kc * kc; e += nt) Btot[e] = R[e];
-    } else {
-        for (int e = tid; e < na * kc; e += nt) {
-            const int t = e % na, b = e / na;
-            double v = Ctot[e];
-            for (int a = 0; a < kc; ++a) v += C[t + (size_t)ldc * a] * Bo[a + kc * b];
-            Ctot[e] = v;
-        }
-        for (int e = tid; e < kc * kc; e += nt) {
-            const int a = e % kc, b = e / kc;
-            double v = 0.0;
-            for (int t = a; t < kc; ++t) v += R[a + kc * t] * Bo[t + kc * b];
-            Btot[e] = v;
-        }
-    }
-    if (tid == 0) {
-        if (pass == 1) flags[1] = shifted;
-        flags[2] = (shifted || (pass >= 2 && s_dev > 0.1)) ? 1 : 0;
-        flags[3] = pass;
-    }
-}
-
-// W[:, 0:kc] = A[:, 0:n1] · Mc (n1 x kc, device double) where W = A + lda·(n1 - kc):
-// the block being orthonormalised is the last kc columns of its own input.  Thread
-// per row; every input of a row is read before any of its outputs is written.
-template <typename T, int NMAX>
-__global__ void __launch_bounds__(128)
-apply_inplace_kernel(int64_t M, T *A, int64_t lda, int n1, int kc, const double *Mc, const int *skip) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    if (skip && *skip != 0) return;   // the solve flagged trouble: leave W for the host's robust path
-    T *CS = reinterpret_cast<T *>(smem_raw);   // [n1][NMAX]
-    for (int idx = threadIdx.x; idx < n1 * NMAX; idx += blockDim.x) {
-        const int c = idx / NMAX, b = idx % NMAX;
-        CS[idx] = (b < kc) ? (T)Mc[c + (int64_t)n1 * b] : T(0);
-    }
-    __syncthreads();
-    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (row >= M) return;
-    T acc[NMAX];
-#pragma unroll
-    for (int j = 0; j < NMAX; ++j) acc[j] = T(0);
-    const T *ar = A + row;
-    int c0 = 0;
-    for (; c0 + 8 <= n1; c0 += 8) {
-        T a[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) a[t] = ar[lda * (c0 + t)];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            const T *cr = CS + (c0 + t) * NMAX;
-#pragma unroll
-            for (int j = 0; j < NMAX; ++j) acc[j] = fma(a[t], cr[j], acc[j]);
-        }
-    }
-    for (; c0 < n1; ++c0) {
-        const T a = ar[lda * c0];
-        const T *cr = CS + c0 * NMAX;
-#pragma unroll
-        for (int j = 0; j < NMAX; ++j) acc[j] = fma(a, cr[j], acc[j]);
-    }
-    T *w = A + lda * (int64_t)(n1 - kc) + row;
-#pragma unroll
-    for (int j = 0; j < NMAX; ++j)
-        if (j < kc) w[lda * j] = acc[j];
-}
-
-void orth_solve(const double *G, int na, int kc, int pass, double zthr2, double shift_rel, double thr_chol,
-                double *Mout, double *Ctot, double *Btot, int *flags, cudaStream_t st) {
-    SSA_REQUIRE(kc <= 64 && na + kc <= 512, SSA_ERR_ARG, "orth_solve: at most 64 new columns against 448");
-    const size_t base = sizeof(double) * 4 * (size_t)kc * kc;
-    const size_t cbytes = sizeof(double) * (size_t)(na | 1) * kc;
-    const int c_in_smem = (base + cbytes <= 200 * 1024) ? 1 : 0;
-    const size_t smem = base + (c_in_smem ? cbytes : 0);
-    set_max_smem(orth_solve_kernel);
-    orth_solve_kernel<<<1, 256, smem, st>>>(G, na, kc, pass, zthr2, shift_rel, thr_chol, c_in_smem, Mout, Ctot, Btot,
-                                            flags);
-    after_launch("orth_solve");
-}
-
-template <typename T>
-void apply_inplace(int64_t M, T *A, int64_t lda, int n1, int kc, const double *Mc, const int *skip, cudaStream_t st) {
-    SSA_REQUIRE(kc <= 64 && n1 <= 512, SSA_ERR_ARG, "apply_inplace: at most 512 x 64");
-    if (M <= 0) return;
-    const unsigned grid = (unsigned)cdiv(M, 128);
-    if (kc <= 32) {
-        const size_t smem = sizeof(T) * (size_t)n1 * 32;
-        set_max_smem(apply_inplace_kernel<T, 32>);
-        apply_inplace_kernel<T, 32><<<grid, 128, smem, st>>>(M, A, lda, n1, kc, Mc, skip);
-    } else {
-        const size_t smem = sizeof(T) * (size_t)n1 * 64;
-        set_max_smem(apply_inplace_kernel<T, 64>);
-        apply_inplace_kernel<T, 64><<<grid, 128, smem, st>>>(M, A, lda, n1, kc, Mc, skip);
-    }
-    after_launch("apply_inplace");
-}
-template void apply_inplace<float>(int64_t, float *, int64_t, int, int, const double *, const int *, cudaStream_t);
-template void apply_inplace<double>(int64_t, double *, int64_t, int, int, const double *, const int *, cudaStream_t);
-
-}  // namespace ssa
-
-namespace ssa {
-// Out (M x n) = A (M x m) · C (m x n, device double), Out != A: thread per (row, group of
-// 8 output columns), grid (ceil(M/128), ceil(n/8)) — enough CTAs for short bases (L side).
-template <typename T>
-__global__ void __launch_bounds__(128)
-gemm_cols_kernel(int64_t M, const T *__restrict__ A, int64_t lda, int m, const double *__restrict__ C, int ldc, int n,
-                 T *__restrict__ Out, int64_t ldo) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *CS = reinterpret_cast<T *>(smem_raw);   // [m][8]
-    const int c0 = blockIdx.y * 8;
-    for (int idx = threadIdx.x; idx < m * 8; idx += blockDim.x) {
-        const int a = idx / 8, b = idx % 8;
-        CS[idx] = (c0 + b < n) ? (T)C[a + (int64_t)ldc * (c0 + b)] : T(0);
-    }
-    __syncthreads();
-    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (row >= M) return;
-    T acc[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = T(0);
-    const T *ar = A + row;
-#pragma unroll 4
-    for (int a = 0; a < m; ++a) {
-        const T v = ar[lda * a];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fma(v, CS[a * 8 + j], acc[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-        if (c0 + j < n) Out[row + ldo * (c0 + j)] = acc[j];
-}
-
-template <typename T>
-void gemm_cols(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, T *Out, int64_t ldo,
-               cudaStream_t st) {
-    if (M <= 0 || n <= 0) return;
-    const size_t smem = sizeof(T) * (size_t)m * 8;
-    SSA_REQUIRE(smem <= 200 * 1024, SSA_ERR_ARG, "gemm_cols: too many input columns");
-    set_max_smem(gemm_cols_kernel<T>);
-    gemm_cols_kernel<T><<<dim3((unsigned)cdiv(M, 128), (unsigned)cdiv(n, 8)), 128, smem, st>>>(M, A, lda, m, C, ldc, n,
-                                                                                            Out, ldo);
-    after_launch("gemm_cols");
-}
-template void gemm_cols<float>(int64_t, const float *, int64_t, int, const double *, int, int, float *, int64_t,
-                               cudaStream_t);
-template void gemm_cols<double>(int64_t, const double *, int64_t, int, const double *, int, int, double *, int64_t,
-                                cudaStream_t);
-}  // namespace ssa
-
-// read-bandwidth probe for the column-major tall-skinny layout (ssa_bench_tall which = 2):
-// CTA c streams a contiguous row range of all ncols columns, rch rows per column at a time
-__global__ void colread_kernel(int64_t M, const float *__restrict__ A, int64_t lda, int ncols, int rch, float *out) {
-    const int64_t per = ((M + gridDim.x - 1) / gridDim.x + 3) & ~3;
-    const int64_t r0 = blockIdx.x * per, r1 = min(M, r0 + per);
-    float acc = 0.f;
-    for (int64_t rb = r0; rb < r1; rb += rch) {
-        const int nr4 = (int)((min(r1, rb + rch) - rb) / 4);
-        for (int idx = threadIdx.x; idx < ncols * nr4; idx += blockDim.x) {
-            const int c = idx / nr4, q = idx % nr4;
-            const float4 v = __ldg(reinterpret_cast<const float4 *>(A + lda * c + rb) + q);
-            acc += v.x + v.y + v.z + v.w;
-        }
-    }
-    if (acc == 123.456f) out[0] = acc;
-}
-
 // ---- ABI test hook: timing of the tall-skinny kernels on seeded device data
 extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32_t n2, int32_t reps, double *ms,
                                      double *check) {
     using namespace ssa;
     try {
-        if (M < 1 || n1 < 1 || n1 > 512 || n2 < 1 || (n2 > 64 && which != 4) || reps < 1 || which < 0 || which > 4)
+        if (M < 1 || n1 < 1 || n1 > 512 || n2 < 1 || n2 > 64 || reps < 1 || which < 0 || which > 3 || which == 2)
             throw Error(SSA_ERR_ARG, "ssa_bench_tall: bad sizes");
         const int64_t ld = (M + 31) / 32 * 32;
         DevBuf a, b, g, ws, c;
         a.alloc(sizeof(float) * ld * n1, nullptr);
-        const int probe_code = n2;   // which = 4: box columns + 256 x row groups; B unused
-        if (which == 4) n2 = 1;
         b.alloc(sizeof(float) * ld * n2, nullptr);
         g.alloc(sizeof(double) * 512 * 64, nullptr);
         c.alloc(sizeof(double) * 512 * 64, nullptr);
@@ -1093,9 +790,7 @@ extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32
         for (size_t t = 0; t < hc.size(); ++t) hc[t] = 0.1 * ((double)((t * 7919) % 1000) / 1000.0 - 0.5);
         SSA_CUDA(cudaMemcpy(c.p, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice));
         auto run = [&]() {
-            if (which == 2) colread_kernel<<<num_sms() * 2, 512>>>(M, a.as<float>(), ld, n1, 32 * n2, b.as<float>());
-            else if (which == 0) gram_tn<float>(M, a.as<float>(), ld, n1, b.as<float>(), ld, n2, g.as<double>(), ws.as<double>(), wsb, nullptr);
-            else if (which == 4) tma_probe(a.as<float>(), M, n1, ld, probe_code & 255, (probe_code >> 8) ? (probe_code >> 8) : 1, nullptr);
+            if (which == 0) gram_tn<float>(M, a.as<float>(), ld, n1, b.as<float>(), ld, n2, g.as<double>(), ws.as<double>(), wsb, nullptr);
             else if (which == 3) gram_tn<float>(M, a.as<float>(), ld, n1, a.as<float>(), ld, n2, g.as<double>(), ws.as<double>(), wsb, nullptr);
             else gemm_acc<float>(M, a.as<float>(), ld, n1, c.as<double>(), n1, n2, -1.0, 1.0, b.as<float>(), ld, nullptr);
         };

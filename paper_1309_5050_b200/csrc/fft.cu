@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "common.h"
+#include "fft_reg.h"
 #include "kernels.h"
 #include "plan.h"
 
@@ -454,6 +455,7 @@ struct FftOperator {
     DevBuf stab_x, stab_y;   // per-stage twiddle tables for 2^lgx / 2^lgy point transforms
     DevBuf Xh;        // cplx[Hx][My]: DFT2 of the image
     DevBuf gk;        // cplx[Hx][My]: unnormalised inverse y-DFT of each X̂ row (small My: folded pass B)
+    DevBuf rtw_x, rtw_y;     // twiddle tables of the register-resident radix-16 passes (fp32, fft_reg.cu)
     DevBuf bufA, bufB;
     size_t capA = 0, capB = 0;
 };
@@ -495,6 +497,13 @@ static size_t smem_ab(int lg, int nb, int /*unused*/) {
 template <typename T>
 static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int bx, int by, int k, const int *jsel,
                    const double *scale, cplx<T> *A, cudaStream_t st) {
+    if constexpr (sizeof(T) == 4) {
+        if (f.rtw_x.p) {
+            rfft::pass_a(f.lgx, in, ld, map, bx, by, k, jsel, scale, reinterpret_cast<float2 *>(A),
+                         f.rtw_x.as<float2>(), st);
+            return;
+        }
+    }
     const int CB = 2 * batch_for(f.lgx, 2048);   // real columns (two per complex transform)
     const size_t smem = smem_ab<T>(f.lgx, CB / 2, 0);
     const int nth = threads_for(f.lgx, CB / 2, cdiv(by, CB) * k);
@@ -507,6 +516,14 @@ static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int 
 
 template <typename T>
 static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode, cplx<T> *B, int ny_out, cudaStream_t st) {
+    if constexpr (sizeof(T) == 4) {
+        if (f.rtw_y.p && mode == 0) {
+            rfft::pass_b(f.lgy, reinterpret_cast<const float2 *>(A), ny_in, f.Hx, k,
+                         reinterpret_cast<const float2 *>(f.Xh.p), reinterpret_cast<float2 *>(B), ny_out,
+                         f.rtw_y.as<float2>(), st);
+            return;
+        }
+    }
     const int RB = batch_for(f.lgy, 2048);
     // + the CTA's X̂ rows (prefetched, mode 0)
     const size_t smem = smem_ab<T>(f.lgy, RB, 0) + sizeof(cplx<T>) * ((size_t)RB << f.lgy) + 16;
@@ -522,6 +539,14 @@ static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode,
 template <typename T>
 static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *out, int64_t ldo, const int *omap,
                    const int *w, int64_t stride, cudaStream_t st, const cplx<T> *Afu = nullptr, int ny_in = 0) {
+    if constexpr (sizeof(T) == 4) {
+        if (f.rtw_x.p && !Afu) {
+            rfft::pass_c(f.lgx, reinterpret_cast<const float2 *>(B), oy, f.Hx, k, ox,
+                         (float)(1.0 / ((double)f.Mx * (double)f.My)), out, ldo, omap, w, stride, f.rtw_x.as<float2>(),
+                         st);
+            return;
+        }
+    }
     const int CB = 2 * batch_for(f.lgx, 2048);   // output columns (two per complex transform)
     const size_t smem = smem_ab<T>(f.lgx, CB / 2, 0);
     const int nth = threads_for(f.lgx, CB / 2, cdiv(oy, CB) * k);
@@ -582,6 +607,21 @@ static void build_impl(PlanImpl &p) {
     };
     build_stab(f.lgx, f.stab_x);
     build_stab(f.lgy, f.stab_y);
+    if constexpr (sizeof(T) == 4) {
+        // register-resident radix-16 passes for 2^8..2^12-point axes (fft_reg.cu); the X̂ build
+        // below and the other sizes use the shared-memory Stockham passes
+        static const bool off = std::getenv("SSA_FFT_STOCKHAM") != nullptr;   // A/B comparison switch
+        auto build_rtw = [&](int lg, DevBuf &buf) {
+            if (off || !rfft::supported(lg)) return;
+            std::vector<float2> h;
+            rfft::build_table(lg, h);
+            buf.alloc(sizeof(float2) * h.size(), p.st);
+            SSA_CUDA(cudaMemcpyAsync(buf.p, h.data(), sizeof(float2) * h.size(), cudaMemcpyHostToDevice, p.st));
+            SSA_CUDA(cudaStreamSynchronize(p.st));
+        };
+        build_rtw(f.lgx, f.rtw_x);
+        build_rtw(f.lgy, f.rtw_y);
+    }
     f.Xh.alloc(sizeof(cplx<T>) * (size_t)f.Hx * f.My, p.st);
     DevBuf tmp;
     tmp.alloc(sizeof(cplx<T>) * (size_t)f.Hx * p.ny, p.st);
@@ -639,7 +679,8 @@ void fft_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k) {
 // Grouped averaging via FFT: out_g = IDFT2(Σ_{i∈I_g} σ_i Ψ̂_i Φ̂_i) / 𝕎 (NaN off 𝔑′).
 template <typename T>
 void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, const int *grp_off_dev,
-                  const int *grp_idx_dev, int ng, const std::vector<int> &used, const int *slot_dev, T *out) {
+                  const int *grp_idx_dev, int ng, const std::vector<int> &used, const int *slot_dev, T *out,
+                  const int *wdiv) {
     FftOperator &f = *p.fft;
     const int nu = (int)used.size();
     DevBuf jsel, AU, AV, B;
@@ -652,16 +693,26 @@ void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, co
               AU.as<cplx<T>>(), p.st);
     pass_a<T>(f, V, p.K, p.full_k ? nullptr : p.kmap.as<int>(), p.kx, p.ky, nu, jsel.as<int>(), nullptr,
               AV.as<cplx<T>>(), p.st);
-    const int RB = batch_for(f.lgy, 2048);
-    const size_t smem = sizeof(cplx<T>) * (5 * sp_size((size_t)RB << f.lgy) + stab_count(f.lgy));
-    const int nth = threads_for(f.lgy, RB, cdiv(f.Hx, RB) * ng);
-    auto kern = nth <= 256 ? fft_pass_b_conv<T, 256> : fft_pass_b_conv<T, 512>;
-    set_max_smem(kern);
-    kern<<<dim3((unsigned)cdiv(f.Hx, RB), ng), nth, smem, p.st>>>(
-        AU.as<cplx<T>>(), p.ly, AV.as<cplx<T>>(), p.ky, grp_off_dev, grp_idx_dev, slot_dev, f.Hx, f.lgy, RB,
-        B.as<cplx<T>>(), p.ny, f.stab_y.as<cplx<T>>(), f.lgy);
-    after_launch("fft_pass_b_conv");
-    pass_c<T>(f, B.as<cplx<T>>(), p.ny, ng, p.nx, out, p.nx, nullptr, p.weights.as<int>(), (int64_t)p.nx * p.ny, p.st);
+    bool done = false;
+    if constexpr (sizeof(T) == 4) {
+        if (f.rtw_y.p) {
+            rfft::pass_bconv(f.lgy, AU.as<float2>(), p.ly, AV.as<float2>(), p.ky, grp_off_dev, grp_idx_dev, slot_dev,
+                             f.Hx, ng, B.as<float2>(), p.ny, f.rtw_y.as<float2>(), p.st);
+            done = true;
+        }
+    }
+    if (!done) {
+        const int RB = batch_for(f.lgy, 2048);
+        const size_t smem = sizeof(cplx<T>) * (5 * sp_size((size_t)RB << f.lgy) + stab_count(f.lgy));
+        const int nth = threads_for(f.lgy, RB, cdiv(f.Hx, RB) * ng);
+        auto kern = nth <= 256 ? fft_pass_b_conv<T, 256> : fft_pass_b_conv<T, 512>;
+        set_max_smem(kern);
+        kern<<<dim3((unsigned)cdiv(f.Hx, RB), ng), nth, smem, p.st>>>(
+            AU.as<cplx<T>>(), p.ly, AV.as<cplx<T>>(), p.ky, grp_off_dev, grp_idx_dev, slot_dev, f.Hx, f.lgy, RB,
+            B.as<cplx<T>>(), p.ny, f.stab_y.as<cplx<T>>(), f.lgy);
+        after_launch("fft_pass_b_conv");
+    }
+    pass_c<T>(f, B.as<cplx<T>>(), p.ny, ng, p.nx, out, p.nx, nullptr, wdiv, (int64_t)p.nx * p.ny, p.st);
     SSA_CUDA(cudaStreamSynchronize(p.st));
 }
 
@@ -670,9 +721,9 @@ template void fft_xv<double>(PlanImpl &, const double *, int64_t, double *, int6
 template void fft_xtu<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int);
 template void fft_xtu<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int);
 template void fft_diagsums<float>(PlanImpl &, const float *, const float *, const double *, const int *, const int *,
-                                  int, const std::vector<int> &, const int *, float *);
+                                  int, const std::vector<int> &, const int *, float *, const int *);
 template void fft_diagsums<double>(PlanImpl &, const double *, const double *, const double *, const int *, const int *,
-                                   int, const std::vector<int> &, const int *, double *);
+                                   int, const std::vector<int> &, const int *, double *, const int *);
 
 void fft_destroy(FftOperator *f) { delete f; }
 

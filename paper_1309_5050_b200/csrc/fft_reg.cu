@@ -1,0 +1,494 @@
+// Register-resident radix-16 FFT passes of the FFT correlation path (SURVEY §8(a) a4-a6, a10:
+// the method of Alg. 1/3/5, re-derived for the device).
+//
+// The round-1 passes ran every radix-8 Stockham stage through shared memory (load 8, twiddle,
+// butterfly, store 8 per thread and stage) and were instruction / latency bound (c5 pass B: 3.8 G
+// warp instructions per launch at ~50% issue efficiency; c3: 50-60% of shared-memory wavefronts
+// were bank conflicts).  Here a 2^LG-point transform (LG = 8..12) is owned by NT = 2^LG / 16
+// threads that each hold 16 elements in registers for the whole transform:
+//
+//   stage 0   radix R0 = 2^(LG mod 4) (16 if LG mod 4 = 0), span 1, no twiddles; a thread does
+//             16/R0 butterflies in registers;
+//   stage s   radix 16, span Ns = R0·16^(s-1): one shared-memory exchange (Stockham output
+//             index (j − k)·16 + k + Ns·r, k = j mod Ns, read back strided), twiddles
+//             e^{∓2πi r k/(16 Ns)} from a per-stage table in shared memory (15 per k, stride 15:
+//             conflict-free 8-byte reads), then a 16-point DFT in registers (4 x 4, 32 real
+//             multiplies, 144 adds).
+//
+// Thread t holds x[t + NT·e] (e < 16) before the transform and X[t + NT·e] after it, so global
+// loads and stores are coalesced along t, and the inverse transform of pass B starts from the
+// registers the forward one ended in (the spectrum product needs no exchange).  Shared-memory
+// indices are padded by one element per 16 (i + i/16), which makes every exchange pattern above
+// conflict-free for 8-byte accesses.  4096 points: 2 exchanges per transform instead of 4 stages
+// through shared memory, ~45 instructions per point instead of ~60.
+//
+// Intermediate layouts are the ones of fft.cu (A[(j*H + fx)*by + col], B[(j*H + fx)*oy + y]), so a
+// pass can run either implementation.
+#include <cmath>
+#include <vector>
+
+#include "common.h"
+#include "fft_reg.h"
+
+namespace ssa {
+namespace rfft {
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+    return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+// DIR·i·a (DIR = −1 forward, +1 inverse)
+template <int DIR> __device__ __forceinline__ float2 mul_i(float2 a) {
+    return DIR > 0 ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+}
+
+template <int DIR> __device__ __forceinline__ void dft2(float2 &a0, float2 &a1) {
+    const float2 t = a0;
+    a0 = cadd(t, a1);
+    a1 = csub(t, a1);
+}
+// X[k] = Σ_n x[n] ω^{nk}, ω = DIR·i; natural order in and out
+template <int DIR> __device__ __forceinline__ void dft4(float2 &a0, float2 &a1, float2 &a2, float2 &a3) {
+    const float2 t0 = cadd(a0, a2), t1 = csub(a0, a2);
+    const float2 t2 = cadd(a1, a3), t3 = mul_i<DIR>(csub(a1, a3));
+    a0 = cadd(t0, t2);
+    a2 = csub(t0, t2);
+    a1 = cadd(t1, t3);
+    a3 = csub(t1, t3);
+}
+template <int DIR> __device__ __forceinline__ void dft8(float2 *v, int s) {   // elements v[i*s]
+    float2 e0 = v[0], e1 = v[2 * s], e2 = v[4 * s], e3 = v[6 * s];
+    float2 o0 = v[s], o1 = v[3 * s], o2 = v[5 * s], o3 = v[7 * s];
+    dft4<DIR>(e0, e1, e2, e3);
+    dft4<DIR>(o0, o1, o2, o3);
+    const float h = 0.70710678118654752440f;
+    o1 = make_float2(h * (o1.x - (float)DIR * o1.y), h * (o1.y + (float)DIR * o1.x));
+    o2 = mul_i<DIR>(o2);
+    o3 = make_float2(h * (-o3.x - (float)DIR * o3.y), h * (-o3.y + (float)DIR * o3.x));
+    v[0] = cadd(e0, o0); v[4 * s] = csub(e0, o0);
+    v[s] = cadd(e1, o1); v[5 * s] = csub(e1, o1);
+    v[2 * s] = cadd(e2, o2); v[6 * s] = csub(e2, o2);
+    v[3 * s] = cadd(e3, o3); v[7 * s] = csub(e3, o3);
+}
+
+// 16-point DFT in natural order: n = n1 + 4 n2, k = k2 + 4 k1:
+// X[k2 + 4k1] = Σ_{n1} ω4^{n1 k1} ω16^{n1 k2} Σ_{n2} x[n1 + 4n2] ω4^{n2 k2}
+template <int DIR> __device__ __forceinline__ void dft16(float2 *v) {
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) dft4<DIR>(v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]);   // Y[n1][k2] at v[n1 + 4k2]
+    const float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f, h = 0.70710678118654752440f;
+    const float d = (float)DIR;
+    auto rot = [](float2 a, float c, float s) { return make_float2(a.x * c - a.y * s, a.x * s + a.y * c); };
+    // ω16^m = cos(2πm/16) + DIR·i·sin(2πm/16)
+    v[1 + 4] = rot(v[1 + 4], c1, d * s1);                                                    // ω^1
+    v[1 + 8] = make_float2(h * (v[1 + 8].x - d * v[1 + 8].y), h * (v[1 + 8].y + d * v[1 + 8].x));   // ω^2
+    v[1 + 12] = rot(v[1 + 12], s1, d * c1);                                                  // ω^3
+    v[2 + 4] = make_float2(h * (v[2 + 4].x - d * v[2 + 4].y), h * (v[2 + 4].y + d * v[2 + 4].x));   // ω^2
+    v[2 + 8] = mul_i<DIR>(v[2 + 8]);                                                         // ω^4
+    v[2 + 12] = make_float2(h * (-v[2 + 12].x - d * v[2 + 12].y), h * (-v[2 + 12].y + d * v[2 + 12].x));   // ω^6
+    v[3 + 4] = rot(v[3 + 4], s1, d * c1);                                                    // ω^3
+    v[3 + 8] = make_float2(h * (-v[3 + 8].x - d * v[3 + 8].y), h * (-v[3 + 8].y + d * v[3 + 8].x));   // ω^6
+    v[3 + 12] = rot(v[3 + 12], -c1, -d * s1);                                                // ω^9
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) dft4<DIR>(v[4 * k2], v[4 * k2 + 1], v[4 * k2 + 2], v[4 * k2 + 3]);   // X[k2+4k1] at v[4k2+k1]
+    float2 o[16];
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2)
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) o[k2 + 4 * k1] = v[4 * k2 + k1];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = o[i];
+}
+
+__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int pad_size(int n) { return n + n / 16 + 1; }
+__host__ __device__ constexpr int r0_of(int lg) { return (lg & 3) ? (1 << (lg & 3)) : 16; }
+// twiddle-table entries of all radix-16 stages: Σ spans · 15 = N − R0
+__host__ __device__ constexpr int tw_count_c(int lg) { return (1 << lg) - r0_of(lg); }
+
+template <int NT> __device__ __forceinline__ void xsync() {
+    if constexpr (NT <= 32) __syncwarp();
+    else __syncthreads();
+}
+
+// stage-0 butterflies: radix R0, 16/R0 per thread, inputs v[b + B·r]
+template <int DIR, int R> __device__ __forceinline__ void stage0(float2 *v) {
+    constexpr int B = 16 / R;
+    if constexpr (R == 16) {
+        dft16<DIR>(v);
+    } else {
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            if constexpr (R == 2) dft2<DIR>(v[b], v[b + B]);
+            else if constexpr (R == 4) dft4<DIR>(v[b], v[b + B], v[b + 2 * B], v[b + 3 * B]);
+            else dft8<DIR>(v + b, B);
+        }
+    }
+}
+
+// Stockham exchange after a stage of radix RP and span NSP: outputs to shared memory, read back
+// x[t + NT·e] for the next stage
+template <int NT, int RP, int NSP> __device__ __forceinline__ void exchange(float2 *v, float2 *S, int t) {
+    constexpr int B = 16 / RP;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        const int j = t + NT * b;
+        const int k = j & (NSP - 1);
+        const int base = (j - k) * RP + k;
+#pragma unroll
+        for (int r = 0; r < RP; ++r) S[pad(base + NSP * r)] = v[b + B * r];
+    }
+    xsync<NT>();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = S[pad(t + NT * e)];
+    xsync<NT>();
+}
+
+template <int LG, int DIR, int RP, int NSP>
+__device__ __forceinline__ void stages16(float2 *v, float2 *S, const float2 *__restrict__ tw, int t) {
+    constexpr int N = 1 << LG, NT = N >> 4, NS = NSP * RP;
+    if constexpr (NS < N) {
+        exchange<NT, RP, NSP>(v, S, t);
+        const int k = t & (NS - 1);
+        const float2 *w = tw + (NS - r0_of(LG)) + 15 * k;   // table of span NS starts at NS − R0
+#pragma unroll
+        for (int r = 1; r < 16; ++r) {
+            float2 c = w[r - 1];
+            if (DIR > 0) c.y = -c.y;
+            v[r] = cmul(v[r], c);
+        }
+        dft16<DIR>(v);
+        stages16<LG, DIR, 16, NS>(v, S, tw, t);
+    }
+}
+
+// Full 2^LG-point DFT of the data held as v[e] = x[t + NT·e]; on return v[e] = X[t + NT·e].
+// triv0: only the r = 0 inputs of every stage-0 butterfly are nonzero (x[i] = 0 for i >= NT·16/R0),
+// so stage 0 just replicates them.  All NT threads of the transform (and, for NT > 32, all threads
+// of the CTA) must call it together.
+template <int LG, int DIR>
+__device__ __forceinline__ void fft(float2 *v, float2 *S, const float2 *__restrict__ tw, int t, bool triv0) {
+    constexpr int R0 = r0_of(LG), B0 = 16 / R0;
+    if (triv0) {
+#pragma unroll
+        for (int b = 0; b < B0; ++b)
+#pragma unroll
+            for (int r = 1; r < R0; ++r) v[b + B0 * r] = v[b];
+    } else {
+        stage0<DIR, R0>(v);
+    }
+    stages16<LG, DIR, R0, 1>(v, S, tw, t);
+}
+
+// Launch shapes.  Passes A and C (HBM-bound, transposed column access) run TPC = 2 transforms
+// (4 real columns: 32-byte segments per fx) per CTA at 2^12 points and 256-thread CTAs below,
+// with 64 registers per thread.  Pass B (compute-bound: two transforms and the spectrum product per
+// row) runs 256-thread CTAs with up to 85 registers (3 CTAs / SM), which avoids the local-memory
+// spills a 64-register budget causes; the grouped averaging keeps a running sum and needs 128.
+template <int LG, bool ROWPASS = false> struct Cfg {
+    static constexpr int N = 1 << LG, NT = N / 16, H = N / 2 + 1;
+    static constexpr int TPC = ROWPASS ? (NT >= 256 ? 1 : 256 / NT) : (NT >= 256 ? 2 : 256 / NT);
+    static constexpr int THREADS = NT * TPC;
+    static constexpr int MINB = ROWPASS ? 3 : 65536 / (THREADS * 64);
+    static constexpr int TW = tw_count_c(LG);
+    static constexpr int TWP = (TW + 1) & ~1;               // keep the buffers 16-B aligned
+    static constexpr int XB = (pad_size(N) + 1) & ~1;       // one exchange buffer
+    static constexpr size_t smem = sizeof(float2) * ((size_t)TWP + (size_t)TPC * XB);
+};
+
+template <int LG> __device__ __forceinline__ float2 *stage_tw(float2 *sm, const float2 *__restrict__ twg) {
+    for (int i = threadIdx.x; i < Cfg<LG>::TW; i += blockDim.x) sm[i] = twg[i];
+    return sm;
+}
+template <int LG> __device__ __forceinline__ float2 *xbuf(float2 *sm, int q) {
+    return sm + Cfg<LG>::TWP + (size_t)q * Cfg<LG>::XB;
+}
+
+// ------------------------------------------------------------------------------------ pass A
+template <int LG>
+__global__ void __launch_bounds__(Cfg<LG>::THREADS, Cfg<LG>::MINB)
+rpass_a(const float *__restrict__ in, int64_t ld, const int *__restrict__ map, int bx, int by,
+        const int *__restrict__ jsel, const double *__restrict__ scale, float2 *__restrict__ A,
+        const float2 *__restrict__ twg) {
+    using C = Cfg<LG>;
+    constexpr int N = C::N, NT = C::NT, H = C::H, CB = 2 * C::TPC;
+    extern __shared__ float2 sm[];
+    const float2 *tw = stage_tw<LG>(sm, twg);
+    const int q = threadIdx.x / NT, t = threadIdx.x % NT;
+    float2 *S = xbuf<LG>(sm, q);
+    const int col0 = blockIdx.x * CB;
+    const int jo = blockIdx.y;
+    const int j = jsel ? jsel[jo] : jo;
+    const float sc = scale ? (float)scale[j] : 1.f;
+    const int ca = col0 + 2 * q, cb = ca + 1;
+    const float *src = in + ld * j;
+    float2 v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int ix = t + NT * e;
+        float a = 0.f, b = 0.f;
+        if (ix < bx) {
+            if (ca < by) {
+                const int64_t box = ix + (int64_t)bx * ca;
+                const int64_t ci = map ? (int64_t)map[box] : box;
+                if (ci >= 0) a = sc * src[ci];
+            }
+            if (cb < by) {
+                const int64_t box = ix + (int64_t)bx * cb;
+                const int64_t ci = map ? (int64_t)map[box] : box;
+                if (ci >= 0) b = sc * src[ci];
+            }
+        }
+        v[e] = make_float2(a, b);
+    }
+    __syncthreads();   // twiddle table staged
+    fft<LG, -1>(v, S, tw, t, false);
+    // Hermitian split of the two packed real columns: X_a[f] = (Z[f] + conj Z[−f]) / 2,
+    // X_b[f] = (Z[f] − conj Z[−f]) / (2i); needs Z[f] and Z[N − f] (held by other threads)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) S[pad(t + NT * e)] = v[e];
+    __syncthreads();
+    // transposed write, consecutive threads -> consecutive columns of one fx
+    for (int idx = threadIdx.x; idx < H * CB; idx += blockDim.x) {
+        const int fx = idx / CB, c = idx - fx * CB;
+        const int col = col0 + c;
+        if (col >= by) continue;
+        const float2 *Sq = xbuf<LG>(sm, c >> 1);
+        const float2 z = Sq[pad(fx)], zm = Sq[pad((N - fx) & (N - 1))];
+        const float2 o = (c & 1) ? make_float2(0.5f * (z.y + zm.y), 0.5f * (zm.x - z.x))
+                                 : make_float2(0.5f * (z.x + zm.x), 0.5f * (z.y - zm.y));
+        A[((int64_t)jo * H + fx) * by + col] = o;
+    }
+}
+
+// ------------------------------------------------------------------------------------ pass B
+// grid (k, ceil(H / TPC)): the k CTAs that use the same X̂ rows run back to back (X̂ stays in L2)
+template <int LG>
+__global__ void __launch_bounds__(Cfg<LG, true>::THREADS, Cfg<LG, true>::MINB)
+rpass_b(const float2 *__restrict__ A, int ny_in, int H, const float2 *__restrict__ Xh, float2 *__restrict__ B,
+        int ny_out, const float2 *__restrict__ twg) {
+    using C = Cfg<LG, true>;
+    constexpr int N = C::N, NT = C::NT, TPC = C::TPC, B0 = 16 / r0_of(LG);
+    extern __shared__ float2 sm[];
+    const float2 *tw = stage_tw<LG>(sm, twg);
+    const int q = threadIdx.x / NT, t = threadIdx.x % NT;
+    float2 *S = xbuf<LG>(sm, q);
+    const int j = blockIdx.x;
+    const int fx = blockIdx.y * TPC + q;
+    const bool ok = fx < H;
+    const float2 *arow = A + ((int64_t)j * H + fx) * ny_in;
+    float2 v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int y = t + NT * e;
+        v[e] = (ok && y < ny_in) ? arow[y] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    fft<LG, -1>(v, S, tw, t, ny_in <= NT * B0);
+    const float2 *xr = Xh + (int64_t)(ok ? fx : 0) * N;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cmulc(__ldg(xr + t + NT * e), v[e]);   // X̂ ⊙ conj(Â)
+    fft<LG, +1>(v, S, tw, t, false);
+    float2 *brow = B + ((int64_t)j * H + fx) * ny_out;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int y = t + NT * e;
+        if (ok && y < ny_out) brow[y] = v[e];
+    }
+}
+
+// averaging: per (g, fx) Σ_{i∈I_g} DFT_y(AU_i) ⊙ DFT_y(AV_i), inverse; the AU transform of a member
+// waits in a thread-private shared-memory slot while the AV transform runs
+template <int LG>
+__global__ void __launch_bounds__(Cfg<LG, true>::THREADS, 1)
+rpass_bconv(const float2 *__restrict__ AU, int ly, const float2 *__restrict__ AV, int ky, const int *__restrict__ grp_off,
+            const int *__restrict__ grp_idx, const int *__restrict__ slot, int H, float2 *__restrict__ B, int ny_out,
+            const float2 *__restrict__ twg) {
+    using C = Cfg<LG, true>;
+    constexpr int NT = C::NT, TPC = C::TPC, B0 = 16 / r0_of(LG);
+    extern __shared__ float2 sm[];
+    const float2 *tw = stage_tw<LG>(sm, twg);
+    const int q = threadIdx.x / NT, t = threadIdx.x % NT;
+    float2 *S = xbuf<LG>(sm, q);
+    float2 *P = xbuf<LG>(sm, TPC + q);      // private slots of this transform
+    const int g = blockIdx.y;
+    const int fx = blockIdx.x * TPC + q;
+    const bool ok = fx < H;
+    float2 acc[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = make_float2(0.f, 0.f);
+    __syncthreads();
+    for (int m = grp_off[g]; m < grp_off[g + 1]; ++m) {
+        const int s = slot[grp_idx[m]];
+        float2 v[16];
+        const float2 *ur = AU + ((int64_t)s * H + fx) * ly;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int y = t + NT * e;
+            v[e] = (ok && y < ly) ? ur[y] : make_float2(0.f, 0.f);
+        }
+        fft<LG, -1>(v, S, tw, t, ly <= NT * B0);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) P[pad(t + NT * e)] = v[e];
+        const float2 *vr = AV + ((int64_t)s * H + fx) * ky;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int y = t + NT * e;
+            v[e] = (ok && y < ky) ? vr[y] : make_float2(0.f, 0.f);
+        }
+        fft<LG, -1>(v, S, tw, t, ky <= NT * B0);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const float2 u = P[pad(t + NT * e)];
+            acc[e] = cadd(acc[e], cmul(u, v[e]));
+        }
+    }
+    fft<LG, +1>(acc, S, tw, t, false);
+    float2 *brow = B + ((int64_t)g * H + fx) * ny_out;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int y = t + NT * e;
+        if (ok && y < ny_out) brow[y] = acc[e];
+    }
+}
+
+// ------------------------------------------------------------------------------------ pass C
+template <int LG>
+__global__ void __launch_bounds__(Cfg<LG>::THREADS, Cfg<LG>::MINB)
+rpass_c(const float2 *__restrict__ B, int oy, int H, int ox, float inv, float *__restrict__ out, int64_t ldo,
+        const int *__restrict__ omap, const int *__restrict__ w, int64_t stride, const float2 *__restrict__ twg) {
+    using C = Cfg<LG>;
+    constexpr int N = C::N, NT = C::NT, CB = 2 * C::TPC;
+    extern __shared__ float2 sm[];
+    const float2 *tw = stage_tw<LG>(sm, twg);
+    const int q = threadIdx.x / NT, t = threadIdx.x % NT;
+    float2 *S = xbuf<LG>(sm, q);
+    const int y0 = blockIdx.x * CB;
+    const int j = blockIdx.y;
+    const int ncol = min(CB, oy - y0);
+    // gather the CB half-spectrum columns: transform q's buffer holds columns 2q (at [0, H)) and
+    // 2q + 1 (at [H, 2H)); consecutive threads read consecutive columns of one fx
+    const float2 *bj = B + (int64_t)j * H * oy + y0;
+    for (int idx = threadIdx.x; idx < H * CB; idx += blockDim.x) {
+        const int fx = idx / CB, c = idx - fx * CB;
+        float2 val = make_float2(0.f, 0.f);
+        if (c < ncol) val = bj[(int64_t)fx * oy + c];
+        xbuf<LG>(sm, c >> 1)[(c & 1) * H + fx] = val;
+    }
+    __syncthreads();
+    // Z[f] = Y_a[f] + i·Y_b[f] over the full spectrum (Y[N − f] = conj Y[f] for real columns;
+    // the bins 0 and N/2 of a real column are real)
+    float2 v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int f = t + NT * e;
+        const bool lo = f <= N / 2;
+        const int fs = lo ? f : N - f;
+        float2 ya = S[fs], yb = S[H + fs];
+        if (!lo) { ya.y = -ya.y; yb.y = -yb.y; }
+        if (f == 0 || f == N / 2) { ya.y = 0.f; yb.y = 0.f; }
+        v[e] = make_float2(ya.x - yb.y, ya.y + yb.x);
+    }
+    __syncthreads();   // the buffers are reused by the exchanges
+    fft<LG, +1>(v, S, tw, t, false);
+    const int ya_col = y0 + 2 * q;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int x = t + NT * e;
+        if (x >= ox) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int y = ya_col + h;
+            if (y - y0 >= ncol) continue;
+            const float val = (h ? v[e].y : v[e].x) * inv;
+            if (w) {
+                const int wn = w[x + (int64_t)ox * y];
+                out[(int64_t)j * stride + x + ldo * y] = wn > 0 ? val / (float)wn : __int_as_float(0x7fc00000);
+            } else {
+                const int64_t box = x + (int64_t)ox * y;
+                const int64_t oi = omap ? (int64_t)omap[box] : box;
+                if (oi >= 0) out[oi + ldo * j] = val;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------ host side
+int tw_count(int lg) { return tw_count_c(lg); }
+
+void build_table(int lg, std::vector<float2> &h) {
+    const int N = 1 << lg, R0 = r0_of(lg);
+    h.assign((size_t)tw_count_c(lg), make_float2(0.f, 0.f));
+    for (int ns = R0; ns < N; ns *= 16)
+        for (int k = 0; k < ns; ++k)
+            for (int r = 1; r < 16; ++r) {
+                const double a = -2.0 * M_PI * (double)(r * k) / (16.0 * ns);
+                h[(size_t)(ns - R0) + 15 * k + (r - 1)] = make_float2((float)std::cos(a), (float)std::sin(a));
+            }
+}
+
+// the kernel's dynamic shared memory exceeds the 48 KB default: raise the cap once per kernel
+template <typename F> static void prep(F *kern, size_t) { set_max_smem(kern); }
+
+#define RFFT_DISPATCH(lg, ...)                       \
+    switch (lg) {                                     \
+    case 8: { constexpr int LG = 8; __VA_ARGS__; } break;    \
+    case 9: { constexpr int LG = 9; __VA_ARGS__; } break;    \
+    case 10: { constexpr int LG = 10; __VA_ARGS__; } break;  \
+    case 11: { constexpr int LG = 11; __VA_ARGS__; } break;  \
+    case 12: { constexpr int LG = 12; __VA_ARGS__; } break;  \
+    default: throw Error(SSA_ERR_ARG, "rfft: unsupported transform size"); \
+    }
+
+void pass_a(int lg, const float *in, int64_t ld, const int *map, int bx, int by, int k, const int *jsel,
+            const double *scale, float2 *A, const float2 *tw, cudaStream_t st) {
+    RFFT_DISPATCH(lg, {
+        using Cf = Cfg<LG>;
+        prep(rpass_a<LG>, Cf::smem);
+        rpass_a<LG><<<dim3((unsigned)cdiv(by, 2 * Cf::TPC), k), Cf::THREADS, Cf::smem, st>>>(in, ld, map, bx, by, jsel,
+                                                                                             scale, A, tw);
+    });
+    after_launch("rfft_pass_a");
+}
+
+void pass_b(int lg, const float2 *A, int ny_in, int H, int k, const float2 *Xh, float2 *B, int ny_out,
+            const float2 *tw, cudaStream_t st) {
+    RFFT_DISPATCH(lg, {
+        using Cf = Cfg<LG, true>;
+        prep(rpass_b<LG>, Cf::smem);
+        rpass_b<LG><<<dim3(k, (unsigned)cdiv(H, Cf::TPC)), Cf::THREADS, Cf::smem, st>>>(A, ny_in, H, Xh, B, ny_out, tw);
+    });
+    after_launch("rfft_pass_b");
+}
+
+void pass_bconv(int lg, const float2 *AU, int ly, const float2 *AV, int ky, const int *grp_off, const int *grp_idx,
+                const int *slot, int H, int ng, float2 *B, int ny_out, const float2 *tw, cudaStream_t st) {
+    RFFT_DISPATCH(lg, {
+        using Cf = Cfg<LG, true>;
+        const size_t smem = Cf::smem + sizeof(float2) * (size_t)Cf::TPC * Cf::XB;
+        prep(rpass_bconv<LG>, smem);
+        rpass_bconv<LG><<<dim3((unsigned)cdiv(H, Cf::TPC), ng), Cf::THREADS, smem, st>>>(AU, ly, AV, ky, grp_off, grp_idx,
+                                                                                          slot, H, B, ny_out, tw);
+    });
+    after_launch("rfft_pass_bconv");
+}
+
+void pass_c(int lg, const float2 *B, int oy, int H, int k, int ox, float inv, float *out, int64_t ldo,
+            const int *omap, const int *w, int64_t stride, const float2 *tw, cudaStream_t st) {
+    RFFT_DISPATCH(lg, {
+        using Cf = Cfg<LG>;
+        static_assert(2 * Cfg<LG>::H <= ((pad_size(1 << LG) + 1) & ~1), "column pair fits the exchange buffer");
+        prep(rpass_c<LG>, Cf::smem);
+        rpass_c<LG><<<dim3((unsigned)cdiv(oy, 2 * Cf::TPC), k), Cf::THREADS, Cf::smem, st>>>(B, oy, H, ox, inv, out, ldo,
+                                                                                             omap, w, stride, tw);
+    });
+    after_launch("rfft_pass_c");
+}
+
+}  // namespace rfft
+}  // namespace ssa

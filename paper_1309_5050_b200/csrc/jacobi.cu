@@ -641,103 +641,9 @@ static bool jacobi_try_cluster(int m, int n, double *T, int *sweeps, cudaStream_
     return false;
 }
 
-// ---------------------------------------------------------------------------
-// Single-CTA one-sided Jacobi with the whole matrix in shared memory (fp64, m·n·8
-// bytes <= ~220 KB): 32 warps rotate the n/2 disjoint column pairs of a round-robin
-// round in parallel (warp w takes pairs w, w+32, ...), one __syncthreads per round,
-// rounds repeat until a whole sweep rotated nothing.  No cross-SM traffic at all,
-// which is what bounds the cluster / grid versions (a cluster barrier per round).
-// Rotation in fp64: ζ = (β−α)/(2γ), t = sign(ζ)/(|ζ| + √(1+ζ²)), c = 1/√(1+t²), s = c·t.
-// ---------------------------------------------------------------------------
-template <int MR>
-__global__ void __launch_bounds__(MR <= 6 ? 1024 : 512, 1)
-jacobi_smem_kernel(int m, int n, double *__restrict__ A, double tol, int max_sweeps, int *__restrict__ sweeps_out) {
-    extern __shared__ __align__(16) double C[];      // [n][ld], ld = m rounded to the warp width
-    __shared__ int rotated;
-    const int ld = ((m + 31) / 32) * 32;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int idx = tid; idx < n * ld; idx += blockDim.x) {
-        const int j = idx / ld, i = idx - j * ld;
-        C[idx] = (i < m) ? A[i + (int64_t)m * j] : 0.0;
-    }
-    const int np = n + (n & 1);                       // even number of positions (one dummy)
-    int sweep = 0;
-    for (; sweep < max_sweeps; ++sweep) {
-        if (tid == 0) rotated = 0;
-        __syncthreads();
-        int rot = 0;
-        for (int r = 0; r < np - 1; ++r) {
-            for (int k = warp; k < np / 2; k += (int)(blockDim.x >> 5)) {
-                int p, q;
-                if (k == 0) { p = np - 1; q = r; }
-                else { p = (r + k) % (np - 1); q = (r - k + (np - 1)) % (np - 1); }
-                if (p >= n || q >= n) continue;
-                double *cp = C + (size_t)ld * p, *cq = C + (size_t)ld * q;
-                double x[MR], y[MR];
-                double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-                for (int u = 0; u < MR; ++u) {
-                    const int i = lane + 32 * u;
-                    x[u] = (i < ld) ? cp[i] : 0.0;
-                    y[u] = (i < ld) ? cq[i] : 0.0;
-                    al = fma(x[u], x[u], al); be = fma(y[u], y[u], be); ga = fma(x[u], y[u], ga);
-                }
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    al += __shfl_xor_sync(0xffffffffu, al, o);
-                    be += __shfl_xor_sync(0xffffffffu, be, o);
-                    ga += __shfl_xor_sync(0xffffffffu, ga, o);
-                }
-                if (!(fabs(ga) > tol * sqrt(al * be))) continue;
-                const double zeta = (be - al) / (2.0 * ga);
-                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-                const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
-#pragma unroll
-                for (int u = 0; u < MR; ++u) {
-                    const int i = lane + 32 * u;
-                    if (i < ld) {
-                        cp[i] = c * x[u] - sn * y[u];
-                        cq[i] = sn * x[u] + c * y[u];
-                    }
-                }
-                rot = 1;
-            }
-            __syncthreads();
-        }
-        if (rot) rotated = 1;   // benign race: every writer stores 1
-        __syncthreads();
-        if (!rotated) break;
-    }
-    for (int idx = tid; idx < n * ld; idx += blockDim.x) {
-        const int j = idx / ld, i = idx - j * ld;
-        if (i < m) A[i + (int64_t)m * j] = C[idx];
-    }
-    if (tid == 0 && sweeps_out) *sweeps_out = sweep + 1;
-}
-
-static size_t jacobi_smem_bytes(int m, int n) { return sizeof(double) * (size_t)((m + 31) / 32 * 32) * n; }
-bool jacobi_smem_fits(int m, int n) { return m <= 32 * 8 && jacobi_smem_bytes(m, n) <= 225 * 1024; }
-
-static bool jacobi_try_smem(int m, int n, double *T, int *sweeps, cudaStream_t st) {
-    // opt-in: one SM is fp64-compute bound (measured 5.5 ms vs 2.1 ms for the 10-CTA cluster
-    // version on 160 x 128), so the cluster kernel stays the default
-    if (!std::getenv("SSA_JACOBI_SMEM") || !jacobi_smem_fits(m, n)) return false;
-    const size_t smem = jacobi_smem_bytes(m, n);
-    void *kern = m <= 32 * 4 ? (void *)jacobi_smem_kernel<4> : m <= 32 * 6 ? (void *)jacobi_smem_kernel<6>
-                                                                            : (void *)jacobi_smem_kernel<8>;
-    set_max_smem(kern);
-    double tol = 1e-12;
-    int max_sweeps = 60;
-    void *args[] = {&m, &n, &T, &tol, &max_sweeps, &sweeps};
-    SSA_CUDA(cudaLaunchKernel(kern, dim3(1), dim3(m <= 32 * 6 ? 1024 : 512), args, smem, st));
-    after_launch("jacobi_smem");
-    return true;
-}
-
 void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st, double tol_d,
                         double early) {
     const float tol = (float)tol_d;
-    if (jacobi_try_smem(m, n, T, sweeps, st)) return;
     if (jacobi_try_cluster(m, n, T, sweeps, st, tol, (float)early)) return;
     int nb = (int)cdiv(n, kBW);
     nb += nb & 1;

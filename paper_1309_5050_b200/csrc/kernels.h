@@ -74,7 +74,6 @@ bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int
              double *partials, size_t partial_bytes, cudaStream_t st);
 void box_kmask(const uint8_t *nmask, int nx, int ny, int lx, int ly, uint8_t *kmask, int32_t *tmp, cudaStream_t st);
 void box_weights(const uint8_t *kmask, int nx, int ny, int lx, int ly, int32_t *w, int32_t *tmp, cudaStream_t st);
-void tma_probe(const float *A, int64_t M, int n, int64_t ld, int bc, int rg, cudaStream_t st);
 // tcgen05 3xTF32 update Out = beta·Out + alpha·A·C (tall_tc.cu); false when unsupported
 bool update_tc(int64_t M, const float *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
                double beta, float *Out, int64_t ldo, cudaStream_t st);
@@ -89,17 +88,6 @@ void gemm_small(int64_t M, const T *A, int64_t lda, int m, const double *C, int 
 template <typename T>
 void gemm_acc(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
               double beta, T *Out, int64_t ldo, cudaStream_t st);
-
-// Out (M x n) = A (M x m) · C (device double); Out != A; column groups across CTAs (short bases).
-template <typename T>
-void gemm_cols(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, T *Out, int64_t ldo,
-               cudaStream_t st);
-
-// Device-resident CGS + CholeskyQR pass (blas.cu): see orth_solve_kernel.
-void orth_solve(const double *G, int na, int kc, int pass, double zthr2, double shift_rel, double thr_chol,
-                double *Mout, double *Ctot, double *Btot, int *flags, cudaStream_t st);
-template <typename T>
-void apply_inplace(int64_t M, T *A, int64_t lda, int n1, int kc, const double *Mc, const int *skip, cudaStream_t st);
 
 // A[:, cols] = N(0,1) from a counter-based generator keyed by (seed, stream_id).
 template <typename T>
@@ -130,10 +118,5 @@ template <typename T>
 void scale_columns(int64_t M, T *A, int64_t lda, int n, const double *s, cudaStream_t st);
 template <typename T>
 void absmax_sign(int64_t M, const T *A, int64_t lda, int n, double *sgn, cudaStream_t st);
-
-// one CholeskyQR pass (G = WᵀW, RᵀR = G, W ← W R⁻¹) in a single cooperative launch (cholqr.cu)
-size_t cholqr_ws_bytes(int kc);
-bool cholqr_fused(int64_t M, float *W, int64_t ld, int kc, double shift_rel, double thr_chol, double *ws, size_t ws_bytes,
-                  double *out, cudaStream_t st);
 
 }  // namespace ssa

@@ -25,7 +25,8 @@ struct PlanImpl {
     cudaStream_t st = nullptr;
     ssa_comm comm{};
     bool has_comm = false;
-    int64_t band_y0 = 0, band_y1 = 0;
+    int64_t band_y0 = 0, band_y1 = 0;   // band plans: this rank's global origin columns
+    int64_t ny_global = 0;              // band plans: columns of the global image
     bool broken = false;          // sticky CUDA / comm failure
 
     // ---- device data ---------------------------------------------------------
@@ -48,6 +49,7 @@ struct PlanImpl {
     // ---- decomposition ------------------------------------------------------
     int r = 0;
     std::vector<double> sigma;
+    std::vector<double> residuals;   // per-triple residual bounds ||Xᵀu_i − σ_i v_i|| of the last decomposition
     DevBuf U;          // T[L*r]
     DevBuf V;          // T[K*r] (valid if v_valid)
     bool v_valid = false;
@@ -66,6 +68,7 @@ void op_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k);   /
 double *small_dev(PlanImpl &p, size_t n_doubles);
 
 // solver.cu
+double sigma_floor(const PlanImpl &p);   // reading Q10: measured σ floor τ of the plan's product paths
 template <typename T>
 void decompose(PlanImpl &p, int r, ssa_decomp_info *info);
 
@@ -78,7 +81,8 @@ template <typename T>
 void fft_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k);
 template <typename T>
 void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, const int *grp_off_dev,
-                  const int *grp_idx_dev, int ng, const std::vector<int> &used, const int *slot_dev, T *out);
+                  const int *grp_idx_dev, int ng, const std::vector<int> &used, const int *slot_dev, T *out,
+                  const int *wdiv);   // wdiv: hit counts of the ÷𝕎 epilogue
 void fft_destroy(FftOperator *f);
 
 }  // namespace ssa

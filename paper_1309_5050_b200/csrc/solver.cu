@@ -95,7 +95,6 @@ struct Staging {
 void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cudaStream_t st, double tol, double early);
 bool jacobi_blocked_fits(int m, int n);
 void ritz_tn(int m, int n, const double *T0, const double *A, double *W, double *nrm, cudaStream_t st);
-bool jacobi_smem_fits(int m, int n);
 
 template <typename T>
 struct Gkl {
@@ -117,19 +116,35 @@ struct Gkl {
     uint64_t sid = 1;
     double thr_abs, thr_rel, thr_chol;
     bool gpu_ritz = true;
-    bool full_k_reorth = false;   // set when K < L (then the K side is the short one)
     bool debug = std::getenv("SSA_DEBUG") != nullptr;
-    bool use_fast = std::getenv("SSA_ORTH_FAST") != nullptr;   // device-resident orth (experimental)
-    DevBuf ow;                    // device workspace of the fast orthonormalisation
     double tw_prod = 0, tw_orthA = 0, tw_orthB = 0, tw_rec = 0, tw_restart = 0;   // host wall ms (SSA_DEBUG)
     double tw_o3_gram[2] = {0, 0}, tw_o3_host[2] = {0, 0}, tw_o3_apply[2] = {0, 0};   // orth3 split [L, K side]
     static double now_ms() {
         return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
     }
     int64_t n_fast = 0, n_fallback = 0;
+    std::vector<double> res;      // residual bounds of the current Ritz triples
+    double drop2 = 0.0;           // Σ squared norms of block columns discarded as numerically zero
+    int warm_cols = 0;            // start-block columns taken from a previous decomposition
+    DevBuf agree_buf;
+
+    // Average `n` host doubles over the ranks of a band partition (identical result on every rank:
+    // the collective returns the same bits everywhere), so per-rank timing decisions agree.
+    void agree(double *v, int n) {
+        agree_buf.alloc(sizeof(double) * 8, st);
+        SSA_CUDA(cudaMemcpyAsync(agree_buf.p, v, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        if (p.comm.allreduce_sum(p.comm.user, agree_buf.p, n, SSA_F64, st) != 0)
+            throw Error(SSA_ERR_COMM, "allreduce of the convergence-check timings failed");
+        SSA_CUDA(cudaMemcpyAsync(v, agree_buf.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        stream_wait(st);
+        for (int i = 0; i < n; ++i) v[i] /= p.comm.world;
+    }
 
     explicit Gkl(PlanImpl &pl) : p(pl), st(pl.st), L(pl.L), K(pl.K) {
-        thr_abs = (sizeof(T) == 4) ? 1e-6 : 1e-14;
+        // breakdown threshold (relative to ||X||): well below both the convergence tolerance and the
+        // fp32 product rounding (~1e-7), so only numerically zero columns are discarded (and their
+        // norms enter the residual bound, drop2); decoupled from tol
+        thr_abs = (sizeof(T) == 4) ? 1e-8 : 1e-14;
         thr_rel = (sizeof(T) == 4) ? 1e-10 : 1e-26;
         thr_chol = (sizeof(T) == 4) ? 1e-6 : 1e-13;
         sg.init(1 << 18, st);
@@ -274,6 +289,7 @@ struct Gkl {
                 const bool tiny_abs = (pass == 0 && refills == 0) && !(d > thr_abs * std::max(anorm, 1e-300));
                 if (tiny_abs || !(d * d > 1e-24 * dmax) || !(dmax > 0.0)) zero.push_back(j);
             }
+            for (int j : zero) drop2 += std::max(G[j + (size_t)kc * j], 0.0);
             if (!zero.empty() && refills < 2) {
                 ++refills;
                 for (int j : zero)
@@ -339,163 +355,6 @@ struct Gkl {
     }
 
 
-    // Device-resident orthonormalisation of W (M x kc) against the na columns that
-    // precede it in the same buffer: two (rarely three) CGS + CholeskyQR passes run as
-    // gram_tn / orth_solve / apply_inplace launches with ONE host synchronisation (the
-    // coefficients and flags come back together).  Returns false — W is then garbage and
-    // the caller recomputes it and takes the robust host path `orth` — when a column is
-    // numerically in span(A) or zero (breakdown), or the passes did not converge.
-    bool orth_fast(int64_t M, T *W, int kc, const T *against, int na, bool kside, double *coef,
-                   std::vector<double> &Bout) {
-        if (!use_fast || kc > 64 || na + kc > 512) return false;
-        if (na > 0 && against + (int64_t)na * LD(M) != W) return false;   // needs [A W] contiguous
-        T *A = na > 0 ? const_cast<T *>(against) : W;
-        const int n1 = na + kc;
-        const size_t nd = 3 * 512 * 64 + 64 * 64 + 16;
-        ow.alloc(sizeof(double) * nd, st);
-        double *dG = ow.as<double>(), *dMc = dG + 512 * 64, *dC = dMc + 512 * 64, *dBt = dC + 512 * 64;
-        int *flags = reinterpret_cast<int *>(dBt + 64 * 64);
-        SSA_CUDA(cudaMemsetAsync(flags, 0, 8 * sizeof(int), st));
-        const double zt = thr_abs * std::max(anorm, 1e-300);
-        const double shift_rel = (sizeof(T) == 4) ? 1e-6 : 1e-13;
-        const size_t ic = sg.take((size_t)na * kc + (size_t)kc * kc + 8);
-        double *hC = sg.h + ic, *hB = hC + (size_t)na * kc;
-        int *hf = reinterpret_cast<int *>(hB + (size_t)kc * kc);
-        for (int pass = 1; pass <= 3; ++pass) {
-            gram_tn<T>(M, A, LD(M), n1, W, LD(M), kc, dG, p.ws_gram.as<double>(), p.ws_gram.bytes, st);
-            if (kside && kside_comm()) {
-                if (p.comm.allreduce_sum(p.comm.user, dG, (int64_t)n1 * kc, SSA_F64, st) != 0)
-                    throw Error(SSA_ERR_COMM, "allreduce of a K-side Gram failed");
-            }
-            orth_solve(dG, na, kc, pass, zt * zt, shift_rel, thr_chol, dMc, dC, dBt, flags, st);
-            apply_inplace<T>(M, A, LD(M), n1, kc, dMc, flags, st);
-            if (pass == 1) continue;
-            if (na > 0) SSA_CUDA(cudaMemcpyAsync(hC, dC, sizeof(double) * na * kc, cudaMemcpyDeviceToHost, st));
-            SSA_CUDA(cudaMemcpyAsync(hB, dBt, sizeof(double) * kc * kc, cudaMemcpyDeviceToHost, st));
-            SSA_CUDA(cudaMemcpyAsync(hf, flags, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
-            SSA_CUDA(cudaStreamSynchronize(st));
-            if (hf[0]) { ++n_fallback; return false; }
-            if (!hf[2]) break;
-            if (pass == 3) { ++n_fallback; return false; }
-        }
-        sg.off = 0;
-        for (size_t t = 0; t < (size_t)na * kc; ++t) coef[t] += hC[t];
-        Bout.assign(hB, hB + (size_t)kc * kc);
-        ++n_fast;
-        return true;
-    }
-
-
-    // Orthonormalisation with one host round trip per pass (the default path).  W (M x kc)
-    // follows the na orthonormal columns `against` in the same buffer, so one Gram launch
-    // gives G = [A W]ᵀ W; the host forms C = G[0:na], Gp = WᵀW − CᵀC (= W'ᵀW' for W' = W − A C),
-    // its Cholesky factor R (shifted when needed) and M = [−C R⁻¹; R⁻¹]; one launch applies
-    // W ← [A W]·M.  Pass 2 repeats on the result (CGS2 + CholeskyQR2); a pass 3 runs only if
-    // pass 2 was shifted or its Gram was far from the identity.  Breakdown (a column whose
-    // projected norm is below thr_abs·‖X‖ or numerically zero) is detected on pass 1's Gram,
-    // before W is touched, and handed to the robust `orth` (random refills, SVQB).
-    // Returns B with W_in = A·coef + W_out·B (coef accumulated, as in `orth`).
-    std::vector<double> orth2(int64_t M, T *W, int kc, const T *against, int na, bool kside, double *coef) {
-        // opt-in (SSA_ORTH2=1): measured no faster than `orth` on c2/c3 (the Gram / update
-        // kernels, not the host round trips, dominate the K side), DESIGN.md §5
-        if (kc > 64 || na + kc > 512 || (na > 0 && against + (int64_t)na * LD(M) != W) || !std::getenv("SSA_ORTH2"))
-            return orth(M, W, kc, against, na, kside, coef);
-        T *A = na > 0 ? const_cast<T *>(against) : W;
-        const int n1 = na + kc;
-        std::vector<double> G((size_t)n1 * kc), Gp((size_t)kc * kc), R, Sinv, Mc((size_t)n1 * kc);
-        std::vector<double> Ctot((size_t)na * kc, 0.0), Btot((size_t)kc * kc, 0.0);
-        const double shift_rel = (sizeof(T) == 4) ? 1e-6 : 1e-13;
-        bool prev_shifted = false;
-        for (int pass = 1; pass <= 3; ++pass) {
-            gram(M, A, LD(M), n1, W, LD(M), kc, G.data(), kside);
-            double dmax = 0.0, dev = 0.0;
-            for (int b = 0; b < kc; ++b)
-                for (int a = 0; a <= b; ++a) {
-                    double v = G[na + a + (size_t)n1 * b];
-                    for (int t = 0; t < na; ++t) v -= G[t + (size_t)n1 * a] * G[t + (size_t)n1 * b];
-                    Gp[a + (size_t)kc * b] = v;
-                    Gp[b + (size_t)kc * a] = v;
-                }
-            for (int j = 0; j < kc; ++j) dmax = std::max(dmax, Gp[j + (size_t)kc * j]);
-            for (int b = 0; b < kc; ++b)
-                for (int a = 0; a < kc; ++a) dev = std::max(dev, std::fabs(Gp[a + (size_t)kc * b] - (a == b ? 1.0 : 0.0)));
-            bool trouble = !(dmax > 0.0) || !std::isfinite(dmax);
-            if (pass == 1)
-                for (int j = 0; j < kc && !trouble; ++j) {
-                    const double d = Gp[j + (size_t)kc * j];
-                    const double nrm = std::sqrt(std::max(d, 0.0));
-                    trouble = !(nrm > thr_abs * std::max(anorm, 1e-300)) || !(d > 1e-24 * dmax) ||
-                              !(d > (sizeof(T) == 4 ? 1e-12 : 1e-24) * G[na + j + (size_t)n1 * j]);   // cancellation
-                }
-            if (trouble) {
-                if (pass == 1) { ++n_fallback; return orth(M, W, kc, against, na, kside, coef); }
-                break;   // W is a valid block already: finish with the robust path below
-            }
-            bool shifted = false, ok = cholesky(kc, Gp.data(), 0.0, thr_chol, R);
-            if (!ok) { ok = cholesky(kc, Gp.data(), shift_rel * dmax, 1e-300, R); shifted = ok; }
-            if (!ok) break;
-            upper_inverse(kc, R, Sinv);
-            for (int b = 0; b < kc; ++b) {
-                for (int t = 0; t < na; ++t) {
-                    double v = 0.0;
-                    for (int a = 0; a <= b; ++a) v -= G[t + (size_t)n1 * a] * Sinv[a + (size_t)kc * b];
-                    Mc[t + (size_t)n1 * b] = v;
-                }
-                for (int a = 0; a < kc; ++a) Mc[na + a + (size_t)n1 * b] = Sinv[a + (size_t)kc * b];
-            }
-            apply(M, A, n1, kc, Mc.data());
-            // coefficients: W_in = A·Ctot + W·Btot
-            if (pass == 1) {
-                for (int b = 0; b < kc; ++b)
-                    for (int t = 0; t < na; ++t) Ctot[t + (size_t)na * b] = G[t + (size_t)n1 * b];
-                Btot = R;
-            } else {
-                for (int b = 0; b < kc; ++b)
-                    for (int t = 0; t < na; ++t) {
-                        double v = 0.0;
-                        for (int a = 0; a < kc; ++a) v += G[t + (size_t)n1 * a] * Btot[a + (size_t)kc * b];
-                        Ctot[t + (size_t)na * b] += v;
-                    }
-                std::vector<double> Bn((size_t)kc * kc, 0.0);
-                for (int b = 0; b < kc; ++b)
-                    for (int a = 0; a < kc; ++a) {
-                        double v = 0.0;
-                        for (int t = a; t < kc; ++t) v += R[a + (size_t)kc * t] * Btot[t + (size_t)kc * b];
-                        Bn[a + (size_t)kc * b] = v;
-                    }
-                Btot.swap(Bn);
-            }
-            const bool good = pass >= 2 && !shifted && !prev_shifted && dev <= 0.1;
-            prev_shifted = shifted;
-            if (good) {
-                if (coef)
-                    for (size_t t = 0; t < Ctot.size(); ++t) coef[t] += Ctot[t];
-                ++n_fast;
-                return Btot;
-            }
-        }
-        // not converged in three passes (or a later pass broke down): the robust path finishes
-        // from the current W; compose its coefficients with the ones gathered so far
-        ++n_fallback;
-        std::vector<double> C2((size_t)na * kc, 0.0);
-        std::vector<double> B2 = orth(M, W, kc, against, na, kside, C2.data());
-        if (coef)
-            for (int b = 0; b < kc; ++b)
-                for (int t = 0; t < na; ++t) {
-                    double v = Ctot[t + (size_t)na * b];
-                    for (int a = 0; a < kc; ++a) v += C2[t + (size_t)na * a] * Btot[a + (size_t)kc * b];
-                    coef[t + (size_t)na * b] += v;
-                }
-        std::vector<double> Bn((size_t)kc * kc, 0.0);
-        for (int b = 0; b < kc; ++b)
-            for (int a = 0; a < kc; ++a) {
-                double v = 0.0;
-                for (int t = 0; t < kc; ++t) v += B2[a + (size_t)kc * t] * Btot[t + (size_t)kc * b];
-                Bn[a + (size_t)kc * b] = v;
-            }
-        return Bn;
-    }
-
     // Projection + CholeskyQR2 with two host round trips (the default).  W (M x kc) follows the
     // na orthonormal columns `against` in the same buffer:
     //   1. one Gram [A W]ᵀW gives C = AᵀW and WᵀW; the projected Gram is Gp = WᵀW − CᵀC
@@ -508,10 +367,9 @@ struct Gkl {
     // untouched and the robust `orth` (second projection, shifts, refills, SVQB) takes over.
     // Returns B with W_in = A·coef + W_out·B (coef accumulated, as in `orth`).
     std::vector<double> orth3(int64_t M, T *W, int kc, const T *against, int na, bool kside, double *coef) {
-        static const bool legacy = std::getenv("SSA_ORTH_LEGACY") != nullptr;
         const int64_t ld = LD(M);
-        if (legacy || kc > 64 || na <= 0 || na + kc > 512 || against + (int64_t)na * ld != W)
-            return orth2(M, W, kc, against, na, kside, coef);
+        if (kc > 64 || na <= 0 || na + kc > 512 || against + (int64_t)na * ld != W)
+            return orth(M, W, kc, against, na, kside, coef);
         T *A = const_cast<T *>(against);
         const int n1 = na + kc;
         std::vector<double> G((size_t)n1 * kc), Gp((size_t)kc * kc), R, Sinv, Mc((size_t)n1 * kc);
@@ -519,30 +377,9 @@ struct Gkl {
         const double shift_rel = (sizeof(T) == 4) ? 1e-6 : 1e-13;
         bool project = true, reproject = false;
         for (int pass = 1; pass <= 4; ++pass) {
-            // plain CholeskyQR passes (no projection) of fp32 blocks whose row slices fit in shared
-            // memory run as one cooperative kernel (Gram, factor, apply; cholqr.cu): one launch and
-            // one small read-back instead of Gram + reduction + round trip + upload + update
-            bool shifted = false, fused = false;
+            bool shifted = false;
             double dev = 0.0;
-            if (!project && sizeof(T) == 4 && !(kside && kside_comm())) {
-                const size_t io = sg.take((size_t)kc * kc + 4);
-                const double tf0 = now_ms();
-                if (cholqr_fused(M, reinterpret_cast<float *>(W), ld, kc, shift_rel, thr_chol, p.ws_gram.template as<double>(),
-                                 p.ws_gram.bytes, sg.dev(io), st)) {
-                    SSA_CUDA(cudaMemcpyAsync(sg.h + io, sg.dev(io), sizeof(double) * ((size_t)kc * kc + 4),
-                                             cudaMemcpyDeviceToHost, st));
-                    stream_wait(st);
-                    sg.off = 0;
-                    const double *ho = sg.h + io;
-                    tw_o3_gram[kside] += now_ms() - tf0;
-                    if (ho[(size_t)kc * kc] == 0.0) break;   // factorisation failed, W untouched: robust path
-                    R.assign(ho, ho + (size_t)kc * kc);
-                    shifted = ho[(size_t)kc * kc + 1] != 0.0;
-                    dev = ho[(size_t)kc * kc + 2];
-                    fused = true;
-                }
-            }
-            if (!fused) {
+            {
                 const int nn = project ? n1 : kc;                       // Gram columns: [A W] or W
                 T *Ab = project ? A : W;
                 const double tg0 = now_ms();
@@ -663,26 +500,6 @@ struct Gkl {
         return Bn;
     }
 
-    // W (= the last kc of the n1 columns of A) ← A[:, 0:n1] · Mc (n1 x kc, host).  Large M:
-    // in place, thread per row; small M: out of place into scratch with column groups across
-    // CTAs (enough parallelism), then copied back.
-    DevBuf oop;
-    void apply(int64_t M, T *A, int n1, int kc, const double *Mc) {
-        const size_t idx = sg.take((size_t)n1 * kc);
-        std::memcpy(sg.h + idx, Mc, sizeof(double) * n1 * kc);
-        SSA_CUDA(cudaMemcpyAsync(sg.dev(idx), sg.h + idx, sizeof(double) * n1 * kc, cudaMemcpyHostToDevice, st));
-        const int64_t ld = LD(M);
-        T *W = A + ld * (int64_t)(n1 - kc);
-        if (M >= 32768) {
-            apply_inplace<T>(M, A, ld, n1, kc, sg.dev(idx), nullptr, st);
-        } else {
-            oop.alloc(sizeof(T) * M * kc, st);
-            gemm_cols<T>(M, A, ld, n1, sg.dev(idx), n1, kc, oop.as<T>(), M, st);
-            SSA_CUDA(cudaMemcpy2DAsync(W, sizeof(T) * ld, oop.p, sizeof(T) * M, sizeof(T) * M, kc,
-                                       cudaMemcpyDeviceToDevice, st));
-        }
-    }
-
     // every block product is bracketed by CUDA events on the plan's stream so the
     // device time spent in the trajectory products is reported (ms_products)
     std::vector<cudaEvent_t> ev;
@@ -742,13 +559,7 @@ struct Gkl {
         // X·Qb = Pb·T holds exactly
         std::vector<double> C((size_t)nP * k, 0.0);
         std::vector<double> B;
-        if (!orth_fast(L, W, k, P(0), nP, false, C.data(), B)) {
-            if (use_fast) {   // the fast path touched W: recompute the product
-                product_xv(Q(qc), W, k);
-                std::fill(C.begin(), C.end(), 0.0);
-            }
-            B = orth3(L, W, k, P(0), nP, false, C.data());
-        }
+        B = orth3(L, W, k, P(0), nP, false, C.data());
         tw_orthA += now_ms() - t0;
         for (int b = 0; b < k; ++b)
             for (int a = 0; a < nP; ++a) Tat(a, qc + b) = C[a + (size_t)nP * b];
@@ -784,16 +595,11 @@ struct Gkl {
         recurrence();
         tw_rec += now_ms() - t0;
         t0 = now_ms();
-        const T *againstK = full_k_reorth ? Q(0) : nullptr;
-        const int naK = full_k_reorth ? nQ : 0;
-        std::vector<double> Cdummy((size_t)std::max(naK, 1) * k, 0.0);
-        if (!orth_fast(K, W, k, againstK, naK, true, Cdummy.data(), Alast)) {
-            if (use_fast) {
-                product_xtu(P(pc), W, k);
-                recurrence();
-            }
-            Alast = orth3(K, W, k, againstK, naK, true, nullptr);
-        }
+        // full reorthogonalisation of the K side as well (CGS2 against the whole K basis): the
+        // one-sided variant needed several times more products with thick restarts
+        const T *againstK = Q(0);
+        const int naK = nQ;
+        Alast = orth3(K, W, k, againstK, naK, true, nullptr);
         tw_orthB += now_ms() - t0;
         nQ += k;
     }
@@ -809,25 +615,25 @@ struct Gkl {
             Jd.alloc(sizeof(double) * (2 * mn + (size_t)n * n + n + 80), st);
             double *Ad = Jd.as<double>(), *T0d = Ad + mn, *Wd = T0d + mn, *nrmd = Wd + (size_t)n * n;
             int *dints = reinterpret_cast<int *>(nrmd + n + 8);
-            const size_t ia = sg.take(mn);
+            // upload and read-back through grow-only pinned blocks kept per thread (the staging ring
+            // is too small for the largest projected matrices; pageable buffers cost page faults and
+            // bounce copies on every Ritz step)
+            static thread_local double *upin = nullptr;
+            static thread_local size_t ucap = 0;
+            if (ucap < mn) {
+                if (upin) { stream_wait(st); SSA_CUDA(cudaFreeHost(upin)); }
+                ucap = std::max(mn, 2 * ucap);
+                SSA_CUDA(cudaMallocHost(&upin, sizeof(double) * ucap));
+            }
+            stream_wait(st);   // the previous upload from upin has completed
             for (int j = 0; j < n; ++j)
-                std::memcpy(sg.h + ia + (size_t)m * j, &Tm[(size_t)ldT * j], sizeof(double) * m);
-            SSA_CUDA(cudaMemcpyAsync(Ad, sg.h + ia, sizeof(double) * mn, cudaMemcpyHostToDevice, st));
+                std::memcpy(upin + (size_t)m * j, &Tm[(size_t)ldT * j], sizeof(double) * m);
+            SSA_CUDA(cudaMemcpyAsync(Ad, upin, sizeof(double) * mn, cudaMemcpyHostToDevice, st));
             SSA_CUDA(cudaMemcpyAsync(T0d, Ad, sizeof(double) * mn, cudaMemcpyDeviceToDevice, st));
             // off-diagonal tolerance: fp32 products resolve ~1e-7 relative, so 1e-9 (fp32) / 1e-12
             // (fp64) leaves the Ritz values exact to rounding and saves the last Jacobi sweep(s)
             static const double jtol = [] { const char *e = std::getenv("SSA_JACOBI_TOL"); return e ? std::atof(e) : 0.0; }();
             const double tolj = jtol > 0 ? jtol : (sizeof(T) == 4 ? 1e-9 : 1e-12);
-            if (const char *dump = std::getenv("SSA_DUMP_T")) {   // debug: projected matrices for offline study
-                static int ndump = 0;
-                const std::string fn = std::string(dump) + "_" + std::to_string(ndump++) + ".bin";
-                if (FILE *f = std::fopen(fn.c_str(), "wb")) {
-                    const int32_t hdr[2] = {m, n};
-                    std::fwrite(hdr, sizeof(hdr), 1, f);
-                    std::fwrite(sg.h + ia, sizeof(double), mn, f);
-                    std::fclose(f);
-                }
-            }
             int *dsw = dints + 64;
             cudaEvent_t je0 = nullptr, je1 = nullptr;
             if (debug) {
@@ -897,9 +703,6 @@ struct Gkl {
     void run(int r_, ssa_decomp_info *info) {
         r = r_;
         const int64_t mn = std::min(L, K);
-        // one-sided reorthogonalisation (K side: recurrence term only) is experimental:
-        // with thick restarts it costs many more products, so full reorth is the default
-        full_k_reorth = (K < L) || std::getenv("SSA_ONESIDED") == nullptr;
         k = std::max(1, std::min<int>(p.block_k, 64));
         if (k > mn) k = (int)mn;
         int extra = std::max(k / 2, r);        // keep ~2r Ritz pairs (parameter sweep)
@@ -913,12 +716,6 @@ struct Gkl {
         // (L·K ~ 8e8, products and K-side Grams dominate) at 6
         int mcyc = ((double)L * (double)K >= 1e8) ? 6 : 4;
         if (const char *e = std::getenv("SSA_MCYC")) mcyc = std::max(1, std::atoi(e));
-        // prefer cycles whose projected matrix fits the single-CTA shared-memory Jacobi
-        if (!std::getenv("SSA_MCYC") && std::getenv("SSA_JACOBI_SMEM")) {
-            int m2 = mcyc;
-            while (m2 > 2 && !jacobi_smem_fits(pk + (m2 + 1) * k, pk + m2 * k)) --m2;
-            if (jacobi_smem_fits(pk + (m2 + 1) * k, pk + m2 * k)) mcyc = m2;
-        }
         while (mcyc > 2 && !jacobi_blocked_fits(pk + (mcyc + 1) * k, pk + mcyc * k)) --mcyc;
         nQmax = pk + k * (mcyc + 1);
         ldT = nQmax;
@@ -942,47 +739,52 @@ struct Gkl {
         const double tol = p.tol > 0 ? p.tol : (sizeof(T) == 4 ? 1e-6 : 1e-10);
         const int64_t maxprod = p.max_products > 0 ? p.max_products : std::max<int64_t>(400, 40 * (nQmax / k));
 
-        // P_1 = orth(random)
+        // P_1: a seeded Gaussian block, or — when the plan already holds a decomposition — a warm
+        // start from its eigenvectors (the paper's "decomposition will be automatically continued",
+        // P:869-873): the stored U_1..U_min(r_prev,k) lead the start block, random columns fill it
         fill_normal<T>(L, P(0), ldP, k, p.seed, 0, st);
+        if (p.r > 0 && p.U.p) {
+            const int nw = std::min(p.r, k);
+            SSA_CUDA(cudaMemcpy2DAsync(P(0), sizeof(T) * ldP, p.U.p, sizeof(T) * L, sizeof(T) * L, nw,
+                                       cudaMemcpyDeviceToDevice, st));
+            warm_cols = nw;
+        }
         orth(L, P(0), k, nullptr, 0, false);
         nP = k;
         stepB();
-        std::vector<double> th, Y, Z, res;
+        std::vector<double> th, Y, Z;
         int nconv = 0, restarts = 0;
-        bool checked_once = false;
         double t_block = 0.0, t_ritz = 0.0;   // host wall ms of the last block pair / Ritz step
-        static const bool near_ok = std::getenv("SSA_NO_NEAR_CHECK") == nullptr;
-        // an early check in the first cycle (SSA_FIRST_BLOCKS = blocks before it) is off by default:
-        // with the cost-aware per-block checks below it only cost c2/c3 a Ritz step (measured)
-        int first_blocks = 1 << 20;
-        if (const char *e = std::getenv("SSA_FIRST_BLOCKS")) first_blocks = std::max(1, std::atoi(e));
-        if (first_blocks >= mcyc) checked_once = true;
         double maxres = 0.0;
         for (;;) {
             const double tb0 = now_ms();
             stepA();
             stepB();
             t_block = now_ms() - tb0;
-            // the first cycle checks convergence early (after first_blocks blocks): well-separated
-            // signals converge there without paying for a full cycle (c4)
             const bool cycle_end = !(nQ + k <= nQmax && nblock < maxprod);
-            const bool first_check = (restarts == 0 && !checked_once && nQ >= first_blocks * k + k);
-            // when a block step costs clearly more than a Ritz step (c4, c5: large operators, few
+            // when a block step costs at least as much as a Ritz step (c4, c5: large operators, few
             // blocks to convergence), check after every block once the basis holds r vectors;
-            // cheap blocks (c2, c3) wait for the first early check / the cycle end
-            const double tr_est = t_ritz > 0.0 ? t_ritz : 1.0;
+            // cheap blocks (c2, c3) wait for the cycle end.  With a band partition every rank must
+            // take the same decision (each check is followed by collectives or by none): the
+            // timings are averaged over the ranks first.
+            double tt[2] = {t_block, t_ritz > 0.0 ? t_ritz : 1.0};
+            if (kside_comm()) agree(tt, 2);
             static const double cost_ratio = [] { const char *e = std::getenv("SSA_CHECK_RATIO"); return e ? std::atof(e) : 1.0; }();
-            const bool costly_blocks = near_ok && nQ - k >= r && t_block >= cost_ratio * tr_est;
-            if (!first_check && !cycle_end && !costly_blocks) continue;
-            checked_once = true;
+            const bool costly_blocks = nQ - k >= r && tt[0] >= cost_ratio * tt[1];
+            if (!cycle_end && !costly_blocks) continue;
             // ---- Ritz extraction from T (nP x nc)
             const int nc = nQ - k;
             const double tr = ms_ritz;
             ritz_svd(nP, nc, th, Y, Z);
             t_ritz = ms_ritz - tr;
             anorm = std::max(anorm, th[0]);
+            // residual bound of triple i: ||Xᵀu_i − θ_i v_i|| <= ||A_last·y_i(last block)||
+            // + sqrt(drop2), drop2 = the squared norms of every block column that orthonormalisation
+            // discarded as numerically zero (a refilled column has no A / B entry, so without this
+            // term its part of the residual would be invisible)
             res.assign(nc, 0.0);
             std::vector<double> sv((size_t)k);
+            const double dropn = std::sqrt(drop2);
             for (int i = 0; i < nc; ++i) {
                 // s = Alast · y_i(last block): k independent accumulators, each in the original b order
                 for (int a = 0; a < k; ++a) sv[a] = 0.0;
@@ -992,7 +794,7 @@ struct Gkl {
                 }
                 double s2 = 0.0;
                 for (int a = 0; a < k; ++a) s2 += sv[a] * sv[a];
-                res[i] = std::sqrt(s2);
+                res[i] = std::sqrt(s2) + dropn;
             }
             nconv = 0; maxres = 0.0;
             for (int i = 0; i < std::min(r, nc); ++i) {
@@ -1004,16 +806,17 @@ struct Gkl {
                 for (double v : Alast) an += v * v;
                 for (int b = 0; b < nc; ++b)
                     for (int a = nP - k; a < nP; ++a) bn += Tat(a, b) * Tat(a, b);
-                std::fprintf(stderr, "[ssa] ritz nP=%d nc=%d prod=%lld th0=%.6e th[r-1]=%.6e res0=%.3e resr=%.3e |Alast|=%.3e |Tlast|=%.3e conv=%d\n",
+                std::fprintf(stderr, "[ssa] ritz nP=%d nc=%d prod=%lld th0=%.6e th[r-1]=%.6e res0=%.3e resr=%.3e |Alast|=%.3e |Tlast|=%.3e drop=%.3e conv=%d\n",
                              nP, nc, (long long)nblock, th[0], th[std::min(r, nc) - 1], res[0] / th[0],
-                             res[std::min(r, nc) - 1] / th[0], std::sqrt(an), std::sqrt(bn), nconv);
+                             res[std::min(r, nc) - 1] / th[0], std::sqrt(an), std::sqrt(bn), dropn, nconv);
             }
-            const bool done = (nconv >= r) || (nblock >= maxprod);
+            const bool done = (nconv >= r) || (nblock >= maxprod && nc >= r);
             if (done) {
                 // U = Pb · Y[:, 0:r]
                 p.U.alloc(sizeof(T) * L * r, st);
                 gemm(L, P(0), ldP, nP, Y.data(), nP, r, 1.0, 0.0, p.U.as<T>(), L);
                 p.sigma.assign(th.begin(), th.begin() + r);
+                p.residuals.assign(res.begin(), res.begin() + r);
                 p.r = r;
                 break;
             }
@@ -1066,12 +869,26 @@ struct Gkl {
             info->n_vectors_xv = vec_xv;
             info->n_vectors_xtu = vec_xtu;
             info->ms_ritz = ms_ritz;
+            // reading Q10: triples below the product path's measured σ floor τ·σ_1 are not resolvable
+            // in this arithmetic (their σ and vectors are rounding-level); report how many there are
+            const double tau = sigma_floor(p);
+            info->sigma_floor_rel = tau;
+            info->n_below_floor = 0;
+            for (int i = 0; i < r; ++i) info->n_below_floor += p.sigma[i] < tau * p.sigma[0] ? 1 : 0;
+            info->drop_norm_rel = anorm > 0 ? std::sqrt(drop2) / anorm : 0.0;
+            info->warm_start_cols = warm_cols;
         }
         if (nconv < r)
             throw Error(SSA_ERR_NOT_CONVERGED, "decomposition stopped at max_products with " + std::to_string(nconv) +
                                                    " of " + std::to_string(r) + " triples converged");
     }
 };
+
+// Reading Q10: the σ floor τ = the smallest σ_i/σ_1 down to which the
+// decomposition's σ_i meet the σ bar (relative error <= 1e-4), MEASURED on the noiseless c5 twin
+// against the closed-form spectrum (scripts/measure_tau.py, profiles/r02/tau.json): 8.7e-5 for the
+// fp32 FFT and tensor-core paths at the default tolerance.  fp64 plans resolve to rounding.
+double sigma_floor(const PlanImpl &p) { return p.dt == SSA_F64 ? 1e-12 : 8.7e-5; }
 
 template <typename T>
 void decompose(PlanImpl &p, int r, ssa_decomp_info *info) {

@@ -31,247 +31,11 @@
 
 namespace ssa {
 
-// debug timeline of CTA 0 (SSA_GRAM_TRACE): [role][chunk] globaltimer ns
-__device__ unsigned long long *g_gram_trace = nullptr;
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-// (the pointer is read once per kernel into `tr`: a global load per call sat on the issue path)
-__device__ __forceinline__ void trace(unsigned long long *tr, int role, int i) {
-    if (tr && blockIdx.x == 0 && blockIdx.y == 0 && i < 64 && role < 8) tr[role * 64 + i] = gtimer();
-}
-
 namespace tallg {
 constexpr int R = 32;                 // rows per chunk (128 B per column: one swizzled row)
-constexpr int KS = R / 8;             // UMMA k-steps per chunk
 constexpr int NTHR = 512;            // warps 0 TMA, 1 MMA, 2-7 convert, 8-15 drain
 
-template <int NM, int NN, int BA = 128, int KA = KS>
-struct Cfg {
-    static constexpr int a_bytes = NM * BA * 128;           // raw/hi A tiles (NM x BA rows of 128 B)
-    static constexpr int b_bytes = NN * 128;
-    static constexpr int stage = 2 * a_bytes + 2 * b_bytes; // hi + lo of A and B
-    // as many chunks in flight as fit (the pipeline is latency-bound per chunk)
-    static constexpr int STAGES = (220 * 1024) / stage > 8 ? 8 : (220 * 1024) / stage;
-    static constexpr int off_bar = STAGES * stage;
-    static constexpr int smem = off_bar + 320 + 1024;       // barriers + alignment slack
-    static constexpr int acc_cols = NM * KA * NN;           // one chunk's accumulators (KA per M-tile)
-    static constexpr int ACCB = 512 / acc_cols >= 4 ? 4 : 2; // accumulator buffers (MMA runs ACCB chunks ahead)
-    static constexpr int tmem_cols = ACCB * acc_cols;
-};
 }  // namespace tallg
-
-template <int NM, int NN, int BA, int KA>
-__global__ void __launch_bounds__(tallg::NTHR, 1)
-gram_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
-               int n1, int n2, int self_b, double *__restrict__ partials) {
-    constexpr int boxa = BA;
-    // BA: A columns per TMA box (a multiple of 32, <= 128; rows beyond it in the tile are stale and
-    // only feed discarded accumulator rows); self_b: B is the first n2 columns of A (AᵀA): no B load,
-    // the B operand descriptors point into the A tile
-    using namespace tc;
-    using C = tallg::Cfg<NM, NN, BA, KA>;
-    constexpr int S = C::STAGES, KS = tallg::KS, KG = KS / KA;   // KG k-steps per accumulator
-    static_assert(C::tmem_cols >= 32 && C::tmem_cols <= 512 && (C::tmem_cols & (C::tmem_cols - 1)) == 0,
-                  "TMEM allocation must be a power of two in [32, 512] columns");
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::off_bar);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 32);
-    const uint32_t bar0 = smem_u32(bars);
-    auto full = [&](int s) { return bar0 + 8u * s; };             // TMA landed            [8]
-    auto conv = [&](int s) { return bar0 + 8u * (8 + s); };       // hi/lo split done      [8]
-    auto empty = [&](int s) { return bar0 + 8u * (16 + s); };     // MMAs of the stage done [8]
-    auto accf = [&](int b) { return bar0 + 8u * (24 + b); };      // accumulators ready     [4]
-    auto acce = [&](int b) { return bar0 + 8u * (28 + b); };      // accumulators drained   [4]
-    constexpr int AB = C::ACCB;
-
-    unsigned long long *const tr = g_gram_trace;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t nchunks = (M + tallg::R - 1) / tallg::R;
-    const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
-    const int64_t c0 = (int64_t)blockIdx.x * per;
-    const int nmy = (int)max((int64_t)0, min(per, nchunks - c0));
-    const int col0 = (int)blockIdx.y * NM * 128;                  // first A column of this CTA
-
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(full(s), 1);
-            mbar_init(conv(s), 6);
-            mbar_init(empty(s), 1);
-        }
-        for (int b = 0; b < AB; ++b) {
-            mbar_init(accf(b), 1);
-            mbar_init(acce(b), 8);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "n"(C::tmem_cols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t sm_u = smem_u32(smem);
-    auto a_hi = [&](int s) { return sm_u + (uint32_t)(s * C::stage); };
-    auto a_lo = [&](int s) { return a_hi(s) + C::a_bytes; };
-    auto b_hi = [&](int s) { return a_hi(s) + 2 * C::a_bytes; };
-    auto b_lo = [&](int s) { return b_hi(s) + C::b_bytes; };
-
-    if (warp == 0) {
-        if (lane == 0) {
-            // ---------------- TMA producer ----------------
-            for (int i = 0; i < nmy; ++i) {
-                const int s = i % S;
-                if (i >= S) mbar_wait(empty(s), ((i / S) - 1) & 1);
-                const int r0 = (int)((c0 + i) * tallg::R);
-                mbar_expect_tx(full(s), NM * boxa * 128 + (self_b ? 0 : C::b_bytes));
-#pragma unroll
-                for (int mt = 0; mt < NM; ++mt) tma_load_2d_true(a_hi(s) + mt * 16384, &tmA, r0, col0 + 128 * mt, full(s));
-                if (!self_b) tma_load_2d_true(b_hi(s), &tmB, r0, 0, full(s));
-                trace(tr, 0, i);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer ----------------
-            constexpr uint32_t idesc = make_idesc(128, NN);
-            for (int i = 0; i < nmy; ++i) {
-                const int s = i % S, b = i % AB;
-                mbar_wait(conv(s), (i / S) & 1);
-                if (i >= AB) mbar_wait(acce(b), ((i / AB) - 1) & 1);
-                tc_fence_after();
-                const uint32_t dbase = tmem + (uint32_t)(b * C::acc_cols);
-#pragma unroll
-                for (int kk = 0; kk < KS; ++kk) {
-                    const uint64_t dBh = make_desc((self_b ? a_hi(s) : b_hi(s)) + kk * 32);
-                    const uint64_t dBl = make_desc((self_b ? a_lo(s) : b_lo(s)) + kk * 32);
-#pragma unroll
-                    for (int mt = 0; mt < NM; ++mt) {
-                        const uint32_t d = dbase + (uint32_t)((mt * KA + kk / KG) * NN);
-                        const uint64_t dAh = make_desc(a_hi(s) + mt * 16384 + kk * 32);
-                        const uint64_t dAl = make_desc(a_lo(s) + mt * 16384 + kk * 32);
-                        mma_tf32(d, dAl, dBh, idesc, kk % KG ? 1u : 0u);
-                        mma_tf32(d, dAh, dBl, idesc, 1u);
-                        mma_tf32(d, dAh, dBh, idesc, 1u);
-                    }
-                }
-                mma_commit(empty(s));
-                mma_commit(accf(b));
-                trace(tr, 2, i);
-            }
-        }
-    } else if (warp >= 2 && warp < 8) {
-        // ---------------- converters (warps 2-7): raw -> hi in place, lo alongside ----------------
-        const int ct = tid - 64;
-        for (int i = 0; i < nmy; ++i) {
-            const int s = i % S;
-            mbar_wait(full(s), (i / S) & 1);
-            if (warp == 2 && lane == 0) trace(tr, 4, i);
-            float4 *ah = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage);
-            float4 *al = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + C::a_bytes);
-            float4 *bh = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + 2 * C::a_bytes);
-            float4 *bl = reinterpret_cast<float4 *>(smem + (size_t)s * C::stage + 2 * C::a_bytes + C::b_bytes);
-            // loaded bytes only: NM tiles of boxa rows (+ the B tile unless B aliases A)
-            auto split = [](float4 *src, float4 *dlo) {
-                const float4 x = *src;
-                float4 hh, l;
-                hh.x = __uint_as_float(tf32_rna(x.x)); l.x = x.x - hh.x;
-                hh.y = __uint_as_float(tf32_rna(x.y)); l.y = x.y - hh.y;
-                hh.z = __uint_as_float(tf32_rna(x.z)); l.z = x.z - hh.z;
-                hh.w = __uint_as_float(tf32_rna(x.w)); l.w = x.w - hh.w;
-                *src = hh;
-                *dlo = l;
-            };
-            constexpr int rows4 = boxa * 8;                           // float4 per M-tile
-            constexpr int na4 = NM * rows4, nt4 = na4 + C::b_bytes / 16;
-            const int nt = self_b ? na4 : nt4;
-#pragma unroll 8
-            for (int e = ct; e < nt; e += 192) {
-                const int ea = (e / rows4) * 1024 + (e % rows4);       // M-tile stride 16 KB = 1024 float4
-                if (e < na4) split(ah + ea, al + ea);
-                else split(bh + (e - na4), bl + (e - na4));
-            }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv(s)) : "memory");
-            if (warp == 2 && lane == 0) trace(tr, 1, i);
-        }
-    } else if (warp >= 8) {
-        // ---------------- drain (warps 8-15) ----------------
-        // warp w reads TMEM lanes 32·(w%4).. (A columns) and the 32-column unit h = (w-8)/4 of
-        // the chunk's NM x NN accumulator columns (M-tile h, or columns 32h..).  The 4 k-step
-        // partials are summed in fp32 and folded into a compensated (Kahan) fp32 running sum.
-        constexpr int UNITS = NM * NN / 32;
-        const int h = (warp - 8) >> 2;
-        const int mt_u = (NM == 2) ? h : 0, n0_u = (NM == 2) ? 0 : 32 * h;
-        const bool has_unit = h < UNITS;
-        float ks[32], kc[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) { ks[j] = 0.f; kc[j] = 0.f; }
-        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        for (int i = 0; i < nmy; ++i) {
-            const int b = i % AB;
-            mbar_wait(accf(b), (i / AB) & 1);
-            tc_fence_after();
-            if (has_unit) {
-#pragma unroll
-                for (int hv = 0; hv < 2; ++hv) {
-                    // the KS k-step partials of 16 columns: all loads in flight, one wait
-                    uint32_t r[KA][16];
-#pragma unroll
-                    for (int kk = 0; kk < KA; ++kk)
-                        tmem_ld16_nowait(lane_base + (uint32_t)(b * C::acc_cols + (mt_u * KA + kk) * NN + n0_u + 16 * hv), r[kk]);
-                    tmem_wait_ld();
-                    float sum[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        float t = 0.f;
-#pragma unroll
-                        for (int kk = 0; kk < KA; ++kk) t += __uint_as_float(r[kk][j]);
-                        sum[j] = t;
-                    }
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int q = 16 * hv + j;
-                        const float y = sum[j] - kc[q];
-                        const float t = ks[q] + y;
-                        kc[q] = (t - ks[q]) - y;
-                        ks[q] = t;
-                    }
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
-            if (warp == 8 && lane == 0) trace(tr, 3, i);
-        }
-        // ---- per-CTA partials in gram_reduce's layout: [64-column block][cta][64 x 64]
-        if (has_unit) {
-            const int nparts = gridDim.x;
-            const int a = col0 + 128 * mt_u + (warp & 3) * 32 + lane;
-            if (a < n1) {
-                double *base = partials + ((int64_t)(a / 64) * nparts + blockIdx.x) * 4096 + (a % 64);
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (n0_u + j < n2) base[64 * (n0_u + j)] = (double)ks[j] - (double)kc[j];
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::tmem_cols) : "memory");
-}
 
 // ---------------------------------------------------------------------------
 // Gram v3 (default): A operand in tensor memory.  Thin-N MMAs (N = k <= 64) with both operands in
@@ -313,7 +77,7 @@ struct Cfg {
 template <int NM, int NN, int BA, int RC, int KG>
 __global__ void __launch_bounds__(tallg::NTHR, 1)
 gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
-                int n1, int n2, int self_b, double *__restrict__ partials, int dbg) {
+                int n1, int n2, int self_b, double *__restrict__ partials) {
     using namespace tc;
     using C = tallg3::Cfg<NM, NN, BA, RC, KG>;
     constexpr int KS = C::KS, KA = C::KA, OPB = C::OPB, AB = C::ACCB;
@@ -333,7 +97,6 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int unit = C::a_raw + (self_b ? 0 : C::b_raw);          // raw bytes per sub-chunk
     const int raw_bytes = RC * unit;
     const int RS = min(tallg3::MAXR, C::ring / raw_bytes);
-    unsigned long long *const tr = g_gram_trace;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t nchunks = (M + 32 * RC - 1) / (32 * RC);
     const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
@@ -388,7 +151,6 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         tma_load_2d_true(dst + rc * unit + mt * BA * 128, &tmA, r0, col0 + 128 * mt, full(r));
                     if (!self_b) tma_load_2d_true(dst + rc * unit + C::a_raw, &tmB, r0, 0, full(r));
                 }
-                trace(tr, 0, i);
             }
         }
     } else if (warp == 1) {
@@ -400,10 +162,9 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 mbar_wait(conv(o), (i / OPB) & 1);
                 if (i >= AB) mbar_wait(acce(b), ((i / AB) - 1) & 1);
                 tc_fence_after();
-                trace(tr, 6, i);
                 const uint32_t dbase = tmem + (uint32_t)(b * C::acc_cols);
                 const uint64_t bh0 = make_desc(b_hi(o, 0));
-                if (!(dbg & 2)) {
+                {
                 constexpr uint64_t b_lo_step = (uint64_t)(C::b_raw >> 4), rc_step = (uint64_t)((2 * C::b_raw) >> 4);
 #pragma unroll
                 for (int g = 0; g < KA; ++g) {
@@ -429,7 +190,6 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 mma_commit(ope(o));
                 mma_commit(accf(b));
-                trace(tr, 2, i);
             }
         }
     } else if (warp < 8) {
@@ -446,9 +206,8 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             mbar_wait(full(r), (i / RS) & 1);
             if (i >= OPB) mbar_wait(ope(o), ((i / OPB) - 1) & 1);
             tc_fence_after();
-            if (warp == 4 && lane == 0) trace(tr, 4, i);
             const unsigned char *rawp = smem + C::off_raw + (size_t)r * raw_bytes;
-            if (a_warp && !(dbg & 1)) {
+            if (a_warp) {
 #pragma unroll
                 for (int rc = 0; rc < RC; ++rc) {
 #pragma unroll
@@ -472,9 +231,8 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 tmem_wait_st();
             }
-            if (warp == 4 && lane == 0) trace(tr, 1, i);
 #pragma unroll
-            for (int rc = 0; rc < (dbg & 1 ? 0 : RC); ++rc) {
+            for (int rc = 0; rc < RC; ++rc) {
                 const float4 *src = reinterpret_cast<const float4 *>(rawp + rc * unit + (self_b ? 0 : C::a_raw));
                 float4 *dh = reinterpret_cast<float4 *>(smem + (size_t)o * C::bop + rc * 2 * C::b_raw);
 #pragma unroll 2
@@ -496,8 +254,6 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rawe(r)) : "memory");
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv(o)) : "memory");
             }
-            if (warp == 2 && lane == 0) trace(tr, 5, i);
-            if (warp == 7 && lane == 0) trace(tr, 7, i);
         }
     } else {
         // ---------------- drain (warps 8-15): KA accumulators summed in fp32, Kahan across stages ----------------
@@ -537,7 +293,6 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             tc_fence_before();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
-            if (warp == 8 && lane == 0) trace(tr, 3, i);
         }
         if (has_unit) {
             const int nparts = gridDim.x;
@@ -557,191 +312,6 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 }
 
 // ---------------------------------------------------------------------------
-// Tensor-core update  Out (M x n) = beta·Out + A (M x m)·(alpha·C) (m x n), n <= NN, fp32, Out may equal
-// A (in place: a 128-row tile is written only after all of its chunks were loaded).  The contraction
-// runs over the columns of A, so A is the MN-major operand: one 3-D TMA box {32 rows, 32 columns,
-// 4 row groups} of the column-major A lands as four 32-row groups of 32 swizzled 128-B column rows =
-// the canonical MN-major SW128 layout (LBO 4096 B between row groups, SBO 1024 B between 8-column
-// k-groups).  B_op = (alpha·C)ᵀ chunk, K-major, built in shared memory by the converter warps from
-// the fp64 coefficients (hi / lo tf32).  Per (tile, 32-column chunk): D = A_lo·B_hi + A_hi·B_lo +
-// A_hi·B_hi over 4 k-steps into a fresh TMEM accumulator (≤ 12 truncating accumulations), drained by
-// warps 8-15 into fp32 registers (round to nearest) and written with the tile's last chunk.
-// ---------------------------------------------------------------------------
-namespace tallu {
-constexpr int ROWS = 128, KC = 32, NBUF = 4, NTHR = 512;
-template <int NN>
-struct Cfg {
-    static constexpr int a_bytes = ROWS * KC * 4;            // 16 KB
-    static constexpr int b_bytes = NN * KC * 4;
-    static constexpr int stage = 2 * a_bytes + 2 * b_bytes;
-    static constexpr int STAGES = 4;
-    static constexpr int off_bar = STAGES * stage;
-    static constexpr int smem = off_bar + 256 + 1024;
-    static constexpr int tmem_cols = NBUF * NN <= 256 ? 256 : 512;
-};
-}  // namespace tallu
-
-template <int NN>
-__global__ void __launch_bounds__(tallu::NTHR, 1)
-update_tc_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, const float *__restrict__ Bpk, int n,
-                 double beta, float *Out, int64_t ldo) {
-    using namespace tc;
-    using Cf = tallu::Cfg<NN>;
-    constexpr int S = Cf::STAGES, NBUF = tallu::NBUF, KC = tallu::KC;
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + Cf::off_bar);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 28);
-    const uint32_t bar0 = smem_u32(bars);
-    auto full = [&](int s) { return bar0 + 8u * s; };
-    auto conv = [&](int s) { return bar0 + 8u * (4 + s); };
-    auto empty = [&](int s) { return bar0 + 8u * (8 + s); };
-    auto accf = [&](int b) { return bar0 + 8u * (12 + b); };
-    auto acce = [&](int b) { return bar0 + 8u * (16 + b); };
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int nchk = (m + KC - 1) / KC;
-    const int64_t ntiles = (M + tallu::ROWS - 1) / tallu::ROWS;
-    const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-    const int64_t t0 = (int64_t)blockIdx.x * per;
-    const int64_t mytiles = max((int64_t)0, min(per, ntiles - t0));
-    const int nitems = (int)(mytiles * nchk);
-
-    if (tid == 0) {
-        for (int s = 0; s < 4; ++s) {
-            mbar_init(full(s), 1);
-            mbar_init(conv(s), 6);
-            mbar_init(empty(s), 1);
-            mbar_init(accf(s), 1);
-            mbar_init(acce(s), 8);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "n"(Cf::tmem_cols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t sm_u = smem_u32(smem);
-    auto a_hi = [&](int s) { return sm_u + (uint32_t)(s * Cf::stage); };
-    auto a_lo = [&](int s) { return a_hi(s) + Cf::a_bytes; };
-    auto b_hi = [&](int s) { return a_hi(s) + 2 * Cf::a_bytes; };
-    auto b_lo = [&](int s) { return b_hi(s) + Cf::b_bytes; };
-
-    if (warp == 0) {
-        if (lane == 0) {
-            for (int i = 0; i < nitems; ++i) {
-                const int s = i % S;
-                if (i >= S) mbar_wait(empty(s), ((i / S) - 1) & 1);
-                const int64_t tile = t0 + i / nchk;
-                const int ch = i % nchk;
-                mbar_expect_tx(full(s), Cf::a_bytes + 2 * Cf::b_bytes);
-                tma_load_2d(a_hi(s), &tmA, 0, ch * KC, (int)(tile * (tallu::ROWS / 32)), full(s));
-                bulk_g2s(b_hi(s), Bpk + (size_t)ch * 2 * (Cf::b_bytes / 4), 2 * Cf::b_bytes, full(s));
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc_amn(128, NN);
-            for (int i = 0; i < nitems; ++i) {
-                const int s = i % S, b = i % NBUF;
-                mbar_wait(conv(s), (i / S) & 1);
-                if (i >= NBUF) mbar_wait(acce(b), ((i / NBUF) - 1) & 1);
-                tc_fence_after();
-                const uint32_t d = tmem + (uint32_t)(b * NN);
-#pragma unroll
-                for (int q = 0; q < KC / 8; ++q) {
-                    const uint64_t dAh = make_desc_mn(a_hi(s) + q * 1024, 4096, 512, 1);
-                    const uint64_t dAl = make_desc_mn(a_lo(s) + q * 1024, 4096, 512, 1);
-                    const uint64_t dBh = make_desc(b_hi(s) + q * 32), dBl = make_desc(b_lo(s) + q * 32);
-                    mma_tf32(d, dAl, dBh, idesc, q > 0 ? 1u : 0u);
-                    mma_tf32(d, dAh, dBl, idesc, 1u);
-                    mma_tf32(d, dAh, dBh, idesc, 1u);
-                }
-                mma_commit(empty(s));
-                mma_commit(accf(b));
-            }
-        }
-    } else if (warp >= 2 && warp < 8) {
-        // ---------------- converters (warps 2-7): A raw -> hi in place + lo ----------------
-        const int ct = tid - 64;
-        for (int i = 0; i < nitems; ++i) {
-            const int s = i % S;
-            mbar_wait(full(s), (i / S) & 1);
-            float4 *ah = reinterpret_cast<float4 *>(smem + (size_t)s * Cf::stage);
-            float4 *al = reinterpret_cast<float4 *>(smem + (size_t)s * Cf::stage + Cf::a_bytes);
-#pragma unroll 6
-            for (int e = ct; e < Cf::a_bytes / 16; e += 192) {
-                const float4 x = ah[e];
-                float4 hh, l;
-                hh.x = __uint_as_float(tf32_rna(x.x)); l.x = x.x - hh.x;
-                hh.y = __uint_as_float(tf32_rna(x.y)); l.y = x.y - hh.y;
-                hh.z = __uint_as_float(tf32_rna(x.z)); l.z = x.z - hh.z;
-                hh.w = __uint_as_float(tf32_rna(x.w)); l.w = x.w - hh.w;
-                ah[e] = hh;
-                al[e] = l;
-            }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv(s)) : "memory");
-        }
-    } else if (warp >= 8) {
-        // ---------------- drain + epilogue: warp w: rows 32·(w%4).., output columns 32·((w-8)/4).. ----------------
-        const int h = (warp - 8) >> 2;
-        const bool has = 32 * h < NN;
-        float acc[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(32 * h);
-        const float fb = (float)beta;
-        for (int i = 0; i < nitems; ++i) {
-            const int b = i % NBUF;
-            mbar_wait(accf(b), (i / NBUF) & 1);
-            tc_fence_after();
-            if (has) {
-                float v[32];
-                tmem_ld32(lane_base + (uint32_t)(b * NN), v);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) acc[j] += v[j];
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
-            if (i % nchk == nchk - 1) {
-                const int64_t row = (t0 + i / nchk) * tallu::ROWS + (warp & 3) * 32 + lane;
-                if (has && row < M) {
-                    // all old values first (independent loads in flight), then the stores
-                    float old[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int col = 32 * h + j;
-                        old[j] = (beta != 0.0 && col < n) ? __ldcg(Out + row + ldo * (int64_t)col) : 0.f;
-                    }
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int col = 32 * h + j;
-                        if (col < n) Out[row + ldo * (int64_t)col] = fmaf(fb, old[j], acc[j]);
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cf::tmem_cols) : "memory");
-}
-
-// ---------------------------------------------------------------------------
 // Update v2 (default): Out = beta·Out + A·(alpha·C) with the A operand in tensor memory.  The
 // contraction runs over A's columns, so an A row (one output row) is one TMEM lane: converter
 // warps 4-7 read the landed raw tile [32 columns][128 rows] (plain TMA box, no swizzle: a warp
@@ -750,7 +320,7 @@ update_tc_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, cons
 // pre-split coefficient tiles (B = (alpha·C)ᵀ chunk, K-major SW128 images) are bulk-copied from L2
 // by warp 2 into OPB slots that the MMAs release.  Per (tile, chunk) one fresh accumulator: the
 // small terms A_lo·B_hi, A_hi·B_lo of the 4 k-steps first, then the exact A_hi·B_hi products.
-// Drain / epilogue as in update_tc_kernel (fp32 register sums across chunks, RMW of the tile).
+// Drain / epilogue: fp32 register sums across chunks, read-modify-write of the tile.
 // ---------------------------------------------------------------------------
 namespace tallu2 {
 constexpr int ROWS = 128, KC = 64, OPB = 2, NBUF = 4, MAXR = 12, MAXB = 24, NTHR = 512;   // KC: A columns per item
@@ -769,7 +339,7 @@ struct Cfg {
 template <int NN>
 __global__ void __launch_bounds__(tallu2::NTHR, 1)
 update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, const float *__restrict__ Bpk, int n,
-                  double beta, float *Out, int64_t ldo, int dbg) {
+                  double beta, float *Out, int64_t ldo) {
     using namespace tc;
     using Cf = tallu2::Cfg<NN>;
     constexpr int OPB = tallu2::OPB, NBUF = tallu2::NBUF, KC = tallu2::KC;
@@ -878,7 +448,7 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
                 // B slot = two 32-column chunks [hi | lo] of NN x 32 each; k-step k: chunk k / 4, k % 4 within
                 const uint64_t b0 = make_desc(bslot(q));
                 constexpr uint64_t lo_step = (uint64_t)((NN * 32 * 4) >> 4), ch_step = 2 * lo_step;
-                if (!(dbg & 2)) {
+                {
 #pragma unroll
                 for (int k = 0; k < KC / 8; ++k) {
                     const uint64_t bh = b0 + (uint64_t)(k >> 2) * ch_step + (uint64_t)(2 * (k & 3));
@@ -906,7 +476,7 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
             if (i >= OPB) mbar_wait(ope(o), ((i / OPB) - 1) & 1);
             tc_fence_after();
             const float *src = reinterpret_cast<const float *>(smem + off_raw + (size_t)r * Cf::a_raw) + r_l;
-            if (!(dbg & 1)) {
+            {
 #pragma unroll
             for (int hh = 0; hh < KC / 32; ++hh) {
                 uint32_t hi[32], lo[32];
@@ -982,54 +552,6 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512) : "memory");
 }
 
-// ---- TMA streaming probe (ssa_bench_tall which = 4 / 5): one thread per CTA streams 3-D boxes
-// {32 rows, bc columns, rg row groups} of a column-major M x n block through 8 smem stages, no
-// consumer work — the achievable TMA read rate for the Gram's access pattern.
-__global__ void __launch_bounds__(32, 1) tma_probe_kernel(const __grid_constant__ CUtensorMap tm, int64_t M, int n,
-                                                          int bc, int rg) {
-    using namespace tc;
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int box = bc * 128 * rg;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 8 * box);
-    const uint32_t bar0 = smem_u32(bars);
-    if (threadIdx.x != 0) return;
-    for (int s = 0; s < 8; ++s) mbar_init(bar0 + 8u * s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const int64_t nrg = (M + 31) / 32;
-    const int64_t nchunks = (nrg + rg - 1) / rg;
-    const int ncb = (n + bc - 1) / bc;
-    const int64_t items = nchunks * ncb;
-    const int64_t per = (items + gridDim.x - 1) / gridDim.x;
-    const int64_t i0 = blockIdx.x * per, i1 = min(items, i0 + per);
-    for (int64_t i = i0; i < i1; ++i) {
-        const int s = (int)((i - i0) % 8);
-        if (i - i0 >= 8) mbar_wait(bar0 + 8u * s, (uint32_t)((((i - i0) / 8) - 1) & 1));
-        mbar_expect_tx(bar0 + 8u * s, box);
-        const int64_t ch = i / ncb;
-        const int cb = (int)(i % ncb);
-        tma_load_2d(smem_u32(smem) + s * box, &tm, 0, cb * bc, (int)(ch * rg), bar0 + 8u * s);
-    }
-    for (int64_t i = max(i0, i1 - 8); i < i1; ++i) {
-        const int s = (int)((i - i0) % 8);
-        mbar_wait(bar0 + 8u * s, (uint32_t)(((i - i0) / 8) & 1));
-    }
-}
-
-void tma_probe(const float *A, int64_t M, int n, int64_t ld, int bc, int rg, cudaStream_t st) {
-    static std::map<std::tuple<const float *, int64_t, int, int>, CUtensorMap> cache;
-    auto key = std::make_tuple(A, M, bc, rg);
-    auto it = cache.find(key);
-    if (it == cache.end())
-        it = cache.emplace(key, make_map3(A, 32, (uint64_t)n, (uint64_t)((M + 31) / 32), (uint64_t)ld * 4, 128, 32,
-                                          (uint32_t)bc, (uint32_t)rg, true)).first;
-    const int smem = 8 * bc * 128 * rg + 128 + 1024;
-    set_max_smem(tma_probe_kernel);
-    tma_probe_kernel<<<num_sms(), 32, smem, st>>>(it->second, M, n, bc, rg);
-    after_launch("tma_probe");
-}
-
 // tensor maps cached per (pointer, rows, columns, ld, box columns)
 static const CUtensorMap &tall_map(const float *base, int64_t M, int ncols, int64_t ld, int boxc) {
     using Key = std::tuple<const float *, int64_t, int, int64_t, int>;
@@ -1038,23 +560,8 @@ static const CUtensorMap &tall_map(const float *base, int64_t M, int ncols, int6
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     if (cache.size() > 256) cache.clear();
-    static const bool p256 = [] { const char *e = std::getenv("SSA_L2P"); return !e || std::atoi(e) == 256; }();
     return cache[key] = make_map2(base, (uint64_t)M, (uint64_t)ncols, (uint64_t)ld * 4, tallg::R, (uint32_t)boxc, true,
-                                  p256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
-}
-
-template <int NM, int NN, int BA, int KA>
-static void launch_gram_tc_ka(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2,
-                              double *partials, int ctas, cudaStream_t st) {
-    using C = tallg::Cfg<NM, NN, BA, KA>;
-    const int self_b = (B == A && ldb == lda && n2 <= n1 && NN <= BA && NM == 1) ? 1 : 0;
-    const CUtensorMap &ma = tall_map(A, M, n1, lda, BA);
-    const CUtensorMap &mb = tall_map(B, M, n2, ldb, NN);
-    auto kern = gram_tc_kernel<NM, NN, BA, KA>;
-    set_max_smem(kern);
-    const int gy = (int)cdiv(n1, NM * 128);
-    kern<<<dim3(ctas, gy), tallg::NTHR, C::smem, st>>>(ma, mb, M, n1, n2, self_b, partials);
-    after_launch("gram_tc");
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
 }
 
 template <int NM, int NN, int BA, int RC, int KG>
@@ -1066,27 +573,16 @@ static void launch_gram_tc3(int64_t M, const float *A, int64_t lda, int n1, cons
     auto kern = gram_tc3_kernel<NM, NN, BA, RC, KG>;
     set_max_smem(kern);
     const int gy = (int)cdiv(n1, NM * 128);
-    static const int dbg = [] { const char *e = std::getenv("SSA_GRAM_DBG"); return e ? std::atoi(e) : 0; }();
-    kern<<<dim3(ctas, gy), tallg::NTHR, tallg3::SMEM, st>>>(ma, mb, M, n1, n2, self_b, partials, dbg);
+    kern<<<dim3(ctas, gy), tallg::NTHR, tallg3::SMEM, st>>>(ma, mb, M, n1, n2, self_b, partials);
     after_launch("gram_tc3");
 }
 
 template <int NM, int NN, int BA>
 static void launch_gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2,
                            double *partials, int ctas, cudaStream_t st) {
-    static const int ver = [] { const char *e = std::getenv("SSA_GRAM_V"); return e ? std::atoi(e) : 3; }();
-    if (ver == 3) {
-        // RC = 2 (64-row stages) where the TMEM A buffers allow it; KG = 4 k-steps per accumulator
-        static const int rc = [] { const char *e = std::getenv("SSA_GRAM_RC"); return e ? std::atoi(e) : 2; }();
-        if constexpr (NM == 1) {
-            if (rc == 2) launch_gram_tc3<NM, NN, BA, 2, 4>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
-            else launch_gram_tc3<NM, NN, BA, 1, 2>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
-        } else {
-            launch_gram_tc3<NM, NN, BA, 1, 2>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
-        }
-        return;
-    }
-    launch_gram_tc_ka<NM, NN, BA, 4>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+    // RC = 2 (64-row stages) where the TMEM A buffers allow it; KG = 4 k-steps per accumulator
+    if constexpr (NM == 1) launch_gram_tc3<NM, NN, BA, 2, 4>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+    else launch_gram_tc3<NM, NN, BA, 1, 2>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
 }
 
 // B tiles of all 32-column chunks, packed once per update as the exact shared-memory images
@@ -1103,23 +599,6 @@ __global__ void coef_pack_kernel(int m, const double *__restrict__ C, int ldc, i
         hi[off] = hv;
         lo[off] = v - hv;
     }
-}
-
-template <int NN>
-static void launch_update_tc(const CUtensorMap &ma, int64_t M, int m, const double *C, int ldc, int n, double alpha,
-                             double beta, float *Out, int64_t ldo, cudaStream_t st) {
-    using Cf = tallu::Cfg<NN>;
-    const int nchk = (m + 31) / 32;
-    static thread_local DevBuf bpk;
-    const size_t need = sizeof(float) * (size_t)nchk * 2 * NN * 32;
-    if (bpk.bytes < need) bpk.alloc(need, st);
-    coef_pack_kernel<NN><<<nchk, 256, 0, st>>>(m, C, ldc, n, alpha, bpk.as<float>());
-    after_launch("coef_pack");
-    auto kern = update_tc_kernel<NN>;
-    set_max_smem(kern);
-    const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallu::ROWS));
-    kern<<<ctas, tallu::NTHR, Cf::smem, st>>>(ma, M, m, bpk.as<float>(), n, beta, Out, ldo);
-    after_launch("update_tc");
 }
 
 template <int NN>
@@ -1143,8 +622,7 @@ static void launch_update_tc2(const float *A, int64_t lda, int64_t M, int m, con
     auto kern = update_tc2_kernel<NN>;
     set_max_smem(kern);
     const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallu2::ROWS));
-    static const int dbg = [] { const char *e = std::getenv("SSA_UPD_DBG"); return e ? std::atoi(e) : 0; }();
-    kern<<<ctas, tallu2::NTHR, tallu2::SMEM, st>>>(it->second, M, m, bpk.as<float>(), n, beta, Out, ldo, dbg);
+    kern<<<ctas, tallu2::NTHR, tallu2::SMEM, st>>>(it->second, M, m, bpk.as<float>(), n, beta, Out, ldo);
     after_launch("update_tc2");
 }
 
@@ -1159,24 +637,8 @@ bool update_tc(int64_t M, const float *A, int64_t lda, int m, const double *C, i
     if (!mode || M < 8192 || n > 64 || m > 4096 || (mode == 1 && m < 64) || (lda & 31) || lda < (M + 31) / 32 * 32 ||
         ((uintptr_t)A & 127))
         return false;
-    static const int ver = [] { const char *e = std::getenv("SSA_UPD_V"); return e ? std::atoi(e) : 2; }();
-    if (ver == 2) {
-        if (n <= 32) launch_update_tc2<32>(A, lda, M, m, C, ldc, n, alpha, beta, Out, ldo, st);
-        else launch_update_tc2<64>(A, lda, M, m, C, ldc, n, alpha, beta, Out, ldo, st);
-        return true;
-    }
-    using Key = std::tuple<const float *, int64_t, int, int64_t>;
-    static thread_local std::map<Key, CUtensorMap> cache;
-    const Key key{A, M, m, lda};
-    auto it = cache.find(key);
-    if (it == cache.end()) {
-        if (cache.size() > 256) cache.clear();
-        it = cache.emplace(key, make_map3(A, 32, (uint64_t)m, (uint64_t)((M + 31) / 32), (uint64_t)lda * 4, 128, 32,
-                                          32, 4, false, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B)).first;
-    }
-    if (n <= 32) launch_update_tc<32>(it->second, M, m, C, ldc, n, alpha, beta, Out, ldo, st);
-    else launch_update_tc<64>(it->second, M, m, C, ldc, n, alpha, beta, Out, ldo, st);
+    if (n <= 32) launch_update_tc2<32>(A, lda, M, m, C, ldc, n, alpha, beta, Out, ldo, st);
+    else launch_update_tc2<64>(A, lda, M, m, C, ldc, n, alpha, beta, Out, ldo, st);
     return true;
 }
 
@@ -1189,37 +651,18 @@ bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int
         return false;
     const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallg::R));
     if ((size_t)ctas * 4096 * sizeof(double) * (size_t)cdiv(n1, 64) > partial_bytes) return false;
-    static unsigned long long *trace_buf = nullptr;
-    if (std::getenv("SSA_GRAM_TRACE") && !trace_buf) {
-        SSA_CUDA(cudaMalloc(&trace_buf, 8 * 64 * 8));
-        SSA_CUDA(cudaMemset(trace_buf, 0, 8 * 64 * 8));
-        SSA_CUDA(cudaMemcpyToSymbol(g_gram_trace, &trace_buf, sizeof(trace_buf)));
-    }
-    static const bool nm2 = [] { const char *e = std::getenv("SSA_GRAM_NM2"); return !e || std::atoi(e) != 0; }();
     // narrow blocks (n1 <= 64, e.g. the CholeskyQR Gram WᵀW): a 64-column A box, B read from the A tile
     if (n2 <= 32) {
         if (n1 <= 64) launch_gram_tc<1, 32, 64>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
         // two M-tiles per CTA (B read once per 256 columns) up to 256 columns; above that a second
         // nearly empty y-block made it slower than 128-column CTAs (n1 = 288: 136 vs 107 µs)
-        else if (n1 <= 128 || n1 > 256 || !nm2) launch_gram_tc<1, 32, 128>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
+        else if (n1 <= 128 || n1 > 256) launch_gram_tc<1, 32, 128>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
         else launch_gram_tc<2, 32, 128>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
     } else {
         if (n1 <= 64) launch_gram_tc<1, 64, 64>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
         else launch_gram_tc<1, 64, 128>(M, A, lda, n1, B, ldb, n2, partials, ctas, st);
     }
     gram_reduce(partials, ctas, n1, n2, G, st);
-    if (trace_buf) {
-        unsigned long long h[8 * 64];
-        SSA_CUDA(cudaStreamSynchronize(st));
-        SSA_CUDA(cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost));
-        std::fprintf(stderr, "[gram trace] M=%lld n1=%d n2=%d (us from first TMA): chunk tma wait convA convB2 convB3 mma0 mma drain\n",
-                     (long long)M, n1, n2);
-        auto us = [&](int k) { return h[k] ? (double)(h[k] - h[0]) * 1e-3 : -1.0; };
-        for (int i = 0; i < 12; ++i)
-            std::fprintf(stderr, "  %2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", i, us(i), us(4 * 64 + i), us(64 + i),
-                         us(5 * 64 + i), us(7 * 64 + i), us(6 * 64 + i), us(128 + i), us(192 + i));
-        std::fprintf(stderr, "  last(42): tma %.2f drain %.2f\n", (h[42] - h[0]) * 1e-3, (h[192 + 42] - h[0]) * 1e-3);
-    }
     return true;
 }
 

@@ -1,11 +1,14 @@
-"""Multi-GPU plumbing for the window-position (𝔎) band partition (SURVEY §8(e), row a12).
+"""Multi-GPU plumbing for the window-position (𝔎) band partition (SURVEY §8(e), rows a12 / (e)).
 
 Each rank owns a contiguous band of origin columns κ_y ∈ [y0, y1) (reading Q13: bands along
-the slow axis of the x-fastest layout).  Xᵀ·U is local to the band; the L x k partials of X·V
-and the k x k K-side Grams are summed across ranks through the `ssa_comm.allreduce_sum`
-callback that the C library calls (stream-ordered, in place).  This module provides the band
-bounds and a torch.distributed implementation of that callback (NCCL on GPUs; the same code
-path works on host buffers with gloo, which is what the CPU tests exercise).
+the slow axis of the x-fastest layout) and holds only the image columns [y0, y1 + Ly − 1) — its
+band plus the (Ly−1)-column halo — so its FFT grid, spectrum and K-side basis are those of the
+sub-image.  Xᵀ·U is local to the band; the L x k partials of X·V and the k x k K-side Grams are
+summed across ranks through the `ssa_comm.allreduce_sum` callback that the C library calls
+(stream-ordered, in place); the reconstruction sums the bands' diagonal-averaging numerators and
+hit counts (the halos overlap) and divides once.  This module provides the band bounds, the
+sub-image slicing and a torch.distributed implementation of that callback (NCCL on GPUs; the same
+code path works on host buffers with gloo, which is what the CPU tests exercise).
 """
 from __future__ import annotations
 
@@ -26,6 +29,24 @@ def band_bounds(ky: int, world: int, rank: int) -> tuple[int, int]:
 def halo_columns(y0: int, y1: int, ly: int) -> tuple[int, int]:
     """Image columns a band needs: [y0, y1 + ly - 1) (the (Ly-1)-column halo)."""
     return y0, y1 + ly - 1
+
+
+def band_slices(ny: int, ly: int, world: int, rank: int):
+    """(y0, y1) origin band and the image columns [c0, c1) = [y0, y1 + ly − 1) of this rank."""
+    y0, y1 = band_bounds(ny - ly + 1, world, rank)
+    c0, c1 = halo_columns(y0, y1, ly)
+    return (y0, y1), (c0, c1)
+
+
+def band_plan(x, window, comm, mask=None, **kw):
+    """The plan of this rank's band: the sub-image x[:, y0 : y1 + Ly − 1] (and mask), with the
+    communicator and the band's global position."""
+    from .api import Plan
+    ny = x.shape[1]
+    (y0, y1), (c0, c1) = band_slices(ny, int(window[1]), comm.world, comm.rank)
+    sub = x[:, c0:c1]
+    msk = None if mask is None else mask[:, c0:c1]
+    return Plan(sub, window, mask=msk, comm=comm, band=(y0, y1), ny_global=ny, **kw)
 
 
 _DTYPES = {0: "float32", 1: "float64"}

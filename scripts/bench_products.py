@@ -15,7 +15,7 @@ from paper_1309_5050_b200 import Plan
 cfg = sys.argv[1]
 paths = (sys.argv[2] if len(sys.argv) > 2 else "tc,fft").split(",")
 w = synth.get(cfg)
-k = int(sys.argv[3]) if len(sys.argv) > 3 else w.block_k
+k = int(sys.argv[3]) if len(sys.argv) > 3 and int(sys.argv[3]) > 0 else w.block_k
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 20
 td = torch.float64 if w.dtype == "f64" else torch.float32
 for path in paths:

@@ -15,7 +15,8 @@ import pytest
 
 import oracle
 import synth
-from test_gpu_parity import FP32_PROD_TOL, FP64_PROD_TOL, check_sigma, relfro
+from parity_util import TAU, check_sigma
+from test_gpu_parity import FP32_PROD_TOL, FP64_PROD_TOL, relfro
 
 pytestmark = pytest.mark.gpu
 
@@ -65,7 +66,7 @@ def test_ssa_1d_as_n_by_1(path, dtype):
     sh = _check_products(p, x, (60, 1), dtype)
     s_or, U_or, V_or, s_all = oracle.svd_dense(x, sh, 7)
     p.decompose(6)
-    check_sigma(p.sigma, s_all, 6)
+    check_sigma(p.sigma, s_all, 6, TAU[path] if dtype == "f32" else TAU["f64"])
     recs = p.reconstruct([[0, 1, 2, 3, 4, 5]], add_rest=True)
     np.testing.assert_allclose(recs[0] + recs[1], x, rtol=0, atol=(1e-4 if dtype == "f32" else 1e-10) * np.abs(x).max())
 
@@ -83,7 +84,7 @@ def test_mssa_unequal_lengths_nan_padded(path):
     assert sh.K == (500 - 99) + (450 - 99) + (380 - 99)
     s_or, U_or, V_or, s_all = oracle.svd_dense(np.nan_to_num(x), sh, 6)
     p.decompose(5)
-    check_sigma(p.sigma, s_all, 5)
+    check_sigma(p.sigma, s_all, 5, TAU[path])
     rec = p.reconstruct([[0, 1, 2, 3, 4]])[0]
     # values exist only on 𝔑′: NaN exactly where the input is NaN here
     assert np.array_equal(np.isnan(rec), ~np.isfinite(x))

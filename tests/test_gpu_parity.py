@@ -12,6 +12,7 @@ import pytest
 import closed_form as cf
 import oracle
 import synth
+from parity_util import TAU, check_sigma, gap_groups
 
 pytestmark = pytest.mark.gpu
 
@@ -42,8 +43,7 @@ def _oracle_input(w, dtype):
     return x
 
 
-def relfro(a, b):
-    return np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b)
+from parity_util import relfro  # noqa: E402
 
 
 def _cases():
@@ -212,46 +212,6 @@ def test_products_closed_form_c5_twin_sampled():
 
 
 # ---------------------------------------------------------------- decomposition + reconstruction
-def _relgaps(s_all, r):
-    s = np.asarray(s_all, np.float64)
-    g = np.full(r, np.inf)
-    for i in range(r):
-        left = s[i - 1] - s[i] if i > 0 else np.inf
-        right = s[i] - s[i + 1] if i + 1 < len(s) else np.inf
-        g[i] = min(left, right) / s[i] if s[i] > 0 else 0.0
-    return g
-
-
-def check_sigma(s_gpu, s_or_all, r, tau=1e-5, rel=1e-4):
-    s_gpu = np.asarray(s_gpu, np.float64)
-    s_or = np.asarray(s_or_all[:r], np.float64)
-    gaps = _relgaps(s_or_all, r)
-    s1 = s_or[0]
-    checked = 0
-    for i in range(r):
-        if gaps[i] >= 1e-3 and s_or[i] >= tau * s1:
-            assert abs(s_gpu[i] - s_or[i]) <= rel * s_or[i], (i, s_gpu[i], s_or[i])
-            checked += 1
-        else:
-            assert abs(s_gpu[i] - s_or[i]) <= 1e-6 * s1 * 10, (i, s_gpu[i], s_or[i])
-    return checked
-
-
-def _gap_groups(s_all, r, thr=1e-3):
-    """Reading Q9: clusters bounded by relative gaps >= thr."""
-    s = np.asarray(s_all, np.float64)
-    groups, cur = [], [0]
-    for i in range(1, r + 1):
-        if i == r or (s[i - 1] - s[i]) / s[i - 1] >= thr:
-            if i == r and (s[r - 1] - s[r]) / s[r - 1] < thr:
-                break
-            groups.append(cur)
-            cur = [i]
-        else:
-            cur.append(i)
-    return groups
-
-
 def _check_recon(p, x, sh, s_or, U_or, V_or, groups, tol=1e-4):
     recs = p.reconstruct(groups)
     ref = oracle.reconstruct(x, sh, s_or, U_or, V_or, groups)
@@ -270,7 +230,7 @@ def test_decompose_c1_fp64(path):
     s_or, U_or, V_or, s_all = oracle.svd_dense(x, sh, 10)
     info = p.decompose(10)
     assert info["n_converged"] == 10
-    assert check_sigma(p.sigma, s_all, 10) >= 6
+    assert len(check_sigma(p.sigma, s_all, 10, TAU["f64"])) >= 6
     np.testing.assert_allclose(p.sigma, s_or, rtol=1e-8)
     _check_recon(p, x, sh, s_or, U_or, V_or, w.groups + [list(range(6))], tol=1e-8)
     # the residual group returns the image (eq. P:440-443)
@@ -286,7 +246,7 @@ def test_decompose_c2_mssa_fp32(path):
     sh = oracle.shapes(x, w.window)
     s_or, U_or, V_or, s_all = oracle.svd_dense(x, sh, 17)
     p.decompose(16)
-    assert check_sigma(p.sigma, s_all, 16) >= 4
+    assert len(check_sigma(p.sigma, s_all, 16, TAU[path])) >= 4
     _check_recon(p, x, sh, s_or, U_or, V_or, [g for g in w.groups if max(g) < 6])
 
 
@@ -300,8 +260,8 @@ def test_decompose_shaped_small(name, path):
     r = w.r
     s_or, U_or, V_or, s_all = oracle.svd_dense(x, sh, r + 1)
     p.decompose(r)
-    check_sigma(p.sigma, s_all, r)
-    groups = _gap_groups(s_all, r)
+    check_sigma(p.sigma, s_all, r, TAU[path])
+    groups = gap_groups(s_all, r)
     if groups:
         _check_recon(p, x, sh, s_or, U_or, V_or, groups)
 
@@ -345,26 +305,41 @@ def test_c5_noiseless_closed_form_sigma():
     noiseless twin against the closed form, with reading Q10's floor for fp32 products."""
     w = synth.config5(noise=False)
     p = _plan(w, path="fft")
-    p.decompose(50, allow_not_converged=True)
+    info = p.decompose(50)
+    assert info["n_converged"] == 50
     s = p.sigma
     s_cf = np.concatenate([cf.sigma_rect(w.terms, 256, 256, 3841, 3841), np.zeros(8)])
     assert cf.rank(w.terms) == 48
-    checked = check_sigma(s, s_cf, 50, tau=1e-5)
-    assert checked >= 8
+    checked = check_sigma(s, s_cf, 50, TAU["fft"])
+    assert len(checked) >= 8
+    # reading Q10: the library reports the same floor and how many triples lie below it
+    assert info["sigma_floor_rel"] == TAU["fft"]
+    assert info["n_below_floor"] == int(np.sum(s < TAU["fft"] * s[0]))
 
 
-def test_wcor_diag_and_symmetry():
-    w = synth.config1()
-    p = _plan(w)
-    p.decompose(10)
-    R = p.wcor([[0], [1], [2], [3], [4, 5]])
+@pytest.mark.parametrize("case", ["c1", "shaped"])
+def test_wcor_and_contributions(case):
+    """Row f1: the w-correlation matrix and the contributions ||X̃_g||²_w / ||X||²_w
+     of the device reconstructions against the oracle's (pinned by the trajectory
+    inner-product identity, tests/test_oracle_pins.py)."""
+    if case == "c1":
+        w, dt, groups = synth.config1(), "f64", [[0], [1], [2], [3], [4, 5], list(range(10))]
+    else:
+        w, dt = synth.small_shaped(seed=23, wmask_drop=3), "f32"
+        groups = [[0], [1, 2], [3, 4, 5], list(range(6))]
+    p = _plan(w, dtype=dt)
+    x = _oracle_input(w, dt)
+    sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
+    r = max(max(g) for g in groups) + 1
+    p.decompose(r)
+    R, con = p.wcor(groups, contributions=True)
     np.testing.assert_allclose(np.diag(R), 1.0, rtol=1e-12)
     np.testing.assert_allclose(R, R.T, atol=1e-12)
-    x = _oracle_input(w, "f64")
-    sh = oracle.shapes(x, w.window)
-    s_or, U_or, V_or, _ = oracle.svd_dense(x, sh, 10)
-    Ro = oracle.wcorr(sh, oracle.reconstruct(x, sh, s_or, U_or, V_or, [[0], [1], [2], [3], [4, 5]]))
-    np.testing.assert_allclose(np.abs(R), np.abs(Ro), atol=1e-8)
+    # the oracle on the device's own triples isolates the w-correlation / contribution arithmetic
+    recs = oracle.reconstruct(x, sh, p.sigma, p.U().astype(np.float64), p.V().astype(np.float64), groups)
+    tol = 1e-9 if dt == "f64" else 2e-5
+    np.testing.assert_allclose(R, oracle.wcorr(sh, recs), atol=tol)
+    np.testing.assert_allclose(con, oracle.contributions(sh, recs, x), rtol=tol, atol=tol)
 
 
 # ---------------------------------------------------------------- error behaviour
@@ -389,36 +364,98 @@ def test_errors():
         p.decompose(21)
     assert e.value.status == 4
     p.decompose(3)
+    # a group index beyond the computed rank continues the decomposition ...
+    p.reconstruct([[0, 3]])
+    assert p.r == 4
+    # ... up to min(L, K) (here L = 20)
     with pytest.raises(SSAError) as e:
-        p.reconstruct([[0, 3]])
+        p.reconstruct([[0, 20]])
     assert e.value.status == 4
 
 
-# ---------------------------------------------------------------- band partition (row a12) on one GPU
+# ---------------------------------------------------------------- band partition (rows a12, (e)) on one GPU
 @pytest.mark.parametrize("path", ["direct", "fft", "tc"])
 def test_band_products_and_decomposition(path):
-    """The multi-GPU band plan on one GPU with an identity all-reduce: X·V is the
-    band's partial sum and Xᵀ·U the band-local product (both against the oracle on the band's
-    𝔎), and the decomposition is the SVD of the band operator X[:, κ ∈ band]."""
-    from paper_1309_5050_b200.dist import LocalComm, band_bounds
+    """The multi-GPU band plan on one GPU with an identity all-reduce: a rank's plan is
+    its sub-image (band + (Ly−1)-column halo); its X·V is the band's partial sum, its Xᵀ·U the band's
+    rows, and the decomposition is the SVD of the band operator X[:, κ ∈ band].  The two bands'
+    partials add up to the global X·V and their Xᵀ·U rows stack to the global one."""
+    from paper_1309_5050_b200.dist import LocalComm, band_plan, band_slices
     w = synth.small_shaped(seed=51, nx=700, ny=10, window=(300, 3), n_holes=2) if path == "tc" else \
         synth.small_shaped(seed=52, nx=40, ny=33, window=(7, 5), wmask_drop=3)
     x = _oracle_input(w, "f32")
     sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
-    y0, y1 = band_bounds(sh.ky, 2, 1)
-    band = oracle.Shapes(sh.nx, sh.ny, sh.lx, sh.ly, sh.nmask, sh.wmask, sh.kmask.copy(order="F"), sh.weights)
-    band.kmask[:, :y0] = 0
-    band.kmask[:, y1:] = 0
-    from paper_1309_5050_b200 import Plan
-    p = Plan(w.data, w.window, mask=w.mask, wmask=w.wmask, dtype="f32", path=path, block_k=8,
-             comm=LocalComm(1, 2), band=(y0, y1))
-    kb = int(band.kmask.sum())
-    assert p.K == kb
     rng = np.random.default_rng(8)
-    V = rng.normal(size=(kb, 5)).astype(np.float32).astype(np.float64)
     U = rng.normal(size=(sh.L, 5)).astype(np.float32).astype(np.float64)
-    assert relfro(p.matmul(V), oracle.xv(x, band, V)) <= FP32_PROD_TOL
-    assert relfro(p.matmul(U, transpose=True), oracle.xtu(x, band, U)) <= FP32_PROD_TOL
-    s_or, _, _, s_all = oracle.svd_dense(x, band, 5)
-    p.decompose(4)
-    check_sigma(p.sigma, s_all, 4)
+    Vfull = rng.normal(size=(sh.K, 5)).astype(np.float32).astype(np.float64)
+    xv_sum, xtu_rows, koff = np.zeros((sh.L, 5)), [], 0
+    for rank in range(2):
+        (y0, y1), (c0, c1) = band_slices(sh.ny, sh.ly, 2, rank)
+        band = oracle.Shapes(sh.nx, sh.ny, sh.lx, sh.ly, sh.nmask, sh.wmask, sh.kmask.copy(order="F"), sh.weights)
+        band.kmask[:, :y0] = 0
+        band.kmask[:, y1:] = 0
+        p = band_plan(w.data, w.window, LocalComm(rank, 2), mask=w.mask, wmask=w.wmask, dtype="f32", path=path,
+                      block_k=8)
+        kb = int(band.kmask.sum())
+        assert p.K == kb and p.ny == c1 - c0
+        V = Vfull[koff:koff + kb]
+        Ub = p.matmul(V)
+        assert relfro(Ub, oracle.xv(x, band, V)) <= FP32_PROD_TOL
+        xv_sum += Ub
+        Vb = p.matmul(U, transpose=True)
+        assert relfro(Vb, oracle.xtu(x, band, U)) <= FP32_PROD_TOL
+        xtu_rows.append(Vb)
+        koff += kb
+        if rank == 0:
+            s_or, _, _, s_all = oracle.svd_dense(x, band, 5)
+            p.decompose(4)
+            check_sigma(p.sigma, s_all, 4, TAU[path])
+    assert koff == sh.K
+    assert relfro(xv_sum, oracle.xv(x, sh, Vfull)) <= FP32_PROD_TOL
+    assert relfro(np.concatenate(xtu_rows), oracle.xtu(x, sh, U)) <= FP32_PROD_TOL
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_band_partition_two_threads_end_to_end(world):
+    """The whole band-partitioned path on one GPU: `world` host threads, each with its band plan
+    (sub-image only) and a thread communicator whose all-reduce really sums the ranks' buffers.
+    The decomposition (X·V partials and K-side Grams summed across the bands) gives the σ of the
+    global operator, and the assembled reconstructions (bands' numerators and hit counts summed
+    over the halos), the rest group, the w-correlations and the contributions equal the global
+    ones — all against the oracle."""
+    import torch
+    from threadcomm import ThreadComm, ThreadGroup, run_threads
+    from paper_1309_5050_b200.dist import band_plan
+    w = synth.small_shaped(seed=53, nx=48, ny=41, window=(8, 6), n_holes=3, wmask_drop=4)
+    x = _oracle_input(w, "f32")
+    sh = oracle.shapes(x, w.window, mask=w.mask, wmask=w.wmask)
+    s_or, U_or, V_or, s_all = oracle.svd_dense(x, sh, 9)
+    groups = gap_groups(s_all, 6)
+    assert groups
+    grp = ThreadGroup(world)
+
+    def rank_fn(r):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            comm = ThreadComm(grp, r)
+            p = band_plan(w.data, w.window, comm, mask=w.mask, wmask=w.wmask, dtype="f32", path="fft", block_k=8,
+                          stream=st.cuda_stream)
+            info = p.decompose(6)
+            recs = p.reconstruct(groups, add_rest=True)
+            R, con = p.wcor(groups, contributions=True)
+            return p.sigma, info, recs, R, con, comm.calls
+
+    res = run_threads(world, rank_fn)
+    for sig, info, recs, R, con, calls in res:
+        assert calls > 0 and info["n_converged"] == 6
+        np.testing.assert_array_equal(sig, res[0][0])     # identical on every rank
+        check_sigma(sig, s_all, 6, TAU["fft"])
+        ref = oracle.reconstruct(x, sh, s_or, U_or, V_or, groups, add_rest=True)
+        for a, b in zip(recs, ref):
+            assert a.shape == (sh.nx, sh.ny)
+            assert np.array_equal(np.isnan(a), np.isnan(b))
+            m = ~np.isnan(b)
+            assert relfro(a[m], b[m]) <= 1e-4
+        ro = oracle.reconstruct(x, sh, s_or, U_or, V_or, groups)
+        np.testing.assert_allclose(R, oracle.wcorr(sh, ro), atol=1e-4)
+        np.testing.assert_allclose(con, oracle.contributions(sh, ro, x), rtol=1e-4)

@@ -62,11 +62,9 @@ print(worst)
 """
 
 
-@pytest.mark.parametrize("env", [{"SSA_GRAM_V": "1", "SSA_UPD_V": "1"}, {"SSA_GRAM_RC": "1"},
-                                 {"SSA_UPD_TC": "2"}])
+@pytest.mark.parametrize("env", [{"SSA_UPD_TC": "2"}])
 def test_kernel_variants_match_fp64(lib, env):
-    """The env-selected variants (v1 Gram / update with both operands in shared memory, 32-row Gram stages,
-    tensor-core update for narrow m) stay correct: the switches are read once per process, so each runs in
+    """The env-selected variant (tensor-core update for narrow m) stays correct: the switches are read once per process, so each runs in
     a subprocess."""
     import os
     import subprocess

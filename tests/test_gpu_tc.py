@@ -10,7 +10,8 @@ import pytest
 
 import oracle
 import synth
-from test_gpu_parity import FP32_PROD_TOL, _check_recon, _oracle_input, check_sigma, relfro
+from parity_util import TAU, check_sigma
+from test_gpu_parity import FP32_PROD_TOL, _check_recon, _oracle_input, relfro
 
 pytestmark = pytest.mark.gpu
 
@@ -96,7 +97,7 @@ def test_tc_decompose_c2():
     sh = oracle.shapes(x, w.window)
     s_or, U_or, V_or, s_all = oracle.svd_dense(x, sh, 17)
     p.decompose(16)
-    assert check_sigma(p.sigma, s_all, 16) >= 4
+    assert len(check_sigma(p.sigma, s_all, 16, TAU["tc"])) >= 4
     _check_recon(p, x, sh, s_or, U_or, V_or, [g for g in w.groups if max(g) < 6])
 
 

@@ -90,6 +90,17 @@ def test_weights_rectangle_and_sum():
     assert sh.weights.sum() == sh.L * sh.K
 
 
+@pytest.mark.parametrize("dims", [(7, 5, 3, 2), (20, 9, 20, 1), (16, 16, 5, 16), (31, 12, 9, 4)])
+def test_shapes_rect_equals_brute_force(dims):
+    """oracle.shapes_rect (closed form for full rectangles, used at the c5 size) against the
+    brute-force 𝔎 / 𝕎 of oracle.shapes."""
+    nx, ny, lx, ly = dims
+    a = oracle.shapes_rect(nx, ny, lx, ly)
+    b = oracle.shapes(np.zeros((nx, ny)), (lx, ly))
+    assert np.array_equal(a.kmask, b.kmask) and np.array_equal(a.weights, b.weights)
+    assert np.array_equal(a.nmask, b.nmask) and np.array_equal(a.wmask, b.wmask)
+
+
 def test_weights_sum_shaped():
     w = synth.small_shaped(seed=3, wmask_drop=4)
     sh = oracle.shapes(w.data, w.window, mask=w.mask, wmask=w.wmask)
@@ -279,6 +290,46 @@ def test_completeness_and_norm_identity():
     R = oracle.wcorr(sh, recs[:5])
     np.testing.assert_allclose(np.diag(R), 1.0, rtol=1e-12)
     np.testing.assert_allclose(R, R.T, atol=1e-12)
+
+
+def test_wcorr_equals_trajectory_inner_products():
+    """Pin of oracle.wcorr by the identity it rests on, (Y, Z)_w = ⟨𝒯(Y), 𝒯(Z)⟩_F:
+    the weighted inner product of two arrays equals the Frobenius inner product of their
+    (independently pinned) trajectory matrices, so dropping the weights w_n, summing outside 𝔑′
+    or using the wrong normalisation fails here.  Arbitrary arrays (not only reconstructions),
+    shaped 𝔑 and a non-rectangular window."""
+    rng = np.random.default_rng(21)
+    w = synth.small_shaped(seed=6, nx=23, ny=19, window=(6, 4), wmask_drop=3)
+    sh = oracle.shapes(w.data, w.window, mask=w.mask, wmask=w.wmask)
+    ys = []
+    for _ in range(4):
+        y = rng.normal(size=(sh.nx, sh.ny))
+        y[~sh.nprime] = np.nan          # reconstructions exist only on 𝔑′ (P:3214-3217)
+        ys.append(y)
+    R = oracle.wcorr(sh, ys)
+    T = [oracle.trajmat(np.nan_to_num(y), sh) for y in ys]
+    G = np.array([[np.sum(a * b) for b in T] for a in T])
+    np.testing.assert_allclose(R, G / np.sqrt(np.outer(np.diag(G), np.diag(G))), rtol=1e-12, atol=1e-13)
+    # and the unnormalised form: (Y, Z)_w = Σ_n w_n y_n z_n = ⟨𝒯(Y), 𝒯(Z)⟩_F
+    y0, y1 = (np.nan_to_num(y) for y in ys[:2])
+    np.testing.assert_allclose(np.sum(sh.weights * y0 * y1), G[0, 1], rtol=1e-12)
+
+
+def test_contributions_pins():
+    """Contributions ||X̃_j||²_w / ||X||²_w: the group of all components reconstructs 𝕏
+    on 𝔑′ and contributes exactly 1; each contribution equals ||𝒯(X̃_j)||²_F / ||𝒯(𝕏)||²_F (the
+    weighted norm is the trajectory norm, via the independently pinned trajmat)."""
+    w = synth.small_shaped(seed=7, nx=21, ny=18, window=(5, 4), wmask_drop=2)
+    sh = oracle.shapes(w.data, w.window, mask=w.mask, wmask=w.wmask)
+    s, U, V, sall = oracle.svd_dense(w.data, sh, min(sh.L, sh.K))
+    d = int(np.sum(sall > 1e-13 * sall[0]))
+    groups = [[0], [1, 2], list(range(3, d)), list(range(d))]
+    recs = oracle.reconstruct(w.data, sh, s, U, V, groups)
+    c = oracle.contributions(sh, recs, w.data)
+    assert abs(c[-1] - 1.0) <= 1e-12
+    tx = np.sum(oracle.trajmat(np.nan_to_num(w.data), sh) ** 2)
+    for g, r in enumerate(recs):
+        np.testing.assert_allclose(c[g], np.sum(oracle.trajmat(np.nan_to_num(r), sh) ** 2) / tx, rtol=1e-11)
 
 
 def test_averaging_returns_rank_one_image_exactly():
