@@ -414,41 +414,55 @@ def oracle_products_per_s(w, budget_s=15.0):
 
 
 def run_sharded(args, rank, world, dist):
-    """--shard: ONE decomposition of the config split over the ranks (strong scaling):
-    rank r owns the window positions κ_y ∈ [r·ky/N, (r+1)·ky/N) (a band plan, halo rows implied by the
-    full image every rank holds); X·V partials and K-side Grams are summed with an NCCL all-reduce
-    through the library's communicator hook (dist.TorchComm).  Reconstruction of a band plan is left
-    to the caller, so a step is plan + decompose.  Not measured at N > 1 in this round (one GPU per
-    gpurun call); at N = 1 it is the full problem without a communicator."""
+    """N > 1 (default) or --shard: ONE decomposition of the config split over the ranks (strong
+    scaling).  Rank r holds only its sub-image, the global columns [y0, y1 + Ly − 1)
+    of its origin band κ_y ∈ [y0, y1) plus the (Ly−1)-column halo (dist.band_plan): its own FFT grid,
+    spectrum and K-side basis.  X·V partials and K-side Grams are summed with an NCCL all-reduce
+    through the library's communicator hook (dist.TorchComm); the reconstruction sums the bands'
+    numerators and hit counts (one all-reduce per group) and returns the global image on every rank.
+    A step = plan + decompose + reconstruct; time = max over ranks; value = the vector products of
+    the ONE decomposition per second (not summed over ranks)."""
     import torch
-    from paper_1309_5050_b200 import Plan, launch_count
-    from paper_1309_5050_b200.dist import TorchComm
+    from paper_1309_5050_b200 import launch_count
+    from paper_1309_5050_b200.dist import TorchComm, band_plan, band_slices
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    w = workload(args.config, seed_offset=0)          # the same problem on every rank
+    w = workload(args.config, seed_offset=0)          # the same global problem on every rank
+    groups = groups_for(w)
     stream = torch.cuda.Stream(device=dev)
     dt_torch = torch.float64 if w.dtype == "f64" else torch.float32
-    img_dev = torch.as_tensor(np.asarray(w.data), dtype=dt_torch, device=dev)
-    mask_np = None if w.mask is None else np.asarray(w.mask)
-    ny = np.asarray(w.data).shape[1]
-    ky = ny - w.window[1] + 1
-    band = (rank * ky // world, (rank + 1) * ky // world)
+    xg = np.asarray(w.data)
+    ny = xg.shape[1]
+    (y0, y1), (c0, c1) = band_slices(ny, w.window[1], max(world, 1), rank)
+    # this rank's data only: its sub-image (device for the timed steps, pinned host for e2e)
+    sub_dev = torch.as_tensor(np.ascontiguousarray(xg[:, c0:c1]), dtype=dt_torch, device=dev)
+    sub_pin = torch.empty((c1 - c0, xg.shape[0]), dtype=dt_torch, pin_memory=True)
+    sub_pin.copy_(torch.as_tensor(np.ascontiguousarray(xg[:, c0:c1].T), dtype=dt_torch))
+    mask = None if w.mask is None else np.asarray(w.mask)
     comm = TorchComm(device="cuda") if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out_pin = torch.empty((len(groups), ny, xg.shape[0]), dtype=dt_torch, pin_memory=True)
 
     def step(host=False):
         with torch.cuda.stream(stream):
-            src = np.asarray(w.data) if host else img_dev
-            kw = dict(comm=comm, band=band) if comm is not None else {}
-            p = Plan(src, w.window, mask=mask_np, wmask=w.wmask, dtype=w.dtype, block_k=w.block_k,
-                     path=args.path, stream=stream.cuda_stream, **kw)
+            src = sub_pin.t() if host else sub_dev
+            kw = dict(dtype=w.dtype, block_k=w.block_k, path=args.path, stream=stream.cuda_stream, wmask=w.wmask)
+            if comm is not None:
+                from paper_1309_5050_b200.api import Plan
+                msk = None if mask is None else mask[:, c0:c1]
+                p = Plan(src, w.window, mask=msk, comm=comm, band=(y0, y1), ny_global=ny, **kw)
+            else:
+                from paper_1309_5050_b200.api import Plan
+                p = Plan(src, w.window, mask=mask, **kw)
             info = p.decompose(w.r, allow_not_converged=True)
+            recs = (p.reconstruct(groups, device=False, out=out_pin.numpy()) if host
+                    else p.reconstruct(groups, device=True))
             sig = np.array(p.sigma)
             p.close()
-        return info, sig
+        return info, sig, recs
 
     for _ in range(args.warmup):
-        info, _ = step()
+        info, _, _ = step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -462,14 +476,14 @@ def run_sharded(args, rank, world, dist):
                 dist.barrier()
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            info, sig = step()
+            info, sig, _ = step()
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
     launches = launch_count(reset=True)
     ms = float(np.sum(times))
     if dist:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
     e2e = []
@@ -477,10 +491,15 @@ def run_sharded(args, rank, world, dist):
         flush.fill_(1); torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         step(host=True)
-        torch.cuda.synchronize()
-        e2e.append((time.perf_counter() - t0) * 1e3)
+        e1.record(stream)
+        e1.synchronize()
+        t_e = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+        if dist:
+            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e2e.append(float(t_e[0]))
     nvec = float(info["n_vector_products"])               # one decomposition: not summed over ranks
     esz = 8 if w.dtype == "f64" else 4
     res = {"metric": "trajectory products/s", "value": nvec / (ms / args.steps / 1e3), "unit": "vector products/s",
@@ -488,12 +507,18 @@ def run_sharded(args, rank, world, dist):
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": w.dtype,
            "data": "synthetic (seeded BASELINE.json generator)",
            "config": {"workload": w.name, "window": list(w.window), "r": w.r, "block_k": w.block_k,
-                      "parallelism": f"bands{world} (window positions along y, NCCL all-reduce)",
-                      "band_of_rank0": list(band), "l2": "flushed (256 MB write) between timed steps"},
+                      "groups": len(groups),
+                      "parallelism": f"bands{world}: origin columns split over ranks, each rank holds its "
+                                     f"sub-image (band + {w.window[1] - 1}-column halo); NCCL all-reduce of "
+                                     f"X·V partials, K-side Grams and reconstruction numerators",
+                      "band_of_rank0": list(band_slices(ny, w.window[1], max(world, 1), 0)[0]),
+                      "l2": "flushed (256 MB write) between timed steps"},
            "e2e": {"value": nvec / (np.mean(e2e) / 1e3), "unit": "vector products/s",
-                   "h2d_bytes_per_step": int(np.asarray(w.data).size * esz), "d2h_bytes_per_step": 8 * w.r},
+                   "h2d_bytes_per_step": int(xg.shape[0] * (c1 - c0) * esz),
+                   "d2h_bytes_per_step": int(len(groups) * xg.size * esz), "ms_per_step": float(np.mean(e2e))},
            "gpu_launches": int(launches), "clocks": clk.summary(), "sigma_head": [float(x) for x in sig[:4]],
-           "decomposition": {k2: info[k2] for k2 in ("n_block_products", "n_restarts", "n_converged")}}
+           "decomposition": {k2: info[k2] for k2 in ("n_block_products", "n_restarts", "n_converged",
+                                                      "max_rel_residual")}}
     return res, w
 
 
@@ -518,7 +543,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--shard", action="store_true",
-                    help="one decomposition split over the ranks by window-position bands (strong scaling)")
+                    help="one decomposition split over the ranks by window-position bands (strong scaling; "
+                         "the default when N > 1)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas (weak scaling) instead of the band partition")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -555,9 +583,10 @@ def main():
         import torch.distributed as tdist
         tdist.init_process_group("nccl")
         dist = tdist
-    res, w = (run_sharded if args.shard else run_ours)(args, rank, world, dist)
+    sharded = args.shard or (world > 1 and not args.replicas)
+    res, w = (run_sharded if sharded else run_ours)(args, rank, world, dist)
     if rank == 0:
-        if not args.no_cpu_baseline and world == 1 and not args.shard:
+        if not args.no_cpu_baseline and world == 1 and not sharded:
             v, cores, sample = oracle_products_per_s(w, budget_s=args.cpu_budget)
             res["cpu_baseline"] = {"value": v, "unit": "vector products/s", "cores": cores, "kind": "oracle",
                                    "sample": sample, "cpu": cpu_model()}

@@ -211,6 +211,24 @@ ssa_status ssa_reconstruct(ssa_plan p, const int32_t *grp_off, const int32_t *gr
 ssa_status ssa_wcor(ssa_plan p, const int32_t *grp_off, const int32_t *grp_idx,
                     int32_t n_groups, double *rho, double *contrib);
 
+/* Parameter estimation: LS-ESPRIT / 2D-ESPRIT on the
+ * eigenvectors U_i, i ∈ idx[0..n) (n <= 64, indices < the computed rank): shift matrices Φ_x, Φ_y
+ * (least squares between the eigenarrays restricted to 𝔏 and to 𝔏 shifted by one cell along x / y)
+ * and their joint diagonalisation.  lambda, mu: n complex values each (re, im interleaved: 2n
+ * doubles), the pairs (λ_k, μ_k) of x_{m,n} = Σ_k c_k λ_k^m μ_k^n; mu may be NULL; for a window of one
+ * column mu = 1.  The order of the pairs is unspecified. */
+ssa_status ssa_esprit(ssa_plan p, const int32_t *idx, int32_t n, double *lambda, double *mu);
+
+/* Vector forecast (Alg. 7 fast column vector forecast, of the vector
+ * MSSA forecast P:1416-1460): 1-D SSA / MSSA plans (window (L, 1), series = columns, NaN-padded at
+ * the end).  For every series p the reconstruction of the group idx (eigenvectors P = U_idx, lagged
+ * vectors W_k = (σ_i V_i[κ_k])) is continued by W_k = D W_{k−1}, D = the LS-ESPRIT shift matrix,
+ * and hankelized: out (ld_out >= nx + M, one column per series, plan dtype) receives z_1 .. z_{N_p+M}
+ * (the reconstruction updated near the end, then M forecast values) and NaN below.  SSA_ERR_ARG for
+ * other plans, band plans, or series whose window positions are not a contiguous prefix. */
+ssa_status ssa_forecast(ssa_plan p, const int32_t *idx, int32_t n, int32_t M, void *out, int64_t ld_out,
+                        int on_device);
+
 /* The solver's projected-matrix SVD as a utility: one-sided
  * block Jacobi in fp64 on the device (one thread-block cluster for n <= 256, a
  * cooperative grid above), for m >= n, m <= 768.  A (host, m x n column-major)

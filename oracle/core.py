@@ -301,6 +301,87 @@ def contributions(sh: Shapes, recs, img):
     return np.array([np.sum(w * np.nan_to_num(r) ** 2) for r in recs]) / den
 
 
+def _shift_pairs(wmask, axis):
+    """Row pairs (a, b) of the 𝔏-lex basis with cell b = cell a shifted by one along `axis`
+    (0 = x, 1 = y), both cells in 𝔏 (the shifted sub-arrays of the eigenarrays)."""
+    wm = np.asarray(wmask, dtype=bool)
+    lx, ly = wm.shape
+    idx = -np.ones((lx, ly), dtype=np.int64)
+    iy, ix = np.nonzero(wm.T)
+    idx[ix, iy] = np.arange(len(ix))
+    a, b = [], []
+    for x in range(lx):
+        for y in range(ly):
+            x2, y2 = (x + 1, y) if axis == 0 else (x, y + 1)
+            if x2 < lx and y2 < ly and idx[x, y] >= 0 and idx[x2, y2] >= 0:
+                a.append(idx[x, y]); b.append(idx[x2, y2])
+    return np.array(a, dtype=np.int64), np.array(b, dtype=np.int64)
+
+
+def esprit(sh: Shapes, U, comb=0.6180339887 + 0.3090169944j):
+    """LS-ESPRIT / 2D-ESPRIT parameter estimation on the eigenvectors U (L x r) of a group
+    (P:675-682 LS-ESPRIT after Roy & Kailath; P:2843-2857 2D-ESPRIT after Rouquette & Najim):
+    the shift matrices Φ_x = (U_x↑)^† U_x↓ and Φ_y = (U_y↑)^† U_y↓ solve the least-squares problems
+    U_x↑ Φ_x ≈ U_x↓ between the eigenarrays restricted to 𝔏 and to 𝔏 shifted by one along x (y);
+    their joint diagonalisation (eigenvectors T of a generic combination Φ_x + c·Φ_y) gives the pairs
+    λ_k = (T⁻¹Φ_xT)_kk, μ_k = (T⁻¹Φ_yT)_kk with x_{m,n} = Σ_k c_k λ_k^m μ_k^n.  For a window of one
+    column (1-D SSA / MSSA) only λ is defined (μ = 1)."""
+    U = np.asarray(U, dtype=np.float64)
+    a, b = _shift_pairs(sh.wmask, 0)
+    phx = np.linalg.lstsq(U[a], U[b], rcond=None)[0]
+    if sh.ly == 1:
+        lam = np.linalg.eigvals(phx)
+        return lam, np.ones_like(lam)
+    a, b = _shift_pairs(sh.wmask, 1)
+    phy = np.linalg.lstsq(U[a], U[b], rcond=None)[0]
+    _, T = np.linalg.eig(phx + comb * phy)
+    Ti = np.linalg.inv(T)
+    return np.diag(Ti @ phx @ T), np.diag(Ti @ phy @ T)
+
+
+def vector_forecast(img, sh: Shapes, sigma, U, V, group, M):
+    """Column vector forecast of 1-D SSA / MSSA (window (L, 1); series = columns of the 2-D packing)
+    by its definition: with P = [U_j, j ∈ group], π = its last row, ν² = ||π||²,
+    Π = the orthogonal projector onto span of the first L−1 rows of P and R_L = Σ_j π_j P_j[:-1]/(1−ν²)
+    (eq. P:1376), every series p continues its reconstructed lagged vectors X̂_1..X̂_{K_p} by
+    Z_j = (Π Z_{j−1}[1:]; R_Lᵀ Z_{j−1}[1:]) for j = K_p+1 .. K_p+M+L−1 (eq. P:1442-1460); the diagonal
+    averaging of [Z_1 : ... : Z_{K_p+M+L−1}] gives z_1..z_{N_p+M+L−1}, of which z_1..z_{N_p+M}
+    (reconstruction updated near the end, then the M forecast values) are returned, one column per
+    series, NaN-padded to max_p N_p + M."""
+    assert sh.ly == 1, "vector forecast: 1-D SSA / MSSA packing (window (L, 1))"
+    g = list(group)
+    P = np.asarray(U, dtype=np.float64)[:, g]
+    Vg = np.asarray(V, dtype=np.float64)[:, g] * np.asarray(sigma, dtype=np.float64)[g][None, :]
+    L = P.shape[0]
+    pi = P[-1, :]
+    nu2 = float(pi @ pi)
+    Pl = P[:-1, :]
+    Pi = Pl @ np.linalg.pinv(Pl)                      # projector onto span(first L−1 rows)
+    R = (Pl @ pi) / (1.0 - nu2)
+    kx, ky = sh.kx, sh.ky
+    kmask = np.asarray(sh.kmask, dtype=bool)
+    Kp = kmask.sum(axis=0)
+    out = np.full((int(Kp.max()) + L - 1 + M, ky), np.nan)
+    koff = np.concatenate([[0], np.cumsum(Kp)])
+    for p in range(ky):
+        K = int(Kp[p])
+        if K == 0:
+            continue
+        Z = [P @ Vg[koff[p] + j] for j in range(K)]    # X̂_j = Σ_i σ_i U_i V_i[κ_j]
+        for _ in range(M + L - 1):
+            f = Z[-1][1:]
+            Z.append(np.concatenate([Pi @ f, [R @ f]]))
+        Zm = np.array(Z).T                               # L x (K + M + L − 1)
+        n = L + Zm.shape[1] - 1
+        num = np.zeros(n); cnt = np.zeros(n)
+        for c in range(Zm.shape[1]):
+            num[c:c + L] += Zm[:, c]
+            cnt[c:c + L] += 1
+        N = K + L - 1
+        out[:N + M, p] = (num / cnt)[:N + M]
+    return out
+
+
 def wcorr(sh: Shapes, recs):
     """w-correlation matrix of reconstructed components:
     ρ_ij = (X̃_i, X̃_j)_w / (‖X̃_i‖_w ‖X̃_j‖_w), (Y, Z)_w = Σ_n w_n y_n z_n."""

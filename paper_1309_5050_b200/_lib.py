@@ -62,7 +62,7 @@ class ssa_decomp_info(C.Structure):
 EXPORTS = ["ssa_plan_create", "ssa_plan_destroy", "ssa_plan_info", "ssa_get_weights", "ssa_get_kmask",
            "ssa_matmul", "ssa_decompose", "ssa_get_rank", "ssa_get_sigma", "ssa_get_residuals", "ssa_get_u", "ssa_get_v",
            "ssa_set_triples", "ssa_reconstruct", "ssa_wcor", "ssa_last_error", "ssa_version",
-           "ssa_launch_count", "ssa_small_svd", "ssa_bench_tall", "ssa_bench_mma"]
+           "ssa_launch_count", "ssa_small_svd", "ssa_bench_tall", "ssa_bench_mma", "ssa_esprit", "ssa_forecast"]
 
 _lib = None
 
@@ -109,6 +109,8 @@ def load(path: str = SO_PATH):
     L.ssa_bench_tall.restype = st
     L.ssa_bench_mma.argtypes = [i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.ssa_bench_mma.restype = st
+    L.ssa_esprit.argtypes = [p, p, i32, p, p]; L.ssa_esprit.restype = st
+    L.ssa_forecast.argtypes = [p, p, i32, i32, p, i64, C.c_int]; L.ssa_forecast.restype = st
     _lib = L
     return L
 

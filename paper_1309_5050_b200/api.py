@@ -269,6 +269,23 @@ class Plan:
         return (rho, con) if contributions else rho
 
 
+    # ------------------------------------------------------------ parameters / forecast (rows f2, f3)
+    def esprit(self, idx):
+        """LS-ESPRIT / 2D-ESPRIT pairs (λ_k, μ_k) of the eigentriples idx."""
+        ii = np.ascontiguousarray(list(idx), dtype=np.int32)
+        lam = np.zeros(2 * len(ii)); mu = np.zeros(2 * len(ii))
+        lib.check(self._L.ssa_esprit(self._h, ii.ctypes.data, len(ii), lam.ctypes.data, mu.ctypes.data))
+        return lam[0::2] + 1j * lam[1::2], mu[0::2] + 1j * mu[1::2]
+
+    def forecast(self, idx, M):
+        """Vector forecast (Alg. 7) of the group idx, M steps: an (nx + M, s) array, series
+        p holding z_1 .. z_{N_p + M} (updated reconstruction, then the forecast) and NaN below."""
+        ii = np.ascontiguousarray(list(idx), dtype=np.int32)
+        out = np.zeros((self.ny, self.nx + M), dtype=self._np_dtype)
+        lib.check(self._L.ssa_forecast(self._h, ii.ctypes.data, len(ii), int(M), out.ctypes.data, self.nx + M, 0))
+        return out.T
+
+
 def version() -> str:
     return lib.load().ssa_version().decode()
 

@@ -499,6 +499,10 @@ static void get_v(PlanImpl &p, const std::vector<int> *need = nullptr) {
     if (std::all_of(p.v_have.begin(), p.v_have.end(), [](char c) { return c != 0; })) p.v_valid = true;
 }
 
+template <typename T> void get_v_cols(PlanImpl &p, const std::vector<int> &need) { get_v<T>(p, &need); }
+template void get_v_cols<float>(PlanImpl &, const std::vector<int> &);
+template void get_v_cols<double>(PlanImpl &, const std::vector<int> &);
+
 template <typename T>
 static void reconstruct_impl(PlanImpl &p, const int32_t *off, const int32_t *idx, int ng, int add_rest, T *out_dev,
                              const int32_t *wdiv = nullptr) {
@@ -604,6 +608,13 @@ using namespace ssa;
 struct ssa_plan_s {
     PlanImpl impl;
 };
+
+namespace ssa {
+PlanImpl &ssa_plan_impl(ssa_plan p) {
+    if (p->impl.broken) throw Error(SSA_ERR_CUDA, "plan is in a failed state (earlier CUDA/comm error); destroy it");
+    return p->impl;
+}
+}  // namespace ssa
 
 #define SSA_API_BEGIN try {
 #define SSA_API_END                                                          \

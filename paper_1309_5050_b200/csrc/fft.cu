@@ -214,7 +214,7 @@ template <typename T, int MAXT>
 __global__ void __launch_bounds__(MAXT, sizeof(T) == 4 ? (MAXT <= 256 ? 6 : 3) : (MAXT <= 256 ? 4 : 2))
 fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, int bx, int by, int jsel_n,
            const int *__restrict__ jsel, const double *__restrict__ scale, int lgx, int CB, cplx<T> *__restrict__ A,
-           const cplx<T> *__restrict__ tw, int lgtw) {
+           int lda, const cplx<T> *__restrict__ tw, int lgtw) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int Mx = 1 << lgx, Hx = Mx / 2 + 1;
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
@@ -258,7 +258,7 @@ fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, in
         const cplx<T> z = res[sp(t * Mx + fx)], zm = res[sp(t * Mx + ((Mx - fx) & (Mx - 1)))];
         const cplx<T> out = (c & 1) ? cplx<T>{(z.y + zm.y) * T(0.5), (zm.x - z.x) * T(0.5)}
                                     : cplx<T>{(z.x + zm.x) * T(0.5), (z.y - zm.y) * T(0.5)};
-        A[((int64_t)jo * Hx + fx) * by + col0 + c] = out;
+        A[((int64_t)jo * Hx + fx) * lda + col0 + c] = out;
     }
 }
 
@@ -270,8 +270,8 @@ fft_pass_a(const T *__restrict__ in, int64_t ld, const int *__restrict__ map, in
 // ---------------------------------------------------------------------------
 template <typename T, int MAXT>
 __global__ void __launch_bounds__(MAXT, sizeof(T) == 4 ? (MAXT <= 256 ? 6 : 3) : (MAXT <= 256 ? 4 : 2))
-fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, const cplx<T> *__restrict__ Xh,
-           int mode, cplx<T> *__restrict__ B, int ny_out, const cplx<T> *__restrict__ tw, int lgtw) {
+fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int lda, int Hx, int lgy, int RB, const cplx<T> *__restrict__ Xh,
+           int mode, cplx<T> *__restrict__ B, int ny_out, int ldb, const cplx<T> *__restrict__ tw, int lgtw) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int My = 1 << lgy;
     cplx<T> *b0 = reinterpret_cast<cplx<T> *>(smem_raw);
@@ -303,7 +303,7 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
     for (int idx = threadIdx.x; idx < RB * My; idx += blockDim.x) {
         const int rr = idx >> lgy, y = idx & (My - 1);
         cplx<T> v{T(0), T(0)};
-        if (rr < nrow && y < ny_in) v = A[((int64_t)j * Hx + fx0 + rr) * ny_in + y];
+        if (rr < nrow && y < ny_in) v = A[((int64_t)j * Hx + fx0 + rr) * lda + y];
         b0[sp(idx)] = v;
     }
     __syncthreads();
@@ -326,16 +326,16 @@ fft_pass_b(const cplx<T> *__restrict__ A, int ny_in, int Hx, int lgy, int RB, co
     #pragma unroll 8
     for (int idx = threadIdx.x; idx < RB * ny_out; idx += blockDim.x) {
         const int rr = idx / ny_out, y = idx - rr * ny_out;
-        if (rr < nrow) B[((int64_t)j * Hx + fx0 + rr) * ny_out + y] = out[sp(rr * My + y)];
+        if (rr < nrow) B[((int64_t)j * Hx + fx0 + rr) * ldb + y] = out[sp(rr * My + y)];
     }
 }
 
 // Pass B (averaging): per (g, fx): Σ_{i∈I_g} DFT_y(AU_i row) ⊙ DFT_y(AV_i row), inverse, keep ny rows.
 template <typename T, int MAXT>
 __global__ void __launch_bounds__(MAXT, sizeof(T) == 4 ? (MAXT <= 256 ? 6 : 3) : (MAXT <= 256 ? 4 : 2))
-fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restrict__ AV, int ky, const int *grp_off,
-                const int *grp_idx, const int *slot, int Hx, int lgy, int RB, cplx<T> *__restrict__ B, int ny_out,
-                const cplx<T> *__restrict__ tw, int lgtw) {
+fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, int ldu, const cplx<T> *__restrict__ AV, int ky, int ldv,
+                const int *grp_off, const int *grp_idx, const int *slot, int Hx, int lgy, int RB,
+                cplx<T> *__restrict__ B, int ny_out, int ldb, const cplx<T> *__restrict__ tw, int lgtw) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int My = 1 << lgy;
     const size_t bs = sp_size((size_t)RB * My);
@@ -358,8 +358,8 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
             const int rr = idx >> lgy, y = idx & (My - 1);
             cplx<T> a{T(0), T(0)}, b{T(0), T(0)};
             if (rr < nrow) {
-                if (y < ly) a = AU[((int64_t)s * Hx + fx0 + rr) * ly + y];
-                if (y < ky) b = AV[((int64_t)s * Hx + fx0 + rr) * ky + y];
+                if (y < ly) a = AU[((int64_t)s * Hx + fx0 + rr) * ldu + y];
+                if (y < ky) b = AV[((int64_t)s * Hx + fx0 + rr) * ldv + y];
             }
             u0[sp(idx)] = a; v0[sp(idx)] = b;
         }
@@ -374,7 +374,7 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
     #pragma unroll 8
     for (int idx = threadIdx.x; idx < RB * ny_out; idx += blockDim.x) {
         const int rr = idx / ny_out, y = idx - rr * ny_out;
-        if (rr < nrow) B[((int64_t)g * Hx + fx0 + rr) * ny_out + y] = out[sp(rr * My + y)];
+        if (rr < nrow) B[((int64_t)g * Hx + fx0 + rr) * ldb + y] = out[sp(rr * My + y)];
     }
 }
 
@@ -386,9 +386,9 @@ fft_pass_b_conv(const cplx<T> *__restrict__ AU, int ly, const cplx<T> *__restric
 // ---------------------------------------------------------------------------
 template <typename T, int MAXT>
 __global__ void __launch_bounds__(MAXT, sizeof(T) == 4 ? (MAXT <= 256 ? 6 : 3) : (MAXT <= 256 ? 4 : 2))
-fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int ox, T inv, T *__restrict__ out,
+fft_pass_c(const cplx<T> *__restrict__ B, int oy, int ldb, int Hx, int lgx, int CB, int ox, T inv, T *__restrict__ out,
            int64_t ldo, const int *__restrict__ omap, const int *__restrict__ w, int64_t stride,
-           const cplx<T> *__restrict__ tw, int lgtw, const cplx<T> *__restrict__ Afu, int ny_in,
+           const cplx<T> *__restrict__ tw, int lgtw, const cplx<T> *__restrict__ Afu, int ny_in, int lda,
            const cplx<T> *__restrict__ gk, int lgy) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int Mx = 1 << lgx;
@@ -411,7 +411,7 @@ fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int o
             // B[fx, y] = Σ_{y'} conj(A[fx, y']) · g[fx, (y + y') mod My], g = unnormalised inverse
             // y-DFT of the X̂ row (plan time)
             const int My = 1 << lgy;
-            const cplx<T> *ar = Afu + ((int64_t)j * Hx + fx) * ny_in;
+            const cplx<T> *ar = Afu + ((int64_t)j * Hx + fx) * lda;
             const cplx<T> *gr = gk + (int64_t)fx * My;
             const int ya_i = y0 + 2 * t;
             for (int yp = 0; yp < ny_in; ++yp) {
@@ -420,7 +420,7 @@ fft_pass_c(const cplx<T> *__restrict__ B, int oy, int Hx, int lgx, int CB, int o
                 if (2 * t + 1 < ncol) yb = cadd(yb, cmulconj(gr[(ya_i + 1 + yp) & (My - 1)], a));
             }
         } else {
-            const int64_t base = ((int64_t)j * Hx + fx) * oy + y0 + 2 * t;
+            const int64_t base = ((int64_t)j * Hx + fx) * ldb + y0 + 2 * t;
             if (2 * t < ncol) ya = B[base];
             if (2 * t + 1 < ncol) yb = B[base + 1];
         }
@@ -456,6 +456,8 @@ struct FftOperator {
     DevBuf Xh;        // cplx[Hx][My]: DFT2 of the image
     DevBuf gk;        // cplx[Hx][My]: unnormalised inverse y-DFT of each X̂ row (small My: folded pass B)
     DevBuf rtw_x, rtw_y;     // twiddle tables of the register-resident radix-16 passes (fp32, fft_reg.cu)
+    DevBuf lowcells;         // cells with 0 < w_n < w_max / 64 (averaging re-done by direct summation)
+    int n_lowcells = -1;
     DevBuf bufA, bufB;
     size_t capA = 0, capB = 0;
 };
@@ -494,12 +496,18 @@ static size_t smem_ab(int lg, int nb, int /*unused*/) {
     return sizeof(cplx<T>) * (2 * sp_size((size_t)nb << lg) + stab_count(lg));
 }
 
+// Row stride of the intermediates A (by columns) and B (oy columns): rounded up to 4 complex
+// values, so that rows start 32-B aligned and the transposed column accesses of passes A and C move
+// 16-B / 32-B vectors (the padding columns are written by no pass and masked on every read)
+static int row_ld(int n) { return (int)rup(n, 4); }
+
 template <typename T>
 static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int bx, int by, int k, const int *jsel,
                    const double *scale, cplx<T> *A, cudaStream_t st) {
+    const int lda = row_ld(by);
     if constexpr (sizeof(T) == 4) {
         if (f.rtw_x.p) {
-            rfft::pass_a(f.lgx, in, ld, map, bx, by, k, jsel, scale, reinterpret_cast<float2 *>(A),
+            rfft::pass_a(f.lgx, in, ld, map, bx, by, k, jsel, scale, reinterpret_cast<float2 *>(A), lda,
                          f.rtw_x.as<float2>(), st);
             return;
         }
@@ -509,18 +517,24 @@ static void pass_a(FftOperator &f, const T *in, int64_t ld, const int *map, int 
     const int nth = threads_for(f.lgx, CB / 2, cdiv(by, CB) * k);
     auto kern = nth <= 256 ? fft_pass_a<T, 256> : fft_pass_a<T, 512>;
     set_max_smem(kern);
-    kern<<<dim3((unsigned)cdiv(by, CB), k), nth, smem, st>>>(in, ld, map, bx, by, k, jsel, scale, f.lgx, CB, A,
+    kern<<<dim3((unsigned)cdiv(by, CB), k), nth, smem, st>>>(in, ld, map, bx, by, k, jsel, scale, f.lgx, CB, A, lda,
                                                                         f.stab_x.as<cplx<T>>(), f.lgx);
     after_launch("fft_pass_a");
 }
 
+// B between pass B and pass C is blocked by pass C's column blocks when both run the register
+// passes (fft_reg.cu boff); the Stockham passes use the row layout
+static int b_blocking(const FftOperator &f) { return (f.rtw_x.p && f.rtw_y.p) ? rfft::cb_of(f.lgx) : 0; }
+static size_t b_cols(const FftOperator &f, int oy) { return (size_t)rup(oy, std::max(4, b_blocking(f))); }
+
 template <typename T>
 static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode, cplx<T> *B, int ny_out, cudaStream_t st) {
+    const int lda = row_ld(ny_in), ldb = mode == 1 ? f.My : row_ld(ny_out);
     if constexpr (sizeof(T) == 4) {
         if (f.rtw_y.p && mode == 0) {
-            rfft::pass_b(f.lgy, reinterpret_cast<const float2 *>(A), ny_in, f.Hx, k,
-                         reinterpret_cast<const float2 *>(f.Xh.p), reinterpret_cast<float2 *>(B), ny_out,
-                         f.rtw_y.as<float2>(), st);
+            rfft::pass_b(f.lgy, reinterpret_cast<const float2 *>(A), ny_in, lda, f.Hx, k,
+                         reinterpret_cast<const float2 *>(f.Xh.p), reinterpret_cast<float2 *>(B), ny_out, ldb,
+                         b_blocking(f), f.rtw_y.as<float2>(), st);
             return;
         }
     }
@@ -530,8 +544,8 @@ static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode,
     const int nth = threads_for(f.lgy, RB, cdiv(f.Hx, RB) * k);
     auto kern = nth <= 256 ? fft_pass_b<T, 256> : fft_pass_b<T, 512>;
     set_max_smem(kern);
-    kern<<<dim3(k, (unsigned)cdiv(f.Hx, RB)), nth, smem, st>>>(A, ny_in, f.Hx, f.lgy, RB,
-                                                                         f.Xh.as<cplx<T>>(), mode, B, ny_out,
+    kern<<<dim3(k, (unsigned)cdiv(f.Hx, RB)), nth, smem, st>>>(A, ny_in, lda, f.Hx, f.lgy, RB,
+                                                                         f.Xh.as<cplx<T>>(), mode, B, ny_out, ldb,
                                                                          f.stab_y.as<cplx<T>>(), f.lgy);
     after_launch("fft_pass_b");
 }
@@ -539,9 +553,10 @@ static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode,
 template <typename T>
 static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *out, int64_t ldo, const int *omap,
                    const int *w, int64_t stride, cudaStream_t st, const cplx<T> *Afu = nullptr, int ny_in = 0) {
+    const int ldb = row_ld(oy), lda = row_ld(ny_in);
     if constexpr (sizeof(T) == 4) {
         if (f.rtw_x.p && !Afu) {
-            rfft::pass_c(f.lgx, reinterpret_cast<const float2 *>(B), oy, f.Hx, k, ox,
+            rfft::pass_c(f.lgx, reinterpret_cast<const float2 *>(B), oy, ldb, b_blocking(f) != 0, f.Hx, k, ox,
                          (float)(1.0 / ((double)f.Mx * (double)f.My)), out, ldo, omap, w, stride, f.rtw_x.as<float2>(),
                          st);
             return;
@@ -553,9 +568,10 @@ static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *o
     auto kern = nth <= 256 ? fft_pass_c<T, 256> : fft_pass_c<T, 512>;
     set_max_smem(kern);
     const T inv = (T)(1.0 / ((double)f.Mx * (double)f.My));
-    kern<<<dim3((unsigned)cdiv(oy, CB), k), nth, smem, st>>>(B, oy, f.Hx, f.lgx, CB, ox, inv, out, ldo, omap,
+    kern<<<dim3((unsigned)cdiv(oy, CB), k), nth, smem, st>>>(B, oy, ldb, f.Hx, f.lgx, CB, ox, inv, out, ldo, omap,
                                                                        w, stride, f.stab_x.as<cplx<T>>(), f.lgx, Afu,
-                                                                       ny_in, Afu ? f.gk.as<cplx<T>>() : nullptr, f.lgy);
+                                                                       ny_in, lda, Afu ? f.gk.as<cplx<T>>() : nullptr,
+                                                                       f.lgy);
     after_launch("fft_pass_c");
 }
 
@@ -624,7 +640,7 @@ static void build_impl(PlanImpl &p) {
     }
     f.Xh.alloc(sizeof(cplx<T>) * (size_t)f.Hx * f.My, p.st);
     DevBuf tmp;
-    tmp.alloc(sizeof(cplx<T>) * (size_t)f.Hx * p.ny, p.st);
+    tmp.alloc(sizeof(cplx<T>) * (size_t)f.Hx * row_ld(p.ny), p.st);
     // X̂: x-DFT of the image columns, then the full-length y-DFT (mode 1)
     pass_a<T>(f, p.img.as<T>(), 0, nullptr, p.nx, p.ny, 1, nullptr, nullptr, tmp.as<cplx<T>>(), p.st);
     pass_b<T>(f, tmp.as<cplx<T>>(), p.ny, 1, 1, f.Xh.as<cplx<T>>(), f.My, p.st);
@@ -650,8 +666,8 @@ static void correlate(PlanImpl &p, const T *in, int64_t ldin, const int *imap, i
     FftOperator &f = *p.fft;
     for (int j0 = 0; j0 < k; j0 += 64) {
         const int kc = std::min(64, k - j0);
-        ensure<T>(f, f.bufA, f.capA, sizeof(cplx<T>) * (size_t)kc * f.Hx * by, p.st);
-        ensure<T>(f, f.bufB, f.capB, sizeof(cplx<T>) * (size_t)kc * f.Hx * oy, p.st);
+        ensure<T>(f, f.bufA, f.capA, sizeof(cplx<T>) * (size_t)kc * f.Hx * row_ld(by), p.st);
+        ensure<T>(f, f.bufB, f.capB, sizeof(cplx<T>) * (size_t)kc * f.Hx * b_cols(f, oy), p.st);
         pass_a<T>(f, in + ldin * j0, ldin, imap, bx, by, kc, nullptr, nullptr, f.bufA.as<cplx<T>>(), p.st);
         static const bool nofold = std::getenv("SSA_FFT_NOFOLD") != nullptr;
         if (f.gk.p && !nofold && by <= 2 && (int64_t)by * oy <= 64) {
@@ -677,6 +693,57 @@ void fft_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k) {
 }
 
 // Grouped averaging via FFT: out_g = IDFT2(Σ_{i∈I_g} σ_i Ψ̂_i Φ̂_i) / 𝕎 (NaN off 𝔑′).
+// ---------------------------------------------------------------------------
+// Low-weight cells of the FFT averaging.  The FFT forms the numerator Σ_{ℓ+κ=n} σ U[ℓ] V[κ] with an
+// absolute rounding error that is uniform over the grid (~ε·RMS of the numerator), and Alg. 4 then
+// divides by w_n: at the borders (w_n down to 1 at the corners, against w_max = |𝔏| in the bulk) the
+// relative error grows by w_max / w_n (c5 corners: ~1.5e-3 of the reconstruction's RMS in fp32,
+// measured).  Cells with w_n < w_max / 64 are therefore re-done by direct summation over their
+// w_n (ℓ, κ) pairs (fp64 accumulation): at most ~1.5e-6·RMS error left anywhere, for a few tens of
+// thousands of cells x w_n terms.
+__global__ void low_weight_cells_kernel(const int *__restrict__ w, int64_t n, int thr, int *list, int *count) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int wn = w[t];
+        if (wn > 0 && wn < thr) list[atomicAdd(count, 1)] = (int)t;
+    }
+}
+
+// one warp per (cell, group): out[g*stride + n] = Σ_{i∈I_g} σ_i Σ_{ℓ∈𝔏, κ=n−ℓ∈𝔎} U_i[ℓ] V_i[κ] / wdiv[n]
+template <typename T>
+__global__ void diagsums_cells_kernel(const int *__restrict__ cells, int ncells, int nx, int lx, int ly,
+                                      const int *__restrict__ lmap, int kx, int ky, const int *__restrict__ kmap,
+                                      const T *__restrict__ U, int64_t ldu, const T *__restrict__ V, int64_t ldv,
+                                      const double *__restrict__ sig, const int *__restrict__ grp_off,
+                                      const int *__restrict__ grp_idx, const int *__restrict__ wdiv, T *out,
+                                      int64_t stride) {
+    const int lane = threadIdx.x & 31;
+    const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int g = blockIdx.y;
+    if (c >= ncells) return;
+    const int n = cells[c];
+    const int i = n % nx, j = n / nx;
+    const int a0 = max(0, i - kx + 1), a1 = min(lx - 1, i), b0 = max(0, j - ky + 1), b1 = min(ly - 1, j);
+    const int na = a1 - a0 + 1, nb = b1 - b0 + 1;
+    double acc = 0.0;
+    for (int m = grp_off[g]; m < grp_off[g + 1]; ++m) {
+        const int t = grp_idx[m];
+        const T *u = U + ldu * t;
+        const T *v = V + ldv * t;
+        double s = 0.0;
+        for (int q = lane; q < na * nb; q += 32) {
+            const int la = a0 + q % na, lb = b0 + q / na;          // ℓ = (la, lb), κ = (i − la, j − lb)
+            const int lbox = la + lx * lb, kbox = (i - la) + kx * (j - lb);
+            const int li = lmap ? lmap[lbox] : lbox;
+            const int ki = kmap ? kmap[kbox] : kbox;
+            if (li >= 0 && ki >= 0) s += (double)u[li] * (double)v[ki];
+        }
+        acc += sig[t] * s;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[(int64_t)g * stride + n] = (T)(acc / (double)wdiv[n]);
+}
+
 template <typename T>
 void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, const int *grp_off_dev,
                   const int *grp_idx_dev, int ng, const std::vector<int> &used, const int *slot_dev, T *out,
@@ -686,9 +753,9 @@ void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, co
     DevBuf jsel, AU, AV, B;
     jsel.alloc(sizeof(int) * std::max(nu, 1), p.st);
     SSA_CUDA(cudaMemcpyAsync(jsel.p, used.data(), sizeof(int) * nu, cudaMemcpyHostToDevice, p.st));
-    AU.alloc(sizeof(cplx<T>) * (size_t)nu * f.Hx * p.ly, p.st);
-    AV.alloc(sizeof(cplx<T>) * (size_t)nu * f.Hx * p.ky, p.st);
-    B.alloc(sizeof(cplx<T>) * (size_t)ng * f.Hx * p.ny, p.st);
+    AU.alloc(sizeof(cplx<T>) * (size_t)nu * f.Hx * row_ld(p.ly), p.st);
+    AV.alloc(sizeof(cplx<T>) * (size_t)nu * f.Hx * row_ld(p.ky), p.st);
+    B.alloc(sizeof(cplx<T>) * (size_t)ng * f.Hx * b_cols(f, p.ny), p.st);
     pass_a<T>(f, U, p.L, p.full_window ? nullptr : p.lmap.as<int>(), p.lx, p.ly, nu, jsel.as<int>(), sig_dev,
               AU.as<cplx<T>>(), p.st);
     pass_a<T>(f, V, p.K, p.full_k ? nullptr : p.kmap.as<int>(), p.kx, p.ky, nu, jsel.as<int>(), nullptr,
@@ -696,8 +763,9 @@ void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, co
     bool done = false;
     if constexpr (sizeof(T) == 4) {
         if (f.rtw_y.p) {
-            rfft::pass_bconv(f.lgy, AU.as<float2>(), p.ly, AV.as<float2>(), p.ky, grp_off_dev, grp_idx_dev, slot_dev,
-                             f.Hx, ng, B.as<float2>(), p.ny, f.rtw_y.as<float2>(), p.st);
+            rfft::pass_bconv(f.lgy, AU.as<float2>(), p.ly, row_ld(p.ly), AV.as<float2>(), p.ky, row_ld(p.ky), grp_off_dev,
+                             grp_idx_dev, slot_dev, f.Hx, ng, B.as<float2>(), p.ny, row_ld(p.ny), b_blocking(f),
+                             f.rtw_y.as<float2>(), p.st);
             done = true;
         }
     }
@@ -708,11 +776,37 @@ void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, co
         auto kern = nth <= 256 ? fft_pass_b_conv<T, 256> : fft_pass_b_conv<T, 512>;
         set_max_smem(kern);
         kern<<<dim3((unsigned)cdiv(f.Hx, RB), ng), nth, smem, p.st>>>(
-            AU.as<cplx<T>>(), p.ly, AV.as<cplx<T>>(), p.ky, grp_off_dev, grp_idx_dev, slot_dev, f.Hx, f.lgy, RB,
-            B.as<cplx<T>>(), p.ny, f.stab_y.as<cplx<T>>(), f.lgy);
+            AU.as<cplx<T>>(), p.ly, row_ld(p.ly), AV.as<cplx<T>>(), p.ky, row_ld(p.ky), grp_off_dev, grp_idx_dev,
+            slot_dev, f.Hx, f.lgy, RB, B.as<cplx<T>>(), p.ny, row_ld(p.ny), f.stab_y.as<cplx<T>>(), f.lgy);
         after_launch("fft_pass_b_conv");
     }
     pass_c<T>(f, B.as<cplx<T>>(), p.ny, ng, p.nx, out, p.nx, nullptr, wdiv, (int64_t)p.nx * p.ny, p.st);
+    // low-weight cells by direct summation (see diagsums_cells_kernel)
+    const int64_t nxy = (int64_t)p.nx * p.ny;
+    if (f.n_lowcells < 0) {
+        const int wmax = (int)std::min<int64_t>(p.L, p.K);
+        const int thr = wmax / 64;
+        f.n_lowcells = 0;
+        if (thr > 1) {
+            DevBuf cnt;
+            cnt.alloc(sizeof(int), p.st);
+            SSA_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), p.st));
+            // upper bound on the list: cells with w < thr lie within ~thr/... of the border; size it by nxy
+            f.lowcells.alloc(sizeof(int) * nxy, p.st);
+            low_weight_cells_kernel<<<(unsigned)std::min<int64_t>(cdiv(nxy, 256), 16 * num_sms()), 256, 0, p.st>>>(
+                p.weights.as<int>(), nxy, thr, f.lowcells.as<int>(), cnt.as<int>());
+            after_launch("low_weight_cells");
+            SSA_CUDA(cudaMemcpyAsync(&f.n_lowcells, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, p.st));
+            SSA_CUDA(cudaStreamSynchronize(p.st));
+        }
+    }
+    if (f.n_lowcells > 0 && ng > 0) {
+        diagsums_cells_kernel<T><<<dim3((unsigned)cdiv(f.n_lowcells, 8), ng), 256, 0, p.st>>>(
+            f.lowcells.as<int>(), f.n_lowcells, p.nx, p.lx, p.ly, p.full_window ? nullptr : p.lmap.as<int>(), p.kx,
+            p.ky, p.full_k ? nullptr : p.kmap.as<int>(), U, p.L, V, p.K, sig_dev, grp_off_dev, grp_idx_dev, wdiv, out,
+            nxy);
+        after_launch("diagsums_cells");
+    }
     SSA_CUDA(cudaStreamSynchronize(p.st));
 }
 

@@ -25,6 +25,8 @@
 // Intermediate layouts are the ones of fft.cu (A[(j*H + fx)*by + col], B[(j*H + fx)*oy + y]), so a
 // pass can run either implementation.
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.h"
@@ -110,6 +112,7 @@ __host__ __device__ constexpr int pad_size(int n) { return n + n / 16 + 1; }
 __host__ __device__ constexpr int r0_of(int lg) { return (lg & 3) ? (1 << (lg & 3)) : 16; }
 // twiddle-table entries of all radix-16 stages: Σ spans · 15 = N − R0
 __host__ __device__ constexpr int tw_count_c(int lg) { return (1 << lg) - r0_of(lg); }
+__host__ __device__ constexpr int H_of(int lg) { return (1 << lg) / 2 + 1; }
 
 template <int NT> __device__ __forceinline__ void xsync() {
     if constexpr (NT <= 32) __syncwarp();
@@ -149,7 +152,9 @@ template <int NT, int RP, int NSP> __device__ __forceinline__ void exchange(floa
     xsync<NT>();
 }
 
-template <int LG, int DIR, int RP, int NSP>
+// KEEP1: only the outputs X[t] (e = 0) are needed (pass B of X·V keeps the first Ly <= NT rows):
+// the last stage then forms just the r = 0 output of its 16-point DFT, Σ_r twiddled inputs
+template <int LG, int DIR, int RP, int NSP, bool KEEP1>
 __device__ __forceinline__ void stages16(float2 *v, float2 *S, const float2 *__restrict__ tw, int t) {
     constexpr int N = 1 << LG, NT = N >> 4, NS = NSP * RP;
     if constexpr (NS < N) {
@@ -162,16 +167,23 @@ __device__ __forceinline__ void stages16(float2 *v, float2 *S, const float2 *__r
             if (DIR > 0) c.y = -c.y;
             v[r] = cmul(v[r], c);
         }
-        dft16<DIR>(v);
-        stages16<LG, DIR, 16, NS>(v, S, tw, t);
+        if constexpr (KEEP1 && NS * 16 == N) {
+            float2 s0 = v[0], s1 = v[1];
+#pragma unroll
+            for (int r = 2; r < 16; r += 2) { s0 = cadd(s0, v[r]); s1 = cadd(s1, v[r + 1]); }
+            v[0] = cadd(s0, s1);
+        } else {
+            dft16<DIR>(v);
+            stages16<LG, DIR, 16, NS, KEEP1>(v, S, tw, t);
+        }
     }
 }
 
-// Full 2^LG-point DFT of the data held as v[e] = x[t + NT·e]; on return v[e] = X[t + NT·e].
-// triv0: only the r = 0 inputs of every stage-0 butterfly are nonzero (x[i] = 0 for i >= NT·16/R0),
-// so stage 0 just replicates them.  All NT threads of the transform (and, for NT > 32, all threads
-// of the CTA) must call it together.
-template <int LG, int DIR>
+// Full 2^LG-point DFT of the data held as v[e] = x[t + NT·e]; on return v[e] = X[t + NT·e] (KEEP1:
+// only v[0] = X[t] is valid).  triv0: only the r = 0 inputs of every stage-0 butterfly are nonzero
+// (x[i] = 0 for i >= NT·16/R0), so stage 0 just replicates them.  All NT threads of the transform
+// (and, for NT > 32, all threads of the CTA) must call it together.
+template <int LG, int DIR, bool KEEP1 = false>
 __device__ __forceinline__ void fft(float2 *v, float2 *S, const float2 *__restrict__ tw, int t, bool triv0) {
     constexpr int R0 = r0_of(LG), B0 = 16 / R0;
     if (triv0) {
@@ -182,7 +194,7 @@ __device__ __forceinline__ void fft(float2 *v, float2 *S, const float2 *__restri
     } else {
         stage0<DIR, R0>(v);
     }
-    stages16<LG, DIR, R0, 1>(v, S, tw, t);
+    stages16<LG, DIR, R0, 1, KEEP1>(v, S, tw, t);
 }
 
 // Launch shapes.  Passes A and C (HBM-bound, transposed column access) run TPC = 2 transforms
@@ -194,7 +206,7 @@ template <int LG, bool ROWPASS = false> struct Cfg {
     static constexpr int N = 1 << LG, NT = N / 16, H = N / 2 + 1;
     static constexpr int TPC = ROWPASS ? (NT >= 256 ? 1 : 256 / NT) : (NT >= 256 ? 2 : 256 / NT);
     static constexpr int THREADS = NT * TPC;
-    static constexpr int MINB = ROWPASS ? 3 : 65536 / (THREADS * 64);
+    static constexpr int MINB = ROWPASS ? (LG == 12 ? 3 : 2) : 65536 / (THREADS * 64);
     static constexpr int TW = tw_count_c(LG);
     static constexpr int TWP = (TW + 1) & ~1;               // keep the buffers 16-B aligned
     static constexpr int XB = (pad_size(N) + 1) & ~1;       // one exchange buffer
@@ -209,96 +221,142 @@ template <int LG> __device__ __forceinline__ float2 *xbuf(float2 *sm, int q) {
     return sm + Cfg<LG>::TWP + (size_t)q * Cfg<LG>::XB;
 }
 
+// All passes are persistent: a grid of (resident CTAs per SM) x (SMs) CTAs loops over the work items,
+// so the twiddle table is staged into shared memory once per CTA rather than once per item (one
+// 32 KB table per 32 KB row of pass B was half of its L2 traffic, ncu), and launch tails vanish.
+
+// Address of element (row fx, column y) of vector / group j in the intermediate B between pass B and
+// pass C: row layout (cbc = 0: B[(j*H + fx)*ldb + y]) or blocked by pass C's column blocks
+// (cbc = its CB: B[((j*nyb + y/cbc)*H + fx)*cbc + y%cbc]), in which pass C's item — all H rows of
+// cbc columns — is one contiguous block: its reads stream instead of gathering a 32-B sector per row
+// (the row layout left c5's Xᵀ·U pass C at 1.5 TB/s, ncu); pass B's writes take the scatter instead.
+__device__ __forceinline__ int64_t boff(int j, int fx, int y, int H, int ldb, int cbc, int nyb) {
+    if (cbc == 0) return ((int64_t)j * H + fx) * ldb + y;
+    const int yb = y / cbc;
+    return (((int64_t)j * nyb + yb) * H + fx) * cbc + (y - yb * cbc);
+}
+
 // ------------------------------------------------------------------------------------ pass A
+// item = (vector jo, block of CB = 2·TPC input columns); consecutive CTAs take consecutive column
+// blocks of one vector (contiguous reads)
 template <int LG>
 __global__ void __launch_bounds__(Cfg<LG>::THREADS, Cfg<LG>::MINB)
-rpass_a(const float *__restrict__ in, int64_t ld, const int *__restrict__ map, int bx, int by,
-        const int *__restrict__ jsel, const double *__restrict__ scale, float2 *__restrict__ A,
+rpass_a(const float *__restrict__ in, int64_t ld, const int *__restrict__ map, int bx, int by, int k,
+        const int *__restrict__ jsel, const double *__restrict__ scale, float2 *__restrict__ A, int lda,
         const float2 *__restrict__ twg) {
     using C = Cfg<LG>;
-    constexpr int N = C::N, NT = C::NT, H = C::H, CB = 2 * C::TPC;
+    constexpr int N = C::N, NT = C::NT, H = C::H, TPC = C::TPC, CB = 2 * TPC;
     extern __shared__ float2 sm[];
     const float2 *tw = stage_tw<LG>(sm, twg);
     const int q = threadIdx.x / NT, t = threadIdx.x % NT;
     float2 *S = xbuf<LG>(sm, q);
-    const int col0 = blockIdx.x * CB;
-    const int jo = blockIdx.y;
-    const int j = jsel ? jsel[jo] : jo;
-    const float sc = scale ? (float)scale[j] : 1.f;
-    const int ca = col0 + 2 * q, cb = ca + 1;
-    const float *src = in + ld * j;
-    float2 v[16];
+    const int nb = (by + CB - 1) / CB, items = nb * k;
+    __syncthreads();   // twiddle table staged
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int jo = it / nb, col0 = (it - jo * nb) * CB;
+        const int j = jsel ? jsel[jo] : jo;
+        const int ca = col0 + 2 * q, cb = ca + 1;
+        const float *src = in + ld * j;
+        float2 v[16];
+        if (!map) {
+            // all 32 loads issued before any use (the round-1 form with a per-element map test and scale
+            // serialised load -> use -> next load: 5.4 ms of latency-bound pass A on c5, ncu)
+            const float *pa = src + (int64_t)bx * min(ca, by - 1), *pb = src + (int64_t)bx * min(cb, by - 1);
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        const int ix = t + NT * e;
-        float a = 0.f, b = 0.f;
-        if (ix < bx) {
-            if (ca < by) {
-                const int64_t box = ix + (int64_t)bx * ca;
-                const int64_t ci = map ? (int64_t)map[box] : box;
-                if (ci >= 0) a = sc * src[ci];
+            for (int e = 0; e < 16; ++e) {
+                const int ix = t + NT * e;
+                v[e].x = ix < bx ? __ldg(pa + ix) : 0.f;
+                v[e].y = ix < bx ? __ldg(pb + ix) : 0.f;
             }
-            if (cb < by) {
-                const int64_t box = ix + (int64_t)bx * cb;
-                const int64_t ci = map ? (int64_t)map[box] : box;
-                if (ci >= 0) b = sc * src[ci];
+            if (ca >= by)
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e].x = 0.f;
+            if (cb >= by)
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e].y = 0.f;
+        } else {
+            int ia[16], ib[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int ix = t + NT * e;
+                ia[e] = (ix < bx && ca < by) ? map[ix + (int64_t)bx * ca] : -1;
+                ib[e] = (ix < bx && cb < by) ? map[ix + (int64_t)bx * cb] : -1;
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                v[e].x = ia[e] >= 0 ? __ldg(src + ia[e]) : 0.f;
+                v[e].y = ib[e] >= 0 ? __ldg(src + ib[e]) : 0.f;
             }
         }
-        v[e] = make_float2(a, b);
-    }
-    __syncthreads();   // twiddle table staged
-    fft<LG, -1>(v, S, tw, t, false);
-    // Hermitian split of the two packed real columns: X_a[f] = (Z[f] + conj Z[−f]) / 2,
-    // X_b[f] = (Z[f] − conj Z[−f]) / (2i); needs Z[f] and Z[N − f] (held by other threads)
+        fft<LG, -1>(v, S, tw, t, false);
+        // Hermitian split of the two packed real columns: X_a[f] = (Z[f] + conj Z[−f]) / 2,
+        // X_b[f] = (Z[f] − conj Z[−f]) / (2i); needs Z[f] and Z[N − f] (held by other threads).  The
+        // per-vector scale (σ_i of the averaging) is linear and applied here.
 #pragma unroll
-    for (int e = 0; e < 16; ++e) S[pad(t + NT * e)] = v[e];
-    __syncthreads();
-    // transposed write, consecutive threads -> consecutive columns of one fx
-    for (int idx = threadIdx.x; idx < H * CB; idx += blockDim.x) {
-        const int fx = idx / CB, c = idx - fx * CB;
-        const int col = col0 + c;
-        if (col >= by) continue;
-        const float2 *Sq = xbuf<LG>(sm, c >> 1);
-        const float2 z = Sq[pad(fx)], zm = Sq[pad((N - fx) & (N - 1))];
-        const float2 o = (c & 1) ? make_float2(0.5f * (z.y + zm.y), 0.5f * (zm.x - z.x))
-                                 : make_float2(0.5f * (z.x + zm.x), 0.5f * (z.y - zm.y));
-        A[((int64_t)jo * H + fx) * by + col] = o;
+        for (int e = 0; e < 16; ++e) S[pad(t + NT * e)] = v[e];
+        __syncthreads();
+        const float hs = 0.5f * (scale ? (float)scale[j] : 1.f);
+        // transposed write: one 16-B store of the column pair (2q2, 2q2 + 1) per (fx, q2);
+        // consecutive threads -> consecutive pairs of one fx (32-B aligned rows of stride lda)
+        float2 *arow = A + (int64_t)jo * H * lda + col0;
+        for (int idx = threadIdx.x; idx < H * TPC; idx += blockDim.x) {
+            const int fx = idx / TPC, q2 = idx - fx * TPC;
+            const int col = col0 + 2 * q2;
+            if (col >= by) continue;
+            const float2 *Sq = xbuf<LG>(sm, q2);
+            const float2 z = Sq[pad(fx)], zm = Sq[pad((N - fx) & (N - 1))];
+            const float4 o = make_float4(hs * (z.x + zm.x), hs * (z.y - zm.y), hs * (z.y + zm.y), hs * (zm.x - z.x));
+            float2 *dst = arow + (int64_t)fx * lda + 2 * q2;
+            if (col + 1 < by) *reinterpret_cast<float4 *>(dst) = o;
+            else *dst = make_float2(o.x, o.y);
+        }
+        __syncthreads();   // the buffers are rewritten by the next item
     }
 }
 
 // ------------------------------------------------------------------------------------ pass B
-// grid (k, ceil(H / TPC)): the k CTAs that use the same X̂ rows run back to back (X̂ stays in L2)
-template <int LG>
+// item = (vector j, block of TPC rows fx); the k items that use the same X̂ rows are consecutive
+// (X̂ stays in L2 while the much larger A stream passes)
+template <int LG, bool KEEP1>
 __global__ void __launch_bounds__(Cfg<LG, true>::THREADS, Cfg<LG, true>::MINB)
-rpass_b(const float2 *__restrict__ A, int ny_in, int H, const float2 *__restrict__ Xh, float2 *__restrict__ B,
-        int ny_out, const float2 *__restrict__ twg) {
+rpass_b(const float2 *__restrict__ A, int ny_in, int lda, int H, int k, const float2 *__restrict__ Xh,
+        float2 *__restrict__ B, int ny_out, int ldb, int cbc, const float2 *__restrict__ twg) {
     using C = Cfg<LG, true>;
     constexpr int N = C::N, NT = C::NT, TPC = C::TPC, B0 = 16 / r0_of(LG);
     extern __shared__ float2 sm[];
     const float2 *tw = stage_tw<LG>(sm, twg);
     const int q = threadIdx.x / NT, t = threadIdx.x % NT;
     float2 *S = xbuf<LG>(sm, q);
-    const int j = blockIdx.x;
-    const int fx = blockIdx.y * TPC + q;
-    const bool ok = fx < H;
-    const float2 *arow = A + ((int64_t)j * H + fx) * ny_in;
-    float2 v[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        const int y = t + NT * e;
-        v[e] = (ok && y < ny_in) ? arow[y] : make_float2(0.f, 0.f);
-    }
+    const int items = k * ((H + TPC - 1) / TPC);
+    const bool triv = ny_in <= NT * B0;
     __syncthreads();
-    fft<LG, -1>(v, S, tw, t, ny_in <= NT * B0);
-    const float2 *xr = Xh + (int64_t)(ok ? fx : 0) * N;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int j = it % k;
+        const int fx = (it / k) * TPC + q;
+        const bool ok = fx < H;
+        const float2 *arow = A + ((int64_t)j * H + (ok ? fx : 0)) * lda;
+        float2 v[16];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = cmulc(__ldg(xr + t + NT * e), v[e]);   // X̂ ⊙ conj(Â)
-    fft<LG, +1>(v, S, tw, t, false);
-    float2 *brow = B + ((int64_t)j * H + fx) * ny_out;
+        for (int e = 0; e < 16; ++e) {
+            const int y = t + NT * e;
+            v[e] = (ok && y < ny_in) ? arow[y] : make_float2(0.f, 0.f);
+        }
+        fft<LG, -1>(v, S, tw, t, triv);
+        const float2 *xr = Xh + (int64_t)(ok ? fx : 0) * N;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        const int y = t + NT * e;
-        if (ok && y < ny_out) brow[y] = v[e];
+        for (int e = 0; e < 16; ++e) v[e] = cmulc(__ldg(xr + t + NT * e), v[e]);   // X̂ ⊙ conj(Â)
+        const int nyb = cbc ? (ny_out + cbc - 1) / cbc : 0;
+        if constexpr (KEEP1) {   // X·V: only the first Ly <= NT rows of the inverse are kept
+            fft<LG, +1, true>(v, S, tw, t, false);
+            if (ok && t < ny_out) B[boff(j, fx, t, H, ldb, cbc, nyb)] = v[0];
+        } else {
+            fft<LG, +1>(v, S, tw, t, false);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int y = t + NT * e;
+                if (ok && y < ny_out) B[boff(j, fx, y, H, ldb, cbc, nyb)] = v[e];
+            }
+        }
     }
 }
 
@@ -306,9 +364,9 @@ rpass_b(const float2 *__restrict__ A, int ny_in, int H, const float2 *__restrict
 // waits in a thread-private shared-memory slot while the AV transform runs
 template <int LG>
 __global__ void __launch_bounds__(Cfg<LG, true>::THREADS, 1)
-rpass_bconv(const float2 *__restrict__ AU, int ly, const float2 *__restrict__ AV, int ky, const int *__restrict__ grp_off,
-            const int *__restrict__ grp_idx, const int *__restrict__ slot, int H, float2 *__restrict__ B, int ny_out,
-            const float2 *__restrict__ twg) {
+rpass_bconv(const float2 *__restrict__ AU, int ly, int ldu, const float2 *__restrict__ AV, int ky, int ldv,
+            const int *__restrict__ grp_off, const int *__restrict__ grp_idx, const int *__restrict__ slot, int H, int ng,
+            float2 *__restrict__ B, int ny_out, int ldb, int cbc, const float2 *__restrict__ twg) {
     using C = Cfg<LG, true>;
     constexpr int NT = C::NT, TPC = C::TPC, B0 = 16 / r0_of(LG);
     extern __shared__ float2 sm[];
@@ -316,105 +374,134 @@ rpass_bconv(const float2 *__restrict__ AU, int ly, const float2 *__restrict__ AV
     const int q = threadIdx.x / NT, t = threadIdx.x % NT;
     float2 *S = xbuf<LG>(sm, q);
     float2 *P = xbuf<LG>(sm, TPC + q);      // private slots of this transform
-    const int g = blockIdx.y;
-    const int fx = blockIdx.x * TPC + q;
-    const bool ok = fx < H;
-    float2 acc[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] = make_float2(0.f, 0.f);
+    const int nfb = (H + TPC - 1) / TPC, items = ng * nfb;
     __syncthreads();
-    for (int m = grp_off[g]; m < grp_off[g + 1]; ++m) {
-        const int s = slot[grp_idx[m]];
-        float2 v[16];
-        const float2 *ur = AU + ((int64_t)s * H + fx) * ly;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int g = it / nfb;
+        const int fx = (it - g * nfb) * TPC + q;
+        const bool ok = fx < H;
+        float2 acc[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[e] = make_float2(0.f, 0.f);
+        for (int m = grp_off[g]; m < grp_off[g + 1]; ++m) {
+            const int s = slot[grp_idx[m]];
+            float2 v[16];
+            const float2 *ur = AU + ((int64_t)s * H + (ok ? fx : 0)) * ldu;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int y = t + NT * e;
+                v[e] = (ok && y < ly) ? ur[y] : make_float2(0.f, 0.f);
+            }
+            fft<LG, -1>(v, S, tw, t, ly <= NT * B0);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) P[pad(t + NT * e)] = v[e];
+            const float2 *vr = AV + ((int64_t)s * H + (ok ? fx : 0)) * ldv;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int y = t + NT * e;
+                v[e] = (ok && y < ky) ? vr[y] : make_float2(0.f, 0.f);
+            }
+            fft<LG, -1>(v, S, tw, t, ky <= NT * B0);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const float2 u = P[pad(t + NT * e)];
+                acc[e] = cadd(acc[e], cmul(u, v[e]));
+            }
+        }
+        fft<LG, +1>(acc, S, tw, t, false);
+        const int nyb = cbc ? (ny_out + cbc - 1) / cbc : 0;
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
             const int y = t + NT * e;
-            v[e] = (ok && y < ly) ? ur[y] : make_float2(0.f, 0.f);
+            if (ok && y < ny_out) B[boff(g, fx, y, H, ldb, cbc, nyb)] = acc[e];
         }
-        fft<LG, -1>(v, S, tw, t, ly <= NT * B0);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) P[pad(t + NT * e)] = v[e];
-        const float2 *vr = AV + ((int64_t)s * H + fx) * ky;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int y = t + NT * e;
-            v[e] = (ok && y < ky) ? vr[y] : make_float2(0.f, 0.f);
-        }
-        fft<LG, -1>(v, S, tw, t, ky <= NT * B0);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const float2 u = P[pad(t + NT * e)];
-            acc[e] = cadd(acc[e], cmul(u, v[e]));
-        }
-    }
-    fft<LG, +1>(acc, S, tw, t, false);
-    float2 *brow = B + ((int64_t)g * H + fx) * ny_out;
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        const int y = t + NT * e;
-        if (ok && y < ny_out) brow[y] = acc[e];
     }
 }
 
 // ------------------------------------------------------------------------------------ pass C
+// item = (vector j, block of CB = 2·TPC output columns)
 template <int LG>
 __global__ void __launch_bounds__(Cfg<LG>::THREADS, Cfg<LG>::MINB)
-rpass_c(const float2 *__restrict__ B, int oy, int H, int ox, float inv, float *__restrict__ out, int64_t ldo,
-        const int *__restrict__ omap, const int *__restrict__ w, int64_t stride, const float2 *__restrict__ twg) {
+rpass_c(const float2 *__restrict__ B, int oy, int ldb, int blocked, int H, int k, int ox, float inv,
+        float *__restrict__ out, int64_t ldo, const int *__restrict__ omap, const int *__restrict__ w, int64_t stride,
+        const float2 *__restrict__ twg) {
     using C = Cfg<LG>;
-    constexpr int N = C::N, NT = C::NT, CB = 2 * C::TPC;
+    constexpr int N = C::N, NT = C::NT, TPC = C::TPC, CB = 2 * TPC, THR = C::THREADS;
+    constexpr int PER = (H_of(LG) * TPC + THR - 1) / THR;   // gathered column pairs per thread
     extern __shared__ float2 sm[];
     const float2 *tw = stage_tw<LG>(sm, twg);
     const int q = threadIdx.x / NT, t = threadIdx.x % NT;
     float2 *S = xbuf<LG>(sm, q);
-    const int y0 = blockIdx.x * CB;
-    const int j = blockIdx.y;
-    const int ncol = min(CB, oy - y0);
-    // gather the CB half-spectrum columns: transform q's buffer holds columns 2q (at [0, H)) and
-    // 2q + 1 (at [H, 2H)); consecutive threads read consecutive columns of one fx
-    const float2 *bj = B + (int64_t)j * H * oy + y0;
-    for (int idx = threadIdx.x; idx < H * CB; idx += blockDim.x) {
-        const int fx = idx / CB, c = idx - fx * CB;
-        float2 val = make_float2(0.f, 0.f);
-        if (c < ncol) val = bj[(int64_t)fx * oy + c];
-        xbuf<LG>(sm, c >> 1)[(c & 1) * H + fx] = val;
-    }
+    const int H0 = C::H;
+    const int nb = (oy + CB - 1) / CB, items = nb * k;
     __syncthreads();
-    // Z[f] = Y_a[f] + i·Y_b[f] over the full spectrum (Y[N − f] = conj Y[f] for real columns;
-    // the bins 0 and N/2 of a real column are real)
-    float2 v[16];
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int j = it / nb, y0 = (it - j * nb) * CB;
+        const int ncol = min(CB, oy - y0);
+        // gather the CB half-spectrum columns: transform q's buffer holds columns 2q (at [0, H)) and
+        // 2q + 1 (at [H, 2H)); one 16-B load per (fx, column pair), consecutive threads -> consecutive
+        // pairs of one fx; all of a thread's loads are issued before the shared-memory stores (the
+        // per-element form was latency-bound: 5.3 ms for c5's Xᵀ·U pass C, ncu)
+        // row layout: rows of stride ldb; blocked layout: this item's H x CB block, contiguous
+        const float2 *bj = blocked ? B + (int64_t)it * H0 * CB : B + (int64_t)j * H0 * ldb + y0;
+        const int64_t rs = blocked ? CB : ldb;
+        float4 tmp[PER];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        const int f = t + NT * e;
-        const bool lo = f <= N / 2;
-        const int fs = lo ? f : N - f;
-        float2 ya = S[fs], yb = S[H + fs];
-        if (!lo) { ya.y = -ya.y; yb.y = -yb.y; }
-        if (f == 0 || f == N / 2) { ya.y = 0.f; yb.y = 0.f; }
-        v[e] = make_float2(ya.x - yb.y, ya.y + yb.x);
-    }
-    __syncthreads();   // the buffers are reused by the exchanges
-    fft<LG, +1>(v, S, tw, t, false);
-    const int ya_col = y0 + 2 * q;
+        for (int u = 0; u < PER; ++u) {
+            const int idx = threadIdx.x + THR * u;
+            const int fx = idx / TPC, q2 = idx - fx * TPC;
+            tmp[u] = (idx < H0 * TPC && 2 * q2 < ncol)
+                         ? __ldg(reinterpret_cast<const float4 *>(bj + (int64_t)fx * rs + 2 * q2))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (2 * q2 + 1 >= ncol) { tmp[u].z = 0.f; tmp[u].w = 0.f; }   // padding column: never written
+        }
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        const int x = t + NT * e;
-        if (x >= ox) continue;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int y = ya_col + h;
-            if (y - y0 >= ncol) continue;
-            const float val = (h ? v[e].y : v[e].x) * inv;
-            if (w) {
-                const int wn = w[x + (int64_t)ox * y];
-                out[(int64_t)j * stride + x + ldo * y] = wn > 0 ? val / (float)wn : __int_as_float(0x7fc00000);
-            } else {
-                const int64_t box = x + (int64_t)ox * y;
-                const int64_t oi = omap ? (int64_t)omap[box] : box;
-                if (oi >= 0) out[oi + ldo * j] = val;
+        for (int u = 0; u < PER; ++u) {
+            const int idx = threadIdx.x + THR * u;
+            const int fx = idx / TPC, q2 = idx - fx * TPC;
+            if (idx < H0 * TPC) {
+                float2 *Sq = xbuf<LG>(sm, q2);
+                Sq[fx] = make_float2(tmp[u].x, tmp[u].y);
+                Sq[H0 + fx] = make_float2(tmp[u].z, tmp[u].w);
             }
         }
+        __syncthreads();
+        // Z[f] = Y_a[f] + i·Y_b[f] over the full spectrum (Y[N − f] = conj Y[f] for real columns;
+        // the bins 0 and N/2 of a real column are real)
+        float2 v[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int f = t + NT * e;
+            const bool lo = f <= N / 2;
+            const int fs = lo ? f : N - f;
+            float2 ya = S[fs], yb = S[H0 + fs];
+            if (!lo) { ya.y = -ya.y; yb.y = -yb.y; }
+            if (f == 0 || f == N / 2) { ya.y = 0.f; yb.y = 0.f; }
+            v[e] = make_float2(ya.x - yb.y, ya.y + yb.x);
+        }
+        __syncthreads();   // the buffers are reused by the exchanges
+        fft<LG, +1>(v, S, tw, t, false);
+        const int ya_col = y0 + 2 * q;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int x = t + NT * e;
+            if (x >= ox) continue;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int y = ya_col + h;
+                if (y - y0 >= ncol) continue;
+                const float val = (h ? v[e].y : v[e].x) * inv;
+                if (w) {
+                    const int wn = w[x + (int64_t)ox * y];
+                    out[(int64_t)j * stride + x + ldo * y] = wn > 0 ? val / (float)wn : __int_as_float(0x7fc00000);
+                } else {
+                    const int64_t box = x + (int64_t)ox * y;
+                    const int64_t oi = omap ? (int64_t)omap[box] : box;
+                    if (oi >= 0) out[oi + ldo * j] = val;
+                }
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -432,8 +519,26 @@ void build_table(int lg, std::vector<float2> &h) {
             }
 }
 
-// the kernel's dynamic shared memory exceeds the 48 KB default: raise the cap once per kernel
-template <typename F> static void prep(F *kern, size_t) { set_max_smem(kern); }
+// the kernel's dynamic shared memory exceeds the 48 KB default: raise the cap once per kernel;
+// persistent grid = resident CTAs per SM (occupancy query, cached per kernel) x SMs, capped by the items
+template <typename F> static int prep(F *kern, int threads, size_t smem, int64_t items) {
+    set_max_smem(kern);
+    static std::mutex mu;
+    static std::map<const void *, int> occ;
+    int per = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto itc = occ.find((const void *)kern);
+        if (itc != occ.end()) {
+            per = itc->second;
+        } else {
+            SSA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem));
+            per = std::max(per, 1);
+            occ[(const void *)kern] = per;
+        }
+    }
+    return (int)std::min<int64_t>(items, (int64_t)per * num_sms());
+}
 
 #define RFFT_DISPATCH(lg, ...)                       \
     switch (lg) {                                     \
@@ -446,46 +551,63 @@ template <typename F> static void prep(F *kern, size_t) { set_max_smem(kern); }
     }
 
 void pass_a(int lg, const float *in, int64_t ld, const int *map, int bx, int by, int k, const int *jsel,
-            const double *scale, float2 *A, const float2 *tw, cudaStream_t st) {
+            const double *scale, float2 *A, int lda, const float2 *tw, cudaStream_t st) {
+    SSA_REQUIRE(lda % 2 == 0 && ((uintptr_t)A & 15) == 0, SSA_ERR_ARG, "rfft pass A: rows must be 16-B aligned");
     RFFT_DISPATCH(lg, {
         using Cf = Cfg<LG>;
-        prep(rpass_a<LG>, Cf::smem);
-        rpass_a<LG><<<dim3((unsigned)cdiv(by, 2 * Cf::TPC), k), Cf::THREADS, Cf::smem, st>>>(in, ld, map, bx, by, jsel,
-                                                                                             scale, A, tw);
+        const int grid = prep(rpass_a<LG>, Cf::THREADS, Cf::smem, cdiv(by, 2 * Cf::TPC) * (int64_t)k);
+        rpass_a<LG><<<grid, Cf::THREADS, Cf::smem, st>>>(in, ld, map, bx, by, k, jsel, scale, A, lda, tw);
     });
     after_launch("rfft_pass_a");
 }
 
-void pass_b(int lg, const float2 *A, int ny_in, int H, int k, const float2 *Xh, float2 *B, int ny_out,
-            const float2 *tw, cudaStream_t st) {
+int cb_of(int lg) {
+    switch (lg) {
+    case 8: return 2 * Cfg<8>::TPC;
+    case 9: return 2 * Cfg<9>::TPC;
+    case 10: return 2 * Cfg<10>::TPC;
+    case 11: return 2 * Cfg<11>::TPC;
+    default: return 2 * Cfg<12>::TPC;
+    }
+}
+
+void pass_b(int lg, const float2 *A, int ny_in, int lda, int H, int k, const float2 *Xh, float2 *B, int ny_out,
+            int ldb, int cbc, const float2 *tw, cudaStream_t st) {
     RFFT_DISPATCH(lg, {
         using Cf = Cfg<LG, true>;
-        prep(rpass_b<LG>, Cf::smem);
-        rpass_b<LG><<<dim3(k, (unsigned)cdiv(H, Cf::TPC)), Cf::THREADS, Cf::smem, st>>>(A, ny_in, H, Xh, B, ny_out, tw);
+        if (ny_out <= Cf::NT) {
+            const int grid = prep(rpass_b<LG, true>, Cf::THREADS, Cf::smem, cdiv(H, Cf::TPC) * (int64_t)k);
+            rpass_b<LG, true><<<grid, Cf::THREADS, Cf::smem, st>>>(A, ny_in, lda, H, k, Xh, B, ny_out, ldb, cbc, tw);
+        } else {
+            const int grid = prep(rpass_b<LG, false>, Cf::THREADS, Cf::smem, cdiv(H, Cf::TPC) * (int64_t)k);
+            rpass_b<LG, false><<<grid, Cf::THREADS, Cf::smem, st>>>(A, ny_in, lda, H, k, Xh, B, ny_out, ldb, cbc, tw);
+        }
     });
     after_launch("rfft_pass_b");
 }
 
-void pass_bconv(int lg, const float2 *AU, int ly, const float2 *AV, int ky, const int *grp_off, const int *grp_idx,
-                const int *slot, int H, int ng, float2 *B, int ny_out, const float2 *tw, cudaStream_t st) {
+void pass_bconv(int lg, const float2 *AU, int ly, int ldu, const float2 *AV, int ky, int ldv, const int *grp_off,
+                const int *grp_idx, const int *slot, int H, int ng, float2 *B, int ny_out, int ldb, int cbc,
+                const float2 *tw, cudaStream_t st) {
     RFFT_DISPATCH(lg, {
         using Cf = Cfg<LG, true>;
         const size_t smem = Cf::smem + sizeof(float2) * (size_t)Cf::TPC * Cf::XB;
-        prep(rpass_bconv<LG>, smem);
-        rpass_bconv<LG><<<dim3((unsigned)cdiv(H, Cf::TPC), ng), Cf::THREADS, smem, st>>>(AU, ly, AV, ky, grp_off, grp_idx,
-                                                                                          slot, H, B, ny_out, tw);
+        const int grid = prep(rpass_bconv<LG>, Cf::THREADS, smem, cdiv(H, Cf::TPC) * (int64_t)ng);
+        rpass_bconv<LG><<<grid, Cf::THREADS, smem, st>>>(AU, ly, ldu, AV, ky, ldv, grp_off, grp_idx, slot, H, ng, B,
+                                                          ny_out, ldb, cbc, tw);
     });
     after_launch("rfft_pass_bconv");
 }
 
-void pass_c(int lg, const float2 *B, int oy, int H, int k, int ox, float inv, float *out, int64_t ldo,
-            const int *omap, const int *w, int64_t stride, const float2 *tw, cudaStream_t st) {
+void pass_c(int lg, const float2 *B, int oy, int ldb, int blocked, int H, int k, int ox, float inv, float *out,
+            int64_t ldo, const int *omap, const int *w, int64_t stride, const float2 *tw, cudaStream_t st) {
+    SSA_REQUIRE(ldb % 2 == 0 && ((uintptr_t)B & 15) == 0, SSA_ERR_ARG, "rfft pass C: rows must be 16-B aligned");
     RFFT_DISPATCH(lg, {
         using Cf = Cfg<LG>;
-        static_assert(2 * Cfg<LG>::H <= ((pad_size(1 << LG) + 1) & ~1), "column pair fits the exchange buffer");
-        prep(rpass_c<LG>, Cf::smem);
-        rpass_c<LG><<<dim3((unsigned)cdiv(oy, 2 * Cf::TPC), k), Cf::THREADS, Cf::smem, st>>>(B, oy, H, ox, inv, out, ldo,
-                                                                                             omap, w, stride, tw);
+        static_assert(2 * Cfg<LG>::H <= Cfg<LG>::XB, "column pair fits the exchange buffer");
+        const int grid = prep(rpass_c<LG>, Cf::THREADS, Cf::smem, cdiv(oy, 2 * Cf::TPC) * (int64_t)k);
+        rpass_c<LG><<<grid, Cf::THREADS, Cf::smem, st>>>(B, oy, ldb, blocked, H, k, ox, inv, out, ldo, omap, w, stride,
+                                                         tw);
     });
     after_launch("rfft_pass_c");
 }

@@ -60,6 +60,9 @@ struct PlanImpl {
     ~PlanImpl();
 };
 
+// the implementation behind an ABI handle (api.cu); throws SSA_ERR_CUDA for a broken plan
+PlanImpl &ssa_plan_impl(ssa_plan p);
+
 // product dispatch (api.cu)
 template <typename T>
 void op_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k);    // U = X V

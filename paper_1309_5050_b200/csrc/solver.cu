@@ -592,14 +592,19 @@ struct Gkl {
             }
         };
         t0 = now_ms();
+        // full reorthogonalisation of the K side as well (CGS2 against the whole K basis): the
+        // one-sided variant needed several times more products with thick restarts.
+        // The recurrence term is removed first by its own streaming update: folding it into the
+        // projection's Gram (WᵀW − CᵀC with the large recurrence part inside C) cancels catastrophically
+        // — squared norms, ε·||b||²/||w'||² — and broke convergence on c1-c3 (measured), whereas the
+        // vector subtraction loses only ε·||b||/||w'||
+        const T *againstK = Q(0);
+        const int naK = nQ;
         recurrence();
         tw_rec += now_ms() - t0;
         t0 = now_ms();
-        // full reorthogonalisation of the K side as well (CGS2 against the whole K basis): the
-        // one-sided variant needed several times more products with thick restarts
-        const T *againstK = Q(0);
-        const int naK = nQ;
         Alast = orth3(K, W, k, againstK, naK, true, nullptr);
+
         tw_orthB += now_ms() - t0;
         nQ += k;
     }

@@ -332,6 +332,65 @@ def test_contributions_pins():
         np.testing.assert_allclose(c[g], np.sum(oracle.trajmat(np.nan_to_num(r), sh) ** 2) / tx, rtol=1e-11)
 
 
+# ---------------------------------------------------------------- f2 / f3: ESPRIT, vector forecast
+def _match_pairs(lam, mu, lam0, mu0):
+    return max(min(abs(lam - a) + abs(mu - b)) for a, b in zip(lam0, mu0))
+
+
+@pytest.mark.parametrize("wmask_drop", [0, 5])
+def test_esprit_2d_recovers_closed_form_roots(wmask_drop):
+    """2D-ESPRIT: on a noiseless separable array (eq. P:4317-4320) the eigenarrays span the
+    exact signal subspace, so the jointly diagonalised shift matrices return the array's (λ_k, μ_k)
+    pairs (closed_form.roots) — also for a non-rectangular window (shifts only between cells of 𝔏)."""
+    rng = np.random.default_rng(3)
+    t = synth.draw_terms(rng, 2)
+    img = synth.separable_image(40, 37, t)
+    wm = None
+    if wmask_drop:
+        wm = np.ones((12, 10), bool)
+        wm[rng.choice(12, wmask_drop), rng.choice(10, wmask_drop)] = False
+        wm[0, 0] = True
+    sh = oracle.shapes(img, (12, 10), wmask=wm)
+    lam0, mu0, _ = cf.roots(t)
+    s, U, V, _ = oracle.svd_dense(img, sh, len(lam0))
+    lam, mu = oracle.esprit(sh, U)
+    assert _match_pairs(lam, mu, lam0, mu0) < 1e-9
+
+
+def test_esprit_1d_ls_roots():
+    """LS-ESPRIT for one series: the shift matrix's eigenvalues are the roots e^{α±2πiω} of a
+    sum of damped sines (Table-2-style finite-rank series, eq. P:4317-4320 in one dimension)."""
+    t = np.arange(400.0)
+    x = (np.exp(-0.002 * t) * np.cos(2 * np.pi * t / 23 + 0.5) + 0.7 * np.exp(0.001 * t) * np.sin(2 * np.pi * t / 9))
+    sh = oracle.shapes(x[:, None], (80, 1))
+    s, U, V, _ = oracle.svd_dense(x[:, None], sh, 4)
+    lam, _ = oracle.esprit(sh, U)
+    ref = np.array([np.exp(-0.002 + s_ * 2j * np.pi / 23) for s_ in (1, -1)] +
+                   [np.exp(0.001 + s_ * 2j * np.pi / 9) for s_ in (1, -1)])
+    assert max(min(abs(lam - r)) for r in ref) < 1e-10
+
+
+def test_vector_forecast_continues_finite_rank_series():
+    """Vector forecast: for noiseless finite-rank series whose signal subspace is the exact
+    span of the eigenvectors, the continued lagged vectors stay on the series' trajectory, so the forecast
+    equals the generator's continuation — for one series and for an MSSA system of series of unequal
+    length (NaN-padded 2-D packing; common subspace, per-series continuation)."""
+    def sig(t, c):
+        return (1 + 0.1 * c) * np.sin(2 * np.pi * t / 17 + 0.4 * c) + 0.5 * np.exp(-0.002 * t) * np.cos(2 * np.pi * t / 7)
+    M = 25
+    for lens in ([300], [300, 260, 280]):
+        N = max(lens)
+        x = np.full((N, len(lens)), np.nan)
+        for c, n in enumerate(lens):
+            x[:n, c] = sig(np.arange(n), c)
+        sh = oracle.shapes(x, (60, 1))
+        s, U, V, _ = oracle.svd_dense(np.nan_to_num(x), sh, 4)
+        f = oracle.vector_forecast(np.nan_to_num(x), sh, s, U, V, range(4), M)
+        for c, n in enumerate(lens):
+            np.testing.assert_allclose(f[:n + M, c], sig(np.arange(n + M), c), atol=1e-11)
+            assert np.all(np.isnan(f[n + M:, c]))
+
+
 def test_averaging_returns_rank_one_image_exactly():
     """P11: x = c·λ^i μ^j has 𝒯(𝕏) = c·a bᵀ; averaging c·a bᵀ returns 𝕏 on 𝔑′ (shaped)."""
     w = synth.small_shaped(seed=5, wmask_drop=3)
