@@ -49,7 +49,7 @@ def _traffic(config, product, path, k):
     try:
         with open(f) as fh:
             for e in json.load(fh)["entries"]:
-                if (e["config"], e["product"], e["path"], e["k"]) == (config, product, path, k):
+                if (e["config"], e["product"], e["path"]) == (config, product, path) and e.get("k", k) == k:
                     return e["traffic_bytes"]
     except (OSError, ValueError, KeyError):
         pass
@@ -293,8 +293,8 @@ def run_ours(args, rank, world, dist):
         r.update({"traffic": tr, "avg_launch_ms": avg_ms, "launches_per_step": nblocks / args.steps,
                   "share_of_step": ms_total / max(ms_local, 1e-9), "path": path})
         if tr is not None:
-            r["traffic_source"] = ("profiles/r01/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of "
-                                   "the block product's kernels, one ncu capture (cold caches)")
+            r["traffic_source"] = (TRAFFIC_FILE + ": dram__bytes_read.sum + dram__bytes_write.sum of the block "
+                                   "product's kernels, one ncu capture (cold caches)")
         return r
 
     prods = {}

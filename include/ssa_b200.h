@@ -75,6 +75,13 @@ typedef enum {
                               whose output box has < 256 rows fall back to FFT / direct) */
 } ssa_path;
 
+/* Decomposition method (the user's choice is always honoured). */
+typedef enum {
+    SSA_SVD_LANCZOS = 0,   /* block Golub-Kahan-Lanczos truncated SVD (default) */
+    SSA_SVD_EIGEN = 1      /* "eigen": S = XXᵀ by the fast products, full
+                              eigendecomposition of S (L <= 768); squares the condition number */
+} ssa_svd_method;
+
 typedef struct {
     int64_t nx, ny;        /* array size Nx x Ny (Ny = number of series for MSSA) */
     int64_t ld;            /* leading dimension >= nx; 0 means nx */
@@ -111,6 +118,7 @@ typedef struct {
     int precision;         /* arithmetic type of the plan: 0 = the input's dtype, 1 = fp32, 2 = fp64
                               (the input is cast once at plan creation); SSA_ERR_ARG otherwise */
     int64_t ny_global;     /* band plans: number of columns of the global image */
+    int svd_method;        /* ssa_svd_method (0 = Lanczos) */
 } ssa_opts;
 
 typedef struct {

@@ -38,7 +38,7 @@ class ssa_opts(C.Structure):
     _fields_ = [("stream", C.c_void_p), ("path", C.c_int), ("block_k", C.c_int), ("tol", C.c_double),
                 ("max_products", C.c_int), ("seed", C.c_uint64), ("comm", C.POINTER(ssa_comm)),
                 ("band_y0", C.c_int64), ("band_y1", C.c_int64), ("precision", C.c_int),
-                ("ny_global", C.c_int64)]
+                ("ny_global", C.c_int64), ("svd_method", C.c_int)]
 
 
 class ssa_plan_info_t(C.Structure):

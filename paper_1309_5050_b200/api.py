@@ -42,7 +42,7 @@ class Plan:
 
     def __init__(self, x, window, mask=None, wmask=None, *, dtype=None, path="auto", block_k=0,
                  tol=0.0, max_products=0, seed=0, stream=None, comm=None, band=None, ny_global=None,
-                 precision=None):
+                 precision=None, svd_method="lanczos"):
         """`comm`/`band`/`ny_global`: a band plan of the window-position partition (see
         dist.band_plan): x is this rank's sub-image = global columns [band[0], band[1] + Ly − 1)."""
         self._L = lib.load()
@@ -94,6 +94,7 @@ class Plan:
         o.seed = int(seed)
         # arithmetic type of the plan when it differs from the input's ("f32" / "f64")
         o.precision = {None: 0, "f32": 1, "f64": 2}[precision]
+        o.svd_method = {"lanczos": 0, "eigen": 1}[svd_method]
         if precision is not None:
             self.dtype = precision
             self._np_dtype = np.float64 if precision == "f64" else np.float32

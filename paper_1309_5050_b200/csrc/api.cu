@@ -677,6 +677,8 @@ ssa_status ssa_plan_create(const ssa_array *x, const ssa_window *w, const uint8_
     P.st = (cudaStream_t)o.stream;
     P.path = o.path;
     P.block_k = o.block_k > 0 ? o.block_k : (P.dt == SSA_F64 ? 16 : 32);
+    if (o.svd_method != SSA_SVD_LANCZOS && o.svd_method != SSA_SVD_EIGEN) throw Error(SSA_ERR_ARG, "bad svd_method");
+    P.svd_method = o.svd_method;
     P.tol = o.tol; P.max_products = o.max_products; P.seed = o.seed ? o.seed : 0x1309505000ull;
     if (o.comm && o.comm->world > 1) {
         // window-position band partition: x is this rank's sub-image, the global image
@@ -798,8 +800,14 @@ ssa_status ssa_decompose(ssa_plan p, int32_t r, ssa_decomp_info *info) {
     const auto t0 = std::chrono::steady_clock::now();
     ssa_status st = SSA_OK;
     try {
-        if (P.dt == SSA_F64) decompose<double>(P, r, inf);
-        else decompose<float>(P, r, inf);
+        if (P.svd_method == SSA_SVD_EIGEN) {
+            if (P.dt == SSA_F64) decompose_eigen<double>(P, r, inf);
+            else decompose_eigen<float>(P, r, inf);
+        } else if (P.dt == SSA_F64) {
+            decompose<double>(P, r, inf);
+        } else {
+            decompose<float>(P, r, inf);
+        }
     } catch (const Error &e) {
         if (e.code != SSA_ERR_NOT_CONVERGED) throw;
         g_err = e.what();

@@ -556,7 +556,7 @@ static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *o
     const int ldb = row_ld(oy), lda = row_ld(ny_in);
     if constexpr (sizeof(T) == 4) {
         if (f.rtw_x.p && !Afu) {
-            rfft::pass_c(f.lgx, reinterpret_cast<const float2 *>(B), oy, ldb, b_blocking(f) != 0, f.Hx, k, ox,
+            rfft::pass_c(f.lgx, reinterpret_cast<const float2 *>(B), oy, ldb, b_blocking(f), f.Hx, k, ox,
                          (float)(1.0 / ((double)f.Mx * (double)f.My)), out, ldo, omap, w, stride, f.rtw_x.as<float2>(),
                          st);
             return;
@@ -698,9 +698,9 @@ void fft_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k) {
 // absolute rounding error that is uniform over the grid (~ε·RMS of the numerator), and Alg. 4 then
 // divides by w_n: at the borders (w_n down to 1 at the corners, against w_max = |𝔏| in the bulk) the
 // relative error grows by w_max / w_n (c5 corners: ~1.5e-3 of the reconstruction's RMS in fp32,
-// measured).  Cells with w_n < w_max / 64 are therefore re-done by direct summation over their
-// w_n (ℓ, κ) pairs (fp64 accumulation): at most ~1.5e-6·RMS error left anywhere, for a few tens of
-// thousands of cells x w_n terms.
+// measured).  Cells with w_n < w_max / 1024 are therefore re-done by direct summation over their
+// w_n (ℓ, κ) pairs (fp64 accumulation): the error left elsewhere is ≲ 1.5e-3·RMS/64 ≈ 2.3e-5·RMS,
+// and the direct work stays small (c5: ~2k cells; at w_max / 64 it was ~50k cells and 4.4 ms).
 __global__ void low_weight_cells_kernel(const int *__restrict__ w, int64_t n, int thr, int *list, int *count) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const int wn = w[t];
@@ -785,7 +785,7 @@ void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, co
     const int64_t nxy = (int64_t)p.nx * p.ny;
     if (f.n_lowcells < 0) {
         const int wmax = (int)std::min<int64_t>(p.L, p.K);
-        const int thr = wmax / 64;
+        const int thr = wmax / 1024;
         f.n_lowcells = 0;
         if (thr > 1) {
             DevBuf cnt;

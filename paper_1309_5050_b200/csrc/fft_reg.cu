@@ -24,6 +24,7 @@
 //
 // Intermediate layouts are the ones of fft.cu (A[(j*H + fx)*by + col], B[(j*H + fx)*oy + y]), so a
 // pass can run either implementation.
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -422,7 +423,7 @@ rpass_bconv(const float2 *__restrict__ AU, int ly, int ldu, const float2 *__rest
 // item = (vector j, block of CB = 2·TPC output columns)
 template <int LG>
 __global__ void __launch_bounds__(Cfg<LG>::THREADS, Cfg<LG>::MINB)
-rpass_c(const float2 *__restrict__ B, int oy, int ldb, int blocked, int H, int k, int ox, float inv,
+rpass_c(const float2 *__restrict__ B, int oy, int ldb, int cblk, int H, int k, int ox, float inv,
         float *__restrict__ out, int64_t ldo, const int *__restrict__ omap, const int *__restrict__ w, int64_t stride,
         const float2 *__restrict__ twg) {
     using C = Cfg<LG>;
@@ -442,9 +443,19 @@ rpass_c(const float2 *__restrict__ B, int oy, int ldb, int blocked, int H, int k
         // 2q + 1 (at [H, 2H)); one 16-B load per (fx, column pair), consecutive threads -> consecutive
         // pairs of one fx; all of a thread's loads are issued before the shared-memory stores (the
         // per-element form was latency-bound: 5.3 ms for c5's Xᵀ·U pass C, ncu)
-        // row layout: rows of stride ldb; blocked layout: this item's H x CB block, contiguous
-        const float2 *bj = blocked ? B + (int64_t)it * H0 * CB : B + (int64_t)j * H0 * ldb + y0;
-        const int64_t rs = blocked ? CB : ldb;
+        // row layout: rows of stride ldb; blocked layout: this item's CB columns inside the H x cblk
+        // block that holds them (rows of stride cblk; the cblk/CB consecutive items of a block read
+        // the 32-B sectors of the same 128-B lines together)
+        const float2 *bj;
+        int64_t rs;
+        if (cblk) {
+            const int nyb = (oy + cblk - 1) / cblk, yb = y0 / cblk;
+            bj = B + ((int64_t)j * nyb + yb) * H0 * cblk + (y0 - yb * cblk);
+            rs = cblk;
+        } else {
+            bj = B + (int64_t)j * H0 * ldb + y0;
+            rs = ldb;
+        }
         float4 tmp[PER];
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
@@ -561,14 +572,20 @@ void pass_a(int lg, const float *in, int64_t ld, const int *map, int bx, int by,
     after_launch("rfft_pass_a");
 }
 
+// block width of the blocked B layout for a 2^lg-point pass C: its column group CB = 2·TPC.  (Blocks of
+// 16 columns — whole 128-B lines for pass B's writes, read as 32-B sectors by 4 consecutive pass-C
+// items — measured worse on c5's Xᵀ·U: pass B 3.8 ms / pass C 4.6 ms, against 4.0 / 3.1 ms here and
+// 2.9 / 5.3 ms for the row layout; ncu launch lists.)
 int cb_of(int lg) {
+    int cb = 0;
     switch (lg) {
-    case 8: return 2 * Cfg<8>::TPC;
-    case 9: return 2 * Cfg<9>::TPC;
-    case 10: return 2 * Cfg<10>::TPC;
-    case 11: return 2 * Cfg<11>::TPC;
-    default: return 2 * Cfg<12>::TPC;
+    case 8: cb = 2 * Cfg<8>::TPC; break;
+    case 9: cb = 2 * Cfg<9>::TPC; break;
+    case 10: cb = 2 * Cfg<10>::TPC; break;
+    case 11: cb = 2 * Cfg<11>::TPC; break;
+    default: cb = 2 * Cfg<12>::TPC; break;
     }
+    return cb;
 }
 
 void pass_b(int lg, const float2 *A, int ny_in, int lda, int H, int k, const float2 *Xh, float2 *B, int ny_out,
@@ -599,14 +616,15 @@ void pass_bconv(int lg, const float2 *AU, int ly, int ldu, const float2 *AV, int
     after_launch("rfft_pass_bconv");
 }
 
-void pass_c(int lg, const float2 *B, int oy, int ldb, int blocked, int H, int k, int ox, float inv, float *out,
+void pass_c(int lg, const float2 *B, int oy, int ldb, int cblk, int H, int k, int ox, float inv, float *out,
             int64_t ldo, const int *omap, const int *w, int64_t stride, const float2 *tw, cudaStream_t st) {
     SSA_REQUIRE(ldb % 2 == 0 && ((uintptr_t)B & 15) == 0, SSA_ERR_ARG, "rfft pass C: rows must be 16-B aligned");
     RFFT_DISPATCH(lg, {
         using Cf = Cfg<LG>;
         static_assert(2 * Cfg<LG>::H <= Cfg<LG>::XB, "column pair fits the exchange buffer");
         const int grid = prep(rpass_c<LG>, Cf::THREADS, Cf::smem, cdiv(oy, 2 * Cf::TPC) * (int64_t)k);
-        rpass_c<LG><<<grid, Cf::THREADS, Cf::smem, st>>>(B, oy, ldb, blocked, H, k, ox, inv, out, ldo, omap, w, stride,
+        SSA_REQUIRE(cblk == 0 || cblk % (2 * Cf::TPC) == 0, SSA_ERR_ARG, "rfft pass C: block width");
+        rpass_c<LG><<<grid, Cf::THREADS, Cf::smem, st>>>(B, oy, ldb, cblk, H, k, ox, inv, out, ldo, omap, w, stride,
                                                          tw);
     });
     after_launch("rfft_pass_c");

@@ -27,14 +27,14 @@ void pass_a(int lg, const float *in, int64_t ld, const int *map, int bx, int by,
 // cbc: layout of B (0 = rows of stride ldb; else blocked by pass C's column blocks of cbc = cb_of(lgx))
 void pass_b(int lg, const float2 *A, int ny_in, int lda, int H, int k, const float2 *Xh, float2 *B, int ny_out,
             int ldb, int cbc, const float2 *tw, cudaStream_t st);
-int cb_of(int lg);   // columns per pass-C work item of a 2^lg-point x transform
+int cb_of(int lg);   // block width of the blocked B layout for a 2^lg-point pass C
 // per (g, fx): B row = IDFT_y( Σ_{i∈I_g} DFT_y(AU_i row) ⊙ DFT_y(AV_i row) ), first ny_out entries
 void pass_bconv(int lg, const float2 *AU, int ly, int ldu, const float2 *AV, int ky, int ldv, const int *grp_off,
                 const int *grp_idx, const int *slot, int H, int ng, float2 *B, int ny_out, int ldb, int cbc,
                 const float2 *tw, cudaStream_t st);
 // per output column y < oy: Hermitian completion, inverse x-DFT (2^lg), rows x < ox, times inv;
 // products: out[omap(x, y) + ldo*j]; averaging (w != null): out[j*stride + x + ldo*y] = v / w (NaN if w = 0)
-void pass_c(int lg, const float2 *B, int oy, int ldb, int blocked, int H, int k, int ox, float inv, float *out,
+void pass_c(int lg, const float2 *B, int oy, int ldb, int cblk, int H, int k, int ox, float inv, float *out,
             int64_t ldo, const int *omap, const int *w, int64_t stride, const float2 *tw, cudaStream_t st);
 // Intermediate rows (A: by columns, B: oy columns) have strides lda / ldb = multiples of 4 complex
 // values (32-B aligned rows); the transposed accesses of passes A and C move 16-B column pairs.

@@ -19,6 +19,7 @@ struct PlanImpl {
     int path = SSA_PATH_DIRECT;   // requested path (AUTO resolved per product below)
     int path_xv = SSA_PATH_DIRECT, path_xtu = SSA_PATH_DIRECT;   // chosen per product
     int block_k = 32;
+    int svd_method = 0;           // SSA_SVD_LANCZOS / SSA_SVD_EIGEN
     double tol = 0;
     int max_products = 0;
     uint64_t seed = 0;
@@ -72,6 +73,9 @@ double *small_dev(PlanImpl &p, size_t n_doubles);
 
 // solver.cu
 double sigma_floor(const PlanImpl &p);   // reading Q10: measured σ floor τ of the plan's product paths
+// eigen.cu: svd.method = "eigen": S = XXᵀ by the fast products, full eigendecomposition
+template <typename T>
+void decompose_eigen(PlanImpl &p, int r, ssa_decomp_info *info);
 template <typename T>
 void decompose(PlanImpl &p, int r, ssa_decomp_info *info);
 

@@ -10,6 +10,9 @@ cfg = sys.argv[1]
 w = synth.get(cfg)
 p = Plan(w.data, w.window, mask=w.mask, wmask=w.wmask, dtype=w.dtype, block_k=w.block_k)
 p.decompose(w.r, allow_not_converged=True)      # warm-up (path autotune, lazy module loading)
+p.close()
+# a fresh plan: a second decomposition on the same plan would be warm-started from its eigenvectors
+p = Plan(w.data, w.window, mask=w.mask, wmask=w.wmask, dtype=w.dtype, block_k=w.block_k)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
 t = time.perf_counter()

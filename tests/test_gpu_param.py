@@ -109,3 +109,62 @@ def test_forecast_noiseless_unequal_series_fp64():
     for c, n in enumerate(lens):
         np.testing.assert_allclose(f[:n + M, c], sig(np.arange(n + M), c), atol=1e-9)
         assert np.all(np.isnan(f[n + M:, c]))
+
+
+# ------------------------------------------------------------------ f4: eigen variant, M-2D-SSA packing
+@pytest.mark.parametrize("path", ["direct", "fft"])
+def test_eigen_svd_method_c1_fp64(path):
+    """svd.method = "eigen": S = XXᵀ from the fast products, full eigendecomposition; on c1
+    (fp64, L = 256) σ, reconstructions and residuals against the oracle's dense SVD."""
+    w = synth.config1()
+    from paper_1309_5050_b200 import Plan
+    p = Plan(w.data, w.window, dtype="f64", path=path, svd_method="eigen")
+    x = np.array(w.data, np.float64)
+    sh = oracle.shapes(x, w.window)
+    s_or, U_or, V_or, _ = oracle.svd_dense(x, sh, 10)
+    info = p.decompose(10)
+    np.testing.assert_allclose(p.sigma, s_or, rtol=1e-10)
+    assert info["max_rel_residual"] <= 1e-9
+    recs = p.reconstruct(w.groups + [list(range(6))])
+    ref = oracle.reconstruct(x, sh, s_or, U_or, V_or, w.groups + [list(range(6))])
+    for a, b in zip(recs, ref):
+        assert relfro(a, b) <= 1e-9
+
+
+def test_eigen_svd_method_mssa_fp64():
+    """The eigen method on an MSSA system (8 series, L = 512, fp64) against the oracle."""
+    w = synth.config2(L=512)
+    from paper_1309_5050_b200 import Plan
+    p = Plan(w.data, w.window, dtype="f64", path="fft", svd_method="eigen")
+    x = np.array(w.data, np.float64)
+    sh = oracle.shapes(x, w.window)
+    s_or, _, _, _ = oracle.svd_dense(x, sh, 12)
+    p.decompose(12)
+    np.testing.assert_allclose(p.sigma, s_or, rtol=1e-9)
+
+
+@pytest.mark.parametrize("path", ["direct", "fft"])
+def test_m2dssa_packing(path):
+    """M-2D-SSA (eq. P:3499-3518) as a shaped array: two images side by side with a one-column NaN separator
+    (P:3512-3515); the decomposition is the SVD of [𝒯(𝕏¹) : 𝒯(𝕏²)] (the stacked trajectory matrices, formed
+    here from the oracle's trajmat of each image) and each image's reconstruction uses the common basis."""
+    rng = np.random.default_rng(71)
+    t = synth.draw_terms(rng, 2)
+    x1 = synth.separable_image(30, 25, t) + rng.normal(0, 0.2, (30, 25))
+    x2 = 0.7 * synth.separable_image(30, 25, t) + rng.normal(0, 0.2, (30, 25))
+    packed = np.concatenate([x1, np.full((30, 1), np.nan), x2], axis=1)
+    win = (6, 5)
+    from paper_1309_5050_b200 import Plan
+    p = Plan(packed, win, dtype="f64", path=path, block_k=8)
+    sh = oracle.shapes(packed, win)
+    T1 = oracle.trajmat(x1, oracle.shapes(x1, win))
+    T2 = oracle.trajmat(x2, oracle.shapes(x2, win))
+    s_stack = np.linalg.svd(np.hstack([T1, T2]), compute_uv=False)
+    assert p.K == T1.shape[1] + T2.shape[1]
+    p.decompose(6)
+    np.testing.assert_allclose(p.sigma, s_stack[:6], rtol=1e-9)
+    s_or, U_or, V_or, _ = oracle.svd_dense(np.nan_to_num(packed), sh, 6)
+    rec = p.reconstruct([[0, 1, 2, 3]])[0]
+    ref = oracle.reconstruct(np.nan_to_num(packed), sh, s_or, U_or, V_or, [[0, 1, 2, 3]])[0]
+    assert np.array_equal(np.isnan(rec), np.isnan(ref))
+    assert relfro(rec[~np.isnan(ref)], ref[~np.isnan(ref)]) <= 1e-9

@@ -391,6 +391,20 @@ def test_vector_forecast_continues_finite_rank_series():
             assert np.all(np.isnan(f[n + M:, c]))
 
 
+def test_m2dssa_packing_is_stacked_trajectory():
+    """P13-type packing equivalence for M-2D-SSA (eq. P:3499-3518): two arrays side by side with a one-column
+    NaN separator have the trajectory matrix [𝒯(𝕏¹) : 𝒯(𝕏²)] (no window straddles the
+    separator)."""
+    rng = np.random.default_rng(5)
+    x1, x2 = rng.normal(size=(9, 7)), rng.normal(size=(9, 7))
+    packed = np.concatenate([x1, np.full((9, 1), np.nan), x2], axis=1)
+    win = (3, 2)
+    T = oracle.trajmat(np.nan_to_num(packed), oracle.shapes(packed, win))
+    T1 = oracle.trajmat(x1, oracle.shapes(x1, win))
+    T2 = oracle.trajmat(x2, oracle.shapes(x2, win))
+    np.testing.assert_array_equal(T, np.hstack([T1, T2]))
+
+
 def test_averaging_returns_rank_one_image_exactly():
     """P11: x = c·λ^i μ^j has 𝒯(𝕏) = c·a bᵀ; averaging c·a bᵀ returns 𝕏 on 𝔑′ (shaped)."""
     w = synth.small_shaped(seed=5, wmask_drop=3)
