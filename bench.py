@@ -269,7 +269,8 @@ def run_ours(args, rank, world, dist):
             per_vec = esz * (K + L) + 2 * (2 * esz) * Hx * (ky_ + w.window[1])
             alg = kk * per_vec + (2 * esz) * Hx * My
             achieved = alg / (avg_ms / 1e3) / 1e9
-            r = {"bound": "hbm", "kernel": f"{name}: FFT correlation (fft_pass_a/b/c)", "achieved": achieved,
+            r = {"bound": "hbm", "kernel": f"{name}: FFT correlation (rpass_a/b/c register radix-16 passes)",
+                 "achieved": achieved,
                  "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)", "algorithmic_bytes_per_launch": alg}
         elif path == "tc":
@@ -307,7 +308,8 @@ def run_ours(args, rank, world, dist):
             prods[key] = rr
     roof = dict(max(prods.values(), key=lambda r: r["share_of_step"])) if prods else {}
     roof["note"] = ("a 'launch' is one block product of k vectors (FFT: 3 passes; tc: pack + MMA kernel"
-                    " + split reduce); events bracket it on the plan's stream, so host launch gaps count")
+                    " + split reduce); events bracket it on the plan's stream, so host launch gaps count; "
+                    "achieved = the 3-pass algorithmic bytes (DESIGN.md §6) / the average device time")
     roof["products"] = prods
     # where the rest of the step goes (the products are the kernels SURVEY §8(d) sizes; on the small
     # configs the Ritz SVD and the orthonormalisation take more of the step)

@@ -102,6 +102,27 @@ __global__ void weighted_sqrt_kernel(T *a, const int32_t *w, int64_t n, int ng) 
     }
 }
 
+// number of nonzero entries of a u8 mask or of an int32 array, on the device
+__global__ void count_nonzero_kernel(const uint8_t *m8, const int32_t *m32, int64_t n, unsigned long long *out) {
+    unsigned long long c = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        c += m8 ? (m8[t] != 0) : (m32[t] > 0);
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+static int64_t count_device(PlanImpl &p, const uint8_t *m8, const int32_t *m32, int64_t n) {
+    DevBuf d;
+    d.alloc(sizeof(unsigned long long), p.st);
+    SSA_CUDA(cudaMemsetAsync(d.p, 0, sizeof(unsigned long long), p.st));
+    count_nonzero_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 8 * num_sms()), 256, 0, p.st>>>(
+        m8, m32, n, d.as<unsigned long long>());
+    after_launch("count_nonzero");
+    unsigned long long h = 0;
+    SSA_CUDA(cudaMemcpyAsync(&h, d.p, sizeof(h), cudaMemcpyDeviceToHost, p.st));
+    SSA_CUDA(cudaStreamSynchronize(p.st));
+    return (int64_t)h;
+}
+
 // ---------------------------------------------------------------- products
 template <typename T>
 static CorrParams<T> base_corr(PlanImpl &p) {
@@ -326,11 +347,8 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
     p.nmask.alloc(nxy, st);
     prep_image<T>(src, ld, p.nx, p.ny, mask_host ? dmask.as<uint8_t>() : nullptr, p.img.as<T>(),
                   p.nmask.as<uint8_t>(), st);
-    std::vector<uint8_t> nm(nxy);
-    SSA_CUDA(cudaMemcpyAsync(nm.data(), p.nmask.p, nxy, cudaMemcpyDeviceToHost, st));
-    SSA_CUDA(cudaStreamSynchronize(st));
-    p.n_valid = 0;
-    for (int64_t t = 0; t < nxy; ++t) p.n_valid += nm[t];
+    // |𝔑| counted on the device (a host copy and loop over the 16.7M cells of c5 cost ~6 ms of the plan)
+    p.n_valid = count_device(p, p.nmask.as<uint8_t>(), nullptr, nxy);
 
     // 𝔏 map
     if (!p.full_window) {
@@ -418,11 +436,7 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
         DevBuf tmp;
         tmp.alloc(sizeof(int32_t) * (size_t)p.nx * p.ky, st);
         box_weights(p.kmask.as<uint8_t>(), p.nx, p.ny, p.lx, p.ly, p.weights.as<int32_t>(), tmp.as<int32_t>(), st);
-        std::vector<int32_t> wh(nxy);
-        SSA_CUDA(cudaMemcpyAsync(wh.data(), p.weights.p, sizeof(int32_t) * nxy, cudaMemcpyDeviceToHost, st));
-        SSA_CUDA(cudaStreamSynchronize(st));
-        int64_t np = 0;
-        for (int64_t t = 0; t < nxy; ++t) np += wh[t] > 0;
+        const int64_t np = count_device(p, nullptr, p.weights.as<int32_t>(), nxy);   // |𝔑′|
         p.n_excluded = p.n_valid - np;   // band plans: cells of the band's sub-image
     } else {
         DevBuf num, go, gi;
@@ -440,11 +454,7 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
         a.w = nullptr; a.out = num.as<T>(); a.ldout = p.nx; a.out_stride = nxy;
         diagsums_direct<T>(a, st);
         box_ones_to_int<T>(num.as<T>(), nxy, p.weights.as<int32_t>(), st);
-        std::vector<int32_t> wh(nxy);
-        SSA_CUDA(cudaMemcpyAsync(wh.data(), p.weights.p, sizeof(int32_t) * nxy, cudaMemcpyDeviceToHost, st));
-        SSA_CUDA(cudaStreamSynchronize(st));
-        int64_t np = 0;
-        for (int64_t t = 0; t < nxy; ++t) np += wh[t] > 0;
+        const int64_t np = count_device(p, nullptr, p.weights.as<int32_t>(), nxy);   // |𝔑′|
         p.n_excluded = p.n_valid - np;   // band plans: cells of the band's sub-image
     }
     // workspaces

@@ -124,6 +124,7 @@ struct Gkl {
     }
     int64_t n_fast = 0, n_fallback = 0;
     std::vector<double> res;      // residual bounds of the current Ritz triples
+    bool anorm_from_next_gram = false;
     double drop2 = 0.0;           // Σ squared norms of block columns discarded as numerically zero
     int warm_cols = 0;            // start-block columns taken from a previous decomposition
     DevBuf agree_buf;
@@ -277,6 +278,10 @@ struct Gkl {
         int refills = 0;
         for (int pass = 0; pass < 6; ++pass) {
             if (!have_gram) gram(M, W, LD(M), kc, W, LD(M), kc, G.data(), kside);
+            if (anorm_from_next_gram) {
+                anorm_from_next_gram = false;
+                for (int j = 0; j < kc; ++j) anorm = std::max(anorm, std::sqrt(std::max(G[j + (size_t)kc * j], 0.0)));
+            }
             have_gram = false;
             // exact breakdown: columns with (numerically) zero norm
             std::vector<int> zero;
@@ -574,11 +579,10 @@ struct Gkl {
         double t0 = now_ms();
         product_xtu(P(pc), W, k);
         tw_prod += now_ms() - t0;
-        if (anorm == 0.0) {
-            std::vector<double> G((size_t)k * k);
-            gram(K, W, ldQ, k, W, ldQ, k, G.data(), true);
-            for (int j = 0; j < k; ++j) anorm = std::max(anorm, std::sqrt(std::max(G[j + (size_t)k * j], 0.0)));
-        }
+        // ||X|| estimate = the largest column norm of the first Xᵀ·U block, taken from the first Gram of
+        // its orthonormalisation (na = 0: orth's pass-0 WᵀW) instead of a Gram of its own (a 3.8 GB
+        // stream on c5)
+        anorm_from_next_gram = anorm == 0.0;
         auto recurrence = [&]() {
             if (nQ > 0) {
                 // remove the recurrence term first (W -= Q_prev·Bᵀ with B = T[P_new, Q_prev], known
