@@ -159,9 +159,18 @@ class Plan:
             vv = v.reshape(nin, -1)
             k = vv.shape[1]
             vs = vv.to(td).t().contiguous()       # (k, nin) storage = column-major (nin, k)
-            o = torch.empty((k, nout), dtype=td, device=v.device) if out is None else out
+            if out is None:
+                o = torch.empty((k, nout), dtype=td, device=v.device)
+            else:
+                # the library writes k columns of nout values at out.data_ptr() (validate)
+                if not (_is_torch(out) and out.is_cuda and out.dtype == td and tuple(out.shape) == (k, nout)
+                        and out.is_contiguous() and out.device == v.device):
+                    raise ValueError(f"out must be a contiguous CUDA tensor of shape ({k}, {nout}) and dtype {td}")
+                o = out
             lib.check(self._L.ssa_matmul(self._h, int(transpose), vs.data_ptr(), nin, o.data_ptr(), nout, k, 1))
             return o.t()
+        if out is not None:
+            raise ValueError("out= is supported for CUDA tensor inputs only")
         va = np.asarray(v)
         squeeze = va.ndim == 1
         va = np.asfortranarray(va.reshape(nin, -1), dtype=self._np_dtype)

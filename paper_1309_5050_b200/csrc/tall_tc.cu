@@ -98,10 +98,11 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int raw_bytes = RC * unit;
     const int RS = min(tallg3::MAXR, C::ring / raw_bytes);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // chunks interleaved over the CTAs (chunk = blockIdx.x + i·gridDim.x): the grid then streams one
+    // contiguous run of ~148·32·RC rows of every column at a time; with a contiguous chunk range per
+    // CTA the DRAM saw (CTAs x columns) separate 128-B streams (c5 K side: 1.8-2.8 TB/s, ncu)
     const int64_t nchunks = (M + 32 * RC - 1) / (32 * RC);
-    const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
-    const int64_t c0 = (int64_t)blockIdx.x * per;
-    const int nmy = (int)max((int64_t)0, min(per, nchunks - c0));
+    const int nmy = (int)max((int64_t)0, (nchunks - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x);
     const int col0 = (int)blockIdx.y * NM * 128;
 
     if (tid == 0) {
@@ -145,7 +146,7 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 mbar_expect_tx(full(r), raw_bytes);
 #pragma unroll
                 for (int rc = 0; rc < RC; ++rc) {
-                    const int r0 = (int)((c0 + i) * 32 * RC + 32 * rc);
+                    const int r0 = (int)(((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * 32 * RC + 32 * rc);
 #pragma unroll
                     for (int mt = 0; mt < NM; ++mt)
                         tma_load_2d_true(dst + rc * unit + mt * BA * 128, &tmA, r0, col0 + 128 * mt, full(r));
@@ -367,10 +368,10 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
     const int BS = bres ? nchk : max(2, min(tallu2::BRING, (Cf::off_bar - 3 * Cf::a_raw) / Cf::b_bytes));
     const int off_raw = BS * Cf::b_bytes;
     const int RS = min(tallu2::MAXR, (Cf::off_bar - off_raw) / Cf::a_raw);
+    // tiles interleaved over the CTAs (tile = blockIdx.x + i·gridDim.x), as in the Gram: the grid
+    // streams one contiguous run of rows of all m columns at a time (DRAM page locality)
     const int64_t ntiles = (M + tallu2::ROWS - 1) / tallu2::ROWS;
-    const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-    const int64_t t0 = (int64_t)blockIdx.x * per;
-    const int64_t mytiles = max((int64_t)0, min(per, ntiles - t0));
+    const int64_t mytiles = max((int64_t)0, (ntiles - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x);
     const int nitems = (int)(mytiles * nchk);
 
     if (tid == 0) {
@@ -413,7 +414,7 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
             for (int i = 0; i < nitems; ++i) {
                 const int r = i % RS;
                 if (i >= RS) mbar_wait(rawe(r), ((i / RS) - 1) & 1);
-                const int64_t tile = t0 + i / nchk;
+                const int64_t tile = (int64_t)blockIdx.x + (int64_t)(i / nchk) * gridDim.x;
                 mbar_expect_tx(fulla(r), Cf::a_raw);
                 tma_load_2d_true(raw(r), &tmA, (int)(tile * tallu2::ROWS), (i % nchk) * KC, fulla(r));
             }
@@ -511,7 +512,7 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
         float old[32];
         for (int i = 0; i < nitems; ++i) {
             const int b = i % NBUF;
-            const int64_t row = (t0 + i / nchk) * tallu2::ROWS + (warp & 3) * 32 + lane;
+            const int64_t row = ((int64_t)blockIdx.x + (int64_t)(i / nchk) * gridDim.x) * tallu2::ROWS + (warp & 3) * 32 + lane;
             if (i % nchk == 0) {
                 // the tile's old output values, loaded a whole tile ahead of the epilogue (their
                 // latency used to stall the drain, and with it the MMAs, once per tile); in place
