@@ -772,7 +772,16 @@ extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32
                                      double *check) {
     using namespace ssa;
     try {
-        if (M < 1 || n1 < 1 || n1 > 512 || n2 < 1 || n2 > 64 || reps < 1 || which < 0 || which > 3 || which == 2)
+        // probe: n1 = columns + 1000 x L2-prefetch distance (stages), n2 = rows per box (32: swizzled)
+        const int pd = which == 4 ? (n1 >= 0 ? n1 / 1000 : -((-n1) / 1000)) : 0, prow = std::abs(n2);
+        if (which == 4 && n1 < 0) n1 = -n1;
+        const bool pswz = n2 == 32;
+        if (which == 4) {
+            n1 %= 1000;
+            n2 = std::min(prow, 64);
+            if (n1 < 1 || n1 > 128 || prow < 8 || prow > 256) throw Error(SSA_ERR_ARG, "ssa_bench_tall: bad probe sizes");
+        }
+        if (M < 1 || n1 < 1 || n1 > 512 || n2 < 1 || n2 > 64 || reps < 1 || which < 0 || which > 4 || which == 2)
             throw Error(SSA_ERR_ARG, "ssa_bench_tall: bad sizes");
         const int64_t ld = (M + 31) / 32 * 32;
         DevBuf a, b, g, ws, c;
@@ -792,6 +801,8 @@ extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32
         auto run = [&]() {
             if (which == 0) gram_tn<float>(M, a.as<float>(), ld, n1, b.as<float>(), ld, n2, g.as<double>(), ws.as<double>(), wsb, nullptr);
             else if (which == 3) gram_tn<float>(M, a.as<float>(), ld, n1, a.as<float>(), ld, n2, g.as<double>(), ws.as<double>(), wsb, nullptr);
+            // probe: n1 columns, n2 = rows per box (32: 128-B swizzled boxes, else unswizzled), 128 rows per stage
+            else if (which == 4) tma_stream_probe(M, a.as<float>(), ld, n1, prow, std::max(1, 128 / prow), pswz, pd, nullptr);
             else gemm_acc<float>(M, a.as<float>(), ld, n1, c.as<double>(), n1, n2, -1.0, 1.0, b.as<float>(), ld, nullptr);
         };
         run();

@@ -105,8 +105,7 @@ hankel_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant_
     constexpr int NP = C::NP, W = C::W, VB = C::VB;
     extern __shared__ unsigned char smem_raw[];
     // 1024-B alignment for the swizzled B tiles
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *smem = smem_align1024(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::off_bar);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 24);
     const uint32_t bar0 = smem_u32(bars);

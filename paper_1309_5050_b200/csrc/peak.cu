@@ -12,7 +12,7 @@ namespace ssa {
 __global__ void __launch_bounds__(128, 1) mma_peak_kernel(int iters, int *sink) {
     using namespace tc;
     extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *smem = smem_align1024(smem_raw);
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 48 * 1024);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 1);
     const int warp = threadIdx.x >> 5;

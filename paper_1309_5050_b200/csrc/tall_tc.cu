@@ -22,6 +22,7 @@
 // warps so the split of chunk c+2, the MMAs of c+1 and the drain of c overlap.  Per-CTA fp64 partials are summed by gram_reduce_kernel in a
 // fixed order (deterministic).  Accuracy: 3xTF32 products (~2^-21 relative per term)
 // and one fp32 truncation per 8-row partial, comparable to the fp32 FFMA Gram.
+#include <type_traits>
 #include <map>
 #include <tuple>
 
@@ -82,8 +83,7 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     using C = tallg3::Cfg<NM, NN, BA, RC, KG>;
     constexpr int KS = C::KS, KA = C::KA, OPB = C::OPB, AB = C::ACCB;
     extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *smem = smem_align1024(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::off_bar);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 64);
     const uint32_t bar0 = smem_u32(bars);
@@ -313,6 +313,243 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 }
 
 // ---------------------------------------------------------------------------
+// Self Gram WᵀW (n <= 64 columns, the CholeskyQR Gram of the K-side blocks): hi and lo stacked on the
+// M dimension.  With the truncating split h = x & ~0x1fff (exact tf32), l = x − h, the tensor core's
+// own reading of the fp32 data as tf32 is h, so the data tile itself is the B operand (no split of B).
+// One MMA per 8-row k-step, A = [h; l] (TMEM lanes 0..NC−1: h of column c, lanes NC..2NC−1: l of c):
+//     D = [ hᵀh ; lᵀh ]   and   WᵀW = hᵀh + lᵀh + (lᵀh)ᵀ  (dropping lᵀl, as 3xTF32 does),
+// combined by gram_reduce_stacked.  (The 3xTF32 form spent three 128-row MMAs per k-step on 64 useful
+// rows and split every B element: ~2.6k cycles per 64-row stage, 1.9 TB/s on c5's K side, ncu.)
+// Loads: TMA boxes of ROWS = 128 rows x NC columns, unswizzled (512 B per column: a probe streamed
+// 128-B-wide boxes, the 128-B-swizzle limit, at 4.6 TB/s and >= 256-B-wide ones at 6.4 TB/s,
+// scripts/probe_tma.py); warps 2-7 copy each landed stage into the canonical K-major 128-B-swizzled
+// B tile (ROWS/32 sub-tiles of 32 rows), then warps 4-7 (one per TMEM lane quarter) read it back conflict-free and split A into
+// TMEM (a separate 2-warp relayout stage was the bottleneck: 1.2 ms, ncu); warp 1 issues; warps 8-15 drain one accumulator per PAIR stages (64·PAIR rows:
+// the accumulator read-back, 32 KB per drain, is the drain's cost) into Kahan-compensated fp32 sums.  Buffers: RS staging slots, OPB B tiles / TMEM A buffers, ACCB
+// accumulators.
+// ---------------------------------------------------------------------------
+namespace tallgs {
+constexpr int ACCB = 4, NTHR = 512;
+constexpr int SMEM = 226 * 1024;
+}  // namespace tallgs
+
+template <int NC, int ROWS, int PAIR>
+__global__ void __launch_bounds__(tallgs::NTHR, 1)
+gram_self_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, double *__restrict__ partials) {
+    using namespace tc;
+    constexpr int STAGE = NC * ROWS * 4;              // bytes per stage (raw [c][ROWS] or B [ROWS/32][c][32])
+    constexpr int OPB = 256 / ROWS < 4 ? 256 / ROWS : 4, AB = tallgs::ACCB;
+    constexpr int RS = (128 * 1024) / STAGE < 8 ? (128 * 1024) / STAGE : 8;
+    constexpr int NSUB = ROWS / 32;                   // 32-row sub-tiles per stage
+    constexpr int CPC = ROWS / 4;                     // 16-B chunks per column and stage
+    constexpr int SUB = NC * 128;                     // one 32-row sub-tile of B
+    constexpr int off_b = RS * STAGE;
+    constexpr int off_bar = off_b + OPB * STAGE;
+    constexpr int NCONV = (2 * NC) / 32;              // converter warps (one per TMEM lane quarter)
+    static_assert(off_bar + 1024 <= tallgs::SMEM - 1024, "shared memory budget");
+    static_assert(AB * NC <= 256 && OPB * ROWS <= 256, "TMEM budget");
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = smem_align1024(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + off_bar);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 64);
+    const uint32_t bar0 = smem_u32(bars);
+    auto full = [&](int r) { return bar0 + 8u * r; };             // raw stage landed       [8]
+    auto rawe = [&](int r) { return bar0 + 8u * (8 + r); };       // raw stage copied       [8]
+    auto bful = [&](int o) { return bar0 + 8u * (16 + o); };      // B tile o written       [4]
+    auto conv = [&](int o) { return bar0 + 8u * (20 + o); };      // A buffer o split       [4]
+    auto ope = [&](int o) { return bar0 + 8u * (24 + o); };       // MMAs of B / A o done   [4]
+    auto accf = [&](int b) { return bar0 + 8u * (28 + b); };      // accumulator ready      [4]
+    auto acce = [&](int b) { return bar0 + 8u * (32 + b); };      // accumulator drained    [4]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t nst = (M + ROWS - 1) / ROWS;
+    const int nmy = (int)max((int64_t)0, (nst - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x);
+
+    if (tid == 0) {
+        for (int r = 0; r < RS; ++r) {
+            mbar_init(full(r), 1);
+            mbar_init(rawe(r), 1);
+        }
+        for (int o = 0; o < OPB; ++o) {
+            mbar_init(bful(o), 1);
+            mbar_init(conv(o), NCONV);
+            mbar_init(ope(o), 1);
+        }
+        for (int b = 0; b < AB; ++b) {
+            mbar_init(accf(b), 1);
+            mbar_init(acce(b), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sm_u = smem_u32(smem);
+    auto a_col = [&](int o) { return (uint32_t)(256 + o * ROWS); };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < nmy; ++i) {
+                const int r = i % RS;
+                if (i >= RS) mbar_wait(rawe(r), ((i / RS) - 1) & 1);
+                mbar_expect_tx(full(r), STAGE);
+                const int r0 = (int)(((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * ROWS);
+                tma_load_2d_true(sm_u + r * STAGE, &tmA, r0, 0, full(r));
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // accumulator g = i / PAIR collects PAIR stages (64·PAIR rows)
+            constexpr uint32_t idesc = make_idesc(128, NC);
+            for (int i = 0; i < nmy; ++i) {
+                const int o = i % OPB, g = i / PAIR, b = g % AB, first = (i % PAIR) == 0;
+                const bool last = (i % PAIR) == PAIR - 1 || i == nmy - 1;
+                mbar_wait(bful(o), (i / OPB) & 1);
+                mbar_wait(conv(o), (i / OPB) & 1);
+                if (first && g >= AB) mbar_wait(acce(b), ((g / AB) - 1) & 1);
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(b * NC), a = tmem + a_col(o);
+#pragma unroll
+                for (int rc = 0; rc < NSUB; ++rc) {
+                    const uint64_t bd = make_desc(sm_u + off_b + o * STAGE + rc * SUB);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        mma_tf32_ts(d, a + 32 * rc + 8 * q, bd + (uint64_t)(2 * q), idesc, (first && !(rc | q)) ? 0u : 1u);
+                }
+                mma_commit(ope(o));
+                if (last) mma_commit(accf(b));
+            }
+        }
+    } else if (warp < 8) {
+        // warps 2-7: relayout raw [c][64 rows] (16 chunks of 16 B per column) -> B tile [rc][c][32 rows],
+        // 128-B swizzle (all loads of a thread before its stores); named barrier; then warps 4-7 split
+        // the A operand (lane m: column c = m mod NC, hi for m < NC, else lo) from the B tile into TMEM
+        const int t = tid - 64;
+        constexpr int PER = (NC * CPC + 191) / 192;
+        const int q = warp & 3, m = 32 * q + lane, c = m % NC;
+        const bool conv_warp = warp >= 4 && 32 * q < 2 * NC, lo_part = m >= NC;
+        const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+        for (int i = 0; i < nmy; ++i) {
+            const int r = i % RS, o = i % OPB;
+            mbar_wait(full(r), (i / RS) & 1);
+            if (i >= OPB) mbar_wait(ope(o), ((i / OPB) - 1) & 1);
+            const float4 *src = reinterpret_cast<const float4 *>(smem + r * STAGE);
+            unsigned char *dst = smem + off_b + o * STAGE;
+            float4 x[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k)
+                if (t + 192 * k < NC * CPC) x[k] = src[t + 192 * k];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int e = t + 192 * k;
+                if (e < NC * CPC) {
+                    const int cc = e / CPC, j = e % CPC, rc = j >> 3, jj = j & 7;
+                    *reinterpret_cast<float4 *>(dst + rc * SUB + cc * 128 + ((jj ^ (cc & 7)) << 4)) = x[k];
+                }
+            }
+            fence_proxy_async();   // the MMAs read the tile through the async proxy
+            asm volatile("bar.sync 1, 192;" ::: "memory");
+            if (t == 0) {
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rawe(r)) : "memory");
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bful(o)) : "memory");
+            }
+            if (conv_warp) {
+                tc_fence_after();
+                auto split = [&](auto lo_tag) {
+#pragma unroll
+                    for (int rc = 0; rc < NSUB; ++rc) {
+                        const unsigned char *row = smem + off_b + o * STAGE + rc * SUB + c * 128;
+                        uint32_t v[32];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float4 y = *reinterpret_cast<const float4 *>(row + ((j ^ (c & 7)) << 4));
+                            const float ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t h = __float_as_uint(ys[u]) & 0xffffe000u;
+                                v[4 * j + u] = decltype(lo_tag)::value ? __float_as_uint(ys[u] - __uint_as_float(h)) : h;
+                            }
+                        }
+                        tmem_st32(tmem + lane_off + a_col(o) + 32 * rc, v);
+                    }
+                };
+                if (lo_part) split(std::true_type{});
+                else split(std::false_type{});
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv(o)) : "memory");
+            }
+        }
+    } else if (warp >= 8) {
+        // warp w: TMEM lanes 32·(w mod 4).., accumulator columns 32·((w − 8) / 4)..
+        const int qd = warp & 3, h = (warp - 8) >> 2;
+        const bool has = 32 * qd < 2 * NC && 32 * h < NC;
+        float ks[32], kc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) { ks[j] = 0.f; kc[j] = 0.f; }
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(32 * h);
+        const int nacc = (nmy + PAIR - 1) / PAIR;
+        for (int i = 0; i < nacc; ++i) {
+            const int b = i % AB;
+            mbar_wait(accf(b), (i / AB) & 1);
+            tc_fence_after();
+            float v[32];
+            if (has) tmem_ld32(lane_base + (uint32_t)(b * NC), v);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
+            if (has) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float y = v[j] - kc[j];
+                    const float u = ks[j] + y;
+                    kc[j] = (u - ks[j]) - y;
+                    ks[j] = u;
+                }
+            }
+        }
+        if (has) {
+            // partial rows a' = TMEM lane (0..2NC−1), columns b = 32h + j, 64 x 64 slabs as gram_reduce reads them
+            const int a = 32 * qd + lane;
+            double *base = partials + ((int64_t)(a / 64) * gridDim.x + blockIdx.x) * 4096 + (a % 64);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) base[64 * (32 * h + j)] = (double)ks[j] - (double)kc[j];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512) : "memory");
+}
+
+// G (n x n) = S(a, b) + S(NC + a, b) + S(NC + b, a), S = the stacked partial sums [hᵀh; lᵀh] (2NC x NC)
+__global__ void gram_reduce_stacked_kernel(const double *__restrict__ partials, int nparts, int nc, int n,
+                                           double *__restrict__ G) {
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+    if (e >= n * n) return;
+    const int a = e % n, b = e / n;
+    auto S = [&](int ap, int bp) {
+        const double *base = partials + (int64_t)(ap / 64) * nparts * 4096 + (ap % 64) + 64 * bp;
+        double s = 0.0;
+        for (int q = lane; q < nparts; q += 32) s += base[(int64_t)q * 4096];
+        return s;
+    };
+    double s = S(a, b) + (S(nc + a, b) + S(nc + b, a));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) G[a + (int64_t)n * b] = s;
+}
+
+// ---------------------------------------------------------------------------
 // Update v2 (default): Out = beta·Out + A·(alpha·C) with the A operand in tensor memory.  The
 // contraction runs over A's columns, so an A row (one output row) is one TMEM lane: converter
 // warps 4-7 read the landed raw tile [32 columns][128 rows] (plain TMA box, no swizzle: a warp
@@ -321,7 +558,11 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 // pre-split coefficient tiles (B = (alpha·C)ᵀ chunk, K-major SW128 images) are bulk-copied from L2
 // by warp 2 into OPB slots that the MMAs release.  Per (tile, chunk) one fresh accumulator: the
 // small terms A_lo·B_hi, A_hi·B_lo of the 4 k-steps first, then the exact A_hi·B_hi products.
-// Drain / epilogue: fp32 register sums across chunks, read-modify-write of the tile.
+// Drain / epilogue: fp32 register sums across chunks; at the tile's end each drain warp stages its
+// 32 x 32 piece in shared memory and one lane issues a tensor store of it (beta = 0) or an add-reduce
+// at L2 (beta = 1: Out += A·C without reading Out into the SM).  The register read-modify-write with
+// 32 scalar loads / stores per thread and tile (other beta) had put half of the kernel's instructions
+// and its top stalls in the epilogue (c5 K side: 3.0 ms = 3.8 TB/s for Out −= A·C, ncu).
 // ---------------------------------------------------------------------------
 namespace tallu2 {
 constexpr int ROWS = 128, KC = 64, OPB = 2, NBUF = 4, MAXR = 12, MAXB = 24, NTHR = 512;   // KC: A columns per item
@@ -333,20 +574,20 @@ struct Cfg {
     static constexpr int a_raw = ROWS * KC * 4;             // 32 KB
     static constexpr int b_bytes = 2 * NN * KC * 4;         // two packed 32-column chunks, each hi | lo
     static constexpr int off_bar = SMEM - 2048;
+    static constexpr int off_stage = off_bar - 8 * 4096;    // epilogue staging: 32 x 32 fp32 per drain warp
     static_assert(NBUF * NN <= 256 && OPB * 2 * KC <= 256, "TMEM budget");
 };
 }  // namespace tallu2
 
 template <int NN>
 __global__ void __launch_bounds__(tallu2::NTHR, 1)
-update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, const float *__restrict__ Bpk, int n,
-                  double beta, float *Out, int64_t ldo) {
+update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmO, int omode, int64_t M,
+                  int m, const float *__restrict__ Bpk, int n, double beta, float *Out, int64_t ldo) {
     using namespace tc;
     using Cf = tallu2::Cfg<NN>;
     constexpr int OPB = tallu2::OPB, NBUF = tallu2::NBUF, KC = tallu2::KC;
     extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *smem = smem_align1024(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + Cf::off_bar);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 96);   // after the 88 barriers
     const uint32_t bar0 = smem_u32(bars);
@@ -365,9 +606,9 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
     // else a ring of BRING slots that runs ahead of the MMAs (a per-item reload from L2 tied to
     // the A buffers had put the L2 latency on the item cadence)
     const bool bres = nchk * Cf::b_bytes <= tallu2::BRES && nchk <= tallu2::MAXB;
-    const int BS = bres ? nchk : max(2, min(tallu2::BRING, (Cf::off_bar - 3 * Cf::a_raw) / Cf::b_bytes));
+    const int BS = bres ? nchk : max(2, min(tallu2::BRING, (Cf::off_stage - 3 * Cf::a_raw) / Cf::b_bytes));
     const int off_raw = BS * Cf::b_bytes;
-    const int RS = min(tallu2::MAXR, (Cf::off_bar - off_raw) / Cf::a_raw);
+    const int RS = min(tallu2::MAXR, (Cf::off_stage - off_raw) / Cf::a_raw);
     // tiles interleaved over the CTAs (tile = blockIdx.x + i·gridDim.x), as in the Gram: the grid
     // streams one contiguous run of rows of all m columns at a time (DRAM page locality)
     const int64_t ntiles = (M + tallu2::ROWS - 1) / tallu2::ROWS;
@@ -393,6 +634,7 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        if (omode) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmO)) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -510,10 +752,11 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
         const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(32 * h);
         const float fb = (float)beta;
         float old[32];
+        float *stg = reinterpret_cast<float *>(smem + Cf::off_stage + (warp - 8) * 4096);   // [col][row], 32 x 32
         for (int i = 0; i < nitems; ++i) {
             const int b = i % NBUF;
             const int64_t row = ((int64_t)blockIdx.x + (int64_t)(i / nchk) * gridDim.x) * tallu2::ROWS + (warp & 3) * 32 + lane;
-            if (i % nchk == 0) {
+            if (i % nchk == 0 && !omode) {
                 // the tile's old output values, loaded a whole tile ahead of the epilogue (their
                 // latency used to stall the drain, and with it the MMAs, once per tile); in place
                 // (Out = A) is safe: these rows are written only by this thread, at the tile's end
@@ -534,7 +777,20 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
             tc_fence_before();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce(b)) : "memory");
-            if (i % nchk == nchk - 1) {
+            if (i % nchk == nchk - 1 && omode) {
+                if (has) {
+                    if (lane == 0) bulk_wait_read0();   // this warp's previous store has read the staging
+                    __syncwarp();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) stg[32 * j + lane] = acc[j];
+                    fence_proxy_async();
+                    __syncwarp();
+                    const int64_t row0 = row - lane;
+                    if (lane == 0 && row0 < M) tma_store_2d(&tmO, smem_u32(stg), (int)row0, 32 * h, omode);
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+            } else if (i % nchk == nchk - 1) {
                 if (has && row < M) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
@@ -546,11 +802,83 @@ update_tc2_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, int m, con
                 for (int j = 0; j < 32; ++j) acc[j] = 0.f;
             }
         }
+        if (omode && lane == 0) bulk_wait0();   // stores complete before the staging is released
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512) : "memory");
+}
+
+// Streaming probe (measurement only, ssa_bench_tall which = 4): TMA loads of an M x n block in stages
+// of `boxes` boxes of [brow rows x n columns] through a ring, released as soon as they land.  Separates
+// the DRAM / TMA side of the tall kernels from their compute pipelines.
+__global__ void __launch_bounds__(64, 1)
+tma_stream_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmp, int pd, int64_t M,
+                  int brow, int boxes, int box_bytes, int ring) {
+    using namespace tc;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = smem_align1024(smem_raw);
+    const int stage = boxes * box_bytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)ring * stage);
+    const uint32_t bar0 = smem_u32(bars);
+    auto full = [&](int r) { return bar0 + 8u * r; };
+    auto emp = [&](int r) { return bar0 + 8u * (32 + r); };
+    const int64_t rows = (int64_t)brow * boxes;
+    const int64_t nst = (M + rows - 1) / rows;
+    const int nmy = (int)max((int64_t)0, (nst - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x);
+    if (threadIdx.x == 0) {
+        for (int r = 0; r < ring; ++r) { mbar_init(full(r), 1); mbar_init(emp(r), 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nmy; ++i) {
+            const int r = i % ring;
+            if (i >= ring) mbar_wait(emp(r), ((i / ring) - 1) & 1);
+            mbar_expect_tx(full(r), stage);
+            const int r0 = (int)(((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * rows);
+            if (pd > 0) {   // L2 prefetch of stage i + pd in one 128-row box per stage
+                const int64_t rp = ((int64_t)blockIdx.x + (int64_t)(i + pd) * gridDim.x) * rows;
+                if (rp < M)
+                    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
+                                 ::"l"(reinterpret_cast<uint64_t>(&tmp)), "r"((int)rp), "r"(0) : "memory");
+            }
+            if (pd < 0) {   // 3D views: -1: box {32 rows, boxes row blocks, n cols}; -2: box {32 rows, n cols, boxes}
+                for (int b = 0; b < boxes; b += 4) {
+                    if (pd == -1) tma_load_2d(smem_u32(smem) + r * stage + b * box_bytes, &tm, 0, r0 / 32 + b, 0, full(r));
+                    else tma_load_2d(smem_u32(smem) + r * stage + b * box_bytes, &tm, 0, 0, r0 / 32 + b, full(r));
+                }
+            } else {
+                for (int b = 0; b < boxes; ++b)
+                    tma_load_2d_true(smem_u32(smem) + r * stage + b * box_bytes, &tm, r0 + brow * b, 0, full(r));
+            }
+        }
+    } else if (threadIdx.x == 32) {
+        for (int i = 0; i < nmy; ++i) {
+            const int r = i % ring;
+            mbar_wait(full(r), (i / ring) & 1);
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(emp(r)) : "memory");
+        }
+    }
+    __syncthreads();
+}
+
+void tma_stream_probe(int64_t M, const float *A, int64_t lda, int n, int brow, int boxes, bool swz, int pd, cudaStream_t st) {
+    const CUtensorMap m =
+        pd == -1 ? make_map3(A, 32, (uint64_t)(M / 32), (uint64_t)n, 128, (uint64_t)lda * 4, 32, 4, (uint32_t)n, true,
+                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)
+        : pd == -2 ? make_map3(A, 32, (uint64_t)n, (uint64_t)(M / 32), (uint64_t)lda * 4, 128, 32, (uint32_t)n, 4, true,
+                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)
+                   : make_map2(A, (uint64_t)M, (uint64_t)n, (uint64_t)lda * 4, (uint32_t)brow, (uint32_t)n, swz,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    const CUtensorMap mp = make_map2(A, (uint64_t)M, (uint64_t)n, (uint64_t)lda * 4, (uint32_t)(brow * boxes), (uint32_t)n,
+                                     false, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    const int box_bytes = brow * n * 4, stage = boxes * box_bytes;
+    const int ring = std::min(32, (200 * 1024) / stage);
+    set_max_smem(tma_stream_kernel);
+    tma_stream_kernel<<<num_sms(), 64, ring * stage + 2048, st>>>(m, mp, pd, M, brow, boxes, box_bytes, ring);
+    after_launch("tma_stream");
 }
 
 // tensor maps cached per (pointer, rows, columns, ld, box columns)
@@ -620,10 +948,25 @@ static void launch_update_tc2(const float *A, int64_t lda, int64_t M, int m, con
     if (bpk.bytes < need) bpk.alloc(need, st);
     coef_pack_kernel<NN><<<nchk, 256, 0, st>>>(m, C, ldc, n, alpha, bpk.as<float>());
     after_launch("coef_pack");
+    // epilogue: tensor store (beta = 0) / add-reduce (beta = 1) when Out's layout allows a tensor map
+    const int omode = ((beta == 0.0 || beta == 1.0) && !(ldo & 3) && !((uintptr_t)Out & 15) && ldo >= M && M <= INT32_MAX)
+                          ? (beta == 0.0 ? 1 : 2) : 0;
+    const CUtensorMap *mo = &it->second;
+    if (omode) {
+        static thread_local std::map<Key, CUtensorMap> ocache;
+        const Key okey{Out, M, n, ldo};
+        auto jt = ocache.find(okey);
+        if (jt == ocache.end()) {
+            if (ocache.size() > 256) ocache.clear();
+            jt = ocache.emplace(okey, make_map2(Out, (uint64_t)M, (uint64_t)n, (uint64_t)ldo * 4, 32, 32, false,
+                                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B)).first;
+        }
+        mo = &jt->second;
+    }
     auto kern = update_tc2_kernel<NN>;
     set_max_smem(kern);
     const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallu2::ROWS));
-    kern<<<ctas, tallu2::NTHR, tallu2::SMEM, st>>>(it->second, M, m, bpk.as<float>(), n, beta, Out, ldo);
+    kern<<<ctas, tallu2::NTHR, tallu2::SMEM, st>>>(it->second, *mo, omode, M, m, bpk.as<float>(), n, beta, Out, ldo);
     after_launch("update_tc2");
 }
 
@@ -651,6 +994,35 @@ bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int
         ((uintptr_t)B & 15) || M > INT32_MAX)
         return false;
     const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallg::R));
+    static const int self_mode = [] { const char *e = std::getenv("SSA_GRAM_SELF"); return e ? std::atoi(e) : 1; }();
+    if (self_mode && B == A && ldb == lda && n2 == n1 && n1 <= 64 && !(lda & 31) && !((uintptr_t)A & 127) &&
+        (size_t)ctas * 4096 * sizeof(double) * 2 <= partial_bytes) {
+        // self Gram WᵀW: hi / lo stacked on M, one MMA per k-step (gram_self_kernel)
+        const int nc = n1 <= 32 ? 32 : 64;
+        constexpr int self_rows = 128;
+        // unswizzled boxes of self_rows rows x nc columns (the kernel relayouts them for the MMA)
+        using Key = std::tuple<const float *, int64_t, int, int64_t, int>;
+        static thread_local std::map<Key, CUtensorMap> cache;
+        const Key key{A, M, n1, lda, nc * 1000 + self_rows};
+        auto it = cache.find(key);
+        if (it == cache.end()) {
+            if (cache.size() > 256) cache.clear();
+            it = cache.emplace(key, make_map2(A, (uint64_t)M, (uint64_t)n1, (uint64_t)lda * 4, self_rows, (uint32_t)nc,
+                                              false, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)).first;
+        }
+        auto go = [&](auto kern) {
+            set_max_smem(kern);
+            kern<<<ctas, tallgs::NTHR, tallgs::SMEM, st>>>(it->second, M, partials);
+        };
+        // one accumulator per 256 rows (32 k-steps of fp32 tensor-core accumulation, then Kahan sums)
+        // (64-row stages with 4 per accumulator: 882 µs vs 806 µs at c5's K side)
+        if (nc == 32) go(gram_self_kernel<32, self_rows, 2>);
+        else go(gram_self_kernel<64, self_rows, 2>);
+        after_launch("gram_self");
+        gram_reduce_stacked_kernel<<<(unsigned)cdiv((int64_t)n1 * n1 * 32, 256), 256, 0, st>>>(partials, ctas, nc, n1, G);
+        after_launch("gram_reduce_stacked");
+        return true;
+    }
     if ((size_t)ctas * 4096 * sizeof(double) * (size_t)cdiv(n1, 64) > partial_bytes) return false;
     // narrow blocks (n1 <= 64, e.g. the CholeskyQR Gram WᵀW): a 64-column A box, B read from the A tile
     if (n2 <= 32) {

@@ -1,0 +1,2 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
+for m in 1 2; do echo "mode $m"; SSA_GRAM_SELF=$m timeout 600 python -m pytest tests/test_gpu_tall.py -q -x -k self 2>&1 | tail -1; SSA_GRAM_SELF=$m timeout 300 python scripts/bench_tall_c5.py 2>&1 | head -1; done
