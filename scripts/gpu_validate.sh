@@ -1,0 +1,24 @@
+#!/bin/bash
+# Round validation on one B200 (run through gpurun from the repo root):
+#   build, smoke, bench c5 (default) + c1..c4, the GPU test suite, and the c5 ncu launch list.
+# Usage: bash scripts/gpu_validate.sh <tag> [quick]
+tag=${1:-val}; out=gpurun_out/$tag; mkdir -p $out
+python -c "import __graft_entry__ as g; g.build()" > $out/build.log 2>&1 || { tail -20 $out/build.log; exit 1; }
+python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1; tail -1 $out/smoke.log
+timeout 900 python bench.py > $out/bench_c5.json 2> $out/bench_c5.err
+python - "$out" <<'P'
+import json, sys
+d = json.loads(open(sys.argv[1] + '/bench_c5.json').read().strip().splitlines()[-1])
+print({k: d.get(k) for k in ('value', 'ms_per_step', 'rank_r_time_ms')}, d.get('phases_device_ms'),
+      d['roofline']['frac'], d['roofline'].get('traffic'), d['roofline'].get('step_shares'))
+P
+for c in c1 c2 c3 c4; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline > $out/bench_$c.json 2> $out/bench_$c.err
+  python -c "import json; d=json.loads(open('$out/bench_$c.json').read().strip().splitlines()[-1]); print('$c', d['ms_per_step'], d.get('rank_r_time_ms'), d['roofline']['frac'])"
+done
+[ "$2" = quick ] && exit 0
+timeout 2400 python -m pytest tests -m gpu -q --timeout 900 > $out/pytest_gpu.log 2>&1
+tail -3 $out/pytest_gpu.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $out/launches_bench_c5.csv \
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $out/ncu_bench.log 2>&1
+python scripts/launch_summary.py $out/launches_bench_c5.csv > $out/launches_bench_c5.summary.txt 2>&1; head -12 $out/launches_bench_c5.summary.txt
