@@ -253,7 +253,8 @@ ssa_status ssa_small_svd(int32_t m, int32_t n, double *A, int32_t *sweeps, doubl
  * *check = max relative error against an fp64 host evaluation (update: on ~1000 sampled
  * rows; Gram: all entries when M·n1·n2 <= 5e8, else the checksum Σ|G|).  which = 3 times
  * the self Gram AᵀA[:, :n2]; which = 4 times a TMA streaming probe of n1 <= 128 columns in
- * boxes of |n2| rows (n2 = 32: 128-B swizzled, else unswizzled; 128 rows per stage or one box).
+ * boxes of |n2| rows (n2 = 32: 128-B swizzled, else unswizzled; 128 rows per stage or one box);
+ * which = 5 times the projection Gram AᵀB with B = the last n2 columns of A (n2 <= n1).
  * SSA_ERR_ARG on bad sizes. */
 ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32_t n2, int32_t reps, double *ms,
                           double *check);

@@ -162,15 +162,20 @@ static void tc_dispatch(PlanImpl &p, bool xv, const T *in, int64_t ldi, T *out, 
 }
 
 template <typename T>
-void op_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k) {
-    if (p.path_xtu == SSA_PATH_FFT && p.fft) { fft_xtu<T>(p, U, ldu, V, ldv, k); return; }
-    if (p.path_xtu == SSA_PATH_TC) { tc_dispatch<T>(p, false, U, ldu, V, ldv, k); return; }
+void op_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k, const double *cs) {
+    if (p.path_xtu == SSA_PATH_FFT && p.fft) { fft_xtu<T>(p, U, ldu, V, ldv, k, cs); return; }
+    if (p.path_xtu == SSA_PATH_TC) {
+        tc_dispatch<T>(p, false, U, ldu, V, ldv, k);
+        if (cs) scale_columns<T>(p.K, V, ldv, k, cs, p.st);
+        return;
+    }
     CorrParams<T> c = base_corr<T>(p);
     c.ox = p.kx; c.oy = p.ky; c.dx = p.lx; c.dy = p.ly;
     c.W = U; c.ldw = ldu; c.wmap = p.full_window ? nullptr : p.lmap.as<int>();
     c.out = V; c.ldo = ldv; c.omap = p.full_k ? nullptr : p.kmap.as<int>();
     c.k = k;
     corr_direct<T>(c, p.ws_corr.as<T>(), p.ws_corr_bytes, p.st);
+    if (cs) scale_columns<T>(p.K, V, ldv, k, cs, p.st);
 }
 
 template <typename T>
@@ -196,8 +201,8 @@ void op_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k) {
             throw Error(SSA_ERR_COMM, "allreduce of X·V partials failed");
     }
 }
-template void op_xtu<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int);
-template void op_xtu<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int);
+template void op_xtu<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int, const double *);
+template void op_xtu<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int, const double *);
 template void op_xv<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int);
 template void op_xv<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int);
 
@@ -488,8 +493,7 @@ static void get_v(PlanImpl &p, const std::vector<int> *need = nullptr) {
         double *d = small_dev(p, std::max(nm, 1));
         SSA_CUDA(cudaMemcpyAsync(d, inv.data(), sizeof(double) * nm, cudaMemcpyHostToDevice, p.st));
         if (nm == p.r) {
-            op_xtu<T>(p, p.U.as<T>(), p.L, p.V.as<T>(), p.K, p.r);
-            scale_columns<T>(p.K, p.V.as<T>(), p.K, p.r, d, p.st);
+            op_xtu<T>(p, p.U.as<T>(), p.L, p.V.as<T>(), p.K, p.r, d);   // ÷σ inside the product
         } else {
             DevBuf ut, vt;
             ut.alloc(sizeof(T) * p.L * nm, p.st);
@@ -497,8 +501,7 @@ static void get_v(PlanImpl &p, const std::vector<int> *need = nullptr) {
             for (int t = 0; t < nm; ++t)
                 SSA_CUDA(cudaMemcpyAsync(ut.as<T>() + p.L * t, p.U.as<T>() + p.L * miss[t], sizeof(T) * p.L,
                                          cudaMemcpyDeviceToDevice, p.st));
-            op_xtu<T>(p, ut.as<T>(), p.L, vt.as<T>(), p.K, nm);
-            scale_columns<T>(p.K, vt.as<T>(), p.K, nm, d, p.st);
+            op_xtu<T>(p, ut.as<T>(), p.L, vt.as<T>(), p.K, nm, d);
             for (int t = 0; t < nm; ++t)
                 SSA_CUDA(cudaMemcpyAsync(p.V.as<T>() + p.K * miss[t], vt.as<T>() + p.K * t, sizeof(T) * p.K,
                                          cudaMemcpyDeviceToDevice, p.st));

@@ -781,7 +781,8 @@ extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32
             n2 = std::min(prow, 64);
             if (n1 < 1 || n1 > 128 || prow < 8 || prow > 256) throw Error(SSA_ERR_ARG, "ssa_bench_tall: bad probe sizes");
         }
-        if (M < 1 || n1 < 1 || n1 > 512 || n2 < 1 || n2 > 64 || reps < 1 || which < 0 || which > 4 || which == 2)
+        if (M < 1 || n1 < 1 || n1 > 512 || n2 < 1 || n2 > 64 || reps < 1 || which < 0 || which > 5 || which == 2 ||
+            (which == 5 && n2 > n1))
             throw Error(SSA_ERR_ARG, "ssa_bench_tall: bad sizes");
         const int64_t ld = (M + 31) / 32 * 32;
         DevBuf a, b, g, ws, c;
@@ -801,6 +802,8 @@ extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32
         auto run = [&]() {
             if (which == 0) gram_tn<float>(M, a.as<float>(), ld, n1, b.as<float>(), ld, n2, g.as<double>(), ws.as<double>(), wsb, nullptr);
             else if (which == 3) gram_tn<float>(M, a.as<float>(), ld, n1, a.as<float>(), ld, n2, g.as<double>(), ws.as<double>(), wsb, nullptr);
+            // projection Gram [A W]ᵀW of the solver: B = the last n2 columns of A (read from A's tiles)
+            else if (which == 5) gram_tn<float>(M, a.as<float>(), ld, n1, a.as<float>() + ld * (n1 - n2), ld, n2, g.as<double>(), ws.as<double>(), wsb, nullptr);
             // probe: n1 columns, n2 = rows per box (32: 128-B swizzled boxes, else unswizzled), 128 rows per stage
             else if (which == 4) tma_stream_probe(M, a.as<float>(), ld, n1, prow, std::max(1, 128 / prow), pswz, pd, nullptr);
             else gemm_acc<float>(M, a.as<float>(), ld, n1, c.as<double>(), n1, n2, -1.0, 1.0, b.as<float>(), ld, nullptr);
@@ -836,7 +839,7 @@ extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32
             *check = emax / std::max(ref_max, 1e-300);
         } else if (check) {
             double s = 0.0;
-            if (which == 0 || which == 3) {
+            if (which == 0 || which == 3 || which == 5) {
                 std::vector<double> hg((size_t)n1 * n2);
                 SSA_CUDA(cudaMemcpy(hg.data(), g.p, sizeof(double) * hg.size(), cudaMemcpyDeviceToHost));
                 if ((double)M * n1 * n2 <= 5e8) {
@@ -844,12 +847,13 @@ extern "C" ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32
                     std::vector<float> ha((size_t)ld * n1), hb((size_t)ld * n2);
                     SSA_CUDA(cudaMemcpy(ha.data(), a.p, sizeof(float) * ha.size(), cudaMemcpyDeviceToHost));
                     SSA_CUDA(cudaMemcpy(hb.data(), b.p, sizeof(float) * hb.size(), cudaMemcpyDeviceToHost));
-                    const std::vector<float> &hB = (which == 3) ? ha : hb;
+                    const std::vector<float> &hB = (which == 3 || which == 5) ? ha : hb;
+                    const int64_t bo = (which == 5) ? (int64_t)(n1 - n2) * ld : 0;
                     double emax = 0.0, gmax = 0.0;
                     for (int j = 0; j < n2; ++j)
                         for (int i = 0; i < n1; ++i) {
                             double v = 0.0;
-                            for (int64_t r = 0; r < M; ++r) v += (double)ha[r + ld * i] * (double)hB[r + ld * j];
+                            for (int64_t r = 0; r < M; ++r) v += (double)ha[r + ld * i] * (double)hB[bo + r + ld * j];
                             emax = std::max(emax, std::fabs(v - hg[i + (size_t)n1 * j]));
                             gmax = std::max(gmax, std::fabs(v));
                         }

@@ -551,14 +551,16 @@ static void pass_b(FftOperator &f, const cplx<T> *A, int ny_in, int k, int mode,
 }
 
 template <typename T>
+// cs (products only): per-column factors; applied here by the register pass, else by scale_columns
 static void pass_c(FftOperator &f, const cplx<T> *B, int oy, int k, int ox, T *out, int64_t ldo, const int *omap,
-                   const int *w, int64_t stride, cudaStream_t st, const cplx<T> *Afu = nullptr, int ny_in = 0) {
+                   const int *w, int64_t stride, cudaStream_t st, const cplx<T> *Afu = nullptr, int ny_in = 0,
+                   const double *cs = nullptr) {
     const int ldb = row_ld(oy), lda = row_ld(ny_in);
     if constexpr (sizeof(T) == 4) {
         if (f.rtw_x.p && !Afu) {
             rfft::pass_c(f.lgx, reinterpret_cast<const float2 *>(B), oy, ldb, b_blocking(f), f.Hx, k, ox,
                          (float)(1.0 / ((double)f.Mx * (double)f.My)), out, ldo, omap, w, stride, f.rtw_x.as<float2>(),
-                         st);
+                         st, cs);
             return;
         }
     }
@@ -662,7 +664,7 @@ void fft_build(PlanImpl &p) {
 // out box (ox x oy) <- correlation of the image with the input box (bx x by)
 template <typename T>
 static void correlate(PlanImpl &p, const T *in, int64_t ldin, const int *imap, int bx, int by, T *out, int64_t ldo,
-                      const int *omap, int ox, int oy, int k) {
+                      const int *omap, int ox, int oy, int k, int64_t nout = 0, const double *cs = nullptr) {
     FftOperator &f = *p.fft;
     for (int j0 = 0; j0 < k; j0 += 64) {
         const int kc = std::min(64, k - j0);
@@ -675,8 +677,13 @@ static void correlate(PlanImpl &p, const T *in, int64_t ldin, const int *imap, i
             pass_c<T>(f, nullptr, oy, kc, ox, out + ldo * j0, ldo, omap, nullptr, 0, p.st, f.bufA.as<cplx<T>>(), by);
         } else {
             pass_b<T>(f, f.bufA.as<cplx<T>>(), by, kc, 0, f.bufB.as<cplx<T>>(), oy, p.st);
-            pass_c<T>(f, f.bufB.as<cplx<T>>(), oy, kc, ox, out + ldo * j0, ldo, omap, nullptr, 0, p.st);
+            const bool reg = sizeof(T) == 4 && f.rtw_x.p;
+            pass_c<T>(f, f.bufB.as<cplx<T>>(), oy, kc, ox, out + ldo * j0, ldo, omap, nullptr, 0, p.st, nullptr, 0,
+                      (cs && reg) ? cs + j0 : nullptr);
+            if (cs && !reg) scale_columns<T>(nout, out + ldo * j0, ldo, kc, cs + j0, p.st);
+            continue;
         }
+        if (cs) scale_columns<T>(nout, out + ldo * j0, ldo, kc, cs + j0, p.st);
     }
 }
 
@@ -687,9 +694,9 @@ void fft_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k) {
 }
 
 template <typename T>
-void fft_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k) {
+void fft_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k, const double *cs) {
     correlate<T>(p, U, ldu, p.full_window ? nullptr : p.lmap.as<int>(), p.lx, p.ly, V, ldv,
-                 p.full_k ? nullptr : p.kmap.as<int>(), p.kx, p.ky, k);
+                 p.full_k ? nullptr : p.kmap.as<int>(), p.kx, p.ky, k, p.K, cs);
 }
 
 // Grouped averaging via FFT: out_g = IDFT2(Σ_{i∈I_g} σ_i Ψ̂_i Φ̂_i) / 𝕎 (NaN off 𝔑′).
@@ -812,8 +819,8 @@ void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, co
 
 template void fft_xv<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int);
 template void fft_xv<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int);
-template void fft_xtu<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int);
-template void fft_xtu<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int);
+template void fft_xtu<float>(PlanImpl &, const float *, int64_t, float *, int64_t, int, const double *);
+template void fft_xtu<double>(PlanImpl &, const double *, int64_t, double *, int64_t, int, const double *);
 template void fft_diagsums<float>(PlanImpl &, const float *, const float *, const double *, const int *, const int *,
                                   int, const std::vector<int> &, const int *, float *, const int *);
 template void fft_diagsums<double>(PlanImpl &, const double *, const double *, const double *, const int *, const int *,

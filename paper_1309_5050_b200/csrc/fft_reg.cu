@@ -26,6 +26,7 @@
 // pass can run either implementation.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -144,22 +145,33 @@ template <int NT, int RP, int NSP> __device__ __forceinline__ void exchange(floa
         const int j = t + NT * b;
         const int k = j & (NSP - 1);
         const int base = (j - k) * RP + k;
+        if constexpr (NSP % 16 == 0 || (NSP == 1 && RP == 16)) {
+            // pad(base + NSP·r) = pad(base) + (NSP + NSP/16)·r (NSP·r a multiple of 16, or r < 16 = RP with
+            // base a multiple of 16)
+            const unsigned pb = (unsigned)base + ((unsigned)base >> 4);
 #pragma unroll
-        for (int r = 0; r < RP; ++r) S[pad(base + NSP * r)] = v[b + B * r];
+            for (int r = 0; r < RP; ++r) S[pb + (NSP + NSP / 16) * r] = v[b + B * r];
+        } else {
+#pragma unroll
+            for (int r = 0; r < RP; ++r) S[pad(base + NSP * r)] = v[b + B * r];
+        }
     }
     xsync<NT>();
+    // pad(t + NT·e) = (t + t/16) + (NT + NT/16)·e for NT % 16 == 0: one base register and immediate
+    // offsets (the signed form cost two address instructions per element, ncu SASS of pass B)
+    const float2 *Sr = S + ((unsigned)t + ((unsigned)t >> 4));
 #pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = S[pad(t + NT * e)];
+    for (int e = 0; e < 16; ++e) v[e] = Sr[(NT + NT / 16) * e];
     xsync<NT>();
 }
 
 // KEEP1: only the outputs X[t] (e = 0) are needed (pass B of X·V keeps the first Ly <= NT rows):
 // the last stage then forms just the r = 0 output of its 16-point DFT, Σ_r twiddled inputs
-template <int LG, int DIR, int RP, int NSP, bool KEEP1>
+template <int LG, int DIR, int RP, int NSP, bool KEEP1, bool SKIPX = false>
 __device__ __forceinline__ void stages16(float2 *v, float2 *S, const float2 *__restrict__ tw, int t) {
     constexpr int N = 1 << LG, NT = N >> 4, NS = NSP * RP;
     if constexpr (NS < N) {
-        exchange<NT, RP, NSP>(v, S, t);
+        if constexpr (!SKIPX) exchange<NT, RP, NSP>(v, S, t);
         const int k = t & (NS - 1);
         const float2 *w = tw + (NS - r0_of(LG)) + 15 * k;   // table of span NS starts at NS − R0
 #pragma unroll
@@ -317,19 +329,33 @@ rpass_a(const float *__restrict__ in, int64_t ld, const int *__restrict__ map, i
 
 // ------------------------------------------------------------------------------------ pass B
 // item = (vector j, block of TPC rows fx); the k items that use the same X̂ rows are consecutive
-// (X̂ stays in L2 while the much larger A stream passes)
-template <int LG, bool KEEP1>
+// (X̂ stays in L2 while the much larger A stream passes).
+// TRIVL (R0 = 16 and ny_in <= NT: Xᵀ·U, whose input rows hold only Ly nonzero entries): stage 0 of
+// every butterfly would just replicate its one nonzero input, so the row is loaded directly in the
+// layout the first exchange produces, v[e] = x[t/16 + (NT/16)·e], and the transform starts at the
+// span-16 stage (one exchange and one stage less).  The B stores use per-thread base addresses and
+// a constant stride per e (the per-element index arithmetic with a division by the block width was
+// ~35% of the Xᵀ·U pass-B instructions, ncu SASS, profiles/r02).
+template <int LG, bool KEEP1, bool TRIVL>
 __global__ void __launch_bounds__(Cfg<LG, true>::THREADS, Cfg<LG, true>::MINB)
 rpass_b(const float2 *__restrict__ A, int ny_in, int lda, int H, int k, const float2 *__restrict__ Xh,
         float2 *__restrict__ B, int ny_out, int ldb, int cbc, const float2 *__restrict__ twg) {
     using C = Cfg<LG, true>;
     constexpr int N = C::N, NT = C::NT, TPC = C::TPC, B0 = 16 / r0_of(LG);
+    static_assert(!TRIVL || r0_of(LG) == 16, "direct exchanged-layout load needs a radix-16 stage 0");
     extern __shared__ float2 sm[];
     const float2 *tw = stage_tw<LG>(sm, twg);
     const int q = threadIdx.x / NT, t = threadIdx.x % NT;
     float2 *S = xbuf<LG>(sm, q);
     const int items = k * ((H + TPC - 1) / TPC);
     const bool triv = ny_in <= NT * B0;
+    const bool full_in = t + NT * 15 < ny_in;
+    // B addressing, y = t + NT·e: fixed base per (j, fx) and a constant stride es per e
+    const int nyb = cbc ? (ny_out + cbc - 1) / cbc : 0;
+    const bool fastst = cbc == 0 || NT % cbc == 0;
+    const int tq = cbc ? t / cbc : 0, tr = cbc ? t - tq * cbc : t;
+    const int64_t es = cbc ? (int64_t)(NT / max(cbc, 1)) * H * cbc : NT;
+    const int ne = t < ny_out ? min(16, (ny_out - t + NT - 1) / NT) : 0;
     __syncthreads();
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
         const int j = it % k;
@@ -337,27 +363,156 @@ rpass_b(const float2 *__restrict__ A, int ny_in, int lda, int H, int k, const fl
         const bool ok = fx < H;
         const float2 *arow = A + ((int64_t)j * H + (ok ? fx : 0)) * lda;
         float2 v[16];
+        if constexpr (TRIVL) {
+            const int t16 = t >> 4;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int y = t + NT * e;
-            v[e] = (ok && y < ny_in) ? arow[y] : make_float2(0.f, 0.f);
+            for (int e = 0; e < 16; ++e) {
+                const int y = t16 + (NT / 16) * e;
+                v[e] = (ok && y < ny_in) ? arow[y] : make_float2(0.f, 0.f);
+            }
+            stages16<LG, -1, 16, 1, false, true>(v, S, tw, t);
+        } else {
+            if (ok && full_in) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = arow[t + NT * e];
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const int y = t + NT * e;
+                    v[e] = (ok && y < ny_in) ? arow[y] : make_float2(0.f, 0.f);
+                }
+            }
+            fft<LG, -1>(v, S, tw, t, triv);
         }
-        fft<LG, -1>(v, S, tw, t, triv);
         const float2 *xr = Xh + (int64_t)(ok ? fx : 0) * N;
 #pragma unroll
         for (int e = 0; e < 16; ++e) v[e] = cmulc(__ldg(xr + t + NT * e), v[e]);   // X̂ ⊙ conj(Â)
-        const int nyb = cbc ? (ny_out + cbc - 1) / cbc : 0;
         if constexpr (KEEP1) {   // X·V: only the first Ly <= NT rows of the inverse are kept
             fft<LG, +1, true>(v, S, tw, t, false);
             if (ok && t < ny_out) B[boff(j, fx, t, H, ldb, cbc, nyb)] = v[0];
         } else {
             fft<LG, +1>(v, S, tw, t, false);
+            if (ok && fastst) {
+                float2 *bp = B + (cbc ? ((((int64_t)j * nyb + tq) * H + fx) * cbc + tr)
+                                      : (((int64_t)j * H + fx) * ldb + t));
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    if (e < ne) bp[e * es] = v[e];
+            } else if (ok) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const int y = t + NT * e;
+                    if (y < ny_out) B[boff(j, fx, y, H, ldb, cbc, nyb)] = v[e];
+                }
+            }
+        }
+    }
+}
+
+// Pass B, X̂-resident form (work unit = one row fx and a chunk of JC vectors): the X̂ row is copied
+// into shared memory once per unit (cp.async, overlapped with the unit's first forward transform)
+// instead of 16 dependent L2 loads per thread and item after the forward transform (the top stall
+// of rpass_b on c5's Xᵀ·U: long scoreboard, ncu); A rows of the next item are loaded into registers
+// while the current item's inverse transform runs.  Shared memory per CTA: twiddles + exchange
+// buffer + X̂ row (~100 KB at 2^12 points: 2 CTAs / SM, up to 128 registers per thread).
+template <int LG> struct CfgB2 {
+    static constexpr int N = 1 << LG, NT = N / 16, THREADS = NT;
+    static constexpr size_t smem = Cfg<LG, true>::smem + sizeof(float2) * (size_t)N;
+};
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int LG, bool KEEP1, bool TRIVL, int JC>
+__global__ void __launch_bounds__(CfgB2<LG>::THREADS, 2)
+rpass_b2(const float2 *__restrict__ A, int ny_in, int lda, int H, int k, const float2 *__restrict__ Xh,
+         float2 *__restrict__ B, int ny_out, int ldb, int cbc, const float2 *__restrict__ twg) {
+    using C = Cfg<LG, true>;
+    constexpr int N = C::N, NT = C::NT, B0 = 16 / r0_of(LG);
+    static_assert(C::TPC == 1, "one transform per CTA");
+    static_assert(!TRIVL || r0_of(LG) == 16, "direct exchanged-layout load needs a radix-16 stage 0");
+    extern __shared__ float2 sm[];
+    const float2 *tw = stage_tw<LG>(sm, twg);
+    float2 *S = xbuf<LG>(sm, 0);
+    float2 *Xs = sm + C::TWP + C::XB;                    // X̂ row of the current unit
+    const int t = threadIdx.x;
+    const int nch = (k + JC - 1) / JC, units = H * nch;
+    const bool triv = ny_in <= NT * B0;
+    const bool full_in = t + NT * 15 < ny_in;
+    const int nyb = cbc ? (ny_out + cbc - 1) / cbc : 0;
+    const bool fastst = cbc == 0 || NT % cbc == 0;
+    const int tq = cbc ? t / cbc : 0, tr = cbc ? t - tq * cbc : t;
+    const int64_t es = cbc ? (int64_t)(NT / max(cbc, 1)) * H * cbc : NT;
+    const int ne = t < ny_out ? min(16, (ny_out - t + NT - 1) / NT) : 0;
+    auto load_row = [&](float2 *v, int j, int fx) {
+        const float2 *arow = A + ((int64_t)j * H + fx) * lda;
+        if constexpr (TRIVL) {
+            const int t16 = t >> 4;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int y = t16 + (NT / 16) * e;
+                v[e] = y < ny_in ? __ldg(arow + y) : make_float2(0.f, 0.f);
+            }
+        } else if (full_in) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = __ldg(arow + t + NT * e);
+        } else {
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
                 const int y = t + NT * e;
-                if (ok && y < ny_out) B[boff(j, fx, y, H, ldb, cbc, nyb)] = v[e];
+                v[e] = y < ny_in ? __ldg(arow + y) : make_float2(0.f, 0.f);
             }
         }
+    };
+    __syncthreads();   // twiddle table staged
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int fx = u / nch, j0 = (u - fx * nch) * JC, j1 = min(k, j0 + JC);
+        // X̂ row -> shared memory (16 B per copy; the previous unit's readers are past a barrier)
+        {
+            const float2 *xr = Xh + (int64_t)fx * N;
+            for (int i = t; i < N / 2; i += NT) cp_async16(Xs + 2 * i, xr + 2 * i);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        float2 v[16];
+        load_row(v, j0, fx);
+        bool xs_ready = false;
+        for (int j = j0; j < j1; ++j) {
+            if constexpr (TRIVL) stages16<LG, -1, 16, 1, false, true>(v, S, tw, t);
+            else fft<LG, -1>(v, S, tw, t, triv);
+            if (!xs_ready) {   // the first forward transform covered the copy's latency
+                cp_async_wait_all();
+                __syncthreads();
+                xs_ready = true;
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = cmulc(Xs[t + NT * e], v[e]);   // X̂ ⊙ conj(Â)
+            float2 vn[16];
+            if (j + 1 < j1) load_row(vn, j + 1, fx);   // in flight during the inverse transform
+            if constexpr (KEEP1) {
+                fft<LG, +1, true>(v, S, tw, t, false);
+                if (t < ny_out) B[boff(j, fx, t, H, ldb, cbc, nyb)] = v[0];
+            } else {
+                fft<LG, +1>(v, S, tw, t, false);
+                if (fastst) {
+                    float2 *bp = B + (cbc ? ((((int64_t)j * nyb + tq) * H + fx) * cbc + tr)
+                                          : (((int64_t)j * H + fx) * ldb + t));
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        if (e < ne) bp[e * es] = v[e];
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const int y = t + NT * e;
+                        if (y < ny_out) B[boff(j, fx, y, H, ldb, cbc, nyb)] = v[e];
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = vn[e];
+        }
+        __syncthreads();   // all reads of Xs done before the next unit's copy
     }
 }
 
@@ -425,7 +580,7 @@ template <int LG>
 __global__ void __launch_bounds__(Cfg<LG>::THREADS, Cfg<LG>::MINB)
 rpass_c(const float2 *__restrict__ B, int oy, int ldb, int cblk, int H, int k, int ox, float inv,
         float *__restrict__ out, int64_t ldo, const int *__restrict__ omap, const int *__restrict__ w, int64_t stride,
-        const float2 *__restrict__ twg) {
+        const float2 *__restrict__ twg, const double *__restrict__ cs) {
     using C = Cfg<LG>;
     constexpr int N = C::N, NT = C::NT, TPC = C::TPC, CB = 2 * TPC, THR = C::THREADS;
     constexpr int PER = (H_of(LG) * TPC + THR - 1) / THR;   // gathered column pairs per thread
@@ -493,6 +648,21 @@ rpass_c(const float2 *__restrict__ B, int oy, int ldb, int cblk, int H, int k, i
         __syncthreads();   // the buffers are reused by the exchanges
         fft<LG, +1>(v, S, tw, t, false);
         const int ya_col = y0 + 2 * q;
+        const float sc = cs ? (float)((double)inv * cs[j]) : inv;
+        if (!w && !omap) {
+            // products on a full box: out[x + ox·y + ldo·j] with x = t + NT·e — one base pointer and
+            // immediate offsets (the generic path below spent ~20 instructions per element)
+            float *o0 = out + ldo * j + (int64_t)ox * ya_col + t;
+            const bool c0 = ya_col - y0 < ncol, c1 = ya_col + 1 - y0 < ncol;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                if (t + NT * e >= ox) break;
+                if (c0) o0[NT * e] = v[e].x * sc;
+                if (c1) o0[ox + NT * e] = v[e].y * sc;
+            }
+            __syncthreads();
+            continue;
+        }
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
             const int x = t + NT * e;
@@ -501,7 +671,7 @@ rpass_c(const float2 *__restrict__ B, int oy, int ldb, int cblk, int H, int k, i
             for (int h = 0; h < 2; ++h) {
                 const int y = ya_col + h;
                 if (y - y0 >= ncol) continue;
-                const float val = (h ? v[e].y : v[e].x) * inv;
+                const float val = (h ? v[e].y : v[e].x) * sc;
                 if (w) {
                     const int wn = w[x + (int64_t)ox * y];
                     out[(int64_t)j * stride + x + ldo * y] = wn > 0 ? val / (float)wn : __int_as_float(0x7fc00000);
@@ -588,18 +758,55 @@ int cb_of(int lg) {
     return cb;
 }
 
+template <int LG>
+static void pass_b_lg(const float2 *A, int ny_in, int lda, int H, int k, const float2 *Xh, float2 *B, int ny_out,
+                      int ldb, int cbc, const float2 *tw, cudaStream_t st) {
+    using Cf = Cfg<LG, true>;
+    // X̂-resident form by default (c5: Xᵀ·U 5.59 -> 5.42 ms, X·V 5.45 -> 5.39 ms per block product);
+    // SSA_RPASS_B2=0 selects the item-per-row form above
+    static const int b2 = [] { const char *e = std::getenv("SSA_RPASS_B2"); return e ? std::atoi(e) : 1; }();
+    if constexpr (Cf::TPC == 1) {
+        if (b2 > 0 && k > 1) {
+            constexpr int JC = 16;
+            const int64_t units = (int64_t)H * cdiv(k, JC);
+            auto launch2 = [&](auto kern) {
+                const int grid = prep(kern, CfgB2<LG>::THREADS, CfgB2<LG>::smem, units);
+                kern<<<grid, CfgB2<LG>::THREADS, CfgB2<LG>::smem, st>>>(A, ny_in, lda, H, k, Xh, B, ny_out, ldb, cbc,
+                                                                          tw);
+            };
+            const bool keep1 = ny_out <= Cf::NT;
+            if constexpr (r0_of(LG) == 16) {
+                if (ny_in <= Cf::NT) {
+                    if (keep1) launch2(rpass_b2<LG, true, true, JC>);
+                    else launch2(rpass_b2<LG, false, true, JC>);
+                    return;
+                }
+            }
+            if (keep1) launch2(rpass_b2<LG, true, false, JC>);
+            else launch2(rpass_b2<LG, false, false, JC>);
+            return;
+        }
+    }
+    const int64_t items = cdiv(H, Cf::TPC) * (int64_t)k;
+    auto launch = [&](auto kern) {
+        const int grid = prep(kern, Cf::THREADS, Cf::smem, items);
+        kern<<<grid, Cf::THREADS, Cf::smem, st>>>(A, ny_in, lda, H, k, Xh, B, ny_out, ldb, cbc, tw);
+    };
+    const bool keep1 = ny_out <= Cf::NT;
+    if constexpr (r0_of(LG) == 16) {
+        if (ny_in <= Cf::NT) {
+            if (keep1) launch(rpass_b<LG, true, true>);
+            else launch(rpass_b<LG, false, true>);
+            return;
+        }
+    }
+    if (keep1) launch(rpass_b<LG, true, false>);
+    else launch(rpass_b<LG, false, false>);
+}
+
 void pass_b(int lg, const float2 *A, int ny_in, int lda, int H, int k, const float2 *Xh, float2 *B, int ny_out,
             int ldb, int cbc, const float2 *tw, cudaStream_t st) {
-    RFFT_DISPATCH(lg, {
-        using Cf = Cfg<LG, true>;
-        if (ny_out <= Cf::NT) {
-            const int grid = prep(rpass_b<LG, true>, Cf::THREADS, Cf::smem, cdiv(H, Cf::TPC) * (int64_t)k);
-            rpass_b<LG, true><<<grid, Cf::THREADS, Cf::smem, st>>>(A, ny_in, lda, H, k, Xh, B, ny_out, ldb, cbc, tw);
-        } else {
-            const int grid = prep(rpass_b<LG, false>, Cf::THREADS, Cf::smem, cdiv(H, Cf::TPC) * (int64_t)k);
-            rpass_b<LG, false><<<grid, Cf::THREADS, Cf::smem, st>>>(A, ny_in, lda, H, k, Xh, B, ny_out, ldb, cbc, tw);
-        }
-    });
+    RFFT_DISPATCH(lg, pass_b_lg<LG>(A, ny_in, lda, H, k, Xh, B, ny_out, ldb, cbc, tw, st));
     after_launch("rfft_pass_b");
 }
 
@@ -617,7 +824,8 @@ void pass_bconv(int lg, const float2 *AU, int ly, int ldu, const float2 *AV, int
 }
 
 void pass_c(int lg, const float2 *B, int oy, int ldb, int cblk, int H, int k, int ox, float inv, float *out,
-            int64_t ldo, const int *omap, const int *w, int64_t stride, const float2 *tw, cudaStream_t st) {
+            int64_t ldo, const int *omap, const int *w, int64_t stride, const float2 *tw, cudaStream_t st,
+            const double *cs) {
     SSA_REQUIRE(ldb % 2 == 0 && ((uintptr_t)B & 15) == 0, SSA_ERR_ARG, "rfft pass C: rows must be 16-B aligned");
     RFFT_DISPATCH(lg, {
         using Cf = Cfg<LG>;
@@ -625,7 +833,7 @@ void pass_c(int lg, const float2 *B, int oy, int ldb, int cblk, int H, int k, in
         const int grid = prep(rpass_c<LG>, Cf::THREADS, Cf::smem, cdiv(oy, 2 * Cf::TPC) * (int64_t)k);
         SSA_REQUIRE(cblk == 0 || cblk % (2 * Cf::TPC) == 0, SSA_ERR_ARG, "rfft pass C: block width");
         rpass_c<LG><<<grid, Cf::THREADS, Cf::smem, st>>>(B, oy, ldb, cblk, H, k, ox, inv, out, ldo, omap, w, stride,
-                                                         tw);
+                                                         tw, cs);
     });
     after_launch("rfft_pass_c");
 }

@@ -34,8 +34,10 @@ void pass_bconv(int lg, const float2 *AU, int ly, int ldu, const float2 *AV, int
                 const float2 *tw, cudaStream_t st);
 // per output column y < oy: Hermitian completion, inverse x-DFT (2^lg), rows x < ox, times inv;
 // products: out[omap(x, y) + ldo*j]; averaging (w != null): out[j*stride + x + ldo*y] = v / w (NaN if w = 0)
+// cs (products only, may be null): output column j is also multiplied by cs[j] (V = XᵀU/σ in one pass)
 void pass_c(int lg, const float2 *B, int oy, int ldb, int cblk, int H, int k, int ox, float inv, float *out,
-            int64_t ldo, const int *omap, const int *w, int64_t stride, const float2 *tw, cudaStream_t st);
+            int64_t ldo, const int *omap, const int *w, int64_t stride, const float2 *tw, cudaStream_t st,
+            const double *cs = nullptr);
 // Intermediate rows (A: by columns, B: oy columns) have strides lda / ldb = multiples of 4 complex
 // values (32-B aligned rows); the transposed accesses of passes A and C move 16-B column pairs.
 

@@ -68,7 +68,8 @@ PlanImpl &ssa_plan_impl(ssa_plan p);
 template <typename T>
 void op_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k);    // U = X V
 template <typename T>
-void op_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k);   // V = Xᵀ U
+void op_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k,
+            const double *cs = nullptr);   // V = Xᵀ U (column j times cs[j] if cs: device array of k)
 double *small_dev(PlanImpl &p, size_t n_doubles);
 
 // solver.cu
@@ -85,7 +86,7 @@ void fft_build(PlanImpl &p);
 template <typename T>
 void fft_xv(PlanImpl &p, const T *V, int64_t ldv, T *U, int64_t ldu, int k);
 template <typename T>
-void fft_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k);
+void fft_xtu(PlanImpl &p, const T *U, int64_t ldu, T *V, int64_t ldv, int k, const double *cs = nullptr);
 template <typename T>
 void fft_diagsums(PlanImpl &p, const T *U, const T *V, const double *sig_dev, const int *grp_off_dev,
                   const int *grp_idx_dev, int ng, const std::vector<int> &used, const int *slot_dev, T *out,

@@ -41,6 +41,13 @@ def test_self_gram_matches_fp64(lib, M, n1, n2):
     assert _run(lib, 3, M, n1, n2) <= TOL
 
 
+@pytest.mark.parametrize("M,n1,n2", [(12345, 128, 64), (20001, 192, 64), (9001, 96, 32), (8200, 320, 64),
+                                     (10007, 64, 64)])
+def test_tail_gram_matches_fp64(lib, M, n1, n2):
+    """[A W]ᵀW with W the last n2 columns of A (the projection Gram of the solver): W read from A's tiles."""
+    assert _run(lib, 5, M, n1, n2) <= TOL
+
+
 @pytest.mark.parametrize("M,n1,n2", [(8200, 65, 33), (8200, 100, 64), (20001, 300, 64), (9001, 33, 17),
                                      (70000, 512, 64), (3000, 224, 32)])
 def test_update_matches_fp64(lib, M, n1, n2):
