@@ -33,6 +33,7 @@
 
 #include "common.h"
 #include "fft_reg.h"
+#include "tc_common.h"
 
 namespace ssa {
 namespace rfft {
@@ -324,6 +325,138 @@ rpass_a(const float *__restrict__ in, int64_t ld, const int *__restrict__ map, i
             else *dst = make_float2(o.x, o.y);
         }
         __syncthreads();   // the buffers are rewritten by the next item
+    }
+}
+
+// ------------------------------------------------------------------------------ pipelined A / C
+// Passes A and C alternate a memory phase (a block of columns in, a block out) with a compute phase
+// (the transforms); run as above, one CTA's loads wait for its own transforms and the two phases add
+// up (c5: X·V pass A and Xᵀ·U pass C at ~2.9 TB/s, with the 4096-point transforms costing about as
+// long as the block's transfer).  Here the CTA owns two buffer sets of TPC exchange buffers: while
+// the transforms of item n run in set n&1 — first as the staging area its input arrived in, then as
+// the exchange buffers — one bulk asynchronous copy (cp.async.bulk, mbarrier completion) brings item
+// n+1's input into the other set, so the HBM stream never waits for the ALUs.  Both inputs are
+// contiguous per item: pass A's CB input columns of the box (x fastest), pass C's H x CB block of the
+// blocked B layout (boff).  Shared memory: twiddles + 2·TPC exchange buffers (172 KB at 2^12 points,
+// one 512-thread CTA per SM).
+template <int LG> struct CfgP {
+    static constexpr int THREADS = Cfg<LG>::THREADS;
+    static constexpr size_t set_elems = (size_t)Cfg<LG>::TPC * Cfg<LG>::XB;   // float2 per buffer set
+    static constexpr size_t smem = sizeof(float2) * ((size_t)Cfg<LG>::TWP + 2 * set_elems) + 16;
+};
+__device__ __forceinline__ void mbar_arrive1(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// bytes (multiple of 16, 16-B aligned ends) from global to shared, completing on `bar`: chunks of
+// at most 32 KB (expect_tx counts per instruction are limited), then the producer's arrival
+__device__ __forceinline__ void bulk_in(float2 *dst, const void *src, uint32_t bytes, uint32_t bar) {
+    const uint32_t d = tc::smem_u32(dst);
+    for (uint32_t o = 0; o < bytes; o += 32768u) {
+        const uint32_t n = min(32768u, bytes - o);
+        tc::mbar_expect_tx_noarrive(bar, n);
+        tc::bulk_g2s(d + o, static_cast<const char *>(src) + o, n, bar);
+    }
+    mbar_arrive1(bar);
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// pass A, pipelined: same items and outputs as rpass_a (identity map: rectangular box).  Staged input
+// of item (jo, col0): the CB columns in[ld·j + bx·col0 ...], bx floats each, from the 16-B boundary at
+// or below their start; the part beyond their last 16-B boundary is read directly from global memory.
+template <int LG>
+__global__ void __launch_bounds__(CfgP<LG>::THREADS, 1)
+rpass_a2(const float *__restrict__ in, int64_t ld, int bx, int by, int k, const int *__restrict__ jsel,
+         const double *__restrict__ scale, float2 *__restrict__ A, int lda, const float2 *__restrict__ twg) {
+    using C = Cfg<LG>;
+    constexpr int N = C::N, NT = C::NT, H = C::H, TPC = C::TPC, CB = 2 * TPC;
+    extern __shared__ float2 sm[];
+    const float2 *tw = stage_tw<LG>(sm, twg);
+    float2 *set0 = sm + C::TWP;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(set0 + 2 * CfgP<LG>::set_elems);
+    const uint32_t bar0 = tc::smem_u32(bars), bar1 = tc::smem_u32(bars + 1);
+    const int q = threadIdx.x / NT, t = threadIdx.x % NT;
+    const int nb = (by + CB - 1) / CB, items = nb * k;
+    auto src_of = [&](int it, int &ncol) {
+        const int jo = it / nb, col0 = (it - jo * nb) * CB;
+        const int j = jsel ? jsel[jo] : jo;
+        ncol = min(CB, by - col0);
+        return in + ld * j + (int64_t)bx * col0;
+    };
+    // staged range: from src rounded down to 16 B (off < 4 floats before it, inside the allocation
+    // since `in` itself is 16-B aligned) to the last 16-B boundary inside the item's columns
+    auto staged = [&](const float *src, int ncol, int &off) {
+        off = (int)((reinterpret_cast<uintptr_t>(src) & 15) >> 2);
+        const int64_t end = (int64_t)off + (int64_t)bx * ncol;
+        return (int)(end & ~int64_t(3));   // staged floats, counted from src - off
+    };
+    auto issue = [&](int it, int s) {
+        int ncol, off;
+        const float *src = src_of(it, ncol);
+        const int nst = staged(src, ncol, off);
+        bulk_in(set0 + s * CfgP<LG>::set_elems, src - off, (uint32_t)nst * 4u, s ? bar1 : bar0);
+    };
+    if (threadIdx.x == 0) {
+        tc::mbar_init(bar0, 1);
+        tc::mbar_init(bar1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();   // twiddle table staged, barriers initialised
+    if (threadIdx.x == 0 && (int)blockIdx.x < items) issue(blockIdx.x, 0);
+    int n = 0;
+    for (int it = blockIdx.x; it < items; it += gridDim.x, ++n) {
+        const int s = n & 1;
+        if (threadIdx.x == 0 && it + (int)gridDim.x < items) issue(it + gridDim.x, s ^ 1);
+        const int jo = it / nb, col0 = (it - jo * nb) * CB;
+        const int j = jsel ? jsel[jo] : jo;
+        int ncol;
+        const float *src = src_of(it, ncol);
+        int off;
+        const int nflt = staged(src, ncol, off) - off;   // staged floats from src on
+        float2 *base = set0 + s * CfgP<LG>::set_elems;
+        const float *raw = reinterpret_cast<const float *>(base) + off;
+        tc::mbar_wait(s ? bar1 : bar0, (n >> 1) & 1);
+        const int ca = 2 * q, cb = ca + 1;
+        float2 v[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int ix = t + NT * e;
+            const int ia = ca * bx + ix, ib = cb * bx + ix;
+            v[e].x = (ix < bx && ca < ncol) ? (ia < nflt ? raw[ia] : __ldg(src + ia)) : 0.f;
+            v[e].y = (ix < bx && cb < ncol) ? (ib < nflt ? raw[ib] : __ldg(src + ib)) : 0.f;
+        }
+        __syncthreads();   // every staged value is in registers: the set becomes the exchange buffers
+        float2 *S = base + (size_t)q * C::XB;
+        fft<LG, -1>(v, S, tw, t, false);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) S[pad(t + NT * e)] = v[e];
+        __syncthreads();
+        const float hs = 0.5f * (scale ? (float)scale[j] : 1.f);
+        float2 *arow = A + (int64_t)jo * H * lda + col0;
+        // unrolled: all shared-memory reads of the thread's (fx, pair) outputs before the first store
+        // (the rolled loop exposed the read latency once per output, ncu source page)
+        constexpr int PER = (H * TPC + C::THREADS - 1) / C::THREADS;
+        float2 zz[PER], zzm[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int idx = threadIdx.x + C::THREADS * u;
+            const int fx = idx / TPC, q2 = idx - fx * TPC;
+            const float2 *Sq = base + (size_t)q2 * C::XB;
+            if (idx < H * TPC) { zz[u] = Sq[pad(fx)]; zzm[u] = Sq[pad((N - fx) & (N - 1))]; }
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int idx = threadIdx.x + C::THREADS * u;
+            const int fx = idx / TPC, q2 = idx - fx * TPC;
+            const int col = col0 + 2 * q2;
+            if (idx >= H * TPC || col >= by) continue;
+            const float2 z = zz[u], zm = zzm[u];
+            const float4 o = make_float4(hs * (z.x + zm.x), hs * (z.y - zm.y), hs * (z.y + zm.y), hs * (zm.x - z.x));
+            float2 *dst = arow + (int64_t)fx * lda + 2 * q2;
+            if (col + 1 < by) *reinterpret_cast<float4 *>(dst) = o;
+            else *dst = make_float2(o.x, o.y);
+        }
+        fence_async_smem();   // generic accesses of this set ordered before the next bulk copy into it
+        __syncthreads();
     }
 }
 
@@ -686,6 +819,108 @@ rpass_c(const float2 *__restrict__ B, int oy, int ldb, int cblk, int H, int k, i
     }
 }
 
+// pass C, pipelined (blocked B layout with cbc = CB only): same items and outputs as rpass_c.  The
+// item's H x CB block is one contiguous bulk copy; transform q reads its column pair (2q, 2q + 1) as
+// one 16-B value per frequency.
+template <int LG>
+__global__ void __launch_bounds__(CfgP<LG>::THREADS, 1)
+rpass_c2(const float2 *__restrict__ B, int oy, int H, int k, int ox, float inv, float *__restrict__ out,
+         int64_t ldo, const int *__restrict__ omap, const int *__restrict__ w, int64_t stride,
+         const float2 *__restrict__ twg, const double *__restrict__ cs) {
+    using C = Cfg<LG>;
+    constexpr int N = C::N, NT = C::NT, TPC = C::TPC, CB = 2 * TPC;
+    extern __shared__ float2 sm[];
+    const float2 *tw = stage_tw<LG>(sm, twg);
+    float2 *set0 = sm + C::TWP;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(set0 + 2 * CfgP<LG>::set_elems);
+    const uint32_t bar0 = tc::smem_u32(bars), bar1 = tc::smem_u32(bars + 1);
+    const int q = threadIdx.x / NT, t = threadIdx.x % NT;
+    const int H0 = C::H;
+    const int nb = (oy + CB - 1) / CB, items = nb * k;
+    const uint32_t bytes = (uint32_t)H0 * CB * sizeof(float2);
+    auto issue = [&](int it, int s) {
+        // item it = (j, block yb) is block j·nb + yb of the blocked layout: blocks are consecutive
+        bulk_in(set0 + s * CfgP<LG>::set_elems, B + (int64_t)it * H0 * CB, bytes, s ? bar1 : bar0);
+    };
+    if (threadIdx.x == 0) {
+        tc::mbar_init(bar0, 1);
+        tc::mbar_init(bar1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (int)blockIdx.x < items) issue(blockIdx.x, 0);
+    int n = 0;
+    for (int it = blockIdx.x; it < items; it += gridDim.x, ++n) {
+        const int s = n & 1;
+        if (threadIdx.x == 0 && it + (int)gridDim.x < items) issue(it + gridDim.x, s ^ 1);
+        const int j = it / nb, y0 = (it - j * nb) * CB;
+        const int ncol = min(CB, oy - y0);
+        float2 *base = set0 + s * CfgP<LG>::set_elems;
+        const float4 *raw = reinterpret_cast<const float4 *>(base) + q;   // (fx, pair q) at raw[fx·TPC]
+        tc::mbar_wait(s ? bar1 : bar0, (n >> 1) & 1);
+        // Z[f] = Y_a[f] + i·Y_b[f] over the full spectrum (as rpass_c); never-written padding columns
+        // of a ragged last block are zeroed
+        const bool za = 2 * q >= ncol, zb = 2 * q + 1 >= ncol;
+        float2 v[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int f = t + NT * e;
+            const bool lo = f <= N / 2;
+            const int fs = lo ? f : N - f;
+            const float4 z = raw[fs * TPC];
+            float2 ya = make_float2(z.x, z.y), yb = make_float2(z.z, z.w);
+            if (!lo) { ya.y = -ya.y; yb.y = -yb.y; }
+            if (f == 0 || f == N / 2) { ya.y = 0.f; yb.y = 0.f; }
+            if (za) ya = make_float2(0.f, 0.f);
+            if (zb) yb = make_float2(0.f, 0.f);
+            v[e] = make_float2(ya.x - yb.y, ya.y + yb.x);
+        }
+        __syncthreads();   // the staged block is in registers: the set becomes the exchange buffers
+        float2 *S = base + (size_t)q * C::XB;
+        fft<LG, +1>(v, S, tw, t, false);
+        const int ya_col = y0 + 2 * q;
+        const float sc = cs ? (float)((double)inv * cs[j]) : inv;
+        if (!w && !omap) {
+            float *o0 = out + ldo * j + (int64_t)ox * ya_col + t;
+            const bool c0 = !za, c1 = !zb;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                if (t + NT * e >= ox) break;
+                if (c0) o0[NT * e] = v[e].x * sc;
+                if (c1) o0[ox + NT * e] = v[e].y * sc;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int x = t + NT * e;
+                if (x >= ox) continue;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int y = ya_col + h;
+                    if (y - y0 >= ncol) continue;
+                    const float val = (h ? v[e].y : v[e].x) * sc;
+                    if (w) {
+                        const int wn = w[x + (int64_t)ox * y];
+                        out[(int64_t)j * stride + x + ldo * y] = wn > 0 ? val / (float)wn : __int_as_float(0x7fc00000);
+                    } else {
+                        const int64_t box = x + (int64_t)ox * y;
+                        const int64_t oi = omap ? (int64_t)omap[box] : box;
+                        if (oi >= 0) out[oi + ldo * j] = val;
+                    }
+                }
+            }
+        }
+        fence_async_smem();
+        __syncthreads();
+    }
+}
+
+// pipelined passes A / C (default; SSA_RPASS_PIPE=0 selects the single-buffered kernels)
+static bool pipe_on() {
+    static const int v = [] { const char *e = std::getenv("SSA_RPASS_PIPE"); return e ? std::atoi(e) : 1; }();
+    return v > 0;
+}
+
 // ------------------------------------------------------------------------------------ host side
 int tw_count(int lg) { return tw_count_c(lg); }
 
@@ -736,6 +971,11 @@ void pass_a(int lg, const float *in, int64_t ld, const int *map, int bx, int by,
     SSA_REQUIRE(lda % 2 == 0 && ((uintptr_t)A & 15) == 0, SSA_ERR_ARG, "rfft pass A: rows must be 16-B aligned");
     RFFT_DISPATCH(lg, {
         using Cf = Cfg<LG>;
+        if (pipe_on() && !map && ((uintptr_t)in & 3) == 0) {
+            const int grid = prep(rpass_a2<LG>, Cf::THREADS, CfgP<LG>::smem, cdiv(by, 2 * Cf::TPC) * (int64_t)k);
+            rpass_a2<LG><<<grid, Cf::THREADS, CfgP<LG>::smem, st>>>(in, ld, bx, by, k, jsel, scale, A, lda, tw);
+            break;
+        }
         const int grid = prep(rpass_a<LG>, Cf::THREADS, Cf::smem, cdiv(by, 2 * Cf::TPC) * (int64_t)k);
         rpass_a<LG><<<grid, Cf::THREADS, Cf::smem, st>>>(in, ld, map, bx, by, k, jsel, scale, A, lda, tw);
     });
@@ -832,6 +1072,11 @@ void pass_c(int lg, const float2 *B, int oy, int ldb, int cblk, int H, int k, in
         static_assert(2 * Cfg<LG>::H <= Cfg<LG>::XB, "column pair fits the exchange buffer");
         const int grid = prep(rpass_c<LG>, Cf::THREADS, Cf::smem, cdiv(oy, 2 * Cf::TPC) * (int64_t)k);
         SSA_REQUIRE(cblk == 0 || cblk % (2 * Cf::TPC) == 0, SSA_ERR_ARG, "rfft pass C: block width");
+        if (pipe_on() && cblk == 2 * Cf::TPC && H == Cf::H) {
+            const int g2 = prep(rpass_c2<LG>, Cf::THREADS, CfgP<LG>::smem, cdiv(oy, 2 * Cf::TPC) * (int64_t)k);
+            rpass_c2<LG><<<g2, Cf::THREADS, CfgP<LG>::smem, st>>>(B, oy, H, k, ox, inv, out, ldo, omap, w, stride, tw, cs);
+            break;
+        }
         rpass_c<LG><<<grid, Cf::THREADS, Cf::smem, st>>>(B, oy, ldb, cblk, H, k, ox, inv, out, ldo, omap, w, stride,
                                                          tw, cs);
     });
