@@ -123,6 +123,7 @@ struct Gkl {
         return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
     }
     int64_t n_fast = 0, n_fallback = 0;
+    int64_t o3_exit[2][6] = {{0}};   // SSA_DEBUG: orth3 exits per side [pass], [5] = reprojections
     std::vector<double> res;      // residual bounds of the current Ritz triples
     bool anorm_from_next_gram = false;
     double drop2 = 0.0;           // Σ squared norms of block columns discarded as numerically zero
@@ -471,7 +472,9 @@ struct Gkl {
             }
             const bool was_projection = project;
             project = (pass == 1 && reproject);
+            if (project) ++o3_exit[kside][5];
             if (pass >= 2 && !project && !shifted && !was_projection && dev <= 0.1) {
+                ++o3_exit[kside][pass];
                 if (coef)
                     for (size_t t = 0; t < Ctot.size(); ++t) coef[t] += Ctot[t];
                 ++n_fast;
@@ -479,6 +482,7 @@ struct Gkl {
             }
             if (pass >= 2 && !project && !shifted && was_projection && dev <= 1e-3) {
                 // the second projection pass already left W orthonormal
+                ++o3_exit[kside][pass];
                 if (coef)
                     for (size_t t = 0; t < Ctot.size(); ++t) coef[t] += Ctot[t];
                 ++n_fast;
@@ -852,6 +856,10 @@ struct Gkl {
         if (debug)
             std::fprintf(stderr, "[ssa] orth3 host ms: L gram(wait) %.2f host %.2f apply(launch) %.2f | K gram %.2f host %.2f apply %.2f\n",
                          tw_o3_gram[0], tw_o3_host[0], tw_o3_apply[0], tw_o3_gram[1], tw_o3_host[1], tw_o3_apply[1]);
+        if (debug)
+            for (int sd = 0; sd < 2; ++sd)
+                std::fprintf(stderr, "[ssa] orth3 %s side: exits at pass 2/3/4 %lld/%lld/%lld, reprojections %lld\n", sd ? "K" : "L",
+                             (long long)o3_exit[sd][2], (long long)o3_exit[sd][3], (long long)o3_exit[sd][4], (long long)o3_exit[sd][5]);
         // sign convention: largest-|.| entry of each U_i positive
         for (int c0 = 0; c0 < r; c0 += 1024) {
             const int nc = std::min(1024, r - c0);
