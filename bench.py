@@ -327,6 +327,8 @@ def run_ours(args, rank, world, dist):
         "unit": "vector products/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_all / args.steps,
+        "step_ms": [round(float(t), 3) for t in times],
+        "step_phases_ms": [[round(float(x), 3) for x in ph_] for ph_ in phase_dev],
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,

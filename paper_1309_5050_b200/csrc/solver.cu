@@ -372,7 +372,9 @@ struct Gkl {
     // norm (Gp_jj < ½ (WᵀW)_jj), or a column is numerically zero, or Cholesky fails, W is left
     // untouched and the robust `orth` (second projection, shifts, refills, SVQB) takes over.
     // Returns B with W_in = A·coef + W_out·B (coef accumulated, as in `orth`).
-    std::vector<double> orth3(int64_t M, T *W, int kc, const T *against, int na, bool kside, double *coef) {
+    // G1 (optional): the pass-1 Gram [A W]ᵀW, already computed (a deferred orthonormalisation, below)
+    std::vector<double> orth3(int64_t M, T *W, int kc, const T *against, int na, bool kside, double *coef,
+                              const std::vector<double> *G1 = nullptr) {
         const int64_t ld = LD(M);
         if (kc > 64 || na <= 0 || na + kc > 512 || against + (int64_t)na * ld != W)
             return orth(M, W, kc, against, na, kside, coef);
@@ -389,7 +391,8 @@ struct Gkl {
                 const int nn = project ? n1 : kc;                       // Gram columns: [A W] or W
                 T *Ab = project ? A : W;
                 const double tg0 = now_ms();
-                gram(M, Ab, ld, nn, W, ld, kc, G.data(), kside);
+                if (pass == 1 && G1 && project) G = *G1;
+                else gram(M, Ab, ld, nn, W, ld, kc, G.data(), kside);
                 const double tg1 = now_ms();
                 tw_o3_gram[kside] += tg1 - tg0;
                 const int off = project ? na : 0;
@@ -617,6 +620,62 @@ struct Gkl {
         nQ += k;
     }
 
+    // Deferred K-side orthonormalisation.  When a Ritz check follows a block pair, the
+    // new K block only matters through A_last (the residual bound) unless the iteration continues:
+    // stepB_check stops after the recurrence and the pass-1 Gram [Q W]ᵀW and takes A_last ≈ R₁,
+    // the Cholesky factor of the projected Gram (the second CholeskyQR pass changes it by the
+    // pass-1 output's deviation from orthonormality).  A check that converges with margin skips
+    // the block's remaining passes (c5: 3 of its 5 K-side streams); otherwise stepB_finish runs
+    // orth3 from the stored Gram and the residuals are recomputed with the exact A_last.
+    std::vector<double> G1def;
+    bool deferred = false;
+    void stepB_check() {
+        const int pc = nP - k, na = nQ, n1 = nQ + k;
+        if (na <= 0 || k > 64 || n1 > 512) { stepB(); return; }
+        T *W = Q(nQ);
+        double t0 = now_ms();
+        product_xtu(P(pc), W, k);
+        tw_prod += now_ms() - t0;
+        t0 = now_ms();
+        {   // recurrence term, as stepB
+            const int qc = nQ - k;
+            std::vector<double> Bt((size_t)k * k);
+            for (int a = 0; a < k; ++a)
+                for (int b = 0; b < k; ++b) Bt[b + (size_t)k * a] = Tat(pc + a, qc + b);
+            gemm(K, Q(qc), ldQ, k, Bt.data(), k, k, -1.0, 1.0, W, ldQ);
+        }
+        G1def.assign((size_t)n1 * k, 0.0);
+        gram(K, Q(0), ldQ, n1, W, ldQ, k, G1def.data(), true);
+        // orth3's pass-1 tests; any of them (breakdown, DGKS reprojection, failed or shifted
+        // Cholesky) -> the full orthonormalisation now, from the same Gram
+        std::vector<double> Gp((size_t)k * k), R;
+        hostla::gram_minus_ctc(k, na, n1, na, G1def.data(), Gp.data());
+        double dmax = 0.0;
+        for (int j = 0; j < k; ++j) dmax = std::max(dmax, Gp[j + (size_t)k * j]);
+        bool fine = dmax > 0.0 && std::isfinite(dmax);
+        for (int j = 0; j < k && fine; ++j) {
+            const double d = Gp[j + (size_t)k * j], h = G1def[na + j + (size_t)n1 * j];
+            fine = std::sqrt(std::max(d, 0.0)) > thr_abs * std::max(anorm, 1e-300) && d > 1e-24 * dmax &&
+                   d > (sizeof(T) == 4 ? 1e-12 : 1e-24) * h && d > 0.5 * h;
+        }
+        fine = fine && cholesky(k, Gp.data(), 0.0, thr_chol, R);
+        if (fine) {
+            Alast = R;
+            deferred = true;
+        } else {
+            Alast = orth3(K, W, k, Q(0), na, true, nullptr, &G1def);
+        }
+        tw_orthB += now_ms() - t0;
+        nQ += k;
+    }
+    void stepB_finish() {
+        if (!deferred) return;
+        deferred = false;
+        const double t0 = now_ms();
+        Alast = orth3(K, Q(nQ - k), k, Q(0), nQ - k, true, nullptr, &G1def);
+        tw_orthB += now_ms() - t0;
+    }
+
     // SVD of T[0:m, 0:n] (m >= n): th (n), Y (m x n), Z (n x n), descending.
     void ritz_svd(int m, int n, std::vector<double> &th, std::vector<double> &Y, std::vector<double> &Z) {
         const auto t0 = std::chrono::steady_clock::now();
@@ -769,22 +828,28 @@ struct Gkl {
         int nconv = 0, restarts = 0;
         double t_block = 0.0, t_ritz = 0.0;   // host wall ms of the last block pair / Ritz step
         double maxres = 0.0;
+        static const bool defer_on = [] { const char *e = std::getenv("SSA_DEFER"); return e ? std::atoi(e) != 0 : true; }();
         for (;;) {
             const double tb0 = now_ms();
             stepA();
-            stepB();
-            t_block = now_ms() - tb0;
-            const bool cycle_end = !(nQ + k <= nQmax && nblock < maxprod);
-            // when a block step costs at least as much as a Ritz step (c4, c5: large operators, few
-            // blocks to convergence), check after every block once the basis holds r vectors;
-            // cheap blocks (c2, c3) wait for the cycle end.  With a band partition every rank must
-            // take the same decision (each check is followed by collectives or by none): the
-            // timings are averaged over the ranks first.
+            // Will a Ritz check follow this pair?  (decided before stepB, so that its
+            // orthonormalisation can be deferred past the check)  The cycle ends when the basis is
+            // full or the product budget is spent.  When a block step costs at least as much as a
+            // Ritz step (c4, c5: large operators, few blocks to convergence), check after every block
+            // once the basis holds r vectors (cost of the previous pair); cheap blocks (c2, c3) wait
+            // for the cycle end.  With a band partition every rank must take the same decision (each
+            // check is followed by collectives or by none): the timings are averaged over the ranks
+            // first.
+            const bool cycle_end = !(nQ + 2 * k <= nQmax && nblock + 1 < maxprod);
             double tt[2] = {t_block, t_ritz > 0.0 ? t_ritz : 1.0};
             if (kside_comm()) agree(tt, 2);
             static const double cost_ratio = [] { const char *e = std::getenv("SSA_CHECK_RATIO"); return e ? std::atof(e) : 1.0; }();
-            const bool costly_blocks = nQ - k >= r && tt[0] >= cost_ratio * tt[1];
-            if (!cycle_end && !costly_blocks) continue;
+            const bool costly_blocks = nQ >= r && tt[0] >= cost_ratio * tt[1];
+            const bool check = cycle_end || costly_blocks;
+            if (check && defer_on) stepB_check();
+            else stepB();
+            t_block = now_ms() - tb0;
+            if (!check) continue;
             // ---- Ritz extraction from T (nP x nc)
             const int nc = nQ - k;
             const double tr = ms_ritz;
@@ -795,19 +860,31 @@ struct Gkl {
             // + sqrt(drop2), drop2 = the squared norms of every block column that orthonormalisation
             // discarded as numerically zero (a refilled column has no A / B entry, so without this
             // term its part of the residual would be invisible)
-            res.assign(nc, 0.0);
-            std::vector<double> sv((size_t)k);
-            const double dropn = std::sqrt(drop2);
-            for (int i = 0; i < nc; ++i) {
-                // s = Alast · y_i(last block): k independent accumulators, each in the original b order
-                for (int a = 0; a < k; ++a) sv[a] = 0.0;
-                for (int b = 0; b < k; ++b) {
-                    const double y = Y[(nP - k + b) + (size_t)nP * i], *al = Alast.data() + (size_t)k * b;
-                    for (int a = 0; a < k; ++a) sv[a] += al[a] * y;
+            auto residuals = [&]() {
+                res.assign(nc, 0.0);
+                std::vector<double> sv((size_t)k);
+                const double dropn = std::sqrt(drop2);
+                for (int i = 0; i < nc; ++i) {
+                    // s = Alast · y_i(last block): k independent accumulators, each in the original b order
+                    for (int a = 0; a < k; ++a) sv[a] = 0.0;
+                    for (int b = 0; b < k; ++b) {
+                        const double y = Y[(nP - k + b) + (size_t)nP * i], *al = Alast.data() + (size_t)k * b;
+                        for (int a = 0; a < k; ++a) sv[a] += al[a] * y;
+                    }
+                    double s2 = 0.0;
+                    for (int a = 0; a < k; ++a) s2 += sv[a] * sv[a];
+                    res[i] = std::sqrt(s2) + dropn;
                 }
-                double s2 = 0.0;
-                for (int a = 0; a < k; ++a) s2 += sv[a] * sv[a];
-                res[i] = std::sqrt(s2) + dropn;
+            };
+            residuals();
+            if (deferred) {
+                // the estimated A_last decides only with a factor-2 margin on every wanted triple
+                bool sure = nc >= r;
+                for (int i = 0; i < std::min(r, nc) && sure; ++i) sure = res[i] <= 0.5 * tol * th[0];
+                if (!sure) {
+                    stepB_finish();
+                    residuals();
+                }
             }
             nconv = 0; maxres = 0.0;
             for (int i = 0; i < std::min(r, nc); ++i) {
@@ -821,7 +898,7 @@ struct Gkl {
                     for (int a = nP - k; a < nP; ++a) bn += Tat(a, b) * Tat(a, b);
                 std::fprintf(stderr, "[ssa] ritz nP=%d nc=%d prod=%lld th0=%.6e th[r-1]=%.6e res0=%.3e resr=%.3e |Alast|=%.3e |Tlast|=%.3e drop=%.3e conv=%d\n",
                              nP, nc, (long long)nblock, th[0], th[std::min(r, nc) - 1], res[0] / th[0],
-                             res[std::min(r, nc) - 1] / th[0], std::sqrt(an), std::sqrt(bn), dropn, nconv);
+                             res[std::min(r, nc) - 1] / th[0], std::sqrt(an), std::sqrt(bn), std::sqrt(drop2), nconv);
             }
             const bool done = (nconv >= r) || (nblock >= maxprod && nc >= r);
             if (done) {
