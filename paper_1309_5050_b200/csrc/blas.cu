@@ -80,7 +80,7 @@ gram_tn_kernel(int64_t M, const T *__restrict__ A, int64_t lda, int n1,
 // One warp per Gram entry: lanes sum strided partials, then a fixed shuffle tree
 // (deterministic order).
 __global__ void gram_reduce_kernel(const double *__restrict__ partials, int nparts, int n1, int n2,
-                                   double *__restrict__ G) {
+                                   double *__restrict__ G, int ldg) {
     const int e = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (e >= n1 * n2) return;
     const int a = e % n1, b = e / n1;
@@ -90,11 +90,12 @@ __global__ void gram_reduce_kernel(const double *__restrict__ partials, int npar
     for (int q = lane; q < nparts; q += 32) s += base[(int64_t)q * 4096 + al + 64 * b];
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) G[a + (int64_t)n1 * b] = s;
+    if (lane == 0) G[a + (int64_t)ldg * b] = s;
 }
 
-void gram_reduce(const double *partials, int nparts, int n1, int n2, double *G, cudaStream_t st) {
-    gram_reduce_kernel<<<(unsigned)cdiv((int64_t)n1 * n2 * 32, 256), 256, 0, st>>>(partials, nparts, n1, n2, G);
+void gram_reduce(const double *partials, int nparts, int n1, int n2, double *G, cudaStream_t st, int ldg) {
+    gram_reduce_kernel<<<(unsigned)cdiv((int64_t)n1 * n2 * 32, 256), 256, 0, st>>>(partials, nparts, n1, n2, G,
+                                                                                     ldg > 0 ? ldg : n1);
     after_launch("gram_reduce");
 }
 
@@ -279,7 +280,7 @@ static bool gram_stream(int64_t M, const float *A, int64_t lda, int n1, const fl
         gram_stream_kernel<64><<<dim3(ctas, gy), 256, smem, st>>>(M, A, lda, n1, B, ldb, n2, YG, contig, partials);
     }
     after_launch("gram_stream");
-    gram_reduce_kernel<<<(unsigned)cdiv((int64_t)n1 * n2 * 32, 256), 256, 0, st>>>(partials, ctas, n1, n2, G);
+    gram_reduce_kernel<<<(unsigned)cdiv((int64_t)n1 * n2 * 32, 256), 256, 0, st>>>(partials, ctas, n1, n2, G, n1);
     after_launch("gram_reduce");
     return true;
 }
@@ -297,7 +298,7 @@ void gram_tn(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb
     SSA_REQUIRE((size_t)ctas * 4096 * sizeof(double) * ych <= partial_bytes, SSA_ERR_ARG, "gram_tn: workspace");
     gram_tn_kernel<T><<<dim3(ctas, ych), 256, 0, st>>>(M, A, lda, n1, B, ldb, n2, partials);
     after_launch("gram_tn");
-    gram_reduce_kernel<<<(unsigned)cdiv((int64_t)n1 * n2 * 32, 256), 256, 0, st>>>(partials, ctas, n1, n2, G);
+    gram_reduce_kernel<<<(unsigned)cdiv((int64_t)n1 * n2 * 32, 256), 256, 0, st>>>(partials, ctas, n1, n2, G, n1);
     after_launch("gram_reduce");
 }
 template void gram_tn<float>(int64_t, const float *, int64_t, int, const float *, int64_t, int, double *,

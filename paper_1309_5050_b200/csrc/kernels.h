@@ -68,7 +68,7 @@ template <typename T>
 void gram_tn(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb, int n2,
              double *G, double *partials, size_t partial_bytes, cudaStream_t st);
 size_t gram_partial_bytes(int64_t M, int n1, int n2);
-void gram_reduce(const double *partials, int nparts, int n1, int n2, double *G, cudaStream_t st);
+void gram_reduce(const double *partials, int nparts, int n1, int n2, double *G, cudaStream_t st, int ldg = 0);
 // TMA streaming probe (measurement only): M x n block in boxes of brow rows, `boxes` per stage
 void tma_stream_probe(int64_t M, const float *A, int64_t lda, int n, int brow, int boxes, bool swz, int pd, cudaStream_t st);
 // tcgen05 3xTF32 Gram (tall_tc.cu); false when the layout is unsupported

@@ -539,7 +539,7 @@ gram_self_kernel(const __grid_constant__ CUtensorMap tmA, int64_t M, double *__r
 
 // G (n x n) = S(a, b) + S(NC + a, b) + S(NC + b, a), S = the stacked partial sums [hᵀh; lᵀh] (2NC x NC)
 __global__ void gram_reduce_stacked_kernel(const double *__restrict__ partials, int nparts, int nc, int n,
-                                           double *__restrict__ G) {
+                                           double *__restrict__ G, int ldg) {
     const int e = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (e >= n * n) return;
     const int a = e % n, b = e / n;
@@ -552,7 +552,7 @@ __global__ void gram_reduce_stacked_kernel(const double *__restrict__ partials, 
     double s = S(a, b) + (S(nc + a, b) + S(nc + b, a));
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) G[a + (int64_t)n * b] = s;
+    if (lane == 0) G[a + (int64_t)ldg * b] = s;
 }
 
 // ---------------------------------------------------------------------------
@@ -1006,19 +1006,23 @@ bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int
         return false;
     const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallg::R));
     static const int self_mode = [] { const char *e = std::getenv("SSA_GRAM_SELF"); return e ? std::atoi(e) : 1; }();
-    if (self_mode && B == A && ldb == lda && n2 == n1 && n1 <= 64 && !(lda & 31) && !((uintptr_t)A & 127) &&
-        (size_t)ctas * 4096 * sizeof(double) * 2 <= partial_bytes) {
-        // self Gram WᵀW: hi / lo stacked on M, one MMA per k-step (gram_self_kernel)
-        const int nc = n1 <= 32 ? 32 : 64;
+    auto self_ok = [&](const float *X, int n) {
+        return self_mode && n <= 64 && !(lda & 31) && !((uintptr_t)X & 127) &&
+               (size_t)ctas * 4096 * sizeof(double) * 2 <= partial_bytes;
+    };
+    // self Gram XᵀX (n <= 64 columns): hi / lo stacked on M, one MMA per k-step (gram_self_kernel);
+    // result into G with leading dimension ldg
+    auto self_gram = [&](const float *X, int n, double *Gout, int ldg) {
+        const int nc = n <= 32 ? 32 : 64;
         constexpr int self_rows = 128;
         // unswizzled boxes of self_rows rows x nc columns (the kernel relayouts them for the MMA)
         using Key = std::tuple<const float *, int64_t, int, int64_t, int>;
         static thread_local std::map<Key, CUtensorMap> cache;
-        const Key key{A, M, n1, lda, nc * 1000 + self_rows};
+        const Key key{X, M, n, lda, nc * 1000 + self_rows};
         auto it = cache.find(key);
         if (it == cache.end()) {
             if (cache.size() > 256) cache.clear();
-            it = cache.emplace(key, make_map2(A, (uint64_t)M, (uint64_t)n1, (uint64_t)lda * 4, self_rows, (uint32_t)nc,
+            it = cache.emplace(key, make_map2(X, (uint64_t)M, (uint64_t)n, (uint64_t)lda * 4, self_rows, (uint32_t)nc,
                                               false, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)).first;
         }
         auto go = [&](auto kern) {
@@ -1030,8 +1034,24 @@ bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int
         if (nc == 32) go(gram_self_kernel<32, self_rows, 2>);
         else go(gram_self_kernel<64, self_rows, 2>);
         after_launch("gram_self");
-        gram_reduce_stacked_kernel<<<(unsigned)cdiv((int64_t)n1 * n1 * 32, 256), 256, 0, st>>>(partials, ctas, nc, n1, G);
+        gram_reduce_stacked_kernel<<<(unsigned)cdiv((int64_t)n * n * 32, 256), 256, 0, st>>>(partials, ctas, nc, n, Gout,
+                                                                                             ldg);
         after_launch("gram_reduce_stacked");
+    };
+    if (B == A && ldb == lda && n2 == n1 && self_ok(A, n1)) {
+        self_gram(A, n1, G, n1);
+        return true;
+    }
+    // [A W]ᵀW with W = the last n2 = 64 columns of A, more than one 128-column block: AᵀW over the first
+    // n1 − n2 columns (W loaded beside them) plus WᵀW by the self-Gram kernel — one full wave each,
+    // instead of a second, nearly empty wave of CTAs that re-reads W (c5 K side, n1 = 192: 4.6 ms, ncu)
+    static const int split_mode = [] { const char *e = std::getenv("SSA_GRAM_SPLIT"); return e ? std::atoi(e) : 1; }();
+    if (split_mode && n2 == 64 && n1 > 128 && ldb == lda && B == A + (int64_t)(n1 - n2) * lda && self_ok(B, n2) &&
+        (size_t)ctas * 4096 * sizeof(double) * (size_t)cdiv(n1 - n2, 64) <= partial_bytes) {
+        const int na = n1 - n2;
+        launch_gram_tc<1, 64, 128>(M, A, lda, na, B, ldb, n2, partials, ctas, st);
+        gram_reduce(partials, ctas, na, n2, G, st, n1);
+        self_gram(B, n2, G + na, n1);
         return true;
     }
     if ((size_t)ctas * 4096 * sizeof(double) * (size_t)cdiv(n1, 64) > partial_bytes) return false;
