@@ -373,7 +373,8 @@ def run_ours(args, rank, world, dist):
                           "ms_ritz_per_step": float(np.sum([i["ms_ritz"] for i in infos])) / args.steps,
                           "host_phases_ms": timed_phases},
         "e2e": {"value": e2e_value, "unit": "vector products/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": float(np.mean(e2e_times))},
+                "d2h_bytes_per_step": d2h, "ms_per_step": float(np.mean(e2e_times)),
+                "step_ms": [round(float(t), 3) for t in e2e_times]},
         "gpu_launches": int(launches),
         "roofline": roof,
         "peaks_measured_here": {"tf32_dense_tflops": tf32_measured,

@@ -102,7 +102,14 @@ struct Gkl {
     cudaStream_t st;
     int64_t L, K;
     int k, r, pk, nQmax;
-    DevBuf Pb, Qb, Ptmp, Qtmp, Jd;
+    DevBuf Pb, Ptmp, Jd;
+    // The K-side basis and its restart copy (c5: 15 + 9 GB) are grow-only buffers kept per host thread
+    // across decompositions: allocated and freed per decomposition, they fragmented the stream-ordered
+    // pool with the plans' FFT intermediates, so later decompositions had to map new memory (host
+    // stalls of 25-600 ms in the first steps of a process, +10-30 ms on the first timed bench step).
+    struct KCache { DevBuf Qb, Qtmp; };
+    static KCache &kcache() { static thread_local KCache c; return c; }
+    DevBuf &Qb = kcache().Qb, &Qtmp = kcache().Qtmp;
     Staging sg;
     int nP = 0, nQ = 0;
     std::vector<double> Tm;   // nQmax x nQmax host, column-major
