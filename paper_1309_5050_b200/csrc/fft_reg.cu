@@ -11,8 +11,8 @@
 //             16/R0 butterflies in registers;
 //   stage s   radix 16, span Ns = R0·16^(s-1): one shared-memory exchange (Stockham output
 //             index (j − k)·16 + k + Ns·r, k = j mod Ns, read back strided), twiddles
-//             e^{∓2πi r k/(16 Ns)} from a per-stage table in shared memory (15 per k, stride 15:
-//             conflict-free 8-byte reads), then a 16-point DFT in registers (4 x 4, 32 real
+//             e^{∓2πi r k/(16 Ns)} from a per-stage table in shared memory (15 per k read as 16-B pairs,
+//             at a 144-B stride: conflict-free), then a 16-point DFT in registers (4 x 4, 32 real
 //             multiplies, 144 adds).
 //
 // Thread t holds x[t + NT·e] (e < 16) before the transform and X[t + NT·e] after it, so global
@@ -114,7 +114,13 @@ __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr int pad_size(int n) { return n + n / 16 + 1; }
 __host__ __device__ constexpr int r0_of(int lg) { return (lg & 3) ? (1 << (lg & 3)) : 16; }
 // twiddle-table entries of all radix-16 stages: Σ spans · 15 = N − R0
-__host__ __device__ constexpr int tw_count_c(int lg) { return (1 << lg) - r0_of(lg); }
+// Twiddle table: per radix-16 stage of span NS, for each k < NS the 15 factors e^{∓2πi r k/(16 NS)},
+// r = 1..15, plus one pad entry, at a stride of TWS = 18 complex values (144 B): the factors are read as
+// 8 16-B pairs, and the 144-B stride puts the 8 threads of a quarter-warp on disjoint banks.  The stage
+// of span NS starts at TWS·(NS − R0)/15 (= TWS·Σ of the earlier spans).
+constexpr int TWS = 18;
+__host__ __device__ constexpr int tw_off(int lg, int ns) { return TWS * ((ns - r0_of(lg)) / 15); }
+__host__ __device__ constexpr int tw_count_c(int lg) { return tw_off(lg, 1 << lg); }
 __host__ __device__ constexpr int H_of(int lg) { return (1 << lg) / 2 + 1; }
 
 template <int NT> __device__ __forceinline__ void xsync() {
@@ -174,12 +180,14 @@ __device__ __forceinline__ void stages16(float2 *v, float2 *S, const float2 *__r
     if constexpr (NS < N) {
         if constexpr (!SKIPX) exchange<NT, RP, NSP>(v, S, t);
         const int k = t & (NS - 1);
-        const float2 *w = tw + (NS - r0_of(LG)) + 15 * k;   // table of span NS starts at NS − R0
+        const float4 *w = reinterpret_cast<const float4 *>(tw + tw_off(LG, NS) + TWS * k);
 #pragma unroll
-        for (int r = 1; r < 16; ++r) {
-            float2 c = w[r - 1];
-            if (DIR > 0) c.y = -c.y;
-            v[r] = cmul(v[r], c);
+        for (int q = 0; q < 8; ++q) {
+            const float4 c4 = w[q];
+            float2 ca = make_float2(c4.x, c4.y), cb = make_float2(c4.z, c4.w);
+            if (DIR > 0) { ca.y = -ca.y; cb.y = -cb.y; }
+            v[2 * q + 1] = cmul(v[2 * q + 1], ca);
+            if (q < 7) v[2 * q + 2] = cmul(v[2 * q + 2], cb);
         }
         if constexpr (KEEP1 && NS * 16 == N) {
             float2 s0 = v[0], s1 = v[1];
@@ -550,11 +558,12 @@ rpass_b(const float2 *__restrict__ A, int ny_in, int lda, int H, int k, const fl
 // buffer + X̂ row (~100 KB at 2^12 points: 2 CTAs / SM, up to 128 registers per thread).
 template <int LG> struct CfgB2 {
     static constexpr int N = 1 << LG, NT = N / 16, THREADS = NT;
-    static constexpr size_t smem = Cfg<LG, true>::smem + sizeof(float2) * (size_t)N;
+    // X̂ row held per thread: element t + NT·e at Xs[t·TWS + e] (16-B pairs, 144-B thread stride)
+    static constexpr size_t smem = Cfg<LG, true>::smem + sizeof(float2) * (size_t)NT * TWS;
 };
-__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc) {
+__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -602,10 +611,12 @@ rpass_b2(const float2 *__restrict__ A, int ny_in, int lda, int H, int k, const f
     __syncthreads();   // twiddle table staged
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int fx = u / nch, j0 = (u - fx * nch) * JC, j1 = min(k, j0 + JC);
-        // X̂ row -> shared memory (16 B per copy; the previous unit's readers are past a barrier)
+        // X̂ row -> shared memory in the thread-major layout (8 B per copy, coalesced global reads; the
+        // previous unit's readers are past a barrier); read back as 8 16-B pairs per thread and item
         {
-            const float2 *xr = Xh + (int64_t)fx * N;
-            for (int i = t; i < N / 2; i += NT) cp_async16(Xs + 2 * i, xr + 2 * i);
+            const float2 *xr = Xh + (int64_t)fx * N + t;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) cp_async8(Xs + TWS * t + e, xr + NT * e);
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
         float2 v[16];
@@ -619,8 +630,15 @@ rpass_b2(const float2 *__restrict__ A, int ny_in, int lda, int H, int k, const f
                 __syncthreads();
                 xs_ready = true;
             }
+            {   // X̂ ⊙ conj(Â)
+                const float4 *xp = reinterpret_cast<const float4 *>(Xs + TWS * t);
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = cmulc(Xs[t + NT * e], v[e]);   // X̂ ⊙ conj(Â)
+                for (int q = 0; q < 8; ++q) {
+                    const float4 x4 = xp[q];
+                    v[2 * q] = cmulc(make_float2(x4.x, x4.y), v[2 * q]);
+                    v[2 * q + 1] = cmulc(make_float2(x4.z, x4.w), v[2 * q + 1]);
+                }
+            }
             float2 vn[16];
             if (j + 1 < j1) load_row(vn, j + 1, fx);   // in flight during the inverse transform
             if constexpr (KEEP1) {
@@ -931,7 +949,7 @@ void build_table(int lg, std::vector<float2> &h) {
         for (int k = 0; k < ns; ++k)
             for (int r = 1; r < 16; ++r) {
                 const double a = -2.0 * M_PI * (double)(r * k) / (16.0 * ns);
-                h[(size_t)(ns - R0) + 15 * k + (r - 1)] = make_float2((float)std::cos(a), (float)std::sin(a));
+                h[(size_t)tw_off(lg, ns) + (size_t)TWS * k + (r - 1)] = make_float2((float)std::cos(a), (float)std::sin(a));
             }
 }
 

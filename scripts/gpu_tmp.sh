@@ -1,10 +1,7 @@
 #!/bin/bash
-out=gpurun_out/s21; mkdir -p $out
+out=gpurun_out/s22; mkdir -p $out
 python -c "import __graft_entry__ as g; g.build()" > $out/build.log 2>&1 || { tail -20 $out/build.log; exit 1; }
-for i in 1 2; do
-SSA_DEBUG=1 timeout 600 python bench.py --no-cpu-baseline > $out/bench_c5_$i.json 2> $out/bench_c5_$i.err
-python -c "import json; d=json.loads(open('$out/bench_c5_$i.json').read().strip().splitlines()[-1]); print('run $i', round(d['ms_per_step'],2), d['step_ms'], d['e2e']['step_ms'], [p[1] for p in d['step_phases_ms']])" 2>&1 | tail -1
-grep -E "host ms: products" $out/bench_c5_$i.err | awk '{print $5}' | tr '\n' ';'; echo
-done
-timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 > $out/pytest_gpu.log 2>&1
-tail -3 $out/pytest_gpu.log
+for c in c5 c5 c3 c4; do timeout 300 python scripts/prof_products.py $c fft 2>&1 | tail -2; done
+timeout 900 python -m pytest tests -m gpu -q -x -k "product or recon or fft or sigma" --timeout 600 > $out/pytest.log 2>&1; tail -2 $out/pytest.log
+timeout 600 python bench.py --no-cpu-baseline > $out/bench_c5.json 2> $out/bench_c5.err
+python -c "import json; d=json.loads(open('$out/bench_c5.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['step_ms'], d.get('rank_r_time_ms'), d['roofline']['frac'], {k: v['avg_launch_ms'] for k, v in d['roofline']['products'].items()})"
