@@ -69,12 +69,13 @@ class ClockSampler:
 
     One long-running `nvidia-smi --loop-ms` process: its start-up (driver / NVML initialisation — on a
     fresh box the first nvidia-smi call stalled the GPU for ~0.9 s, and every new process for ~10 ms)
-    completes before __enter__ returns, so only its periodic queries overlap the timed steps.
+    completes before __enter__ returns (its first sample marks the start of the timed region), so only
+    its periodic queries overlap the timed steps.
     """
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index=0, period_ms=100):
+    def __init__(self, gpu_index=0, period_ms=50):
         self.idx = gpu_index
         self.period = period_ms
         self.samples = []
@@ -87,10 +88,10 @@ class ClockSampler:
             line = line.strip()
             if not line:
                 continue
-            if self._first.is_set():
-                self.samples.append([s.strip() for s in line.split(",")])
-            else:
-                self._first.set()          # the sample taken before the timed region: dropped
+            # the first sample is taken as the timed region starts (kept: short regions, c1-c4, may
+            # end before the next one)
+            self.samples.append([s.strip() for s in line.split(",")])
+            self._first.set()
 
     def __enter__(self):
         try:
