@@ -142,3 +142,38 @@ def test_full_rank_request_and_wide_block():
     np.testing.assert_allclose(p.sigma, s_or, rtol=1e-9, atol=1e-12 * s_or[0])
     recs = p.reconstruct([list(range(r))])
     np.testing.assert_allclose(recs[0], x, rtol=1e-9, atol=1e-9)
+
+
+_DEFER_SCRIPT = r"""
+import json
+import synth
+from paper_1309_5050_b200 import Plan
+w = synth.get("c4")
+p = Plan(w.data, w.window, mask=w.mask, wmask=w.wmask, dtype=w.dtype, block_k=w.block_k)
+info = p.decompose(w.r)
+print(json.dumps({"sigma": [float(s) for s in p.sigma], "n_block_products": info["n_block_products"],
+                  "max_rel_residual": info["max_rel_residual"]}))
+"""
+
+
+def test_deferred_orthonormalisation_matches_full():
+    """The K-side orthonormalisation deferred past a Ritz check (c4: checks after every
+    block pair) gives the decomposition of the undeferred solver: same block products, σ to the
+    fp32 floor, residual bound below tol in both."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, SSA_DEFER=flag, PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+        r = subprocess.run([sys.executable, "-c", _DEFER_SCRIPT], capture_output=True, text=True, env=env, cwd=root,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[flag] = json.loads(r.stdout.strip().splitlines()[-1])
+    a, b = out["0"], out["1"]
+    assert a["n_block_products"] == b["n_block_products"]
+    s0, s1 = np.array(a["sigma"]), np.array(b["sigma"])
+    assert np.max(np.abs(s0 - s1)) <= 1e-6 * s0[0]
+    assert a["max_rel_residual"] <= 1e-6 and b["max_rel_residual"] <= 1e-6
