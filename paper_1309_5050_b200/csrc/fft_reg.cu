@@ -989,7 +989,9 @@ void pass_a(int lg, const float *in, int64_t ld, const int *map, int bx, int by,
     SSA_REQUIRE(lda % 2 == 0 && ((uintptr_t)A & 15) == 0, SSA_ERR_ARG, "rfft pass A: rows must be 16-B aligned");
     RFFT_DISPATCH(lg, {
         using Cf = Cfg<LG>;
-        if (pipe_on() && !map && ((uintptr_t)in & 3) == 0) {
+        // (a 16-B aligned base keeps the staged ranges, which start at the 16-B boundary at or below each
+        // item, inside the input)
+        if (pipe_on() && !map && ((uintptr_t)in & 15) == 0) {
             const int grid = prep(rpass_a2<LG>, Cf::THREADS, CfgP<LG>::smem, cdiv(by, 2 * Cf::TPC) * (int64_t)k);
             rpass_a2<LG><<<grid, Cf::THREADS, CfgP<LG>::smem, st>>>(in, ld, bx, by, k, jsel, scale, A, lda, tw);
             break;
