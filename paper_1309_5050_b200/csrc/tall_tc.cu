@@ -78,7 +78,7 @@ struct Cfg {
 template <int NM, int NN, int BA, int RC, int KG>
 __global__ void __launch_bounds__(tallg::NTHR, 1)
 gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
-                int n1, int n2, int b_col, double *__restrict__ partials) {
+                int n1, int n2, int b_col, double *__restrict__ partials, int per) {
     using namespace tc;
     using C = tallg3::Cfg<NM, NN, BA, RC, KG>;
     constexpr int KS = C::KS, KA = C::KA, OPB = C::OPB, AB = C::ACCB;
@@ -164,10 +164,13 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (lane == 0) {
             // ---------------- MMA issuer ----------------
             constexpr uint32_t idesc = make_idesc(128, NN);
+            // accumulators live for `per` consecutive stages (one drain per period: the fp32 tensor-core
+            // accumulation then spans per·32·RC rows before the Kahan sums)
             for (int i = 0; i < nmy; ++i) {
-                const int o = i % OPB, b = i % AB;
+                const int pi = i / per, sp = i - pi * per;
+                const int o = i % OPB, b = pi % AB;
                 mbar_wait(conv(o), (i / OPB) & 1);
-                if (i >= AB) mbar_wait(acce(b), ((i / AB) - 1) & 1);
+                if (sp == 0 && pi >= AB) mbar_wait(acce(b), ((pi / AB) - 1) & 1);
                 tc_fence_after();
                 const uint32_t dbase = tmem + (uint32_t)(b * C::acc_cols);
                 const uint64_t bh0 = make_desc(b_hi(o, 0));
@@ -183,7 +186,7 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         for (int q = 0; q < KG; ++q) {
                             const int kk = g * KG + q;
                             const uint64_t bh = bh0 + (uint64_t)(kk >> 2) * rc_step + (uint64_t)(2 * (kk & 3));
-                            mma_tf32_ts(d, al + 8 * kk, bh, idesc, q ? 1u : 0u);
+                            mma_tf32_ts(d, al + 8 * kk, bh, idesc, (q || sp) ? 1u : 0u);
                             mma_tf32_ts(d, ah + 8 * kk, bh + b_lo_step, idesc, 1u);
                         }
 #pragma unroll
@@ -196,7 +199,7 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 }
                 mma_commit(ope(o));
-                mma_commit(accf(b));
+                if (sp == per - 1 || i == nmy - 1) mma_commit(accf(b));
             }
         }
     } else if (warp < 8) {
@@ -272,7 +275,8 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
         for (int j = 0; j < 32; ++j) { ks[j] = 0.f; kc[j] = 0.f; }
         const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        for (int i = 0; i < nmy; ++i) {
+        const int nper = (nmy + per - 1) / per;
+        for (int i = 0; i < nper; ++i) {
             const int b = i % AB;
             mbar_wait(accf(b), (i / AB) & 1);
             tc_fence_after();
@@ -913,7 +917,9 @@ static void launch_gram_tc3(int64_t M, const float *A, int64_t lda, int n1, cons
     auto kern = gram_tc3_kernel<NM, NN, BA, RC, KG>;
     set_max_smem(kern);
     const int gy = (int)cdiv(n1, NM * 128);
-    kern<<<dim3(ctas, gy), tallg::NTHR, tallg3::SMEM, st>>>(ma, mb, M, n1, n2, b_col, partials);
+    // stages per accumulator drain (measured at c5's K side, scripts/bench_tall_c5.py)
+    static const int per = [] { const char *e = std::getenv("SSA_GRAM_PER"); return e ? std::max(1, std::atoi(e)) : 4; }();
+    kern<<<dim3(ctas, gy), tallg::NTHR, tallg3::SMEM, st>>>(ma, mb, M, n1, n2, b_col, partials, per);
     after_launch("gram_tc3");
 }
 
