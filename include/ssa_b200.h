@@ -264,6 +264,13 @@ ssa_status ssa_bench_tall(int32_t which, int64_t M, int32_t n1, int32_t n2, int3
  * *ms = device time, *tflops = dense tf32 TFLOP/s (2·128·256·8 per MMA). */
 ssa_status ssa_bench_mma(int32_t iters, int32_t ctas, double *ms, double *tflops);
 
+/* Release the calling thread's solver workspace.  The K-side Lanczos basis and its restart copy
+ * (ssa_decompose; c5: 15 + 9 GB) are kept per host thread across decompositions and plans, grow-only,
+ * so that repeated plan / decompose / destroy cycles reuse them instead of fragmenting the
+ * stream-ordered memory pool; this call frees them (they are also freed at thread exit).  Safe to
+ * call at any time outside a running ssa_decompose on the same thread; SSA_OK. */
+ssa_status ssa_release_workspace(void);
+
 const char *ssa_last_error(void);
 const char *ssa_version(void);
 /* Number of kernels this library launched on the calling thread since the last

@@ -5,5 +5,5 @@ averaging, as hand-written sm_100a CUDA kernels behind a C ABI (include/ssa_b200
 This package never imports oracle/ (test infrastructure) and has no CPU fallback:
 importing the API requires the built libssa_b200.so.
 """
-from .api import Plan, version, launch_count  # noqa: F401
+from .api import Plan, version, launch_count, release_workspace  # noqa: F401
 from ._lib import SSAError, SO_PATH  # noqa: F401

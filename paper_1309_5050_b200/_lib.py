@@ -62,7 +62,8 @@ class ssa_decomp_info(C.Structure):
 EXPORTS = ["ssa_plan_create", "ssa_plan_destroy", "ssa_plan_info", "ssa_get_weights", "ssa_get_kmask",
            "ssa_matmul", "ssa_decompose", "ssa_get_rank", "ssa_get_sigma", "ssa_get_residuals", "ssa_get_u", "ssa_get_v",
            "ssa_set_triples", "ssa_reconstruct", "ssa_wcor", "ssa_last_error", "ssa_version",
-           "ssa_launch_count", "ssa_small_svd", "ssa_bench_tall", "ssa_bench_mma", "ssa_esprit", "ssa_forecast"]
+           "ssa_launch_count", "ssa_small_svd", "ssa_bench_tall", "ssa_bench_mma", "ssa_esprit", "ssa_forecast",
+           "ssa_release_workspace"]
 
 _lib = None
 
@@ -103,6 +104,7 @@ def load(path: str = SO_PATH):
     L.ssa_last_error.argtypes = []; L.ssa_last_error.restype = C.c_char_p
     L.ssa_version.argtypes = []; L.ssa_version.restype = C.c_char_p
     L.ssa_launch_count.argtypes = [C.c_int]; L.ssa_launch_count.restype = i64
+    L.ssa_release_workspace.argtypes = []; L.ssa_release_workspace.restype = C.c_int
     L.ssa_small_svd.argtypes = [i32, i32, p, C.POINTER(i32), C.POINTER(C.c_double)]
     L.ssa_small_svd.restype = st
     L.ssa_bench_tall.argtypes = [i32, C.c_int64, i32, i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]

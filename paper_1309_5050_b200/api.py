@@ -302,3 +302,8 @@ def version() -> str:
 
 def launch_count(reset: bool = False) -> int:
     return int(lib.load().ssa_launch_count(int(reset)))
+
+
+def release_workspace() -> None:
+    """Free the calling thread's cached solver workspace (ssa_release_workspace)."""
+    lib.check(lib.load().ssa_release_workspace())

@@ -650,6 +650,12 @@ static ssa_status check_plan(ssa_plan p) {
 
 extern "C" {
 
+ssa_status ssa_release_workspace(void) {
+    ssa::release_workspace();
+    if (cudaDeviceSynchronize() != cudaSuccess) cudaGetLastError();   // the frees are stream-ordered
+    return SSA_OK;
+}
+
 const char *ssa_last_error(void) { return g_err.c_str(); }
 const char *ssa_version(void) { return "ssa_b200 0.1 (sm_100a)"; }
 int64_t ssa_launch_count(int reset) {

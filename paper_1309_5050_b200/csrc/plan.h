@@ -79,6 +79,7 @@ template <typename T>
 void decompose_eigen(PlanImpl &p, int r, ssa_decomp_info *info);
 template <typename T>
 void decompose(PlanImpl &p, int r, ssa_decomp_info *info);
+void release_workspace();   // the calling thread's grow-only K-side solver buffers (solver.cu)
 
 // fft.cu
 bool fft_supported(const PlanImpl &p);

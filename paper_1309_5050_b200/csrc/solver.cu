@@ -96,6 +96,15 @@ void jacobi_svd_blocked(int m, int n, double *T, int *counters, int *sweeps, cud
 bool jacobi_blocked_fits(int m, int n);
 void ritz_tn(int m, int n, const double *T0, const double *A, double *W, double *nrm, cudaStream_t st);
 
+// per-thread grow-only K-side workspace (see Gkl::Qb; freed by ssa_release_workspace or at thread exit)
+struct KCache { DevBuf Qb, Qtmp; };
+static KCache &kside_cache() { static thread_local KCache c; return c; }
+void release_workspace() {
+    KCache &c = kside_cache();
+    c.Qb.release();
+    c.Qtmp.release();
+}
+
 template <typename T>
 struct Gkl {
     PlanImpl &p;
@@ -107,9 +116,7 @@ struct Gkl {
     // across decompositions: allocated and freed per decomposition, they fragmented the stream-ordered
     // pool with the plans' FFT intermediates, so later decompositions had to map new memory (host
     // stalls of 25-600 ms in the first steps of a process, +10-30 ms on the first timed bench step).
-    struct KCache { DevBuf Qb, Qtmp; };
-    static KCache &kcache() { static thread_local KCache c; return c; }
-    DevBuf &Qb = kcache().Qb, &Qtmp = kcache().Qtmp;
+    DevBuf &Qb = kside_cache().Qb, &Qtmp = kside_cache().Qtmp;
     Staging sg;
     int nP = 0, nQ = 0;
     std::vector<double> Tm;   // nQmax x nQmax host, column-major

@@ -90,3 +90,10 @@ def test_product_path_never_imports_oracle():
             if f.endswith((".cu", ".cpp", ".h")):
                 assert "oracle" not in open(os.path.join(dirpath, f)).read().lower().replace(
                     "oracle-matching", ""), f
+
+
+def test_release_workspace_is_safe_without_a_decomposition(lib):
+    """ssa_release_workspace frees the calling thread's cached K-side solver buffers; with none
+    allocated (or no device) it is a no-op that returns SSA_OK."""
+    assert lib.ssa_release_workspace() == 0
+    assert lib.ssa_release_workspace() == 0

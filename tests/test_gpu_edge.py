@@ -177,3 +177,18 @@ def test_deferred_orthonormalisation_matches_full():
     s0, s1 = np.array(a["sigma"]), np.array(b["sigma"])
     assert np.max(np.abs(s0 - s1)) <= 1e-6 * s0[0]
     assert a["max_rel_residual"] <= 1e-6 and b["max_rel_residual"] <= 1e-6
+
+
+def test_release_workspace_between_decompositions():
+    """The per-thread K-side workspace (grow-only across decompositions) can be released between
+    decompositions; the next decomposition re-allocates it and returns the same triples."""
+    from paper_1309_5050_b200 import Plan, release_workspace
+    w = synth.get("c3")
+    s = []
+    for _ in range(2):
+        p = Plan(w.data, w.window, dtype=w.dtype, block_k=w.block_k)
+        p.decompose(w.r)
+        s.append(np.array(p.sigma))
+        p.close()
+        release_workspace()
+    assert np.array_equal(s[0], s[1])
