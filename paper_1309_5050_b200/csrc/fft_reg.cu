@@ -669,8 +669,10 @@ rpass_b2(const float2 *__restrict__ A, int ny_in, int lda, int H, int k, const f
 
 // averaging: per (g, fx) Σ_{i∈I_g} DFT_y(AU_i) ⊙ DFT_y(AV_i), inverse; the AU transform of a member
 // waits in a thread-private shared-memory slot while the AV transform runs
+// (2^12 points: two CTAs per SM within 128 registers — c5's averaging was latency-bound at one;
+// smaller transforms spill at that budget and keep one)
 template <int LG>
-__global__ void __launch_bounds__(Cfg<LG, true>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg<LG, true>::THREADS, LG == 12 ? 2 : 1)
 rpass_bconv(const float2 *__restrict__ AU, int ly, int ldu, const float2 *__restrict__ AV, int ky, int ldv,
             const int *__restrict__ grp_off, const int *__restrict__ grp_idx, const int *__restrict__ slot, int H, int ng,
             float2 *__restrict__ B, int ny_out, int ldb, int cbc, const float2 *__restrict__ twg) {

@@ -917,8 +917,11 @@ static void launch_gram_tc3(int64_t M, const float *A, int64_t lda, int n1, cons
     auto kern = gram_tc3_kernel<NM, NN, BA, RC, KG>;
     set_max_smem(kern);
     const int gy = (int)cdiv(n1, NM * 128);
-    // stages per accumulator drain (measured at c5's K side, scripts/bench_tall_c5.py)
-    static const int per = [] { const char *e = std::getenv("SSA_GRAM_PER"); return e ? std::max(1, std::atoi(e)) : 4; }();
+    // stages per accumulator drain: 1.  Four (256 rows of fp32 tensor-core accumulation per Kahan
+    // step) was 0.3 ms faster per isolated c5 Gram (scripts/bench_tall_c5.py) but cost the c5
+    // decomposition 9 ms (49.5 -> 58.6 ms, measured twice): the coarser accumulation changed the
+    // orthonormalisation's decisions downstream.  SSA_GRAM_PER selects it for experiments.
+    static const int per = [] { const char *e = std::getenv("SSA_GRAM_PER"); return e ? std::max(1, std::atoi(e)) : 1; }();
     kern<<<dim3(ctas, gy), tallg::NTHR, tallg3::SMEM, st>>>(ma, mb, M, n1, n2, b_col, partials, per);
     after_launch("gram_tc3");
 }
