@@ -192,7 +192,10 @@ ssa_status ssa_decompose(ssa_plan p, int32_t r, ssa_decomp_info *info);
  * P:1720-1723).  Signs: the largest-|.| entry of each U_i is positive. */
 ssa_status ssa_get_rank(ssa_plan p, int32_t *r);
 ssa_status ssa_get_sigma(ssa_plan p, double *sigma);
-/* Per-triple residual bounds ||Xᵀu_i − σ_i v_i|| (r doubles, absolute) of the last decomposition. */
+/* Per-triple residual bounds ||Xᵀu_i − σ_i v_i|| (r doubles, absolute) of the last decomposition.
+ * When the final convergence check was taken with the K-side orthonormalisation of the last block
+ * deferred, the bounds use A_last ≈ R₁ (the pass-1 Cholesky factor) and convergence was
+ * only accepted with every bound below tol·σ_1 / 2. */
 ssa_status ssa_get_residuals(ssa_plan p, double *res);
 ssa_status ssa_get_u(ssa_plan p, void *U, int on_device);
 ssa_status ssa_get_v(ssa_plan p, void *V, int on_device);
