@@ -4,11 +4,16 @@
 // thread, operands resident in shared memory (128-B swizzled K-major tiles, contents irrelevant
 // for the rate), alternating between two TMEM accumulators; one commit + mbarrier wait at the end.
 // The rate is 2·128·256·8 flops per MMA over the kernel's device time.
+#include <cstdlib>
+
 #include "common.h"
 #include "tc_common.h"
 
 namespace ssa {
 
+// N (accumulator width) and TS (A operand from tensor memory, as the Gram / update kernels issue it)
+// are measurement variants: SSA_MMA_N = 64 / 128 / 256 (default 256), SSA_MMA_TS = 1
+template <int N, bool TS>
 __global__ void __launch_bounds__(128, 1) mma_peak_kernel(int iters, int *sink) {
     using namespace tc;
     extern __shared__ unsigned char smem_raw[];
@@ -31,8 +36,14 @@ __global__ void __launch_bounds__(128, 1) mma_peak_kernel(int iters, int *sink) 
     if (threadIdx.x == 32) {
         const uint64_t adesc = make_desc(smem_u32(smem));               // A: 128 rows x 128 B
         const uint64_t bdesc = make_desc(smem_u32(smem + 16 * 1024));   // B: 256 rows x 128 B
-        constexpr uint32_t idesc = make_idesc(128, 256);
-        for (int i = 0; i < iters; ++i) mma_tf32(tmem + (uint32_t)((i & 1) * 256), adesc, bdesc, idesc, i > 1);
+        constexpr uint32_t idesc = make_idesc(128, N);
+        if constexpr (TS) {
+            // A (128 lanes x 8 tf32) from tensor-memory columns [256, 264); accumulators alternate in [0, 256)
+            for (int i = 0; i < iters; ++i)
+                mma_tf32_ts(tmem + (uint32_t)((i & 1) * (N <= 128 ? N : 0)), tmem + 256u, bdesc, idesc, i > 1);
+        } else {
+            for (int i = 0; i < iters; ++i) mma_tf32(tmem + (uint32_t)((i & 1) * 256), adesc, bdesc, idesc, i > 1);
+        }
         mma_commit(smem_u32(bar));
     }
     __syncwarp();
@@ -58,14 +69,21 @@ extern "C" ssa_status ssa_bench_mma(int32_t iters, int32_t ctas, double *ms, dou
         DevBuf sink;
         sink.alloc(16, nullptr);
         const size_t smem = 48 * 1024 + 1024 + 64;
-        set_max_smem(mma_peak_kernel);
-        mma_peak_kernel<<<ctas, 128, smem>>>(8, sink.as<int>());   // warm-up
+        static const int nvar = [] { const char *e = std::getenv("SSA_MMA_N"); return e ? std::atoi(e) : 256; }();
+        static const int ts = [] { const char *e = std::getenv("SSA_MMA_TS"); return e ? std::atoi(e) : 0; }();
+        auto kern = mma_peak_kernel<256, false>;
+        if (nvar == 64) kern = ts ? mma_peak_kernel<64, true> : mma_peak_kernel<64, false>;
+        else if (nvar == 128) kern = ts ? mma_peak_kernel<128, true> : mma_peak_kernel<128, false>;
+        else if (ts) kern = mma_peak_kernel<256, true>;
+        const int nmma = (nvar == 64 || nvar == 128) ? nvar : 256;
+        set_max_smem(kern);
+        kern<<<ctas, 128, smem>>>(8, sink.as<int>());   // warm-up
         after_launch("mma_peak");
         cudaEvent_t e0, e1;
         SSA_CUDA(cudaEventCreate(&e0));
         SSA_CUDA(cudaEventCreate(&e1));
         SSA_CUDA(cudaEventRecord(e0, nullptr));
-        mma_peak_kernel<<<ctas, 128, smem>>>(iters, sink.as<int>());
+        kern<<<ctas, 128, smem>>>(iters, sink.as<int>());
         after_launch("mma_peak");
         SSA_CUDA(cudaEventRecord(e1, nullptr));
         SSA_CUDA(cudaEventSynchronize(e1));
@@ -74,7 +92,7 @@ extern "C" ssa_status ssa_bench_mma(int32_t iters, int32_t ctas, double *ms, dou
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (ms) *ms = t;
-        if (tflops) *tflops = 2.0 * 128 * 256 * 8 * (double)iters * ctas / (t * 1e-3) / 1e12;
+        if (tflops) *tflops = 2.0 * 128 * nmma * 8 * (double)iters * ctas / (t * 1e-3) / 1e12;
         return SSA_OK;
     } catch (const Error &e) {
         ssa_set_error(e.what());

@@ -7,5 +7,5 @@ from paper_1309_5050_b200 import _lib
 L = _lib.load()
 which, n1, n2 = (int(a) for a in sys.argv[1:4])
 ms = C.c_double(); ck = C.c_double()
-st = L.ssa_bench_tall(which, 14753281, n1, n2, 1, C.byref(ms), C.byref(ck))
+st = L.ssa_bench_tall(which, 14753281, n1, n2, 2, C.byref(ms), C.byref(ck))
 print(which, n1, n2, st, ms.value * 1e3, "us")
