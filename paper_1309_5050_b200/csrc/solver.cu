@@ -175,22 +175,28 @@ struct Gkl {
 
     bool kside_comm() const { return p.has_comm && p.comm.world > 1; }
 
-    // G (n1 x n2, host, column-major ld n1) = Aᵀ B; one launch per 512 x 64 chunk, one sync.
+    // G (n1 x n2, host, column-major ld n1) = Aᵀ B; one launch per 512 x 64 chunk, one sync.  Without a
+    // cross-rank reduction the Gram's final reduce kernel writes straight into the pinned staging block
+    // (host memory mapped into the device address space): no copy-engine transfer on the round trip.
     void gram(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb, int n2, double *G, bool kside) {
         struct Chunk { int a0, na, b0, nb; size_t idx; };
+        static const bool zc_env = [] { const char *e = std::getenv("SSA_GRAM_ZC"); return e ? std::atoi(e) != 0 : true; }();
+        const bool reduce = kside && kside_comm();
+        const bool zc = zc_env && !reduce;
         std::vector<Chunk> ch;
         for (int a0 = 0; a0 < n1; a0 += 512) {
             const int na = std::min(512, n1 - a0);
             for (int b0 = 0; b0 < n2; b0 += 64) {
                 const int nb = std::min(64, n2 - b0);
                 const size_t idx = sg.take((size_t)na * nb);
-                gram_tn<T>(M, A + lda * a0, lda, na, B + ldb * b0, ldb, nb, sg.dev(idx), p.ws_gram.as<double>(),
-                           p.ws_gram.bytes, st);
-                if (kside && kside_comm()) {
+                gram_tn<T>(M, A + lda * a0, lda, na, B + ldb * b0, ldb, nb, zc ? sg.h + idx : sg.dev(idx),
+                           p.ws_gram.as<double>(), p.ws_gram.bytes, st);
+                if (reduce) {
                     if (p.comm.allreduce_sum(p.comm.user, sg.dev(idx), (int64_t)na * nb, SSA_F64, st) != 0)
                         throw Error(SSA_ERR_COMM, "allreduce of a K-side Gram failed");
                 }
-                SSA_CUDA(cudaMemcpyAsync(sg.h + idx, sg.dev(idx), sizeof(double) * na * nb, cudaMemcpyDeviceToHost, st));
+                if (!zc)
+                    SSA_CUDA(cudaMemcpyAsync(sg.h + idx, sg.dev(idx), sizeof(double) * na * nb, cudaMemcpyDeviceToHost, st));
                 ch.push_back({a0, na, b0, nb, idx});
             }
         }
@@ -216,6 +222,7 @@ struct Gkl {
                 double *h = sg.h + idx;
                 for (int b = 0; b < nc; ++b)
                     for (int a = 0; a < mc; ++a) h[a + (size_t)mc * b] = C[(m0 + a) + (int64_t)ldc * (c0 + b)];
+                // (a kernel reading the pinned block through its device mapping was slower: c2 7.6 -> 7.7-8.0 ms)
                 SSA_CUDA(cudaMemcpyAsync(sg.dev(idx), h, sizeof(double) * mc * nc, cudaMemcpyHostToDevice, st));
                 if (inplace)
                     gemm_small<T>(M, A + lda * m0, lda, mc, sg.dev(idx), mc, nc, alpha, (m0 == 0) ? beta : 1.0,
