@@ -601,6 +601,17 @@ struct Gkl {
         nP += k;
     }
 
+    // Lanczos recurrence term of a new K block W = Xᵀ·P(pc): W −= Q_prev·Bᵀ with B = T[P_new, Q_prev]
+    // (known exactly), removed before the full projection so that the projection only removes
+    // rounding-level components and one CGS pass normally suffices
+    void remove_recurrence(T *W, int pc) {
+        const int qc = nQ - k;
+        std::vector<double> Bt((size_t)k * k);
+        for (int a = 0; a < k; ++a)
+            for (int b = 0; b < k; ++b) Bt[b + (size_t)k * a] = Tat(pc + a, qc + b);   // (T block)ᵀ
+        gemm(K, Q(qc), ldQ, k, Bt.data(), k, k, -1.0, 1.0, W, ldQ);
+    }
+
     void stepB() {
         const int pc = nP - k;
         T *W = Q(nQ);
@@ -611,18 +622,7 @@ struct Gkl {
         // its orthonormalisation (na = 0: orth's pass-0 WᵀW) instead of a Gram of its own (a 3.8 GB
         // stream on c5)
         anorm_from_next_gram = anorm == 0.0;
-        auto recurrence = [&]() {
-            if (nQ > 0) {
-                // remove the recurrence term first (W -= Q_prev·Bᵀ with B = T[P_new, Q_prev], known
-                // exactly), so that the full projection below only removes rounding-level
-                // components and one CGS pass normally suffices
-                const int qc = nQ - k;
-                std::vector<double> Bt((size_t)k * k);
-                for (int a = 0; a < k; ++a)
-                    for (int b = 0; b < k; ++b) Bt[b + (size_t)k * a] = Tat(pc + a, qc + b);   // (T block)ᵀ
-                gemm(K, Q(qc), ldQ, k, Bt.data(), k, k, -1.0, 1.0, W, ldQ);
-            }
-        };
+        auto recurrence = [&]() { if (nQ > 0) remove_recurrence(W, pc); };
         t0 = now_ms();
         // full reorthogonalisation of the K side as well (CGS2 against the whole K basis): the
         // one-sided variant needed several times more products with thick restarts.
@@ -658,13 +658,7 @@ struct Gkl {
         product_xtu(P(pc), W, k);
         tw_prod += now_ms() - t0;
         t0 = now_ms();
-        {   // recurrence term, as stepB
-            const int qc = nQ - k;
-            std::vector<double> Bt((size_t)k * k);
-            for (int a = 0; a < k; ++a)
-                for (int b = 0; b < k; ++b) Bt[b + (size_t)k * a] = Tat(pc + a, qc + b);
-            gemm(K, Q(qc), ldQ, k, Bt.data(), k, k, -1.0, 1.0, W, ldQ);
-        }
+        remove_recurrence(W, pc);
         G1def.assign((size_t)n1 * k, 0.0);
         gram(K, Q(0), ldQ, n1, W, ldQ, k, G1def.data(), true);
         // orth3's pass-1 tests; any of them (breakdown, DGKS reprojection, failed or shifted
