@@ -369,7 +369,7 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
         SSA_CUDA(cudaMemsetAsync(p.kmask.p, 1, nk, st));
         p.full_k = true;
         p.K = nk;
-    } else if (p.full_window && !std::getenv("SSA_PLAN_CORR")) {
+    } else if (p.full_window) {
         // rectangular window: 𝔎 by separable box sums of 1_𝔑 (exact int32; same set as the
         // correlation below, without an L·K-flop kernel)
         DevBuf tmp;
@@ -436,7 +436,7 @@ static void build_plan(PlanImpl &p, const ssa_array *x, const uint8_t *mask_host
         weights_rect(p.nx, p.ny, p.lx, p.ly, p.weights.as<int32_t>(), st);
         p.n_excluded = p.n_valid - nxy;   // all cells valid in this case -> 0
         if (p.n_excluded < 0) p.n_excluded = 0;
-    } else if (p.full_window && !std::getenv("SSA_PLAN_CORR")) {
+    } else if (p.full_window) {
         // 𝕎 = box sum of 1_𝔎 over the window (exact int32)
         DevBuf tmp;
         tmp.alloc(sizeof(int32_t) * (size_t)p.nx * p.ky, st);

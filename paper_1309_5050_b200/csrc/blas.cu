@@ -132,7 +132,7 @@ template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.as
 template <int NB>
 __global__ void __launch_bounds__(256, 1)
 gram_stream_kernel(int64_t M, const float *__restrict__ A, int64_t lda, int n1, const float *__restrict__ B,
-                   int64_t ldb, int n2, int YG, int contig, double *__restrict__ partials) {
+                   int64_t ldb, int n2, int YG, double *__restrict__ partials) {
     using namespace gram2;
     extern __shared__ __align__(16) unsigned char gs_raw[];
     float *sm = reinterpret_cast<float *>(gs_raw);
@@ -166,16 +166,10 @@ gram_stream_kernel(int64_t M, const float *__restrict__ A, int64_t lda, int n1, 
     // zero the column padding once (columns n1c..ncolA-1 and n2..NB-1 stay zero)
     for (int idx = tid; idx < STAGES * stage_f; idx += NT) sm[idx] = 0.f;
     __syncthreads();
-    // chunks of this CTA: a contiguous range (contig) or every gridDim.x-th chunk
-    int64_t c0, cstep, my;
-    if (contig) {
-        const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
-        c0 = blockIdx.x * per; cstep = 1;
-        my = max((int64_t)0, min(per, nchunks - c0));
-    } else {
-        c0 = blockIdx.x; cstep = gridDim.x;
-        my = (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x;
-    }
+    // chunks of this CTA: a contiguous range
+    const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+    const int64_t c0 = blockIdx.x * per, cstep = 1;
+    const int64_t my = max((int64_t)0, min(per, nchunks - c0));
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < my) load(c0 + (int64_t)s * cstep, s);
@@ -259,25 +253,23 @@ gram_stream_kernel(int64_t M, const float *__restrict__ A, int64_t lda, int n1, 
 
 static bool gram_stream(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2,
                         double *G, double *partials, size_t partial_bytes, cudaStream_t st) {
-    static const bool off = std::getenv("SSA_GRAM_OLD") != nullptr;
-    if (off || M < 4096 || (lda & 3) || (ldb & 3) || ((uintptr_t)A & 15) || ((uintptr_t)B & 15) || n2 > 64) return false;
+    if (M < 4096 || (lda & 3) || (ldb & 3) || ((uintptr_t)A & 15) || ((uintptr_t)B & 15) || n2 > 64) return false;
     const int NB = n2 <= 32 ? 32 : 64;
     const int tiles = (NB == 32) ? 4 : 2;               // 64 x NB tiles computed in parallel per CTA
     const int ych = (int)cdiv(n1, 64);
     const int YG = std::min(ych, tiles);
     const int gy = (int)cdiv(ych, YG);
     const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, gram2::R));
-    static const int contig = [] { const char *e = std::getenv("SSA_GRAM_CONTIG"); return e ? std::atoi(e) : 1; }();
     if ((size_t)ctas * 4096 * sizeof(double) * (size_t)ych > partial_bytes) return false;
     // pipeline stages; reused at the end for the row-group combine ([RG][YG][64][NB] doubles)
     const size_t smem = std::max(sizeof(float) * (size_t)gram2::STAGES * (64 * YG + NB) * gram2::LDR,
                                  sizeof(double) * (size_t)tiles * 64 * NB);
     if (NB == 32) {
         set_max_smem(gram_stream_kernel<32>);
-        gram_stream_kernel<32><<<dim3(ctas, gy), 256, smem, st>>>(M, A, lda, n1, B, ldb, n2, YG, contig, partials);
+        gram_stream_kernel<32><<<dim3(ctas, gy), 256, smem, st>>>(M, A, lda, n1, B, ldb, n2, YG, partials);
     } else {
         set_max_smem(gram_stream_kernel<64>);
-        gram_stream_kernel<64><<<dim3(ctas, gy), 256, smem, st>>>(M, A, lda, n1, B, ldb, n2, YG, contig, partials);
+        gram_stream_kernel<64><<<dim3(ctas, gy), 256, smem, st>>>(M, A, lda, n1, B, ldb, n2, YG, partials);
     }
     after_launch("gram_stream");
     gram_reduce_kernel<<<(unsigned)cdiv((int64_t)n1 * n2 * 32, 256), 256, 0, st>>>(partials, ctas, n1, n2, G, n1);
@@ -470,9 +462,8 @@ tall_update_kernel(int64_t M, const float *A, int64_t lda, int m, const double *
 static bool tall_update(int64_t M, const float *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
                         double beta, float *Out, int64_t ldo, cudaStream_t st) {
     // measured (scripts/bench_tall.py): faster than the thread-per-row kernel only for wide
-    // blocks (m >= 256, n > 32: 4.2 vs 7.1 ms at M = 1.8M, m = 356, n = 64); SSA_UPD=1 forces it
-    static const int mode = [] { const char *e = std::getenv("SSA_UPD"); return e ? std::atoi(e) : -1; }();
-    if (mode == 0 || (mode < 0 && !(m >= 256 && n > 32))) return false;
+    // blocks (m >= 256, n > 32: 4.2 vs 7.1 ms at M = 1.8M, m = 356, n = 64)
+    if (!(m >= 256 && n > 32)) return false;
     if (M < 8192 || n > 64 || m > 512 || (lda & 3) || (ldo & 1) || ((uintptr_t)A & 15) || ((uintptr_t)Out & 7))
         return false;
     const int NC = n <= 32 ? 32 : 64;
@@ -616,8 +607,7 @@ gemm_acc_split_kernel(int64_t M, const T *A, int64_t lda, int m, const double *_
 template <typename T>
 static bool gemm_split(int64_t M, const T *A, int64_t lda, int m, const double *C, int ldc, int n, double alpha,
                        double beta, T *Out, int64_t ldo, cudaStream_t st) {
-    static const bool split_off = std::getenv("SSA_SPLIT_OFF") != nullptr;
-    if (M >= 16384 || split_off || n > 64) return false;
+    if (M >= 16384 || n > 64) return false;
     const unsigned g = (unsigned)cdiv(M, 32);
     if (n <= 32) {
         const size_t smem = sizeof(T) * ((size_t)m * 32 + 8 * 32 * 33);

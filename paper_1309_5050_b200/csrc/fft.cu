@@ -486,8 +486,6 @@ static int threads_for(int lg, int nb, int64_t nctas) {
 }
 
 static int batch_for(int lg, int target) {
-    static const int scale = [] { const char *e = std::getenv("SSA_FFT_BATCH"); return e ? std::atoi(e) : 0; }();
-    if (scale > 0) target = scale;
     return std::max(1, target >> lg);
 }
 
@@ -671,8 +669,7 @@ static void correlate(PlanImpl &p, const T *in, int64_t ldin, const int *imap, i
         ensure<T>(f, f.bufA, f.capA, sizeof(cplx<T>) * (size_t)kc * f.Hx * row_ld(by), p.st);
         ensure<T>(f, f.bufB, f.capB, sizeof(cplx<T>) * (size_t)kc * f.Hx * b_cols(f, oy), p.st);
         pass_a<T>(f, in + ldin * j0, ldin, imap, bx, by, kc, nullptr, nullptr, f.bufA.as<cplx<T>>(), p.st);
-        static const bool nofold = std::getenv("SSA_FFT_NOFOLD") != nullptr;
-        if (f.gk.p && !nofold && by <= 2 && (int64_t)by * oy <= 64) {
+        if (f.gk.p && by <= 2 && (int64_t)by * oy <= 64) {
             // MSSA-like shapes (few rows in and out): pass B folded into pass C
             pass_c<T>(f, nullptr, oy, kc, ox, out + ldo * j0, ldo, omap, nullptr, 0, p.st, f.bufA.as<cplx<T>>(), by);
         } else {

@@ -935,11 +935,6 @@ rpass_c2(const float2 *__restrict__ B, int oy, int H, int k, int ox, float inv, 
     }
 }
 
-// pipelined passes A / C (default; SSA_RPASS_PIPE=0 selects the single-buffered kernels)
-static bool pipe_on() {
-    static const int v = [] { const char *e = std::getenv("SSA_RPASS_PIPE"); return e ? std::atoi(e) : 1; }();
-    return v > 0;
-}
 
 // ------------------------------------------------------------------------------------ host side
 int tw_count(int lg) { return tw_count_c(lg); }
@@ -993,7 +988,7 @@ void pass_a(int lg, const float *in, int64_t ld, const int *map, int bx, int by,
         using Cf = Cfg<LG>;
         // (a 16-B aligned base keeps the staged ranges, which start at the 16-B boundary at or below each
         // item, inside the input)
-        if (pipe_on() && !map && ((uintptr_t)in & 15) == 0) {
+        if (!map && ((uintptr_t)in & 15) == 0) {
             const int grid = prep(rpass_a2<LG>, Cf::THREADS, CfgP<LG>::smem, cdiv(by, 2 * Cf::TPC) * (int64_t)k);
             rpass_a2<LG><<<grid, Cf::THREADS, CfgP<LG>::smem, st>>>(in, ld, bx, by, k, jsel, scale, A, lda, tw);
             break;
@@ -1025,10 +1020,9 @@ static void pass_b_lg(const float2 *A, int ny_in, int lda, int H, int k, const f
                       int ldb, int cbc, const float2 *tw, cudaStream_t st) {
     using Cf = Cfg<LG, true>;
     // X̂-resident form by default (c5: Xᵀ·U 5.59 -> 5.42 ms, X·V 5.45 -> 5.39 ms per block product);
-    // SSA_RPASS_B2=0 selects the item-per-row form above
-    static const int b2 = [] { const char *e = std::getenv("SSA_RPASS_B2"); return e ? std::atoi(e) : 1; }();
+    // (k = 1: the item-per-row form above)
     if constexpr (Cf::TPC == 1) {
-        if (b2 > 0 && k > 1) {
+        if (k > 1) {
             constexpr int JC = 16;
             const int64_t units = (int64_t)H * cdiv(k, JC);
             auto launch2 = [&](auto kern) {
@@ -1094,7 +1088,7 @@ void pass_c(int lg, const float2 *B, int oy, int ldb, int cblk, int H, int k, in
         static_assert(2 * Cfg<LG>::H <= Cfg<LG>::XB, "column pair fits the exchange buffer");
         const int grid = prep(rpass_c<LG>, Cf::THREADS, Cf::smem, cdiv(oy, 2 * Cf::TPC) * (int64_t)k);
         SSA_REQUIRE(cblk == 0 || cblk % (2 * Cf::TPC) == 0, SSA_ERR_ARG, "rfft pass C: block width");
-        if (pipe_on() && cblk == 2 * Cf::TPC && H == Cf::H) {
+        if (cblk == 2 * Cf::TPC && H == Cf::H) {
             const int g2 = prep(rpass_c2<LG>, Cf::THREADS, CfgP<LG>::smem, cdiv(oy, 2 * Cf::TPC) * (int64_t)k);
             rpass_c2<LG><<<g2, Cf::THREADS, CfgP<LG>::smem, st>>>(B, oy, H, k, ox, inv, out, ldo, omap, w, stride, tw, cs);
             break;

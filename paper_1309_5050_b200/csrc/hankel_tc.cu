@@ -462,13 +462,9 @@ static void tc_run(const TcCorrParams &P, int j0, cudaStream_t st) {
     }
     const CUtensorMap &mAh = it->second.ah, &mAl = it->second.al, &mB = it->second.b;
     // split the reduction (d_y first, then k-block ranges of whole chunks) to ~one CTA per SM
-    static const int target = [] {
-        const char *e = std::getenv("SSA_TC_CTAS");
-        return e ? std::max(1, std::atoi(e)) : 0;
-    }();
     const int64_t per_split = (int64_t)a.ntiles * 256 * 128 * sizeof(float);
     const int64_t max_ws = std::max<int64_t>(1, (int64_t)(P.ws_bytes / per_split));
-    int64_t want = std::max<int64_t>(1, (target ? target : num_sms()) / a.ntiles);
+    int64_t want = std::max<int64_t>(1, num_sms() / a.ntiles);
     want = std::min(want, 8 * max_ws);   // clusters of 8 keep one partial tile per cluster
     int64_t nsy = std::min<int64_t>(want, P.by);
     a.dy_split = (int)cdiv(P.by, nsy);

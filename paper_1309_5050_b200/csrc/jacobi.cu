@@ -299,17 +299,6 @@ __device__ __forceinline__ bool pair_rotation(double al, double be, double ga, d
     return true;
 }
 
-// debug timeline (SSA_JACOBI_TRACE): CTA 0 thread 0 globaltimer at the phase boundaries of the
-// first 32 rounds: [round][0 start, 1 Gram done, 2 steps done, 3 C·V done, 4 cluster barrier done]
-__device__ unsigned long long *g_jac_trace = nullptr;
-__device__ __forceinline__ void jtrace(int round, int ph) {
-    if (g_jac_trace && blockIdx.x == 0 && threadIdx.x == 0 && round < 32) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_jac_trace[round * 5 + ph] = t;
-    }
-}
-
 template <int NC>
 __global__ void __launch_bounds__(256, 1)
 jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, float early, int max_sweeps,
@@ -378,7 +367,6 @@ jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, floa
         if (tid == 0) { rot_sh = 0; mrel_sh = 0; }
         for (int round = 0; round < nb - 1; ++round, ++t) {
             const double *C = bufs + cur * NC * ldc;
-            if (sweep == 0) jtrace(round, 0);
             // ---- 1. Gram G = CᵀC (tensor cores), k split over warps when there are few tiles
             {
                 const int ks = warp % Cfg::KSPLIT;
@@ -410,7 +398,6 @@ jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, floa
                 Vs[x * LDG + y] = (x == y) ? 1.0 : 0.0;
             }
             __syncthreads();
-            if (sweep == 0) jtrace(round, 1);
             // ---- 2. Jacobi steps on G, V accumulated: G_new = Jᵀ G J, V_new = V J (ping-pong
             // buffers, one barrier per step).  Every warp computes the NC/2 rotations of the step
             // (lane w -> pair w; identical on every warp) and hands them to the lanes owning
@@ -468,7 +455,6 @@ jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, floa
                 if (rot) rot_sh = 1;   // benign races: every writer stores 1 / a larger value
                 if (lane == 0 && mrel > 0.f) atomicMax(&mrel_sh, __float_as_int(mrel));
             }
-            if (sweep == 0) jtrace(round, 2);
             // ---- 3. C·V on the tensor cores, stored into the next-round buffers
             {
                 const double *V = Vs + gi * NC * LDG;
@@ -517,9 +503,7 @@ jacobi_gram_kernel(int m, int n, int nb, double *__restrict__ A, float tol, floa
                     }
                 }
             }
-            if (sweep == 0) jtrace(round, 3);
             cluster.sync();
-            if (sweep == 0) jtrace(round, 4);
             cur ^= 1;
         }
         // convergence: no rotation anywhere, or the largest relative off-diagonal rotated in this
@@ -574,24 +558,8 @@ static bool launch_gram(int m, int n, double *T, int *sweeps, cudaStream_t st, f
     attr[0].val.clusterDim.x = ncta; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr; cfg.numAttrs = 1;
     int max_sweeps = 60;
-    static unsigned long long *tb = nullptr;
-    if (std::getenv("SSA_JACOBI_TRACE") && !tb) {
-        SSA_CUDA(cudaMalloc(&tb, 32 * 5 * 8));
-        SSA_CUDA(cudaMemset(tb, 0, 32 * 5 * 8));
-        SSA_CUDA(cudaMemcpyToSymbol(g_jac_trace, &tb, sizeof(tb)));
-    }
     SSA_CUDA(cudaLaunchKernelEx(&cfg, kern, m, n, nb, T, tol, early, max_sweeps, sweeps));
     after_launch("jacobi_gram");
-    if (tb) {
-        unsigned long long h[32 * 5];
-        SSA_CUDA(cudaStreamSynchronize(st));
-        SSA_CUDA(cudaMemcpy(h, tb, sizeof(h), cudaMemcpyDeviceToHost));
-        std::fprintf(stderr, "[jacobi trace] m=%d n=%d nb=%d (us per phase: gram steps cv sync)\n", m, n, nb);
-        for (int r = 0; r < std::min(nb - 1, 6); ++r)
-            std::fprintf(stderr, "  round %d: %.2f %.2f %.2f %.2f\n", r, (h[r * 5 + 1] - h[r * 5]) * 1e-3,
-                         (h[r * 5 + 2] - h[r * 5 + 1]) * 1e-3, (h[r * 5 + 3] - h[r * 5 + 2]) * 1e-3,
-                         (h[r * 5 + 4] - h[r * 5 + 3]) * 1e-3);
-    }
     return true;
 }
 
@@ -624,16 +592,8 @@ static bool launch_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st
 
 // prefer the cluster kernel; fall back to the cooperative-grid kernel for large n
 static bool jacobi_try_cluster(int m, int n, double *T, int *sweeps, cudaStream_t st, float tol, float early) {
-    if (std::getenv("SSA_JACOBI_GRID")) return false;
-    static const int nc_env = [] { const char *e = std::getenv("SSA_JACOBI_NC"); return e ? std::atoi(e) : 16; }();
-    if (nc_env == 16 && launch_gram<16>(m, n, T, sweeps, st, tol, early)) return true;
-    if ((nc_env == 16 || nc_env == 32) && launch_gram<32>(m, n, T, sweeps, st, tol, early)) return true;
-    static const int bw16 = std::getenv("SSA_JACOBI_BW16") ? 1 : 0;
-    if (bw16 && n <= 256) {
-        if (m <= 128) return launch_cluster<4, 16>(m, n, T, sweeps, st, tol);
-        if (m <= 192) return launch_cluster<6, 16>(m, n, T, sweeps, st, tol);
-        if (m <= 256) return launch_cluster<8, 16>(m, n, T, sweeps, st, tol);
-    }
+    if (launch_gram<16>(m, n, T, sweeps, st, tol, early)) return true;
+    if (launch_gram<32>(m, n, T, sweeps, st, tol, early)) return true;
     if (m <= 128) return n <= 256 ? launch_cluster<4, 8>(m, n, T, sweeps, st, tol) : launch_cluster<4, 16>(m, n, T, sweeps, st, tol);
     if (m <= 192) return n <= 256 ? launch_cluster<6, 8>(m, n, T, sweeps, st, tol) : launch_cluster<6, 16>(m, n, T, sweeps, st, tol);
     if (m <= 256) return n <= 256 ? launch_cluster<8, 8>(m, n, T, sweeps, st, tol) : launch_cluster<8, 16>(m, n, T, sweeps, st, tol);

@@ -36,11 +36,8 @@ namespace ssa {
 
 // Host wait for everything queued on `st`: an event polled in a tight loop (the solver waits
 // ~60 times per decomposition for small Gram results; a blocking stream synchronisation adds
-// the OS wake-up latency to every one of these round trips).  SSA_BLOCKING_SYNC=1 restores
-// cudaStreamSynchronize.
+// the OS wake-up latency to every one of these round trips).
 static void stream_wait(cudaStream_t st) {
-    static const bool blocking = std::getenv("SSA_BLOCKING_SYNC") != nullptr;
-    if (blocking) { SSA_CUDA(cudaStreamSynchronize(st)); return; }
     static thread_local cudaEvent_t ev = nullptr;
     if (!ev) SSA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     SSA_CUDA(cudaEventRecord(ev, st));
@@ -180,9 +177,8 @@ struct Gkl {
     // (host memory mapped into the device address space): no copy-engine transfer on the round trip.
     void gram(int64_t M, const T *A, int64_t lda, int n1, const T *B, int64_t ldb, int n2, double *G, bool kside) {
         struct Chunk { int a0, na, b0, nb; size_t idx; };
-        static const bool zc_env = [] { const char *e = std::getenv("SSA_GRAM_ZC"); return e ? std::atoi(e) != 0 : true; }();
         const bool reduce = kside && kside_comm();
-        const bool zc = zc_env && !reduce;
+        const bool zc = !reduce;
         std::vector<Chunk> ch;
         for (int a0 = 0; a0 < n1; a0 += 512) {
             const int na = std::min(512, n1 - a0);
@@ -719,8 +715,7 @@ struct Gkl {
             SSA_CUDA(cudaMemcpyAsync(T0d, Ad, sizeof(double) * mn, cudaMemcpyDeviceToDevice, st));
             // off-diagonal tolerance: fp32 products resolve ~1e-7 relative, so 1e-9 (fp32) / 1e-12
             // (fp64) leaves the Ritz values exact to rounding and saves the last Jacobi sweep(s)
-            static const double jtol = [] { const char *e = std::getenv("SSA_JACOBI_TOL"); return e ? std::atof(e) : 0.0; }();
-            const double tolj = jtol > 0 ? jtol : (sizeof(T) == 4 ? 1e-9 : 1e-12);
+            const double tolj = sizeof(T) == 4 ? 1e-9 : 1e-12;
             int *dsw = dints + 64;
             cudaEvent_t je0 = nullptr, je1 = nullptr;
             if (debug) {
@@ -729,8 +724,7 @@ struct Gkl {
             }
             // early stop once a sweep's largest rotated relative off-diagonal is below 1e-4 (fp32) /
             // 1e-6 (fp64): the columns then end orthogonal to ~1e-8 / 1e-12 (quadratic convergence)
-            static const double jearly = [] { const char *e = std::getenv("SSA_JACOBI_EARLY"); return e ? std::atof(e) : -1.0; }();
-            const double early = jearly >= 0 ? jearly : (sizeof(T) == 4 ? 1e-4 : 1e-6);
+            const double early = sizeof(T) == 4 ? 1e-4 : 1e-6;
             jacobi_svd_blocked(m, n, Ad, dints, debug ? dsw : nullptr, st, tolj, early);
             if (debug) {
                 SSA_CUDA(cudaEventRecord(je1, st));
@@ -858,8 +852,7 @@ struct Gkl {
             const bool cycle_end = !(nQ + 2 * k <= nQmax && nblock + 1 < maxprod);
             double tt[2] = {t_block, t_ritz > 0.0 ? t_ritz : 1.0};
             if (kside_comm()) agree(tt, 2);
-            static const double cost_ratio = [] { const char *e = std::getenv("SSA_CHECK_RATIO"); return e ? std::atof(e) : 1.0; }();
-            const bool costly_blocks = nQ >= r && tt[0] >= cost_ratio * tt[1];
+            const bool costly_blocks = nQ >= r && tt[0] >= tt[1];
             const bool check = cycle_end || costly_blocks;
             if (check && defer_on) stepB_check();
             else stepB();

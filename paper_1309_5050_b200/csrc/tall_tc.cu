@@ -81,7 +81,7 @@ gram_tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 int n1, int n2, int b_col, double *__restrict__ partials, int per) {
     using namespace tc;
     using C = tallg3::Cfg<NM, NN, BA, RC, KG>;
-    constexpr int KS = C::KS, KA = C::KA, OPB = C::OPB, AB = C::ACCB;
+    constexpr int KA = C::KA, OPB = C::OPB, AB = C::ACCB;
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = smem_align1024(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::off_bar);
@@ -920,8 +920,8 @@ static void launch_gram_tc3(int64_t M, const float *A, int64_t lda, int n1, cons
     // stages per accumulator drain: 1.  Four (256 rows of fp32 tensor-core accumulation per Kahan
     // step) was 0.3 ms faster per isolated c5 Gram (scripts/bench_tall_c5.py) but cost the c5
     // decomposition 9 ms (49.5 -> 58.6 ms, measured twice): the coarser accumulation changed the
-    // orthonormalisation's decisions downstream.  SSA_GRAM_PER selects it for experiments.
-    static const int per = [] { const char *e = std::getenv("SSA_GRAM_PER"); return e ? std::max(1, std::atoi(e)) : 1; }();
+    // orthonormalisation's decisions downstream.
+    constexpr int per = 1;
     kern<<<dim3(ctas, gy), tallg::NTHR, tallg3::SMEM, st>>>(ma, mb, M, n1, n2, b_col, partials, per);
     after_launch("gram_tc3");
 }
@@ -1009,14 +1009,12 @@ bool update_tc(int64_t M, const float *A, int64_t lda, int m, const double *C, i
 // Returns false when the shape / layout is not supported (the caller uses the CUDA-core path).
 bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int64_t ldb, int n2, double *G,
              double *partials, size_t partial_bytes, cudaStream_t st) {
-    static const int mode = [] { const char *e = std::getenv("SSA_GRAM_TC"); return e ? std::atoi(e) : 1; }();
-    if (!mode || M < 8192 || n2 > 64 || n1 > 512 || (lda & 3) || (ldb & 3) || ((uintptr_t)A & 15) ||
+    if (M < 8192 || n2 > 64 || n1 > 512 || (lda & 3) || (ldb & 3) || ((uintptr_t)A & 15) ||
         ((uintptr_t)B & 15) || M > INT32_MAX)
         return false;
     const int ctas = (int)std::min<int64_t>(num_sms(), cdiv(M, tallg::R));
-    static const int self_mode = [] { const char *e = std::getenv("SSA_GRAM_SELF"); return e ? std::atoi(e) : 1; }();
     auto self_ok = [&](const float *X, int n) {
-        return self_mode && n <= 64 && !(lda & 31) && !((uintptr_t)X & 127) &&
+        return n <= 64 && !(lda & 31) && !((uintptr_t)X & 127) &&
                (size_t)ctas * 4096 * sizeof(double) * 2 <= partial_bytes;
     };
     // self Gram XᵀX (n <= 64 columns): hi / lo stacked on M, one MMA per k-step (gram_self_kernel);
@@ -1054,8 +1052,7 @@ bool gram_tc(int64_t M, const float *A, int64_t lda, int n1, const float *B, int
     // [A W]ᵀW with W = the last n2 = 64 columns of A, more than one 128-column block: AᵀW over the first
     // n1 − n2 columns (W loaded beside them) plus WᵀW by the self-Gram kernel — one full wave each,
     // instead of a second, nearly empty wave of CTAs that re-reads W (c5 K side, n1 = 192: 4.6 ms, ncu)
-    static const int split_mode = [] { const char *e = std::getenv("SSA_GRAM_SPLIT"); return e ? std::atoi(e) : 1; }();
-    if (split_mode && n2 == 64 && n1 > 128 && ldb == lda && B == A + (int64_t)(n1 - n2) * lda && self_ok(B, n2) &&
+    if (n2 == 64 && n1 > 128 && ldb == lda && B == A + (int64_t)(n1 - n2) * lda && self_ok(B, n2) &&
         (size_t)ctas * 4096 * sizeof(double) * (size_t)cdiv(n1 - n2, 64) <= partial_bytes) {
         const int na = n1 - n2;
         launch_gram_tc<1, 64, 128>(M, A, lda, na, B, ldb, n2, partials, ctas, st);

@@ -316,10 +316,6 @@ static inline CUtensorMap make_map3(const void *base, uint64_t d0, uint64_t d1, 
                                    swz != CU_TENSOR_MAP_SWIZZLE_NONE ? swz : (swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE),
                                    l2p, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     SSA_REQUIRE(r == CUDA_SUCCESS, SSA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-    if (std::getenv("SSA_TC_DUMP"))
-        std::fprintf(stderr, "[tc] map base=%p dims=%llu,%llu,%llu strides=%llu,%llu box=%u,%u,%u swz=%d\n", base,
-                     (unsigned long long)d0, (unsigned long long)d1, (unsigned long long)d2, (unsigned long long)s1,
-                     (unsigned long long)s2, b0, b1, b2, (int)swz128);
     return m;
 }
 
