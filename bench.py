@@ -67,10 +67,11 @@ def _peaks():
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region.
 
-    One long-running `nvidia-smi --loop-ms` process: its start-up (driver / NVML initialisation — on a
-    fresh box the first nvidia-smi call stalled the GPU for ~0.9 s, and every new process for ~10 ms)
-    completes before __enter__ returns (its first sample marks the start of the timed region), so only
-    its periodic queries overlap the timed steps.
+    One long-running `nvidia-smi --loop-ms` process, started BEFORE the warm-up steps: its start-up
+    (driver / NVML initialisation — on a fresh box the first nvidia-smi call stalled the GPU for ~0.9 s,
+    every new process for ~10 ms, and a first timed c5 step of 728 ms was seen with the sampler started
+    right before it) then falls into the warm-up.  `mark()` opens the timed region: only samples read
+    after it (and the last one before it, for regions shorter than the period) are reported.
     """
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -82,6 +83,16 @@ class ClockSampler:
         self._p = None
         self._t = None
         self._first = threading.Event()
+        self._t0 = 0.0
+        self._t1 = float("inf")
+
+    def mark(self):
+        """Start of the timed region."""
+        self._t0 = time.perf_counter()
+
+    def stop(self):
+        """End of the timed region (the process keeps running until __exit__)."""
+        self._t1 = time.perf_counter()
 
     def _read(self):
         for line in self._p.stdout:
@@ -90,10 +101,12 @@ class ClockSampler:
                 continue
             # the first sample is taken as the timed region starts (kept: short regions, c1-c4, may
             # end before the next one)
-            self.samples.append([s.strip() for s in line.split(",")])
+            self.samples.append([time.perf_counter()] + [s.strip() for s in line.split(",")])
             self._first.set()
 
     def __enter__(self):
+        if os.environ.get("SSA_BENCH_NO_CLOCKS"):      # diagnosis only: the line then says "unsampled"
+            return self
         try:
             self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
                                         "--format=csv,noheader,nounits", f"--loop-ms={self.period}"],
@@ -116,14 +129,17 @@ class ClockSampler:
             self._t.join(timeout=5)
 
     def summary(self):
-        if not self.samples:
+        before = [s for s in self.samples if s[0] < self._t0]
+        inside = [s for s in self.samples if self._t0 <= s[0] <= self._t1]
+        use = [s[1:] for s in (before[-1:] + inside)]
+        if not use:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in use if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in use if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
+        reasons = sorted({names[i] for s in use for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "n_samples": len(self.samples)}
+                "reasons": reasons, "n_samples": len(use)}
 
 
 def measured_tf32_peak():
@@ -152,7 +168,7 @@ def groups_for(w):
 def run_ours(args, rank, world, dist):
     import torch
     from paper_1309_5050_b200 import Plan, launch_count
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", 0 if args.one_gpu_rehearsal else int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     w = workload(args.config, seed_offset=rank)
     groups = groups_for(w)
@@ -211,18 +227,19 @@ def run_ours(args, rank, world, dist):
             phase_dev.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])])
         return info, recs, p
 
-    # warm-up (also compiles nothing: the library is AOT-built)
-    for _ in range(args.warmup):
-        info, recs, p = step()
-    torch.cuda.synchronize()
-    L, K, k = p.L, p.K, info["block_k"]
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    times, infos = [], []
-    launches0 = launch_count(reset=True)
-    phases.clear()
     with ClockSampler(dev.index) as clk:
+        # warm-up (also compiles nothing: the library is AOT-built)
+        for _ in range(args.warmup):
+            info, recs, p = step()
+        torch.cuda.synchronize()
+        L, K, k = p.L, p.K, info["block_k"]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        times, infos = [], []
+        launches0 = launch_count(reset=True)
+        phases.clear()
+        clk.mark()
         for _ in range(args.steps):
             flush.fill_(1)                         # flush L2 between timed iterations
             torch.cuda.synchronize()
@@ -233,6 +250,7 @@ def run_ours(args, rank, world, dist):
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
             infos.append(info)
+        clk.stop()
     launches = launch_count(reset=True)
     timed_phases = {k: float(np.mean([ph[k] for ph in phases])) for k in phases[0]} if phases else {}
     torch.cuda.synchronize()
@@ -252,6 +270,8 @@ def run_ours(args, rank, world, dist):
 
     # ---- end-to-end through the C ABI with host buffers (H2D input, D2H reconstructions)
     e2e_times = []
+    step(host=True)                                # untimed: the host-buffer path's first pool allocations
+    torch.cuda.synchronize()
     for _ in range(max(1, min(args.steps, 5))):
         flush.fill_(1); torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -456,7 +476,7 @@ def run_sharded(args, rank, world, dist):
     import torch
     from paper_1309_5050_b200 import launch_count
     from paper_1309_5050_b200.dist import TorchComm, band_plan, band_slices
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", 0 if args.one_gpu_rehearsal else int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     w = workload(args.config, seed_offset=0)          # the same global problem on every rank
     groups = groups_for(w)
@@ -474,6 +494,8 @@ def run_sharded(args, rank, world, dist):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     out_pin = torch.empty((len(groups), ny, xg.shape[0]), dtype=dt_torch, pin_memory=True)
 
+    shape_info = {}
+
     def step(host=False):
         with torch.cuda.stream(stream):
             src = sub_pin.t() if host else sub_dev
@@ -489,17 +511,19 @@ def run_sharded(args, rank, world, dist):
             recs = (p.reconstruct(groups, device=False, out=out_pin.numpy()) if host
                     else p.reconstruct(groups, device=True))
             sig = np.array(p.sigma)
+            shape_info.update(L=p.L, K=p.K, path_xv=p.path_xv, path_xtu=p.path_xtu)
             p.close()
         return info, sig, recs
 
-    for _ in range(args.warmup):
-        info, _, _ = step()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    times = []
-    launch_count(reset=True)
     with ClockSampler(dev.index) as clk:
+        for _ in range(args.warmup):
+            info, _, _ = step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        times = []
+        launch_count(reset=True)
+        clk.mark()
         for _ in range(args.steps):
             flush.fill_(1)
             torch.cuda.synchronize()
@@ -511,6 +535,7 @@ def run_sharded(args, rank, world, dist):
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
+        clk.stop()
     launches = launch_count(reset=True)
     ms = float(np.sum(times))
     if dist:
@@ -533,6 +558,35 @@ def run_sharded(args, rank, world, dist):
         e2e.append(float(t_e[0]))
     nvec = float(info["n_vector_products"])               # one decomposition: not summed over ranks
     esz = 8 if w.dtype == "f64" else 4
+    # roofline of rank 0's band-sized block products (the last timed step; same 3-pass byte model as N = 1,
+    # DESIGN.md §6, on the band's own grid).  The X·V events include the all-reduce of the L x k partials.
+    roof = {}
+    Lb, Kb = shape_info["L"], shape_info["K"]
+    nxb, nyb = xg.shape[0], c1 - c0
+    for name, key in (("X·V", "xv"), ("Xᵀ·U", "xtu")):
+        nb, path = info[f"n_products_{key}"], shape_info[f"path_{key}"]
+        if nb <= 0:
+            continue
+        avg_ms, kk = info[f"ms_products_{key}"] / nb, info[f"n_vectors_{key}"] / nb
+        if path == "fft":
+            Mx = 1 << int(np.ceil(np.log2(nxb))); My = 1 << int(np.ceil(np.log2(max(nyb, 1))))
+            Hx = Mx // 2 + 1
+            alg = kk * (esz * (Kb + Lb) + 4 * esz * Hx * ((nyb - w.window[1] + 1) + w.window[1])) + 2 * esz * Hx * My
+            peak = _peaks()["hbm_gbs"]
+            r_ = {"bound": "hbm", "achieved": alg / (avg_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                  "algorithmic_bytes_per_launch": alg}
+        else:
+            flops = 2.0 * Lb * Kb * kk
+            peak = (measured_tf32_peak() / 3.0 if path == "tc"
+                    else (FP64_PEAK_TFLOPS if w.dtype == "f64" else FFMA_PEAK_TFLOPS))
+            r_ = {"bound": "tensor" if path == "tc" else "alu", "achieved": flops / (avg_ms / 1e3) / 1e12,
+                  "peak": peak, "unit": "TFLOP/s", "algorithmic_flops_per_launch": flops}
+        r_.update(frac=r_["achieved"] / r_["peak"], traffic=None, avg_launch_ms=avg_ms, path=path,
+                  kernel=f"{name} on rank 0's band ({nxb} x {nyb} sub-image)",
+                  share_of_step=info[f"ms_products_{key}"] / max(times[-1], 1e-9))
+        roof[key] = r_
+    roofline = dict(max(roof.values(), key=lambda r_: r_["share_of_step"])) if roof else {}
+    roofline["products"] = roof
     res = {"metric": "trajectory products/s", "value": nvec / (ms / args.steps / 1e3), "unit": "vector products/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": w.dtype,
@@ -547,6 +601,7 @@ def run_sharded(args, rank, world, dist):
            "e2e": {"value": nvec / (np.mean(e2e) / 1e3), "unit": "vector products/s",
                    "h2d_bytes_per_step": int(xg.shape[0] * (c1 - c0) * esz),
                    "d2h_bytes_per_step": int(len(groups) * xg.size * esz), "ms_per_step": float(np.mean(e2e))},
+           "roofline": roofline,
            "gpu_launches": int(launches), "clocks": clk.summary(), "sigma_head": [float(x) for x in sig[:4]],
            "decomposition": {k2: info[k2] for k2 in ("n_block_products", "n_restarts", "n_converged",
                                                       "max_rel_residual")}}
@@ -576,6 +631,10 @@ def main():
     ap.add_argument("--shard", action="store_true",
                     help="one decomposition split over the ranks by window-position bands (strong scaling; "
                          "the default when N > 1)")
+    ap.add_argument("--one-gpu-rehearsal", action="store_true",
+                    help="correctness rehearsal of the N > 1 code path on a one-GPU box: every rank uses cuda:0 and "
+                         "the process group is gloo (host-synchronised all-reduce of the device buffers; no kernel "
+                         "waits on another rank's kernel).  Its timings are NOT a measurement")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas (weak scaling) instead of the band partition")
     args = ap.parse_args()
@@ -612,7 +671,7 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl")
+        tdist.init_process_group("gloo" if args.one_gpu_rehearsal else "nccl")
         dist = tdist
     sharded = args.shard or (world > 1 and not args.replicas)
     res, w = (run_sharded if sharded else run_ours)(args, rank, world, dist)
@@ -621,6 +680,9 @@ def main():
             v, cores, sample = oracle_products_per_s(w, budget_s=args.cpu_budget)
             res["cpu_baseline"] = {"value": v, "unit": "vector products/s", "cores": cores, "kind": "oracle",
                                    "sample": sample, "cpu": cpu_model()}
+        if args.one_gpu_rehearsal:
+            res["rehearsal"] = (f"{world} ranks sharing cuda:0 over gloo: checks the N > 1 code path, "
+                                "its timings are not a measurement")
         res["paper_context"] = {"rssa_nutrlan_s": {"mars_25x25": 0.519, "mars_160x80_r50": 0.587},
                                 "hardware": "not stated in the paper (P:2518-2624)"}
         print(json.dumps(res))
