@@ -142,6 +142,16 @@ class ClockSampler:
                 "reasons": reasons, "n_samples": len(use)}
 
 
+def _quiet_gc():
+    """No cyclic-GC passes inside the timed regions (as `timeit` does): a generation-2 collection of a
+    torch process's ~10^6 objects is a 15-50 ms host pause, seen as one-off +16..+50 ms steps in about one
+    step of ten (gpurun r2: the decomposition's own host phases were unchanged in the slow steps)."""
+    import gc
+    gc.collect()
+    gc.freeze()
+    gc.disable()
+
+
 def measured_tf32_peak():
     """Dense tcgen05 kind::tf32 TFLOP/s measured on this GPU (library microbenchmark)."""
     import ctypes
@@ -193,6 +203,7 @@ def run_ours(args, rank, world, dist):
     out_pin = torch.empty((len(groups), ny_, nx_), dtype=dt_torch, pin_memory=True)
 
     phase_dev = []   # device ms of (plan, decompose, reconstruct) per timed step
+    rec_host = []    # host ms of (torch output allocation, ssa_reconstruct call) per timed step
 
     def step(host=False, events=False):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if events else None
@@ -217,6 +228,7 @@ def run_ours(args, rank, world, dist):
                     else p.reconstruct(groups, add_rest=False, device=True))
             if ev:
                 ev[3].record(stream)
+                rec_host.append([round(x, 3) for x in getattr(p, "last_reconstruct_host_ms", (0.0, 0.0))])
             t3 = time.perf_counter()
             p.close()
             t4 = time.perf_counter()
@@ -227,6 +239,7 @@ def run_ours(args, rank, world, dist):
             phase_dev.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])])
         return info, recs, p
 
+    _quiet_gc()
     with ClockSampler(dev.index) as clk:
         # warm-up (also compiles nothing: the library is AOT-built)
         for _ in range(args.warmup):
@@ -375,6 +388,7 @@ def run_ours(args, rank, world, dist):
         "ms_per_step": ms_all / args.steps,
         "step_ms": [round(float(t), 3) for t in times],
         "step_phases_ms": [[round(float(x), 3) for x in ph_] for ph_ in phase_dev],
+        "step_reconstruct_host_ms": rec_host,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -515,6 +529,7 @@ def run_sharded(args, rank, world, dist):
             p.close()
         return info, sig, recs
 
+    _quiet_gc()
     with ClockSampler(dev.index) as clk:
         for _ in range(args.warmup):
             info, _, _ = step()

@@ -270,8 +270,11 @@ ssa_status ssa_bench_mma(int32_t iters, int32_t ctas, double *ms, double *tflops
 /* Release the calling thread's solver workspace.  The K-side Lanczos basis and its restart copy
  * (ssa_decompose; c5: 15 + 9 GB) are kept per host thread across decompositions and plans, grow-only,
  * so that repeated plan / decompose / destroy cycles reuse them instead of fragmenting the
- * stream-ordered memory pool; this call frees them (they are also freed at thread exit).  Safe to
- * call at any time outside a running ssa_decompose on the same thread; SSA_OK. */
+ * stream-ordered memory pool; this call frees them (they are also freed at thread exit).  It also
+ * empties the thread's cache of large freed device blocks: every internal buffer of 8 MB or more is
+ * kept, when freed, for the next allocation of exactly that size on this thread (at most 64 GB in all,
+ * oldest returned to the pool first), so that steady-state plans of one shape never go back to the
+ * pool allocator.  Safe to call at any time outside a running ssa_decompose on the same thread; SSA_OK. */
 ssa_status ssa_release_workspace(void);
 
 const char *ssa_last_error(void);

@@ -13,6 +13,8 @@ from __future__ import annotations
 
 import ctypes as C
 
+import time
+
 import numpy as np
 
 from . import _lib as lib
@@ -258,9 +260,13 @@ class Plan:
         if device:
             torch = _torch()
             td = torch.float64 if self.dtype == "f64" else torch.float32
+            t0 = time.perf_counter()
             o = torch.empty((n, self.ny_out, self.nx), dtype=td, device="cuda")
+            t1 = time.perf_counter()
             lib.check(self._L.ssa_reconstruct(self._h, off.ctypes.data, idx.ctypes.data, len(groups),
                                               int(add_rest), o.data_ptr(), 1))
+            # host ms of (output allocation by torch, the ABI call): diagnostics for bench.py
+            self.last_reconstruct_host_ms = ((t1 - t0) * 1e3, (time.perf_counter() - t1) * 1e3)
             return [o[g].t() for g in range(n)]
         o = np.zeros((n, self.ny_out, self.nx), dtype=self._np_dtype)
         lib.check(self._L.ssa_reconstruct(self._h, off.ctypes.data, idx.ctypes.data, len(groups),

@@ -39,6 +39,67 @@ void pool_init() {
     done_dev = dev;
 }
 
+namespace {
+struct BigBlock { void *p; size_t bytes; cudaStream_t st; cudaEvent_t ev; int dev; };
+struct BigCache {
+    std::vector<BigBlock> blocks;   // oldest first
+    size_t total = 0;
+    void drop(size_t i) {
+        BigBlock b = blocks[i];
+        blocks.erase(blocks.begin() + (std::ptrdiff_t)i);
+        total -= b.bytes;
+        // the free is ordered after the block's last use through its event; the legacy default stream
+        // may outlive the stream the block was last used on
+        if (cudaStreamWaitEvent(cudaStreamPerThread, b.ev, 0) == cudaSuccess) cudaFreeAsync(b.p, cudaStreamPerThread);
+        else { cudaGetLastError(); cudaFree(b.p); }
+        cudaEventDestroy(b.ev);
+    }
+    void clear() { while (!blocks.empty()) drop(blocks.size() - 1); }
+    ~BigCache() { clear(); cudaGetLastError(); }
+};
+BigCache &big_cache() { static thread_local BigCache c; return c; }
+constexpr size_t kBigCacheCap = (size_t)64 << 30;
+}  // namespace
+
+void *big_take(size_t n, cudaStream_t st) {
+    BigCache &c = big_cache();
+    if (c.blocks.empty()) return nullptr;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (size_t i = c.blocks.size(); i-- > 0;) {
+        BigBlock &b = c.blocks[i];
+        if (b.bytes != n || b.dev != dev) continue;
+        if (b.st != st && cudaStreamWaitEvent(st, b.ev, 0) != cudaSuccess) { cudaGetLastError(); continue; }
+        void *p = b.p;
+        cudaEventDestroy(b.ev);
+        c.total -= b.bytes;
+        c.blocks.erase(c.blocks.begin() + (std::ptrdiff_t)i);
+        return p;
+    }
+    return nullptr;
+}
+
+bool big_give(void *p, size_t n, cudaStream_t st) {
+    BigCache &c = big_cache();
+    if (n > kBigCacheCap) return false;
+    BigBlock b{p, n, st, nullptr, 0};
+    if (cudaGetDevice(&b.dev) != cudaSuccess || cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (cudaEventRecord(b.ev, st) != cudaSuccess) {
+        cudaGetLastError();
+        cudaEventDestroy(b.ev);
+        return false;
+    }
+    c.blocks.push_back(b);
+    c.total += n;
+    while (c.total > kBigCacheCap && c.blocks.size() > 1) c.drop(0);
+    return true;
+}
+
+void big_release_all() { big_cache().clear(); }
+
 int num_sms() {
     static int n = 0;
     if (n == 0) {

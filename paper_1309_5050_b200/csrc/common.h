@@ -41,6 +41,17 @@ void after_launch(const char *what);
 // plan's stream; the device's default pool keeps freed blocks cached, so creating and
 // destroying plans does not pay cudaMalloc/cudaFree each time).
 void pool_init();
+// Large blocks (>= 8 MB) are kept, when freed, in a per-host-thread cache keyed by their exact size and
+// handed back to the next allocation of that size (any stream: the new stream waits on an event recorded
+// at the free).  A plan's large buffers have the same sizes in every plan of a shape, so steady-state plans
+// never return to the pool allocator: freed to the pool, the multi-GB buffers of plan, decomposition and
+// reconstruction were re-carved differently from step to step and the pool had to map new memory now and
+// then (host stalls of 15-700 ms inside ssa_reconstruct / ssa_decompose, gpurun r1-r4).  The cache holds
+// at most 64 GB (oldest blocks go back to the pool first); ssa_release_workspace empties it.
+void *big_take(size_t n, cudaStream_t st);
+bool big_give(void *p, size_t n, cudaStream_t st);
+void big_release_all();
+constexpr size_t kBigBlock = (size_t)8 << 20;
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
@@ -59,11 +70,15 @@ struct DevBuf {
         release();
         pool_init();
         s = st;
-        SSA_CUDA(cudaMallocAsync(&p, n ? n : 16, st));
+        if (n >= kBigBlock) p = big_take(n, st);
+        if (!p) SSA_CUDA(cudaMallocAsync(&p, n ? n : 16, st));
         bytes = n;
     }
     void release() {
-        if (p) { cudaFreeAsync(p, s); p = nullptr; bytes = 0; }
+        if (p) {
+            if (bytes < kBigBlock || !big_give(p, bytes, s)) cudaFreeAsync(p, s);
+            p = nullptr; bytes = 0;
+        }
     }
     template <class T> T *as() const { return static_cast<T *>(p); }
 };

@@ -100,6 +100,7 @@ void release_workspace() {
     KCache &c = kside_cache();
     c.Qb.release();
     c.Qtmp.release();
+    big_release_all();
 }
 
 template <typename T>

@@ -24,6 +24,10 @@ for c in c1 c2 c3 c4; do
   python -c "import json; d=json.loads(open('$out/bench_$c.json').read().strip().splitlines()[-1]); print('$c', d['ms_per_step'], d.get('rank_r_time_ms'), d['roofline']['frac'])"
 done
 timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > $out/bench_ref.json 2> $out/bench_ref.err
+# the N = 2 command on one GPU (gloo, all ranks on cuda:0): correctness rehearsal, not a measurement
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 \
+  bench.py --gpus 2 --one-gpu-rehearsal --steps 2 --warmup 3 > $out/bench_c5_rehearsal_n2.json 2> $out/bench_c5_rehearsal_n2.err
+python -c "import json; d=json.loads([l for l in open('$out/bench_c5_rehearsal_n2.json') if l.startswith('{')][-1]); print('rehearsal n2', d['ms_per_step'], d['sigma_head'], d['decomposition'])"
 [ "$2" = quick ] && exit 0
 timeout 2400 python -m pytest tests -m gpu -q --timeout 900 > $out/pytest_gpu.log 2>&1
 tail -3 $out/pytest_gpu.log
