@@ -143,9 +143,9 @@ class ClockSampler:
 
 
 def _quiet_gc():
-    """No cyclic-GC passes inside the timed regions (as `timeit` does): a generation-2 collection of a
-    torch process's ~10^6 objects is a 15-50 ms host pause, seen as one-off +16..+50 ms steps in about one
-    step of ten (gpurun r2: the decomposition's own host phases were unchanged in the slow steps)."""
+    """No cyclic-GC passes inside the timed regions (as `timeit` does).  (The one-off +15..+700 ms steps
+    of gpurun r1-r4 were NOT this: they persisted with the collector off and went away with the library's
+    large-block cache.)"""
     import gc
     gc.collect()
     gc.freeze()
