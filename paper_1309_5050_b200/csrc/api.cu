@@ -1,6 +1,7 @@
 // C ABI of libssa_b200 (include/ssa_b200.h): plan creation (embedding, step 1),
 // product dispatch, decomposition (step 2), reconstruction (steps 3-4).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -41,47 +42,80 @@ void pool_init() {
 
 namespace {
 struct BigBlock { void *p; size_t bytes; cudaStream_t st; cudaEvent_t ev; int dev; };
+// free a cached block: ordered after its last use through its event (the stream it was last used on may
+// be gone by now)
+void big_free(const BigBlock &b) {
+    if (cudaStreamWaitEvent(cudaStreamPerThread, b.ev, 0) == cudaSuccess) cudaFreeAsync(b.p, cudaStreamPerThread);
+    else { cudaGetLastError(); cudaFree(b.p); }
+    cudaEventDestroy(b.ev);
+}
+// blocks of host threads that have exited: any thread may take them.  Allocated once and never destroyed:
+// no CUDA call and no destructor may run during process exit (the runtime may already be gone).
+struct Orphans { std::mutex m; std::vector<BigBlock> blocks; std::atomic<size_t> n{0}; };
+Orphans &orphans() { static Orphans *o = new Orphans; return *o; }
+thread_local bool tl_big_dead = false;   // trivially destructible: still valid after ~BigCache
 struct BigCache {
     std::vector<BigBlock> blocks;   // oldest first
     size_t total = 0;
     void drop(size_t i) {
-        BigBlock b = blocks[i];
+        const BigBlock b = blocks[i];
         blocks.erase(blocks.begin() + (std::ptrdiff_t)i);
         total -= b.bytes;
-        // the free is ordered after the block's last use through its event; the legacy default stream
-        // may outlive the stream the block was last used on
-        if (cudaStreamWaitEvent(cudaStreamPerThread, b.ev, 0) == cudaSuccess) cudaFreeAsync(b.p, cudaStreamPerThread);
-        else { cudaGetLastError(); cudaFree(b.p); }
-        cudaEventDestroy(b.ev);
+        big_free(b);
     }
     void clear() { while (!blocks.empty()) drop(blocks.size() - 1); }
-    ~BigCache() { clear(); cudaGetLastError(); }
+    // thread exit (for the main thread: process exit): no CUDA calls here; the blocks go to the orphan list
+    ~BigCache() {
+        tl_big_dead = true;
+        if (blocks.empty()) return;
+        Orphans &o = orphans();
+        std::lock_guard<std::mutex> g(o.m);
+        o.blocks.insert(o.blocks.end(), blocks.begin(), blocks.end());
+        o.n = o.blocks.size();
+    }
 };
 BigCache &big_cache() { static thread_local BigCache c; return c; }
 constexpr size_t kBigCacheCap = (size_t)64 << 30;
+
+bool big_match(const BigBlock &b, size_t n, int dev, cudaStream_t st) {
+    if (b.bytes != n || b.dev != dev) return false;
+    if (b.st != st && cudaStreamWaitEvent(st, b.ev, 0) != cudaSuccess) { cudaGetLastError(); return false; }
+    return true;
+}
 }  // namespace
 
 void *big_take(size_t n, cudaStream_t st) {
+    if (tl_big_dead) return nullptr;
     BigCache &c = big_cache();
-    if (c.blocks.empty()) return nullptr;
+    Orphans &o = orphans();
+    if (c.blocks.empty() && o.n == 0) return nullptr;
     int dev = 0;
     cudaGetDevice(&dev);
     for (size_t i = c.blocks.size(); i-- > 0;) {
-        BigBlock &b = c.blocks[i];
-        if (b.bytes != n || b.dev != dev) continue;
-        if (b.st != st && cudaStreamWaitEvent(st, b.ev, 0) != cudaSuccess) { cudaGetLastError(); continue; }
-        void *p = b.p;
-        cudaEventDestroy(b.ev);
-        c.total -= b.bytes;
+        if (!big_match(c.blocks[i], n, dev, st)) continue;
+        void *p = c.blocks[i].p;
+        cudaEventDestroy(c.blocks[i].ev);
+        c.total -= n;
         c.blocks.erase(c.blocks.begin() + (std::ptrdiff_t)i);
         return p;
+    }
+    if (o.n != 0) {
+        std::lock_guard<std::mutex> g(o.m);
+        for (size_t i = o.blocks.size(); i-- > 0;) {
+            if (!big_match(o.blocks[i], n, dev, st)) continue;
+            void *p = o.blocks[i].p;
+            cudaEventDestroy(o.blocks[i].ev);
+            o.blocks.erase(o.blocks.begin() + (std::ptrdiff_t)i);
+            o.n = o.blocks.size();
+            return p;
+        }
     }
     return nullptr;
 }
 
 bool big_give(void *p, size_t n, cudaStream_t st) {
+    if (tl_big_dead || n > kBigCacheCap) return false;   // dead: a thread_local holder outlived the cache
     BigCache &c = big_cache();
-    if (n > kBigCacheCap) return false;
     BigBlock b{p, n, st, nullptr, 0};
     if (cudaGetDevice(&b.dev) != cudaSuccess || cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
@@ -98,7 +132,14 @@ bool big_give(void *p, size_t n, cudaStream_t st) {
     return true;
 }
 
-void big_release_all() { big_cache().clear(); }
+void big_release_all() {
+    if (!tl_big_dead) big_cache().clear();
+    Orphans &o = orphans();
+    std::lock_guard<std::mutex> g(o.m);
+    for (const BigBlock &b : o.blocks) big_free(b);
+    o.blocks.clear();
+    o.n = 0;
+}
 
 int num_sms() {
     static int n = 0;

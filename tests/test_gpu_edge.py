@@ -192,3 +192,29 @@ def test_release_workspace_between_decompositions():
         p.close()
         release_workspace()
     assert np.array_equal(s[0], s[1])
+
+
+def test_large_block_cache_reuse_across_streams():
+    """Freed device blocks >= 8 MB are kept per host thread by exact size and handed to the next plan of
+    the shape, also when that plan runs on another stream: the reuse is ordered after the
+    previous plan's last kernel by an event.  Same input, three plans on alternating streams, products
+    issued back to back without a host synchronisation in between: identical results."""
+    import torch
+    from paper_1309_5050_b200 import Plan
+    w = synth.get("c3")
+    rng = np.random.default_rng(5)
+    K = (w.data.shape[0] - w.window[0] + 1) * (w.data.shape[1] - w.window[1] + 1)
+    V = rng.normal(size=(K, w.block_k)).astype(np.float32)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs, sig = [], []
+    for i in range(3):
+        st = streams[i % 2]
+        with torch.cuda.stream(st):
+            p = Plan(w.data, w.window, dtype=w.dtype, block_k=w.block_k, stream=st.cuda_stream)
+            outs.append(np.array(p.matmul(V)))
+            p.decompose(w.r)
+            sig.append(np.array(p.sigma))
+            p.close()
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    np.testing.assert_allclose(sig[1], sig[0], rtol=1e-6)
+    np.testing.assert_allclose(sig[2], sig[0], rtol=1e-6)
